@@ -1,0 +1,222 @@
+/* mpic_b200.h — C ABI of the B200-native MPIC partial-reuse prefill path.
+ *
+ * This is the drop-in boundary: plain C types, plain pointers and sizes, explicit CUDA
+ * streams (passed as void*, i.e. a cudaStream_t), no C++ or torch types, no exceptions.
+ * The C++ host library (include/mpic/*.h, same API as the reference's
+ * proj/include/mpic/*.h) sits on top of it; a cgo / JNI / ctypes binding would bind
+ * exactly these symbols.
+ *
+ * Every call returns an mpic_status; codes map 1:1 onto the reference's exception
+ * classes (proj/include/mpic/errors.h:10-62). mpic_last_error() returns the message of
+ * the calling thread's last failure.
+ *
+ * Layouts (reference proj/include/mpic/tensor.h:11-55): KV is [L][T][H][D] row-major,
+ * keys stored post-RoPE; weights are row-major [out][in] and every projection is
+ * y = x·Wᵀ (proj/src/linker.cpp:64-65).
+ */
+#ifndef MPIC_B200_H
+#define MPIC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MPIC_OK = 0,
+    MPIC_ERR_CONFIG = 1,     /* mpic::config_error */
+    MPIC_ERR_VALIDATION = 2, /* mpic::validation_error */
+    MPIC_ERR_STATE = 3,      /* mpic::state_error */
+    MPIC_ERR_LINK = 4,       /* mpic::link_error */
+    MPIC_ERR_CONTRACT = 5,   /* mpic::contract_error */
+    MPIC_ERR_FORMAT = 6,     /* mpic::format_error */
+    MPIC_ERR_INTEGRITY = 7,  /* mpic::integrity_error */
+    MPIC_ERR_IO = 8,         /* mpic::io_error */
+    MPIC_ERR_NOT_FOUND = 9,  /* mpic::not_found_error */
+    MPIC_ERR_REQUEST = 10,   /* mpic::request_error */
+    MPIC_ERR_CUDA = 20,      /* CUDA runtime failure (no reference equivalent) */
+    MPIC_ERR_NO_DEVICE = 21  /* no sm_100 device: the path never falls back to the CPU */
+} mpic_status;
+
+typedef enum { MPIC_F32 = 0, MPIC_BF16 = 1 } mpic_dtype;
+
+typedef enum { MPIC_AS_STORED = 0, MPIC_REROTATE = 1 } mpic_reposition; /* linker.h:81-88 */
+
+/* mpic::ModelConfig (proj/include/mpic/config.h:7-24), same field order and meaning. */
+typedef struct {
+    uint32_t n_layers;
+    uint32_t n_heads;
+    uint32_t head_dim;
+    uint32_t hidden_dim;
+    uint32_t vocab_size;
+    uint32_t image_token_count;
+    float rope_base;
+    uint64_t seed;
+} mpic_model_config;
+
+typedef struct mpic_model_s* mpic_model_t;         /* device-resident weights */
+typedef struct mpic_kv_s* mpic_kv_t;               /* device KV tensor [L][T][H][D] */
+typedef struct mpic_workspace_s* mpic_workspace_t; /* per-request scratch */
+
+const char* mpic_last_error(void);
+const char* mpic_version(void);
+
+/* ModelConfig::validate / fingerprint (proj/src/config.cpp:12-47). */
+int mpic_config_validate(const mpic_model_config* cfg);
+uint64_t mpic_config_fingerprint(const mpic_model_config* cfg);
+
+/* ---- model ---------------------------------------------------------------------- */
+/* build_model (proj/src/model.cpp:103-123), synthesised ON DEVICE: every fp32 weight is
+ * bit-identical to the reference's counter_uniform(seed, (tag<<32)|layer, i) * scale,
+ * then rounded to nearest-even when dtype == MPIC_BF16. */
+int mpic_model_create(const mpic_model_config* cfg, int device, mpic_dtype dtype,
+                      mpic_model_t* out);
+/* The same model from caller-provided host weights (mpic::Model, model.h:16-30):
+ * layer_w holds 6 pointers per layer in the order wq, wk, wv, wo, w1, w2. */
+int mpic_model_upload(const mpic_model_config* cfg, int device, mpic_dtype dtype,
+                      const float* embedding, const float* lm_head,
+                      const float* const* layer_w, mpic_model_t* out);
+int mpic_model_destroy(mpic_model_t model);
+int mpic_model_config_get(mpic_model_t model, mpic_model_config* out);
+mpic_dtype mpic_model_dtype(mpic_model_t model);
+/* Copy one weight matrix back to host fp32 (which: 0 emb, 1 lm_head, 2..7 wq wk wv wo
+ * w1 w2). Test hook for the bit-exact synthesis check. */
+int mpic_model_download_weight(mpic_model_t model, int which, uint32_t layer, float* out);
+
+/* ---- KV tensors ------------------------------------------------------------------ */
+int mpic_kv_alloc(uint32_t n_layers, uint32_t n_tokens, uint32_t n_heads, uint32_t head_dim,
+                  mpic_dtype dtype, int device, mpic_kv_t* out);
+int mpic_kv_free(mpic_kv_t kv);
+int mpic_kv_shape(mpic_kv_t kv, uint32_t* shape4, mpic_dtype* dtype);
+/* Device pointers of the K and V planes (each L*T*H*D elements of the kv dtype). */
+int mpic_kv_device_ptrs(mpic_kv_t kv, void** k, void** v);
+/* Host fp32 <-> device (converting to/from bf16 on the device when needed).
+ * Synchronous on `stream`. */
+int mpic_kv_upload(mpic_kv_t kv, const float* k, const float* v, void* stream);
+int mpic_kv_download(mpic_kv_t kv, float* k, float* v, void* stream);
+/* Zero-fill rows [row0, row0+rows) of every layer (async). */
+int mpic_kv_zero_rows(mpic_kv_t kv, uint32_t row0, uint32_t rows, void* stream);
+
+/* ---- assembly: assemble_linked_cache (proj/src/linker.cpp:260-314) ---------------- */
+/* One cached chunk placed into the request cache: rows [src_row0, src_row0+rows) of
+ * `src` go to rows [dst_row0, ...) of the destination, for every layer. Under
+ * MPIC_REROTATE the K rows are rotated by delta = dst_row0 - (position_base + src_row0)
+ * (model.cpp:64-83; the delta is the same for every row of a chunk). */
+typedef struct {
+    mpic_kv_t src;
+    uint32_t src_row0;
+    uint32_t dst_row0;
+    uint32_t rows;
+    uint32_t position_base; /* KvCacheEntry::position_base of the chunk */
+} mpic_chunk_ref;
+
+/* Gathers all chunks into dst in ONE launch (async on `stream`). When zero_gaps != 0,
+ * every dst row not covered by a chunk is zero-filled (the reference's Dummy slots,
+ * tensor.h:20-23). Source and destination dtypes may differ (fp32 chunks from a host
+ * staging buffer into a bf16 request cache). */
+int mpic_assemble(void* stream, const mpic_chunk_ref* chunks, uint32_t n_chunks, mpic_kv_t dst,
+                  mpic_reposition reposition, float rope_base, int zero_gaps);
+/* Same with raw device pointers for the sources (e.g. a pinned/H2D staging ring):
+ * src_k[i]/src_v[i] point at [L][src_tokens[i]][H][D] planes of dtype src_dtype. */
+int mpic_assemble_raw(void* stream, const void* const* src_k, const void* const* src_v,
+                      const uint32_t* src_tokens, mpic_dtype src_dtype,
+                      const mpic_chunk_ref* chunks, uint32_t n_chunks, mpic_kv_t dst,
+                      mpic_reposition reposition, float rope_base, int zero_gaps);
+
+/* ---- selective recompute --------------------------------------------------------- */
+/* Scratch for up to max_rows recomputed rows over caches of up to max_ctx tokens. */
+int mpic_workspace_create(mpic_model_t model, uint32_t max_rows, uint32_t max_ctx,
+                          mpic_workspace_t* out);
+int mpic_workspace_destroy(mpic_workspace_t ws);
+
+/* selective_core (proj/src/linker.cpp:35-135): recompute Q/K/V and the full layer
+ * stack for the `m` rows `rows` (ascending cache indices; token ids `ids`), rotate Q/K
+ * at their own index, scatter K/V into `kv`, attend each row over kv rows [0, row],
+ * and write the first-token logits (vocab floats) of the last row.
+ * Host pointers; synchronous (returns when logits are in host memory). */
+int mpic_selective_prefill(mpic_model_t model, mpic_workspace_t ws, const int32_t* ids,
+                           const uint32_t* rows, uint32_t m, mpic_kv_t kv, float* logits,
+                           void* stream);
+/* extend_rows (proj/src/model.cpp:211-330): rows [start, start+m) of kv recomputed for
+ * `ids` at rotary positions position_base+start+i. kv must already hold start+m rows. */
+int mpic_prefill_extend(mpic_model_t model, mpic_workspace_t ws, const int32_t* ids, uint32_t m,
+                        uint32_t start, uint32_t position_base, mpic_kv_t kv, float* logits,
+                        void* stream);
+/* Fully asynchronous form of both: every pointer is a DEVICE pointer, ids are assumed
+ * in-vocabulary (the host forms validate), max_pos >= every row and rotary position,
+ * logits land in d_logits on `stream`. */
+int mpic_forward_rows_async(mpic_model_t model, mpic_workspace_t ws, const int32_t* d_ids,
+                            const uint32_t* d_rows, const uint32_t* d_rope_pos, uint32_t m,
+                            uint32_t max_pos, mpic_kv_t kv, float* d_logits, void* stream);
+
+/* ---- request-level host logic (integer work; bit-exact with the reference) -------- */
+/* A segmented prompt (SegmentedPrompt, proj/include/mpic/linker.h:14-54) as flat arrays. */
+typedef struct {
+    uint32_t n_segments;
+    const uint8_t* kinds;    /* per segment: 0 = text, 1 = image */
+    const uint32_t* lens;    /* per segment token count */
+    const int32_t* text_ids; /* text segments' ids, concatenated in order */
+    const uint8_t* hashes;   /* 32-byte content hash per image segment, in order */
+} mpic_prompt;
+
+typedef enum {
+    MPIC_POLICY_MPIC_K = 0, /* MpicKPolicy (linker.h:58-63) */
+    MPIC_POLICY_TEXT_ONLY = 1,
+    MPIC_POLICY_ALL = 2,
+    MPIC_POLICY_PREFIX_ONLY = 3
+} mpic_policy_tag;
+
+typedef struct {
+    int policy;        /* mpic_policy_tag */
+    uint32_t k;        /* MpicKPolicy::k */
+    int global_budget; /* MpicKPolicy::global */
+} mpic_policy;
+
+/* image_token_ids (proj/src/model.cpp:148-156). */
+int mpic_image_token_ids(const mpic_model_config* cfg, const uint8_t* hash32, uint32_t count,
+                         int32_t* out);
+/* select_tokens (proj/src/linker.cpp:209-258): out holds total_tokens entries; *m = |mask|. */
+int mpic_select_tokens(const mpic_prompt* prompt, const mpic_policy* policy, uint32_t* out,
+                       uint32_t* m);
+/* SegmentedPrompt::flatten_ids (proj/src/linker.cpp:160-172): out holds total_tokens ids. */
+int mpic_flatten_ids(const mpic_model_config* cfg, const mpic_prompt* prompt, int32_t* out);
+
+/* One MPIC-k request end to end on the device: select_tokens -> assemble_linked_cache ->
+ * selective_prefill (the composition of test_transfer.cpp:153-188). chunks[i] is the
+ * device-resident (Device tier) entry of the i-th image segment, position_bases[i] its
+ * KvCacheEntry::position_base. `linked` receives the finished [L][n][H][D] cache;
+ * `selected` (may be NULL; else n entries) the recompute set, *m_out its size; logits
+ * (host, vocab floats) the first-token logits. Synchronous on `stream`. */
+int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
+                         const mpic_policy* policy, const mpic_kv_t* chunks,
+                         mpic_reposition reposition, const uint32_t* position_bases,
+                         mpic_kv_t linked, float* logits, uint32_t* selected, uint32_t* m_out,
+                         void* stream);
+/* Same request with the chunk KV in HOST memory (fp32 [L][len][H][D] per image, pinned for
+ * full PCIe rate): the loader streams layer l of every chunk to HBM on a side stream while
+ * layer l-1 is being recomputed; each landed layer is assembled (and cast to the model
+ * dtype) right before it is used. */
+int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
+                              const mpic_policy* policy, const float* const* chunk_k,
+                              const float* const* chunk_v, const uint32_t* position_bases,
+                              mpic_reposition reposition, mpic_kv_t linked, float* logits,
+                              uint32_t* selected, uint32_t* m_out, void* stream);
+
+/* Pinned host memory for chunk staging (cudaMallocHost); mpic_host_free releases it. */
+int mpic_host_alloc(size_t bytes, void** out);
+int mpic_host_free(void* p);
+
+/* Test hook: out[M][N] (fp32, device) = A[M][K] . W[N][K]^T for bf16 device operands,
+ * through the tcgen05 GEMM (path 1) or the SIMT GEMM (path 0). Async on `stream`. */
+int mpic_test_gemm(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uint32_t K, int path,
+                   float* d_out, void* stream);
+
+/* Number of kernels the last forward/assemble call on this thread launched. */
+uint32_t mpic_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPIC_B200_H */

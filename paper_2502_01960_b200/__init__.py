@@ -1,0 +1,297 @@
+"""B200-native MPIC partial-reuse prefill (arxiv 2502.01960) — Python host binding.
+
+The product is the native library ``lib/libmpic_b200.so`` (sm_100a CUDA kernels + the C
+ABI declared in ``include/mpic_b200.h`` + the C++ ``mpic::`` host API declared in
+``include/mpic/*.h``). This module is a thin ctypes mirror of the reference's public
+interface (``proj/include/mpic/*.h``) for Python callers, tests and the bench: same
+names, argument meaning and error classes. Every call goes to the native library; if it
+is missing the call raises ``ExtensionMissing`` (there is no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import (ChunkRef, ExtensionMissing, ModelConfig, MpicError, PolicyDesc, PromptDesc,
+                   check, lib)
+
+__all__ = ["ModelConfig", "Model", "KV", "Workspace", "Prompt", "MpicError", "ExtensionMissing",
+           "F32", "BF16", "AS_STORED", "REROTATE", "POLICY_MPIC_K", "POLICY_TEXT_ONLY",
+           "POLICY_ALL", "POLICY_PREFIX_ONLY", "config", "fingerprint", "image_token_ids",
+           "select_tokens", "flatten_ids", "assemble", "selective_prefill", "prefill_extend",
+           "request_prefill", "request_prefill_host", "last_launch_count", "HostBuffer"]
+
+F32, BF16 = 0, 1
+AS_STORED, REROTATE = 0, 1
+POLICY_MPIC_K, POLICY_TEXT_ONLY, POLICY_ALL, POLICY_PREFIX_ONLY = 0, 1, 2, 3
+
+
+def config(n_layers=2, n_heads=2, head_dim=8, hidden_dim=None, vocab_size=256,
+           image_token_count=16, rope_base=10000.0, seed=0) -> ModelConfig:
+    """mpic::ModelConfig with the reference's defaults (config.h:7-15)."""
+    if hidden_dim is None:
+        hidden_dim = n_heads * head_dim
+    return ModelConfig(n_layers, n_heads, head_dim, hidden_dim, vocab_size, image_token_count,
+                       rope_base, seed)
+
+
+def fingerprint(cfg: ModelConfig) -> int:
+    return int(lib().mpic_config_fingerprint(C.byref(cfg)))
+
+
+def last_launch_count() -> int:
+    """Kernels launched by the last library call on this thread."""
+    return int(lib().mpic_last_launch_count())
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return int(getattr(stream, "cuda_stream", stream))
+
+
+class Model:
+    """Device-resident model: build_model (model.cpp:103-123) synthesised on the GPU."""
+
+    def __init__(self, cfg: ModelConfig, dtype: int = F32, device: int = 0, weights=None):
+        self.cfg, self.dtype, self.device = cfg, dtype, device
+        h = C.c_void_p()
+        if weights is None:
+            check(lib().mpic_model_create(C.byref(cfg), device, dtype, C.byref(h)))
+        else:
+            emb, lm, layers = weights
+            self._keep = [np.ascontiguousarray(a, np.float32) for a in [emb, lm] + list(layers)]
+            ptrs = (C.c_void_p * len(layers))(*[a.ctypes.data for a in self._keep[2:]])
+            check(lib().mpic_model_upload(C.byref(cfg), device, dtype, self._keep[0].ctypes.data,
+                                          self._keep[1].ctypes.data, ptrs, C.byref(h)))
+        self.handle = h.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().mpic_model_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+    def weight(self, which: int, layer: int = 0) -> np.ndarray:
+        c = self.cfg
+        h = c.hidden_dim
+        shape = {0: (c.vocab_size, h), 1: (c.vocab_size, h), 6: (4 * h, h),
+                 7: (h, 4 * h)}.get(which, (h, h))
+        out = np.zeros(shape, np.float32)
+        check(lib().mpic_model_download_weight(self.handle, which, layer, out.ctypes.data))
+        return out
+
+
+class KV:
+    """Device KV tensor [L][T][H][D] (KvTensor, tensor.h:11-55)."""
+
+    def __init__(self, L, T, H, D, dtype=F32, device=0):
+        h = C.c_void_p()
+        check(lib().mpic_kv_alloc(L, T, H, D, dtype, device, C.byref(h)))
+        self.handle, self.shape, self.dtype = h.value, (L, T, H * D), dtype
+
+    @classmethod
+    def from_host(cls, k: np.ndarray, v: np.ndarray, H: int, D: int, dtype=F32, device=0,
+                  stream=None):
+        L, T = k.shape[0], k.shape[1]
+        kv = cls(L, T, H, D, dtype, device)
+        kv.upload(k, v, stream)
+        return kv
+
+    def upload(self, k, v, stream=None):
+        k = np.ascontiguousarray(k, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        assert k.size == self.shape[0] * self.shape[1] * self.shape[2]
+        check(lib().mpic_kv_upload(self.handle, k.ctypes.data, v.ctypes.data, _stream_ptr(stream)))
+
+    def download(self, stream=None):
+        k = np.zeros(self.shape, np.float32)
+        v = np.zeros(self.shape, np.float32)
+        check(lib().mpic_kv_download(self.handle, k.ctypes.data, v.ctypes.data,
+                                     _stream_ptr(stream)))
+        return k, v
+
+    def device_ptrs(self):
+        k, v = C.c_void_p(), C.c_void_p()
+        check(lib().mpic_kv_device_ptrs(self.handle, C.byref(k), C.byref(v)))
+        return k.value, v.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().mpic_kv_free(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+
+class Workspace:
+    def __init__(self, model: Model, max_rows: int, max_ctx: int = 0):
+        h = C.c_void_p()
+        check(lib().mpic_workspace_create(model.handle, max_rows, max_ctx, C.byref(h)))
+        self.handle, self.model = h.value, model
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().mpic_workspace_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+
+class HostBuffer:
+    """Pinned host memory (cudaMallocHost) viewed as a numpy array."""
+
+    def __init__(self, shape, dtype=np.float32):
+        n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = C.c_void_p()
+        check(lib().mpic_host_alloc(max(n, 1), C.byref(p)))
+        self.ptr = p.value
+        buf = (C.c_uint8 * max(n, 1)).from_address(self.ptr)
+        self.array = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            self.array = None
+            lib().mpic_host_free(self.ptr)
+            self.ptr = None
+
+    __del__ = close
+
+
+@dataclass
+class Prompt:
+    """SegmentedPrompt (linker.h:14-54) as flat arrays: kinds 0=text/1=image, lens,
+    concatenated text ids, 32-byte content hash per image."""
+
+    kinds: np.ndarray
+    lens: np.ndarray
+    text_ids: np.ndarray
+    hashes: np.ndarray
+
+    @classmethod
+    def from_segments(cls, segments):
+        """segments: ('text', ids) or ('image', hash32, token_count)."""
+        kinds, lens, text, hashes = [], [], [], []
+        for seg in segments:
+            if seg[0] == "text":
+                kinds.append(0)
+                lens.append(len(seg[1]))
+                text.extend(int(t) for t in seg[1])
+            else:
+                kinds.append(1)
+                lens.append(int(seg[2]))
+                hashes.append(np.frombuffer(bytes(seg[1]), np.uint8))
+        return cls(np.array(kinds, np.uint8), np.array(lens, np.uint32), np.array(text, np.int32),
+                   np.concatenate(hashes) if hashes else np.zeros(0, np.uint8))
+
+    @property
+    def n(self) -> int:
+        return int(self.lens.sum())
+
+    def desc(self) -> PromptDesc:
+        self._keep = [np.ascontiguousarray(self.kinds, np.uint8),
+                      np.ascontiguousarray(self.lens, np.uint32),
+                      np.ascontiguousarray(self.text_ids if self.text_ids.size else np.zeros(1),
+                                           np.int32),
+                      np.ascontiguousarray(self.hashes if self.hashes.size else np.zeros(32),
+                                           np.uint8)]
+        return PromptDesc(len(self.kinds), *[a.ctypes.data for a in self._keep])
+
+
+def image_token_ids(cfg: ModelConfig, hash32: bytes, count: int) -> np.ndarray:
+    out = np.zeros(count, np.int32)
+    h = np.frombuffer(bytes(hash32), np.uint8).copy()
+    check(lib().mpic_image_token_ids(C.byref(cfg), h.ctypes.data, count, out.ctypes.data))
+    return out
+
+
+def select_tokens(prompt: Prompt, policy: int = POLICY_MPIC_K, k: int = 32,
+                  global_budget: bool = False) -> np.ndarray:
+    out = np.zeros(max(prompt.n, 1), np.uint32)
+    m = C.c_uint32()
+    pol = PolicyDesc(policy, k, int(global_budget))
+    check(lib().mpic_select_tokens(C.byref(prompt.desc()), C.byref(pol), out.ctypes.data,
+                                   C.byref(m)))
+    return out[:m.value].copy()
+
+
+def flatten_ids(cfg: ModelConfig, prompt: Prompt) -> np.ndarray:
+    out = np.zeros(prompt.n, np.int32)
+    check(lib().mpic_flatten_ids(C.byref(cfg), C.byref(prompt.desc()), out.ctypes.data))
+    return out
+
+
+def assemble(chunks, dst: KV, reposition: int = AS_STORED, rope_base: float = 10000.0,
+             zero_gaps: bool = True, stream=None):
+    """chunks: list of (KV src, src_row0, dst_row0, rows, position_base)."""
+    arr = (ChunkRef * max(len(chunks), 1))(
+        *[ChunkRef(c[0].handle, c[1], c[2], c[3], c[4]) for c in chunks])
+    check(lib().mpic_assemble(_stream_ptr(stream), arr, len(chunks), dst.handle, reposition,
+                              rope_base, int(zero_gaps)))
+
+
+def selective_prefill(model: Model, ws: Workspace, ids, rows, kv: KV, stream=None) -> np.ndarray:
+    ids = np.ascontiguousarray(ids, np.int32)
+    rows = np.ascontiguousarray(rows, np.uint32)
+    logits = np.zeros(model.cfg.vocab_size, np.float32)
+    check(lib().mpic_selective_prefill(model.handle, ws.handle, ids.ctypes.data, rows.ctypes.data,
+                                       len(ids), kv.handle, logits.ctypes.data,
+                                       _stream_ptr(stream)))
+    return logits
+
+
+def prefill_extend(model: Model, ws: Workspace, ids, start: int, position_base: int, kv: KV,
+                   stream=None) -> np.ndarray:
+    ids = np.ascontiguousarray(ids, np.int32)
+    logits = np.zeros(model.cfg.vocab_size, np.float32)
+    check(lib().mpic_prefill_extend(model.handle, ws.handle, ids.ctypes.data, len(ids), start,
+                                    position_base, kv.handle, logits.ctypes.data,
+                                    _stream_ptr(stream)))
+    return logits
+
+
+def request_prefill(model: Model, ws: Workspace, prompt: Prompt, chunks, linked: KV,
+                    policy: int = POLICY_MPIC_K, k: int = 32, global_budget: bool = False,
+                    reposition: int = AS_STORED, position_bases=None, stream=None):
+    """select_tokens -> assemble_linked_cache -> selective_prefill with device-resident
+    chunks (one KV per image segment). Returns (logits, selected rows)."""
+    n_img = int((prompt.kinds == 1).sum())
+    arr = (C.c_void_p * max(n_img, 1))(*[c.handle for c in chunks])
+    pb = np.ascontiguousarray(position_bases if position_bases is not None else np.zeros(n_img),
+                              np.uint32)
+    logits = np.zeros(model.cfg.vocab_size, np.float32)
+    sel = np.zeros(prompt.n, np.uint32)
+    m = C.c_uint32()
+    pol = PolicyDesc(policy, k, int(global_budget))
+    check(lib().mpic_request_prefill(model.handle, ws.handle, C.byref(prompt.desc()),
+                                     C.byref(pol), arr, reposition, pb.ctypes.data, linked.handle,
+                                     logits.ctypes.data, sel.ctypes.data, C.byref(m),
+                                     _stream_ptr(stream)))
+    return logits, sel[:m.value].copy()
+
+
+def request_prefill_host(model: Model, ws: Workspace, prompt: Prompt, chunk_k, chunk_v,
+                         linked: KV, policy: int = POLICY_MPIC_K, k: int = 32,
+                         global_budget: bool = False, reposition: int = AS_STORED,
+                         position_bases=None, stream=None, logits_out=None):
+    """Same request with chunk KV in host memory (numpy fp32 [L][len][h], ideally pinned
+    HostBuffer arrays): the loader streams them layer by layer to HBM."""
+    n_img = len(chunk_k)
+    kp = (C.c_void_p * max(n_img, 1))(*[a.ctypes.data for a in chunk_k])
+    vp = (C.c_void_p * max(n_img, 1))(*[a.ctypes.data for a in chunk_v])
+    pb = np.ascontiguousarray(position_bases if position_bases is not None else np.zeros(n_img),
+                              np.uint32)
+    logits = logits_out if logits_out is not None else np.zeros(model.cfg.vocab_size, np.float32)
+    sel = np.zeros(prompt.n, np.uint32)
+    m = C.c_uint32()
+    pol = PolicyDesc(policy, k, int(global_budget))
+    check(lib().mpic_request_prefill_host(model.handle, ws.handle, C.byref(prompt.desc()),
+                                          C.byref(pol), kp, vp, pb.ctypes.data, reposition,
+                                          linked.handle, logits.ctypes.data, sel.ctypes.data,
+                                          C.byref(m), _stream_ptr(stream)))
+    return logits, sel[:m.value].copy()

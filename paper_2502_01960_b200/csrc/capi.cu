@@ -1,0 +1,1076 @@
+// C ABI of the MPIC B200 path (include/mpic_b200.h): handles, the per-layer launch
+// sequence of the selective recompute, and the assembly entry points.
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mpicb {
+namespace {
+thread_local std::string g_last_error;
+thread_local uint32_t g_launches = 0;
+}  // namespace
+void note_launch(uint32_t n) { g_launches += n; }
+}  // namespace mpicb
+
+using namespace mpicb;
+
+struct mpic_model_s {
+    mpic_model_config cfg{};
+    int device = 0;
+    mpic_dtype dtype = MPIC_F32;
+    float* emb = nullptr;      // [V][h] fp32 (gathered, never multiplied)
+    void* lm_head = nullptr;   // [V][h] dtype
+    std::vector<void*> wqkv;   // per layer [3h][h]: wq | wk | wv rows
+    std::vector<void*> wo;     // [h][h]
+    std::vector<void*> w1;     // [4h][h]
+    std::vector<void*> w2;     // [h][4h]
+    double* inv_freq = nullptr;  // [D/2]
+    float2* rope = nullptr;      // [rope_cap][D/2]
+    uint32_t rope_cap = 0;
+    std::vector<float2*> retired;  // old tables kept alive (other streams may read them)
+    std::mutex mu;
+};
+
+struct mpic_kv_s {
+    uint32_t L = 0, T = 0, H = 0, D = 0;
+    mpic_dtype dtype = MPIC_F32;
+    int device = 0;
+    void* k = nullptr;
+    void* v = nullptr;
+    size_t elems() const { return (size_t)L * T * H * D; }
+};
+
+struct mpic_workspace_s {
+    mpic_model_t model = nullptr;
+    uint32_t max_rows = 0, max_ctx = 0, m_pad = 0;
+    int32_t* d_ids = nullptr;
+    uint32_t* d_rows = nullptr;
+    uint32_t* d_pos = nullptr;
+    float* x = nullptr;                 // residual stream fp32 [m_pad][h]
+    __nv_bfloat16* xb = nullptr;        // bf16 copy of x (GEMM A operand, bf16 mode)
+    void* q = nullptr;                  // [m_pad][h] dtype
+    void* attn = nullptr;               // [m_pad][h] dtype
+    void* ffn = nullptr;                // [m_pad][4h] dtype
+    float* d_logits = nullptr;          // [V]
+    int32_t* h_ids = nullptr;           // pinned staging
+    uint32_t* h_rows = nullptr;
+    uint32_t* h_pos = nullptr;
+    float* h_logits = nullptr;
+    // loader lane (mpic_request_prefill_host): side stream, 2-slot HBM staging ring
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_ready[2] = {nullptr, nullptr};
+    cudaEvent_t ev_free[2] = {nullptr, nullptr};
+    void* stage[2] = {nullptr, nullptr};
+    size_t stage_cap = 0;
+};
+
+#define API_BEGIN \
+    try {         \
+        g_launches = 0;
+#define API_END                                   \
+    return MPIC_OK;                               \
+    }                                             \
+    catch (const mpicb::Error& e) {               \
+        mpicb::g_last_error = e.what();           \
+        return e.code;                            \
+    }                                             \
+    catch (const std::exception& e) {             \
+        mpicb::g_last_error = e.what();           \
+        return MPIC_ERR_CUDA;                     \
+    }
+
+namespace {
+
+void set_device(int dev) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        throw Error(MPIC_ERR_NO_DEVICE, "no CUDA device: the MPIC B200 path has no CPU fallback");
+    MPIC_REQUIRE(dev >= 0 && dev < n, MPIC_ERR_VALIDATION, "device index out of range");
+    MPIC_CUDA(cudaSetDevice(dev));
+    cudaDeviceProp p;
+    MPIC_CUDA(cudaGetDeviceProperties(&p, dev));
+    if (p.major != 10)
+        throw Error(MPIC_ERR_NO_DEVICE, std::string("device ") + p.name +
+                                            " is not sm_100 (this library is built for sm_100a only)");
+}
+
+void validate_cfg(const mpic_model_config* c) {
+    MPIC_REQUIRE(c, MPIC_ERR_VALIDATION, "null config");
+    // ModelConfig::validate (proj/src/config.cpp:12-28)
+    MPIC_REQUIRE(c->n_layers && c->n_heads && c->head_dim && c->hidden_dim, MPIC_ERR_CONFIG,
+                 "model dimensions must be positive");
+    MPIC_REQUIRE(c->hidden_dim == c->n_heads * c->head_dim, MPIC_ERR_CONFIG,
+                 "hidden_dim must equal n_heads * head_dim");
+    MPIC_REQUIRE(c->vocab_size >= 2, MPIC_ERR_CONFIG, "vocab_size must be at least 2");
+    MPIC_REQUIRE(c->image_token_count > 0, MPIC_ERR_CONFIG, "image_token_count must be positive");
+    MPIC_REQUIRE(c->rope_base > 0.0f, MPIC_ERR_CONFIG, "rope_base must be positive");
+}
+
+void validate_device_cfg(const mpic_model_config* c) {
+    // Limits of this implementation (documented in DESIGN.md).
+    MPIC_REQUIRE(c->head_dim % 2 == 0, MPIC_ERR_CONFIG, "head_dim must be even on the B200 path");
+    MPIC_REQUIRE(c->head_dim <= 256, MPIC_ERR_CONFIG, "head_dim must be <= 256 on the B200 path");
+}
+
+template <typename T>
+T* dmalloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    MPIC_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+size_t esz(mpic_dtype d) { return d == MPIC_BF16 ? 2 : 4; }
+
+void free_model(mpic_model_t m) {
+    if (!m) return;
+    cudaSetDevice(m->device);
+    cudaFree(m->emb);
+    cudaFree(m->lm_head);
+    for (auto* p : m->wqkv) cudaFree(p);
+    for (auto* p : m->wo) cudaFree(p);
+    for (auto* p : m->w1) cudaFree(p);
+    for (auto* p : m->w2) cudaFree(p);
+    cudaFree(m->inv_freq);
+    cudaFree(m->rope);
+    for (auto* p : m->retired) cudaFree(p);
+    delete m;
+}
+
+void alloc_model(mpic_model_t m) {
+    const size_t h = m->cfg.hidden_dim, V = m->cfg.vocab_size, L = m->cfg.n_layers;
+    const size_t e = esz(m->dtype);
+    m->emb = dmalloc<float>(V * h);
+    MPIC_CUDA(cudaMalloc(&m->lm_head, V * h * e));
+    for (size_t l = 0; l < L; ++l) {
+        void* p;
+        MPIC_CUDA(cudaMalloc(&p, 3 * h * h * e));
+        m->wqkv.push_back(p);
+        MPIC_CUDA(cudaMalloc(&p, h * h * e));
+        m->wo.push_back(p);
+        MPIC_CUDA(cudaMalloc(&p, 4 * h * h * e));
+        m->w1.push_back(p);
+        MPIC_CUDA(cudaMalloc(&p, 4 * h * h * e));
+        m->w2.push_back(p);
+    }
+    const uint32_t D = m->cfg.head_dim;
+    std::vector<double> inv(D / 2);
+    for (uint32_t i = 0; i + 1 < D; i += 2)  // model.cpp:51-53
+        inv[i / 2] = std::pow(static_cast<double>(m->cfg.rope_base), -static_cast<double>(i) / D);
+    m->inv_freq = dmalloc<double>(D / 2);
+    MPIC_CUDA(cudaMemcpy(m->inv_freq, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+// Pointer to weight `which` (0 emb, 1 lm_head, 2..7 wq wk wv wo w1 w2) and its size.
+void* weight_ptr(mpic_model_t m, int which, uint32_t layer, size_t* count) {
+    const size_t h = m->cfg.hidden_dim, V = m->cfg.vocab_size;
+    const size_t e = esz(m->dtype);
+    MPIC_REQUIRE(which >= 0 && which <= 7, MPIC_ERR_VALIDATION, "bad weight index");
+    MPIC_REQUIRE(which < 2 || layer < m->cfg.n_layers, MPIC_ERR_VALIDATION, "layer out of range");
+    switch (which) {
+        case 0: *count = V * h; return m->emb;
+        case 1: *count = V * h; return m->lm_head;
+        case 2: *count = h * h; return m->wqkv[layer];
+        case 3: *count = h * h; return (char*)m->wqkv[layer] + h * h * e;
+        case 4: *count = h * h; return (char*)m->wqkv[layer] + 2 * h * h * e;
+        case 5: *count = h * h; return m->wo[layer];
+        case 6: *count = 4 * h * h; return m->w1[layer];
+        default: *count = 4 * h * h; return m->w2[layer];
+    }
+}
+
+// Grow the cached RoPE (cos, sin) table to cover positions [0, need).
+void ensure_rope(mpic_model_t m, uint32_t need, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(m->mu);
+    if (need <= m->rope_cap) return;
+    uint32_t cap = 4096;
+    while (cap < need) cap *= 2;
+    const uint32_t half = m->cfg.head_dim / 2;
+    float2* t = dmalloc<float2>((size_t)cap * half);
+    launch_rope_table(m->inv_freq, half, 0, cap, t, s);
+    MPIC_CUDA(cudaStreamSynchronize(s));
+    if (m->rope) m->retired.push_back(m->rope);
+    m->rope = t;
+    m->rope_cap = cap;
+}
+
+// Upload n host fp32 values into a device buffer of dtype dt (cast on device).
+void upload_cast(void* dst, mpic_dtype dt, const float* src, size_t n, cudaStream_t s) {
+    if (dt == MPIC_F32) {
+        MPIC_CUDA(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyHostToDevice, s));
+        MPIC_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    const size_t chunk = std::min<size_t>(n, (size_t)64 << 20);
+    float* tmp = dmalloc<float>(chunk);
+    for (size_t off = 0; off < n; off += chunk) {
+        const size_t c = std::min(chunk, n - off);
+        MPIC_CUDA(cudaMemcpyAsync(tmp, src + off, c * 4, cudaMemcpyHostToDevice, s));
+        launch_f32_to_bf16(tmp, static_cast<__nv_bfloat16*>(dst) + off, c, s);
+    }
+    MPIC_CUDA(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+}
+
+void download_cast(float* dst, const void* src, mpic_dtype dt, size_t n, cudaStream_t s) {
+    if (dt == MPIC_F32) {
+        MPIC_CUDA(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyDeviceToHost, s));
+        MPIC_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    const size_t chunk = std::min<size_t>(n, (size_t)64 << 20);
+    float* tmp = dmalloc<float>(chunk);
+    for (size_t off = 0; off < n; off += chunk) {
+        const size_t c = std::min(chunk, n - off);
+        launch_bf16_to_f32(static_cast<const __nv_bfloat16*>(src) + off, tmp, c, s);
+        MPIC_CUDA(cudaMemcpyAsync(dst + off, tmp, c * 4, cudaMemcpyDeviceToHost, s));
+    }
+    MPIC_CUDA(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+}
+
+// One projection GEMM with its fused epilogue; tcgen05 for bf16, SIMT FFMA for fp32.
+void run_gemm(mpic_model_t md, const void* A, const void* W, uint32_t M, uint32_t N, uint32_t K,
+              const EpiParams& ep, cudaStream_t s) {
+    if (md->dtype == MPIC_BF16) {
+        if (tc_gemm_supported(M, N, K)) {
+            launch_gemm_tc(static_cast<const __nv_bfloat16*>(A), K,
+                           static_cast<const __nv_bfloat16*>(W), M, N, K, ep, s);
+            return;
+        }
+        EpiParams e2 = ep;
+        e2.split_k = 1;
+        launch_gemm_simt(A, MPIC_BF16, K, W, MPIC_BF16, M, N, K, e2, MPIC_BF16, s);
+        return;
+    }
+    launch_gemm_simt(A, MPIC_F32, K, W, MPIC_F32, M, N, K, ep, MPIC_F32, s);
+}
+
+// selective_core / extend_rows on the device (linker.cpp:35-135, model.cpp:211-330).
+void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
+                  const uint32_t* d_rows, const uint32_t* d_pos, uint32_t m, uint32_t max_pos,
+                  mpic_kv_t kv, float* d_logits, cudaStream_t s,
+                  const std::function<void(uint32_t)>& before_layer = {}) {
+    const mpic_model_config& c = md->cfg;
+    const uint32_t h = c.hidden_dim, H = c.n_heads, D = c.head_dim;
+    MPIC_REQUIRE(m > 0, MPIC_ERR_VALIDATION, "no tokens to prefill");
+    MPIC_REQUIRE(m <= ws->max_rows, MPIC_ERR_VALIDATION, "more rows than the workspace holds");
+    MPIC_REQUIRE(kv->L == c.n_layers && kv->H == H && kv->D == D, MPIC_ERR_VALIDATION,
+                 "cache shape does not match model");
+    MPIC_REQUIRE(kv->dtype == md->dtype, MPIC_ERR_VALIDATION, "cache dtype does not match model");
+    ensure_rope(md, max_pos + 1, s);
+    const bool bf = md->dtype == MPIC_BF16;
+    const size_t e = esz(md->dtype);
+    const size_t plane = (size_t)kv->T * h * e;
+
+    launch_embed(md->emb, d_ids, m, h, ws->x, bf ? ws->xb : nullptr, s);
+    for (uint32_t l = 0; l < c.n_layers; ++l) {
+        void* kl = (char*)kv->k + l * plane;
+        void* vl = (char*)kv->v + l * plane;
+        if (before_layer) before_layer(l);
+        EpiParams qkv;
+        qkv.mode = EPI_QKV;
+        qkv.q = ws->q;
+        qkv.kv_k = kl;
+        qkv.kv_v = vl;
+        qkv.kv_rows = d_rows;
+        qkv.rope_pos = d_pos;
+        qkv.rope = md->rope;
+        qkv.hidden = h;
+        qkv.head_dim = D;
+        run_gemm(md, bf ? (const void*)ws->xb : (const void*)ws->x, md->wqkv[l], m, 3 * h, h, qkv, s);
+
+        launch_attn_simt(ws->q, kl, vl, md->dtype, d_rows, m, H, D, ws->attn, s);
+
+        EpiParams res;
+        res.mode = EPI_RESID;
+        res.x = ws->x;
+        res.ldx = h;
+        run_gemm(md, ws->attn, md->wo[l], m, h, h, res, s);
+        if (bf) launch_x_to_bf16(ws->x, ws->xb, m, h, s);
+
+        EpiParams gl;
+        gl.mode = EPI_GELU;
+        gl.out = ws->ffn;
+        gl.ldo = 4 * h;
+        run_gemm(md, bf ? (const void*)ws->xb : (const void*)ws->x, md->w1[l], m, 4 * h, h, gl, s);
+
+        run_gemm(md, ws->ffn, md->w2[l], m, h, 4 * h, res, s);
+        if (bf && l + 1 < c.n_layers) launch_x_to_bf16(ws->x, ws->xb, m, h, s);
+    }
+    launch_lm_head(ws->x + (size_t)(m - 1) * h, md->lm_head, md->dtype, c.vocab_size, h, d_logits, s);
+    (void)e;
+}
+
+void check_ids(mpic_model_t md, const int32_t* ids, uint32_t m) {
+    for (uint32_t i = 0; i < m; ++i)
+        if (ids[i] < 0 || static_cast<uint32_t>(ids[i]) >= md->cfg.vocab_size)
+            throw Error(MPIC_ERR_VALIDATION, "token id " + std::to_string(ids[i]) + " out of vocabulary");
+}
+
+// Host-pointer form: stage into pinned memory, run, bring logits back; synchronous.
+void forward_host(mpic_model_t md, mpic_workspace_t ws, const int32_t* ids, const uint32_t* rows,
+                  const uint32_t* pos, uint32_t m, mpic_kv_t kv, float* logits, cudaStream_t s) {
+    MPIC_REQUIRE(ws && ws->model == md, MPIC_ERR_VALIDATION, "workspace belongs to another model");
+    MPIC_REQUIRE(m > 0, MPIC_ERR_VALIDATION, "no tokens to prefill");
+    MPIC_REQUIRE(m <= ws->max_rows, MPIC_ERR_VALIDATION, "more rows than the workspace holds");
+    check_ids(md, ids, m);
+    uint32_t max_pos = 0;
+    for (uint32_t i = 0; i < m; ++i) {
+        MPIC_REQUIRE(rows[i] < kv->T, MPIC_ERR_VALIDATION, "row index outside the cache");
+        MPIC_REQUIRE(i == 0 || rows[i] > rows[i - 1], MPIC_ERR_CONTRACT, "rows must be ascending and unique");
+        max_pos = std::max(max_pos, std::max(rows[i], pos[i]));
+    }
+    std::memcpy(ws->h_ids, ids, m * sizeof(int32_t));
+    std::memcpy(ws->h_rows, rows, m * sizeof(uint32_t));
+    std::memcpy(ws->h_pos, pos, m * sizeof(uint32_t));
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_ids, ws->h_ids, m * 4, cudaMemcpyHostToDevice, s));
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_rows, ws->h_rows, m * 4, cudaMemcpyHostToDevice, s));
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_pos, ws->h_pos, m * 4, cudaMemcpyHostToDevice, s));
+    forward_rows(md, ws, ws->d_ids, ws->d_rows, ws->d_pos, m, max_pos, kv, ws->d_logits, s);
+    MPIC_CUDA(cudaMemcpyAsync(ws->h_logits, ws->d_logits, md->cfg.vocab_size * 4,
+                              cudaMemcpyDeviceToHost, s));
+    MPIC_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(logits, ws->h_logits, md->cfg.vocab_size * sizeof(float));
+}
+
+// Host-side chunk placement: AsmChunk descriptors + per-chunk rerotation tables.
+struct AsmPlan {
+    std::vector<AsmChunk> chunks;
+    std::vector<float2> tables;
+    uint32_t n_tables = 0;
+};
+
+AsmPlan plan_assembly(const void* const* src_k, const void* const* src_v, const uint32_t* src_T,
+                      const mpic_chunk_ref* chunks, uint32_t n, uint32_t T_dst, uint32_t D,
+                      mpic_reposition rep, float rope_base) {
+    MPIC_REQUIRE(D % 2 == 0, MPIC_ERR_CONFIG, "head_dim must be even on the B200 path");
+    AsmPlan p;
+    p.chunks.resize(n);
+    for (uint32_t i = 0; i < n; ++i) {
+        const mpic_chunk_ref& c = chunks[i];
+        MPIC_REQUIRE(c.dst_row0 + c.rows <= T_dst, MPIC_ERR_LINK, "chunk does not fit the request cache");
+        MPIC_REQUIRE(c.src_row0 + c.rows <= src_T[i], MPIC_ERR_LINK, "chunk rows exceed the source entry");
+        for (uint32_t j = 0; j < i; ++j)
+            MPIC_REQUIRE(c.dst_row0 >= chunks[j].dst_row0 + chunks[j].rows ||
+                             chunks[j].dst_row0 >= c.dst_row0 + c.rows,
+                         MPIC_ERR_LINK, "chunks overlap in the request cache");
+        AsmChunk a{};
+        a.src_k = src_k ? src_k[i] : nullptr;
+        a.src_v = src_v ? src_v[i] : nullptr;
+        a.src_tokens = src_T[i];
+        a.src_row0 = c.src_row0;
+        a.dst_row0 = c.dst_row0;
+        a.rows = c.rows;
+        // rerotate_key from = position_base + j, to = start + j (linker.cpp:302-303):
+        // the delta is constant over the chunk; from == to is a no-op (model.cpp:66-68).
+        const double delta = static_cast<double>(c.dst_row0) -
+                             (static_cast<double>(c.position_base) + static_cast<double>(c.src_row0));
+        if (rep == MPIC_REROTATE && delta != 0.0) {
+            a.rotate = 1;
+            a.table = p.n_tables++;
+            for (uint32_t q = 0; q + 1 < D; q += 2) {  // model.cpp:72-76
+                const double freq = std::pow(static_cast<double>(rope_base), -static_cast<double>(q) / D);
+                const double theta = delta * freq;
+                p.tables.push_back(make_float2(static_cast<float>(std::cos(theta)),
+                                               static_cast<float>(std::sin(theta))));
+            }
+        }
+        p.chunks[i] = a;
+    }
+    return p;
+}
+
+// Copies a plan to a stream-ordered device buffer; returns (chunks, tables) pointers.
+void* upload_plan(const AsmPlan& p, cudaStream_t s, const AsmChunk** dc, const float2** dt) {
+    const size_t bytes_c = std::max<size_t>(1, p.chunks.size()) * sizeof(AsmChunk);
+    const size_t bytes_t = std::max<size_t>(1, p.tables.size()) * sizeof(float2);
+    void* dbuf = nullptr;
+    MPIC_CUDA(cudaMallocAsync(&dbuf, bytes_c + bytes_t, s));
+    if (!p.chunks.empty())
+        MPIC_CUDA(cudaMemcpyAsync(dbuf, p.chunks.data(), p.chunks.size() * sizeof(AsmChunk),
+                                  cudaMemcpyHostToDevice, s));
+    if (!p.tables.empty())
+        MPIC_CUDA(cudaMemcpyAsync((char*)dbuf + bytes_c, p.tables.data(), p.tables.size() * sizeof(float2),
+                                  cudaMemcpyHostToDevice, s));
+    *dc = static_cast<const AsmChunk*>(dbuf);
+    *dt = reinterpret_cast<const float2*>((char*)dbuf + bytes_c);
+    return dbuf;
+}
+
+void do_assemble(cudaStream_t s, const void* const* src_k, const void* const* src_v,
+                 const uint32_t* src_T, mpic_dtype src_t, const mpic_chunk_ref* chunks,
+                 uint32_t n, mpic_kv_t dst, mpic_reposition rep, int zero_gaps, float rope_base) {
+    MPIC_REQUIRE(dst, MPIC_ERR_VALIDATION, "null destination cache");
+    const AsmPlan p = plan_assembly(src_k, src_v, src_T, chunks, n, dst->T, dst->D, rep, rope_base);
+    const AsmChunk* dc;
+    const float2* dt;
+    void* buf = upload_plan(p, s, &dc, &dt);
+    launch_assemble(dc, n, dt, p.n_tables, src_t, dst->k, dst->v, dst->dtype, dst->L, dst->T,
+                    dst->H, dst->D, zero_gaps, s);
+    MPIC_CUDA(cudaFreeAsync(buf, s));
+}
+
+// ---- request-level host logic -------------------------------------------------------
+uint64_t fnv1a(const uint8_t* p, size_t n) {  // hash.h:18-25
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (size_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+uint64_t mix64h(uint64_t x) {  // rng.h:10-17
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    x ^= x >> 31;
+    return x;
+}
+uint64_t counter_hash_h(uint64_t seed, uint64_t stream, uint64_t i) {  // rng.h:19-24
+    const uint64_t phi = 0x9e3779b97f4a7c15ull;
+    uint64_t h = mix64h(seed + phi);
+    h = mix64h(h ^ (stream + phi));
+    return mix64h(h ^ (i + phi));
+}
+
+uint64_t fingerprint_of(const mpic_model_config* c);
+
+void image_ids(const mpic_model_config* c, const uint8_t* hash32, uint32_t count, int32_t* out) {
+    // model.cpp:148-156; the first two mixing rounds depend only on the key.
+    const uint64_t key = fnv1a(hash32, 32) ^ fingerprint_of(c);
+    const uint64_t phi = 0x9e3779b97f4a7c15ull;
+    const uint64_t h1 = mix64h(mix64h(key + phi) ^ (0x696d67ull + phi));
+    for (uint32_t i = 0; i < count; ++i)
+        out[i] = static_cast<int32_t>(mix64h(h1 ^ (i + phi)) % c->vocab_size);
+}
+
+uint32_t prompt_tokens(const mpic_prompt* p) {
+    MPIC_REQUIRE(p && p->n_segments > 0, MPIC_ERR_VALIDATION, "prompt needs at least one segment");
+    uint32_t n = 0;
+    for (uint32_t s = 0; s < p->n_segments; ++s) {
+        MPIC_REQUIRE(p->lens[s] > 0, MPIC_ERR_VALIDATION,
+                     p->kinds[s] == 0 ? "empty text segment" : "image segment token_count must be positive");
+        n += p->lens[s];
+    }
+    return n;
+}
+
+uint32_t select_rows(const mpic_prompt* p, const mpic_policy* pol, uint32_t* out) {
+    // linker.cpp:209-258; segments emit ascending indices, so the final sort is a no-op.
+    const uint32_t n = prompt_tokens(p);
+    if (pol->policy == MPIC_POLICY_ALL) {
+        for (uint32_t i = 0; i < n; ++i) out[i] = i;
+        return n;
+    }
+    if (pol->policy == MPIC_POLICY_PREFIX_ONLY) return 0;
+    MPIC_REQUIRE(pol->policy == MPIC_POLICY_MPIC_K || pol->policy == MPIC_POLICY_TEXT_ONLY,
+                 MPIC_ERR_VALIDATION, "unknown selection policy");
+    const bool mk = pol->policy == MPIC_POLICY_MPIC_K;
+    uint32_t budget = (mk && pol->global_budget) ? pol->k : 0, m = 0, at = 0;
+    for (uint32_t s = 0; s < p->n_segments; ++s) {
+        const uint32_t len = p->lens[s];
+        if (p->kinds[s] == 0) {
+            for (uint32_t i = 0; i < len; ++i) out[m++] = at + i;
+        } else if (mk) {
+            uint32_t take;
+            if (pol->global_budget) {
+                take = std::min(budget, len);
+                budget -= take;
+            } else {
+                take = std::min(pol->k, len);
+            }
+            for (uint32_t i = 0; i < take; ++i) out[m++] = at + i;
+        }
+        at += len;
+    }
+    return m;
+}
+
+void flatten(const mpic_model_config* c, const mpic_prompt* p, int32_t* out) {
+    // linker.cpp:160-172
+    uint32_t ti = 0, hi = 0, at = 0;
+    for (uint32_t s = 0; s < p->n_segments; ++s) {
+        const uint32_t len = p->lens[s];
+        if (p->kinds[s] == 0) {
+            std::memcpy(out + at, p->text_ids + ti, len * sizeof(int32_t));
+            ti += len;
+        } else {
+            image_ids(c, p->hashes + 32 * hi, len, out + at);
+            ++hi;
+        }
+        at += len;
+    }
+}
+
+// selective_prefill's contract checks (linker.cpp:319-340) for a freshly assembled cache
+// whose Dummy slots are exactly the text segments.
+void check_contract(const mpic_prompt* p, const uint32_t* sel, uint32_t m, uint32_t n) {
+    MPIC_REQUIRE(m > 0, MPIC_ERR_CONTRACT, "selection mask is empty");
+    MPIC_REQUIRE(sel[m - 1] < n, MPIC_ERR_CONTRACT, "selection mask index out of range");
+    MPIC_REQUIRE(sel[m - 1] == n - 1, MPIC_ERR_CONTRACT, "final prompt token must be selected");
+    uint32_t at = 0, j = 0;
+    for (uint32_t s = 0; s < p->n_segments; ++s) {
+        if (p->kinds[s] == 0)
+            for (uint32_t i = at; i < at + p->lens[s]; ++i) {
+                while (j < m && sel[j] < i) ++j;
+                MPIC_REQUIRE(j < m && sel[j] == i, MPIC_ERR_CONTRACT,
+                             "dummy slot " + std::to_string(i) + " not selected");
+            }
+        at += p->lens[s];
+    }
+}
+
+struct RequestPlan {
+    uint32_t n = 0, m = 0;
+    std::vector<uint32_t> sel;
+    std::vector<int32_t> ids_sel;
+    std::vector<mpic_chunk_ref> refs;  // one per image segment, dst_row0 = segment start
+};
+
+RequestPlan plan_request(mpic_model_t md, const mpic_prompt* p, const mpic_policy* pol,
+                         const uint32_t* position_bases) {
+    RequestPlan r;
+    r.n = prompt_tokens(p);
+    r.sel.resize(r.n);
+    r.m = select_rows(p, pol, r.sel.data());
+    r.sel.resize(r.m);
+    check_contract(p, r.sel.data(), r.m, r.n);
+    std::vector<int32_t> flat(r.n);
+    flatten(&md->cfg, p, flat.data());
+    r.ids_sel.resize(r.m);
+    for (uint32_t i = 0; i < r.m; ++i) r.ids_sel[i] = flat[r.sel[i]];
+    uint32_t at = 0, img = 0;
+    for (uint32_t s = 0; s < p->n_segments; ++s) {
+        if (p->kinds[s] == 1) {
+            mpic_chunk_ref c{};
+            c.src_row0 = 0;
+            c.dst_row0 = at;
+            c.rows = p->lens[s];
+            c.position_base = position_bases ? position_bases[img] : 0;
+            r.refs.push_back(c);
+            ++img;
+        }
+        at += p->lens[s];
+    }
+    return r;
+}
+
+void run_request(mpic_model_t md, mpic_workspace_t ws, const RequestPlan& r, mpic_kv_t linked,
+                 float* logits, uint32_t* selected, uint32_t* m_out, cudaStream_t s,
+                 const std::function<void(uint32_t)>& before_layer) {
+    MPIC_REQUIRE(r.m <= ws->max_rows, MPIC_ERR_VALIDATION, "more rows than the workspace holds");
+    check_ids(md, r.ids_sel.data(), r.m);
+    std::memcpy(ws->h_ids, r.ids_sel.data(), r.m * sizeof(int32_t));
+    std::memcpy(ws->h_rows, r.sel.data(), r.m * sizeof(uint32_t));
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_ids, ws->h_ids, r.m * 4, cudaMemcpyHostToDevice, s));
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_rows, ws->h_rows, r.m * 4, cudaMemcpyHostToDevice, s));
+    forward_rows(md, ws, ws->d_ids, ws->d_rows, ws->d_rows, r.m, r.n - 1, linked, ws->d_logits, s,
+                 before_layer);
+    MPIC_CUDA(cudaMemcpyAsync(ws->h_logits, ws->d_logits, md->cfg.vocab_size * 4,
+                              cudaMemcpyDeviceToHost, s));
+    MPIC_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(logits, ws->h_logits, md->cfg.vocab_size * sizeof(float));
+    if (selected) std::memcpy(selected, r.sel.data(), r.m * sizeof(uint32_t));
+    if (m_out) *m_out = r.m;
+}
+
+void check_linked(mpic_model_t md, mpic_kv_t linked, uint32_t n) {
+    MPIC_REQUIRE(linked, MPIC_ERR_VALIDATION, "null linked cache");
+    MPIC_REQUIRE(linked->T == n, MPIC_ERR_CONTRACT, "linked cache length does not match prompt");
+    MPIC_REQUIRE(linked->L == md->cfg.n_layers && linked->H == md->cfg.n_heads &&
+                     linked->D == md->cfg.head_dim && linked->dtype == md->dtype,
+                 MPIC_ERR_VALIDATION, "linked cache shape does not match model");
+}
+
+}  // namespace
+
+extern "C" uint64_t mpic_config_fingerprint(const mpic_model_config* c);
+namespace {
+uint64_t fingerprint_of(const mpic_model_config* c) { return mpic_config_fingerprint(c); }
+}  // namespace
+
+extern "C" {
+
+const char* mpic_last_error(void) { return g_last_error.c_str(); }
+const char* mpic_version(void) { return "mpic-b200 0.1 (sm_100a)"; }
+uint32_t mpic_last_launch_count(void) { return g_launches; }
+
+int mpic_config_validate(const mpic_model_config* cfg) {
+    API_BEGIN
+    validate_cfg(cfg);
+    API_END
+}
+
+uint64_t mpic_config_fingerprint(const mpic_model_config* c) {
+    // ModelConfig::fingerprint (proj/src/config.cpp:30-47)
+    uint32_t rb;
+    std::memcpy(&rb, &c->rope_base, 4);
+    const uint64_t f[8] = {c->n_layers, c->n_heads, c->head_dim, c->hidden_dim,
+                           c->vocab_size, c->image_token_count, rb, c->seed};
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (uint64_t v : f)
+        for (int b = 0; b < 8; ++b) {
+            h ^= static_cast<uint8_t>(v >> (8 * b));
+            h *= 0x100000001b3ull;
+        }
+    return h;
+}
+
+int mpic_model_create(const mpic_model_config* cfg, int device, mpic_dtype dtype, mpic_model_t* out) {
+    mpic_model_t m = nullptr;
+    API_BEGIN
+    validate_cfg(cfg);
+    validate_device_cfg(cfg);
+    set_device(device);
+    m = new mpic_model_s();
+    m->cfg = *cfg;
+    m->device = device;
+    m->dtype = dtype;
+    alloc_model(m);
+    const size_t h = cfg->hidden_dim, V = cfg->vocab_size;
+    const float scale = 1.0f / std::sqrt(static_cast<float>(h));  // model.cpp:106
+    const size_t e = esz(dtype);
+    cudaStream_t s = 0;
+    launch_synth(cfg->seed, 100, 0, V * h, 1.0f, m->emb, MPIC_F32, s);
+    launch_synth(cfg->seed, 101, 0, V * h, scale, m->lm_head, dtype, s);
+    for (uint32_t l = 0; l < cfg->n_layers; ++l) {
+        launch_synth(cfg->seed, 1, l, h * h, scale, m->wqkv[l], dtype, s);
+        launch_synth(cfg->seed, 2, l, h * h, scale, (char*)m->wqkv[l] + h * h * e, dtype, s);
+        launch_synth(cfg->seed, 3, l, h * h, scale, (char*)m->wqkv[l] + 2 * h * h * e, dtype, s);
+        launch_synth(cfg->seed, 4, l, h * h, scale, m->wo[l], dtype, s);
+        launch_synth(cfg->seed, 5, l, 4 * h * h, scale, m->w1[l], dtype, s);
+        launch_synth(cfg->seed, 6, l, 4 * h * h, scale, m->w2[l], dtype, s);
+    }
+    ensure_rope(m, 1, s);
+    MPIC_CUDA(cudaDeviceSynchronize());
+    *out = m;
+    m = nullptr;
+    API_END
+}
+
+int mpic_model_upload(const mpic_model_config* cfg, int device, mpic_dtype dtype,
+                      const float* embedding, const float* lm_head, const float* const* layer_w,
+                      mpic_model_t* out) {
+    mpic_model_t m = nullptr;
+    API_BEGIN
+    validate_cfg(cfg);
+    validate_device_cfg(cfg);
+    set_device(device);
+    m = new mpic_model_s();
+    m->cfg = *cfg;
+    m->device = device;
+    m->dtype = dtype;
+    alloc_model(m);
+    cudaStream_t s = 0;
+    for (int which = 0; which < 8; ++which) {
+        const uint32_t nl = which < 2 ? 1 : cfg->n_layers;
+        for (uint32_t l = 0; l < nl; ++l) {
+            size_t cnt;
+            void* dst = weight_ptr(m, which, l, &cnt);
+            const float* src = which == 0 ? embedding : which == 1 ? lm_head : layer_w[6 * l + (which - 2)];
+            upload_cast(dst, which == 0 ? MPIC_F32 : dtype, src, cnt, s);
+        }
+    }
+    ensure_rope(m, 1, s);
+    *out = m;
+    m = nullptr;
+    API_END
+}
+
+int mpic_model_destroy(mpic_model_t model) {
+    API_BEGIN
+    free_model(model);
+    API_END
+}
+
+int mpic_model_config_get(mpic_model_t model, mpic_model_config* out) {
+    API_BEGIN
+    *out = model->cfg;
+    API_END
+}
+
+mpic_dtype mpic_model_dtype(mpic_model_t model) { return model->dtype; }
+
+int mpic_model_download_weight(mpic_model_t m, int which, uint32_t layer, float* out) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(m->device));
+    size_t cnt;
+    void* src = weight_ptr(m, which, layer, &cnt);
+    download_cast(out, src, which == 0 ? MPIC_F32 : m->dtype, cnt, 0);
+    API_END
+}
+
+int mpic_kv_alloc(uint32_t L, uint32_t T, uint32_t H, uint32_t D, mpic_dtype dtype, int device,
+                  mpic_kv_t* out) {
+    mpic_kv_t kv = nullptr;
+    API_BEGIN
+    MPIC_REQUIRE(L && H && D, MPIC_ERR_VALIDATION, "degenerate cache shape");
+    set_device(device);
+    kv = new mpic_kv_s();
+    kv->L = L; kv->T = T; kv->H = H; kv->D = D;
+    kv->dtype = dtype;
+    kv->device = device;
+    const size_t bytes = std::max<size_t>(1, kv->elems()) * esz(dtype);
+    MPIC_CUDA(cudaMalloc(&kv->k, bytes));
+    MPIC_CUDA(cudaMalloc(&kv->v, bytes));
+    *out = kv;
+    kv = nullptr;
+    API_END
+}
+
+int mpic_kv_free(mpic_kv_t kv) {
+    API_BEGIN
+    if (kv) {
+        cudaSetDevice(kv->device);
+        cudaFree(kv->k);
+        cudaFree(kv->v);
+        delete kv;
+    }
+    API_END
+}
+
+int mpic_kv_shape(mpic_kv_t kv, uint32_t* shape4, mpic_dtype* dtype) {
+    API_BEGIN
+    shape4[0] = kv->L; shape4[1] = kv->T; shape4[2] = kv->H; shape4[3] = kv->D;
+    if (dtype) *dtype = kv->dtype;
+    API_END
+}
+
+int mpic_kv_device_ptrs(mpic_kv_t kv, void** k, void** v) {
+    API_BEGIN
+    *k = kv->k;
+    *v = kv->v;
+    API_END
+}
+
+int mpic_kv_upload(mpic_kv_t kv, const float* k, const float* v, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(kv->device));
+    upload_cast(kv->k, kv->dtype, k, kv->elems(), (cudaStream_t)stream);
+    upload_cast(kv->v, kv->dtype, v, kv->elems(), (cudaStream_t)stream);
+    API_END
+}
+
+int mpic_kv_download(mpic_kv_t kv, float* k, float* v, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(kv->device));
+    if (k) download_cast(k, kv->k, kv->dtype, kv->elems(), (cudaStream_t)stream);
+    if (v) download_cast(v, kv->v, kv->dtype, kv->elems(), (cudaStream_t)stream);
+    API_END
+}
+
+int mpic_kv_zero_rows(mpic_kv_t kv, uint32_t row0, uint32_t rows, void* stream) {
+    API_BEGIN
+    MPIC_REQUIRE(row0 + rows <= kv->T, MPIC_ERR_VALIDATION, "rows outside the cache");
+    MPIC_CUDA(cudaSetDevice(kv->device));
+    const size_t row_b = (size_t)kv->H * kv->D * esz(kv->dtype);
+    const size_t plane = (size_t)kv->T * row_b;
+    if (rows) {
+        MPIC_CUDA(cudaMemset2DAsync((char*)kv->k + row0 * row_b, plane, 0, rows * row_b, kv->L, (cudaStream_t)stream));
+        MPIC_CUDA(cudaMemset2DAsync((char*)kv->v + row0 * row_b, plane, 0, rows * row_b, kv->L, (cudaStream_t)stream));
+    }
+    API_END
+}
+
+int mpic_assemble(void* stream, const mpic_chunk_ref* chunks, uint32_t n_chunks, mpic_kv_t dst,
+                  mpic_reposition reposition, float rope_base, int zero_gaps) {
+    API_BEGIN
+    MPIC_REQUIRE(dst, MPIC_ERR_VALIDATION, "null destination cache");
+    MPIC_CUDA(cudaSetDevice(dst->device));
+    std::vector<const void*> ks(n_chunks), vs(n_chunks);
+    std::vector<uint32_t> ts(n_chunks);
+    mpic_dtype st = dst->dtype;
+    for (uint32_t i = 0; i < n_chunks; ++i) {
+        const mpic_kv_t s = chunks[i].src;
+        MPIC_REQUIRE(s, MPIC_ERR_LINK, "null chunk");
+        MPIC_REQUIRE(s->L == dst->L && s->H == dst->H && s->D == dst->D, MPIC_ERR_LINK,
+                     "entry tensor shape does not match model");
+        MPIC_REQUIRE(i == 0 || s->dtype == st, MPIC_ERR_VALIDATION, "mixed chunk dtypes");
+        st = s->dtype;
+        ks[i] = s->k;
+        vs[i] = s->v;
+        ts[i] = s->T;
+    }
+    do_assemble((cudaStream_t)stream, ks.data(), vs.data(), ts.data(), st, chunks, n_chunks, dst,
+                reposition, zero_gaps, rope_base);
+    API_END
+}
+
+int mpic_assemble_raw(void* stream, const void* const* src_k, const void* const* src_v,
+                      const uint32_t* src_tokens, mpic_dtype src_dtype, const mpic_chunk_ref* chunks,
+                      uint32_t n_chunks, mpic_kv_t dst, mpic_reposition reposition, float rope_base,
+                      int zero_gaps) {
+    API_BEGIN
+    MPIC_REQUIRE(dst, MPIC_ERR_VALIDATION, "null destination cache");
+    MPIC_CUDA(cudaSetDevice(dst->device));
+    do_assemble((cudaStream_t)stream, src_k, src_v, src_tokens, src_dtype, chunks, n_chunks, dst,
+                reposition, zero_gaps, rope_base);
+    API_END
+}
+
+int mpic_workspace_create(mpic_model_t md, uint32_t max_rows, uint32_t max_ctx, mpic_workspace_t* out) {
+    mpic_workspace_t ws = nullptr;
+    API_BEGIN
+    MPIC_REQUIRE(md && max_rows > 0, MPIC_ERR_VALIDATION, "bad workspace request");
+    MPIC_CUDA(cudaSetDevice(md->device));
+    ws = new mpic_workspace_s();
+    ws->model = md;
+    ws->max_rows = max_rows;
+    ws->max_ctx = max_ctx;
+    ws->m_pad = (max_rows + 127) / 128 * 128;
+    const size_t h = md->cfg.hidden_dim, mp = ws->m_pad;
+    const size_t e = esz(md->dtype);
+    ws->d_ids = dmalloc<int32_t>(mp);
+    ws->d_rows = dmalloc<uint32_t>(mp);
+    ws->d_pos = dmalloc<uint32_t>(mp);
+    ws->x = dmalloc<float>(mp * h);
+    ws->xb = dmalloc<__nv_bfloat16>(mp * h);
+    MPIC_CUDA(cudaMalloc(&ws->q, mp * h * e));
+    MPIC_CUDA(cudaMalloc(&ws->attn, mp * h * e));
+    MPIC_CUDA(cudaMalloc(&ws->ffn, mp * 4 * h * e));
+    // Padding rows of the GEMM A operands are read (never written back): keep them finite.
+    MPIC_CUDA(cudaMemset(ws->xb, 0, mp * h * 2));
+    MPIC_CUDA(cudaMemset(ws->attn, 0, mp * h * e));
+    MPIC_CUDA(cudaMemset(ws->ffn, 0, mp * 4 * h * e));
+    ws->d_logits = dmalloc<float>(md->cfg.vocab_size);
+    MPIC_CUDA(cudaMallocHost(&ws->h_ids, mp * 4));
+    MPIC_CUDA(cudaMallocHost(&ws->h_rows, mp * 4));
+    MPIC_CUDA(cudaMallocHost(&ws->h_pos, mp * 4));
+    MPIC_CUDA(cudaMallocHost(&ws->h_logits, md->cfg.vocab_size * 4));
+    MPIC_CUDA(cudaStreamCreateWithFlags(&ws->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+        MPIC_CUDA(cudaEventCreateWithFlags(&ws->ev_ready[i], cudaEventDisableTiming));
+        MPIC_CUDA(cudaEventCreateWithFlags(&ws->ev_free[i], cudaEventDisableTiming));
+    }
+    *out = ws;
+    ws = nullptr;
+    API_END
+}
+
+int mpic_workspace_destroy(mpic_workspace_t ws) {
+    API_BEGIN
+    if (ws) {
+        cudaSetDevice(ws->model->device);
+        cudaFree(ws->d_ids); cudaFree(ws->d_rows); cudaFree(ws->d_pos);
+        cudaFree(ws->x); cudaFree(ws->xb); cudaFree(ws->q); cudaFree(ws->attn); cudaFree(ws->ffn);
+        cudaFree(ws->d_logits);
+        cudaFreeHost(ws->h_ids); cudaFreeHost(ws->h_rows); cudaFreeHost(ws->h_pos);
+        cudaFreeHost(ws->h_logits);
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(ws->stage[i]);
+            if (ws->ev_ready[i]) cudaEventDestroy(ws->ev_ready[i]);
+            if (ws->ev_free[i]) cudaEventDestroy(ws->ev_free[i]);
+        }
+        if (ws->copy_stream) cudaStreamDestroy(ws->copy_stream);
+        delete ws;
+    }
+    API_END
+}
+
+int mpic_selective_prefill(mpic_model_t model, mpic_workspace_t ws, const int32_t* ids,
+                           const uint32_t* rows, uint32_t m, mpic_kv_t kv, float* logits, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(model->device));
+    // selective_core rotates each row at its own global index (linker.cpp:67-70).
+    forward_host(model, ws, ids, rows, rows, m, kv, logits, (cudaStream_t)stream);
+    API_END
+}
+
+int mpic_prefill_extend(mpic_model_t model, mpic_workspace_t ws, const int32_t* ids, uint32_t m,
+                        uint32_t start, uint32_t position_base, mpic_kv_t kv, float* logits, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(model->device));
+    MPIC_REQUIRE(start + m <= kv->T, MPIC_ERR_VALIDATION, "cache too short for the new rows");
+    std::vector<uint32_t> rows(m), pos(m);
+    for (uint32_t i = 0; i < m; ++i) {  // model.cpp:253
+        rows[i] = start + i;
+        pos[i] = position_base + start + i;
+    }
+    forward_host(model, ws, ids, rows.data(), pos.data(), m, kv, logits, (cudaStream_t)stream);
+    API_END
+}
+
+int mpic_forward_rows_async(mpic_model_t model, mpic_workspace_t ws, const int32_t* d_ids,
+                            const uint32_t* d_rows, const uint32_t* d_rope_pos, uint32_t m,
+                            uint32_t max_pos, mpic_kv_t kv, float* d_logits, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(model->device));
+    forward_rows(model, ws, d_ids, d_rows, d_rope_pos, m, max_pos, kv, d_logits, (cudaStream_t)stream);
+    API_END
+}
+
+
+int mpic_image_token_ids(const mpic_model_config* cfg, const uint8_t* hash32, uint32_t count,
+                         int32_t* out) {
+    API_BEGIN
+    validate_cfg(cfg);
+    image_ids(cfg, hash32, count, out);
+    API_END
+}
+
+int mpic_select_tokens(const mpic_prompt* prompt, const mpic_policy* policy, uint32_t* out,
+                       uint32_t* m) {
+    API_BEGIN
+    *m = select_rows(prompt, policy, out);
+    API_END
+}
+
+int mpic_flatten_ids(const mpic_model_config* cfg, const mpic_prompt* prompt, int32_t* out) {
+    API_BEGIN
+    prompt_tokens(prompt);
+    flatten(cfg, prompt, out);
+    API_END
+}
+
+int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
+                         const mpic_policy* policy, const mpic_kv_t* chunks,
+                         mpic_reposition reposition, const uint32_t* position_bases,
+                         mpic_kv_t linked, float* logits, uint32_t* selected, uint32_t* m_out,
+                         void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(model->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const RequestPlan r = plan_request(model, prompt, policy, position_bases);
+    check_linked(model, linked, r.n);
+    const uint32_t n_img = (uint32_t)r.refs.size();
+    std::vector<const void*> ks(n_img), vs(n_img);
+    std::vector<uint32_t> ts(n_img);
+    for (uint32_t i = 0; i < n_img; ++i) {
+        const mpic_kv_t c = chunks[i];
+        MPIC_REQUIRE(c, MPIC_ERR_LINK, "no fetched entry for image segment");
+        MPIC_REQUIRE(c->T == r.refs[i].rows, MPIC_ERR_LINK, "token_count mismatch for image segment");
+        MPIC_REQUIRE(c->L == linked->L && c->H == linked->H && c->D == linked->D, MPIC_ERR_LINK,
+                     "entry tensor shape does not match model");
+        MPIC_REQUIRE(c->dtype == chunks[0]->dtype, MPIC_ERR_VALIDATION, "mixed chunk dtypes");
+        ks[i] = c->k;
+        vs[i] = c->v;
+        ts[i] = c->T;
+    }
+    do_assemble(s, ks.data(), vs.data(), ts.data(), n_img ? chunks[0]->dtype : model->dtype,
+                r.refs.data(), n_img, linked, reposition, 1, model->cfg.rope_base);
+    run_request(model, ws, r, linked, logits, selected, m_out, s, {});
+    API_END
+}
+
+int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
+                              const mpic_policy* policy, const float* const* chunk_k,
+                              const float* const* chunk_v, const uint32_t* position_bases,
+                              mpic_reposition reposition, mpic_kv_t linked, float* logits,
+                              uint32_t* selected, uint32_t* m_out, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(model->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const RequestPlan r = plan_request(model, prompt, policy, position_bases);
+    check_linked(model, linked, r.n);
+    const uint32_t n_img = (uint32_t)r.refs.size();
+    const size_t h = model->cfg.hidden_dim;
+    // Staging slot = one layer of every chunk, fp32, K then V.
+    std::vector<size_t> off(n_img);
+    size_t img_rows = 0;
+    for (uint32_t i = 0; i < n_img; ++i) {
+        off[i] = img_rows * h;
+        img_rows += r.refs[i].rows;
+    }
+    const size_t slot_bytes = std::max<size_t>(1, img_rows) * h * 4 * 2;
+    if (ws->stage_cap < slot_bytes) {
+        MPIC_CUDA(cudaStreamSynchronize(ws->copy_stream));
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(ws->stage[i]);
+            ws->stage[i] = nullptr;
+            MPIC_CUDA(cudaMalloc(&ws->stage[i], slot_bytes));
+        }
+        ws->stage_cap = slot_bytes;
+    }
+    // Per-slot placement plans (source pointers differ by slot; L = 1 per launch).
+    std::vector<uint32_t> ts(n_img);
+    for (uint32_t i = 0; i < n_img; ++i) ts[i] = r.refs[i].rows;
+    const AsmChunk* dc[2];
+    const float2* dt[2];
+    void* bufs[2];
+    uint32_t n_tab = 0;
+    for (int sl = 0; sl < 2; ++sl) {
+        std::vector<const void*> ks(n_img), vs(n_img);
+        float* base = static_cast<float*>(ws->stage[sl]);
+        for (uint32_t i = 0; i < n_img; ++i) {
+            ks[i] = base + off[i];
+            vs[i] = base + img_rows * h + off[i];
+        }
+        const AsmPlan p = plan_assembly(ks.data(), vs.data(), ts.data(), r.refs.data(), n_img,
+                                        linked->T, linked->D, reposition, model->cfg.rope_base);
+        n_tab = p.n_tables;
+        bufs[sl] = upload_plan(p, s, &dc[sl], &dt[sl]);
+    }
+    const size_t e = esz(linked->dtype);
+    const size_t plane = (size_t)linked->T * h * e;
+    cudaStream_t cs = ws->copy_stream;
+    // The copy lane may not start before the plans (and any earlier user of the ring)
+    // are done on the compute stream.
+    MPIC_CUDA(cudaEventRecord(ws->ev_free[0], s));
+    MPIC_CUDA(cudaEventRecord(ws->ev_free[1], s));
+    auto issue_copy = [&](uint32_t l) {
+        const int sl = l & 1;
+        float* base = static_cast<float*>(ws->stage[sl]);
+        MPIC_CUDA(cudaStreamWaitEvent(cs, ws->ev_free[sl], 0));
+        for (uint32_t i = 0; i < n_img; ++i) {
+            const size_t cnt = (size_t)r.refs[i].rows * h;
+            MPIC_CUDA(cudaMemcpyAsync(base + off[i], chunk_k[i] + (size_t)l * cnt, cnt * 4,
+                                      cudaMemcpyHostToDevice, cs));
+            MPIC_CUDA(cudaMemcpyAsync(base + img_rows * h + off[i], chunk_v[i] + (size_t)l * cnt,
+                                      cnt * 4, cudaMemcpyHostToDevice, cs));
+        }
+        MPIC_CUDA(cudaEventRecord(ws->ev_ready[sl], cs));
+    };
+    const uint32_t L = model->cfg.n_layers;
+    issue_copy(0);
+    auto before_layer = [&](uint32_t l) {
+        if (l + 1 < L) issue_copy(l + 1);  // waits for layer l-1's assembly to free the slot
+        const int sl = l & 1;
+        MPIC_CUDA(cudaStreamWaitEvent(s, ws->ev_ready[sl], 0));
+        launch_assemble(dc[sl], n_img, dt[sl], n_tab, MPIC_F32, (char*)linked->k + l * plane,
+                        (char*)linked->v + l * plane, linked->dtype, 1, linked->T, linked->H,
+                        linked->D, 1, s);
+        MPIC_CUDA(cudaEventRecord(ws->ev_free[sl], s));
+    };
+    run_request(model, ws, r, linked, logits, selected, m_out, s, before_layer);
+    for (int sl = 0; sl < 2; ++sl) MPIC_CUDA(cudaFreeAsync(bufs[sl], s));
+    API_END
+}
+
+int mpic_test_gemm(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uint32_t K,
+                   int path, float* d_out, void* stream) {
+    API_BEGIN
+    EpiParams ep;
+    ep.mode = EPI_STORE_F32;
+    ep.out = d_out;
+    ep.ldo = N;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (path == 1) {
+        MPIC_REQUIRE(tc_gemm_supported(M, N, K), MPIC_ERR_VALIDATION, "shape not supported by the tcgen05 gemm");
+        launch_gemm_tc(static_cast<const __nv_bfloat16*>(d_a), K, static_cast<const __nv_bfloat16*>(d_w), M, N, K, ep, s);
+    } else {
+        launch_gemm_simt(d_a, MPIC_BF16, K, d_w, MPIC_BF16, M, N, K, ep, MPIC_BF16, s);
+    }
+    API_END
+}
+
+int mpic_host_alloc(size_t bytes, void** out) {
+    API_BEGIN
+    MPIC_CUDA(cudaMallocHost(out, bytes));
+    API_END
+}
+
+int mpic_host_free(void* p) {
+    API_BEGIN
+    MPIC_CUDA(cudaFreeHost(p));
+    API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+// Internal kernel launchers of the MPIC B200 library (not part of the C ABI).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mpic_b200.h"
+
+namespace mpicb {
+
+enum EpiMode : int { EPI_STORE = 0, EPI_QKV = 1, EPI_RESID = 2, EPI_GELU = 3, EPI_STORE_F32 = 4 };
+
+// Fused GEMM epilogue description (shared by the SIMT and tcgen05 GEMMs).
+struct EpiParams {
+    int mode = EPI_STORE;
+    // EPI_QKV: columns [0,h) -> q (rotated), [h,2h) -> kv_k[kv_rows[r]] (rotated),
+    // [2h,3h) -> kv_v[kv_rows[r]]. kv_k/kv_v point at the layer's plane.
+    void* q = nullptr;
+    void* kv_k = nullptr;
+    void* kv_v = nullptr;
+    const uint32_t* kv_rows = nullptr;
+    const uint32_t* rope_pos = nullptr;
+    const float2* rope = nullptr;  // [pos][head_dim/2] (cos, sin)
+    uint32_t hidden = 0;
+    uint32_t head_dim = 0;
+    // EPI_RESID: x[row][col] += acc (atomic when split_k > 1)
+    float* x = nullptr;
+    uint32_t ldx = 0;
+    uint32_t split_k = 1;
+    // EPI_STORE / EPI_GELU
+    void* out = nullptr;
+    uint32_t ldo = 0;
+};
+
+// One chunk placement for the assembly kernel (device-side descriptor).
+struct AsmChunk {
+    const void* src_k;
+    const void* src_v;
+    uint32_t src_tokens;  // T of the source planes
+    uint32_t src_row0;
+    uint32_t dst_row0;
+    uint32_t rows;
+    uint32_t table;  // index of this chunk's (cos,sin) table in the rerotate tables
+    uint32_t rotate; // 1 when this chunk's K rows are rotated
+};
+
+void launch_embed(const float* emb, const int32_t* ids, uint32_t m, uint32_t h, float* x,
+                  __nv_bfloat16* xb, cudaStream_t s);
+void launch_rope_table(const double* inv_freq, uint32_t half_d, uint32_t p0, uint32_t p1,
+                       float2* tab, cudaStream_t s);
+void launch_gemm_simt(const void* A, mpic_dtype a_t, uint32_t lda, const void* W, mpic_dtype w_t,
+                      uint32_t M, uint32_t N, uint32_t K, const EpiParams& ep, mpic_dtype o_t,
+                      cudaStream_t s);
+void launch_attn_simt(const void* q, const void* k, const void* v, mpic_dtype dt,
+                      const uint32_t* rows, uint32_t m, uint32_t H, uint32_t D, void* out,
+                      cudaStream_t s);
+void launch_lm_head(const float* x_last, const void* W, mpic_dtype w_t, uint32_t V, uint32_t h,
+                    float* logits, cudaStream_t s);
+void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, size_t n, cudaStream_t s);
+void launch_bf16_to_f32(const __nv_bfloat16* in, float* out, size_t n, cudaStream_t s);
+void launch_x_to_bf16(const float* x, __nv_bfloat16* xb, uint32_t m, uint32_t h, cudaStream_t s);
+
+// Weight synthesis (model.cpp:28-36): dst[i] = counter_uniform(seed, (tag<<32)|layer, i)*scale
+void launch_synth(uint64_t seed, uint64_t tag, uint32_t layer, size_t count, float scale,
+                  void* dst, mpic_dtype dt, cudaStream_t s);
+
+// Chunk gather + optional K rerotation + dtype cast + gap zero-fill (linker.cpp:260-314).
+void launch_assemble(const AsmChunk* d_chunks, uint32_t n_chunks, const float2* d_tables,
+                     uint32_t n_tables, mpic_dtype src_t, void* dst_k, void* dst_v,
+                     mpic_dtype dst_t, uint32_t L, uint32_t T_dst, uint32_t H, uint32_t D,
+                     int zero_gaps, cudaStream_t s);
+
+// tcgen05 / TMA kernels (tc_gemm.cu, tc_attn.cu)
+struct TcGemmPlan;
+bool tc_gemm_supported(uint32_t M, uint32_t N, uint32_t K);
+void launch_gemm_tc(const __nv_bfloat16* A, uint32_t lda, const __nv_bfloat16* W, uint32_t M,
+                    uint32_t N, uint32_t K, const EpiParams& ep, cudaStream_t s);
+
+} // namespace mpicb

@@ -1,0 +1,334 @@
+// Non-tensor-core kernels of the selective recompute: embedding gather, RoPE table,
+// the fp32 parity-mode GEMM (SIMT FFMA; TF32 would miss the 1e-4 bar), selective
+// causal attention (fp32 accumulation, online softmax), lm_head GEMV and dtype casts.
+// The bf16 production path uses these only for the small non-GEMM steps; its GEMMs and
+// attention are the tcgen05 kernels in tc_gemm.cu / tc_attn.cu.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mpicb {
+
+// ---- embedding gather (proj/src/model.cpp:89-99) -----------------------------------
+__global__ void embed_kernel(const float* __restrict__ emb, const int32_t* __restrict__ ids,
+                             uint32_t m, uint32_t h, float* __restrict__ x,
+                             __nv_bfloat16* __restrict__ xb, uint32_t ld) {
+    const uint32_t i = blockIdx.x;
+    if (i >= m) return;
+    const float* src = emb + (size_t)ids[i] * h;
+    for (uint32_t c = threadIdx.x; c < h; c += blockDim.x) {
+        const float v = src[c];
+        x[(size_t)i * ld + c] = v;
+        if (xb) xb[(size_t)i * ld + c] = __float2bfloat16_rn(v);
+    }
+}
+
+void launch_embed(const float* emb, const int32_t* ids, uint32_t m, uint32_t h, float* x,
+                  __nv_bfloat16* xb, cudaStream_t s) {
+    embed_kernel<<<m, 256, 0, s>>>(emb, ids, m, h, x, xb, h);
+    MPIC_LAUNCHED();
+}
+
+// ---- RoPE cos/sin table: tab[p][i] = (float)cos/sin(p * inv_freq[i]) -----------------
+// inv_freq[i] = pow(base, -(2i)/D) is computed on the host in double exactly as
+// proj/src/model.cpp:51-53; the product and cos/sin are evaluated here in double.
+__global__ void rope_table_kernel(const double* __restrict__ inv_freq, uint32_t half_d,
+                                  uint32_t p0, uint32_t p1, float2* __restrict__ tab) {
+    const uint64_t total = (uint64_t)(p1 - p0) * half_d;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = p0 + (uint32_t)(e / half_d);
+        const uint32_t i = (uint32_t)(e % half_d);
+        const double theta = (double)p * inv_freq[i];
+        double sn, cs;
+        sincos(theta, &sn, &cs);
+        tab[(size_t)p * half_d + i] = make_float2((float)cs, (float)sn);
+    }
+}
+
+void launch_rope_table(const double* inv_freq, uint32_t half_d, uint32_t p0, uint32_t p1,
+                       float2* tab, cudaStream_t s) {
+    if (p1 <= p0) return;
+    rope_table_kernel<<<kNumSMs * 4, 256, 0, s>>>(inv_freq, half_d, p0, p1, tab);
+    MPIC_LAUNCHED();
+}
+
+// ---- epilogues shared by the SIMT and tcgen05 GEMMs ---------------------------------
+// Handles the adjacent column pair (col, col+1) of output row `row` (< m).
+template <typename TO>
+__device__ __forceinline__ void epi_pair(const EpiParams& ep, uint32_t row, uint32_t col, float v0,
+                                         float v1) {
+    switch (ep.mode) {
+        case EPI_QKV: {
+            // linker.cpp:64-78: q,k rotated at rope_pos[row]; k,v scattered to kv[rows[row]].
+            const uint32_t h = ep.hidden;
+            const uint32_t part = col / h, c = col - part * h;
+            if (part < 2) {
+                const uint32_t i = (c % ep.head_dim) >> 1;
+                const float2 cs = ep.rope[(size_t)ep.rope_pos[row] * (ep.head_dim >> 1) + i];
+                rope_pair(v0, v1, cs.x, cs.y);
+            }
+            TO* dst;
+            if (part == 0) dst = static_cast<TO*>(ep.q) + (size_t)row * h + c;
+            else dst = static_cast<TO*>(part == 1 ? ep.kv_k : ep.kv_v) + (size_t)ep.kv_rows[row] * h + c;
+            dst[0] = from_f32<TO>(v0);
+            dst[1] = from_f32<TO>(v1);
+            break;
+        }
+        case EPI_RESID: {  // x += proj (linker.cpp:115-118, 124-128)
+            float* x = ep.x + (size_t)row * ep.ldx + col;
+            if (ep.split_k > 1) {
+                atomicAdd(x, v0);
+                atomicAdd(x + 1, v1);
+            } else {
+                x[0] += v0;
+                x[1] += v1;
+            }
+            break;
+        }
+        case EPI_GELU: {  // ffn = gelu(x W1^T) (linker.cpp:119-123)
+            TO* o = static_cast<TO*>(ep.out) + (size_t)row * ep.ldo + col;
+            o[0] = from_f32<TO>(gelu_ref(v0));
+            o[1] = from_f32<TO>(gelu_ref(v1));
+            break;
+        }
+        case EPI_STORE_F32: {
+            float* o = static_cast<float*>(ep.out) + (size_t)row * ep.ldo + col;
+            o[0] = v0;
+            o[1] = v1;
+            break;
+        }
+        default: {
+            TO* o = static_cast<TO*>(ep.out) + (size_t)row * ep.ldo + col;
+            o[0] = from_f32<TO>(v0);
+            o[1] = from_f32<TO>(v1);
+        }
+    }
+}
+
+// ---- fp32 SIMT GEMM: C[m x N] = A[m x K] . W[N x K]^T, fused epilogue ---------------
+constexpr int SB_M = 64, SB_N = 64, SB_K = 16;
+
+template <typename TA, typename TW, typename TO>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const TA* __restrict__ A, uint32_t lda,
+                                                        const TW* __restrict__ W, uint32_t M,
+                                                        uint32_t N, uint32_t K, EpiParams ep) {
+    __shared__ float As[SB_K][SB_M + 4];
+    __shared__ float Ws[SB_K][SB_N + 4];
+    const uint32_t tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+    const uint32_t m0 = blockIdx.y * SB_M, n0 = blockIdx.x * SB_N;
+    float acc[4][4] = {};
+    for (uint32_t k0 = 0; k0 < K; k0 += SB_K) {
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+            const uint32_t idx = tid + 256 * it, r = idx / SB_K, c = idx % SB_K;
+            const uint32_t gm = m0 + r, gn = n0 + r, gk = k0 + c;
+            As[c][r] = (gm < M && gk < K) ? to_f32<TA>(A[(size_t)gm * lda + gk]) : 0.0f;
+            Ws[c][r] = (gn < N && gk < K) ? to_f32<TW>(W[(size_t)gn * K + gk]) : 0.0f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < SB_K; ++kk) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                a[i] = As[kk][ty * 4 + i];
+                b[i] = Ws[kk][tx * 4 + i];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t row = m0 + ty * 4 + i;
+        if (row >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; j += 2) {
+            const uint32_t col = n0 + tx * 4 + j;
+            if (col < N) epi_pair<TO>(ep, row, col, acc[i][j], acc[i][j + 1]);
+        }
+    }
+}
+
+void launch_gemm_simt(const void* A, mpic_dtype a_t, uint32_t lda, const void* W, mpic_dtype w_t,
+                      uint32_t M, uint32_t N, uint32_t K, const EpiParams& ep, mpic_dtype o_t,
+                      cudaStream_t s) {
+    dim3 grid(ceil_div(N, SB_N), ceil_div(M, SB_M));
+#define GEMM_CASE(TA, TW, TO) \
+    gemm_simt_kernel<TA, TW, TO><<<grid, 256, 0, s>>>((const TA*)A, lda, (const TW*)W, M, N, K, ep)
+    if (a_t == MPIC_F32 && w_t == MPIC_F32 && o_t == MPIC_F32) GEMM_CASE(float, float, float);
+    else if (a_t == MPIC_F32 && w_t == MPIC_BF16 && o_t == MPIC_BF16) GEMM_CASE(float, __nv_bfloat16, __nv_bfloat16);
+    else if (a_t == MPIC_BF16 && w_t == MPIC_BF16 && o_t == MPIC_BF16) GEMM_CASE(__nv_bfloat16, __nv_bfloat16, __nv_bfloat16);
+    else throw Error(MPIC_ERR_VALIDATION, "unsupported simt gemm dtype combination");
+#undef GEMM_CASE
+    MPIC_LAUNCHED();
+}
+
+// ---- selective causal attention (linker.cpp:80-113), online softmax -----------------
+// One CTA per (recomputed row, head). Row i attends over cache rows [0, rows[i]].
+constexpr int AT_CH = 256;
+
+template <typename TQ, typename TKV, typename TO>
+__global__ void __launch_bounds__(128) attn_simt_kernel(const TQ* __restrict__ q,
+                                                        const TKV* __restrict__ kk,
+                                                        const TKV* __restrict__ vv,
+                                                        const uint32_t* __restrict__ rows,
+                                                        uint32_t h, uint32_t D, float inv_sqrt_d,
+                                                        TO* __restrict__ out) {
+    __shared__ float qs[256];
+    __shared__ float sc[AT_CH];
+    __shared__ float red[8];
+    const uint32_t i = blockIdx.x, head = blockIdx.y, tid = threadIdx.x;
+    const uint32_t lane = tid & 31, warp = tid >> 5;
+    const uint32_t count = rows[i] + 1;
+    const size_t hoff = (size_t)head * D;
+    for (uint32_t d = tid; d < D; d += 128) qs[d] = to_f32<TQ>(q[(size_t)i * h + hoff + d]);
+    __syncthreads();
+    float run_max = -INFINITY, run_sum = 0.0f, acc0 = 0.0f, acc1 = 0.0f;
+    for (uint32_t c0 = 0; c0 < count; c0 += AT_CH) {
+        const uint32_t nk = min((uint32_t)AT_CH, count - c0);
+        for (uint32_t j = warp; j < nk; j += 4) {
+            const TKV* kr = kk + (size_t)(c0 + j) * h + hoff;
+            float dot = 0.0f;
+            for (uint32_t d = lane; d < D; d += 32) dot = fmaf(qs[d], to_f32<TKV>(kr[d]), dot);
+            dot = warp_sum(dot);
+            if (lane == 0) sc[j] = dot * inv_sqrt_d;
+        }
+        __syncthreads();
+        float mx = -INFINITY;
+        for (uint32_t j = tid; j < nk; j += 128) mx = fmaxf(mx, sc[j]);
+        mx = warp_max(mx);
+        if (lane == 0) red[warp] = mx;
+        __syncthreads();
+        mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+        const float new_max = fmaxf(run_max, mx);
+        const float alpha = expf(run_max - new_max);
+        float ls = 0.0f;
+        for (uint32_t j = tid; j < nk; j += 128) {
+            const float p = expf(sc[j] - new_max);
+            sc[j] = p;
+            ls += p;
+        }
+        ls = warp_sum(ls);
+        __syncthreads();  // red[] reads above complete before reuse
+        if (lane == 0) red[4 + warp] = ls;
+        __syncthreads();
+        run_sum = run_sum * alpha + (red[4] + red[5] + red[6] + red[7]);
+        run_max = new_max;
+        const TKV* vb = vv + (size_t)c0 * h + hoff;
+        if (tid < D) {
+            float a = 0.0f;
+            for (uint32_t j = 0; j < nk; ++j) a = fmaf(sc[j], to_f32<TKV>(vb[(size_t)j * h + tid]), a);
+            acc0 = acc0 * alpha + a;
+        }
+        if (tid + 128 < D) {
+            float a = 0.0f;
+            for (uint32_t j = 0; j < nk; ++j) a = fmaf(sc[j], to_f32<TKV>(vb[(size_t)j * h + tid + 128]), a);
+            acc1 = acc1 * alpha + a;
+        }
+        __syncthreads();
+    }
+    const float inv = 1.0f / run_sum;
+    if (tid < D) out[(size_t)i * h + hoff + tid] = from_f32<TO>(acc0 * inv);
+    if (tid + 128 < D) out[(size_t)i * h + hoff + tid + 128] = from_f32<TO>(acc1 * inv);
+}
+
+void launch_attn_simt(const void* q, const void* k, const void* v, mpic_dtype dt,
+                      const uint32_t* rows, uint32_t m, uint32_t H, uint32_t D, void* out,
+                      cudaStream_t s) {
+    const uint32_t h = H * D;
+    const float inv_sqrt_d = 1.0f / sqrtf((float)D);
+    dim3 grid(m, H);
+    if (dt == MPIC_F32)
+        attn_simt_kernel<float, float, float><<<grid, 128, 0, s>>>(
+            (const float*)q, (const float*)k, (const float*)v, rows, h, D, inv_sqrt_d, (float*)out);
+    else
+        attn_simt_kernel<__nv_bfloat16, __nv_bfloat16, __nv_bfloat16><<<grid, 128, 0, s>>>(
+            (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, rows, h, D,
+            inv_sqrt_d, (__nv_bfloat16*)out);
+    MPIC_LAUNCHED();
+}
+
+// ---- lm_head GEMV on the last recomputed row (linker.cpp:131-133) -------------------
+template <typename TW>
+__global__ void __launch_bounds__(256) lm_head_kernel(const float* __restrict__ x,
+                                                      const TW* __restrict__ W, uint32_t V,
+                                                      uint32_t h, float* __restrict__ logits) {
+    extern __shared__ float xs[];
+    for (uint32_t c = threadIdx.x; c < h; c += blockDim.x) xs[c] = x[c];
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warps = blockDim.x >> 5;
+    for (uint32_t r = blockIdx.x * warps + (threadIdx.x >> 5); r < V; r += gridDim.x * warps) {
+        const TW* w = W + (size_t)r * h;
+        float acc = 0.0f;
+        if constexpr (sizeof(TW) == 2) {
+            // 8 bf16 per 16-byte load
+            for (uint32_t c = lane * 8; c + 8 <= h; c += 256) {
+                const uint4 raw = *reinterpret_cast<const uint4*>(w + c);
+                const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(p2[e]);
+                    acc = fmaf(xs[c + 2 * e], f.x, acc);
+                    acc = fmaf(xs[c + 2 * e + 1], f.y, acc);
+                }
+            }
+            for (uint32_t c = (h / 8) * 8 + lane; c < h; c += 32) acc = fmaf(xs[c], to_f32<TW>(w[c]), acc);
+        } else {
+            for (uint32_t c = lane; c < h; c += 32) acc = fmaf(xs[c], to_f32<TW>(w[c]), acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) logits[r] = acc;
+    }
+}
+
+void launch_lm_head(const float* x_last, const void* W, mpic_dtype w_t, uint32_t V, uint32_t h,
+                    float* logits, cudaStream_t s) {
+    const uint32_t blocks = std::min<uint32_t>(ceil_div(V, 8), kNumSMs * 8);
+    const size_t smem = (size_t)h * sizeof(float);
+    if (w_t == MPIC_F32) {
+        if (smem > 48 * 1024)
+            MPIC_CUDA(cudaFuncSetAttribute(lm_head_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        lm_head_kernel<float><<<blocks, 256, smem, s>>>(x_last, (const float*)W, V, h, logits);
+    } else {
+        if (smem > 48 * 1024)
+            MPIC_CUDA(cudaFuncSetAttribute(lm_head_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        lm_head_kernel<__nv_bfloat16><<<blocks, 256, smem, s>>>(x_last, (const __nv_bfloat16*)W, V, h, logits);
+    }
+    MPIC_LAUNCHED();
+}
+
+// ---- dtype casts --------------------------------------------------------------------
+__global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                   size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        out[i] = __float2bfloat16_rn(in[i]);
+}
+__global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ in, float* __restrict__ out,
+                                   size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        out[i] = __bfloat162float(in[i]);
+}
+void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, size_t n, cudaStream_t s) {
+    if (!n) return;
+    f32_to_bf16_kernel<<<kNumSMs * 8, 256, 0, s>>>(in, out, n);
+    MPIC_LAUNCHED();
+}
+void launch_bf16_to_f32(const __nv_bfloat16* in, float* out, size_t n, cudaStream_t s) {
+    if (!n) return;
+    bf16_to_f32_kernel<<<kNumSMs * 8, 256, 0, s>>>(in, out, n);
+    MPIC_LAUNCHED();
+}
+
+// x (fp32 residual stream, m rows, ld h) -> bf16 A operand for the next GEMM.
+void launch_x_to_bf16(const float* x, __nv_bfloat16* xb, uint32_t m, uint32_t h, cudaStream_t s) {
+    launch_f32_to_bf16(x, xb, (size_t)m * h, s);
+}
+
+} // namespace mpicb

@@ -1,0 +1,246 @@
+"""GPU parity of the B200 path against the reference (golden fixtures generated from the
+unmodified reference build, and the plain-C oracle). All calls go through the C ABI.
+
+Tolerances: integer/byte outputs (weights, assembly copies, rerotation, selection)
+bit-exact; fp32 mode max-abs 1e-5 (the reference tests' own bar, test_linker.cpp:437-439)
+and max relative 1e-4 (north star); bf16 mode max relative 1e-2 (north star)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2502_01960_b200 as mp
+from helpers import rel_err
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TAGS = {"k2": (0, 2, False), "k0": (0, 0, False), "text": (1, 0, False), "all": (2, 0, False),
+        "g7": (0, 7, True)}
+
+
+def tiny_cfg():
+    return mp.config(3, 2, 8, vocab_size=101, image_token_count=8, seed=7)
+
+
+def bf16_round(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16).float().numpy()
+
+
+@pytest.fixture(scope="module")
+def g():
+    return dict(np.load(os.path.join(GOLD, "tiny.npz")))
+
+
+@pytest.fixture(scope="module")
+def models():
+    return {mp.F32: mp.Model(tiny_cfg(), mp.F32), mp.BF16: mp.Model(tiny_cfg(), mp.BF16)}
+
+
+def case(g, ci):
+    name = f"tiny.c{ci}"
+    p = mp.Prompt(g[f"{name}.kinds"], g[f"{name}.lens"], g[f"{name}.text_ids"], g[f"{name}.hashes"])
+    asm_k, asm_v = g[f"{name}.as.asm_k"], g[f"{name}.as.asm_v"]
+    bounds, at = [], 0
+    for ln in p.lens:
+        bounds.append((at, at + int(ln)))
+        at += int(ln)
+    chunks = []
+    for (s, e), kind in zip(bounds, p.kinds):
+        if kind == 1:
+            chunks.append((np.ascontiguousarray(asm_k[:, s:e]), np.ascontiguousarray(asm_v[:, s:e]), s))
+    return name, p, chunks, [int(b) for b in g[f"{name}.chunk_base"]]
+
+
+def device_chunks(chunks, dtype):
+    return [mp.KV.from_host(k, v, 2, 8, dtype) for k, v, _ in chunks]
+
+
+def assemble_dev(p, chunks, bases, dtype, rr):
+    kvs = device_chunks(chunks, dtype)
+    dst = mp.KV(3, p.n, 2, 8, dtype)
+    refs = [(kv, 0, s, k.shape[1], b) for kv, (k, v, s), b in zip(kvs, chunks, bases)]
+    mp.assemble(refs, dst, mp.REROTATE if rr else mp.AS_STORED, 10000.0)
+    torch.cuda.synchronize()
+    return dst, kvs
+
+
+def test_weight_synthesis_bit_exact(g, models):
+    m = models[mp.F32]
+    for w in range(8):
+        assert np.array_equal(m.weight(w, 0), g[f"tiny.w{w}.l0"]), w
+    assert np.array_equal(m.weight(7, 2), g["tiny.w7.l2"])
+    mb = models[mp.BF16]
+    for w in range(1, 8):  # embedding stays fp32 (gathered, never multiplied)
+        assert np.array_equal(mb.weight(w, 0), bf16_round(g[f"tiny.w{w}.l0"])), w
+
+
+def test_weight_synthesis_bit_exact_wide():
+    cfg = oracle.Config(2, 8, 64, 512, 4096, 96, 10000.0, 1)
+    om = oracle.OracleC().model(cfg)
+    m = mp.Model(mp.config(2, 8, 64, vocab_size=4096, image_token_count=96, seed=1), mp.F32)
+    for w in range(8):
+        for layer in ([0] if w < 2 else [0, 1]):
+            assert np.array_equal(m.weight(w, layer), om.weight(w, layer)), (w, layer)
+
+
+@pytest.mark.parametrize("ci", range(5))
+@pytest.mark.parametrize("rr", [False, True])
+def test_assembly_bit_exact(g, ci, rr):
+    name, p, chunks, bases = case(g, ci)
+    dst, _ = assemble_dev(p, chunks, bases, mp.F32, rr)
+    k, v = dst.download()
+    key = f"{name}.{'rr' if rr else 'as'}"
+    assert np.array_equal(k, g[f"{key}.asm_k"])
+    assert np.array_equal(v, g[f"{key}.asm_v"])
+
+
+@pytest.mark.parametrize("ci", [0, 2])
+def test_assembly_bf16(g, ci):
+    name, p, chunks, bases = case(g, ci)
+    dst, _ = assemble_dev(p, chunks, bases, mp.BF16, False)
+    k, v = dst.download()
+    assert np.array_equal(k, bf16_round(g[f"{name}.as.asm_k"]))
+    assert np.array_equal(v, bf16_round(g[f"{name}.as.asm_v"]))
+    dst, _ = assemble_dev(p, chunks, bases, mp.BF16, True)
+    k, _ = dst.download()
+    assert rel_err(k, g[f"{name}.rr.asm_k"]) < 1e-2
+
+
+@pytest.mark.parametrize("ci", range(5))
+@pytest.mark.parametrize("rr", [False, True])
+def test_selective_prefill_fp32(g, models, ci, rr):
+    name, p, chunks, bases = case(g, ci)
+    m = models[mp.F32]
+    ws = mp.Workspace(m, 64)
+    flat = g[f"{name}.flat"]
+    key = f"{name}.{'rr' if rr else 'as'}"
+    for tag in TAGS:
+        if f"{key}.{tag}.logits" not in g:
+            continue
+        sel = g[f"{name}.sel.{tag}"]
+        dst, _ = assemble_dev(p, chunks, bases, mp.F32, rr)
+        logits = mp.selective_prefill(m, ws, flat[sel], sel, dst)
+        k, v = dst.download()
+        ref_l, ref_k, ref_v = g[f"{key}.{tag}.logits"], g[f"{key}.{tag}.k"], g[f"{key}.{tag}.v"]
+        assert np.abs(logits - ref_l).max() < 1e-5, tag
+        assert np.abs(k - ref_k).max() < 1e-5 and np.abs(v - ref_v).max() < 1e-5, tag
+        assert rel_err(logits, ref_l) < 1e-4
+
+
+@pytest.mark.parametrize("ci", [0, 2, 3])
+def test_selective_prefill_bf16(g, models, ci):
+    name, p, chunks, bases = case(g, ci)
+    m = models[mp.BF16]
+    ws = mp.Workspace(m, 64)
+    flat = g[f"{name}.flat"]
+    for tag in ["k2", "all"]:
+        sel = g[f"{name}.sel.{tag}"]
+        dst, _ = assemble_dev(p, chunks, bases, mp.BF16, False)
+        logits = mp.selective_prefill(m, ws, flat[sel], sel, dst)
+        assert rel_err(logits, g[f"{name}.as.{tag}.logits"]) < 1e-2, tag
+
+
+def test_prefill_extend_golden(g, models):
+    m = models[mp.F32]
+    ws = mp.Workspace(m, 64)
+    ids = g["tiny.prefill.ids"]
+    kv = mp.KV(3, len(ids), 2, 8, mp.F32)
+    logits = mp.prefill_extend(m, ws, ids, 0, 3, kv)
+    k, v = kv.download()
+    assert np.abs(logits - g["tiny.prefill.logits"]).max() < 1e-5
+    assert np.abs(k - g["tiny.prefill.k"]).max() < 1e-5
+    assert np.abs(v - g["tiny.prefill.v"]).max() < 1e-5
+
+
+@pytest.mark.parametrize("ci", [0, 2, 3])
+@pytest.mark.parametrize("host", [False, True])
+def test_request_prefill_end_to_end(g, models, ci, host):
+    """select_tokens -> assemble -> selective_prefill through one C-ABI call, with the
+    chunks device-resident or streamed from (pinned) host memory by the loader lane."""
+    name, p, chunks, bases = case(g, ci)
+    m = models[mp.F32]
+    ws = mp.Workspace(m, 64)
+    linked = mp.KV(3, p.n, 2, 8, mp.F32)
+    if host:
+        pins = []
+        for k, v, _ in chunks:
+            hk, hv = mp.HostBuffer(k.shape), mp.HostBuffer(v.shape)
+            hk.array[...] = k
+            hv.array[...] = v
+            pins += [hk, hv]
+        logits, sel = mp.request_prefill_host(m, ws, p, [x.array for x in pins[0::2]],
+                                              [x.array for x in pins[1::2]], linked, k=2,
+                                              reposition=mp.REROTATE, position_bases=bases)
+    else:
+        kvs = device_chunks(chunks, mp.F32)
+        logits, sel = mp.request_prefill(m, ws, p, kvs, linked, k=2, reposition=mp.REROTATE,
+                                         position_bases=bases)
+    assert np.array_equal(sel, g[f"{name}.sel.k2"])
+    assert np.abs(logits - g[f"{name}.rr.k2.logits"]).max() < 1e-5
+    k, v = linked.download()
+    assert np.abs(k - g[f"{name}.rr.k2.k"]).max() < 1e-5
+    assert np.abs(v - g[f"{name}.rr.k2.v"]).max() < 1e-5
+
+
+def test_error_contract(g, models):
+    name, p, chunks, bases = case(g, 0)
+    m = models[mp.F32]
+    ws = mp.Workspace(m, 64)
+    linked = mp.KV(3, p.n, 2, 8, mp.F32)
+    kvs = device_chunks(chunks, mp.F32)
+    with pytest.raises(mp.MpicError) as e:  # PrefixOnly -> empty mask
+        mp.request_prefill(m, ws, p, kvs, linked, policy=mp.POLICY_PREFIX_ONLY)
+    assert e.value.kind == "contract_error"
+    short = mp.KV(3, 3, 2, 8, mp.F32)
+    with pytest.raises(mp.MpicError) as e:  # token_count mismatch
+        mp.request_prefill(m, ws, p, [short], linked)
+    assert e.value.kind == "link_error"
+    with pytest.raises(mp.MpicError) as e:  # OOV id
+        mp.selective_prefill(m, ws, np.array([101], np.int32), np.array([0], np.uint32), linked)
+    assert e.value.kind == "validation_error"
+    with pytest.raises(mp.MpicError) as e:
+        mp.selective_prefill(m, ws, np.array([1, 2], np.int32), np.array([1, 0], np.uint32), linked)
+    assert e.value.kind == "contract_error"
+
+
+@pytest.mark.parametrize("dtype", [mp.F32, mp.BF16])
+def test_config_a96(dtype):
+    """Config A shape (L2 H8 D64 V4096) with 2x96-token images, k=32 and All."""
+    ga = dict(np.load(os.path.join(GOLD, "config_a96.npz")))
+    cfg = mp.config(2, 8, 64, vocab_size=4096, image_token_count=96, seed=1)
+    m = mp.Model(cfg, dtype)
+    p = mp.Prompt(ga["a.kinds"], ga["a.lens"], ga["a.text_ids"], ga["a.hashes"])
+    seed = int(ga["a.chunk_seed"][0])
+    chunks = []
+    for i in range(2):
+        gg = np.random.default_rng(seed + i)
+        k = (gg.random((2, 96, 512)) - 0.5).astype(np.float32)
+        v = (gg.random((2, 96, 512)) - 0.5).astype(np.float32)
+        chunks.append(mp.KV.from_host(k, v, 8, 64, dtype))
+    ws = mp.Workspace(m, 512)
+    for tag, pol in [("k32", mp.POLICY_MPIC_K), ("all", mp.POLICY_ALL)]:
+        linked = mp.KV(2, p.n, 8, 64, dtype)
+        logits, sel = mp.request_prefill(m, ws, p, chunks, linked, policy=pol, k=32)
+        assert np.array_equal(sel, ga[f"a.sel.{tag}"])
+        ref = ga[f"a.as.{tag}.logits"]
+        k, v = linked.download()
+        tol = 1e-4 if dtype == mp.F32 else 1e-2
+        assert rel_err(logits, ref) < tol, (tag, rel_err(logits, ref))
+        assert rel_err(k[-1][sel[-8:]], ga[f"a.as.{tag}.k_last_sel"]) < tol
+        assert rel_err(v[-1][sel[-8:]], ga[f"a.as.{tag}.v_last_sel"]) < tol
+    if dtype == mp.F32:  # assembly bytes == reference's assembled cache, by digest
+        import hashlib
+        linked = mp.KV(2, p.n, 8, 64, dtype)
+        refs, at, i = [], 0, 0
+        for kind, ln in zip(p.kinds, p.lens):
+            if kind == 1:
+                refs.append((chunks[i], 0, at, int(ln), 0))
+                i += 1
+            at += int(ln)
+        mp.assemble(refs, linked)
+        k, v = linked.download()
+        assert hashlib.sha256(k.tobytes()).digest() == ga["a.as.asm_sha_k"].tobytes()
+        assert hashlib.sha256(v.tobytes()).digest() == ga["a.as.asm_sha_v"].tobytes()
