@@ -1,0 +1,432 @@
+"""Bench: MPIC-k partial-reuse prefill (BASELINE.json metric: prefill tokens/s and p50 TTFT).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+
+One step = one MPIC-k request end to end on one GPU: select_tokens -> assemble the
+request's KV from its cached image chunks (K2) -> selective recompute of the text tokens
+plus the first k tokens of every image through all layers (K3-K8) -> first-token logits.
+Default workload is config C: LLaVA-1.6-7B shape, 32 layers x 32 heads x
+128, vocab 32000, 4 images of 2304 tokens each preceded by 32+7i text tokens, 32-token
+tail, k=32 => n=9418 prompt tokens, m=330 recomputed rows. bf16 weights synthesised on
+the device from seed 1 (bit-exact build_model, rounded to bf16); synthetic chunk KV.
+
+value : prompt tokens/s with the chunks resident in HBM (the store's Device tier),
+        device-timed with CUDA events; each rank serves its own requests (request
+        sharding, no collective) and value = all ranks' tokens / max-over-ranks time.
+e2e   : the same request through mpic_request_prefill_host with the chunk KV in pinned
+        HOST memory (fp32, as the .mpic store holds it): the per-layer H2D copies, the
+        ids upload and the logits download are inside the timed region.
+--impl reference: the unmodified reference (oracle/_ref, built from proj/src) on the
+        host cores, same workload, bounded sample (2 of 32 layers, scaled x16).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (L, H, D, V, [image tokens], k, text prefix fn)
+    "A": (2, 8, 64, 4096, [576, 576], 32),
+    "B": (32, 32, 128, 32000, [576], 32),
+    "C": (32, 32, 128, 32000, [2304] * 4, 32),
+    "D": (32, 32, 128, 32000, [2304] * 8, 32),
+}
+WORKLOAD_NAMES = {
+    "A": "A: tiny decoder L2 H8 D64 V4096, 2x576-token images + text, MPIC-k k=32",
+    "B": "B: LLaVA-1.5-7B shape L32 H32 D128 V32000, 1x576-token image + text, MPIC-k k=32",
+    "C": "C: LLaVA-1.6-7B shape L32 H32 D128 V32000, 4x2304-token images interleaved with "
+         "text (32+7i prefix tokens, 32-token tail), MPIC-k k=32, AsStored",
+    "D": "D: MRAG 8x2304-token retrieved images, LLaVA-1.6 shape, MPIC-k k=32",
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return (float(p["hbm_gbs"]), float(p["bf16_tflops"]), float(p["bf16_tflops_sustained"]),
+                "measured")
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def build_prompt(cfg_name, V, seed=42):
+    L, H, D, _, images, k = CONFIGS[cfg_name]
+    rng = np.random.default_rng(seed)
+    segs = []
+    for i, t in enumerate(images):
+        segs.append(("text", rng.integers(0, V - 1, 32 + 7 * i).tolist()))
+        segs.append(("image", rng.bytes(32), t))
+    segs.append(("text", rng.integers(0, V - 1, 32).tolist()))
+    return segs
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock/throttle sampling (NVML) during the timed region."""
+
+    def __init__(self, device_index=0, period=0.1):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self.period = period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for n, bit in names.items():
+                    if r & bit and n != "gpu_idle":
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def allreduce_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def algorithmic(cfg_name, n, m, sel, elt=2):
+    """Algorithmic bytes / FLOPs per step."""
+    L, H, D, V, images, _ = CONFIGS[cfg_name]
+    h = H * D
+    img = sum(images)
+    asm_bytes = 2 * img * L * 2 * h * elt  # read chunks + write assembled K and V
+    attn_flops_layer = 4.0 * h * float(np.sum(sel.astype(np.float64) + 1))
+    gemm = {"qkv": 2.0 * m * 3 * h * h, "wo": 2.0 * m * h * h, "w1": 2.0 * m * 4 * h * h,
+            "w2": 2.0 * m * 4 * h * h}
+    gemm_bytes = {"qkv": 3 * h * h * elt, "wo": h * h * elt, "w1": 4 * h * h * elt,
+                  "w2": 4 * h * h * elt}
+    return asm_bytes, attn_flops_layer, gemm, gemm_bytes, 2.0 * h * V
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_2502_01960_b200 as mp
+
+    L, H, D, V, images, k = CONFIGS[args.config]
+    h = H * D
+    dev = local
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    cfg = mp.config(L, H, D, vocab_size=V, image_token_count=images[0], seed=1)
+    model = mp.Model(cfg, mp.BF16, device=dev)
+    segs = build_prompt(args.config, V, seed=42 + rank)
+    prompt = mp.Prompt.from_segments(segs)
+    n = prompt.n
+    sel = mp.select_tokens(prompt, mp.POLICY_MPIC_K, k)
+    m = len(sel)
+    ws = mp.Workspace(model, m, n)
+
+    # chunk KV: pinned host fp32 (Host tier / .mpic payload) and a bf16 HBM copy (Device tier)
+    host_k, host_v, dev_chunks = [], [], []
+    g = np.random.default_rng(1234 + rank)
+    for t in images:
+        hk, hv = mp.HostBuffer((L, t, h)), mp.HostBuffer((L, t, h))
+        rk = g.random((t, h), dtype=np.float32) - 0.5  # U(-0.5, 0.5), one draw per chunk
+        rv = g.random((t, h), dtype=np.float32) - 0.5
+        for l in range(L):
+            hk.array[l] = rk
+            hv.array[l] = rv
+        kv = mp.KV(L, t, H, D, mp.BF16, dev)
+        kv.upload(hk.array, hv.array)
+        host_k.append(hk)
+        host_v.append(hv)
+        dev_chunks.append(kv)
+    linked = mp.KV(L, n, H, D, mp.BF16, dev)
+
+    def step_device():
+        logits, _ = mp.request_prefill(model, ws, prompt, dev_chunks, linked, k=k, stream=stream)
+        return mp.last_launch_count()
+
+    def step_host():
+        logits, _ = mp.request_prefill_host(model, ws, prompt, [x.array for x in host_k],
+                                            [x.array for x in host_v], linked, k=k,
+                                            stream=stream)
+        return mp.last_launch_count()
+
+    # ---- device-resident path (value) ----
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    mp.profile_enable(True)
+    mp.profile_collect()
+    barrier(world)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    launches = 0
+    per_step = []
+    with ClockSampler(dev) as clk:
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            for i in range(args.steps):
+                launches += step_device()
+                ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    mp.profile_enable(False)
+    phases = mp.profile_collect()
+    for i in range(args.steps):
+        per_step.append(ev[i].elapsed_time(ev[i + 1]))
+    total_ms = ev[0].elapsed_time(ev[-1])
+    total_ms = allreduce_max(total_ms, world)
+    ms_per_step = total_ms / args.steps
+    value = world * n * args.steps / (total_ms / 1e3)
+
+    # ---- end-to-end through the host-buffer C ABI call (e2e) ----
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(max(1, min(args.warmup, 2))):
+            step_host()
+        torch.cuda.synchronize()
+        barrier(world)
+        e_steps = args.steps
+        t0 = time.perf_counter()
+        ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(e_steps + 1)]
+        e2e_steps = []
+        with torch.cuda.stream(stream):
+            ev2[0].record(stream)
+            for i in range(e_steps):
+                launches_h = step_host()
+                ev2[i + 1].record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        for i in range(e_steps):
+            e2e_steps.append(ev2[i].elapsed_time(ev2[i + 1]))
+        e_ms = allreduce_max(ev2[0].elapsed_time(ev2[-1]), world)
+        h2d = sum(x.array.nbytes for x in host_k + host_v) + 2 * 4 * m
+        e2e = {"value": world * n * e_steps / (e_ms / 1e3), "unit": "prompt tokens/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * V),
+               "ttft_p50_ms": float(statistics.median(e2e_steps)),
+               "wall_s": wall, "path": "mpic_request_prefill_host (pinned fp32 chunks -> "
+                                       "per-layer H2D on a side stream, overlapped)"}
+
+    # ---- roofline of the dominant phase ----
+    hbm, tf_burst, tf_sust, peak_src = load_peaks()
+    asm_bytes, attn_fl, gemm_fl, gemm_b, lm_fl = algorithmic(args.config, n, m, sel)
+    steps = args.steps
+    per_phase = {}
+    for p, (ms, cnt) in phases.items():
+        if cnt == 0:
+            continue
+        avg = ms / cnt
+        if p == "assemble":
+            algo, unit = asm_bytes / (cnt / steps), "GB/s"
+            ach = algo / (avg / 1e3) / 1e9
+            pk = hbm
+            bound = "hbm"
+        elif p == "attn":
+            algo, unit = attn_fl, "TFLOP/s"
+            ach = algo / (avg / 1e3) / 1e12
+            pk = tf_sust
+            bound = "tensor"
+        elif p in gemm_fl:
+            algo, unit = gemm_fl[p], "TFLOP/s"
+            ach = algo / (avg / 1e3) / 1e12
+            pk = tf_sust
+            bound = "tensor"
+            per_phase.setdefault("weight_stream_GBps", {})[p] = round(
+                gemm_b[p] / (avg / 1e3) / 1e9, 1)
+        else:
+            per_phase[p] = {"ms_per_step": round(ms / steps, 4), "launches": cnt}
+            continue
+        per_phase[p] = {"ms_per_step": round(ms / steps, 4), "launches": cnt,
+                        "avg_launch_ms": round(avg, 5), "achieved": round(ach, 2), "unit": unit,
+                        "bound": bound, "frac": round(ach / pk, 4)}
+    cand = [(v["ms_per_step"], p) for p, v in per_phase.items()
+            if isinstance(v, dict) and "achieved" in v]
+    dom = max(cand)[1]
+    d = per_phase[dom]
+    roofline = {"bound": d["bound"], "achieved": d["achieved"],
+                "peak": hbm if d["bound"] == "hbm" else tf_sust, "unit": d["unit"],
+                "frac": d["frac"], "traffic": None, "kernel": dom,
+                "peak_source": peak_src + (" HBM copy" if d["bound"] == "hbm"
+                                           else " bf16 sustained"),
+                "per_launch_algorithmic": (asm_bytes if dom == "assemble" else
+                                           attn_fl if dom == "attn" else gemm_fl.get(dom))}
+    # whole-request fraction: sum over phases of max(F/P, B/BW) / step time
+    floor_ms = (asm_bytes / (hbm * 1e9) + L * (
+        max(sum(gemm_fl.values()) / (tf_sust * 1e12), sum(gemm_b.values()) / (hbm * 1e9)) +
+        attn_fl / (tf_sust * 1e12))) * 1e3
+    return dict(value=value, ms_per_step=ms_per_step, per_step=per_step, e2e=e2e,
+                launches=launches, roofline=roofline, phases=per_phase, clocks=clk.summary(),
+                n=n, m=m, floor_ms=floor_ms, world=world)
+
+
+def cpu_reference(cfg_name, steps, warmup, threads=None, layers_sample=2, seed=42):
+    """Time the unmodified reference's assemble_linked_cache + selective_prefill on the
+    host cores (oracle/_ref). Bounded sample: `layers_sample` of L layers, scaled."""
+    import oracle
+    L, H, D, V, images, k = CONFIGS[cfg_name]
+    h = H * D
+    if not oracle.have_ref():
+        return None, "oracle/_ref not built"
+    r = oracle.RefLib()
+    threads = threads or os.cpu_count()
+    r.set_threads(threads)
+    ls = min(layers_sample, L)
+    cfg = oracle.Config(ls, H, D, h, V, images[0], 10000.0, 1)
+    rm = r.model(cfg)
+    segs = build_prompt(cfg_name, V, seed)
+    p = oracle.make_prompt(segs, "")
+    g = np.random.default_rng(1234)
+    for t in images:
+        p.chunk_k.append((g.random((ls, t, h), dtype=np.float32) - 0.5))
+        p.chunk_v.append((g.random((ls, t, h), dtype=np.float32) - 0.5))
+        p.chunk_base.append(0)
+    sel = rm.select(p, 0, k)
+    ents = rm.entries(p)
+    times = []
+    try:
+        for i in range(warmup + steps):
+            res = rm.link_and_prefill(p, sel=sel, want_asm=False, want_final=False, entries=ents)
+            if i >= warmup:
+                times.append((res["ms_assemble"] + res["ms_selective"]) * (L / ls))
+    finally:
+        r.lib.ref_entries_free(ents)
+    return dict(ms=float(statistics.median(times)), n=p.n, m=len(sel), threads=threads,
+                sample=f"{ls} of {L} layers of config {cfg_name} (n={p.n}, m={len(sel)}), "
+                       f"per-request time scaled x{L / ls:g}; assemble_linked_cache + "
+                       f"selective_prefill, OpenBLAS {threads} threads"), None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    L, H, D, V, images, k = CONFIGS[args.config]
+    cfg_json = {"workload": WORKLOAD_NAMES[args.config], "layers": L, "heads": H, "head_dim": D,
+                "vocab": V, "image_tokens": images, "k": k,
+                "parallelism": f"request-sharded x{args.gpus} (no collective)",
+                "l2": "inputs larger than L2: 12.9 GB bf16 weights + 4.8 GB chunk KV stream "
+                      "through HBM every step"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        res, why = cpu_reference(args.config, args.steps, args.warmup)
+        if res is None:
+            print(json.dumps({"impl": "reference", "unavailable": why}))
+            return
+        val = res["n"] / (res["ms"] / 1e3)
+        line = {"metric": "MPIC-k prefill tokens/s (p50 TTFT alongside)", "impl": "reference",
+                "value": val, "unit": "prompt tokens/s", "n_gpus": 0, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": res["ms"], "ttft_p50_ms": res["ms"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic (seeded ids, U(-0.5,0.5) chunk KV)",
+                "config": cfg_json,
+                "cpu_baseline": {"value": val, "unit": "prompt tokens/s", "cores": res["threads"],
+                                 "kind": "reference", "sample": res["sample"]},
+                "e2e": {"value": val, "unit": "prompt tokens/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    world, rank, local = dist_setup(args.gpus)
+    r = run_ours(args, world, rank, local)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res, why = cpu_reference(args.config, steps=2, warmup=1)
+        if res is not None:
+            cpu = {"value": res["n"] / (res["ms"] / 1e3), "unit": "prompt tokens/s",
+                   "cores": res["threads"], "kind": "reference", "sample": res["sample"],
+                   "ttft_ms": res["ms"]}
+        else:
+            cpu = {"value": None, "unavailable": why}
+    if rank == 0:
+        line = {"metric": "MPIC-k prefill tokens/s (p50 TTFT alongside)", "value": r["value"],
+                "unit": "prompt tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+                "ttft_p50_ms": float(statistics.median(r["per_step"])),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "bf16", "data": "synthetic (seeded ids and hashes, U(-0.5,0.5) chunk "
+                                         "KV, weights synthesised from seed 1)",
+                "config": dict(cfg_json, n_tokens=r["n"], recompute_rows=r["m"]),
+                "e2e": r["e2e"], "gpu_launches": r["launches"], "roofline": r["roofline"],
+                "request_roofline_frac": round(r["floor_ms"] / r["ms_per_step"], 4),
+                "phases": r["phases"], "cpu_baseline": cpu, "clocks": r["clocks"]}
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -213,6 +213,25 @@ int mpic_host_free(void* p);
 int mpic_test_gemm(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uint32_t K, int path,
                    float* d_out, void* stream);
 
+/* ---- per-phase device timing ------------------------------------------------------ */
+typedef enum {
+    MPIC_PHASE_ASSEMBLE = 0, /* K2 chunk gather (+ rerotate, cast) */
+    MPIC_PHASE_EMBED = 1,
+    MPIC_PHASE_QKV = 2,      /* K3 QKV GEMM + RoPE + KV scatter */
+    MPIC_PHASE_ATTN = 3,     /* K4 selective attention */
+    MPIC_PHASE_WO = 4,       /* K5 Wo GEMM + residual */
+    MPIC_PHASE_W1 = 5,       /* K6 W1 GEMM + GELU */
+    MPIC_PHASE_W2 = 6,       /* K7 W2 GEMM + residual */
+    MPIC_PHASE_CAST = 7,     /* fp32 residual -> bf16 operand */
+    MPIC_PHASE_LM_HEAD = 8,  /* K8 */
+    MPIC_PHASE_COUNT = 9
+} mpic_phase;
+/* When enabled, every phase records CUDA events on its launching stream. collect()
+ * waits for them and returns per-phase summed milliseconds and instance counts
+ * (arrays of MPIC_PHASE_COUNT), then resets. */
+int mpic_profile_enable(int on);
+int mpic_profile_collect(double* ms, uint32_t* counts);
+
 /* Number of kernels the last forward/assemble call on this thread launched. */
 uint32_t mpic_last_launch_count(void);
 

@@ -295,3 +295,19 @@ def request_prefill_host(model: Model, ws: Workspace, prompt: Prompt, chunk_k, c
                                           linked.handle, logits.ctypes.data, sel.ctypes.data,
                                           C.byref(m), _stream_ptr(stream)))
     return logits, sel[:m.value].copy()
+
+
+PHASES = ["assemble", "embed", "qkv", "attn", "wo", "w1", "w2", "cast", "lm_head"]
+
+
+def profile_enable(on: bool = True):
+    """Per-phase CUDA-event timing inside the library (mpic_profile_enable)."""
+    check(lib().mpic_profile_enable(int(on)))
+
+
+def profile_collect() -> dict:
+    """{phase: (summed ms, instances)} since the last collect (mpic_profile_collect)."""
+    ms = np.zeros(len(PHASES), np.float64)
+    cnt = np.zeros(len(PHASES), np.uint32)
+    check(lib().mpic_profile_collect(ms.ctypes.data, cnt.ctypes.data))
+    return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(PHASES)}

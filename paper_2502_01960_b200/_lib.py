@@ -92,6 +92,8 @@ SIGNATURES = {
     "mpic_request_prefill_host": (_int, [_vp, _vp, _P(PromptDesc), _P(PolicyDesc), _vp, _vp,
                                          _vp, _int, _vp, _vp, _vp, _P(_u32), _vp]),
     "mpic_test_gemm": (_int, [_vp, _vp, _u32, _u32, _u32, _int, _vp, _vp]),
+    "mpic_profile_enable": (_int, [_int]),
+    "mpic_profile_collect": (_int, [_vp, _vp]),
     "mpic_host_alloc": (_int, [C.c_size_t, _P(_vp)]),
     "mpic_host_free": (_int, [_vp]),
 }

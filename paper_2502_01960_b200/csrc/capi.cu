@@ -2,6 +2,7 @@
 // sequence of the selective recompute, and the assembly entry points.
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <functional>
 #include <mutex>
 #include <string>
@@ -16,6 +17,50 @@ thread_local std::string g_last_error;
 thread_local uint32_t g_launches = 0;
 }  // namespace
 void note_launch(uint32_t n) { g_launches += n; }
+
+// ---- per-phase device timing (CUDA events on the launching stream) ------------------
+// Enabled by mpic_profile_enable(1); each phase of a forward/assembly records a start and
+// stop event around its launches; mpic_profile_collect() synchronizes and sums them.
+namespace {
+struct ProfRec {
+    int cls;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof_recs;
+std::vector<cudaEvent_t> g_prof_pool;
+
+cudaEvent_t prof_event() {
+    if (!g_prof_pool.empty()) {
+        cudaEvent_t e = g_prof_pool.back();
+        g_prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    MPIC_CUDA(cudaEventCreate(&e));
+    return e;
+}
+}  // namespace
+
+struct ProfScope {
+    cudaStream_t s;
+    int cls;
+    cudaEvent_t a = nullptr;
+    ProfScope(cudaStream_t st, int c) : s(st), cls(c) {
+        if (!g_prof_on) return;
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        a = prof_event();
+        cudaEventRecord(a, s);
+    }
+    ~ProfScope() {
+        if (!a) return;
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        cudaEvent_t b = prof_event();
+        cudaEventRecord(b, s);
+        g_prof_recs.push_back({cls, a, b});
+    }
+};
 }  // namespace mpicb
 
 using namespace mpicb;
@@ -58,6 +103,8 @@ struct mpic_workspace_s {
     void* attn = nullptr;               // [m_pad][h] dtype
     void* ffn = nullptr;                // [m_pad][4h] dtype
     float* d_logits = nullptr;          // [V]
+    float* partial = nullptr;           // split-K partials [8][m_pad][h]
+    size_t partial_cap = 0;
     int32_t* h_ids = nullptr;           // pinned staging
     uint32_t* h_rows = nullptr;
     uint32_t* h_pos = nullptr;
@@ -68,6 +115,16 @@ struct mpic_workspace_s {
     cudaEvent_t ev_free[2] = {nullptr, nullptr};
     void* stage[2] = {nullptr, nullptr};
     size_t stage_cap = 0;
+    // tcgen05 attention plan (per request) and split partials
+    AttnUnit* d_units = nullptr;
+    AttnCombine* d_comb = nullptr;
+    size_t units_cap = 0, comb_cap = 0;
+    float* part_o = nullptr;
+    float2* part_ml = nullptr;
+    size_t slots_cap = 0;
+    void* h_plan = nullptr;  // pinned staging for the plan
+    size_t h_plan_cap = 0;
+    uint32_t n_units = 0, n_comb = 0;
 };
 
 #define API_BEGIN \
@@ -252,11 +309,62 @@ void run_gemm(mpic_model_t md, const void* A, const void* W, uint32_t M, uint32_
     launch_gemm_simt(A, MPIC_F32, K, W, MPIC_F32, M, N, K, ep, MPIC_F32, s);
 }
 
+bool use_tc_attention(mpic_model_t md) {
+    return md->dtype == MPIC_BF16 && md->cfg.head_dim == 128;
+}
+
+// Build the attention work plan from host rows (or, without them, a conservative plan in
+// which every query may see keys up to max_pos) and upload it to the workspace.
+void upload_attn_plan(mpic_workspace_t ws, const uint32_t* h_rows, uint32_t m, uint32_t max_pos,
+                      uint32_t H, cudaStream_t s) {
+    std::vector<uint32_t> conservative;
+    if (!h_rows) {
+        conservative.assign(m, max_pos);
+        h_rows = conservative.data();
+    }
+    const AttnPlan plan = plan_attention(h_rows, m, H);
+    auto grow = [&](auto*& ptr, size_t& cap, size_t need, size_t elt) {
+        if (cap >= need) return;
+        MPIC_CUDA(cudaStreamSynchronize(s));
+        cudaFree(ptr);
+        ptr = nullptr;
+        MPIC_CUDA(cudaMalloc((void**)&ptr, std::max<size_t>(need, 1) * elt));
+        cap = need;
+    };
+    grow(ws->d_units, ws->units_cap, plan.units.size(), sizeof(AttnUnit));
+    grow(ws->d_comb, ws->comb_cap, plan.combine.size(), sizeof(AttnCombine));
+    if (ws->slots_cap < plan.slots) {
+        MPIC_CUDA(cudaStreamSynchronize(s));
+        cudaFree(ws->part_o);
+        cudaFree(ws->part_ml);
+        MPIC_CUDA(cudaMalloc(&ws->part_o, (size_t)plan.slots * 128 * 128 * sizeof(float)));
+        MPIC_CUDA(cudaMalloc(&ws->part_ml, (size_t)plan.slots * 128 * sizeof(float2)));
+        ws->slots_cap = plan.slots;
+    }
+    const size_t bu = plan.units.size() * sizeof(AttnUnit);
+    const size_t bc = plan.combine.size() * sizeof(AttnCombine);
+    if (ws->h_plan_cap < bu + bc) {
+        MPIC_CUDA(cudaStreamSynchronize(s));
+        cudaFreeHost(ws->h_plan);
+        MPIC_CUDA(cudaMallocHost(&ws->h_plan, bu + bc));
+        ws->h_plan_cap = bu + bc;
+    } else {
+        MPIC_CUDA(cudaStreamSynchronize(s));  // previous request's plan copy has landed
+    }
+    std::memcpy(ws->h_plan, plan.units.data(), bu);
+    std::memcpy((char*)ws->h_plan + bu, plan.combine.data(), bc);
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_units, ws->h_plan, bu, cudaMemcpyHostToDevice, s));
+    if (bc) MPIC_CUDA(cudaMemcpyAsync(ws->d_comb, (char*)ws->h_plan + bu, bc, cudaMemcpyHostToDevice, s));
+    ws->n_units = (uint32_t)plan.units.size();
+    ws->n_comb = (uint32_t)plan.combine.size();
+}
+
 // selective_core / extend_rows on the device (linker.cpp:35-135, model.cpp:211-330).
 void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
                   const uint32_t* d_rows, const uint32_t* d_pos, uint32_t m, uint32_t max_pos,
                   mpic_kv_t kv, float* d_logits, cudaStream_t s,
-                  const std::function<void(uint32_t)>& before_layer = {}) {
+                  const std::function<void(uint32_t)>& before_layer = {},
+                  const uint32_t* h_rows = nullptr) {
     const mpic_model_config& c = md->cfg;
     const uint32_t h = c.hidden_dim, H = c.n_heads, D = c.head_dim;
     MPIC_REQUIRE(m > 0, MPIC_ERR_VALIDATION, "no tokens to prefill");
@@ -269,7 +377,12 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
     const size_t e = esz(md->dtype);
     const size_t plane = (size_t)kv->T * h * e;
 
-    launch_embed(md->emb, d_ids, m, h, ws->x, bf ? ws->xb : nullptr, s);
+    {
+        ProfScope ps(s, MPIC_PHASE_EMBED);
+        launch_embed(md->emb, d_ids, m, h, ws->x, bf ? ws->xb : nullptr, s);
+    }
+    const bool tc_attn = use_tc_attention(md);
+    if (tc_attn) upload_attn_plan(ws, h_rows, m, max_pos, H, s);
     for (uint32_t l = 0; l < c.n_layers; ++l) {
         void* kl = (char*)kv->k + l * plane;
         void* vl = (char*)kv->v + l * plane;
@@ -284,27 +397,52 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
         qkv.rope = md->rope;
         qkv.hidden = h;
         qkv.head_dim = D;
-        run_gemm(md, bf ? (const void*)ws->xb : (const void*)ws->x, md->wqkv[l], m, 3 * h, h, qkv, s);
-
-        launch_attn_simt(ws->q, kl, vl, md->dtype, d_rows, m, H, D, ws->attn, s);
+        {
+            ProfScope ps(s, MPIC_PHASE_QKV);
+            run_gemm(md, bf ? (const void*)ws->xb : (const void*)ws->x, md->wqkv[l], m, 3 * h, h, qkv, s);
+        }
+        {
+            ProfScope ps(s, MPIC_PHASE_ATTN);
+            if (tc_attn)
+                launch_attn_tc(static_cast<const __nv_bfloat16*>(ws->q), static_cast<const __nv_bfloat16*>(kl),
+                               static_cast<const __nv_bfloat16*>(vl), kv->T, d_rows, m, H, ws->d_units,
+                               ws->n_units, ws->d_comb, ws->n_comb, ws->part_o, ws->part_ml,
+                               static_cast<__nv_bfloat16*>(ws->attn), s);
+            else
+                launch_attn_simt(ws->q, kl, vl, md->dtype, d_rows, m, H, D, ws->attn, s);
+        }
 
         EpiParams res;
         res.mode = EPI_RESID;
         res.x = ws->x;
         res.ldx = h;
-        run_gemm(md, ws->attn, md->wo[l], m, h, h, res, s);
-        if (bf) launch_x_to_bf16(ws->x, ws->xb, m, h, s);
+        if (bf) {  // residual add also emits the bf16 operand of the next GEMM
+            res.xb = ws->xb;
+            res.partial = ws->partial;
+            res.partial_cap = ws->partial_cap;
+        }
+        {
+            ProfScope ps(s, MPIC_PHASE_WO);
+            run_gemm(md, ws->attn, md->wo[l], m, h, h, res, s);
+        }
 
         EpiParams gl;
         gl.mode = EPI_GELU;
         gl.out = ws->ffn;
         gl.ldo = 4 * h;
-        run_gemm(md, bf ? (const void*)ws->xb : (const void*)ws->x, md->w1[l], m, 4 * h, h, gl, s);
-
-        run_gemm(md, ws->ffn, md->w2[l], m, h, 4 * h, res, s);
-        if (bf && l + 1 < c.n_layers) launch_x_to_bf16(ws->x, ws->xb, m, h, s);
+        {
+            ProfScope ps(s, MPIC_PHASE_W1);
+            run_gemm(md, bf ? (const void*)ws->xb : (const void*)ws->x, md->w1[l], m, 4 * h, h, gl, s);
+        }
+        {
+            ProfScope ps(s, MPIC_PHASE_W2);
+            run_gemm(md, ws->ffn, md->w2[l], m, h, 4 * h, res, s);
+        }
     }
-    launch_lm_head(ws->x + (size_t)(m - 1) * h, md->lm_head, md->dtype, c.vocab_size, h, d_logits, s);
+    {
+        ProfScope ps(s, MPIC_PHASE_LM_HEAD);
+        launch_lm_head(ws->x + (size_t)(m - 1) * h, md->lm_head, md->dtype, c.vocab_size, h, d_logits, s);
+    }
     (void)e;
 }
 
@@ -333,7 +471,8 @@ void forward_host(mpic_model_t md, mpic_workspace_t ws, const int32_t* ids, cons
     MPIC_CUDA(cudaMemcpyAsync(ws->d_ids, ws->h_ids, m * 4, cudaMemcpyHostToDevice, s));
     MPIC_CUDA(cudaMemcpyAsync(ws->d_rows, ws->h_rows, m * 4, cudaMemcpyHostToDevice, s));
     MPIC_CUDA(cudaMemcpyAsync(ws->d_pos, ws->h_pos, m * 4, cudaMemcpyHostToDevice, s));
-    forward_rows(md, ws, ws->d_ids, ws->d_rows, ws->d_pos, m, max_pos, kv, ws->d_logits, s);
+    forward_rows(md, ws, ws->d_ids, ws->d_rows, ws->d_pos, m, max_pos, kv, ws->d_logits, s, {},
+                 rows);
     MPIC_CUDA(cudaMemcpyAsync(ws->h_logits, ws->d_logits, md->cfg.vocab_size * 4,
                               cudaMemcpyDeviceToHost, s));
     MPIC_CUDA(cudaStreamSynchronize(s));
@@ -412,8 +551,11 @@ void do_assemble(cudaStream_t s, const void* const* src_k, const void* const* sr
     const AsmChunk* dc;
     const float2* dt;
     void* buf = upload_plan(p, s, &dc, &dt);
-    launch_assemble(dc, n, dt, p.n_tables, src_t, dst->k, dst->v, dst->dtype, dst->L, dst->T,
-                    dst->H, dst->D, zero_gaps, s);
+    {
+        ProfScope ps(s, MPIC_PHASE_ASSEMBLE);
+        launch_assemble(dc, n, dt, p.n_tables, src_t, dst->k, dst->v, dst->dtype, dst->L, dst->T,
+                        dst->H, dst->D, zero_gaps, s);
+    }
     MPIC_CUDA(cudaFreeAsync(buf, s));
 }
 
@@ -573,7 +715,7 @@ void run_request(mpic_model_t md, mpic_workspace_t ws, const RequestPlan& r, mpi
     MPIC_CUDA(cudaMemcpyAsync(ws->d_ids, ws->h_ids, r.m * 4, cudaMemcpyHostToDevice, s));
     MPIC_CUDA(cudaMemcpyAsync(ws->d_rows, ws->h_rows, r.m * 4, cudaMemcpyHostToDevice, s));
     forward_rows(md, ws, ws->d_ids, ws->d_rows, ws->d_rows, r.m, r.n - 1, linked, ws->d_logits, s,
-                 before_layer);
+                 before_layer, r.sel.data());
     MPIC_CUDA(cudaMemcpyAsync(ws->h_logits, ws->d_logits, md->cfg.vocab_size * 4,
                               cudaMemcpyDeviceToHost, s));
     MPIC_CUDA(cudaStreamSynchronize(s));
@@ -841,6 +983,10 @@ int mpic_workspace_create(mpic_model_t md, uint32_t max_rows, uint32_t max_ctx, 
     MPIC_CUDA(cudaMemset(ws->attn, 0, mp * h * e));
     MPIC_CUDA(cudaMemset(ws->ffn, 0, mp * 4 * h * e));
     ws->d_logits = dmalloc<float>(md->cfg.vocab_size);
+    if (md->dtype == MPIC_BF16) {
+        ws->partial_cap = 8 * mp * h;
+        ws->partial = dmalloc<float>(ws->partial_cap);
+    }
     MPIC_CUDA(cudaMallocHost(&ws->h_ids, mp * 4));
     MPIC_CUDA(cudaMallocHost(&ws->h_rows, mp * 4));
     MPIC_CUDA(cudaMallocHost(&ws->h_pos, mp * 4));
@@ -862,6 +1008,7 @@ int mpic_workspace_destroy(mpic_workspace_t ws) {
         cudaFree(ws->d_ids); cudaFree(ws->d_rows); cudaFree(ws->d_pos);
         cudaFree(ws->x); cudaFree(ws->xb); cudaFree(ws->q); cudaFree(ws->attn); cudaFree(ws->ffn);
         cudaFree(ws->d_logits);
+        cudaFree(ws->partial);
         cudaFreeHost(ws->h_ids); cudaFreeHost(ws->h_rows); cudaFreeHost(ws->h_pos);
         cudaFreeHost(ws->h_logits);
         for (int i = 0; i < 2; ++i) {
@@ -870,6 +1017,11 @@ int mpic_workspace_destroy(mpic_workspace_t ws) {
             if (ws->ev_free[i]) cudaEventDestroy(ws->ev_free[i]);
         }
         if (ws->copy_stream) cudaStreamDestroy(ws->copy_stream);
+        cudaFree(ws->d_units);
+        cudaFree(ws->d_comb);
+        cudaFree(ws->part_o);
+        cudaFree(ws->part_ml);
+        cudaFreeHost(ws->h_plan);
         delete ws;
     }
     API_END
@@ -1034,6 +1186,7 @@ int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpi
         if (l + 1 < L) issue_copy(l + 1);  // waits for layer l-1's assembly to free the slot
         const int sl = l & 1;
         MPIC_CUDA(cudaStreamWaitEvent(s, ws->ev_ready[sl], 0));
+        ProfScope ps(s, MPIC_PHASE_ASSEMBLE);
         launch_assemble(dc[sl], n_img, dt[sl], n_tab, MPIC_F32, (char*)linked->k + l * plane,
                         (char*)linked->v + l * plane, linked->dtype, 1, linked->T, linked->H,
                         linked->D, 1, s);
@@ -1057,6 +1210,39 @@ int mpic_test_gemm(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uin
         launch_gemm_tc(static_cast<const __nv_bfloat16*>(d_a), K, static_cast<const __nv_bfloat16*>(d_w), M, N, K, ep, s);
     } else {
         launch_gemm_simt(d_a, MPIC_BF16, K, d_w, MPIC_BF16, M, N, K, ep, MPIC_BF16, s);
+    }
+    API_END
+}
+
+int mpic_profile_enable(int on) {
+    API_BEGIN
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = on != 0;
+    API_END
+}
+
+int mpic_profile_collect(double* ms, uint32_t* launches) {
+    API_BEGIN
+    std::vector<ProfRec> recs;
+    {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        recs.swap(g_prof_recs);
+    }
+    for (int i = 0; i < MPIC_PHASE_COUNT; ++i) {
+        ms[i] = 0.0;
+        launches[i] = 0;
+    }
+    for (const ProfRec& r : recs) {
+        MPIC_CUDA(cudaEventSynchronize(r.b));
+        float t = 0.f;
+        MPIC_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+        ms[r.cls] += t;
+        launches[r.cls] += 1;
+    }
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (const ProfRec& r : recs) {
+        g_prof_pool.push_back(r.a);
+        g_prof_pool.push_back(r.b);
     }
     API_END
 }

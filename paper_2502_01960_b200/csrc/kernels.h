@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "mpic_b200.h"
 
 namespace mpicb {
@@ -24,10 +26,16 @@ struct EpiParams {
     const float2* rope = nullptr;  // [pos][head_dim/2] (cos, sin)
     uint32_t hidden = 0;
     uint32_t head_dim = 0;
-    // EPI_RESID: x[row][col] += acc (atomic when split_k > 1)
+    // EPI_RESID: x[row][col] += acc, and xb = bf16(x) when xb != null. The tcgen05 GEMM
+    // may split K: partials go to `partial` ([split][rows_total][ldx] fp32, capacity
+    // partial_cap floats) and a reduction kernel adds them (deterministic order).
     float* x = nullptr;
+    __nv_bfloat16* xb = nullptr;
     uint32_t ldx = 0;
     uint32_t split_k = 1;
+    float* partial = nullptr;
+    size_t partial_cap = 0;
+    uint32_t rows_total = 0;
     // EPI_STORE / EPI_GELU
     void* out = nullptr;
     uint32_t ldo = 0;
@@ -70,6 +78,26 @@ void launch_assemble(const AsmChunk* d_chunks, uint32_t n_chunks, const float2* 
                      uint32_t n_tables, mpic_dtype src_t, void* dst_k, void* dst_v,
                      mpic_dtype dst_t, uint32_t L, uint32_t T_dst, uint32_t H, uint32_t D,
                      int zero_gaps, cudaStream_t s);
+
+// Attention work plan (tc_attn.cu): units = (query tile, head, key-block range).
+struct AttnUnit {
+    uint32_t tile, head, b0, b1;
+    uint32_t slot;  // 0xffffffff: write the final output; else partial slot for the combine
+};
+struct AttnCombine {
+    uint32_t tile, head, slot0, n;
+};
+struct AttnPlan {
+    std::vector<AttnUnit> units;
+    std::vector<AttnCombine> combine;
+    uint32_t slots = 0;
+};
+AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads);
+void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const __nv_bfloat16* vcache,
+                    uint32_t n_ctx, const uint32_t* d_rows, uint32_t m, uint32_t H,
+                    const AttnUnit* d_units, uint32_t n_units, const AttnCombine* d_combine,
+                    uint32_t n_combine, float* part_o, float2* part_ml, __nv_bfloat16* out,
+                    cudaStream_t s);
 
 // tcgen05 / TMA kernels (tc_gemm.cu, tc_attn.cu)
 struct TcGemmPlan;

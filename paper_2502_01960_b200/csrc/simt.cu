@@ -76,12 +76,11 @@ __device__ __forceinline__ void epi_pair(const EpiParams& ep, uint32_t row, uint
         }
         case EPI_RESID: {  // x += proj (linker.cpp:115-118, 124-128)
             float* x = ep.x + (size_t)row * ep.ldx + col;
-            if (ep.split_k > 1) {
-                atomicAdd(x, v0);
-                atomicAdd(x + 1, v1);
-            } else {
-                x[0] += v0;
-                x[1] += v1;
+            x[0] += v0;
+            x[1] += v1;
+            if (ep.xb) {
+                ep.xb[(size_t)row * ep.ldx + col] = __float2bfloat16_rn(x[0]);
+                ep.xb[(size_t)row * ep.ldx + col + 1] = __float2bfloat16_rn(x[1]);
             }
             break;
         }

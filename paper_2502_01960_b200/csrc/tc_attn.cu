@@ -1,0 +1,400 @@
+// K4 — selective causal attention on the 5th-gen tensor cores (head_dim 128).
+//
+// For recomputed row i (cache position rows[i]) and head hd, attend over cache keys
+// [0, rows[i]] of the just-scattered layer cache (proj/src/linker.cpp:80-113): the
+// per-row causal limit is the row's POSITION, not its index in the tile.
+//
+// Work unit = (128-query tile, head, range of 128-key blocks). The host splits long key
+// ranges (flash-decoding style) so that ~3 waves of units cover the 148 SMs; partial
+// results are merged by attn_combine_kernel. One CTA per unit:
+//
+//   warp 0     TMA: Q tile [128 x 128] once, K/V blocks [128 keys x 128] into 2-stage rings
+//   warp 1     TMEM alloc (512 cols: S0 | S1 | O) + single-thread tcgen05.mma issuer:
+//              S_b = Q . K_b^T (SS, K-major) and O += P_b . V_b (P K-major from smem,
+//              V MN-major), in the order S0 S1 PV0 S2 PV1 S3 ...
+//   warps 2-5  softmax, one thread per query row (TMEM lane): scale, per-row causal mask,
+//              online max with lazy rescaling of O in TMEM (only when the max grows by
+//              more than 2^8), exp2, row sums, P written to smem in the SWIZZLE_128B
+//              K-major layout the MMA descriptor expects; final O / l epilogue.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace mpicb {
+
+CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                           uint32_t box_outer);
+
+namespace {
+
+constexpr uint32_t kAttnThreads = 192;
+constexpr uint32_t kTile = 32 * 1024;  // one [128 x 128] bf16 tile as 2 swizzled 64-col halves
+constexpr uint32_t kHalf = 16 * 1024;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct AttnParams {
+    const AttnUnit* units;
+    const uint32_t* rows;
+    uint32_t m;
+    uint32_t h;
+    float scale_log2;       // inv_sqrt_d * log2(e)
+    __nv_bfloat16* out;     // [m][h]
+    float* part_o;          // [slots][128][128]
+    float2* part_ml;        // [slots][128] (m_used, l)
+};
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+__global__ void __launch_bounds__(kAttnThreads, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;
+    uint8_t* sK = smem + kTile;          // 2 stages
+    uint8_t* sV = smem + 3 * kTile;      // 2 stages
+    uint8_t* sP = smem + 5 * kTile;      // 2 buffers
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 7 * kTile);
+    uint64_t* q_full = bars + 0;
+    uint64_t* k_full = bars + 1;   // [2]
+    uint64_t* k_empty = bars + 3;  // [2]
+    uint64_t* v_full = bars + 5;   // [2]
+    uint64_t* v_empty = bars + 7;  // [2]
+    uint64_t* s_full = bars + 9;   // [2]
+    uint64_t* p_full = bars + 11;  // [2]
+    uint64_t* o_full = bars + 13;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 14);
+
+    const AttnUnit u = p.units[blockIdx.x];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t q0 = u.tile * 128u;
+    const uint32_t nb = u.b1 - u.b0;
+    const int hcol = (int)(u.head * 128u);
+
+    if (warp == 0 && lane == 0) {
+        tc::tma_prefetch_desc(&tmQ);
+        tc::tma_prefetch_desc(&tmK);
+        tc::tma_prefetch_desc(&tmV);
+        tc::mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&k_full[i], 1);
+            tc::mbar_init(&k_empty[i], 1);
+            tc::mbar_init(&v_full[i], 1);
+            tc::mbar_init(&v_empty[i], 1);
+            tc::mbar_init(&s_full[i], 1);
+            tc::mbar_init(&p_full[i], 128);
+        }
+        tc::mbar_init(o_full, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_holder, 512);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_holder;
+    constexpr uint32_t idesc_s = tc::idesc_bf16(128, 128, false);
+    constexpr uint32_t idesc_o = tc::idesc_bf16(128, 128, true);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tc::mbar_arrive_expect_tx(q_full, kTile);
+            tc::tma_load_2d(sQ, &tmQ, q_full, hcol, (int)q0);
+            tc::tma_load_2d(sQ + kHalf, &tmQ, q_full, hcol + 64, (int)q0);
+            for (uint32_t b = 0; b < nb; ++b) {
+                const uint32_t s = b & 1, ph = (b >> 1) & 1;
+                const int j0 = (int)((u.b0 + b) * 128u);
+                tc::mbar_wait(&k_empty[s], ph ^ 1);
+                tc::mbar_arrive_expect_tx(&k_full[s], kTile);
+                tc::tma_load_2d(sK + s * kTile, &tmK, &k_full[s], hcol, j0);
+                tc::tma_load_2d(sK + s * kTile + kHalf, &tmK, &k_full[s], hcol + 64, j0);
+                tc::mbar_wait(&v_empty[s], ph ^ 1);
+                tc::mbar_arrive_expect_tx(&v_full[s], kTile);
+                tc::tma_load_2d(sV + s * kTile, &tmV, &v_full[s], hcol, j0);
+                tc::tma_load_2d(sV + s * kTile + kHalf, &tmV, &v_full[s], hcol + 64, j0);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t qa = tc::smem_u32(sQ);
+            auto issue_s = [&](uint32_t b) {
+                const uint32_t s = b & 1;
+                tc::mbar_wait(&k_full[s], (b >> 1) & 1);
+                tc::tc_fence_after();
+                const uint32_t ka = tc::smem_u32(sK + s * kTile);
+#pragma unroll
+                for (uint32_t kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+                    tc::mma_bf16(tmem + s * 128, tc::desc_k_sw128(qa + off), tc::desc_k_sw128(ka + off),
+                                 idesc_s, kk > 0 ? 1u : 0u);
+                }
+                tc::mma_commit(&k_empty[s]);
+                tc::mma_commit(&s_full[s]);
+            };
+            tc::mbar_wait(q_full, 0);
+            issue_s(0);
+            if (nb > 1) issue_s(1);
+            for (uint32_t b = 0; b < nb; ++b) {
+                const uint32_t s = b & 1, ph = (b >> 1) & 1;
+                tc::mbar_wait(&p_full[s], ph);
+                tc::mbar_wait(&v_full[s], ph);
+                tc::tc_fence_after();
+                const uint32_t pa = tc::smem_u32(sP + s * kTile);
+                const uint32_t va = tc::smem_u32(sV + s * kTile);
+#pragma unroll
+                for (uint32_t kk = 0; kk < 8; ++kk) {
+                    const uint64_t adesc = tc::desc_k_sw128(pa + (kk >> 2) * kHalf + (kk & 3) * 32);
+                    const uint64_t bdesc = tc::desc_mn_sw128(va + kk * 2048, kHalf);
+                    tc::mma_bf16(tmem + 256, adesc, bdesc, idesc_o, (b > 0 || kk > 0) ? 1u : 0u);
+                }
+                tc::mma_commit(&v_empty[s]);
+                tc::mma_commit(o_full);
+                if (b + 2 < nb) issue_s(b + 2);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---- softmax / correction / epilogue: thread <-> query row (TMEM lane) ----
+        const uint32_t quarter = warp & 3;
+        const uint32_t r = quarter * 32 + lane;
+        const uint32_t qi = q0 + r;
+        const bool valid = qi < p.m;
+        const uint32_t limit = valid ? p.rows[qi] : 0u;
+        const uint32_t lane_base = (quarter * 32u) << 16;
+        float m_used = -INFINITY, l = 0.0f;
+        for (uint32_t b = 0; b < nb; ++b) {
+            const uint32_t s = b & 1;
+            const uint32_t j0 = (u.b0 + b) * 128u;
+            tc::mbar_wait(&s_full[s], (b >> 1) & 1);
+            tc::tc_fence_after();
+            const uint32_t sa = tmem + lane_base + s * 128;
+            // pass 1: masked row max (log2 domain)
+            float mx = -INFINITY;
+#pragma unroll
+            for (uint32_t c = 0; c < 8; ++c) {
+                uint32_t v[16];
+                tc::tmem_ld16(sa + c * 16, v);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (uint32_t e = 0; e < 16; ++e) {
+                    const uint32_t key = j0 + c * 16 + e;
+                    const float x = __uint_as_float(v[e]) * p.scale_log2;
+                    mx = key <= limit ? fmaxf(mx, x) : mx;
+                }
+            }
+            float alpha = 1.0f;
+            const bool grow = mx > m_used + kRescaleThreshold || (m_used == -INFINITY && mx > -INFINITY);
+            if (grow) {
+                alpha = m_used == -INFINITY ? 0.0f : exp2f(m_used - mx);
+                m_used = mx;
+                l *= alpha;
+            }
+            // PV_{b-1} (and everything before it) must be complete before O is rescaled
+            // and before P buffer (b&1) is overwritten (it was read by PV_{b-2}).
+            if (b > 0) {
+                tc::mbar_wait(o_full, (b - 1) & 1);
+                tc::tc_fence_after();
+                if (__any_sync(0xffffffffu, grow && alpha != 1.0f)) {
+                    const uint32_t oa = tmem + lane_base + 256;
+#pragma unroll
+                    for (uint32_t c = 0; c < 8; ++c) {
+                        uint32_t v[16];
+                        tc::tmem_ld16(oa + c * 16, v);
+                        tc::tmem_ld_wait();
+#pragma unroll
+                        for (uint32_t e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
+                        tc::tmem_st16(oa + c * 16, v);
+                    }
+                    tc::tmem_st_wait();
+                }
+            }
+            // pass 2: probabilities -> P (bf16, 128B-swizzled K-major rows)
+            uint8_t* prow = sP + s * kTile + r * 128;
+#pragma unroll
+            for (uint32_t c = 0; c < 8; ++c) {
+                uint32_t v[16];
+                tc::tmem_ld16(sa + c * 16, v);
+                tc::tmem_ld_wait();
+                float pv[16];
+#pragma unroll
+                for (uint32_t e = 0; e < 16; ++e) {
+                    const uint32_t key = j0 + c * 16 + e;
+                    const float x = __uint_as_float(v[e]) * p.scale_log2;
+                    pv[e] = (key <= limit && m_used != -INFINITY) ? exp2f(x - m_used) : 0.0f;
+                    l += pv[e];
+                }
+                // 16 keys = two 16-byte units; keys 64c' .. live in half (c >> 2)
+                const uint32_t half = c >> 2, unit0 = (c & 3) * 2;
+                uint8_t* base = prow + half * kHalf;
+#pragma unroll
+                for (uint32_t w = 0; w < 2; ++w) {
+                    const uint32_t unit = (unit0 + w) ^ (r & 7);
+                    uint4 q4;
+                    q4.x = pack_bf16(pv[8 * w + 0], pv[8 * w + 1]);
+                    q4.y = pack_bf16(pv[8 * w + 2], pv[8 * w + 3]);
+                    q4.z = pack_bf16(pv[8 * w + 4], pv[8 * w + 5]);
+                    q4.w = pack_bf16(pv[8 * w + 6], pv[8 * w + 7]);
+                    *reinterpret_cast<uint4*>(base + unit * 16) = q4;
+                }
+            }
+            tc::fence_async_shared();
+            tc::tc_fence_before();
+            tc::mbar_arrive(&p_full[s]);
+        }
+        // epilogue: O / l
+        tc::mbar_wait(o_full, (nb - 1) & 1);
+        tc::tc_fence_after();
+        const uint32_t oa = tmem + lane_base + 256;
+        const bool direct = u.slot == 0xffffffffu;
+        const float inv = l > 0.0f ? 1.0f / l : 0.0f;
+#pragma unroll
+        for (uint32_t c = 0; c < 8; ++c) {
+            uint32_t v[16];
+            tc::tmem_ld16(oa + c * 16, v);
+            tc::tmem_ld_wait();
+            if (!valid) continue;
+            if (direct) {
+                __nv_bfloat16* o = p.out + (size_t)qi * p.h + u.head * 128u + c * 16;
+                uint4 a, b2;
+                a.x = pack_bf16(__uint_as_float(v[0]) * inv, __uint_as_float(v[1]) * inv);
+                a.y = pack_bf16(__uint_as_float(v[2]) * inv, __uint_as_float(v[3]) * inv);
+                a.z = pack_bf16(__uint_as_float(v[4]) * inv, __uint_as_float(v[5]) * inv);
+                a.w = pack_bf16(__uint_as_float(v[6]) * inv, __uint_as_float(v[7]) * inv);
+                b2.x = pack_bf16(__uint_as_float(v[8]) * inv, __uint_as_float(v[9]) * inv);
+                b2.y = pack_bf16(__uint_as_float(v[10]) * inv, __uint_as_float(v[11]) * inv);
+                b2.z = pack_bf16(__uint_as_float(v[12]) * inv, __uint_as_float(v[13]) * inv);
+                b2.w = pack_bf16(__uint_as_float(v[14]) * inv, __uint_as_float(v[15]) * inv);
+                reinterpret_cast<uint4*>(o)[0] = a;
+                reinterpret_cast<uint4*>(o)[1] = b2;
+            } else {
+                float4* o = reinterpret_cast<float4*>(p.part_o + ((size_t)u.slot * 128 + r) * 128 + c * 16);
+#pragma unroll
+                for (uint32_t e = 0; e < 4; ++e)
+                    o[e] = make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]),
+                                       __uint_as_float(v[4 * e + 2]), __uint_as_float(v[4 * e + 3]));
+            }
+        }
+        if (valid && !direct) p.part_ml[(size_t)u.slot * 128 + r] = make_float2(m_used, l);
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+// Merge split partials of one (tile, head): O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s
+__global__ void __launch_bounds__(128) attn_combine_kernel(const AttnCombine* __restrict__ jobs,
+                                                           const float* __restrict__ part_o,
+                                                           const float2* __restrict__ part_ml,
+                                                           uint32_t m, uint32_t h,
+                                                           __nv_bfloat16* __restrict__ out) {
+    const AttnCombine j = jobs[blockIdx.x];
+    const uint32_t r = threadIdx.x;
+    const uint32_t qi = j.tile * 128u + r;
+    if (qi >= m) return;
+    float M = -INFINITY;
+    for (uint32_t s = 0; s < j.n; ++s) M = fmaxf(M, part_ml[(size_t)(j.slot0 + s) * 128 + r].x);
+    float L = 0.0f;
+    for (uint32_t s = 0; s < j.n; ++s) {
+        const float2 ml = part_ml[(size_t)(j.slot0 + s) * 128 + r];
+        L += (ml.x == -INFINITY ? 0.0f : exp2f(ml.x - M)) * ml.y;
+    }
+    const float inv = L > 0.0f ? 1.0f / L : 0.0f;
+    __nv_bfloat16* o = out + (size_t)qi * h + j.head * 128u;
+    for (uint32_t d = 0; d < 128; d += 4) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (uint32_t s = 0; s < j.n; ++s) {
+            const float mls = part_ml[(size_t)(j.slot0 + s) * 128 + r].x;
+            const float ws = mls == -INFINITY ? 0.0f : exp2f(mls - M);
+            if (ws == 0.0f) continue;
+            const float4 v = *reinterpret_cast<const float4*>(part_o + ((size_t)(j.slot0 + s) * 128 + r) * 128 + d);
+            acc.x += ws * v.x;
+            acc.y += ws * v.y;
+            acc.z += ws * v.z;
+            acc.w += ws * v.w;
+        }
+        o[d] = __float2bfloat16_rn(acc.x * inv);
+        o[d + 1] = __float2bfloat16_rn(acc.y * inv);
+        o[d + 2] = __float2bfloat16_rn(acc.z * inv);
+        o[d + 3] = __float2bfloat16_rn(acc.w * inv);
+    }
+}
+
+}  // namespace
+
+// Host: split every (query tile, head) key range into units of at most `chunk` blocks.
+AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads) {
+    AttnPlan plan;
+    const uint32_t tiles = ceil_div(m, 128);
+    std::vector<uint32_t> nblk(tiles);
+    uint64_t total = 0;
+    for (uint32_t t = 0; t < tiles; ++t) {
+        const uint32_t last = std::min(m, (t + 1) * 128) - 1;
+        nblk[t] = rows[last] / 128 + 1;
+        total += (uint64_t)nblk[t] * n_heads;
+    }
+    // ~3 waves of units; never split below 2 blocks per unit
+    uint32_t chunk = (uint32_t)std::max<uint64_t>(2, (total + 3 * kNumSMs - 1) / (3 * kNumSMs));
+    uint32_t slot = 0;
+    for (uint32_t t = 0; t < tiles; ++t) {
+        const uint32_t splits = ceil_div(nblk[t], chunk);
+        for (uint32_t hd = 0; hd < n_heads; ++hd) {
+            if (splits > 1) plan.combine.push_back(AttnCombine{t, hd, slot, splits});
+            for (uint32_t sp = 0; sp < splits; ++sp) {
+                AttnUnit u;
+                u.tile = t;
+                u.head = hd;
+                u.b0 = sp * chunk;
+                u.b1 = std::min(nblk[t], (sp + 1) * chunk);
+                u.slot = splits > 1 ? slot + sp : 0xffffffffu;
+                plan.units.push_back(u);
+            }
+            if (splits > 1) slot += splits;
+        }
+    }
+    plan.slots = slot;
+    // longest units first (they set the critical path)
+    std::stable_sort(plan.units.begin(), plan.units.end(),
+                     [](const AttnUnit& a, const AttnUnit& b) { return a.b1 - a.b0 > b.b1 - b.b0; });
+    return plan;
+}
+
+void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const __nv_bfloat16* vcache,
+                    uint32_t n_ctx, const uint32_t* d_rows, uint32_t m, uint32_t H,
+                    const AttnUnit* d_units, uint32_t n_units, const AttnCombine* d_combine,
+                    uint32_t n_combine, float* part_o, float2* part_ml, __nv_bfloat16* out,
+                    cudaStream_t s) {
+    const uint32_t h = H * 128;
+    const CUtensorMap tmQ = make_tmap_bf16(q, h, m, 64, 128);
+    const CUtensorMap tmK = make_tmap_bf16(kcache, h, n_ctx, 64, 128);
+    const CUtensorMap tmV = make_tmap_bf16(vcache, h, n_ctx, 64, 128);
+    AttnParams p;
+    p.units = d_units;
+    p.rows = d_rows;
+    p.m = m;
+    p.h = h;
+    p.scale_log2 = (1.0f / sqrtf(128.0f)) * 1.4426950408889634f;
+    p.out = out;
+    p.part_o = part_o;
+    p.part_ml = part_ml;
+    const size_t smem = 7 * kTile + 1024 + 256;
+    static bool attr = false;
+    if (!attr) {
+        MPIC_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    attn_tc_kernel<<<n_units, kAttnThreads, smem, s>>>(tmQ, tmK, tmV, p);
+    MPIC_LAUNCHED();
+    if (n_combine) {
+        attn_combine_kernel<<<n_combine, 128, 0, s>>>(d_combine, part_o, part_ml, m, h, out);
+        MPIC_LAUNCHED();
+    }
+}
+
+}  // namespace mpicb

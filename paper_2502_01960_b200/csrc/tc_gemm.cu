@@ -37,7 +37,8 @@ constexpr uint32_t kXBoxBytes = kXBoxRows * 64 * 2;  // 16 KB
 struct TcGemmArgs {
     uint32_t M, N, K;
     uint32_t tt;            // token columns per CTA (multiple of 16, <= 512)
-    uint32_t x_boxes;       // 128-row TMA boxes per stage for X
+    uint32_t xr;            // X rows loaded (and multicast) by each CTA of the cluster
+    uint32_t cl;            // cluster size along the feature-tile axis (1, 2 or 4)
     uint32_t kb_per_split;  // 64-wide K blocks per CTA
     uint32_t stages;
     uint32_t tmem_cols;
@@ -45,28 +46,17 @@ struct TcGemmArgs {
 };
 
 template <typename TO>
-__device__ __forceinline__ void tc_epilogue(const EpiParams& ep, uint32_t t, uint32_t f, float v,
-                                            uint32_t lane) {
+__device__ __forceinline__ void tc_epilogue(const EpiParams& ep, uint32_t t, uint32_t f, float v) {
     switch (ep.mode) {
-        case EPI_QKV: {
-            const uint32_t h = ep.hidden;
-            const uint32_t part = f / h, c = f - part * h;  // warp-uniform (h % 32 == 0)
-            const float vp = __shfl_xor_sync(0xffffffffu, v, 1);
-            if (part < 2) {
-                const float2 cs = ep.rope[(size_t)ep.rope_pos[t] * (ep.head_dim >> 1) + ((c % ep.head_dim) >> 1)];
-                float x0 = (lane & 1) ? vp : v, x1 = (lane & 1) ? v : vp;
-                rope_pair(x0, x1, cs.x, cs.y);
-                v = (lane & 1) ? x1 : x0;
-            }
-            TO* dst = part == 0 ? static_cast<TO*>(ep.q) + (size_t)t * h + c
-                                : static_cast<TO*>(part == 1 ? ep.kv_k : ep.kv_v) + (size_t)ep.kv_rows[t] * h + c;
-            *dst = from_f32<TO>(v);
-            break;
-        }
         case EPI_RESID: {
-            float* x = ep.x + (size_t)t * ep.ldx + f;
-            if (ep.split_k > 1) atomicAdd(x, v);
-            else *x += v;
+            if (ep.split_k > 1) {  // deterministic split-K: partial tile, reduced afterwards
+                ep.partial[((size_t)blockIdx.z * ep.rows_total + t) * ep.ldx + f] = v;
+            } else {
+                float* x = ep.x + (size_t)t * ep.ldx + f;
+                const float nv = *x + v;
+                *x = nv;
+                if (ep.xb) ep.xb[(size_t)t * ep.ldx + f] = __float2bfloat16_rn(nv);
+            }
             break;
         }
         case EPI_GELU:
@@ -85,7 +75,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                    const TcGemmArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t stage_bytes = kWTileBytes + a.x_boxes * kXBoxBytes;
+    const uint32_t x_bytes = a.cl * a.xr * 128;
+    const uint32_t stage_bytes = kWTileBytes + x_bytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
     uint64_t* empty = full + a.stages;
     uint64_t* tmem_full = empty + a.stages;
@@ -94,27 +85,30 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t n0 = blockIdx.x * 128, t0 = blockIdx.y * a.tt;
     const uint32_t kb0 = blockIdx.z * a.kb_per_split;
+    const uint32_t rank = a.cl > 1 ? tc::cluster_ctarank() : 0;
+    const uint16_t mask = (uint16_t)((1u << a.cl) - 1);
 
     if (warp == 0 && lane == 0) {
         tc::tma_prefetch_desc(&tmW);
         tc::tma_prefetch_desc(&tmX);
         for (uint32_t s = 0; s < a.stages; ++s) {
             tc::mbar_init(&full[s], 1);
-            tc::mbar_init(&empty[s], 1);
+            tc::mbar_init(&empty[s], a.cl);  // every CTA's MMA must release a multicast stage
         }
         tc::mbar_init(tmem_full, 1);
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc(tmem_holder, a.tmem_cols);
     tc::tc_fence_before();
-    __syncthreads();
+    if (a.cl > 1) tc::cluster_sync();  // peers' barriers are initialised before any multicast
+    else __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
 
     if (warp == 0) {
         if (lane == 0) {
             const uint64_t pol_w = tc::policy_evict_first();  // weights stream through once
-            const uint64_t pol_x = tc::policy_evict_last();   // token tile re-read by every CTA
+            const uint64_t pol_x = tc::policy_evict_last();   // token tile re-read by every cluster
             for (uint32_t i = 0; i < a.kb_per_split; ++i) {
                 const uint32_t s = i % a.stages, ph = (i / a.stages) & 1;
                 tc::mbar_wait(&empty[s], ph ^ 1);
@@ -122,9 +116,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const int k = (int)((kb0 + i) * 64);
                 uint8_t* st = smem + s * stage_bytes;
                 tc::tma_load_2d_hint(st, &tmW, &full[s], k, (int)n0, pol_w);
-                for (uint32_t b = 0; b < a.x_boxes; ++b)
-                    tc::tma_load_2d_hint(st + kWTileBytes + b * kXBoxBytes, &tmX, &full[s], k,
-                                         (int)(t0 + b * kXBoxRows), pol_x);
+                uint8_t* xs = st + kWTileBytes + rank * a.xr * 128;
+                const int row = (int)(t0 + rank * a.xr);
+                if (a.cl > 1) tc::tma_load_2d_mcast(xs, &tmX, &full[s], k, row, mask, pol_x);
+                else tc::tma_load_2d_hint(xs, &tmX, &full[s], k, row, pol_x);
             }
         }
         __syncwarp();
@@ -146,7 +141,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                                      (i > 0 || kk > 0) ? 1u : 0u);
                     }
                 }
-                tc::mma_commit(&empty[s]);
+                if (a.cl > 1) tc::mma_commit_mcast(&empty[s], mask);
+                else tc::mma_commit(&empty[s]);
             }
             tc::mma_commit(tmem_full);
         }
@@ -157,21 +153,81 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t f = n0 + q * 32 + lane;
         tc::mbar_wait(tmem_full, 0);
         tc::tc_fence_after();
+        const bool qkv = a.ep.mode == EPI_QKV;
+        const uint32_t part = qkv ? f / a.ep.hidden : 0;  // warp-uniform (hidden % 128 == 0)
+        const uint32_t pair = qkv ? ((f - part * a.ep.hidden) % a.ep.head_dim) >> 1 : 0;
         for (uint32_t c = 0; c < a.tt; c += 16) {
             uint32_t r[16];
             tc::tmem_ld16(tmem_base + ((q * 32u) << 16) + c, r);
-            tc::tmem_ld_wait();
+            if (qkv) {
+                // issue every per-token load of this chunk before the first store
+                uint32_t dst_row[16];
+                float2 cs[16];
 #pragma unroll
-            for (uint32_t j = 0; j < 16; ++j) {
-                const uint32_t t = t0 + c + j;
-                if (t < a.M) tc_epilogue<__nv_bfloat16>(a.ep, t, f, __uint_as_float(r[j]), lane);
+                for (uint32_t j = 0; j < 16; ++j) {
+                    const uint32_t t = min(t0 + c + j, a.M - 1);
+                    dst_row[j] = part == 0 ? t : __ldg(a.ep.kv_rows + t);
+                    cs[j] = part < 2 ? __ldg(a.ep.rope + (size_t)__ldg(a.ep.rope_pos + t) * (a.ep.head_dim >> 1) + pair)
+                                     : make_float2(1.f, 0.f);
+                }
+                tc::tmem_ld_wait();
+                __nv_bfloat16* base = static_cast<__nv_bfloat16*>(part == 0 ? a.ep.q : part == 1 ? a.ep.kv_k : a.ep.kv_v) +
+                                      (f - part * a.ep.hidden);
+#pragma unroll
+                for (uint32_t j = 0; j < 16; ++j) {
+                    float v = __uint_as_float(r[j]);
+                    const float vp = __shfl_xor_sync(0xffffffffu, v, 1);
+                    if (part < 2) {
+                        float x0 = (lane & 1) ? vp : v, x1 = (lane & 1) ? v : vp;
+                        rope_pair(x0, x1, cs[j].x, cs[j].y);
+                        v = (lane & 1) ? x1 : x0;
+                    }
+                    if (t0 + c + j < a.M) base[(size_t)dst_row[j] * a.ep.hidden] = __float2bfloat16_rn(v);
+                }
+            } else {
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (uint32_t j = 0; j < 16; ++j) {
+                    const uint32_t t = t0 + c + j;
+                    if (t < a.M) tc_epilogue<__nv_bfloat16>(a.ep, t, f, __uint_as_float(r[j]));
+                }
             }
         }
     }
     tc::tc_fence_before();
-    __syncthreads();
+    if (a.cl > 1) tc::cluster_sync();  // no CTA exits while peers may still signal its barriers
+    else __syncthreads();
     tc::tc_fence_after();
     if (warp == 1) tc::tmem_dealloc(tmem_base, a.tmem_cols);
+}
+
+// x += sum_z partial[z]; xb = bf16(x) — the deterministic split-K reduction, fused with
+// the cast that produces the next GEMM's bf16 operand.
+__global__ void __launch_bounds__(256) resid_reduce_kernel(const float* __restrict__ partial,
+                                                           uint32_t split, size_t plane,
+                                                           float* __restrict__ x,
+                                                           __nv_bfloat16* __restrict__ xb,
+                                                           size_t n4) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
+         i += (size_t)gridDim.x * blockDim.x) {
+        float4 acc = reinterpret_cast<const float4*>(x)[i];
+        for (uint32_t z = 0; z < split; ++z) {
+            const float4 p = __ldcs(reinterpret_cast<const float4*>(partial + z * plane) + i);
+            acc.x += p.x;
+            acc.y += p.y;
+            acc.z += p.z;
+            acc.w += p.w;
+        }
+        reinterpret_cast<float4*>(x)[i] = acc;
+        if (xb) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z, acc.w);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&lo);
+            pk.y = *reinterpret_cast<uint32_t*>(&hi);
+            reinterpret_cast<uint2*>(xb)[i] = pk;
+        }
+    }
 }
 
 // ---- host side ----------------------------------------------------------------------
@@ -249,22 +305,16 @@ void launch_gemm_tc(const __nv_bfloat16* A, uint32_t lda, const __nv_bfloat16* W
     a.K = K;
     a.tt = M <= 512 ? (M + 15) / 16 * 16 : 256;
     const uint32_t tiles_t = ceil_div(M, a.tt);
-    a.x_boxes = ceil_div(a.tt, kXBoxRows);
-    const uint32_t stage_bytes = kWTileBytes + a.x_boxes * kXBoxBytes;
-    const uint32_t budget = 227 * 1024 - 1024 - 256;
-    a.stages = std::min<uint32_t>(8, budget / stage_bytes);
-    MPIC_REQUIRE(a.stages >= 2, MPIC_ERR_VALIDATION, "tc gemm tile does not fit shared memory");
-    a.tmem_cols = 32;
-    while (a.tmem_cols < a.tt) a.tmem_cols *= 2;
+    const uint32_t ntiles = N / 128;
     const uint32_t kblocks = K / 64;
-    const uint32_t tiles = (N / 128) * tiles_t;
+    // split-K (residual epilogues only, into a partial buffer) to fill the SMs
     uint32_t split = 1;
-    if (ep_in.mode == EPI_RESID) {
-        // pick the split with the best wave efficiency (ties -> fewer splits)
+    if (ep_in.mode == EPI_RESID && ep_in.partial) {
         double best = 0.0;
-        for (uint32_t sp = 1; sp <= 16; sp *= 2) {
+        for (uint32_t sp = 1; sp <= 8; sp *= 2) {
             if (kblocks % sp || kblocks / sp < 4) break;
-            const uint32_t ctas = tiles * sp;
+            if ((size_t)sp * M * N > ep_in.partial_cap) break;
+            const uint32_t ctas = ntiles * tiles_t * sp;
             const double eff = (double)ctas / (kNumSMs * ceil_div(ctas, kNumSMs));
             const double score = std::min(1.0, (double)ctas / kNumSMs) * eff;
             if (score > best + 1e-9) {
@@ -273,20 +323,50 @@ void launch_gemm_tc(const __nv_bfloat16* A, uint32_t lda, const __nv_bfloat16* W
             }
         }
     }
+    // cluster multicast of the token tile: 4 CTAs share it when they fit in one wave
+    // (4-CTA clusters strand a few SMs per GPC), else 2.
+    const uint32_t ctas = ntiles * tiles_t * split;
+    a.cl = (ntiles % 4 == 0 && ctas <= 132) ? 4 : (ntiles % 2 == 0 ? 2 : 1);
+    a.xr = (ceil_div(a.tt, a.cl) + 7) / 8 * 8;
+    const uint32_t stage_bytes = kWTileBytes + a.cl * a.xr * 128;
+    const uint32_t budget = 227 * 1024 - 1024 - 256;
+    a.stages = std::min<uint32_t>(8, budget / stage_bytes);
+    MPIC_REQUIRE(a.stages >= 2, MPIC_ERR_VALIDATION, "tc gemm tile does not fit shared memory");
+    a.tmem_cols = 32;
+    while (a.tmem_cols < a.tt) a.tmem_cols *= 2;
     a.kb_per_split = kblocks / split;
     a.ep = ep_in;
     a.ep.split_k = split;
+    a.ep.rows_total = M;
     const CUtensorMap tmW = make_tmap_bf16(W, K, N, 64, 128);
     // Rows >= M are out of bounds for the map: TMA zero-fills them.
-    const CUtensorMap tmX = make_tmap_bf16(A, K, M, 64, kXBoxRows);
+    const CUtensorMap tmX = make_tmap_bf16(A, K, M, 64, a.xr);
     const size_t smem = (size_t)a.stages * stage_bytes + 1024 + (2 * a.stages + 1) * 8 + 16;
     static std::once_flag once;
     std::call_once(once, [] {
         MPIC_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        MPIC_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     });
-    dim3 grid(N / 128, tiles_t, split);
-    tc_gemm_kernel<<<grid, kTcThreads, smem, s>>>(tmW, tmX, a);
-    MPIC_LAUNCHED();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles, tiles_t, split);
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = a.cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MPIC_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel, tmW, tmX, a));
+    note_launch();
+    if (split > 1) {
+        const size_t n4 = (size_t)M * N / 4;
+        resid_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(ep_in.partial, split, (size_t)M * N, ep_in.x,
+                                                         ep_in.xb, n4);
+        MPIC_LAUNCHED();
+    }
 }
 
 }  // namespace mpicb

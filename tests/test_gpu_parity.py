@@ -244,3 +244,45 @@ def test_config_a96(dtype):
         k, v = linked.download()
         assert hashlib.sha256(k.tobytes()).digest() == ga["a.as.asm_sha_k"].tobytes()
         assert hashlib.sha256(v.tobytes()).digest() == ga["a.as.asm_sha_v"].tobytes()
+
+
+@pytest.mark.parametrize("layout,policy", [
+    ([("t", 40), ("i", 300), ("t", 50), ("i", 260), ("t", 30)], mp.POLICY_MPIC_K),
+    ([("t", 40), ("i", 300), ("t", 50), ("i", 260), ("t", 30)], mp.POLICY_ALL),
+    ([("t", 40), ("i", 1400), ("t", 20), ("i", 1500), ("t", 30)], mp.POLICY_MPIC_K),
+])
+def test_head_dim_128_bf16_vs_oracle(layout, policy):
+    """head_dim 128 takes the tcgen05 attention (and tcgen05 GEMMs) in bf16 mode; checked
+    against the plain-C oracle on the same seeded chunks (max rel <= 1e-2)."""
+    from helpers import rand_hash
+    L, H, D, V = 2, 4, 128, 4096
+    cfg_o = oracle.Config(L, H, D, H * D, V, 64, 10000.0, 3)
+    cfg = mp.config(L, H, D, vocab_size=V, image_token_count=64, seed=3)
+    o = oracle.OracleC()
+    om = o.model(cfg_o)
+    rng = np.random.default_rng(len(layout) * 1000 + policy)
+    segs = []
+    for kind, ln in layout:
+        segs.append(("text", rng.integers(0, V - 1, ln).tolist()) if kind == "t"
+                    else ("image", rand_hash(rng), ln))
+    po = oracle.make_prompt(segs)
+    for kind, ln in layout:
+        if kind == "i":
+            po.chunk_k.append((rng.random((L, ln, H * D), dtype=np.float32) - 0.5))
+            po.chunk_v.append((rng.random((L, ln, H * D), dtype=np.float32) - 0.5))
+            po.chunk_base.append(0)
+    sel = o.select(po, policy, 32)
+    ak, av = o.assemble(cfg_o, po, False)
+    rk, rv, ref_logits = om.selective(cfg_o, po, sel, ak, av)
+
+    m = mp.Model(cfg, mp.BF16)
+    ws = mp.Workspace(m, len(sel))
+    p = mp.Prompt.from_segments(segs)
+    kvs = [mp.KV.from_host(k, v, H, D, mp.BF16) for k, v in zip(po.chunk_k, po.chunk_v)]
+    linked = mp.KV(L, p.n, H, D, mp.BF16)
+    logits, got = mp.request_prefill(m, ws, p, kvs, linked, policy=policy, k=32)
+    assert np.array_equal(got, sel)
+    assert rel_err(logits, ref_logits) < 1e-2, rel_err(logits, ref_logits)
+    k, v = linked.download()
+    assert rel_err(k[-1][sel], rk[-1][sel]) < 1e-2
+    assert rel_err(v[-1][sel], rv[-1][sel]) < 1e-2
