@@ -2,8 +2,8 @@
  *
  * This is the drop-in boundary: plain C types, plain pointers and sizes, explicit CUDA
  * streams (passed as void*, i.e. a cudaStream_t), no C++ or torch types, no exceptions.
- * The C++ host library (include/mpic/*.h, same API as the reference's
- * proj/include/mpic/*.h) sits on top of it; a cgo / JNI / ctypes binding would bind
+ * The C++ host library (include/mpic/ headers, same API as the reference
+ * proj/include/mpic headers) sits on top of it; a cgo / JNI / ctypes binding would bind
  * exactly these symbols.
  *
  * Every call returns an mpic_status; codes map 1:1 onto the reference's exception
@@ -144,6 +144,17 @@ int mpic_selective_prefill(mpic_model_t model, mpic_workspace_t ws, const int32_
 int mpic_prefill_extend(mpic_model_t model, mpic_workspace_t ws, const int32_t* ids, uint32_t m,
                         uint32_t start, uint32_t position_base, mpic_kv_t kv, float* logits,
                         void* stream);
+/* General host form behind both: ids/rows/rope_pos are host arrays. Optional outputs:
+ * hidden_out [m][hidden_dim] final-layer hidden rows (mean_pooled_hidden, model.cpp:369-389);
+ * attn_capture [L][H][T][T] normalised attention of each recomputed row at query index
+ * rows[i] (AttentionDump, model.h:50-71; fp32 models only; other rows left zero). */
+int mpic_forward_rows(mpic_model_t model, mpic_workspace_t ws, const int32_t* ids,
+                      const uint32_t* rows, const uint32_t* rope_pos, uint32_t m, mpic_kv_t kv,
+                      float* logits, float* hidden_out, float* attn_capture, void* stream);
+/* Layer-0 keys of `ids` rotated at `positions`, out [m][hidden_dim] fp32 (the CacheBlend
+ * deviation probe, proj/src/linker.cpp:485-499). Synchronous. */
+int mpic_layer0_keys(mpic_model_t model, mpic_workspace_t ws, const int32_t* ids,
+                     const uint32_t* positions, uint32_t m, float* out, void* stream);
 /* Fully asynchronous form of both: every pointer is a DEVICE pointer, ids are assumed
  * in-vocabulary (the host forms validate), max_pos >= every row and rotary position,
  * logits land in d_logits on `stream`. */
@@ -203,6 +214,11 @@ int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpi
                               const float* const* chunk_v, const uint32_t* position_bases,
                               mpic_reposition reposition, mpic_kv_t linked, float* logits,
                               uint32_t* selected, uint32_t* m_out, void* stream);
+
+/* Host-pointer fp32 GEMM on the device: c[M][N] = a[M][K] . b[N][K]^T (SIMT FFMA). Backs the
+ * reference's gemm_nt/gemm_nn shims (proj/include/mpic/matmul.h:11-21). Synchronous. */
+int mpic_host_gemm_f32(const float* a, const float* b, uint32_t M, uint32_t N, uint32_t K, float* c,
+                       int device);
 
 /* Pinned host memory for chunk staging (cudaMallocHost); mpic_host_free releases it. */
 int mpic_host_alloc(size_t bytes, void** out);

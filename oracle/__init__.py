@@ -393,6 +393,9 @@ def build_oracle(with_ref: bool | None = None) -> None:
         with_ref = os.path.isdir("/root/reference/proj/src")
     if with_ref:
         targets += ["ref", "reftests"]
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_2502_01960_b200", "lib",
+                                       "libmpic_b200.so")):
+            targets.append("conformance")
     subprocess.run(["make", "-s", "-C", HERE, "-j8", *targets], check=True)
 
 

@@ -83,6 +83,8 @@ SIGNATURES = {
     "mpic_workspace_destroy": (_int, [_vp]),
     "mpic_selective_prefill": (_int, [_vp, _vp, _vp, _vp, _u32, _vp, _vp, _vp]),
     "mpic_prefill_extend": (_int, [_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _vp]),
+    "mpic_forward_rows": (_int, [_vp, _vp, _vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp]),
+    "mpic_layer0_keys": (_int, [_vp, _vp, _vp, _vp, _u32, _vp, _vp]),
     "mpic_forward_rows_async": (_int, [_vp, _vp, _vp, _vp, _vp, _u32, _u32, _vp, _vp, _vp]),
     "mpic_image_token_ids": (_int, [_P(ModelConfig), _vp, _u32, _vp]),
     "mpic_select_tokens": (_int, [_P(PromptDesc), _P(PolicyDesc), _vp, _P(_u32)]),
@@ -94,6 +96,7 @@ SIGNATURES = {
     "mpic_test_gemm": (_int, [_vp, _vp, _u32, _u32, _u32, _int, _vp, _vp]),
     "mpic_profile_enable": (_int, [_int]),
     "mpic_profile_collect": (_int, [_vp, _vp]),
+    "mpic_host_gemm_f32": (_int, [_vp, _vp, _u32, _u32, _u32, _vp, _int]),
     "mpic_host_alloc": (_int, [C.c_size_t, _P(_vp)]),
     "mpic_host_free": (_int, [_vp]),
 }

@@ -1,0 +1,211 @@
+// Host pieces of the mpic:: API: config, hashing, KvTensor, the GEMM shims, and the glue
+// to the C ABI (device.h).
+#include "device.h"
+
+#include "mpic/config.h"
+#include "mpic/hash.h"
+#include "mpic/matmul.h"
+#include "mpic/tensor.h"
+
+#include <openssl/evp.h>
+#include <zlib.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+namespace mpic {
+
+// ---- config (proj/src/config.cpp:12-47 semantics) -------------------------------------
+void ModelConfig::validate() const {
+    const mpic_model_config c = b200::to_c(*this);
+    b200::check(mpic_config_validate(&c));
+}
+
+uint64_t ModelConfig::fingerprint() const {
+    const mpic_model_config c = b200::to_c(*this);
+    return mpic_config_fingerprint(&c);
+}
+
+// ---- hashing --------------------------------------------------------------------------
+Hash256 sha256(std::span<const uint8_t> bytes) {
+    Hash256 out{};
+    unsigned int n = 0;
+    EVP_MD_CTX* ctx = EVP_MD_CTX_new();
+    const bool ok = ctx && EVP_DigestInit_ex(ctx, EVP_sha256(), nullptr) == 1 &&
+                    EVP_DigestUpdate(ctx, bytes.data(), bytes.size()) == 1 &&
+                    EVP_DigestFinal_ex(ctx, out.data(), &n) == 1 && n == out.size();
+    EVP_MD_CTX_free(ctx);
+    if (!ok) throw io_error("sha256 failed");
+    return out;
+}
+
+std::string hash_to_hex(const Hash256& h) {
+    static constexpr char kHex[] = "0123456789abcdef";
+    std::string s(64, '0');
+    for (size_t i = 0; i < h.size(); ++i) {
+        s[2 * i] = kHex[h[i] >> 4];
+        s[2 * i + 1] = kHex[h[i] & 15];
+    }
+    return s;
+}
+
+Hash256 hash_from_hex(std::string_view hex) {
+    if (hex.size() != 64) throw validation_error("content hash must be 64 hex characters");
+    auto val = [](char c) -> int {
+        if (c >= '0' && c <= '9') return c - '0';
+        if (c >= 'a' && c <= 'f') return c - 'a' + 10;
+        if (c >= 'A' && c <= 'F') return c - 'A' + 10;
+        return -1;
+    };
+    Hash256 h{};
+    for (size_t i = 0; i < 32; ++i) {
+        const int hi = val(hex[2 * i]), lo = val(hex[2 * i + 1]);
+        if (hi < 0 || lo < 0) throw validation_error("content hash contains non-hex characters");
+        h[i] = static_cast<uint8_t>(hi * 16 + lo);
+    }
+    return h;
+}
+
+uint32_t crc32_of(std::span<const uint8_t> bytes) {
+    uLong c = crc32(0L, Z_NULL, 0);
+    // zlib takes 32-bit lengths: feed large payloads in pieces
+    size_t off = 0;
+    while (off < bytes.size()) {
+        const size_t n = std::min<size_t>(bytes.size() - off, size_t(1) << 30);
+        c = crc32(c, bytes.data() + off, static_cast<uInt>(n));
+        off += n;
+    }
+    return static_cast<uint32_t>(c);
+}
+
+// ---- KvTensor -------------------------------------------------------------------------
+void KvTensor::resize_tokens(uint32_t new_tokens) {
+    if (new_tokens == n_tokens) return;
+    const size_t row = row_size();
+    const size_t keep = size_t(std::min(n_tokens, new_tokens)) * row;
+    std::vector<float> nk(size_t(n_layers) * new_tokens * row, 0.0f), nv(nk.size(), 0.0f);
+    for (uint32_t l = 0; l < n_layers; ++l) {
+        std::copy_n(k.data() + size_t(l) * n_tokens * row, keep, nk.data() + size_t(l) * new_tokens * row);
+        std::copy_n(v.data() + size_t(l) * n_tokens * row, keep, nv.data() + size_t(l) * new_tokens * row);
+    }
+    k.swap(nk);
+    v.swap(nv);
+    n_tokens = new_tokens;
+}
+
+bool KvTensor::all_finite() const {
+    auto fin = [](const std::vector<float>& a) {
+        return std::all_of(a.begin(), a.end(), [](float x) { return std::isfinite(x); });
+    };
+    return fin(k) && fin(v);
+}
+
+// ---- GEMM shims (run on the device, fp32 SIMT) ----------------------------------------
+namespace {
+int g_threads = 0;
+
+void device_gemm_nt(int m, int n, int k, const float* a, int lda, const float* b, int ldb, float* c,
+                    int ldc) {
+    if (m <= 0 || n <= 0) return;
+    if (k <= 0) {
+        for (int i = 0; i < m; ++i) std::fill_n(c + size_t(i) * ldc, n, 0.0f);
+        return;
+    }
+    std::vector<float> A(size_t(m) * k), B(size_t(n) * k), Cm(size_t(m) * n);
+    for (int i = 0; i < m; ++i) std::copy_n(a + size_t(i) * lda, k, A.data() + size_t(i) * k);
+    for (int j = 0; j < n; ++j) std::copy_n(b + size_t(j) * ldb, k, B.data() + size_t(j) * k);
+    b200::check(mpic_host_gemm_f32(A.data(), B.data(), uint32_t(m), uint32_t(n), uint32_t(k), Cm.data(),
+                                   b200::device()));
+    for (int i = 0; i < m; ++i) std::copy_n(Cm.data() + size_t(i) * n, n, c + size_t(i) * ldc);
+}
+}  // namespace
+
+void gemm_nt(int m, int n, int k, const float* a, int lda, const float* b, int ldb, float* c, int ldc) {
+    device_gemm_nt(m, n, k, a, lda, b, ldb, c, ldc);
+}
+
+void gemm_nn(int m, int n, int k, const float* a, int lda, const float* b, int ldb, float* c, int ldc) {
+    std::vector<float> bt(size_t(n) * std::max(k, 1));  // B[k x n] -> B^T[n x k]
+    for (int r = 0; r < k; ++r)
+        for (int j = 0; j < n; ++j) bt[size_t(j) * k + r] = b[size_t(r) * ldb + j];
+    device_gemm_nt(m, n, k, a, lda, bt.data(), k, c, ldc);
+}
+
+void set_compute_threads(int n) { g_threads = n; }
+
+}  // namespace mpic
+
+namespace mpic::b200 {
+
+void check(int rc) {
+    if (rc == MPIC_OK) return;
+    const std::string msg = mpic_last_error();
+    switch (rc) {
+        case MPIC_ERR_CONFIG: throw config_error(msg);
+        case MPIC_ERR_VALIDATION: throw validation_error(msg);
+        case MPIC_ERR_STATE: throw state_error(msg);
+        case MPIC_ERR_LINK: throw link_error(msg);
+        case MPIC_ERR_CONTRACT: throw contract_error(msg);
+        case MPIC_ERR_FORMAT: throw format_error(msg);
+        case MPIC_ERR_INTEGRITY: throw integrity_error(msg);
+        case MPIC_ERR_IO: throw io_error(msg);
+        case MPIC_ERR_NOT_FOUND: throw not_found_error(msg);
+        case MPIC_ERR_REQUEST: throw request_error(msg);
+        default: throw error("B200 runtime: " + msg);
+    }
+}
+
+int device() {
+    static const int dev = [] {
+        const char* e = std::getenv("MPIC_DEVICE");
+        return e ? std::atoi(e) : 0;
+    }();
+    return dev;
+}
+
+mpic_model_config to_c(const ModelConfig& c) {
+    mpic_model_config o{};
+    o.n_layers = c.n_layers;
+    o.n_heads = c.n_heads;
+    o.head_dim = c.head_dim;
+    o.hidden_dim = c.hidden_dim;
+    o.vocab_size = c.vocab_size;
+    o.image_token_count = c.image_token_count;
+    o.rope_base = c.rope_base;
+    o.seed = c.seed;
+    return o;
+}
+
+DeviceModel::DeviceModel(const Model& m) {
+    const mpic_model_config c = to_c(m.config);
+    std::vector<const float*> lw;
+    lw.reserve(6 * m.layers.size());
+    for (const LayerWeights& l : m.layers)
+        for (const std::vector<float>* w : {&l.wq, &l.wk, &l.wv, &l.wo, &l.w1, &l.w2}) lw.push_back(w->data());
+    check(mpic_model_upload(&c, device(), MPIC_F32, m.embedding.data(), m.lm_head.data(), lw.data(), &h_));
+}
+DeviceModel::~DeviceModel() { mpic_model_destroy(h_); }
+
+DeviceKv::DeviceKv(uint32_t layers, uint32_t tokens, uint32_t heads, uint32_t dim) {
+    check(mpic_kv_alloc(layers, tokens, heads, dim, MPIC_F32, device(), &h_));
+}
+DeviceKv::DeviceKv(const KvTensor& t) : DeviceKv(t.n_layers, t.n_tokens, t.n_heads, t.head_dim) {
+    upload(t);
+}
+DeviceKv::~DeviceKv() { mpic_kv_free(h_); }
+void DeviceKv::upload(const KvTensor& t) {
+    if (!t.k.empty()) check(mpic_kv_upload(h_, t.k.data(), t.v.data(), nullptr));
+}
+void DeviceKv::download(KvTensor& t) const {
+    if (!t.k.empty()) check(mpic_kv_download(h_, t.k.data(), t.v.data(), nullptr));
+}
+
+Workspace::Workspace(const DeviceModel& m, uint32_t rows, uint32_t ctx) {
+    check(mpic_workspace_create(m.get(), std::max(rows, 1u), ctx, &h_));
+}
+Workspace::~Workspace() { mpic_workspace_destroy(h_); }
+
+}  // namespace mpic::b200

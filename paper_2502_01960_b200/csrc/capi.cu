@@ -364,7 +364,7 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
                   const uint32_t* d_rows, const uint32_t* d_pos, uint32_t m, uint32_t max_pos,
                   mpic_kv_t kv, float* d_logits, cudaStream_t s,
                   const std::function<void(uint32_t)>& before_layer = {},
-                  const uint32_t* h_rows = nullptr) {
+                  const uint32_t* h_rows = nullptr, float* d_capture = nullptr) {
     const mpic_model_config& c = md->cfg;
     const uint32_t h = c.hidden_dim, H = c.n_heads, D = c.head_dim;
     MPIC_REQUIRE(m > 0, MPIC_ERR_VALIDATION, "no tokens to prefill");
@@ -403,7 +403,10 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
         }
         {
             ProfScope ps(s, MPIC_PHASE_ATTN);
-            if (tc_attn)
+            if (d_capture)
+                launch_attn_simt(ws->q, kl, vl, md->dtype, d_rows, m, H, D, ws->attn, s,
+                                 d_capture + (size_t)l * H * kv->T * kv->T, kv->T);
+            else if (tc_attn)
                 launch_attn_tc(static_cast<const __nv_bfloat16*>(ws->q), static_cast<const __nv_bfloat16*>(kl),
                                static_cast<const __nv_bfloat16*>(vl), kv->T, d_rows, m, H, ws->d_units,
                                ws->n_units, ws->d_comb, ws->n_comb, ws->part_o, ws->part_ml,
@@ -454,7 +457,8 @@ void check_ids(mpic_model_t md, const int32_t* ids, uint32_t m) {
 
 // Host-pointer form: stage into pinned memory, run, bring logits back; synchronous.
 void forward_host(mpic_model_t md, mpic_workspace_t ws, const int32_t* ids, const uint32_t* rows,
-                  const uint32_t* pos, uint32_t m, mpic_kv_t kv, float* logits, cudaStream_t s) {
+                  const uint32_t* pos, uint32_t m, mpic_kv_t kv, float* logits, cudaStream_t s,
+                  float* hidden_out = nullptr, float* capture_out = nullptr) {
     MPIC_REQUIRE(ws && ws->model == md, MPIC_ERR_VALIDATION, "workspace belongs to another model");
     MPIC_REQUIRE(m > 0, MPIC_ERR_VALIDATION, "no tokens to prefill");
     MPIC_REQUIRE(m <= ws->max_rows, MPIC_ERR_VALIDATION, "more rows than the workspace holds");
@@ -471,10 +475,24 @@ void forward_host(mpic_model_t md, mpic_workspace_t ws, const int32_t* ids, cons
     MPIC_CUDA(cudaMemcpyAsync(ws->d_ids, ws->h_ids, m * 4, cudaMemcpyHostToDevice, s));
     MPIC_CUDA(cudaMemcpyAsync(ws->d_rows, ws->h_rows, m * 4, cudaMemcpyHostToDevice, s));
     MPIC_CUDA(cudaMemcpyAsync(ws->d_pos, ws->h_pos, m * 4, cudaMemcpyHostToDevice, s));
+    float* d_cap = nullptr;
+    const size_t cap_elems = (size_t)md->cfg.n_layers * md->cfg.n_heads * kv->T * kv->T;
+    if (capture_out) {
+        MPIC_REQUIRE(md->dtype == MPIC_F32, MPIC_ERR_VALIDATION, "attention capture needs an fp32 model");
+        MPIC_CUDA(cudaMallocAsync((void**)&d_cap, cap_elems * 4, s));
+        MPIC_CUDA(cudaMemsetAsync(d_cap, 0, cap_elems * 4, s));
+    }
     forward_rows(md, ws, ws->d_ids, ws->d_rows, ws->d_pos, m, max_pos, kv, ws->d_logits, s, {},
-                 rows);
+                 rows, d_cap);
     MPIC_CUDA(cudaMemcpyAsync(ws->h_logits, ws->d_logits, md->cfg.vocab_size * 4,
                               cudaMemcpyDeviceToHost, s));
+    if (hidden_out)
+        MPIC_CUDA(cudaMemcpyAsync(hidden_out, ws->x, (size_t)m * md->cfg.hidden_dim * 4,
+                                  cudaMemcpyDeviceToHost, s));
+    if (capture_out) {
+        MPIC_CUDA(cudaMemcpyAsync(capture_out, d_cap, cap_elems * 4, cudaMemcpyDeviceToHost, s));
+        MPIC_CUDA(cudaFreeAsync(d_cap, s));
+    }
     MPIC_CUDA(cudaStreamSynchronize(s));
     std::memcpy(logits, ws->h_logits, md->cfg.vocab_size * sizeof(float));
 }
@@ -1050,6 +1068,62 @@ int mpic_prefill_extend(mpic_model_t model, mpic_workspace_t ws, const int32_t* 
     API_END
 }
 
+int mpic_forward_rows(mpic_model_t model, mpic_workspace_t ws, const int32_t* ids,
+                      const uint32_t* rows, const uint32_t* rope_pos, uint32_t m, mpic_kv_t kv,
+                      float* logits, float* hidden_out, float* attn_capture, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(model->device));
+    forward_host(model, ws, ids, rows, rope_pos, m, kv, logits, (cudaStream_t)stream, hidden_out,
+                 attn_capture);
+    API_END
+}
+
+int mpic_layer0_keys(mpic_model_t model, mpic_workspace_t ws, const int32_t* ids,
+                     const uint32_t* positions, uint32_t m, float* out, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(model->device));
+    MPIC_REQUIRE(ws && ws->model == model && m <= ws->max_rows, MPIC_ERR_VALIDATION, "bad workspace");
+    if (m == 0) return MPIC_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    check_ids(model, ids, m);
+    const mpic_model_config& c = model->cfg;
+    const uint32_t h = c.hidden_dim;
+    uint32_t max_pos = 0;
+    for (uint32_t i = 0; i < m; ++i) max_pos = std::max(max_pos, positions[i]);
+    ensure_rope(model, max_pos + 1, s);
+    std::vector<uint32_t> rows(m);
+    for (uint32_t i = 0; i < m; ++i) rows[i] = i;
+    std::memcpy(ws->h_ids, ids, m * 4);
+    std::memcpy(ws->h_rows, rows.data(), m * 4);
+    std::memcpy(ws->h_pos, positions, m * 4);
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_ids, ws->h_ids, m * 4, cudaMemcpyHostToDevice, s));
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_rows, ws->h_rows, m * 4, cudaMemcpyHostToDevice, s));
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_pos, ws->h_pos, m * 4, cudaMemcpyHostToDevice, s));
+    const bool bf = model->dtype == MPIC_BF16;
+    launch_embed(model->emb, ws->d_ids, m, h, ws->x, bf ? ws->xb : nullptr, s);
+    const size_t e = esz(model->dtype);
+    void* kbuf = nullptr;
+    void* vbuf = nullptr;
+    MPIC_CUDA(cudaMallocAsync(&kbuf, (size_t)m * h * e, s));
+    MPIC_CUDA(cudaMallocAsync(&vbuf, (size_t)m * h * e, s));
+    EpiParams qkv;  // layer-0 Q/K/V with K rotated at `positions` (linker.cpp:493-499)
+    qkv.mode = EPI_QKV;
+    qkv.q = ws->q;
+    qkv.kv_k = kbuf;
+    qkv.kv_v = vbuf;
+    qkv.kv_rows = ws->d_rows;
+    qkv.rope_pos = ws->d_pos;
+    qkv.rope = model->rope;
+    qkv.hidden = h;
+    qkv.head_dim = c.head_dim;
+    run_gemm(model, bf ? (const void*)ws->xb : (const void*)ws->x, model->wqkv[0], m, 3 * h, h, qkv, s);
+    download_cast(out, kbuf, model->dtype, (size_t)m * h, s);
+    MPIC_CUDA(cudaFreeAsync(kbuf, s));
+    MPIC_CUDA(cudaFreeAsync(vbuf, s));
+    MPIC_CUDA(cudaStreamSynchronize(s));
+    API_END
+}
+
 int mpic_forward_rows_async(mpic_model_t model, mpic_workspace_t ws, const int32_t* d_ids,
                             const uint32_t* d_rows, const uint32_t* d_rope_pos, uint32_t m,
                             uint32_t max_pos, mpic_kv_t kv, float* d_logits, void* stream) {
@@ -1244,6 +1318,29 @@ int mpic_profile_collect(double* ms, uint32_t* launches) {
         g_prof_pool.push_back(r.a);
         g_prof_pool.push_back(r.b);
     }
+    API_END
+}
+
+int mpic_host_gemm_f32(const float* a, const float* b, uint32_t M, uint32_t N, uint32_t K, float* c,
+                       int device) {
+    API_BEGIN
+    set_device(device);
+    float *da = nullptr, *db = nullptr, *dc = nullptr;
+    cudaStream_t s = 0;
+    MPIC_CUDA(cudaMalloc(&da, std::max<size_t>(1, (size_t)M * K) * 4));
+    MPIC_CUDA(cudaMalloc(&db, std::max<size_t>(1, (size_t)N * K) * 4));
+    MPIC_CUDA(cudaMalloc(&dc, std::max<size_t>(1, (size_t)M * N) * 4));
+    MPIC_CUDA(cudaMemcpy(da, a, (size_t)M * K * 4, cudaMemcpyHostToDevice));
+    MPIC_CUDA(cudaMemcpy(db, b, (size_t)N * K * 4, cudaMemcpyHostToDevice));
+    EpiParams ep;
+    ep.mode = EPI_STORE_F32;
+    ep.out = dc;
+    ep.ldo = N;
+    launch_gemm_simt(da, MPIC_F32, K, db, MPIC_F32, M, N, K, ep, MPIC_F32, s);
+    MPIC_CUDA(cudaMemcpy(c, dc, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+    cudaFree(da);
+    cudaFree(db);
+    cudaFree(dc);
     API_END
 }
 

@@ -62,7 +62,7 @@ void launch_gemm_simt(const void* A, mpic_dtype a_t, uint32_t lda, const void* W
                       cudaStream_t s);
 void launch_attn_simt(const void* q, const void* k, const void* v, mpic_dtype dt,
                       const uint32_t* rows, uint32_t m, uint32_t H, uint32_t D, void* out,
-                      cudaStream_t s);
+                      cudaStream_t s, float* capture = nullptr, uint32_t T = 0);
 void launch_lm_head(const float* x_last, const void* W, mpic_dtype w_t, uint32_t V, uint32_t h,
                     float* logits, cudaStream_t s);
 void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, size_t n, cudaStream_t s);

@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const TQ* __restrict__ q
                                                         const TKV* __restrict__ vv,
                                                         const uint32_t* __restrict__ rows,
                                                         uint32_t h, uint32_t D, float inv_sqrt_d,
-                                                        TO* __restrict__ out) {
+                                                        TO* __restrict__ out,
+                                                        float* __restrict__ capture, uint32_t T) {
     __shared__ float qs[256];
     __shared__ float sc[AT_CH];
     __shared__ float red[8];
@@ -233,21 +234,33 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const TQ* __restrict__ q
     const float inv = 1.0f / run_sum;
     if (tid < D) out[(size_t)i * h + hoff + tid] = from_f32<TO>(acc0 * inv);
     if (tid + 128 < D) out[(size_t)i * h + hoff + tid + 128] = from_f32<TO>(acc1 * inv);
+    if (capture) {
+        // AttentionDump (model.cpp:294-297): normalised probabilities of this row/head.
+        float* crow = capture + ((size_t)head * T + rows[i]) * T;
+        for (uint32_t j = warp; j < count; j += 4) {
+            const TKV* kr = kk + (size_t)j * h + hoff;
+            float dot = 0.0f;
+            for (uint32_t d = lane; d < D; d += 32) dot = fmaf(qs[d], to_f32<TKV>(kr[d]), dot);
+            dot = warp_sum(dot);
+            if (lane == 0) crow[j] = expf(dot * inv_sqrt_d - run_max) * inv;
+        }
+    }
 }
 
 void launch_attn_simt(const void* q, const void* k, const void* v, mpic_dtype dt,
                       const uint32_t* rows, uint32_t m, uint32_t H, uint32_t D, void* out,
-                      cudaStream_t s) {
+                      cudaStream_t s, float* capture, uint32_t T) {
     const uint32_t h = H * D;
     const float inv_sqrt_d = 1.0f / sqrtf((float)D);
     dim3 grid(m, H);
     if (dt == MPIC_F32)
         attn_simt_kernel<float, float, float><<<grid, 128, 0, s>>>(
-            (const float*)q, (const float*)k, (const float*)v, rows, h, D, inv_sqrt_d, (float*)out);
+            (const float*)q, (const float*)k, (const float*)v, rows, h, D, inv_sqrt_d, (float*)out,
+            capture, T);
     else
         attn_simt_kernel<__nv_bfloat16, __nv_bfloat16, __nv_bfloat16><<<grid, 128, 0, s>>>(
             (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, rows, h, D,
-            inv_sqrt_d, (__nv_bfloat16*)out);
+            inv_sqrt_d, (__nv_bfloat16*)out, capture, T);
     MPIC_LAUNCHED();
 }
 

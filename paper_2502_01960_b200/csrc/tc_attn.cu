@@ -174,24 +174,40 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             tc::mbar_wait(&s_full[s], (b >> 1) & 1);
             tc::tc_fence_after();
             const uint32_t sa = tmem + lane_base + s * 128;
-            // pass 1: masked row max (log2 domain)
-            float mx = -INFINITY;
+            // blocks entirely inside every row's causal limit skip the per-key mask
+            const bool masked = __any_sync(0xffffffffu, j0 + 127 > limit);
+            // pass 1: row max of the raw scores (scale > 0 commutes with max)
+            float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-            for (uint32_t c = 0; c < 8; ++c) {
-                uint32_t v[16];
-                tc::tmem_ld16(sa + c * 16, v);
+            for (uint32_t c = 0; c < 4; ++c) {
+                uint32_t v[32];
+                tc::tmem_ld32(sa + c * 32, v);
                 tc::tmem_ld_wait();
+                if (masked) {
 #pragma unroll
-                for (uint32_t e = 0; e < 16; ++e) {
-                    const uint32_t key = j0 + c * 16 + e;
-                    const float x = __uint_as_float(v[e]) * p.scale_log2;
-                    mx = key <= limit ? fmaxf(mx, x) : mx;
+                    for (uint32_t e = 0; e < 32; e += 4) {
+                        const uint32_t key = j0 + c * 32 + e;
+                        mx0 = key + 0 <= limit ? fmaxf(mx0, __uint_as_float(v[e + 0])) : mx0;
+                        mx1 = key + 1 <= limit ? fmaxf(mx1, __uint_as_float(v[e + 1])) : mx1;
+                        mx2 = key + 2 <= limit ? fmaxf(mx2, __uint_as_float(v[e + 2])) : mx2;
+                        mx3 = key + 3 <= limit ? fmaxf(mx3, __uint_as_float(v[e + 3])) : mx3;
+                    }
+                } else {
+#pragma unroll
+                    for (uint32_t e = 0; e < 32; e += 4) {
+                        mx0 = fmaxf(mx0, __uint_as_float(v[e + 0]));
+                        mx1 = fmaxf(mx1, __uint_as_float(v[e + 1]));
+                        mx2 = fmaxf(mx2, __uint_as_float(v[e + 2]));
+                        mx3 = fmaxf(mx3, __uint_as_float(v[e + 3]));
+                    }
                 }
             }
+            const float mraw = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+            const float mx = mraw * p.scale_log2;  // -inf stays -inf
             float alpha = 1.0f;
             const bool grow = mx > m_used + kRescaleThreshold || (m_used == -INFINITY && mx > -INFINITY);
             if (grow) {
-                alpha = m_used == -INFINITY ? 0.0f : exp2f(m_used - mx);
+                alpha = m_used == -INFINITY ? 0.0f : tc::ex2_approx(m_used - mx);
                 m_used = mx;
                 l *= alpha;
             }
@@ -214,26 +230,35 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     tc::tmem_st_wait();
                 }
             }
-            // pass 2: probabilities -> P (bf16, 128B-swizzled K-major rows)
+            // pass 2: p = 2^(s*scale - m) -> P (bf16, 128B-swizzled K-major rows)
+            const float neg_m = m_used == -INFINITY ? 0.0f : -m_used;
+            const bool row_dead = m_used == -INFINITY;  // every key so far masked
             uint8_t* prow = sP + s * kTile + r * 128;
+            float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
 #pragma unroll
-            for (uint32_t c = 0; c < 8; ++c) {
-                uint32_t v[16];
-                tc::tmem_ld16(sa + c * 16, v);
+            for (uint32_t c = 0; c < 4; ++c) {
+                uint32_t v[32];
+                tc::tmem_ld32(sa + c * 32, v);
                 tc::tmem_ld_wait();
-                float pv[16];
+                float pv[32];
 #pragma unroll
-                for (uint32_t e = 0; e < 16; ++e) {
-                    const uint32_t key = j0 + c * 16 + e;
-                    const float x = __uint_as_float(v[e]) * p.scale_log2;
-                    pv[e] = (key <= limit && m_used != -INFINITY) ? exp2f(x - m_used) : 0.0f;
-                    l += pv[e];
+                for (uint32_t e = 0; e < 32; ++e) {
+                    float x = tc::ex2_approx(fmaf(__uint_as_float(v[e]), p.scale_log2, neg_m));
+                    if (masked) x = (j0 + c * 32 + e <= limit && !row_dead) ? x : 0.0f;
+                    pv[e] = x;
                 }
-                // 16 keys = two 16-byte units; keys 64c' .. live in half (c >> 2)
-                const uint32_t half = c >> 2, unit0 = (c & 3) * 2;
+#pragma unroll
+                for (uint32_t e = 0; e < 32; e += 4) {
+                    l0 += pv[e];
+                    l1 += pv[e + 1];
+                    l2 += pv[e + 2];
+                    l3 += pv[e + 3];
+                }
+                // 32 keys = four 16-byte units; keys 64h .. 64h+63 live in half h
+                const uint32_t half = c >> 1, unit0 = (c & 1) * 4;
                 uint8_t* base = prow + half * kHalf;
 #pragma unroll
-                for (uint32_t w = 0; w < 2; ++w) {
+                for (uint32_t w = 0; w < 4; ++w) {
                     const uint32_t unit = (unit0 + w) ^ (r & 7);
                     uint4 q4;
                     q4.x = pack_bf16(pv[8 * w + 0], pv[8 * w + 1]);
@@ -243,6 +268,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     *reinterpret_cast<uint4*>(base + unit * 16) = q4;
                 }
             }
+            l += (l0 + l1) + (l2 + l3);
             tc::fence_async_shared();
             tc::tc_fence_before();
             tc::mbar_arrive(&p_full[s]);

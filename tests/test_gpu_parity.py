@@ -286,3 +286,17 @@ def test_head_dim_128_bf16_vs_oracle(layout, policy):
     k, v = linked.download()
     assert rel_err(k[-1][sel], rk[-1][sel]) < 1e-2
     assert rel_err(v[-1][sel], rv[-1][sel]) < 1e-2
+
+
+CONF_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle",
+                        "_ref", "conformance")
+
+
+@pytest.mark.skipif(not os.path.isdir(CONF_DIR), reason="conformance binaries not built")
+@pytest.mark.parametrize("suite", ["test_model", "test_cache", "test_linker", "test_transfer"])
+def test_reference_suites_on_b200_library(suite):
+    """Drop-in conformance: the reference's own doctest suites (proj/tests/*.cpp), compiled
+    unchanged against include/mpic + libmpic_b200.so, pass on the GPU."""
+    import subprocess
+    r = subprocess.run([os.path.join(CONF_DIR, suite)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
