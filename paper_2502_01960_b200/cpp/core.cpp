@@ -14,6 +14,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <vector>
 
 namespace mpic {
@@ -203,8 +205,69 @@ void DeviceKv::download(KvTensor& t) const {
     if (!t.k.empty()) check(mpic_kv_download(h_, t.k.data(), t.v.data(), nullptr));
 }
 
-Workspace::Workspace(const DeviceModel& m, uint32_t rows, uint32_t ctx) {
-    check(mpic_workspace_create(m.get(), std::max(rows, 1u), ctx, &h_));
+Workspace::Workspace(const DeviceModel& m, uint32_t rows, uint32_t ctx) : rows_(std::max(rows, 1u)), ctx_(ctx) {
+    check(mpic_workspace_create(m.get(), rows_, ctx, &h_));
+}
+
+namespace {
+uint64_t weight_hash(const Model& m) {
+    uint64_t acc = 0x9e3779b97f4a7c15ull ^ m.config.fingerprint();
+    auto feed = [&](const std::vector<float>& w) {
+        const auto* p = reinterpret_cast<const uint32_t*>(w.data());
+        for (size_t i = 0; i < w.size(); ++i) acc = (acc ^ p[i]) * 0x100000001b3ull;
+        acc ^= w.size();
+    };
+    feed(m.embedding);
+    feed(m.lm_head);
+    for (const LayerWeights& l : m.layers)
+        for (const std::vector<float>* w : {&l.wq, &l.wk, &l.wv, &l.wo, &l.w1, &l.w2}) feed(*w);
+    return acc;
+}
+
+struct ModelCacheEntry {
+    const Model* addr;
+    uint64_t hash;
+    std::shared_ptr<DeviceModel> dev;
+};
+std::mutex g_model_cache_mu;
+std::vector<ModelCacheEntry> g_model_cache;  // most recent last, at most 4 entries
+
+struct WsCacheEntry {
+    std::shared_ptr<DeviceModel> model;
+    std::unique_ptr<Workspace> ws;
+};
+thread_local std::vector<WsCacheEntry> t_ws_cache;
+}  // namespace
+
+std::shared_ptr<DeviceModel> device_model_for(const Model& m) {
+    const uint64_t h = weight_hash(m);
+    std::lock_guard<std::mutex> lk(g_model_cache_mu);
+    for (auto it = g_model_cache.begin(); it != g_model_cache.end(); ++it)
+        if (it->addr == &m && it->hash == h) {
+            ModelCacheEntry e = *it;
+            g_model_cache.erase(it);
+            g_model_cache.push_back(e);
+            return e.dev;
+        }
+    auto dev = std::make_shared<DeviceModel>(m);
+    g_model_cache.push_back({&m, h, dev});
+    if (g_model_cache.size() > 4) g_model_cache.erase(g_model_cache.begin());
+    return dev;
+}
+
+Workspace& workspace_for(const std::shared_ptr<DeviceModel>& m, uint32_t rows, uint32_t ctx) {
+    for (auto it = t_ws_cache.begin(); it != t_ws_cache.end(); ++it)
+        if (it->model == m) {
+            if (it->ws->rows() < rows || it->ws->ctx() < ctx)
+                it->ws = std::make_unique<Workspace>(*m, std::max(rows, it->ws->rows()), std::max(ctx, it->ws->ctx()));
+            return *it->ws;
+        }
+    // drop workspaces of models that left the model cache
+    t_ws_cache.erase(std::remove_if(t_ws_cache.begin(), t_ws_cache.end(),
+                                    [](const WsCacheEntry& e) { return e.model.use_count() <= 1; }),
+                     t_ws_cache.end());
+    t_ws_cache.push_back({m, std::make_unique<Workspace>(*m, rows, ctx)});
+    return *t_ws_cache.back().ws;
 }
 Workspace::~Workspace() { mpic_workspace_destroy(h_); }
 

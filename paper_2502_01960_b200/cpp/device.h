@@ -7,6 +7,7 @@
 #include "mpic/tensor.h"
 #include "mpic_b200.h"
 
+#include <memory>
 #include <string>
 
 namespace mpic::b200 {
@@ -44,6 +45,12 @@ private:
     mpic_kv_t h_ = nullptr;
 };
 
+// Device copy of a host Model, cached across calls. The value-semantic API lets callers
+// edit weights between calls (proj/tests/test_model.cpp zero_weights), so the cache key is
+// the model's address, its config fingerprint and a 64-bit hash of every weight word,
+// recomputed on each lookup; a mismatch re-uploads.
+std::shared_ptr<DeviceModel> device_model_for(const Model& m);
+
 class Workspace {
 public:
     Workspace(const DeviceModel& m, uint32_t rows, uint32_t ctx);
@@ -51,9 +58,15 @@ public:
     Workspace(const Workspace&) = delete;
     Workspace& operator=(const Workspace&) = delete;
     mpic_workspace_t get() const { return h_; }
+    uint32_t rows() const { return rows_; }
+    uint32_t ctx() const { return ctx_; }
 
 private:
     mpic_workspace_t h_ = nullptr;
+    uint32_t rows_ = 0, ctx_ = 0;
 };
+
+// Per-thread workspace reuse for a cached device model (grows on demand).
+Workspace& workspace_for(const std::shared_ptr<DeviceModel>& m, uint32_t rows, uint32_t ctx);
 
 }  // namespace mpic::b200

@@ -35,8 +35,8 @@ PrefillResult extend(const Model& model, std::span<const int32_t> ids, KvTensor&
     res.kv.resize_tokens(start + m);
     const uint32_t n = start + m;
 
-    b200::DeviceModel dm(model);
-    b200::Workspace ws(dm, m, n);
+    const auto dm = b200::device_model_for(model);
+    b200::Workspace& ws = b200::workspace_for(dm, m, n);
     b200::DeviceKv kv(res.kv);
     std::vector<uint32_t> rows(m), pos(m);
     for (uint32_t i = 0; i < m; ++i) {
@@ -52,7 +52,7 @@ PrefillResult extend(const Model& model, std::span<const int32_t> ids, KvTensor&
         capture->model_fingerprint = c.fingerprint();
         capture->scores.assign(size_t(c.n_layers) * c.n_heads * n * n, 0.0f);
     }
-    b200::check(mpic_forward_rows(dm.get(), ws.get(), ids.data(), rows.data(), pos.data(), m, kv.get(),
+    b200::check(mpic_forward_rows(dm->get(), ws.get(), ids.data(), rows.data(), pos.data(), m, kv.get(),
                                   res.logits.data(), hidden ? hidden->data() : nullptr,
                                   capture ? capture->scores.data() : nullptr, nullptr));
     kv.download(res.kv);

@@ -296,7 +296,7 @@ void download_cast(float* dst, const void* src, mpic_dtype dt, size_t n, cudaStr
 void run_gemm(mpic_model_t md, const void* A, const void* W, uint32_t M, uint32_t N, uint32_t K,
               const EpiParams& ep, cudaStream_t s) {
     if (md->dtype == MPIC_BF16) {
-        if (tc_gemm_supported(M, N, K)) {
+        if (tc_gemm_supported(M, N, K) && (ep.mode != EPI_QKV || md->cfg.head_dim % 32 == 0)) {
             launch_gemm_tc(static_cast<const __nv_bfloat16*>(A), K,
                            static_cast<const __nv_bfloat16*>(W), M, N, K, ep, s);
             return;

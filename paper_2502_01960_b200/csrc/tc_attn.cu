@@ -30,7 +30,8 @@ CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t outer, uint
 
 namespace {
 
-constexpr uint32_t kAttnThreads = 192;
+constexpr uint32_t kAttnThreads = 320;  // TMA, MMA, 8 softmax warps
+constexpr uint32_t kSoftmaxThreads = 256;
 constexpr uint32_t kTile = 32 * 1024;  // one [128 x 128] bf16 tile as 2 swizzled 64-col halves
 constexpr uint32_t kHalf = 16 * 1024;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
@@ -68,8 +69,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     uint64_t* v_empty = bars + 7;  // [2]
     uint64_t* s_full = bars + 9;   // [2]
     uint64_t* p_full = bars + 11;  // [2]
-    uint64_t* o_full = bars + 13;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 14);
+    uint64_t* o_full = bars + 13;  // [2] — PV_b completes on o_full[b & 1]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 15);
 
     const AttnUnit u = p.units[blockIdx.x];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -88,9 +89,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             tc::mbar_init(&v_full[i], 1);
             tc::mbar_init(&v_empty[i], 1);
             tc::mbar_init(&s_full[i], 1);
-            tc::mbar_init(&p_full[i], 128);
+            tc::mbar_init(&p_full[i], kSoftmaxThreads);
+            tc::mbar_init(&o_full[i], 1);
         }
-        tc::mbar_init(o_full, 1);
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc(tmem_holder, 512);
@@ -154,32 +155,34 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     tc::mma_bf16(tmem + 256, adesc, bdesc, idesc_o, (b > 0 || kk > 0) ? 1u : 0u);
                 }
                 tc::mma_commit(&v_empty[s]);
-                tc::mma_commit(o_full);
+                tc::mma_commit(&o_full[s]);
                 if (b + 2 < nb) issue_s(b + 2);
             }
         }
         __syncwarp();
     } else {
-        // ---- softmax / correction / epilogue: thread <-> query row (TMEM lane) ----
+        // ---- softmax: 8 warps, a pair per TMEM lane quarter; warp hsel owns score columns
+        // (keys) and O columns (head dims) [64*hsel, 64*hsel+64) of its 32 query rows.
         const uint32_t quarter = warp & 3;
+        const uint32_t hsel = (warp - 2) >> 2;
         const uint32_t r = quarter * 32 + lane;
         const uint32_t qi = q0 + r;
         const bool valid = qi < p.m;
         const uint32_t limit = valid ? p.rows[qi] : 0u;
         const uint32_t lane_base = (quarter * 32u) << 16;
+        const uint32_t xchg = tmem + lane_base + 384;  // partner exchange columns 384..391
+        const uint32_t bar_id = 1 + quarter;
         float m_used = -INFINITY, l = 0.0f;
         for (uint32_t b = 0; b < nb; ++b) {
             const uint32_t s = b & 1;
-            const uint32_t j0 = (u.b0 + b) * 128u;
+            const uint32_t j0 = (u.b0 + b) * 128u + hsel * 64u;  // first key of my half
             tc::mbar_wait(&s_full[s], (b >> 1) & 1);
             tc::tc_fence_after();
-            const uint32_t sa = tmem + lane_base + s * 128;
-            // blocks entirely inside every row's causal limit skip the per-key mask
-            const bool masked = __any_sync(0xffffffffu, j0 + 127 > limit);
-            // pass 1: row max of the raw scores (scale > 0 commutes with max)
+            const uint32_t sa = tmem + lane_base + s * 128 + hsel * 64;
+            const bool masked = __any_sync(0xffffffffu, j0 + 63 > limit);
             float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-            for (uint32_t c = 0; c < 4; ++c) {
+            for (uint32_t c = 0; c < 2; ++c) {
                 uint32_t v[32];
                 tc::tmem_ld32(sa + c * 32, v);
                 tc::tmem_ld_wait();
@@ -202,8 +205,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     }
                 }
             }
-            const float mraw = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-            const float mx = mraw * p.scale_log2;  // -inf stays -inf
+            // row max across the two halves, exchanged through spare TMEM columns
+            float mraw = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+            tc::tmem_st1(xchg + s * 2 + hsel, __float_as_uint(mraw));
+            tc::tmem_st_wait();
+            tc::tc_fence_before();
+            tc::named_bar_sync(bar_id, 64);
+            tc::tc_fence_after();
+            mraw = fmaxf(mraw, __uint_as_float(tc::tmem_ld1(xchg + s * 2 + (hsel ^ 1))));
+            tc::tmem_ld_wait();
+            const float mx = mraw * p.scale_log2;
             float alpha = 1.0f;
             const bool grow = mx > m_used + kRescaleThreshold || (m_used == -INFINITY && mx > -INFINITY);
             if (grow) {
@@ -211,32 +222,33 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 m_used = mx;
                 l *= alpha;
             }
-            // PV_{b-1} (and everything before it) must be complete before O is rescaled
-            // and before P buffer (b&1) is overwritten (it was read by PV_{b-2}).
-            if (b > 0) {
-                tc::mbar_wait(o_full, (b - 1) & 1);
+            if (b > 0 && __any_sync(0xffffffffu, grow && alpha != 1.0f)) {
+                // every earlier PV must have landed before O is rescaled
+                tc::mbar_wait(&o_full[(b - 1) & 1], ((b - 1) >> 1) & 1);
                 tc::tc_fence_after();
-                if (__any_sync(0xffffffffu, grow && alpha != 1.0f)) {
-                    const uint32_t oa = tmem + lane_base + 256;
+                const uint32_t oa = tmem + lane_base + 256 + hsel * 64;
 #pragma unroll
-                    for (uint32_t c = 0; c < 8; ++c) {
-                        uint32_t v[16];
-                        tc::tmem_ld16(oa + c * 16, v);
-                        tc::tmem_ld_wait();
+                for (uint32_t c = 0; c < 4; ++c) {
+                    uint32_t v[16];
+                    tc::tmem_ld16(oa + c * 16, v);
+                    tc::tmem_ld_wait();
 #pragma unroll
-                        for (uint32_t e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
-                        tc::tmem_st16(oa + c * 16, v);
-                    }
-                    tc::tmem_st_wait();
+                    for (uint32_t e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
+                    tc::tmem_st16(oa + c * 16, v);
                 }
+                tc::tmem_st_wait();
             }
-            // pass 2: p = 2^(s*scale - m) -> P (bf16, 128B-swizzled K-major rows)
+            // P buffer s was read by PV_{b-2}
+            if (b >= 2) {
+                tc::mbar_wait(&o_full[s], ((b - 2) >> 1) & 1);
+                tc::tc_fence_after();
+            }
             const float neg_m = m_used == -INFINITY ? 0.0f : -m_used;
-            const bool row_dead = m_used == -INFINITY;  // every key so far masked
-            uint8_t* prow = sP + s * kTile + r * 128;
+            const bool row_dead = m_used == -INFINITY;
+            uint8_t* prow = sP + s * kTile + hsel * kHalf + r * 128;
             float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
 #pragma unroll
-            for (uint32_t c = 0; c < 4; ++c) {
+            for (uint32_t c = 0; c < 2; ++c) {
                 uint32_t v[32];
                 tc::tmem_ld32(sa + c * 32, v);
                 tc::tmem_ld_wait();
@@ -254,18 +266,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     l2 += pv[e + 2];
                     l3 += pv[e + 3];
                 }
-                // 32 keys = four 16-byte units; keys 64h .. 64h+63 live in half h
-                const uint32_t half = c >> 1, unit0 = (c & 1) * 4;
-                uint8_t* base = prow + half * kHalf;
 #pragma unroll
                 for (uint32_t w = 0; w < 4; ++w) {
-                    const uint32_t unit = (unit0 + w) ^ (r & 7);
+                    const uint32_t unit = (c * 4 + w) ^ (r & 7);
                     uint4 q4;
                     q4.x = pack_bf16(pv[8 * w + 0], pv[8 * w + 1]);
                     q4.y = pack_bf16(pv[8 * w + 2], pv[8 * w + 3]);
                     q4.z = pack_bf16(pv[8 * w + 4], pv[8 * w + 5]);
                     q4.w = pack_bf16(pv[8 * w + 6], pv[8 * w + 7]);
-                    *reinterpret_cast<uint4*>(base + unit * 16) = q4;
+                    *reinterpret_cast<uint4*>(prow + unit * 16) = q4;
                 }
             }
             l += (l0 + l1) + (l2 + l3);
@@ -273,20 +282,27 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             tc::tc_fence_before();
             tc::mbar_arrive(&p_full[s]);
         }
-        // epilogue: O / l
-        tc::mbar_wait(o_full, (nb - 1) & 1);
+        // ---- epilogue: O / l over both halves' partial row sums
+        tc::tmem_st1(xchg + 4 + hsel, __float_as_uint(l));
+        tc::tmem_st_wait();
+        tc::mbar_wait(&o_full[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
+        tc::tc_fence_before();
+        tc::named_bar_sync(bar_id, 64);
         tc::tc_fence_after();
-        const uint32_t oa = tmem + lane_base + 256;
+        l += __uint_as_float(tc::tmem_ld1(xchg + 4 + (hsel ^ 1)));
+        tc::tmem_ld_wait();
+        const uint32_t oa = tmem + lane_base + 256 + hsel * 64;
         const bool direct = u.slot == 0xffffffffu;
         const float inv = l > 0.0f ? 1.0f / l : 0.0f;
 #pragma unroll
-        for (uint32_t c = 0; c < 8; ++c) {
+        for (uint32_t c = 0; c < 4; ++c) {
             uint32_t v[16];
             tc::tmem_ld16(oa + c * 16, v);
             tc::tmem_ld_wait();
             if (!valid) continue;
+            const uint32_t d0 = hsel * 64 + c * 16;
             if (direct) {
-                __nv_bfloat16* o = p.out + (size_t)qi * p.h + u.head * 128u + c * 16;
+                __nv_bfloat16* o = p.out + (size_t)qi * p.h + u.head * 128u + d0;
                 uint4 a, b2;
                 a.x = pack_bf16(__uint_as_float(v[0]) * inv, __uint_as_float(v[1]) * inv);
                 a.y = pack_bf16(__uint_as_float(v[2]) * inv, __uint_as_float(v[3]) * inv);
@@ -299,14 +315,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 reinterpret_cast<uint4*>(o)[0] = a;
                 reinterpret_cast<uint4*>(o)[1] = b2;
             } else {
-                float4* o = reinterpret_cast<float4*>(p.part_o + ((size_t)u.slot * 128 + r) * 128 + c * 16);
+                float4* o = reinterpret_cast<float4*>(p.part_o + ((size_t)u.slot * 128 + r) * 128 + d0);
 #pragma unroll
                 for (uint32_t e = 0; e < 4; ++e)
                     o[e] = make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]),
                                        __uint_as_float(v[4 * e + 2]), __uint_as_float(v[4 * e + 3]));
             }
         }
-        if (valid && !direct) p.part_ml[(size_t)u.slot * 128 + r] = make_float2(m_used, l);
+        if (valid && !direct && hsel == 0) p.part_ml[(size_t)u.slot * 128 + r] = make_float2(m_used, l);
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -409,7 +425,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     p.out = out;
     p.part_o = part_o;
     p.part_ml = part_ml;
-    const size_t smem = 7 * kTile + 1024 + 256;
+    const size_t smem = 7 * kTile + 1024 + 16 * 8 + 16;
     static bool attr = false;
     if (!attr) {
         MPIC_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

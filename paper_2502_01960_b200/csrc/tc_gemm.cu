@@ -47,6 +47,11 @@ struct TcGemmArgs {
     EpiParams ep;
 };
 
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
 template <typename TO>
 __device__ __forceinline__ void tc_epilogue(const EpiParams& ep, uint32_t t, uint32_t f, float v) {
     switch (ep.mode) {
@@ -318,6 +323,184 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     if (warp == 1) tc::tmem_dealloc_pair(tmem_base, a.tmem_cols);
 }
 
+
+// ---- token-major GEMM (the production path) ---------------------------------------------
+// UMMA M = 128 TOKENS (TMEM lane = token row), N = bn FEATURES (<= 256). Each epilogue
+// thread owns one token row and a run of consecutive features, so every epilogue store
+// is a 16-byte vector (the swap-AB kernels above issue one scalar store per element), RoPE
+// pairs sit in adjacent registers, and the KV scatter row is one index per thread.
+struct TokArgs {
+    uint32_t M, N, K;
+    uint32_t bn;        // features per CTA (64, 128 or 256)
+    uint32_t kblocks;   // 64-wide K blocks in total
+    uint32_t split;     // K split (blockIdx.z), uneven ranges allowed
+    uint32_t stages;
+    uint32_t tmem_cols;
+    EpiParams ep;
+};
+
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32]) {
+#pragma unroll
+    for (uint32_t w = 0; w < 4; ++w) {
+        uint4 q;
+        q.x = pack_bf16x2(v[8 * w + 0], v[8 * w + 1]);
+        q.y = pack_bf16x2(v[8 * w + 2], v[8 * w + 3]);
+        q.z = pack_bf16x2(v[8 * w + 4], v[8 * w + 5]);
+        q.w = pack_bf16x2(v[8 * w + 6], v[8 * w + 7]);
+        reinterpret_cast<uint4*>(dst)[w] = q;
+    }
+}
+
+__device__ __forceinline__ void tok_epilogue_chunk(const EpiParams& ep, uint32_t t, uint32_t f0,
+                                                   float (&v)[32]) {
+    switch (ep.mode) {
+        case EPI_QKV: {
+            // linker.cpp:64-78 — q/k rotated at rope_pos[t], k/v scattered to kv[kv_rows[t]]
+            const uint32_t h = ep.hidden, part = f0 / h, c = f0 - part * h;
+            if (part < 2) {
+                const float4* cs4 = reinterpret_cast<const float4*>(
+                    ep.rope + (size_t)__ldg(ep.rope_pos + t) * (ep.head_dim >> 1) + ((c % ep.head_dim) >> 1));
+#pragma unroll
+                for (uint32_t i = 0; i < 8; ++i) {
+                    const float4 cs = __ldg(cs4 + i);  // (cos, sin) of pairs 2i, 2i+1
+                    rope_pair(v[4 * i + 0], v[4 * i + 1], cs.x, cs.y);
+                    rope_pair(v[4 * i + 2], v[4 * i + 3], cs.z, cs.w);
+                }
+            }
+            __nv_bfloat16* dst = part == 0 ? static_cast<__nv_bfloat16*>(ep.q) + (size_t)t * h + c
+                                           : static_cast<__nv_bfloat16*>(part == 1 ? ep.kv_k : ep.kv_v) +
+                                                 (size_t)__ldg(ep.kv_rows + t) * h + c;
+            store_bf16x32(dst, v);
+            break;
+        }
+        case EPI_RESID: {
+            if (ep.split_k > 1) {
+                float4* pp = reinterpret_cast<float4*>(ep.partial + ((size_t)blockIdx.z * ep.rows_total + t) * ep.ldx + f0);
+#pragma unroll
+                for (uint32_t i = 0; i < 8; ++i) pp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            } else {
+                float4* xp = reinterpret_cast<float4*>(ep.x + (size_t)t * ep.ldx + f0);
+#pragma unroll
+                for (uint32_t i = 0; i < 8; ++i) {
+                    float4 a = xp[i];
+                    a.x += v[4 * i];
+                    a.y += v[4 * i + 1];
+                    a.z += v[4 * i + 2];
+                    a.w += v[4 * i + 3];
+                    xp[i] = a;
+                    v[4 * i] = a.x;
+                    v[4 * i + 1] = a.y;
+                    v[4 * i + 2] = a.z;
+                    v[4 * i + 3] = a.w;
+                }
+                if (ep.xb) store_bf16x32(ep.xb + (size_t)t * ep.ldx + f0, v);
+            }
+            break;
+        }
+        case EPI_GELU:
+#pragma unroll
+            for (uint32_t i = 0; i < 32; ++i) v[i] = gelu_ref(v[i]);
+            store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (size_t)t * ep.ldo + f0, v);
+            break;
+        case EPI_STORE_F32: {
+            float4* o = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + (size_t)t * ep.ldo + f0);
+#pragma unroll
+            for (uint32_t i = 0; i < 8; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            break;
+        }
+        default:
+            store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (size_t)t * ep.ldo + f0, v);
+    }
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    tc_gemm_tok_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                       const TokArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t w_bytes = a.bn * 128;
+    const uint32_t stage_bytes = kXBoxBytes + w_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
+    uint64_t* empty = full + a.stages;
+    uint64_t* tmem_full = empty + a.stages;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t n0 = blockIdx.x * a.bn, t0 = blockIdx.y * 128;
+    const uint32_t kb0 = blockIdx.z * a.kblocks / a.split;
+    const uint32_t kb1 = (blockIdx.z + 1) * a.kblocks / a.split;
+
+    if (warp == 0 && lane == 0) {
+        tc::tma_prefetch_desc(&tmX);
+        tc::tma_prefetch_desc(&tmW);
+        for (uint32_t s = 0; s < a.stages; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        tc::mbar_init(tmem_full, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_holder, a.tmem_cols);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_w = tc::policy_evict_first();  // weights stream through once
+            const uint64_t pol_x = tc::policy_evict_last();   // token tiles are re-read
+            for (uint32_t kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
+                const uint32_t s = i % a.stages, ph = (i / a.stages) & 1;
+                tc::mbar_wait(&empty[s], ph ^ 1);
+                tc::mbar_arrive_expect_tx(&full[s], stage_bytes);
+                uint8_t* st = smem + s * stage_bytes;
+                tc::tma_load_2d_hint(st, &tmX, &full[s], (int)(kb * 64), (int)t0, pol_x);
+                tc::tma_load_2d_hint(st + kXBoxBytes, &tmW, &full[s], (int)(kb * 64), (int)n0, pol_w);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = tc::idesc_bf16(128, a.bn);
+            for (uint32_t kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
+                const uint32_t s = i % a.stages, ph = (i / a.stages) & 1;
+                tc::mbar_wait(&full[s], ph);
+                tc::tc_fence_after();
+                const uint32_t x_base = tc::smem_u32(smem + s * stage_bytes);
+                const uint32_t w_base = x_base + kXBoxBytes;
+#pragma unroll
+                for (uint32_t kk = 0; kk < 4; ++kk)
+                    tc::mma_bf16(tmem_base, tc::desc_k_sw128(x_base + kk * 32), tc::desc_k_sw128(w_base + kk * 32),
+                                 idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                tc::mma_commit(&empty[s]);
+            }
+            tc::mma_commit(tmem_full);
+        }
+        __syncwarp();
+    } else {
+        const uint32_t q = warp & 3;
+        const uint32_t t = t0 + q * 32 + lane;
+        tc::mbar_wait(tmem_full, 0);
+        tc::tc_fence_after();
+        for (uint32_t c = 0; c < a.bn; c += 32) {
+            uint32_t r[32];
+            tc::tmem_ld32(tmem_base + ((q * 32u) << 16) + c, r);
+            tc::tmem_ld_wait();
+            if (t < a.M) {
+                float v[32];
+#pragma unroll
+                for (uint32_t i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+                tok_epilogue_chunk(a.ep, t, n0 + c, v);
+            }
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    if (warp == 1) tc::tmem_dealloc(tmem_base, a.tmem_cols);
+}
+
 // x += sum_z partial[z]; xb = bf16(x) — the deterministic split-K reduction, fused with
 // the cast that produces the next GEMM's bf16 operand.
 __global__ void __launch_bounds__(256) resid_reduce_kernel(const float* __restrict__ partial,
@@ -410,8 +593,71 @@ CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t outer, uint
 }
 
 bool tc_gemm_supported(uint32_t M, uint32_t N, uint32_t K) {
-    return M > 0 && N % 128 == 0 && K % 64 == 0 && K >= 64;
+    return M > 0 && N % 64 == 0 && K % 64 == 0 && K >= 64;
 }
+
+namespace {
+// Token-major launch: picks the feature tile (bn), K split and CTAs/SM for best SM fill.
+void launch_tok(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint32_t N, uint32_t K,
+                const EpiParams& ep_in, cudaStream_t s) {
+    const uint32_t mt = ceil_div(M, 128), kblocks = K / 64;
+    const bool can_split = ep_in.mode == EPI_RESID && ep_in.partial != nullptr;
+    double best = -1.0;
+    uint32_t bn = 64, split = 1;
+    for (uint32_t b : {256u, 128u, 64u}) {
+        if (N % b) continue;
+        for (uint32_t sp = 1; sp <= (can_split ? 4u : 1u); ++sp) {
+            if (kblocks / sp < 8 && sp > 1) break;
+            if (sp > 1 && (size_t)sp * M * N > ep_in.partial_cap) break;
+            const uint32_t ctas = (N / b) * mt * sp;
+            const uint32_t per_sm = ctas > (uint32_t)kNumSMs ? 2 : 1;
+            const uint32_t slots = kNumSMs * per_sm;
+            const double waves = std::ceil((double)ctas / slots);
+            // fill of the busiest wave, discounted for small tiles (more operand re-reads)
+            // and for split-K (partial traffic)
+            double score = (double)ctas / (slots * waves) * (b == 256 ? 1.0 : b == 128 ? 0.93 : 0.8) *
+                           (1.0 - 0.03 * (sp - 1));
+            if (score > best + 1e-9) {
+                best = score;
+                bn = b;
+                split = sp;
+            }
+        }
+    }
+    TokArgs a{};
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.bn = bn;
+    a.kblocks = kblocks;
+    a.split = split;
+    const uint32_t ctas = (N / bn) * mt * split;
+    const uint32_t per_sm = ctas > (uint32_t)kNumSMs ? 2 : 1;
+    const uint32_t stage_bytes = kXBoxBytes + bn * 128;
+    const uint32_t budget = (227 * 1024) / per_sm - 1024 - 256;
+    a.stages = std::min<uint32_t>(8, budget / stage_bytes);
+    MPIC_REQUIRE(a.stages >= 2, MPIC_ERR_VALIDATION, "tc gemm tile does not fit shared memory");
+    a.tmem_cols = std::max(32u, bn);
+    a.ep = ep_in;
+    a.ep.split_k = split;
+    a.ep.rows_total = M;
+    const CUtensorMap tmX = make_tmap_bf16(A, K, M, 64, 128);
+    const CUtensorMap tmW = make_tmap_bf16(W, K, N, 64, bn);
+    const size_t smem = (size_t)a.stages * stage_bytes + 1024 + (2 * a.stages + 1) * 8 + 16;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        MPIC_CUDA(cudaFuncSetAttribute(tc_gemm_tok_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    });
+    tc_gemm_tok_kernel<<<dim3(N / bn, mt, split), kTcThreads, smem, s>>>(tmX, tmW, a);
+    MPIC_LAUNCHED();
+    if (split > 1) {
+        const size_t n4 = (size_t)M * N / 4;
+        resid_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(ep_in.partial, split, (size_t)M * N, ep_in.x,
+                                                         ep_in.xb, n4);
+        MPIC_LAUNCHED();
+    }
+}
+}  // namespace
 
 namespace {
 void launch_pair(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint32_t N, uint32_t K,
@@ -463,6 +709,14 @@ void launch_pair(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uin
 void launch_gemm_tc(const __nv_bfloat16* A, uint32_t lda, const __nv_bfloat16* W, uint32_t M,
                     uint32_t N, uint32_t K, const EpiParams& ep_in, cudaStream_t s) {
     MPIC_REQUIRE(tc_gemm_supported(M, N, K) && lda == K, MPIC_ERR_VALIDATION, "unsupported tc gemm shape");
+    static const char* variant = getenv("MPIC_GEMM_VARIANT");  // diagnostics: "swap", "pair"
+    if (!variant || (variant[0] != 's' && variant[0] != 'p')) {
+        MPIC_REQUIRE(ep_in.mode != EPI_QKV || (ep_in.head_dim % 32 == 0 && ep_in.hidden % 32 == 0),
+                     MPIC_ERR_VALIDATION, "tc gemm QKV epilogue needs head_dim % 32 == 0");
+        launch_tok(A, W, M, N, K, ep_in, s);
+        return;
+    }
+    MPIC_REQUIRE(N % 128 == 0, MPIC_ERR_VALIDATION, "swap-AB gemm needs N % 128 == 0");
     TcGemmArgs a{};
     a.M = M;
     a.N = N;
@@ -492,8 +746,7 @@ void launch_gemm_tc(const __nv_bfloat16* A, uint32_t lda, const __nv_bfloat16* W
         return e ? (uint32_t)atoi(e) : 0u;
     }();
     a.dbg = dbg;
-    static const bool no_pair = getenv("MPIC_GEMM_NO_PAIR") != nullptr;
-    if (N % 256 == 0 && !no_pair && !dbg) {
+    if (N % 256 == 0 && variant[0] == 'p' && !dbg) {
         launch_pair(A, W, M, N, K, a.tt, tiles_t, split, kblocks, ep_in, s);
         return;
     }
