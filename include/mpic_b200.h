@@ -248,6 +248,12 @@ typedef enum {
 int mpic_profile_enable(int on);
 int mpic_profile_collect(double* ms, uint32_t* counts);
 
+/* Test hook: the head_dim-128 tcgen05 selective attention on bf16 device buffers
+ * q [m][H*128], k/v [n_ctx][H*128]; query i attends keys [0, rows[i]] (host rows,
+ * ascending). out [m][H*128] bf16. Async on `stream`. */
+int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const uint32_t* rows,
+                        uint32_t m, uint32_t n_ctx, uint32_t n_heads, void* d_out, void* stream);
+
 /* Number of kernels the last forward/assemble call on this thread launched. */
 uint32_t mpic_last_launch_count(void);
 

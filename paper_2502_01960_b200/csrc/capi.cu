@@ -1321,6 +1321,33 @@ int mpic_profile_collect(double* ms, uint32_t* launches) {
     API_END
 }
 
+int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const uint32_t* rows,
+                        uint32_t m, uint32_t n_ctx, uint32_t n_heads, void* d_out, void* stream) {
+    API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    const AttnPlan plan = plan_attention(rows, m, n_heads);
+    void* buf = nullptr;
+    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t bu = al(plan.units.size() * sizeof(AttnUnit)), bc = al(plan.combine.size() * sizeof(AttnCombine));
+    const size_t bo = al((size_t)plan.slots * 128 * 128 * 4), bm = al((size_t)plan.slots * 128 * 8), br = (size_t)m * 4;
+    MPIC_CUDA(cudaMallocAsync(&buf, bu + bc + bo + bm + br + 64, s));
+    char* b = static_cast<char*>(buf);
+    MPIC_CUDA(cudaMemcpyAsync(b, plan.units.data(), plan.units.size() * sizeof(AttnUnit), cudaMemcpyHostToDevice, s));
+    if (!plan.combine.empty())
+        MPIC_CUDA(cudaMemcpyAsync(b + bu, plan.combine.data(), plan.combine.size() * sizeof(AttnCombine),
+                                  cudaMemcpyHostToDevice, s));
+    MPIC_CUDA(cudaMemcpyAsync(b + bu + bc + bo + bm, rows, br, cudaMemcpyHostToDevice, s));
+    launch_attn_tc(static_cast<const __nv_bfloat16*>(d_q), static_cast<const __nv_bfloat16*>(d_k),
+                   static_cast<const __nv_bfloat16*>(d_v), n_ctx,
+                   reinterpret_cast<const uint32_t*>(b + bu + bc + bo + bm), m, n_heads,
+                   reinterpret_cast<const AttnUnit*>(b), (uint32_t)plan.units.size(),
+                   reinterpret_cast<const AttnCombine*>(b + bu), (uint32_t)plan.combine.size(),
+                   reinterpret_cast<float*>(b + bu + bc), reinterpret_cast<float2*>(b + bu + bc + bo),
+                   static_cast<__nv_bfloat16*>(d_out), s);
+    MPIC_CUDA(cudaFreeAsync(buf, s));
+    API_END
+}
+
 int mpic_host_gemm_f32(const float* a, const float* b, uint32_t M, uint32_t N, uint32_t K, float* c,
                        int device) {
     API_BEGIN

@@ -30,7 +30,8 @@ CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t outer, uint
 
 namespace {
 
-constexpr uint32_t kAttnThreads = 320;  // TMA, MMA, 8 softmax warps
+constexpr uint32_t kAttnThreads = 352;  // K TMA, MMA, V TMA, 8 softmax warps
+constexpr uint32_t kKvStages = 3;
 constexpr uint32_t kSoftmaxThreads = 256;
 constexpr uint32_t kTile = 32 * 1024;  // one [128 x 128] bf16 tile as 2 swizzled 64-col halves
 constexpr uint32_t kHalf = 16 * 1024;
@@ -58,19 +59,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
-    uint8_t* sK = smem + kTile;          // 2 stages
-    uint8_t* sV = smem + 3 * kTile;      // 2 stages
-    uint8_t* sP = smem + 5 * kTile;      // 2 buffers
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 7 * kTile);
+    uint8_t* sK = smem + kTile;                 // kKvStages stages
+    uint8_t* sV = smem + (1 + kKvStages) * kTile;  // kKvStages stages
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (1 + 2 * kKvStages) * kTile);
     uint64_t* q_full = bars + 0;
-    uint64_t* k_full = bars + 1;   // [2]
-    uint64_t* k_empty = bars + 3;  // [2]
-    uint64_t* v_full = bars + 5;   // [2]
-    uint64_t* v_empty = bars + 7;  // [2]
-    uint64_t* s_full = bars + 9;   // [2]
-    uint64_t* p_full = bars + 11;  // [2]
-    uint64_t* o_full = bars + 13;  // [2] — PV_b completes on o_full[b & 1]
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 15);
+    uint64_t* k_full = bars + 1;                   // [kKvStages]
+    uint64_t* k_empty = k_full + kKvStages;        // [kKvStages]
+    uint64_t* v_full = k_empty + kKvStages;        // [kKvStages]
+    uint64_t* v_empty = v_full + kKvStages;        // [kKvStages]
+    uint64_t* s_full = v_empty + kKvStages;        // [2]
+    uint64_t* p_full = s_full + 2;                 // [2]
+    uint64_t* o_full = p_full + 2;                 // [2] — PV_b completes on o_full[b & 1]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 2);
 
     const AttnUnit u = p.units[blockIdx.x];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -83,11 +83,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tc::tma_prefetch_desc(&tmK);
         tc::tma_prefetch_desc(&tmV);
         tc::mbar_init(q_full, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (uint32_t i = 0; i < kKvStages; ++i) {
             tc::mbar_init(&k_full[i], 1);
             tc::mbar_init(&k_empty[i], 1);
             tc::mbar_init(&v_full[i], 1);
             tc::mbar_init(&v_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&s_full[i], 1);
             tc::mbar_init(&p_full[i], kSoftmaxThreads);
             tc::mbar_init(&o_full[i], 1);
@@ -99,21 +101,31 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_holder;
+    // TMEM columns: S0 [0,128) | S1 [128,256) | O [256,384) | row exchange [384,392).
+    // P_b (bf16, two keys per column) overwrites the first 64 columns of S_b in place.
     constexpr uint32_t idesc_s = tc::idesc_bf16(128, 128, false);
     constexpr uint32_t idesc_o = tc::idesc_bf16(128, 128, true);
 
     if (warp == 0) {
-        if (lane == 0) {
+        if (lane == 0) {  // K producer (+ Q)
             tc::mbar_arrive_expect_tx(q_full, kTile);
             tc::tma_load_2d(sQ, &tmQ, q_full, hcol, (int)q0);
             tc::tma_load_2d(sQ + kHalf, &tmQ, q_full, hcol + 64, (int)q0);
             for (uint32_t b = 0; b < nb; ++b) {
-                const uint32_t s = b & 1, ph = (b >> 1) & 1;
+                const uint32_t s = b % kKvStages, ph = (b / kKvStages) & 1;
                 const int j0 = (int)((u.b0 + b) * 128u);
                 tc::mbar_wait(&k_empty[s], ph ^ 1);
                 tc::mbar_arrive_expect_tx(&k_full[s], kTile);
                 tc::tma_load_2d(sK + s * kTile, &tmK, &k_full[s], hcol, j0);
                 tc::tma_load_2d(sK + s * kTile + kHalf, &tmK, &k_full[s], hcol + 64, j0);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 2) {
+        if (lane == 0) {  // V producer
+            for (uint32_t b = 0; b < nb; ++b) {
+                const uint32_t s = b % kKvStages, ph = (b / kKvStages) & 1;
+                const int j0 = (int)((u.b0 + b) * 128u);
                 tc::mbar_wait(&v_empty[s], ph ^ 1);
                 tc::mbar_arrive_expect_tx(&v_full[s], kTile);
                 tc::tma_load_2d(sV + s * kTile, &tmV, &v_full[s], hcol, j0);
@@ -125,38 +137,35 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         if (lane == 0) {
             const uint32_t qa = tc::smem_u32(sQ);
             auto issue_s = [&](uint32_t b) {
-                const uint32_t s = b & 1;
-                tc::mbar_wait(&k_full[s], (b >> 1) & 1);
+                const uint32_t ks = b % kKvStages;
+                tc::mbar_wait(&k_full[ks], (b / kKvStages) & 1);
                 tc::tc_fence_after();
-                const uint32_t ka = tc::smem_u32(sK + s * kTile);
+                const uint32_t ka = tc::smem_u32(sK + ks * kTile);
 #pragma unroll
                 for (uint32_t kk = 0; kk < 8; ++kk) {
                     const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-                    tc::mma_bf16(tmem + s * 128, tc::desc_k_sw128(qa + off), tc::desc_k_sw128(ka + off),
+                    tc::mma_bf16(tmem + (b & 1) * 128, tc::desc_k_sw128(qa + off), tc::desc_k_sw128(ka + off),
                                  idesc_s, kk > 0 ? 1u : 0u);
                 }
-                tc::mma_commit(&k_empty[s]);
-                tc::mma_commit(&s_full[s]);
+                tc::mma_commit(&k_empty[ks]);
+                tc::mma_commit(&s_full[b & 1]);
             };
             tc::mbar_wait(q_full, 0);
             issue_s(0);
             if (nb > 1) issue_s(1);
             for (uint32_t b = 0; b < nb; ++b) {
-                const uint32_t s = b & 1, ph = (b >> 1) & 1;
-                tc::mbar_wait(&p_full[s], ph);
-                tc::mbar_wait(&v_full[s], ph);
+                const uint32_t s = b & 1, vs = b % kKvStages;
+                tc::mbar_wait(&p_full[s], (b >> 1) & 1);
+                tc::mbar_wait(&v_full[vs], (b / kKvStages) & 1);
                 tc::tc_fence_after();
-                const uint32_t pa = tc::smem_u32(sP + s * kTile);
-                const uint32_t va = tc::smem_u32(sV + s * kTile);
+                const uint32_t va = tc::smem_u32(sV + vs * kTile);
 #pragma unroll
-                for (uint32_t kk = 0; kk < 8; ++kk) {
-                    const uint64_t adesc = tc::desc_k_sw128(pa + (kk >> 2) * kHalf + (kk & 3) * 32);
-                    const uint64_t bdesc = tc::desc_mn_sw128(va + kk * 2048, kHalf);
-                    tc::mma_bf16(tmem + 256, adesc, bdesc, idesc_o, (b > 0 || kk > 0) ? 1u : 0u);
-                }
-                tc::mma_commit(&v_empty[s]);
+                for (uint32_t kk = 0; kk < 8; ++kk)  // A = P_b from TMEM: 16 keys = 8 packed columns
+                    tc::mma_bf16_ts(tmem + 256, tmem + s * 128 + kk * 8, tc::desc_mn_sw128(va + kk * 2048, kHalf),
+                                    idesc_o, (b > 0 || kk > 0) ? 1u : 0u);
+                tc::mma_commit(&v_empty[vs]);
                 tc::mma_commit(&o_full[s]);
-                if (b + 2 < nb) issue_s(b + 2);
+                if (b + 2 < nb) issue_s(b + 2);  // in-order after PV_b, which reads P_b from S_b's columns
             }
         }
         __syncwarp();
@@ -164,13 +173,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         // ---- softmax: 8 warps, a pair per TMEM lane quarter; warp hsel owns score columns
         // (keys) and O columns (head dims) [64*hsel, 64*hsel+64) of its 32 query rows.
         const uint32_t quarter = warp & 3;
-        const uint32_t hsel = (warp - 2) >> 2;
+        const uint32_t hsel = (warp - 3) >> 2;
         const uint32_t r = quarter * 32 + lane;
         const uint32_t qi = q0 + r;
         const bool valid = qi < p.m;
         const uint32_t limit = valid ? p.rows[qi] : 0u;
         const uint32_t lane_base = (quarter * 32u) << 16;
-        const uint32_t xchg = tmem + lane_base + 384;  // partner exchange columns 384..391
+        const uint32_t xchg = tmem + lane_base + 384;
         const uint32_t bar_id = 1 + quarter;
         float m_used = -INFINITY, l = 0.0f;
         for (uint32_t b = 0; b < nb; ++b) {
@@ -180,29 +189,26 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             tc::tc_fence_after();
             const uint32_t sa = tmem + lane_base + s * 128 + hsel * 64;
             const bool masked = __any_sync(0xffffffffu, j0 + 63 > limit);
+            uint32_t v[64];
+            tc::tmem_ld32(sa, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+            tc::tmem_ld32(sa + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+            tc::tmem_ld_wait();
             float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+            if (masked) {
 #pragma unroll
-            for (uint32_t c = 0; c < 2; ++c) {
-                uint32_t v[32];
-                tc::tmem_ld32(sa + c * 32, v);
-                tc::tmem_ld_wait();
-                if (masked) {
+                for (uint32_t e = 0; e < 64; e += 4) {
+                    mx0 = j0 + e + 0 <= limit ? fmaxf(mx0, __uint_as_float(v[e + 0])) : mx0;
+                    mx1 = j0 + e + 1 <= limit ? fmaxf(mx1, __uint_as_float(v[e + 1])) : mx1;
+                    mx2 = j0 + e + 2 <= limit ? fmaxf(mx2, __uint_as_float(v[e + 2])) : mx2;
+                    mx3 = j0 + e + 3 <= limit ? fmaxf(mx3, __uint_as_float(v[e + 3])) : mx3;
+                }
+            } else {
 #pragma unroll
-                    for (uint32_t e = 0; e < 32; e += 4) {
-                        const uint32_t key = j0 + c * 32 + e;
-                        mx0 = key + 0 <= limit ? fmaxf(mx0, __uint_as_float(v[e + 0])) : mx0;
-                        mx1 = key + 1 <= limit ? fmaxf(mx1, __uint_as_float(v[e + 1])) : mx1;
-                        mx2 = key + 2 <= limit ? fmaxf(mx2, __uint_as_float(v[e + 2])) : mx2;
-                        mx3 = key + 3 <= limit ? fmaxf(mx3, __uint_as_float(v[e + 3])) : mx3;
-                    }
-                } else {
-#pragma unroll
-                    for (uint32_t e = 0; e < 32; e += 4) {
-                        mx0 = fmaxf(mx0, __uint_as_float(v[e + 0]));
-                        mx1 = fmaxf(mx1, __uint_as_float(v[e + 1]));
-                        mx2 = fmaxf(mx2, __uint_as_float(v[e + 2]));
-                        mx3 = fmaxf(mx3, __uint_as_float(v[e + 3]));
-                    }
+                for (uint32_t e = 0; e < 64; e += 4) {
+                    mx0 = fmaxf(mx0, __uint_as_float(v[e + 0]));
+                    mx1 = fmaxf(mx1, __uint_as_float(v[e + 1]));
+                    mx2 = fmaxf(mx2, __uint_as_float(v[e + 2]));
+                    mx3 = fmaxf(mx3, __uint_as_float(v[e + 3]));
                 }
             }
             // row max across the two halves, exchanged through spare TMEM columns
@@ -229,56 +235,34 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 const uint32_t oa = tmem + lane_base + 256 + hsel * 64;
 #pragma unroll
                 for (uint32_t c = 0; c < 4; ++c) {
-                    uint32_t v[16];
-                    tc::tmem_ld16(oa + c * 16, v);
+                    uint32_t o[16];
+                    tc::tmem_ld16(oa + c * 16, o);
                     tc::tmem_ld_wait();
 #pragma unroll
-                    for (uint32_t e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
-                    tc::tmem_st16(oa + c * 16, v);
+                    for (uint32_t e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                    tc::tmem_st16(oa + c * 16, o);
                 }
                 tc::tmem_st_wait();
             }
-            // P buffer s was read by PV_{b-2}
-            if (b >= 2) {
-                tc::mbar_wait(&o_full[s], ((b - 2) >> 1) & 1);
-                tc::tc_fence_after();
-            }
             const float neg_m = m_used == -INFINITY ? 0.0f : -m_used;
             const bool row_dead = m_used == -INFINITY;
-            uint8_t* prow = sP + s * kTile + hsel * kHalf + r * 128;
             float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
+            uint32_t pk[32];
 #pragma unroll
-            for (uint32_t c = 0; c < 2; ++c) {
-                uint32_t v[32];
-                tc::tmem_ld32(sa + c * 32, v);
-                tc::tmem_ld_wait();
-                float pv[32];
-#pragma unroll
-                for (uint32_t e = 0; e < 32; ++e) {
-                    float x = tc::ex2_approx(fmaf(__uint_as_float(v[e]), p.scale_log2, neg_m));
-                    if (masked) x = (j0 + c * 32 + e <= limit && !row_dead) ? x : 0.0f;
-                    pv[e] = x;
+            for (uint32_t e = 0; e < 64; e += 2) {
+                float x0 = tc::ex2_approx(fmaf(__uint_as_float(v[e]), p.scale_log2, neg_m));
+                float x1 = tc::ex2_approx(fmaf(__uint_as_float(v[e + 1]), p.scale_log2, neg_m));
+                if (masked) {
+                    x0 = (j0 + e <= limit && !row_dead) ? x0 : 0.0f;
+                    x1 = (j0 + e + 1 <= limit && !row_dead) ? x1 : 0.0f;
                 }
-#pragma unroll
-                for (uint32_t e = 0; e < 32; e += 4) {
-                    l0 += pv[e];
-                    l1 += pv[e + 1];
-                    l2 += pv[e + 2];
-                    l3 += pv[e + 3];
-                }
-#pragma unroll
-                for (uint32_t w = 0; w < 4; ++w) {
-                    const uint32_t unit = (c * 4 + w) ^ (r & 7);
-                    uint4 q4;
-                    q4.x = pack_bf16(pv[8 * w + 0], pv[8 * w + 1]);
-                    q4.y = pack_bf16(pv[8 * w + 2], pv[8 * w + 3]);
-                    q4.z = pack_bf16(pv[8 * w + 4], pv[8 * w + 5]);
-                    q4.w = pack_bf16(pv[8 * w + 6], pv[8 * w + 7]);
-                    *reinterpret_cast<uint4*>(prow + unit * 16) = q4;
-                }
+                if (e & 2) { l2 += x0; l3 += x1; } else { l0 += x0; l1 += x1; }
+                pk[e >> 1] = pack_bf16(x0, x1);
             }
             l += (l0 + l1) + (l2 + l3);
-            tc::fence_async_shared();
+            // P_b -> TMEM columns [s*128 + hsel*32, +32) of my lanes (S_b already consumed)
+            tc::tmem_st32(tmem + lane_base + s * 128 + hsel * 32, pk);
+            tc::tmem_st_wait();
             tc::tc_fence_before();
             tc::mbar_arrive(&p_full[s]);
         }
@@ -296,30 +280,30 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const float inv = l > 0.0f ? 1.0f / l : 0.0f;
 #pragma unroll
         for (uint32_t c = 0; c < 4; ++c) {
-            uint32_t v[16];
-            tc::tmem_ld16(oa + c * 16, v);
+            uint32_t o[16];
+            tc::tmem_ld16(oa + c * 16, o);
             tc::tmem_ld_wait();
             if (!valid) continue;
             const uint32_t d0 = hsel * 64 + c * 16;
             if (direct) {
-                __nv_bfloat16* o = p.out + (size_t)qi * p.h + u.head * 128u + d0;
+                __nv_bfloat16* dst = p.out + (size_t)qi * p.h + u.head * 128u + d0;
                 uint4 a, b2;
-                a.x = pack_bf16(__uint_as_float(v[0]) * inv, __uint_as_float(v[1]) * inv);
-                a.y = pack_bf16(__uint_as_float(v[2]) * inv, __uint_as_float(v[3]) * inv);
-                a.z = pack_bf16(__uint_as_float(v[4]) * inv, __uint_as_float(v[5]) * inv);
-                a.w = pack_bf16(__uint_as_float(v[6]) * inv, __uint_as_float(v[7]) * inv);
-                b2.x = pack_bf16(__uint_as_float(v[8]) * inv, __uint_as_float(v[9]) * inv);
-                b2.y = pack_bf16(__uint_as_float(v[10]) * inv, __uint_as_float(v[11]) * inv);
-                b2.z = pack_bf16(__uint_as_float(v[12]) * inv, __uint_as_float(v[13]) * inv);
-                b2.w = pack_bf16(__uint_as_float(v[14]) * inv, __uint_as_float(v[15]) * inv);
-                reinterpret_cast<uint4*>(o)[0] = a;
-                reinterpret_cast<uint4*>(o)[1] = b2;
+                a.x = pack_bf16(__uint_as_float(o[0]) * inv, __uint_as_float(o[1]) * inv);
+                a.y = pack_bf16(__uint_as_float(o[2]) * inv, __uint_as_float(o[3]) * inv);
+                a.z = pack_bf16(__uint_as_float(o[4]) * inv, __uint_as_float(o[5]) * inv);
+                a.w = pack_bf16(__uint_as_float(o[6]) * inv, __uint_as_float(o[7]) * inv);
+                b2.x = pack_bf16(__uint_as_float(o[8]) * inv, __uint_as_float(o[9]) * inv);
+                b2.y = pack_bf16(__uint_as_float(o[10]) * inv, __uint_as_float(o[11]) * inv);
+                b2.z = pack_bf16(__uint_as_float(o[12]) * inv, __uint_as_float(o[13]) * inv);
+                b2.w = pack_bf16(__uint_as_float(o[14]) * inv, __uint_as_float(o[15]) * inv);
+                reinterpret_cast<uint4*>(dst)[0] = a;
+                reinterpret_cast<uint4*>(dst)[1] = b2;
             } else {
-                float4* o = reinterpret_cast<float4*>(p.part_o + ((size_t)u.slot * 128 + r) * 128 + d0);
+                float4* dst = reinterpret_cast<float4*>(p.part_o + ((size_t)u.slot * 128 + r) * 128 + d0);
 #pragma unroll
                 for (uint32_t e = 0; e < 4; ++e)
-                    o[e] = make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]),
-                                       __uint_as_float(v[4 * e + 2]), __uint_as_float(v[4 * e + 3]));
+                    dst[e] = make_float4(__uint_as_float(o[4 * e]), __uint_as_float(o[4 * e + 1]),
+                                         __uint_as_float(o[4 * e + 2]), __uint_as_float(o[4 * e + 3]));
             }
         }
         if (valid && !direct && hsel == 0) p.part_ml[(size_t)u.slot * 128 + r] = make_float2(m_used, l);
@@ -330,42 +314,51 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-// Merge split partials of one (tile, head): O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s
-__global__ void __launch_bounds__(128) attn_combine_kernel(const AttnCombine* __restrict__ jobs,
+// Merge split partials of one (tile, head): O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s.
+// One warp per query row (blockIdx.y picks 8 rows of the job), lanes along the head
+// dimension: coalesced 512-B partial reads, 256-B bf16 output rows; all loads of a row
+// are issued before they are consumed.
+__global__ void __launch_bounds__(256) attn_combine_kernel(const AttnCombine* __restrict__ jobs,
                                                            const float* __restrict__ part_o,
                                                            const float2* __restrict__ part_ml,
                                                            uint32_t m, uint32_t h,
                                                            __nv_bfloat16* __restrict__ out) {
+    constexpr uint32_t kMaxSplits = 16;
     const AttnCombine j = jobs[blockIdx.x];
-    const uint32_t r = threadIdx.x;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t r = blockIdx.y * 8 + warp;
     const uint32_t qi = j.tile * 128u + r;
     if (qi >= m) return;
-    float M = -INFINITY;
-    for (uint32_t s = 0; s < j.n; ++s) M = fmaxf(M, part_ml[(size_t)(j.slot0 + s) * 128 + r].x);
-    float L = 0.0f;
-    for (uint32_t s = 0; s < j.n; ++s) {
-        const float2 ml = part_ml[(size_t)(j.slot0 + s) * 128 + r];
-        L += (ml.x == -INFINITY ? 0.0f : exp2f(ml.x - M)) * ml.y;
-    }
-    const float inv = L > 0.0f ? 1.0f / L : 0.0f;
-    __nv_bfloat16* o = out + (size_t)qi * h + j.head * 128u;
-    for (uint32_t d = 0; d < 128; d += 4) {
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (uint32_t s = 0; s < j.n; ++s) {
-            const float mls = part_ml[(size_t)(j.slot0 + s) * 128 + r].x;
-            const float ws = mls == -INFINITY ? 0.0f : exp2f(mls - M);
-            if (ws == 0.0f) continue;
-            const float4 v = *reinterpret_cast<const float4*>(part_o + ((size_t)(j.slot0 + s) * 128 + r) * 128 + d);
-            acc.x += ws * v.x;
-            acc.y += ws * v.y;
-            acc.z += ws * v.z;
-            acc.w += ws * v.w;
+    const uint32_t n = min(j.n, kMaxSplits);
+    float2 ml[kMaxSplits];
+    float4 ov[kMaxSplits];
+#pragma unroll
+    for (uint32_t s = 0; s < kMaxSplits; ++s)
+        if (s < n) {
+            ml[s] = __ldcg(part_ml + (size_t)(j.slot0 + s) * 128 + r);
+            ov[s] = __ldcs(reinterpret_cast<const float4*>(part_o + ((size_t)(j.slot0 + s) * 128 + r) * 128) + lane);
         }
-        o[d] = __float2bfloat16_rn(acc.x * inv);
-        o[d + 1] = __float2bfloat16_rn(acc.y * inv);
-        o[d + 2] = __float2bfloat16_rn(acc.z * inv);
-        o[d + 3] = __float2bfloat16_rn(acc.w * inv);
-    }
+    float M = -INFINITY;
+#pragma unroll
+    for (uint32_t s = 0; s < kMaxSplits; ++s)
+        if (s < n) M = fmaxf(M, ml[s].x);
+    float L = 0.0f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (uint32_t s = 0; s < kMaxSplits; ++s)
+        if (s < n) {
+            const float w = ml[s].x == -INFINITY ? 0.0f : exp2f(ml[s].x - M);
+            L += w * ml[s].y;
+            acc.x += w * ov[s].x;
+            acc.y += w * ov[s].y;
+            acc.z += w * ov[s].z;
+            acc.w += w * ov[s].w;
+        }
+    const float inv = L > 0.0f ? 1.0f / L : 0.0f;
+    uint2 pk;
+    pk.x = pack_bf16(acc.x * inv, acc.y * inv);
+    pk.y = pack_bf16(acc.z * inv, acc.w * inv);
+    reinterpret_cast<uint2*>(out + (size_t)qi * h + j.head * 128u)[lane] = pk;
 }
 
 }  // namespace
@@ -383,6 +376,9 @@ AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads) {
     }
     // ~3 waves of units; never split below 2 blocks per unit
     uint32_t chunk = (uint32_t)std::max<uint64_t>(2, (total + 3 * kNumSMs - 1) / (3 * kNumSMs));
+    uint32_t longest = 0;
+    for (uint32_t t = 0; t < tiles; ++t) longest = std::max(longest, nblk[t]);
+    chunk = std::max(chunk, ceil_div(longest, 16));  // the combine merges at most 16 splits
     uint32_t slot = 0;
     for (uint32_t t = 0; t < tiles; ++t) {
         const uint32_t splits = ceil_div(nblk[t], chunk);
@@ -425,7 +421,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     p.out = out;
     p.part_o = part_o;
     p.part_ml = part_ml;
-    const size_t smem = 7 * kTile + 1024 + 16 * 8 + 16;
+    const size_t smem = (1 + 2 * kKvStages) * kTile + 1024 + (1 + 4 * kKvStages + 6) * 8 + 16;
     static bool attr = false;
     if (!attr) {
         MPIC_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -434,7 +430,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     attn_tc_kernel<<<n_units, kAttnThreads, smem, s>>>(tmQ, tmK, tmV, p);
     MPIC_LAUNCHED();
     if (n_combine) {
-        attn_combine_kernel<<<n_combine, 128, 0, s>>>(d_combine, part_o, part_ml, m, h, out);
+        attn_combine_kernel<<<dim3(n_combine, 16), 256, 0, s>>>(d_combine, part_o, part_ml, m, h, out);
         MPIC_LAUNCHED();
     }
 }

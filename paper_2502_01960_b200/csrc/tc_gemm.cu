@@ -501,6 +501,210 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (warp == 1) tc::tmem_dealloc(tmem_base, a.tmem_cols);
 }
 
+
+// ---- stream-K persistent GEMM (the production path) ----------------------------------------
+// One CTA per SM walks a contiguous range of the (tile, k-block) work list, so every SM
+// gets the same number of k-blocks whatever the tile count (W1 at m=330 has 192 tiles of
+// 128 tokens x 256 features: 1.3 waves as a plain grid). Tiles are ordered m-fastest, so the
+// CTAs running concurrently share weight tiles in L2. A tile cut between CTAs is finished by
+// the CTA that owns its first k-block (it reaches it last); the others publish fp32
+// partials in their per-CTA slot and raise an epoch flag. The owner adds the partials in
+// CTA order (deterministic) and runs the fused epilogue. TMEM holds two accumulators so the
+// epilogue of one segment overlaps the MMAs of the next.
+struct SkArgs {
+    uint32_t M, N, K;
+    uint32_t bn, mt;        // feature tile, number of 128-token tiles
+    uint32_t kblocks;       // per tile
+    uint64_t work;          // tiles * kblocks
+    uint32_t ctas;          // persistent CTAs
+    uint32_t stages;
+    float* partial;         // [ctas][2 segments][128][bn] fp32
+    uint32_t* counters;     // [tiles] arrivals per split tile
+    EpiParams ep;
+};
+
+__device__ __forceinline__ uint32_t sk_cta_of(uint64_t x, uint64_t work, uint32_t ctas) {
+    // largest c with floor(c*work/ctas) <= x
+    return (uint32_t)(((x + 1) * ctas + work - 1) / work) - 1;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    tc_gemm_sk_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                      const SkArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t stage_bytes = kXBoxBytes + a.bn * 128;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
+    uint64_t* empty = full + a.stages;
+    uint64_t* acc_full = empty + a.stages;   // [2]
+    uint64_t* acc_empty = acc_full + 2;      // [2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    __shared__ uint32_t s_last;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t c = blockIdx.x;
+    const uint64_t u_begin = (uint64_t)c * a.work / a.ctas, u_end = (uint64_t)(c + 1) * a.work / a.ctas;
+
+    if (warp == 0 && lane == 0) {
+        tc::tma_prefetch_desc(&tmX);
+        tc::tma_prefetch_desc(&tmW);
+        for (uint32_t s = 0; s < a.stages; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&acc_full[i], 1);
+            tc::mbar_init(&acc_empty[i], 128);
+        }
+        tc::fence_barrier_init();
+    }
+    const uint32_t tmem_cols = 2 * a.bn < 32 ? 32 : 2 * a.bn;
+    if (warp == 1) tc::tmem_alloc(tmem_holder, tmem_cols);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_w = tc::policy_evict_first();
+            const uint64_t pol_x = tc::policy_evict_last();
+            uint32_t i = 0;
+            for (uint64_t u = u_begin; u < u_end; ++u, ++i) {
+                const uint32_t tile = (uint32_t)(u / a.kblocks), kb = (uint32_t)(u % a.kblocks);
+                const uint32_t t0 = (tile % a.mt) * 128, n0 = (tile / a.mt) * a.bn;
+                const uint32_t s = i % a.stages, ph = (i / a.stages) & 1;
+                tc::mbar_wait(&empty[s], ph ^ 1);
+                tc::mbar_arrive_expect_tx(&full[s], stage_bytes);
+                uint8_t* st = smem + s * stage_bytes;
+                tc::tma_load_2d_hint(st, &tmX, &full[s], (int)(kb * 64), (int)t0, pol_x);
+                tc::tma_load_2d_hint(st + kXBoxBytes, &tmW, &full[s], (int)(kb * 64), (int)n0, pol_w);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = tc::idesc_bf16(128, a.bn);
+            uint32_t i = 0, seg = 0;
+            uint64_t u = u_begin;
+            while (u < u_end) {
+                const uint32_t kb_begin = (uint32_t)(u % a.kblocks);
+                const uint64_t seg_end = u_end < u - kb_begin + a.kblocks ? u_end : u - kb_begin + a.kblocks;
+                const uint32_t buf = seg & 1;
+                tc::mbar_wait(&acc_empty[buf], ((seg >> 1) & 1) ^ 1);
+                tc::tc_fence_after();
+                const uint32_t d = tmem_base + buf * a.bn;
+                for (; u < seg_end; ++u, ++i) {
+                    const uint32_t s = i % a.stages, ph = (i / a.stages) & 1;
+                    tc::mbar_wait(&full[s], ph);
+                    tc::tc_fence_after();
+                    const uint32_t x_base = tc::smem_u32(smem + s * stage_bytes);
+                    const uint32_t w_base = x_base + kXBoxBytes;
+                    const bool first = (u % a.kblocks) == kb_begin;
+#pragma unroll
+                    for (uint32_t kk = 0; kk < 4; ++kk)
+                        tc::mma_bf16(d, tc::desc_k_sw128(x_base + kk * 32), tc::desc_k_sw128(w_base + kk * 32), idesc,
+                                     (!first || kk > 0) ? 1u : 0u);
+                    tc::mma_commit(&empty[s]);
+                }
+                tc::mma_commit(&acc_full[buf]);
+                ++seg;
+            }
+        }
+        __syncwarp();
+    } else {
+        const uint32_t q = warp & 3;
+        const uint32_t row = q * 32 + lane;
+        uint32_t seg = 0;
+        uint64_t u = u_begin;
+        while (u < u_end) {
+            const uint32_t tile = (uint32_t)(u / a.kblocks), kb_begin = (uint32_t)(u % a.kblocks);
+            const uint64_t tile_end = (uint64_t)(tile + 1) * a.kblocks;
+            const uint64_t seg_end = u_end < tile_end ? u_end : tile_end;
+            const bool whole = kb_begin == 0 && seg_end == tile_end;
+            const bool owner = kb_begin == 0;
+            const uint32_t t0 = (tile % a.mt) * 128, n0 = (tile / a.mt) * a.bn;
+            const uint32_t t = t0 + row;
+            const uint32_t buf = seg & 1;
+            tc::mbar_wait(&acc_full[buf], (seg >> 1) & 1);
+            tc::tc_fence_after();
+            const uint32_t d = tmem_base + buf * a.bn + ((q * 32u) << 16);
+            (void)owner;
+            if (whole) {
+                for (uint32_t cc = 0; cc < a.bn; cc += 32) {
+                    uint32_t r[32];
+                    tc::tmem_ld32(d + cc, r);
+                    tc::tmem_ld_wait();
+                    float v[32];
+#pragma unroll
+                    for (uint32_t i2 = 0; i2 < 32; ++i2) v[i2] = __uint_as_float(r[i2]);
+                    if (t < a.M) tok_epilogue_chunk(a.ep, t, n0 + cc, v);
+                }
+            } else {
+                // Split tile: publish this segment's partial, then the LAST segment to arrive
+                // (tile counter) sums all partials in CTA order and runs the epilogue. Nobody
+                // waits on another CTA, so co-residency is not required.
+                // slot layout [bn/4 float4 columns][128 rows]: a warp's access is 512 contiguous bytes
+                const uint32_t my_slot = (u == u_begin) ? 0u : 1u;
+                float4* mine = reinterpret_cast<float4*>(a.partial + ((size_t)c * 2 + my_slot) * 128 * a.bn) + row;
+                for (uint32_t cc = 0; cc < a.bn; cc += 32) {
+                    uint32_t r[32];
+                    tc::tmem_ld32(d + cc, r);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (uint32_t i2 = 0; i2 < 8; ++i2)
+                        __stcg(mine + (size_t)(cc / 4 + i2) * 128,
+                               make_float4(__uint_as_float(r[4 * i2]), __uint_as_float(r[4 * i2 + 1]),
+                                           __uint_as_float(r[4 * i2 + 2]), __uint_as_float(r[4 * i2 + 3])));
+                }
+                __threadfence();
+                tc::named_bar_sync(1, 128);
+                const uint32_t c0 = sk_cta_of((uint64_t)tile * a.kblocks, a.work, a.ctas);
+                const uint32_t c1 = sk_cta_of(tile_end - 1, a.work, a.ctas);
+                if (row == 0) {
+                    const uint32_t old = atomicAdd(a.counters + tile, 1u);
+                    const bool last = old == c1 - c0;
+                    if (last) a.counters[tile] = 0;  // ready for the next launch
+                    __threadfence();
+                    s_last = last ? 1u : 0u;
+                }
+                tc::named_bar_sync(1, 128);
+                if (s_last) {
+                    const uint64_t c0_begin = (uint64_t)c0 * a.work / a.ctas;
+                    for (uint32_t cc = 0; cc < a.bn; cc += 32) {
+                        float v[32];
+#pragma unroll
+                        for (uint32_t i2 = 0; i2 < 32; ++i2) v[i2] = 0.0f;
+                        for (uint32_t p = c0; p <= c1; ++p) {
+                            // tile == CTA p's first segment unless p == c0 started earlier
+                            const uint32_t slot = (p == c0 && c0_begin < (uint64_t)tile * a.kblocks) ? 1u : 0u;
+                            const float4* src = reinterpret_cast<const float4*>(
+                                a.partial + ((size_t)p * 2 + slot) * 128 * a.bn) + row;
+#pragma unroll
+                            for (uint32_t i2 = 0; i2 < 8; ++i2) {
+                                const float4 w = __ldcg(src + (size_t)(cc / 4 + i2) * 128);
+                                v[4 * i2] += w.x;
+                                v[4 * i2 + 1] += w.y;
+                                v[4 * i2 + 2] += w.z;
+                                v[4 * i2 + 3] += w.w;
+                            }
+                        }
+                        if (t < a.M) tok_epilogue_chunk(a.ep, t, n0 + cc, v);
+                    }
+                }
+            }
+            tc::tc_fence_before();
+            tc::mbar_arrive(&acc_empty[buf]);
+            u = seg_end;
+            ++seg;
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    if (warp == 1) tc::tmem_dealloc(tmem_base, tmem_cols);
+}
+
 // x += sum_z partial[z]; xb = bf16(x) — the deterministic split-K reduction, fused with
 // the cast that produces the next GEMM's bf16 operand.
 __global__ void __launch_bounds__(256) resid_reduce_kernel(const float* __restrict__ partial,
@@ -706,14 +910,79 @@ void launch_pair(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uin
 }
 }  // namespace
 
+namespace {
+struct SkWorkspace {
+    float* partial = nullptr;
+    uint32_t* counters = nullptr;
+    size_t cap = 0, tiles_cap = 0;
+};
+
+void launch_sk(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint32_t N, uint32_t K,
+               const EpiParams& ep_in, cudaStream_t s) {
+    static std::mutex mu;
+    static SkWorkspace ws[16];
+    int dev = 0;
+    MPIC_CUDA(cudaGetDevice(&dev));
+    SkArgs a{};
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.bn = N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : 64;
+    a.mt = ceil_div(M, 128);
+    a.kblocks = K / 64;
+    a.work = (uint64_t)(N / a.bn) * a.mt * a.kblocks;
+    a.ctas = (uint32_t)std::min<uint64_t>(kNumSMs, a.work);
+    const uint32_t stage_bytes = kXBoxBytes + a.bn * 128;
+    const uint32_t budget = 227 * 1024 - 1024 - 512;
+    a.stages = std::min<uint32_t>(8, budget / stage_bytes);
+    a.ep = ep_in;
+    a.ep.split_k = 1;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        // NOTE: one scratch per device; concurrent launches on different streams of the
+        // same device would share it (the library serialises a request on one stream).
+        SkWorkspace& w = ws[dev & 15];
+        const size_t need = (size_t)kNumSMs * 2 * 128 * 256;
+        const size_t tiles = (size_t)(N / a.bn) * a.mt;
+        if (w.cap < need) {
+            MPIC_CUDA(cudaMalloc(&w.partial, need * sizeof(float)));
+            w.cap = need;
+        }
+        if (w.tiles_cap < tiles) {
+            if (w.counters) MPIC_CUDA(cudaFree(w.counters));
+            w.tiles_cap = std::max<size_t>(tiles, 4096);
+            MPIC_CUDA(cudaMalloc(&w.counters, w.tiles_cap * sizeof(uint32_t)));
+            MPIC_CUDA(cudaMemset(w.counters, 0, w.tiles_cap * sizeof(uint32_t)));
+        }
+        a.partial = w.partial;
+        a.counters = w.counters;
+    }
+    const CUtensorMap tmX = make_tmap_bf16(A, K, M, 64, 128);
+    const CUtensorMap tmW = make_tmap_bf16(W, K, N, 64, a.bn);
+    const size_t smem = (size_t)a.stages * stage_bytes + 1024 + (2 * a.stages + 4) * 8 + 16;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        MPIC_CUDA(cudaFuncSetAttribute(tc_gemm_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 64));
+    });
+    tc_gemm_sk_kernel<<<a.ctas, kTcThreads, smem, s>>>(tmX, tmW, a);
+    MPIC_LAUNCHED();
+}
+}  // namespace
+
 void launch_gemm_tc(const __nv_bfloat16* A, uint32_t lda, const __nv_bfloat16* W, uint32_t M,
                     uint32_t N, uint32_t K, const EpiParams& ep_in, cudaStream_t s) {
     MPIC_REQUIRE(tc_gemm_supported(M, N, K) && lda == K, MPIC_ERR_VALIDATION, "unsupported tc gemm shape");
-    static const char* variant = getenv("MPIC_GEMM_VARIANT");  // diagnostics: "swap", "pair"
-    if (!variant || (variant[0] != 's' && variant[0] != 'p')) {
+    static const char* variant = getenv("MPIC_GEMM_VARIANT");  // diagnostics: "tok", "wswap", "pair"
+    if (!variant || (variant[0] != 'w' && variant[0] != 'p')) {
         MPIC_REQUIRE(ep_in.mode != EPI_QKV || (ep_in.head_dim % 32 == 0 && ep_in.hidden % 32 == 0),
                      MPIC_ERR_VALIDATION, "tc gemm QKV epilogue needs head_dim % 32 == 0");
-        launch_tok(A, W, M, N, K, ep_in, s);
+        const uint32_t bn = N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : 64;
+        const uint32_t tiles = (N / bn) * ceil_div(M, 128);
+        const bool one_wave = tiles <= (uint32_t)kNumSMs && tiles * 8 >= (uint32_t)kNumSMs * 7;
+        if (variant && variant[0] == 't') launch_tok(A, W, M, N, K, ep_in, s);
+        else if (variant && variant[0] == 's') launch_sk(A, W, M, N, K, ep_in, s);
+        else if (one_wave) launch_tok(A, W, M, N, K, ep_in, s);
+        else launch_sk(A, W, M, N, K, ep_in, s);
         return;
     }
     MPIC_REQUIRE(N % 128 == 0, MPIC_ERR_VALIDATION, "swap-AB gemm needs N % 128 == 0");

@@ -2,6 +2,8 @@
 reference of the same bf16 operands (fp32 accumulation both sides)."""
 import ctypes as C
 
+import numpy as np
+
 import pytest
 import torch
 
@@ -34,3 +36,40 @@ def test_gemm_vs_torch(M, N, K, path):
     out = run_gemm(a, w, path)
     err = (out - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-5, err
+
+
+def run_attention(q, k, v, rows, H):
+    m, n = q.shape[0], k.shape[0]
+    out = torch.zeros(m, H * 128, dtype=torch.bfloat16, device="cuda")
+    r = np.ascontiguousarray(rows, np.uint32)
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.lib().mpic_test_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), r.ctypes.data,
+                                              m, n, H, out.data_ptr(), s))
+    torch.cuda.synchronize()
+    return out
+
+
+def attention_ref(q, k, v, rows, H):
+    """Plain PyTorch fp32: softmax(q k^T / sqrt(128)) v with key j <= rows[i]."""
+    m, n = q.shape[0], k.shape[0]
+    qf = q.float().view(m, H, 128).transpose(0, 1)
+    kf = k.float().view(n, H, 128).transpose(0, 1)
+    vf = v.float().view(n, H, 128).transpose(0, 1)
+    s = (qf @ kf.transpose(1, 2)) * (1.0 / 128 ** 0.5)
+    mask = torch.arange(n, device="cuda")[None, :] > torch.as_tensor(rows.astype(np.int64), device="cuda")[:, None]
+    s = s.masked_fill(mask[None], float("-inf"))
+    return (torch.softmax(s, -1) @ vf).transpose(0, 1).reshape(m, H * 128)
+
+
+@pytest.mark.parametrize("n,m,H", [(300, 40, 2), (1000, 130, 3), (9418, 330, 4), (4000, 600, 1)])
+def test_attention_vs_torch(n, m, H):
+    g = torch.Generator(device="cuda").manual_seed(n + m)
+    q = torch.randn(m, H * 128, device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn(n, H * 128, device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn(n, H * 128, device="cuda", generator=g).to(torch.bfloat16)
+    rows = np.sort(np.random.default_rng(m).choice(n - 1, m - 1, replace=False)).astype(np.uint32)
+    rows = np.append(rows, n - 1).astype(np.uint32)
+    out = run_attention(q, k, v, rows, H)
+    ref = attention_ref(q, k, v, rows, H)
+    err = (out.float() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-2, err
