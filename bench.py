@@ -26,7 +26,6 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 
 import numpy as np
@@ -72,56 +71,56 @@ def build_prompt(cfg_name, V, seed=42):
 
 
 class ClockSampler:
-    """nvidia-smi-equivalent clock/throttle sampling (NVML) during the timed region."""
+    """Clocks and throttle reasons DURING the timed region, sampled by an `nvidia-smi -lms`
+    subprocess (B200_PROFILING.md recipe) so no Python thread competes with the timed loop."""
 
-    def __init__(self, device_index=0, period=0.1):
-        self.samples, self.reasons = [], set()
-        self.max_mhz = None
-        self.period = period
-        self._stop = threading.Event()
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception:
-            self.nv = None
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
 
-    def _run(self):
-        nv = self.nv
-        names = {
-            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
-            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
-            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
-        }
-        while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for n, bit in names.items():
-                    if r & bit and n != "gpu_idle":
-                        self.reasons.add(n)
-            except Exception:
-                pass
-            time.sleep(self.period)
+    def __init__(self, device_index=0, period_ms=100):
+        self.dev, self.period = device_index, period_ms
+        self.proc, self.rows = None, []
 
     def __enter__(self):
-        if self.nv:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+        import subprocess
+        import tempfile
+        self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", f"-lms={self.period}"],
+                stdout=self.out, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self.nv:
-            self.t.join()
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.out.seek(0)
+            for line in self.out.read().splitlines():
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) == 6:
+                    self.rows.append(parts)
+        try:
+            os.unlink(self.out.name)
+        except Exception:
+            pass
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
-        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.strip().lower() == "active"})
+        return {"sm_mhz": float(statistics.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
 
 
 def dist_setup(n_gpus):
@@ -189,17 +188,17 @@ def run_ours(args, world, rank, local):
     host_k, host_v, dev_chunks = [], [], []
     g = np.random.default_rng(1234 + rank)
     for t in images:
-        hk, hv = mp.HostBuffer((L, t, h)), mp.HostBuffer((L, t, h))
         rk = g.random((t, h), dtype=np.float32) - 0.5  # U(-0.5, 0.5), one draw per chunk
         rv = g.random((t, h), dtype=np.float32) - 0.5
-        for l in range(L):
-            hk.array[l] = rk
-            hv.array[l] = rv
         kv = mp.KV(L, t, H, D, mp.BF16, dev)
-        kv.upload(hk.array, hv.array)
-        host_k.append(hk)
-        host_v.append(hv)
+        kv.upload(np.broadcast_to(rk, (L, t, h)), np.broadcast_to(rv, (L, t, h)))
         dev_chunks.append(kv)
+        if not args.no_e2e:  # the Host tier copy the e2e leg streams from (pinned fp32)
+            hk, hv = mp.HostBuffer((L, t, h)), mp.HostBuffer((L, t, h))
+            hk.array[:] = rk
+            hv.array[:] = rv
+            host_k.append(hk)
+            host_v.append(hv)
     linked = mp.KV(L, n, H, D, mp.BF16, dev)
 
     def step_device():
@@ -223,12 +222,15 @@ def run_ours(args, world, rank, local):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     launches = 0
     per_step = []
+    host_ms = []
     with ClockSampler(dev) as clk:
         with torch.cuda.stream(stream):
             ev[0].record(stream)
             for i in range(args.steps):
+                h0 = time.perf_counter()
                 launches += step_device()
                 ev[i + 1].record(stream)
+                host_ms.append((time.perf_counter() - h0) * 1e3)
         torch.cuda.synchronize()
     barrier(world)
     mp.profile_enable(False)
@@ -315,7 +317,7 @@ def run_ours(args, world, rank, local):
     floor_ms = (asm_bytes / (hbm * 1e9) + L * (
         max(sum(gemm_fl.values()) / (tf_sust * 1e12), sum(gemm_b.values()) / (hbm * 1e9)) +
         attn_fl / (tf_sust * 1e12))) * 1e3
-    return dict(value=value, ms_per_step=ms_per_step, per_step=per_step, e2e=e2e,
+    return dict(value=value, ms_per_step=ms_per_step, per_step=per_step, host_ms=host_ms, e2e=e2e,
                 launches=launches, roofline=roofline, phases=per_phase, clocks=clk.summary(),
                 n=n, m=m, floor_ms=floor_ms, world=world)
 
@@ -421,7 +423,9 @@ def main():
                 "config": dict(cfg_json, n_tokens=r["n"], recompute_rows=r["m"]),
                 "e2e": r["e2e"], "gpu_launches": r["launches"], "roofline": r["roofline"],
                 "request_roofline_frac": round(r["floor_ms"] / r["ms_per_step"], 4),
-                "phases": r["phases"], "cpu_baseline": cpu, "clocks": r["clocks"]}
+                "phases": r["phases"], "cpu_baseline": cpu, "clocks": r["clocks"],
+                "step_ms": [round(x, 3) for x in r["per_step"]],
+                "host_ms": [round(x, 3) for x in r["host_ms"]]}
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist

@@ -96,6 +96,10 @@ int mpic_kv_device_ptrs(mpic_kv_t kv, void** k, void** v);
  * Synchronous on `stream`. */
 int mpic_kv_upload(mpic_kv_t kv, const float* k, const float* v, void* stream);
 int mpic_kv_download(mpic_kv_t kv, float* k, float* v, void* stream);
+/* Download only cache rows rows[0..n_rows) of every layer into host k/v laid out as the
+ * full [L][T][H*D] tensor (other rows untouched). Synchronous. */
+int mpic_kv_download_rows(mpic_kv_t kv, const uint32_t* rows, uint32_t n_rows, float* k, float* v,
+                          void* stream);
 /* Zero-fill rows [row0, row0+rows) of every layer (async). */
 int mpic_kv_zero_rows(mpic_kv_t kv, uint32_t row0, uint32_t rows, void* stream);
 
@@ -225,9 +229,16 @@ int mpic_host_alloc(size_t bytes, void** out);
 int mpic_host_free(void* p);
 
 /* Test hook: out[M][N] (fp32, device) = A[M][K] . W[N][K]^T for bf16 device operands,
- * through the tcgen05 GEMM (path 1) or the SIMT GEMM (path 0). Async on `stream`. */
+ * through the tcgen05 GEMM (path 1), the tcgen05 GEMM on a blocked copy of W made on the
+ * device (path 2), the tcgen05 GEMM with d_w already blocked [N/128][K/64][128][64]
+ * (path 3) or the SIMT GEMM (path 0). Async on `stream`. */
 int mpic_test_gemm(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uint32_t K, int path,
                    float* d_out, void* stream);
+/* Test hook: the tcgen05 GEMM with a fused epilogue. mode 0: residual (d_x fp32 [M][N]
+ * += A.W^T, d_xb bf16 copy of the new x); mode 1: GELU (d_out bf16 [M][N]); mode 2: plain
+ * bf16 store (d_out). Async on `stream`. */
+int mpic_test_gemm_epi(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uint32_t K, int mode,
+                       float* d_x, void* d_xb, void* d_out, void* stream);
 
 /* ---- per-phase device timing ------------------------------------------------------ */
 typedef enum {

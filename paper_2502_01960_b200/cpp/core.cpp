@@ -191,18 +191,57 @@ DeviceModel::DeviceModel(const Model& m) {
 }
 DeviceModel::~DeviceModel() { mpic_model_destroy(h_); }
 
+namespace {
+struct KvPoolEntry {
+    uint32_t L, T, H, D;
+    mpic_kv_t h;
+};
+struct KvPool {
+    std::vector<KvPoolEntry> free;
+    ~KvPool() {
+        for (const KvPoolEntry& e : free) mpic_kv_free(e.h);
+    }
+};
+thread_local KvPool t_kv_pool;
+}  // namespace
+
 DeviceKv::DeviceKv(uint32_t layers, uint32_t tokens, uint32_t heads, uint32_t dim) {
+    auto& pool = t_kv_pool.free;
+    for (auto it = pool.begin(); it != pool.end(); ++it)
+        if (it->L == layers && it->T == tokens && it->H == heads && it->D == dim) {
+            h_ = it->h;
+            pool.erase(it);
+            return;
+        }
     check(mpic_kv_alloc(layers, tokens, heads, dim, MPIC_F32, device(), &h_));
 }
 DeviceKv::DeviceKv(const KvTensor& t) : DeviceKv(t.n_layers, t.n_tokens, t.n_heads, t.head_dim) {
     upload(t);
 }
-DeviceKv::~DeviceKv() { mpic_kv_free(h_); }
+DeviceKv::~DeviceKv() {
+    uint32_t shape[4];
+    mpic_dtype dt;
+    auto& pool = t_kv_pool.free;
+    if (h_ && mpic_kv_shape(h_, shape, &dt) == MPIC_OK) {
+        pool.push_back({shape[0], shape[1], shape[2], shape[3], h_});
+        if (pool.size() > 8) {
+            mpic_kv_free(pool.front().h);
+            pool.erase(pool.begin());
+        }
+    } else {
+        mpic_kv_free(h_);
+    }
+}
 void DeviceKv::upload(const KvTensor& t) {
     if (!t.k.empty()) check(mpic_kv_upload(h_, t.k.data(), t.v.data(), nullptr));
 }
 void DeviceKv::download(KvTensor& t) const {
     if (!t.k.empty()) check(mpic_kv_download(h_, t.k.data(), t.v.data(), nullptr));
+}
+void DeviceKv::download_rows(KvTensor& t, std::span<const uint32_t> rows) const {
+    if (!t.k.empty() && !rows.empty())
+        check(mpic_kv_download_rows(h_, rows.data(), static_cast<uint32_t>(rows.size()), t.k.data(), t.v.data(),
+                                    nullptr));
 }
 
 Workspace::Workspace(const DeviceModel& m, uint32_t rows, uint32_t ctx) : rows_(std::max(rows, 1u)), ctx_(ctx) {

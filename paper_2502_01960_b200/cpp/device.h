@@ -8,6 +8,7 @@
 #include "mpic_b200.h"
 
 #include <memory>
+#include <span>
 #include <string>
 
 namespace mpic::b200 {
@@ -30,6 +31,8 @@ private:
     mpic_model_t h_ = nullptr;
 };
 
+// Device KV tensors are recycled through a small per-thread pool keyed by shape, so the
+// value-semantic API does not pay a cudaMalloc/cudaFree pair per call.
 class DeviceKv {
 public:
     DeviceKv(uint32_t layers, uint32_t tokens, uint32_t heads, uint32_t dim);
@@ -39,6 +42,8 @@ public:
     DeviceKv& operator=(const DeviceKv&) = delete;
     void upload(const KvTensor& t);
     void download(KvTensor& t) const;  // t must have the matching shape
+    // Only rows[] of every layer (the rows a selective pass rewrote).
+    void download_rows(KvTensor& t, std::span<const uint32_t> rows) const;
     mpic_kv_t get() const { return h_; }
 
 private:

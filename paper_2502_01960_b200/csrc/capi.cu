@@ -98,6 +98,7 @@ struct mpic_workspace_s {
     uint32_t* d_rows = nullptr;
     uint32_t* d_pos = nullptr;
     float* x = nullptr;                 // residual stream fp32 [m_pad][h]
+    float2* rope_tok = nullptr;         // (cos, sin) of each row's position [m_pad][D/2]
     __nv_bfloat16* xb = nullptr;        // bf16 copy of x (GEMM A operand, bf16 mode)
     void* q = nullptr;                  // [m_pad][h] dtype
     void* attn = nullptr;               // [m_pad][h] dtype
@@ -381,6 +382,7 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
         ProfScope ps(s, MPIC_PHASE_EMBED);
         launch_embed(md->emb, d_ids, m, h, ws->x, bf ? ws->xb : nullptr, s);
     }
+    if (bf) launch_rope_gather(md->rope, d_pos, m, D / 2, ws->rope_tok, s);
     const bool tc_attn = use_tc_attention(md);
     if (tc_attn) upload_attn_plan(ws, h_rows, m, max_pos, H, s);
     for (uint32_t l = 0; l < c.n_layers; ++l) {
@@ -395,6 +397,7 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
         qkv.kv_rows = d_rows;
         qkv.rope_pos = d_pos;
         qkv.rope = md->rope;
+        qkv.rope_tok = bf ? ws->rope_tok : nullptr;
         qkv.hidden = h;
         qkv.head_dim = D;
         {
@@ -919,6 +922,35 @@ int mpic_kv_upload(mpic_kv_t kv, const float* k, const float* v, void* stream) {
     API_END
 }
 
+int mpic_kv_download_rows(mpic_kv_t kv, const uint32_t* rows, uint32_t n_rows, float* k, float* v,
+                          void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(kv->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n_rows == 0) return MPIC_OK;
+    const size_t h = (size_t)kv->H * kv->D, per = (size_t)kv->L * n_rows * h;
+    for (uint32_t i = 0; i < n_rows; ++i)
+        MPIC_REQUIRE(rows[i] < kv->T, MPIC_ERR_VALIDATION, "row index outside the cache");
+    uint32_t* d_rows = nullptr;
+    float* stage = nullptr;
+    MPIC_CUDA(cudaMallocAsync((void**)&d_rows, n_rows * sizeof(uint32_t), s));
+    MPIC_CUDA(cudaMallocAsync((void**)&stage, 2 * per * sizeof(float), s));
+    MPIC_CUDA(cudaMemcpyAsync(d_rows, rows, n_rows * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    launch_gather_rows(kv->k, kv->v, kv->dtype, kv->L, kv->T, (uint32_t)h, d_rows, n_rows, stage, stage + per, s);
+    std::vector<float> host(2 * per);
+    MPIC_CUDA(cudaMemcpyAsync(host.data(), stage, 2 * per * sizeof(float), cudaMemcpyDeviceToHost, s));
+    MPIC_CUDA(cudaFreeAsync(d_rows, s));
+    MPIC_CUDA(cudaFreeAsync(stage, s));
+    MPIC_CUDA(cudaStreamSynchronize(s));
+    for (uint32_t l = 0; l < kv->L; ++l)
+        for (uint32_t i = 0; i < n_rows; ++i) {
+            const size_t src = ((size_t)l * n_rows + i) * h, dst = ((size_t)l * kv->T + rows[i]) * h;
+            if (k) std::memcpy(k + dst, host.data() + src, h * sizeof(float));
+            if (v) std::memcpy(v + dst, host.data() + per + src, h * sizeof(float));
+        }
+    API_END
+}
+
 int mpic_kv_download(mpic_kv_t kv, float* k, float* v, void* stream) {
     API_BEGIN
     MPIC_CUDA(cudaSetDevice(kv->device));
@@ -992,6 +1024,7 @@ int mpic_workspace_create(mpic_model_t md, uint32_t max_rows, uint32_t max_ctx, 
     ws->d_rows = dmalloc<uint32_t>(mp);
     ws->d_pos = dmalloc<uint32_t>(mp);
     ws->x = dmalloc<float>(mp * h);
+    ws->rope_tok = dmalloc<float2>(mp * (md->cfg.head_dim / 2));
     ws->xb = dmalloc<__nv_bfloat16>(mp * h);
     MPIC_CUDA(cudaMalloc(&ws->q, mp * h * e));
     MPIC_CUDA(cudaMalloc(&ws->attn, mp * h * e));
@@ -1024,7 +1057,7 @@ int mpic_workspace_destroy(mpic_workspace_t ws) {
     if (ws) {
         cudaSetDevice(ws->model->device);
         cudaFree(ws->d_ids); cudaFree(ws->d_rows); cudaFree(ws->d_pos);
-        cudaFree(ws->x); cudaFree(ws->xb); cudaFree(ws->q); cudaFree(ws->attn); cudaFree(ws->ffn);
+        cudaFree(ws->x); cudaFree(ws->rope_tok); cudaFree(ws->xb); cudaFree(ws->q); cudaFree(ws->attn); cudaFree(ws->ffn);
         cudaFree(ws->d_logits);
         cudaFree(ws->partial);
         cudaFreeHost(ws->h_ids); cudaFreeHost(ws->h_rows); cudaFreeHost(ws->h_pos);
@@ -1282,9 +1315,39 @@ int mpic_test_gemm(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uin
     if (path == 1) {
         MPIC_REQUIRE(tc_gemm_supported(M, N, K), MPIC_ERR_VALIDATION, "shape not supported by the tcgen05 gemm");
         launch_gemm_tc(static_cast<const __nv_bfloat16*>(d_a), K, static_cast<const __nv_bfloat16*>(d_w), M, N, K, ep, s);
+    } else if (path == 3) {  // d_w already in the blocked layout
+        launch_gemm_tc(static_cast<const __nv_bfloat16*>(d_a), K, static_cast<const __nv_bfloat16*>(d_w), M, N, K, ep, s,
+                       true);
+    } else if (path == 2) {  // the same weights in the blocked layout
+        MPIC_REQUIRE(pgemm_supported(M, N, K), MPIC_ERR_VALIDATION, "shape not supported by the pair gemm");
+        __nv_bfloat16* wb = nullptr;
+        MPIC_CUDA(cudaMallocAsync((void**)&wb, (size_t)N * K * 2, s));
+        launch_block_weights(static_cast<const __nv_bfloat16*>(d_w), wb, N, K, true, s);
+        launch_gemm_tc(static_cast<const __nv_bfloat16*>(d_a), K, wb, M, N, K, ep, s, true);
+        MPIC_CUDA(cudaFreeAsync(wb, s));
     } else {
         launch_gemm_simt(d_a, MPIC_BF16, K, d_w, MPIC_BF16, M, N, K, ep, MPIC_BF16, s);
     }
+    API_END
+}
+
+int mpic_test_gemm_epi(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uint32_t K, int mode,
+                       float* d_x, void* d_xb, void* d_out, void* stream) {
+    API_BEGIN
+    MPIC_REQUIRE(tc_gemm_supported(M, N, K), MPIC_ERR_VALIDATION, "shape not supported by the tcgen05 gemm");
+    EpiParams ep;
+    if (mode == 0) {
+        ep.mode = EPI_RESID;
+        ep.x = d_x;
+        ep.xb = static_cast<__nv_bfloat16*>(d_xb);
+        ep.ldx = N;
+    } else {
+        ep.mode = mode == 1 ? EPI_GELU : EPI_STORE;
+        ep.out = d_out;
+        ep.ldo = N;
+    }
+    launch_gemm_tc(static_cast<const __nv_bfloat16*>(d_a), K, static_cast<const __nv_bfloat16*>(d_w), M, N, K, ep,
+                   (cudaStream_t)stream);
     API_END
 }
 

@@ -24,6 +24,7 @@ struct EpiParams {
     const uint32_t* kv_rows = nullptr;
     const uint32_t* rope_pos = nullptr;
     const float2* rope = nullptr;  // [pos][head_dim/2] (cos, sin)
+    const float2* rope_tok = nullptr;  // optional [row][head_dim/2] (cos, sin) at rope_pos[row]
     uint32_t hidden = 0;
     uint32_t head_dim = 0;
     // EPI_RESID: x[row][col] += acc, and xb = bf16(x) when xb != null. The tcgen05 GEMM
@@ -55,6 +56,9 @@ struct AsmChunk {
 
 void launch_embed(const float* emb, const int32_t* ids, uint32_t m, uint32_t h, float* x,
                   __nv_bfloat16* xb, cudaStream_t s);
+// out[i][j] = tab[pos[i]][j] for i < m, j < half_d (per-request RoPE rows).
+void launch_rope_gather(const float2* tab, const uint32_t* pos, uint32_t m, uint32_t half_d, float2* out,
+                        cudaStream_t s);
 void launch_rope_table(const double* inv_freq, uint32_t half_d, uint32_t p0, uint32_t p1,
                        float2* tab, cudaStream_t s);
 void launch_gemm_simt(const void* A, mpic_dtype a_t, uint32_t lda, const void* W, mpic_dtype w_t,
@@ -65,6 +69,9 @@ void launch_attn_simt(const void* q, const void* k, const void* v, mpic_dtype dt
                       cudaStream_t s, float* capture = nullptr, uint32_t T = 0);
 void launch_lm_head(const float* x_last, const void* W, mpic_dtype w_t, uint32_t V, uint32_t h,
                     float* logits, cudaStream_t s);
+// out_k/out_v[l][i][:] = k/v[l][rows[i]][:] as fp32 (rows of a [L][T][h] cache).
+void launch_gather_rows(const void* k, const void* v, mpic_dtype dt, uint32_t L, uint32_t T, uint32_t h,
+                        const uint32_t* rows, uint32_t n_rows, float* out_k, float* out_v, cudaStream_t s);
 void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, size_t n, cudaStream_t s);
 void launch_bf16_to_f32(const __nv_bfloat16* in, float* out, size_t n, cudaStream_t s);
 void launch_x_to_bf16(const float* x, __nv_bfloat16* xb, uint32_t m, uint32_t h, cudaStream_t s);
@@ -102,7 +109,16 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
 // tcgen05 / TMA kernels (tc_gemm.cu, tc_attn.cu)
 struct TcGemmPlan;
 bool tc_gemm_supported(uint32_t M, uint32_t N, uint32_t K);
+// w_blocked: W is stored in 16 KB tiles [N/128][K/64][128][64] (pgemm_weight_layout), so
+// every TMA box of the weight stream is one contiguous DRAM burst.
 void launch_gemm_tc(const __nv_bfloat16* A, uint32_t lda, const __nv_bfloat16* W, uint32_t M,
-                    uint32_t N, uint32_t K, const EpiParams& ep, cudaStream_t s);
+                    uint32_t N, uint32_t K, const EpiParams& ep, cudaStream_t s, bool w_blocked = false);
+// Persistent CTA-pair stream-K GEMM (tc_pgemm.cu): N % 256 == 0, K % 64 == 0.
+bool pgemm_supported(uint32_t M, uint32_t N, uint32_t K);
+void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint32_t N, uint32_t K,
+                  const EpiParams& ep, cudaStream_t s, bool w_blocked = false);
+// Row-major [N][K] bf16 <-> the blocked weight layout (N % 128 == 0, K % 64 == 0).
+void launch_block_weights(const __nv_bfloat16* src, __nv_bfloat16* dst, uint32_t N, uint32_t K, bool to_blocked,
+                          cudaStream_t s);
 
 } // namespace mpicb

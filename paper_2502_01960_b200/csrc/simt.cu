@@ -45,6 +45,42 @@ __global__ void rope_table_kernel(const double* __restrict__ inv_freq, uint32_t 
     }
 }
 
+__global__ void rope_gather_kernel(const float2* __restrict__ tab, const uint32_t* __restrict__ pos,
+                                   uint32_t m, uint32_t half_d, float2* __restrict__ out) {
+    const uint32_t i = blockIdx.x;
+    const uint32_t p = pos[i];
+    for (uint32_t j = threadIdx.x; j < half_d; j += blockDim.x) out[(size_t)i * half_d + j] = tab[(size_t)p * half_d + j];
+}
+
+void launch_rope_gather(const float2* tab, const uint32_t* pos, uint32_t m, uint32_t half_d, float2* out,
+                        cudaStream_t s) {
+    rope_gather_kernel<<<m, 64, 0, s>>>(tab, pos, m, half_d, out);
+    MPIC_LAUNCHED();
+}
+
+template <typename T>
+__global__ void gather_rows_kernel(const T* __restrict__ k, const T* __restrict__ v, uint32_t T_, uint32_t h,
+                                   const uint32_t* __restrict__ rows, uint32_t n_rows, float* __restrict__ ok,
+                                   float* __restrict__ ov) {
+    const uint32_t l = blockIdx.y, i = blockIdx.x;
+    const size_t src = ((size_t)l * T_ + rows[i]) * h, dst = ((size_t)l * n_rows + i) * h;
+    for (uint32_t j = threadIdx.x; j < h; j += blockDim.x) {
+        ok[dst + j] = to_f32(k[src + j]);
+        ov[dst + j] = to_f32(v[src + j]);
+    }
+}
+
+void launch_gather_rows(const void* k, const void* v, mpic_dtype dt, uint32_t L, uint32_t T, uint32_t h,
+                        const uint32_t* rows, uint32_t n_rows, float* out_k, float* out_v, cudaStream_t s) {
+    const dim3 grid(n_rows, L);
+    if (dt == MPIC_F32)
+        gather_rows_kernel<float><<<grid, 128, 0, s>>>((const float*)k, (const float*)v, T, h, rows, n_rows, out_k, out_v);
+    else
+        gather_rows_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>((const __nv_bfloat16*)k, (const __nv_bfloat16*)v, T, h,
+                                                                  rows, n_rows, out_k, out_v);
+    MPIC_LAUNCHED();
+}
+
 void launch_rope_table(const double* inv_freq, uint32_t half_d, uint32_t p0, uint32_t p1,
                        float2* tab, cudaStream_t s) {
     if (p1 <= p0) return;

@@ -970,9 +970,13 @@ void launch_sk(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint3
 }  // namespace
 
 void launch_gemm_tc(const __nv_bfloat16* A, uint32_t lda, const __nv_bfloat16* W, uint32_t M,
-                    uint32_t N, uint32_t K, const EpiParams& ep_in, cudaStream_t s) {
+                    uint32_t N, uint32_t K, const EpiParams& ep_in, cudaStream_t s, bool w_blocked) {
     MPIC_REQUIRE(tc_gemm_supported(M, N, K) && lda == K, MPIC_ERR_VALIDATION, "unsupported tc gemm shape");
-    static const char* variant = getenv("MPIC_GEMM_VARIANT");  // diagnostics: "tok", "wswap", "pair"
+    static const char* variant = getenv("MPIC_GEMM_VARIANT");  // diagnostics: "tok", "sk", "wswap", "pair"
+    if (w_blocked || (!variant && pgemm_supported(M, N, K))) {
+        launch_pgemm(A, W, M, N, K, ep_in, s, w_blocked);
+        return;
+    }
     if (!variant || (variant[0] != 'w' && variant[0] != 'p')) {
         MPIC_REQUIRE(ep_in.mode != EPI_QKV || (ep_in.head_dim % 32 == 0 && ep_in.hidden % 32 == 0),
                      MPIC_ERR_VALIDATION, "tc gemm QKV epilogue needs head_dim % 32 == 0");

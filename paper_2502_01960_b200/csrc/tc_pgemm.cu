@@ -1,0 +1,601 @@
+// K3/K5/K6/K7 production GEMM — persistent CTA-pair (cta_group::2) swap-AB, data-parallel
+// tiles with in-cluster split-K.
+//
+//   out[t][f] = sum_k X[t][k] * W[f][k]      (y = x . W^T, proj/src/linker.cpp:64-128)
+//
+// Shape regime of MPIC's selective pass: few token rows (m = 96 .. ~2000 recomputed rows)
+// against large weights (h x h .. 4h x h). The UMMA M side is the WEIGHT: a CTA pair owns
+// 256 output features (128 per CTA, one TMEM lane per feature) and the UMMA N side is a
+// token GROUP of up to 512 tokens issued as one or two instructions of <= 256 columns,
+// so padding costs at most 15 rows per piece and every weight tile is read from HBM once.
+// Each CTA of the pair TMA-loads its 128 weight rows and HALF of the group's token rows;
+// the leader issues tcgen05.mma.cta_group::2 over both shared memories: per k-block of
+// 64 a CTA moves 16 KB + G*64 B for 2*128*G*64 FLOPs (G = 336: 147 FLOP per L2 byte,
+// 1.7x the 1-CTA 128x256 tile).
+//
+// Scheduling. tile = (256-feature block, token group). A cluster of S pairs (2S CTAs)
+// owns tiles c, c + C, c + 2C, ... (C clusters); pair s of the cluster computes the
+// k-blocks [s*kb/S, (s+1)*kb/S) of each. S = 1 is plain data-parallel (QKV, W1: 48 / 64
+// tiles). S = 2 or 4 is used when the tile count is small (Wo, W2 at h=4096: 16 tiles) and
+// every cluster holds a single tile: the S partial accumulators are reduced through
+// distributed shared memory — each CTA pushes the 32-token chunks it does not own into
+// the owner's (now idle) stage buffers, and the owner sums the S contributions in split
+// order (deterministic) before the fused epilogue. No partial ever goes to HBM/L2.
+//
+// Warp roles (320 threads per CTA):
+//   warp 0     TMA producer (both CTAs), 4-8 stage smem ring
+//   warp 1     TMEM allocator (pair) + MMA issuer (even CTA of the pair, one thread)
+//   warps 2-9  epilogue (two warps per TMEM lane quarter, alternate 32-token chunks):
+//              tcgen05.ld, thread <-> feature; fused RoPE + KV scatter (QKV), GELU (W1),
+//              residual add + bf16 copy (Wo, W2). Stores are coalesced across lanes (32
+//              consecutive features of one token row).
+// TMEM holds two accumulators when the group fits 256 columns, so the epilogue of one
+// tile overlaps the MMAs of the next; larger groups use one buffer.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+
+namespace mpicb {
+
+CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                           uint32_t box_outer);
+
+namespace {
+
+constexpr uint32_t kPgThreads = 320;  // producer, MMA, 8 epilogue warps
+constexpr uint32_t kPgWBytes = 128 * 64 * 2;  // one CTA's weight rows per k-block (16 KB)
+constexpr uint32_t kChunkBytes = 32 * 128 * 4;  // one 32-token x 128-feature fp32 chunk
+
+struct PgArgs {
+    uint32_t M, N, K;
+    uint32_t P0, P1;     // token pieces of a group (P1 == 0: one piece)
+    uint32_t G;          // tokens per group (P0 + P1)
+    uint32_t ngroups;
+    uint32_t kblocks;    // K / 64
+    uint32_t tiles;      // (N / 256) * ngroups
+    uint32_t S;          // pairs per cluster = K splits per tile
+    uint32_t clusters;
+    uint32_t stages;
+    uint32_t stage_bytes;
+    uint32_t sub_bytes;  // one k-block (64) of both operands; a stage holds kps of them
+    uint32_t kps;
+    uint32_t xoff1;      // byte offset of piece 1 in a stage's token region
+    uint32_t nbuf;       // TMEM accumulators (1 or 2)
+    uint32_t tmem_cols;
+    uint32_t w_evict_first;
+    uint32_t dbg;        // diagnostics: 1 skip epilogue, 2 skip X loads, 4 skip W loads, 8 skip MMA
+    uint32_t stage_rope; // QKV: stage rope/kv_rows of the (single) group in the idle stage buffers
+    uint32_t rows_off;   // byte offset of the staged kv_rows
+    uint32_t w_blocked;  // W stored as [N/128][K/64][128][64] tiles
+    EpiParams ep;
+};
+
+// GELU (tanh form, proj/src/model.cpp:85-87) with the hardware tanh: the result is rounded
+// to bf16, whose 2^-8 step is coarser than tanh.approx's error (bf16 mode only; the fp32
+// parity path uses the exact expression).
+__device__ __forceinline__ float gelu_fast(float x) {
+    float t;
+    const float inner = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(inner));
+    return 0.5f * x * (1.0f + t);
+}
+
+// Fused epilogue of 32 consecutive tokens [tb, tb+32) of feature f (accumulators r);
+// tokens at or beyond M (the group's end) are skipped. Lanes hold consecutive features,
+// so every store instruction writes one contiguous run per token row. Specialised per
+// mode (and for full chunks) so the per-element loops are branch-free.
+// s_rows / s_rope: this group's kv_rows and (cos, sin) rows staged in shared memory
+// (indexed from the group's first token tg), or null to read them from global memory.
+template <int MODE>
+__device__ __forceinline__ void pg_epi(const EpiParams& ep, uint32_t M, uint32_t tb, uint32_t f, uint32_t lane,
+                                       const uint32_t (&r)[32], const uint32_t* s_rows, const float2* s_rope,
+                                       uint32_t tg) {
+    const uint32_t n = min(32u, M - tb);  // valid tokens in this chunk
+    if constexpr (MODE == EPI_QKV) {
+        // linker.cpp:64-78 — q/k rotated at their position (interleaved pairs live on
+        // adjacent lanes), k/v scattered to the cache row kv_rows[t]
+        const uint32_t h = ep.hidden, part = f / h, d = f - part * h;
+        const uint32_t hd2 = ep.head_dim >> 1, pr = (d % ep.head_dim) >> 1;
+        __nv_bfloat16* base = static_cast<__nv_bfloat16*>(part == 0 ? ep.q : part == 1 ? ep.kv_k : ep.kv_v) + d;
+        const bool odd = lane & 1;
+        if (part == 2) {  // V: no rotation
+#pragma unroll
+            for (uint32_t j = 0; j < 32; ++j) {
+                if (j >= n) continue;
+                const uint32_t t = tb + j;
+                const uint32_t row = s_rows ? s_rows[t - tg] : __ldg(ep.kv_rows + t);
+                base[(size_t)row * h] = __float2bfloat16_rn(__uint_as_float(r[j]));
+            }
+            return;
+        }
+#pragma unroll
+        for (uint32_t j0 = 0; j0 < 32; j0 += 16) {
+            uint32_t row[16];
+            float2 cs[16];
+#pragma unroll
+            for (uint32_t j = 0; j < 16; ++j) {
+                const uint32_t t = min(tb + j0 + j, M - 1);
+                if (s_rows) {
+                    row[j] = part == 0 ? t : s_rows[t - tg];
+                    cs[j] = s_rope[(t - tg) * hd2 + pr];
+                } else {
+                    row[j] = part == 0 ? t : __ldg(ep.kv_rows + t);
+                    cs[j] = ep.rope_tok ? __ldg(ep.rope_tok + (size_t)t * hd2 + pr)
+                                        : __ldg(ep.rope + (size_t)__ldg(ep.rope_pos + t) * hd2 + pr);
+                }
+            }
+            __nv_bfloat16 o[16];
+#pragma unroll
+            for (uint32_t j = 0; j < 16; ++j) {
+                const float val = __uint_as_float(r[j0 + j]);
+                const float vp = __shfl_xor_sync(0xffffffffu, val, 1);
+                float x0 = odd ? vp : val, x1 = odd ? val : vp;
+                rope_pair(x0, x1, cs[j].x, cs[j].y);
+                o[j] = __float2bfloat16_rn(odd ? x1 : x0);
+            }
+            if (j0 + 16 <= n) {
+#pragma unroll
+                for (uint32_t j = 0; j < 16; ++j) base[(size_t)row[j] * h] = o[j];
+            } else {
+#pragma unroll
+                for (uint32_t j = 0; j < 16; ++j)
+                    if (j0 + j < n) base[(size_t)row[j] * h] = o[j];
+            }
+        }
+    } else if constexpr (MODE == EPI_RESID) {
+        float* xp = ep.x + (size_t)tb * ep.ldx + f;
+        __nv_bfloat16* xbp = ep.xb ? ep.xb + (size_t)tb * ep.ldx + f : nullptr;
+        if (n == 32) {
+            float xo[32];
+#pragma unroll
+            for (uint32_t j = 0; j < 32; ++j) xo[j] = __ldcg(xp + (size_t)j * ep.ldx);
+#pragma unroll
+            for (uint32_t j = 0; j < 32; ++j) {
+                const float nv = xo[j] + __uint_as_float(r[j]);
+                xp[(size_t)j * ep.ldx] = nv;
+                if (xbp) xbp[(size_t)j * ep.ldx] = __float2bfloat16_rn(nv);
+            }
+        } else {
+#pragma unroll
+            for (uint32_t j = 0; j < 32; ++j) {
+                if (j < n) {
+                    const float nv = __ldcg(xp + (size_t)j * ep.ldx) + __uint_as_float(r[j]);
+                    xp[(size_t)j * ep.ldx] = nv;
+                    if (xbp) xbp[(size_t)j * ep.ldx] = __float2bfloat16_rn(nv);
+                }
+            }
+        }
+    } else if constexpr (MODE == EPI_GELU) {
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + (size_t)tb * ep.ldo + f;
+#pragma unroll
+        for (uint32_t j = 0; j < 32; ++j)
+            if (j < n) o[(size_t)j * ep.ldo] = __float2bfloat16_rn(gelu_fast(__uint_as_float(r[j])));
+    } else if constexpr (MODE == EPI_STORE_F32) {
+        float* o = static_cast<float*>(ep.out) + (size_t)tb * ep.ldo + f;
+#pragma unroll
+        for (uint32_t j = 0; j < 32; ++j)
+            if (j < n) o[(size_t)j * ep.ldo] = __uint_as_float(r[j]);
+    } else {
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + (size_t)tb * ep.ldo + f;
+#pragma unroll
+        for (uint32_t j = 0; j < 32; ++j)
+            if (j < n) o[(size_t)j * ep.ldo] = __float2bfloat16_rn(__uint_as_float(r[j]));
+    }
+}
+
+__device__ __forceinline__ void pg_epilogue(const EpiParams& ep, uint32_t M, uint32_t tb, uint32_t f,
+                                            uint32_t lane, const uint32_t (&r)[32],
+                                            const uint32_t* s_rows = nullptr, const float2* s_rope = nullptr,
+                                            uint32_t tg = 0) {
+    switch (ep.mode) {
+        case EPI_QKV: pg_epi<EPI_QKV>(ep, M, tb, f, lane, r, s_rows, s_rope, tg); break;
+        case EPI_RESID: pg_epi<EPI_RESID>(ep, M, tb, f, lane, r, s_rows, s_rope, tg); break;
+        case EPI_GELU: pg_epi<EPI_GELU>(ep, M, tb, f, lane, r, s_rows, s_rope, tg); break;
+        case EPI_STORE_F32: pg_epi<EPI_STORE_F32>(ep, M, tb, f, lane, r, s_rows, s_rope, tg); break;
+        default: pg_epi<EPI_STORE>(ep, M, tb, f, lane, r, s_rows, s_rope, tg);
+    }
+}
+
+__global__ void __launch_bounds__(kPgThreads, 1)
+    tc_pgemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX0,
+                    const __grid_constant__ CUtensorMap tmX1, const PgArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * a.stage_bytes);
+    uint64_t* empty = full + a.stages;
+    uint64_t* acc_full = empty + a.stages;  // [2]
+    uint64_t* acc_empty = acc_full + 2;     // [2], the even CTA's copy is the one used
+    uint64_t* epi_bar = acc_empty + 2;      // epilogue side-input staging (bulk copies)
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(epi_bar + 1);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t crank = tc::cluster_ctarank();
+    const uint32_t rank = crank & 1;          // CTA within the pair
+    const uint32_t split = crank >> 1;        // pair within the cluster = K split
+    const uint32_t cl = blockIdx.x / (2 * a.S);
+    const uint32_t kb0 = split * a.kblocks / a.S, kb1 = (split + 1) * a.kblocks / a.S;
+    const uint16_t pair_mask = (uint16_t)(0x3u << (2 * split));
+
+    if (warp == 0 && lane == 0) {
+        tc::tma_prefetch_desc(&tmW);
+        tc::tma_prefetch_desc(&tmX0);
+        tc::tma_prefetch_desc(&tmX1);
+        for (uint32_t s = 0; s < a.stages; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (uint32_t b = 0; b < 2; ++b) {
+            tc::mbar_init(&acc_full[b], 1);
+            tc::mbar_init(&acc_empty[b], 16);  // 8 epilogue warps x 2 CTAs
+        }
+        tc::mbar_init(epi_bar, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) tc::tmem_alloc_pair(tmem_holder, a.tmem_cols);
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_w = a.w_evict_first ? tc::policy_evict_first() : tc::policy_evict_last();
+            const uint64_t pol_x = tc::policy_evict_last();
+            const uint32_t xbytes = (a.dbg & 2) ? 0u : a.sub_bytes - kPgWBytes;
+            const uint32_t wbytes = (a.dbg & 4) ? 0u : kPgWBytes;
+            const int xr0 = (int)(rank * (a.P0 / 2)), xr1 = (int)(a.P0 + rank * (a.P1 / 2));
+            const uint32_t leader_full = tc::mapa_shared(tc::smem_u32(full), crank & ~1u);
+            uint32_t s = 0, ph = 0;
+            for (uint32_t tile = cl; tile < a.tiles; tile += a.clusters) {
+                const uint32_t fb = tile / a.ngroups, g = tile % a.ngroups;
+                const int t0 = (int)(g * a.G), w_row = (int)(fb * 256 + rank * 128);
+                for (uint32_t kb = kb0; kb < kb1; kb += a.kps) {
+                    const uint32_t nsub = min(a.kps, kb1 - kb);
+                    tc::mbar_wait(&empty[s], ph ^ 1);
+                    if (rank == 0) tc::mbar_arrive_expect_tx(&full[s], 2 * nsub * (xbytes + wbytes));
+                    const uint32_t bar = leader_full + s * 8;
+                    for (uint32_t j = 0; j < nsub; ++j) {
+                        uint8_t* st = smem + s * a.stage_bytes + j * a.sub_bytes;
+                        const int k = (int)((kb + j) * 64);
+                        if (wbytes) {
+                            if (a.w_blocked)  // one contiguous 16 KB tile per box
+                                tc::tma_load_2d_cg2(st, &tmW, bar, 0, (int)(((2 * fb + rank) * a.kblocks + kb + j) * 128),
+                                                    pol_w);
+                            else
+                                tc::tma_load_2d_cg2(st, &tmW, bar, k, w_row, pol_w);
+                        }
+                        if (xbytes) tc::tma_load_2d_cg2(st + kPgWBytes, &tmX0, bar, k, t0 + xr0, pol_x);
+                        if (xbytes && a.P1) tc::tma_load_2d_cg2(st + kPgWBytes + a.xoff1, &tmX1, bar, k, t0 + xr1, pol_x);
+                    }
+                    if (++s == a.stages) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            const uint32_t idesc0 = tc::idesc_bf16(256, a.P0);
+            const uint32_t idesc1 = tc::idesc_bf16(256, a.P1 ? a.P1 : 16);
+            uint32_t item = 0, s = 0, ph = 0;
+            for (uint32_t tile = cl; tile < a.tiles; tile += a.clusters, ++item) {
+                const uint32_t b = a.nbuf == 2 ? (item & 1) : 0u;
+                const uint32_t use = a.nbuf == 2 ? (item >> 1) : item;
+                tc::mbar_wait_cluster(&acc_empty[b], (use & 1) ^ 1);
+                tc::tc_fence_after();
+                const uint32_t d = tmem + b * a.G;
+                for (uint32_t kb = kb0; kb < kb1; kb += a.kps) {
+                    const uint32_t nsub = min(a.kps, kb1 - kb);
+                    tc::mbar_wait(&full[s], ph);
+                    tc::tc_fence_after();
+                    for (uint32_t j = 0; j < nsub && !(a.dbg & 8); ++j) {
+                        const uint32_t w_base = tc::smem_u32(smem + s * a.stage_bytes + j * a.sub_bytes);
+                        const uint32_t x_base = w_base + kPgWBytes;
+#pragma unroll
+                        for (uint32_t kk = 0; kk < 4; ++kk) {
+                            const uint64_t adesc = tc::desc_k_sw128(w_base + kk * 32);
+                            const uint32_t acc = (kb + j > kb0 || kk > 0) ? 1u : 0u;
+                            tc::mma_bf16_pair(d, adesc, tc::desc_k_sw128(x_base + kk * 32), idesc0, acc);
+                            if (a.P1)
+                                tc::mma_bf16_pair(d + a.P0, adesc, tc::desc_k_sw128(x_base + a.xoff1 + kk * 32),
+                                                  idesc1, acc);
+                        }
+                    }
+                    tc::mma_commit_pair_mcast(&empty[s], pair_mask);
+                    if (++s == a.stages) { s = 0; ph ^= 1; }
+                }
+                tc::mma_commit_pair_mcast(&acc_full[b], pair_mask);
+            }
+        }
+        __syncwarp();
+    } else {
+        // 8 epilogue warps: warp w reads TMEM lane quarter w % 4; the two warps of a quarter
+        // take alternate 32-token chunks.
+        const uint32_t q = warp & 3;
+        const uint32_t half = (warp - 2) >> 2;
+        const uint32_t row = q * 32 + lane;
+        const uint32_t lane_off = (q * 32u) << 16;
+        const uint32_t acc_empty_leader = tc::mapa_shared(tc::smem_u32(&acc_empty[0]), crank & ~1u);
+        uint32_t item = 0;
+        for (uint32_t tile = cl; tile < a.tiles; tile += a.clusters, ++item) {
+            const uint32_t fb = tile / a.ngroups, g = tile % a.ngroups;
+            const uint32_t f = fb * 256 + rank * 128 + row;
+            const uint32_t tg = g * a.G;
+            const uint32_t tend = min(a.M, tg + a.G);  // tokens of this group: [tg, tend)
+            const uint32_t b = a.nbuf == 2 ? (item & 1) : 0u;
+            const uint32_t use = a.nbuf == 2 ? (item >> 1) : item;
+            tc::mbar_wait(&acc_full[b], use & 1);
+            tc::tc_fence_after();
+            const uint32_t dcol = tmem + lane_off + b * a.G;
+            if (a.S == 1) {
+                // QKV with one tile per pair: every MMA has retired, so the idle stage buffers
+                // take this group's kv_rows and per-token (cos, sin) rows in two bulk copies
+                // and the epilogue never waits on a dependent global load
+                const uint32_t* s_rows = nullptr;
+                const float2* s_rope = nullptr;
+                if (a.stage_rope && !(a.dbg & 1)) {
+                    const uint32_t nt = tend - tg, hd2 = a.ep.head_dim >> 1;
+                    const uint32_t rope_bytes = nt * hd2 * 8, rows_bytes = (nt * 4 + 15) & ~15u;
+                    if (warp == 2 && lane == 0) {
+                        tc::mbar_arrive_expect_tx(epi_bar, rope_bytes + rows_bytes);
+                        tc::bulk_load(smem, a.ep.rope_tok + (size_t)tg * hd2, rope_bytes, epi_bar);
+                        tc::bulk_load(smem + a.rows_off, a.ep.kv_rows + tg, rows_bytes, epi_bar);
+                    }
+                    tc::mbar_wait(epi_bar, 0);
+                    s_rope = reinterpret_cast<const float2*>(smem);
+                    s_rows = reinterpret_cast<const uint32_t*>(smem + a.rows_off);
+                }
+                if (!(a.dbg & 1))
+                    for (uint32_t c = half * 32; c < a.G && tg + c < tend; c += 64) {
+                        uint32_t r[32];
+                        tc::tmem_ld32(dcol + c, r);
+                        tc::tmem_ld_wait();
+                        pg_epilogue(a.ep, tend, tg + c, f, lane, r, s_rows, s_rope, tg);
+                    }
+            } else {
+                // in-cluster split-K (one tile per cluster): chunk j (32 tokens) belongs to split
+                // j % S. Every MMA of every pair has completed once all CTAs pass this barrier,
+                // so the stage buffers are free to receive [src split][j / S][32 cols][128 rows].
+                tc::cluster_arrive();
+                tc::cluster_wait();
+                const uint32_t nchunks = (a.G + 31) / 32;
+                const uint32_t per = (nchunks + a.S - 1) / a.S;
+                const uint32_t recv = tc::smem_u32(smem) + split * per * kChunkBytes + row * 4;
+                for (uint32_t j = half; j < nchunks; j += 2) {
+                    const uint32_t owner = j % a.S;
+                    if (owner == split) continue;
+                    uint32_t r[32];
+                    tc::tmem_ld32(dcol + j * 32, r);
+                    tc::tmem_ld_wait();
+                    const uint32_t dst = tc::mapa_shared(recv + (j / a.S) * kChunkBytes, 2 * owner + rank);
+#pragma unroll
+                    for (uint32_t i = 0; i < 32; ++i) tc::st_cluster_f32(dst + i * 512, r[i]);
+                }
+                tc::cluster_arrive();  // release: the pushed chunks are visible after the wait
+                tc::cluster_wait();
+                for (uint32_t j = split + half * a.S; j < nchunks; j += 2 * a.S) {
+                    if (a.dbg & 1) break;
+                    uint32_t r[32];
+                    tc::tmem_ld32(dcol + j * 32, r);
+                    tc::tmem_ld_wait();
+                    float v[32];
+#pragma unroll
+                    for (uint32_t i = 0; i < 32; ++i) v[i] = 0.0f;
+                    for (uint32_t s2 = 0; s2 < a.S; ++s2) {  // split order: deterministic
+                        if (s2 == split) {
+#pragma unroll
+                            for (uint32_t i = 0; i < 32; ++i) v[i] += __uint_as_float(r[i]);
+                        } else {
+                            const float* src = reinterpret_cast<const float*>(smem + (s2 * per + j / a.S) * kChunkBytes) + row;
+#pragma unroll
+                            for (uint32_t i = 0; i < 32; ++i) v[i] += src[i * 128];
+                        }
+                    }
+                    if (tg + j * 32 < tend) {
+#pragma unroll
+                        for (uint32_t i = 0; i < 32; ++i) r[i] = __float_as_uint(v[i]);
+                        pg_epilogue(a.ep, tend, tg + j * 32, f, lane, r);
+                    }
+                }
+            }
+            // release the accumulator to the pair's MMA issuer (one arrive per warp)
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive_remote(acc_empty_leader + b * 8);
+        }
+    }
+    if (a.S > 1 && warp < 2) {  // the producer / MMA warps take part in the reduction barriers
+        tc::cluster_arrive();
+        tc::cluster_wait();
+        tc::cluster_arrive();
+        tc::cluster_wait();
+    }
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    tc::tc_fence_after();
+    if (warp == 1) tc::tmem_dealloc_pair(tmem, a.tmem_cols);
+}
+
+uint32_t round16(uint32_t x) { return (x + 15) / 16 * 16; }
+
+// Largest number of co-resident clusters of `size` CTAs at this kernel's footprint.
+uint32_t max_clusters(uint32_t size, size_t smem) {
+    static std::mutex mu;
+    static std::unordered_map<uint64_t, uint32_t> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    uint32_t& v = cache[((uint64_t)size << 32) | smem];
+    if (!v) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(size * 32);
+        cfg.blockDim = dim3(kPgThreads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = size;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int n = 0;
+        MPIC_CUDA(cudaOccupancyMaxActiveClusters(&n, tc_pgemm_kernel, &cfg));
+        v = (uint32_t)std::max(1, n);
+    }
+    return v;
+}
+
+}  // namespace
+
+bool pgemm_supported(uint32_t M, uint32_t N, uint32_t K) {
+    return M > 0 && N % 256 == 0 && K % 64 == 0 && K >= 64;
+}
+
+void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint32_t N, uint32_t K,
+                  const EpiParams& ep_in, cudaStream_t s, bool w_blocked) {
+    MPIC_REQUIRE(pgemm_supported(M, N, K), MPIC_ERR_VALIDATION, "unsupported pair gemm shape");
+    MPIC_REQUIRE(ep_in.mode != EPI_QKV || (ep_in.head_dim % 2 == 0 && ep_in.hidden % 32 == 0),
+                 MPIC_ERR_VALIDATION, "pair gemm QKV epilogue needs hidden % 32 == 0");
+    static const uint32_t group_max = [] {
+        const char* e = getenv("MPIC_PG_GROUP");  // diagnostics: max tokens per group (256 or 512)
+        return e ? (uint32_t)atoi(e) : 512u;
+    }();
+    static const uint32_t dbg = [] {
+        const char* e = getenv("MPIC_PG_DBG");
+        return e ? (uint32_t)atoi(e) : 0u;
+    }();
+    static const uint32_t force_s = [] {
+        const char* e = getenv("MPIC_PG_SPLIT");  // diagnostics: force the in-cluster K split
+        return e ? (uint32_t)atoi(e) : 0u;
+    }();
+    static const uint32_t kps_env = [] {
+        const char* e = getenv("MPIC_PG_KPS");  // diagnostics: k-blocks per pipeline stage
+        return e ? (uint32_t)atoi(e) : 0u;
+    }();
+    static std::once_flag once;
+    std::call_once(once, [] {
+        MPIC_CUDA(cudaFuncSetAttribute(tc_pgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        MPIC_CUDA(cudaFuncSetAttribute(tc_pgemm_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    });
+    PgArgs best_a{};
+    double best = 1e30;
+    // Plan: token groups (1 natural, or the tokens cut into 2-3 groups to create tiles) x
+    // in-cluster K split S. Cost model per pair, in cycles: rounds x k-blocks x
+    // max(MMA 2G, operand fill 256 + G) (+ a reduction allowance for S > 1).
+    const uint32_t ng_nat = M <= 512 ? 1 : ceil_div(M, 256);
+    for (uint32_t gm : {1u, 2u, 3u}) {
+        PgArgs a{};
+        a.M = M;
+        a.N = N;
+        a.K = K;
+        a.dbg = dbg;
+        a.ngroups = ng_nat * gm;
+        if (a.ngroups == 1 && M > 256 && M <= group_max) {
+            a.P0 = round16((M + 1) / 2);
+            a.P1 = round16(M - a.P0);
+        } else {
+            if (a.ngroups == 1 && M > 256) continue;  // MPIC_PG_GROUP=256 diagnostics
+            a.P0 = round16(ceil_div(M, a.ngroups));
+            a.P1 = 0;
+            if (a.P0 > 256 || (gm > 1 && a.P0 < 64)) continue;
+        }
+        a.G = a.P0 + a.P1;
+        a.nbuf = 2 * a.G <= 512 ? 2 : 1;
+        a.tmem_cols = 32;
+        while (a.tmem_cols < a.nbuf * a.G) a.tmem_cols *= 2;
+        a.kblocks = K / 64;
+        a.tiles = (N / 256) * a.ngroups;
+        a.sub_bytes = kPgWBytes + a.G * 64;
+        a.kps = kps_env ? kps_env : 2;
+        a.stage_bytes = a.kps * a.sub_bytes;
+        a.xoff1 = a.P0 * 64;
+        const uint32_t budget = 227 * 1024 - 1024 - 128;
+        a.stages = std::min<uint32_t>(8, budget / a.stage_bytes);
+        if (a.stages < 3 && a.kps > 1) {  // keep at least 3 stages in flight
+            a.kps = 1;
+            a.stage_bytes = a.sub_bytes;
+            a.stages = std::min<uint32_t>(8, budget / a.stage_bytes);
+        }
+        if (a.stages < 2) continue;
+        a.w_evict_first = a.ngroups == 1;
+        a.ep = ep_in;
+        const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 5) * 8 + 16;
+        const uint32_t nchunks = (a.G + 31) / 32;
+        const double t_kb = std::max(2.0 * a.G, 256.0 + a.G);
+        for (uint32_t S : {1u, 2u, 3u, 4u}) {
+            if (force_s && S != force_s && S != 1) continue;
+            if (S > 1 && a.kblocks / S < 2) continue;
+            const uint32_t C = max_clusters(2 * S, smem);
+            if (S > 1 && (a.tiles > C || (size_t)S * ceil_div(nchunks, S) * kChunkBytes > (size_t)a.stages * a.stage_bytes))
+                continue;
+            const double cost = (double)ceil_div(a.tiles, std::min(C, a.tiles)) * ceil_div(a.kblocks, S) * t_kb +
+                                (S > 1 ? 2000.0 : 0.0) + (force_s > 1 && S == 1 ? 1e20 : 0.0);
+            if (cost < best - 1e-9) {
+                best = cost;
+                best_a = a;
+                best_a.S = S;
+                best_a.clusters = std::min(C, a.tiles);
+            }
+        }
+    }
+    MPIC_REQUIRE(best < 1e29, MPIC_ERR_VALIDATION, "pair gemm: no feasible tiling");
+    PgArgs a = best_a;
+    a.w_blocked = w_blocked ? 1u : 0u;
+
+    const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 5) * 8 + 16;
+    static const bool verbose = getenv("MPIC_PG_VERBOSE") != nullptr;
+    if (verbose)
+        fprintf(stderr, "pgemm M=%u N=%u K=%u: groups=%u P0=%u P1=%u S=%u clusters=%u stages=%u x %u kb nbuf=%u\n", M,
+                N, K, a.ngroups, a.P0, a.P1, a.S, a.clusters, a.stages, a.kps, a.nbuf);
+    if (ep_in.mode == EPI_QKV && ep_in.rope_tok && a.S == 1 && a.clusters >= a.tiles && a.ngroups == 1) {
+        const uint32_t rope_bytes = a.G * (ep_in.head_dim / 2) * 8;
+        a.rows_off = (rope_bytes + 1023) & ~1023u;
+        a.stage_rope = a.rows_off + a.G * 4 + 16 <= a.stages * a.stage_bytes;
+    }
+    const CUtensorMap tmW = w_blocked ? make_tmap_bf16(W, 64, (uint64_t)N * a.kblocks, 64, 128)
+                                      : make_tmap_bf16(W, K, N, 64, 128);
+    const CUtensorMap tmX0 = make_tmap_bf16(A, K, M, 64, a.P0 / 2);
+    const CUtensorMap tmX1 = a.P1 ? make_tmap_bf16(A, K, M, 64, a.P1 / 2) : tmX0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.clusters * 2 * a.S);
+    cfg.blockDim = dim3(kPgThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2 * a.S;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MPIC_CUDA(cudaLaunchKernelEx(&cfg, tc_pgemm_kernel, tmW, tmX0, tmX1, a));
+    MPIC_LAUNCHED();
+}
+
+__global__ void block_weights_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                     uint32_t N, uint32_t K, bool to_blocked) {
+    // one 16-B vector (8 elements) per thread step; blocked index of (n, k):
+    //   ((n/128)*(K/64) + k/64)*8192 + (n%128)*64 + k%64
+    const size_t total = (size_t)N * K / 8;
+    const uint32_t kb = K / 64;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
+        const size_t e = v * 8;
+        const uint32_t n = (uint32_t)(e / K), k = (uint32_t)(e % K);
+        const size_t b = ((size_t)(n / 128) * kb + k / 64) * 8192 + (n % 128) * 64 + k % 64;
+        if (to_blocked) reinterpret_cast<uint4*>(dst)[b / 8] = reinterpret_cast<const uint4*>(src)[v];
+        else reinterpret_cast<uint4*>(dst)[v] = reinterpret_cast<const uint4*>(src)[b / 8];
+    }
+}
+
+void launch_block_weights(const __nv_bfloat16* src, __nv_bfloat16* dst, uint32_t N, uint32_t K, bool to_blocked,
+                          cudaStream_t s) {
+    MPIC_REQUIRE(N % 128 == 0 && K % 64 == 0, MPIC_ERR_VALIDATION, "blocked weights need N % 128, K % 64");
+    block_weights_kernel<<<kNumSMs * 8, 256, 0, s>>>(src, dst, N, K, to_blocked);
+    MPIC_LAUNCHED();
+}
+
+}  // namespace mpicb

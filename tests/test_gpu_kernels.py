@@ -26,16 +26,53 @@ def run_gemm(a, w, path):
 
 @pytest.mark.parametrize("M,N,K", [(1, 128, 64), (17, 256, 128), (96, 512, 512),
                                    (330, 1024, 512), (512, 256, 1024), (600, 384, 256),
-                                   (1100, 128, 192), (330, 4096, 4096)])
-@pytest.mark.parametrize("path", [1, 0])
+                                   (1100, 128, 192), (330, 4096, 4096),
+                                   # persistent pair GEMM: one piece, two pieces, groups;
+                                   # stream-K splits at 1 .. many pairs per tile
+                                   (256, 256, 64), (257, 512, 128), (330, 12288, 4096),
+                                   (330, 4096, 16384), (96, 16384, 512), (2000, 1024, 320),
+                                   (513, 768, 4096), (48, 256, 12288)])
+@pytest.mark.parametrize("path", [1, 2, 0])
 def test_gemm_vs_torch(M, N, K, path):
+    if path == 2 and N % 256:
+        pytest.skip("blocked weights feed the pair GEMM (N % 256 == 0)")
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
     a = (torch.rand(M, K, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
     w = (torch.rand(N, K, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
     ref = a.float() @ w.float().t()
     out = run_gemm(a, w, path)
     err = (out - ref).abs().max().item() / ref.abs().max().item()
-    assert err < 1e-5, err
+    # fp32 accumulation of K products: the rounding envelope grows with K (and with the
+    # order the partial sums are combined in), so the bound scales with K / 4096
+    assert err < 1e-5 * max(1.0, K / 4096), err
+
+
+@pytest.mark.parametrize("M,N,K", [(330, 4096, 4096), (96, 1024, 2048), (600, 512, 256),
+                                   (330, 16384, 512)])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_gemm_epilogues_vs_torch(M, N, K, mode):
+    """Fused epilogues of the tcgen05 GEMM: residual add (+ bf16 copy), GELU (tanh form,
+    proj/src/model.cpp:85-87), plain bf16 store."""
+    g = torch.Generator(device="cuda").manual_seed(M + N * 3 + K + mode)
+    a = (torch.rand(M, K, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    w = (torch.rand(N, K, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    y = a.float() @ w.float().t()
+    x = torch.rand(M, N, device="cuda", generator=g) - 0.5
+    xb = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    out = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    x_in = x.clone()
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.lib().mpic_test_gemm_epi(a.data_ptr(), w.data_ptr(), M, N, K, mode, x.data_ptr(),
+                                             xb.data_ptr(), out.data_ptr(), s))
+    torch.cuda.synchronize()
+    if mode == 0:
+        ref = x_in + y
+        assert (x - ref).abs().max().item() / ref.abs().max().item() < 1e-5
+        assert torch.equal(xb, x.to(torch.bfloat16))
+    else:
+        ref = torch.nn.functional.gelu(y, approximate="tanh") if mode == 1 else y
+        err = (out.float() - ref).abs().max().item() / ref.abs().max().item()
+        assert err < 1e-2, err
 
 
 def run_attention(q, k, v, rows, H):

@@ -3,7 +3,9 @@
 #include "mpic/linker.h"
 #include "mpic/model.h"
 #include "test_util.h"
+#include "device.h"
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <random>
 using namespace mpic;
@@ -34,6 +36,34 @@ int main() {
         std::sort(t.begin(), t.end());
         std::printf("  median %.3f\n", t[5]);
     };
+    // breakdown of one selective_prefill call (the steps of linker.cpp recompute_rows)
+    {
+        using clk = std::chrono::steady_clock;
+        auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        const SelectionMask mask = select_tokens(p, MpicKPolicy{16});
+        for (int rep = 0; rep < 5; ++rep) {
+            LinkedCache lc = assemble_linked_cache(p, entries, model);
+            const TokenIds flat = p.flatten_ids(model.config);
+            const uint32_t m = mask.selected.size();
+            TokenIds ids(m);
+            for (uint32_t i = 0; i < m; ++i) ids[i] = flat[mask.selected[i]];
+            auto t0 = clk::now();
+            auto dm = b200::device_model_for(model);
+            auto t1 = clk::now();
+            b200::Workspace& ws = b200::workspace_for(dm, m, lc.kv.n_tokens);
+            auto t2 = clk::now();
+            auto* dkv = new b200::DeviceKv(lc.kv);
+            auto t3 = clk::now();
+            Logits logits(model.config.vocab_size);
+            b200::check(mpic_selective_prefill(dm->get(), ws.get(), ids.data(), mask.selected.data(), m, dkv->get(), logits.data(), nullptr));
+            auto t4 = clk::now();
+            dkv->download(lc.kv);
+            auto t5 = clk::now();
+            delete dkv;
+            auto t6 = clk::now();
+            std::printf("model %.3f ws %.3f kv_alloc+up %.3f prefill %.3f down %.3f free %.3f\n", ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5), ms(t5, t6));
+        }
+    }
     for (int round = 0; round < 2; ++round) {
         run("k0  ", select_tokens(p, MpicKPolicy{0}));
         run("k16 ", select_tokens(p, MpicKPolicy{16}));
