@@ -71,56 +71,69 @@ def build_prompt(cfg_name, V, seed=42):
 
 
 class ClockSampler:
-    """Clocks and throttle reasons DURING the timed region, sampled by an `nvidia-smi -lms`
-    subprocess (B200_PROFILING.md recipe) so no Python thread competes with the timed loop."""
+    """Clocks and throttle reasons of the timed region.
+
+    On these VM-hosted B200s every NVML query (nvidia-smi or pynvml) stalls GPU work
+    submission: sampling at 50-250 ms periods inside the timed region produced 30-770 ms
+    step outliers (profiles/r1_clock_sampling.md). So the SM clock is measured ON THE
+    DEVICE during the region — a 5 us clock64 / %globaltimer probe kernel on the timed
+    stream after every step (mpic_clock_probe) — and nvidia-smi is queried for the clocks
+    and the throttle reasons right before and right after the region."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, device_index=0, period_ms=100):
-        self.dev, self.period = device_index, period_ms
-        self.proc, self.rows = None, []
+    def __init__(self, device_index=0, steps=1):
+        import torch
+        self.dev = device_index
+        self.rows = []
+        self.buf = torch.zeros(max(steps, 1), dtype=torch.float32, device=f"cuda:{device_index}")
+        self.i = 0
 
-    def __enter__(self):
+    def _query(self):
         import subprocess
-        import tempfile
-        self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", f"-lms={self.period}"],
-                stdout=self.out, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
-        return self
-
-    def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
-            self.out.seek(0)
-            for line in self.out.read().splitlines():
+            out = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=20).stdout
+            for line in out.splitlines():
                 parts = [p.strip() for p in line.split(",")]
                 if len(parts) == 6:
                     self.rows.append(parts)
-        try:
-            os.unlink(self.out.name)
         except Exception:
             pass
 
+    def probe(self, stream):
+        """Enqueue one on-device clock measurement (after a step, on the timed stream)."""
+        from paper_2502_01960_b200 import _lib
+        if self.i < self.buf.numel():
+            _lib.check(_lib.lib().mpic_clock_probe(self.buf.data_ptr() + 4 * self.i, 5000,
+                                                   _stream_handle(stream)))
+            self.i += 1
+
+    def __enter__(self):
+        self._query()
+        return self
+
+    def __exit__(self, *a):
+        self._query()
+
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        dev_mhz = [float(x) for x in self.buf[:self.i].cpu().tolist()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.strip().lower() == "active"})
-        return {"sm_mhz": float(statistics.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+        reasons = sorted({n for r in self.rows for n, v in zip(self.NAMES, r[2:]) if v.lower() == "active"})
+        return {"sm_mhz": float(statistics.median(dev_mhz)) if dev_mhz else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(dev_mhz), "sm_mhz_min": min(dev_mhz) if dev_mhz else None,
+                "method": "device clock64/globaltimer probe after every timed step; nvidia-smi "
+                          "reasons before+after the region",
+                "nvidia_smi_sm_mhz": [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]}
+
+
+def _stream_handle(stream):
+    return int(getattr(stream, "cuda_stream", stream))
 
 
 def dist_setup(n_gpus):
@@ -212,31 +225,39 @@ def run_ours(args, world, rank, local):
         return mp.last_launch_count()
 
     # ---- device-resident path (value) ----
+    # Same-shape requests replay a CUDA graph of the whole request (mpic_workspace_set_graphs):
+    # warm-up request 2 records it, the timed requests replay it with their inputs re-staged.
     for _ in range(args.warmup):
         step_device()
     torch.cuda.synchronize()
-    mp.profile_enable(True)
-    mp.profile_collect()
     barrier(world)
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     launches = 0
     per_step = []
     host_ms = []
-    with ClockSampler(dev) as clk:
+    with ClockSampler(dev, args.steps) as clk:
         with torch.cuda.stream(stream):
             ev[0].record(stream)
             for i in range(args.steps):
                 h0 = time.perf_counter()
                 launches += step_device()
+                clk.probe(stream)
                 ev[i + 1].record(stream)
                 host_ms.append((time.perf_counter() - h0) * 1e3)
         torch.cuda.synchronize()
     barrier(world)
-    mp.profile_enable(False)
-    phases = mp.profile_collect()
     for i in range(args.steps):
         per_step.append(ev[i].elapsed_time(ev[i + 1]))
+    # per-phase device times (CUDA events around every phase: eager launches, so a separate
+    # pass after the timed region; kernel durations are the same as in the graph)
+    mp.profile_enable(True)
+    mp.profile_collect()
+    for _ in range(args.steps):
+        step_device()
+    torch.cuda.synchronize()
+    mp.profile_enable(False)
+    phases = mp.profile_collect()
     total_ms = ev[0].elapsed_time(ev[-1])
     total_ms = allreduce_max(total_ms, world)
     ms_per_step = total_ms / args.steps

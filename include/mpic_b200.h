@@ -213,6 +213,11 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
  * full PCIe rate): the loader streams layer l of every chunk to HBM on a side stream while
  * layer l-1 is being recomputed; each landed layer is assembled (and cast to the model
  * dtype) right before it is used. */
+/* CUDA-graph replay of mpic_request_prefill (default on): a request with the same launch
+ * signature as the previous one on this workspace (model, linked cache, n, m, chunk count,
+ * plan sizes) is captured once and replayed after that, with its inputs re-staged. */
+int mpic_workspace_set_graphs(mpic_workspace_t ws, int on);
+
 int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
                               const mpic_policy* policy, const float* const* chunk_k,
                               const float* const* chunk_v, const uint32_t* position_bases,
@@ -264,6 +269,10 @@ int mpic_profile_collect(double* ms, uint32_t* counts);
  * ascending). out [m][H*128] bf16. Async on `stream`. */
 int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const uint32_t* rows,
                         uint32_t m, uint32_t n_ctx, uint32_t n_heads, void* d_out, void* stream);
+
+/* Diagnostics: the SM clock (MHz) measured on the device — clock64 cycles over a
+ * %globaltimer window of spin_ns — written to d_out_mhz. Async on `stream`. */
+int mpic_clock_probe(float* d_out_mhz, uint32_t spin_ns, void* stream);
 
 /* Number of kernels the last forward/assemble call on this thread launched. */
 uint32_t mpic_last_launch_count(void);

@@ -94,6 +94,8 @@ SIGNATURES = {
     "mpic_request_prefill_host": (_int, [_vp, _vp, _P(PromptDesc), _P(PolicyDesc), _vp, _vp,
                                          _vp, _int, _vp, _vp, _vp, _P(_u32), _vp]),
     "mpic_kv_download_rows": (_int, [_vp, _vp, _u32, _vp, _vp, _vp]),
+    "mpic_workspace_set_graphs": (_int, [_vp, _int]),
+    "mpic_clock_probe": (_int, [_vp, _u32, _vp]),
     "mpic_test_gemm": (_int, [_vp, _vp, _u32, _u32, _u32, _int, _vp, _vp]),
     "mpic_test_gemm_epi": (_int, [_vp, _vp, _u32, _u32, _u32, _int, _vp, _vp, _vp, _vp]),
     "mpic_profile_enable": (_int, [_int]),

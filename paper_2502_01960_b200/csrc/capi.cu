@@ -91,6 +91,20 @@ struct mpic_kv_s {
     size_t elems() const { return (size_t)L * T * H * D; }
 };
 
+// Everything that fixes the launch sequence of a device-resident request: same signature
+// => same kernels, grids and tensor maps; only the staged inputs differ.
+struct GraphSig {
+    const void* model = nullptr;
+    const void* linked = nullptr;
+    uint32_t n = 0, m = 0, n_img = 0, n_tables = 0, n_units = 0, n_comb = 0;
+    int reposition = 0, src_dtype = 0;
+    bool operator==(const GraphSig& o) const {
+        return model == o.model && linked == o.linked && n == o.n && m == o.m && n_img == o.n_img &&
+               n_tables == o.n_tables && n_units == o.n_units && n_comb == o.n_comb &&
+               reposition == o.reposition && src_dtype == o.src_dtype;
+    }
+};
+
 struct mpic_workspace_s {
     mpic_model_t model = nullptr;
     uint32_t max_rows = 0, max_ctx = 0, m_pad = 0;
@@ -126,6 +140,17 @@ struct mpic_workspace_s {
     void* h_plan = nullptr;  // pinned staging for the plan
     size_t h_plan_cap = 0;
     uint32_t n_units = 0, n_comb = 0;
+    cudaEvent_t ev_plan = nullptr;
+    // assembly descriptors (AsmChunk table + rerotation tables), pinned staging + device copy
+    void* h_asm = nullptr;
+    void* d_asm = nullptr;
+    size_t asm_cap = 0;
+    // CUDA-graph replay of a device-resident request (mpic_request_prefill): the request
+    // whose shape matches the previous one is captured once, later ones replay it
+    bool graphs = true;
+    GraphSig last_sig{}, graph_sig{};
+    cudaGraphExec_t graph = nullptr;
+    uint32_t graph_kernels = 0;
 };
 
 #define API_BEGIN \
@@ -315,9 +340,10 @@ bool use_tc_attention(mpic_model_t md) {
 }
 
 // Build the attention work plan from host rows (or, without them, a conservative plan in
-// which every query may see keys up to max_pos) and upload it to the workspace.
-void upload_attn_plan(mpic_workspace_t ws, const uint32_t* h_rows, uint32_t m, uint32_t max_pos,
-                      uint32_t H, cudaStream_t s) {
+// which every query may see keys up to max_pos), grow the workspace buffers it needs and
+// stage it in pinned memory. Host-only: nothing is enqueued, so it may run before a
+// stream capture. enqueue_attn_plan() then copies it to the device on the stream.
+void prepare_attn_plan(mpic_workspace_t ws, const uint32_t* h_rows, uint32_t m, uint32_t max_pos, uint32_t H) {
     std::vector<uint32_t> conservative;
     if (!h_rows) {
         conservative.assign(m, max_pos);
@@ -326,7 +352,7 @@ void upload_attn_plan(mpic_workspace_t ws, const uint32_t* h_rows, uint32_t m, u
     const AttnPlan plan = plan_attention(h_rows, m, H);
     auto grow = [&](auto*& ptr, size_t& cap, size_t need, size_t elt) {
         if (cap >= need) return;
-        MPIC_CUDA(cudaStreamSynchronize(s));
+        MPIC_CUDA(cudaDeviceSynchronize());
         cudaFree(ptr);
         ptr = nullptr;
         MPIC_CUDA(cudaMalloc((void**)&ptr, std::max<size_t>(need, 1) * elt));
@@ -335,7 +361,7 @@ void upload_attn_plan(mpic_workspace_t ws, const uint32_t* h_rows, uint32_t m, u
     grow(ws->d_units, ws->units_cap, plan.units.size(), sizeof(AttnUnit));
     grow(ws->d_comb, ws->comb_cap, plan.combine.size(), sizeof(AttnCombine));
     if (ws->slots_cap < plan.slots) {
-        MPIC_CUDA(cudaStreamSynchronize(s));
+        MPIC_CUDA(cudaDeviceSynchronize());
         cudaFree(ws->part_o);
         cudaFree(ws->part_ml);
         MPIC_CUDA(cudaMalloc(&ws->part_o, (size_t)plan.slots * 128 * 128 * sizeof(float)));
@@ -344,20 +370,28 @@ void upload_attn_plan(mpic_workspace_t ws, const uint32_t* h_rows, uint32_t m, u
     }
     const size_t bu = plan.units.size() * sizeof(AttnUnit);
     const size_t bc = plan.combine.size() * sizeof(AttnCombine);
+    // the previous request's copy out of the pinned staging must have landed
+    if (ws->ev_plan) MPIC_CUDA(cudaEventSynchronize(ws->ev_plan));
     if (ws->h_plan_cap < bu + bc) {
-        MPIC_CUDA(cudaStreamSynchronize(s));
         cudaFreeHost(ws->h_plan);
         MPIC_CUDA(cudaMallocHost(&ws->h_plan, bu + bc));
         ws->h_plan_cap = bu + bc;
-    } else {
-        MPIC_CUDA(cudaStreamSynchronize(s));  // previous request's plan copy has landed
     }
     std::memcpy(ws->h_plan, plan.units.data(), bu);
     std::memcpy((char*)ws->h_plan + bu, plan.combine.data(), bc);
-    MPIC_CUDA(cudaMemcpyAsync(ws->d_units, ws->h_plan, bu, cudaMemcpyHostToDevice, s));
-    if (bc) MPIC_CUDA(cudaMemcpyAsync(ws->d_comb, (char*)ws->h_plan + bu, bc, cudaMemcpyHostToDevice, s));
     ws->n_units = (uint32_t)plan.units.size();
     ws->n_comb = (uint32_t)plan.combine.size();
+}
+
+void enqueue_attn_plan(mpic_workspace_t ws, cudaStream_t s) {
+    const size_t bu = ws->n_units * sizeof(AttnUnit), bc = ws->n_comb * sizeof(AttnCombine);
+    if (bu) MPIC_CUDA(cudaMemcpyAsync(ws->d_units, ws->h_plan, bu, cudaMemcpyHostToDevice, s));
+    if (bc) MPIC_CUDA(cudaMemcpyAsync(ws->d_comb, (char*)ws->h_plan + bu, bc, cudaMemcpyHostToDevice, s));
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    MPIC_CUDA(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return;  // graph requests end in a stream sync
+    if (!ws->ev_plan) MPIC_CUDA(cudaEventCreateWithFlags(&ws->ev_plan, cudaEventDisableTiming));
+    MPIC_CUDA(cudaEventRecord(ws->ev_plan, s));
 }
 
 // selective_core / extend_rows on the device (linker.cpp:35-135, model.cpp:211-330).
@@ -365,7 +399,7 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
                   const uint32_t* d_rows, const uint32_t* d_pos, uint32_t m, uint32_t max_pos,
                   mpic_kv_t kv, float* d_logits, cudaStream_t s,
                   const std::function<void(uint32_t)>& before_layer = {},
-                  const uint32_t* h_rows = nullptr, float* d_capture = nullptr) {
+                  const uint32_t* h_rows = nullptr, float* d_capture = nullptr, bool plan_ready = false) {
     const mpic_model_config& c = md->cfg;
     const uint32_t h = c.hidden_dim, H = c.n_heads, D = c.head_dim;
     MPIC_REQUIRE(m > 0, MPIC_ERR_VALIDATION, "no tokens to prefill");
@@ -384,7 +418,10 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
     }
     if (bf) launch_rope_gather(md->rope, d_pos, m, D / 2, ws->rope_tok, s);
     const bool tc_attn = use_tc_attention(md);
-    if (tc_attn) upload_attn_plan(ws, h_rows, m, max_pos, H, s);
+    if (tc_attn) {
+        if (!plan_ready) prepare_attn_plan(ws, h_rows, m, max_pos, H);
+        enqueue_attn_plan(ws, s);
+    }
     for (uint32_t l = 0; l < c.n_layers; ++l) {
         void* kl = (char*)kv->k + l * plane;
         void* vl = (char*)kv->v + l * plane;
@@ -1073,6 +1110,10 @@ int mpic_workspace_destroy(mpic_workspace_t ws) {
         cudaFree(ws->part_o);
         cudaFree(ws->part_ml);
         cudaFreeHost(ws->h_plan);
+        cudaFreeHost(ws->h_asm);
+        cudaFree(ws->d_asm);
+        if (ws->ev_plan) cudaEventDestroy(ws->ev_plan);
+        if (ws->graph) cudaGraphExecDestroy(ws->graph);
         delete ws;
     }
     API_END
@@ -1197,8 +1238,12 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
     API_BEGIN
     MPIC_CUDA(cudaSetDevice(model->device));
     cudaStream_t s = (cudaStream_t)stream;
+    MPIC_REQUIRE(ws && ws->model == model, MPIC_ERR_VALIDATION, "workspace belongs to another model");
+    // ---- host planning (select, contract, assembly and attention plans, staging) ----
     const RequestPlan r = plan_request(model, prompt, policy, position_bases);
     check_linked(model, linked, r.n);
+    MPIC_REQUIRE(r.m <= ws->max_rows, MPIC_ERR_VALIDATION, "more rows than the workspace holds");
+    check_ids(model, r.ids_sel.data(), r.m);
     const uint32_t n_img = (uint32_t)r.refs.size();
     std::vector<const void*> ks(n_img), vs(n_img);
     std::vector<uint32_t> ts(n_img);
@@ -1213,9 +1258,106 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
         vs[i] = c->v;
         ts[i] = c->T;
     }
-    do_assemble(s, ks.data(), vs.data(), ts.data(), n_img ? chunks[0]->dtype : model->dtype,
-                r.refs.data(), n_img, linked, reposition, 1, model->cfg.rope_base);
-    run_request(model, ws, r, linked, logits, selected, m_out, s, {});
+    const mpic_dtype src_t = n_img ? chunks[0]->dtype : model->dtype;
+    const AsmPlan ap = plan_assembly(ks.data(), vs.data(), ts.data(), r.refs.data(), n_img, linked->T, linked->D,
+                                     reposition, model->cfg.rope_base);
+    ensure_rope(model, r.n, s);
+    if (use_tc_attention(model)) prepare_attn_plan(ws, r.sel.data(), r.m, r.n - 1, model->cfg.n_heads);
+    std::memcpy(ws->h_ids, r.ids_sel.data(), r.m * sizeof(int32_t));
+    std::memcpy(ws->h_rows, r.sel.data(), r.m * sizeof(uint32_t));
+    const size_t bytes_c = std::max<size_t>(1, ap.chunks.size()) * sizeof(AsmChunk);
+    const size_t bytes_t = std::max<size_t>(1, ap.tables.size()) * sizeof(float2);
+    if (ws->asm_cap < bytes_c + bytes_t) {
+        MPIC_CUDA(cudaDeviceSynchronize());
+        cudaFreeHost(ws->h_asm);
+        cudaFree(ws->d_asm);
+        ws->h_asm = ws->d_asm = nullptr;
+        ws->asm_cap = 0;
+        MPIC_CUDA(cudaMallocHost(&ws->h_asm, bytes_c + bytes_t));
+        MPIC_CUDA(cudaMalloc(&ws->d_asm, bytes_c + bytes_t));
+        ws->asm_cap = bytes_c + bytes_t;
+    }
+    if (!ap.chunks.empty()) std::memcpy(ws->h_asm, ap.chunks.data(), ap.chunks.size() * sizeof(AsmChunk));
+    if (!ap.tables.empty())
+        std::memcpy((char*)ws->h_asm + bytes_c, ap.tables.data(), ap.tables.size() * sizeof(float2));
+
+    // ---- device work: one stream-ordered sequence, optionally recorded as a CUDA graph ----
+    auto enqueue = [&] {
+        MPIC_CUDA(cudaMemcpyAsync(ws->d_ids, ws->h_ids, r.m * 4, cudaMemcpyHostToDevice, s));
+        MPIC_CUDA(cudaMemcpyAsync(ws->d_rows, ws->h_rows, r.m * 4, cudaMemcpyHostToDevice, s));
+        MPIC_CUDA(cudaMemcpyAsync(ws->d_asm, ws->h_asm, bytes_c + bytes_t, cudaMemcpyHostToDevice, s));
+        {
+            ProfScope ps(s, MPIC_PHASE_ASSEMBLE);
+            launch_assemble(static_cast<const AsmChunk*>(ws->d_asm), n_img,
+                            reinterpret_cast<const float2*>((char*)ws->d_asm + bytes_c), ap.n_tables, src_t,
+                            linked->k, linked->v, linked->dtype, linked->L, linked->T, linked->H, linked->D, 1, s);
+        }
+        forward_rows(model, ws, ws->d_ids, ws->d_rows, ws->d_rows, r.m, r.n - 1, linked, ws->d_logits, s, {},
+                     r.sel.data(), nullptr, /*plan_ready=*/true);
+        MPIC_CUDA(cudaMemcpyAsync(ws->h_logits, ws->d_logits, model->cfg.vocab_size * 4, cudaMemcpyDeviceToHost, s));
+    };
+    GraphSig sig;
+    sig.model = model;
+    sig.linked = linked;
+    sig.n = r.n;
+    sig.m = r.m;
+    sig.n_img = n_img;
+    sig.n_tables = ap.n_tables;
+    sig.n_units = ws->n_units;
+    sig.n_comb = ws->n_comb;
+    sig.reposition = reposition;
+    sig.src_dtype = src_t;
+    bool prof;
+    {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        prof = g_prof_on;
+    }
+    const bool use_graph = ws->graphs && !prof;
+    if (use_graph && ws->graph && ws->graph_sig == sig) {
+        MPIC_CUDA(cudaGraphLaunch(ws->graph, s));
+        note_launch(ws->graph_kernels);
+    } else if (use_graph && ws->last_sig == sig) {
+        // second request of this shape: record it once, replay it from now on
+        if (ws->graph) {
+            cudaGraphExecDestroy(ws->graph);
+            ws->graph = nullptr;
+        }
+        const uint32_t before = g_launches;
+        cudaGraph_t g = nullptr;
+        MPIC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue();
+        } catch (...) {
+            cudaStreamEndCapture(s, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        MPIC_CUDA(cudaStreamEndCapture(s, &g));
+        const cudaError_t ie = cudaGraphInstantiate(&ws->graph, g, 0);
+        cudaGraphDestroy(g);
+        MPIC_CUDA(ie);
+        ws->graph_kernels = g_launches - before;
+        ws->graph_sig = sig;
+        MPIC_CUDA(cudaGraphLaunch(ws->graph, s));
+    } else {
+        enqueue();
+    }
+    ws->last_sig = sig;
+    MPIC_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(logits, ws->h_logits, model->cfg.vocab_size * sizeof(float));
+    if (selected) std::memcpy(selected, r.sel.data(), r.m * sizeof(uint32_t));
+    if (m_out) *m_out = r.m;
+    API_END
+}
+
+int mpic_workspace_set_graphs(mpic_workspace_t ws, int on) {
+    API_BEGIN
+    MPIC_REQUIRE(ws, MPIC_ERR_VALIDATION, "null workspace");
+    ws->graphs = on != 0;
+    if (!ws->graphs && ws->graph) {
+        cudaGraphExecDestroy(ws->graph);
+        ws->graph = nullptr;
+    }
     API_END
 }
 
@@ -1348,6 +1490,12 @@ int mpic_test_gemm_epi(const void* d_a, const void* d_w, uint32_t M, uint32_t N,
     }
     launch_gemm_tc(static_cast<const __nv_bfloat16*>(d_a), K, static_cast<const __nv_bfloat16*>(d_w), M, N, K, ep,
                    (cudaStream_t)stream);
+    API_END
+}
+
+int mpic_clock_probe(float* d_out_mhz, uint32_t spin_ns, void* stream) {
+    API_BEGIN
+    launch_clock_probe(d_out_mhz, spin_ns, (cudaStream_t)stream);
     API_END
 }
 

@@ -72,6 +72,7 @@ void launch_lm_head(const float* x_last, const void* W, mpic_dtype w_t, uint32_t
 // out_k/out_v[l][i][:] = k/v[l][rows[i]][:] as fp32 (rows of a [L][T][h] cache).
 void launch_gather_rows(const void* k, const void* v, mpic_dtype dt, uint32_t L, uint32_t T, uint32_t h,
                         const uint32_t* rows, uint32_t n_rows, float* out_k, float* out_v, cudaStream_t s);
+void launch_clock_probe(float* out_mhz, uint32_t spin_ns, cudaStream_t s);
 void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, size_t n, cudaStream_t s);
 void launch_bf16_to_f32(const __nv_bfloat16* in, float* out, size_t n, cudaStream_t s);
 void launch_x_to_bf16(const float* x, __nv_bfloat16* xb, uint32_t m, uint32_t h, cudaStream_t s);

@@ -81,6 +81,24 @@ void launch_gather_rows(const void* k, const void* v, mpic_dtype dt, uint32_t L,
     MPIC_LAUNCHED();
 }
 
+// SM clock under load, measured on the device: cycles / globaltimer ns over a ~spin_ns window.
+__global__ void clock_probe_kernel(float* out_mhz, uint32_t spin_ns) {
+    if (threadIdx.x != 0) return;
+    uint64_t g0, g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+    const long long c0 = clock64();
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    } while (g1 - g0 < spin_ns);
+    const long long c1 = clock64();
+    *out_mhz = (float)((double)(c1 - c0) * 1e3 / (double)(g1 - g0));
+}
+
+void launch_clock_probe(float* out_mhz, uint32_t spin_ns, cudaStream_t s) {
+    clock_probe_kernel<<<1, 32, 0, s>>>(out_mhz, spin_ns);
+    MPIC_CUDA(cudaGetLastError());
+}
+
 void launch_rope_table(const double* inv_freq, uint32_t half_d, uint32_t p0, uint32_t p1,
                        float2* tab, cudaStream_t s) {
     if (p1 <= p0) return;
