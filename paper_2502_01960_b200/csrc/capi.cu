@@ -1556,6 +1556,22 @@ int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const
                    reinterpret_cast<float*>(b + bu + bc), reinterpret_cast<float2*>(b + bu + bc + bo),
                    static_cast<__nv_bfloat16*>(d_out), s);
     MPIC_CUDA(cudaFreeAsync(buf, s));
+    if (unsigned long long* dbg = attn_debug_buffer()) {  // MPIC_ATTN_TS diagnostics
+        std::vector<unsigned long long> h(8 * 64);
+        MPIC_CUDA(cudaStreamSynchronize(s));
+        MPIC_CUDA(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
+        MPIC_CUDA(cudaMemset(dbg, 0, h.size() * 8));
+        const AttnUnit& u0 = plan.units[0];
+        fprintf(stderr, "attn CTA0 item: head %u b0 %u tiles %u/%u b1 %u/%u\n", u0.head, u0.b0, u0.tile[0], u0.tile[1],
+                u0.b1[0], u0.b1[1]);
+        const unsigned long long t0 = h[0];
+        for (int j = 0; j < 64 && h[j * 8]; ++j)
+            fprintf(stderr, "j=%2d start %7.2f v_full %7.2f pA %7.2f pB %7.2f k_next %7.2f | A got S %7.2f max %7.2f A put P %7.2f us\n",
+                    j, (h[j * 8] - t0) / 1e3, (h[j * 8 + 1] - t0) / 1e3, h[j * 8 + 2] ? (h[j * 8 + 2] - t0) / 1e3 : -1.0,
+                    h[j * 8 + 3] ? (h[j * 8 + 3] - t0) / 1e3 : -1.0, h[j * 8 + 4] ? (h[j * 8 + 4] - t0) / 1e3 : -1.0,
+                    ((long long)h[j * 8 + 5] - (long long)t0) / 1e3, ((long long)h[j * 8 + 7] - (long long)t0) / 1e3,
+                    ((long long)h[j * 8 + 6] - (long long)t0) / 1e3);
+    }
     API_END
 }
 

@@ -87,10 +87,14 @@ void launch_assemble(const AsmChunk* d_chunks, uint32_t n_chunks, const float2* 
                      mpic_dtype dst_t, uint32_t L, uint32_t T_dst, uint32_t H, uint32_t D,
                      int zero_gaps, cudaStream_t s);
 
-// Attention work plan (tc_attn.cu): units = (query tile, head, key-block range).
+// Attention work plan (tc_attn.cu): an item is up to two query tiles of one head that
+// stream the same key blocks [b0, max(b1)) — tile[1] == kNoTile when the item has one.
+constexpr uint32_t kNoTile = 0xffffffffu;
 struct AttnUnit {
-    uint32_t tile, head, b0, b1;
-    uint32_t slot;  // 0xffffffff: write the final output; else partial slot for the combine
+    uint32_t head, b0;
+    uint32_t tile[2];
+    uint32_t b1[2];    // per-tile end block
+    uint32_t slot[2];  // kNoTile: write the final output; else partial slot for the combine
 };
 struct AttnCombine {
     uint32_t tile, head, slot0, n;
@@ -100,6 +104,7 @@ struct AttnPlan {
     std::vector<AttnCombine> combine;
     uint32_t slots = 0;
 };
+unsigned long long* attn_debug_buffer();
 AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads);
 void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const __nv_bfloat16* vcache,
                     uint32_t n_ctx, const uint32_t* d_rows, uint32_t m, uint32_t H,

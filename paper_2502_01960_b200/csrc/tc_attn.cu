@@ -4,19 +4,25 @@
 // [0, rows[i]] of the just-scattered layer cache (proj/src/linker.cpp:80-113): the
 // per-row causal limit is the row's POSITION, not its index in the tile.
 //
-// Work unit = (128-query tile, head, range of 128-key blocks). The host splits long key
-// ranges (flash-decoding style) so that ~3 waves of units cover the 148 SMs; partial
-// results are merged by attn_combine_kernel. One CTA per unit:
+// Work item = one head x a range of 128-key blocks x up to TWO 128-query tiles that need
+// those keys. The host splits long key ranges (flash-decoding style) so ~3 waves of items
+// cover the 148 SMs; attn_combine_kernel merges split partials. One CTA per item, the two
+// query tiles in ping-pong (FlashAttention-4 style), sharing every K/V block they load:
 //
-//   warp 0     TMA: Q tile [128 x 128] once, K/V blocks [128 keys x 128] into 2-stage rings
-//   warp 1     TMEM alloc (512 cols: S0 | S1 | O) + single-thread tcgen05.mma issuer:
-//              S_b = Q . K_b^T (SS, K-major) and O += P_b . V_b (P K-major from smem,
-//              V MN-major), in the order S0 S1 PV0 S2 PV1 S3 ...
-//   warps 2-5  softmax, one thread per query row (TMEM lane): scale, per-row causal mask,
-//              online max with lazy rescaling of O in TMEM (only when the max grows by
-//              more than 2^8), exp2, row sums, P written to smem in the SWIZZLE_128B
-//              K-major layout the MMA descriptor expects; final O / l epilogue.
+//   warp 0     control warp, one role per lane (independent thread scheduling): lane 0 TMA
+//              loads Q_A, Q_B once and K_j into a 2-stage ring, lane 16 V_j into a 3-stage
+//              ring ([128 keys x 128] blocks), lane 8 issues every tcgen05.mma; the warp also
+//              owns TMEM (512 cols: S_A | O_A | S_B | O_B). MMAs: S_X(j) = Q_X . K_j^T (SS, K-major) and O_X += P_X(j) . V_j (P from
+//              TMEM, V MN-major), ordered PV_A(j) S_A(j+1) PV_B(j) S_B(j+1), so one tile's
+//              MMAs run while the other tile's softmax works
+//   warps 1-3  idle (warpgroup 0 hands its registers to the softmax warpgroups: setmaxnreg)
+//   warps 4-7  softmax of tile A, warps 8-11 of tile B, 224 registers per thread: ONE THREAD PER QUERY ROW holding
+//              its 128 scores (no cross-warp reduction), scale, per-row causal mask, online
+//              max with lazy O rescaling (only when the max grows by more than 2^8), exp2
+//              with half of the exponentials on the FMA pipe (degree-3 polynomial, exact to
+//              bf16) and half on MUFU, row sums; P written back over S in TMEM as bf16.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -30,11 +36,12 @@ CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t outer, uint
 
 namespace {
 
-constexpr uint32_t kAttnThreads = 352;  // K TMA, MMA, V TMA, 8 softmax warps
-constexpr uint32_t kKvStages = 3;
-constexpr uint32_t kSoftmaxThreads = 256;
-constexpr uint32_t kTile = 32 * 1024;  // one [128 x 128] bf16 tile as 2 swizzled 64-col halves
+constexpr uint32_t kAttnThreads = 384;  // 3 warpgroups: control, softmax tile A, softmax tile B
+constexpr uint32_t kCtrlRegs = 56, kSoftmaxRegs = 224;  // setmaxnreg split of the 64K registers
+constexpr uint32_t kTile = 32 * 1024;   // one [128 x 128] bf16 tile as 2 swizzled 64-col halves
 constexpr uint32_t kHalf = 16 * 1024;
+constexpr uint32_t kKStages = 2;
+constexpr uint32_t kVStages = 3;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 struct AttnParams {
@@ -46,11 +53,54 @@ struct AttnParams {
     __nv_bfloat16* out;     // [m][h]
     float* part_o;          // [slots][128][128]
     float2* part_ml;        // [slots][128] (m_used, l)
+    unsigned long long* dbg;  // diagnostics: per-block event times of CTA 0, or null
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// Packed fp32 pair ops (FFMA2 / FADD2 on sm_100): two elements per instruction.
+struct f2 {
+    unsigned long long v;
+};
+__device__ __forceinline__ f2 mk2(float a, float b) {
+    return f2{(unsigned long long)__float_as_uint(a) | ((unsigned long long)__float_as_uint(b) << 32)};
+}
+__device__ __forceinline__ float lo(f2 a) { return __uint_as_float((uint32_t)a.v); }
+__device__ __forceinline__ float hi(f2 a) { return __uint_as_float((uint32_t)(a.v >> 32)); }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    f2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return d;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+    f2 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+    return d;
+}
+
+// 2^x for two x <= 0 on the FMA/ALU pipes only (no F2I/FRND, which share the MUFU pipe):
+// round x with the 1.5*2^23 magic constant, degree-3 fit of 2^f on [-1/2, 1/2] (max rel.
+// error 1.7e-4, below the bf16 rounding P gets next), exponent added in the integer domain.
+__device__ __forceinline__ f2 exp2_poly2(f2 x) {
+    x = mk2(fmaxf(lo(x), -126.0f), fmaxf(hi(x), -126.0f));
+    const f2 magic = mk2(12582912.0f, 12582912.0f), nmagic = mk2(-12582912.0f, -12582912.0f);
+    const f2 t = add2(x, magic);
+    const f2 j = add2(t, nmagic);
+    const f2 f = add2(x, mk2(-lo(j), -hi(j)));
+    f2 p = fma2(mk2(0.05302752f, 0.05302752f), f, mk2(0.24221394f, 0.24221394f));
+    p = fma2(p, f, mk2(0.69357257f, 0.69357257f));
+    p = fma2(p, f, mk2(1.0f, 1.0f));
+    const int e0 = (__float_as_int(lo(t)) - 0x4B400000) << 23, e1 = (__float_as_int(hi(t)) - 0x4B400000) << 23;
+    return mk2(__int_as_float(__float_as_int(lo(p)) + e0), __int_as_float(__float_as_int(hi(p)) + e1));
 }
 
 __global__ void __launch_bounds__(kAttnThreads, 1)
@@ -58,24 +108,25 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                    const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;
-    uint8_t* sK = smem + kTile;                 // kKvStages stages
-    uint8_t* sV = smem + (1 + kKvStages) * kTile;  // kKvStages stages
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (1 + 2 * kKvStages) * kTile);
-    uint64_t* q_full = bars + 0;
-    uint64_t* k_full = bars + 1;                   // [kKvStages]
-    uint64_t* k_empty = k_full + kKvStages;        // [kKvStages]
-    uint64_t* v_full = k_empty + kKvStages;        // [kKvStages]
-    uint64_t* v_empty = v_full + kKvStages;        // [kKvStages]
-    uint64_t* s_full = v_empty + kKvStages;        // [2]
-    uint64_t* p_full = s_full + 2;                 // [2]
-    uint64_t* o_full = p_full + 2;                 // [2] — PV_b completes on o_full[b & 1]
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 2);
+    uint8_t* sQ = smem;                          // [2] tiles
+    uint8_t* sK = smem + 2 * kTile;              // [kKStages]
+    uint8_t* sV = sK + kKStages * kTile;         // [kVStages]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVStages * kTile);
+    uint64_t* q_full = bars;
+    uint64_t* k_full = q_full + 1;               // [kKStages]
+    uint64_t* k_empty = k_full + kKStages;
+    uint64_t* v_full = k_empty + kKStages;       // [kVStages]
+    uint64_t* v_empty = v_full + kVStages;
+    uint64_t* s_full = v_empty + kVStages;       // [2 tiles]
+    uint64_t* p_full = s_full + 2;               // [2 tiles]
+    uint64_t* o_done = p_full + 2;               // [2 tiles]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_done + 2);
 
     const AttnUnit u = p.units[blockIdx.x];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t q0 = u.tile * 128u;
-    const uint32_t nb = u.b1 - u.b0;
+    const bool has_b = u.tile[1] != kNoTile;
+    const uint32_t nb0 = u.b1[0] - u.b0, nb1 = has_b ? u.b1[1] - u.b0 : 0;
+    const uint32_t nbmax = max(nb0, nb1);
     const int hcol = (int)(u.head * 128u);
 
     if (warp == 0 && lane == 0) {
@@ -83,235 +134,260 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tc::tma_prefetch_desc(&tmK);
         tc::tma_prefetch_desc(&tmV);
         tc::mbar_init(q_full, 1);
-        for (uint32_t i = 0; i < kKvStages; ++i) {
+        for (uint32_t i = 0; i < kKStages; ++i) {
             tc::mbar_init(&k_full[i], 1);
             tc::mbar_init(&k_empty[i], 1);
+        }
+        for (uint32_t i = 0; i < kVStages; ++i) {
             tc::mbar_init(&v_full[i], 1);
             tc::mbar_init(&v_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&s_full[i], 1);
-            tc::mbar_init(&p_full[i], kSoftmaxThreads);
-            tc::mbar_init(&o_full[i], 1);
+            tc::mbar_init(&p_full[i], 128);
+            tc::mbar_init(&o_done[i], 1);
         }
         tc::fence_barrier_init();
     }
-    if (warp == 1) tc::tmem_alloc(tmem_holder, 512);
+    if (warp == 0) tc::tmem_alloc(tmem_holder, 512);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_holder;
-    // TMEM columns: S0 [0,128) | S1 [128,256) | O [256,384) | row exchange [384,392).
-    // P_b (bf16, two keys per column) overwrites the first 64 columns of S_b in place.
+    // TMEM columns: tile X uses S_X [256X, 256X+128) and O_X [256X+128, 256X+256).
+    // P_X(j) (bf16, two keys per column) overwrites the first 64 columns of S_X in place.
     constexpr uint32_t idesc_s = tc::idesc_bf16(128, 128, false);
     constexpr uint32_t idesc_o = tc::idesc_bf16(128, 128, true);
 
+    if (warp < 4) {
+        tc::reg_dealloc<kCtrlRegs>();
+    } else {
+        tc::reg_alloc<kSoftmaxRegs>();
+    }
     if (warp == 0) {
-        if (lane == 0) {  // K producer (+ Q)
-            tc::mbar_arrive_expect_tx(q_full, kTile);
-            tc::tma_load_2d(sQ, &tmQ, q_full, hcol, (int)q0);
-            tc::tma_load_2d(sQ + kHalf, &tmQ, q_full, hcol + 64, (int)q0);
-            for (uint32_t b = 0; b < nb; ++b) {
-                const uint32_t s = b % kKvStages, ph = (b / kKvStages) & 1;
-                const int j0 = (int)((u.b0 + b) * 128u);
-                tc::mbar_wait(&k_empty[s], ph ^ 1);
-                tc::mbar_arrive_expect_tx(&k_full[s], kTile);
-                tc::tma_load_2d(sK + s * kTile, &tmK, &k_full[s], hcol, j0);
-                tc::tma_load_2d(sK + s * kTile + kHalf, &tmK, &k_full[s], hcol + 64, j0);
-            }
-        }
-        __syncwarp();
-    } else if (warp == 2) {
-        if (lane == 0) {  // V producer
-            for (uint32_t b = 0; b < nb; ++b) {
-                const uint32_t s = b % kKvStages, ph = (b / kKvStages) & 1;
-                const int j0 = (int)((u.b0 + b) * 128u);
-                tc::mbar_wait(&v_empty[s], ph ^ 1);
-                tc::mbar_arrive_expect_tx(&v_full[s], kTile);
-                tc::tma_load_2d(sV + s * kTile, &tmV, &v_full[s], hcol, j0);
-                tc::tma_load_2d(sV + s * kTile + kHalf, &tmV, &v_full[s], hcol + 64, j0);
-            }
-        }
-        __syncwarp();
-    } else if (warp == 1) {
+        // lane 0: Q tiles then the K ring; lane 16: the V ring (independent producers, so a
+        // late PV never holds back the next K block)
         if (lane == 0) {
-            const uint32_t qa = tc::smem_u32(sQ);
-            auto issue_s = [&](uint32_t b) {
-                const uint32_t ks = b % kKvStages;
-                tc::mbar_wait(&k_full[ks], (b / kKvStages) & 1);
-                tc::tc_fence_after();
-                const uint32_t ka = tc::smem_u32(sK + ks * kTile);
+            tc::mbar_arrive_expect_tx(q_full, (has_b ? 2 : 1) * kTile);
+#pragma unroll
+            for (uint32_t x = 0; x < 2; ++x) {
+                if (x == 1 && !has_b) break;
+                const int q0 = (int)((x ? u.tile[1] : u.tile[0]) * 128u);
+                tc::tma_load_2d(sQ + x * kTile, &tmQ, q_full, hcol, q0);
+                tc::tma_load_2d(sQ + x * kTile + kHalf, &tmQ, q_full, hcol + 64, q0);
+            }
+            for (uint32_t j = 0; j < nbmax; ++j) {
+                const uint32_t st = j % kKStages, ph = (j / kKStages) & 1;
+                const int j0 = (int)((u.b0 + j) * 128u);
+                tc::mbar_wait(&k_empty[st], ph ^ 1);
+                tc::mbar_arrive_expect_tx(&k_full[st], kTile);
+                tc::tma_load_2d(sK + st * kTile, &tmK, &k_full[st], hcol, j0);
+                tc::tma_load_2d(sK + st * kTile + kHalf, &tmK, &k_full[st], hcol + 64, j0);
+            }
+        } else if (lane == 16) {
+            for (uint32_t j = 0; j < nbmax; ++j) {
+                const uint32_t st = j % kVStages, ph = (j / kVStages) & 1;
+                const int j0 = (int)((u.b0 + j) * 128u);
+                tc::mbar_wait(&v_empty[st], ph ^ 1);
+                tc::mbar_arrive_expect_tx(&v_full[st], kTile);
+                tc::tma_load_2d(sV + st * kTile, &tmV, &v_full[st], hcol, j0);
+                tc::tma_load_2d(sV + st * kTile + kHalf, &tmV, &v_full[st], hcol + 64, j0);
+            }
+        }
+        else if (lane == 8) {
+            const uint32_t nbx[2] = {nb0, nb1};
+            auto issue_s = [&](uint32_t x, uint32_t j) {
+                const uint32_t qa = tc::smem_u32(sQ + x * kTile);
+                const uint32_t ka = tc::smem_u32(sK + (j % kKStages) * kTile);
 #pragma unroll
                 for (uint32_t kk = 0; kk < 8; ++kk) {
                     const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-                    tc::mma_bf16(tmem + (b & 1) * 128, tc::desc_k_sw128(qa + off), tc::desc_k_sw128(ka + off),
-                                 idesc_s, kk > 0 ? 1u : 0u);
+                    tc::mma_bf16(tmem + x * 256, tc::desc_k_sw128(qa + off), tc::desc_k_sw128(ka + off), idesc_s,
+                                 kk > 0 ? 1u : 0u);
                 }
-                tc::mma_commit(&k_empty[ks]);
-                tc::mma_commit(&s_full[b & 1]);
+                tc::mma_commit(&s_full[x]);
             };
             tc::mbar_wait(q_full, 0);
-            issue_s(0);
-            if (nb > 1) issue_s(1);
-            for (uint32_t b = 0; b < nb; ++b) {
-                const uint32_t s = b & 1, vs = b % kKvStages;
-                tc::mbar_wait(&p_full[s], (b >> 1) & 1);
-                tc::mbar_wait(&v_full[vs], (b / kKvStages) & 1);
-                tc::tc_fence_after();
-                const uint32_t va = tc::smem_u32(sV + vs * kTile);
+            tc::mbar_wait(&k_full[0], 0);
+            tc::tc_fence_after();
 #pragma unroll
-                for (uint32_t kk = 0; kk < 8; ++kk)  // A = P_b from TMEM: 16 keys = 8 packed columns
-                    tc::mma_bf16_ts(tmem + 256, tmem + s * 128 + kk * 8, tc::desc_mn_sw128(va + kk * 2048, kHalf),
-                                    idesc_o, (b > 0 || kk > 0) ? 1u : 0u);
-                tc::mma_commit(&v_empty[vs]);
-                tc::mma_commit(&o_full[s]);
-                if (b + 2 < nb) issue_s(b + 2);  // in-order after PV_b, which reads P_b from S_b's columns
+            for (uint32_t x = 0; x < 2; ++x)
+                if (nbx[x] > 0) issue_s(x, 0);
+            tc::mma_commit(&k_empty[0]);
+            for (uint32_t j = 0; j < nbmax; ++j) {
+                const uint32_t st = j % kVStages, ph = (j / kVStages) & 1;
+                const bool nxt = j + 1 < nbmax;
+                if (p.dbg && blockIdx.x == 0) p.dbg[j * 8 + 0] = globaltimer_ns();
+                tc::mbar_wait(&v_full[st], ph);
+                if (p.dbg && blockIdx.x == 0) p.dbg[j * 8 + 1] = globaltimer_ns();
+                bool k_ready = false;
+#pragma unroll
+                for (uint32_t x = 0; x < 2; ++x) {
+                    if (j >= nbx[x]) continue;
+                    tc::mbar_wait(&p_full[x], j & 1);
+                    if (p.dbg && blockIdx.x == 0) p.dbg[j * 8 + 2 + x] = globaltimer_ns();
+                    tc::tc_fence_after();
+                    const uint32_t va = tc::smem_u32(sV + st * kTile);
+#pragma unroll
+                    for (uint32_t kk = 0; kk < 8; ++kk)  // A = P_X(j) from TMEM: 16 keys = 8 packed columns
+                        tc::mma_bf16_ts(tmem + x * 256 + 128, tmem + x * 256 + kk * 8,
+                                        tc::desc_mn_sw128(va + kk * 2048, kHalf), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+                    tc::mma_commit(&o_done[x]);
+                    // in-order after PV_X(j), which reads P_X(j) from S_X's columns
+                    if (j + 1 < nbx[x]) {
+                        if (!k_ready) {
+                            tc::mbar_wait(&k_full[(j + 1) % kKStages], ((j + 1) / kKStages) & 1);
+                            if (p.dbg && blockIdx.x == 0) p.dbg[j * 8 + 4] = globaltimer_ns();
+                            tc::tc_fence_after();
+                            k_ready = true;
+                        }
+                        issue_s(x, j + 1);
+                    }
+                }
+                tc::mma_commit(&v_empty[st]);
+                if (nxt) {
+                    if (!k_ready) {  // no tile needs K_{j+1} any more: just release it
+                        tc::mbar_wait(&k_full[(j + 1) % kKStages], ((j + 1) / kKStages) & 1);
+                        tc::tc_fence_after();
+                    }
+                    tc::mma_commit(&k_empty[(j + 1) % kKStages]);
+                }
             }
         }
         __syncwarp();
-    } else {
-        // ---- softmax: 8 warps, a pair per TMEM lane quarter; warp hsel owns score columns
-        // (keys) and O columns (head dims) [64*hsel, 64*hsel+64) of its 32 query rows.
-        const uint32_t quarter = warp & 3;
-        const uint32_t hsel = (warp - 3) >> 2;
-        const uint32_t r = quarter * 32 + lane;
-        const uint32_t qi = q0 + r;
-        const bool valid = qi < p.m;
-        const uint32_t limit = valid ? p.rows[qi] : 0u;
-        const uint32_t lane_base = (quarter * 32u) << 16;
-        const uint32_t xchg = tmem + lane_base + 384;
-        const uint32_t bar_id = 1 + quarter;
-        float m_used = -INFINITY, l = 0.0f;
-        for (uint32_t b = 0; b < nb; ++b) {
-            const uint32_t s = b & 1;
-            const uint32_t j0 = (u.b0 + b) * 128u + hsel * 64u;  // first key of my half
-            tc::mbar_wait(&s_full[s], (b >> 1) & 1);
-            tc::tc_fence_after();
-            const uint32_t sa = tmem + lane_base + s * 128 + hsel * 64;
-            const bool masked = __any_sync(0xffffffffu, j0 + 63 > limit);
-            uint32_t v[64];
-            tc::tmem_ld32(sa, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-            tc::tmem_ld32(sa + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
-            tc::tmem_ld_wait();
-            float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-            if (masked) {
-#pragma unroll
-                for (uint32_t e = 0; e < 64; e += 4) {
-                    mx0 = j0 + e + 0 <= limit ? fmaxf(mx0, __uint_as_float(v[e + 0])) : mx0;
-                    mx1 = j0 + e + 1 <= limit ? fmaxf(mx1, __uint_as_float(v[e + 1])) : mx1;
-                    mx2 = j0 + e + 2 <= limit ? fmaxf(mx2, __uint_as_float(v[e + 2])) : mx2;
-                    mx3 = j0 + e + 3 <= limit ? fmaxf(mx3, __uint_as_float(v[e + 3])) : mx3;
-                }
-            } else {
-#pragma unroll
-                for (uint32_t e = 0; e < 64; e += 4) {
-                    mx0 = fmaxf(mx0, __uint_as_float(v[e + 0]));
-                    mx1 = fmaxf(mx1, __uint_as_float(v[e + 1]));
-                    mx2 = fmaxf(mx2, __uint_as_float(v[e + 2]));
-                    mx3 = fmaxf(mx3, __uint_as_float(v[e + 3]));
-                }
-            }
-            // row max across the two halves, exchanged through spare TMEM columns
-            float mraw = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-            tc::tmem_st1(xchg + s * 2 + hsel, __float_as_uint(mraw));
-            tc::tmem_st_wait();
-            tc::tc_fence_before();
-            tc::named_bar_sync(bar_id, 64);
-            tc::tc_fence_after();
-            mraw = fmaxf(mraw, __uint_as_float(tc::tmem_ld1(xchg + s * 2 + (hsel ^ 1))));
-            tc::tmem_ld_wait();
-            const float mx = mraw * p.scale_log2;
-            float alpha = 1.0f;
-            const bool grow = mx > m_used + kRescaleThreshold || (m_used == -INFINITY && mx > -INFINITY);
-            if (grow) {
-                alpha = m_used == -INFINITY ? 0.0f : tc::ex2_approx(m_used - mx);
-                m_used = mx;
-                l *= alpha;
-            }
-            if (b > 0 && __any_sync(0xffffffffu, grow && alpha != 1.0f)) {
-                // every earlier PV must have landed before O is rescaled
-                tc::mbar_wait(&o_full[(b - 1) & 1], ((b - 1) >> 1) & 1);
+    } else if (warp >= 4) {
+        // ---- softmax: tile x = warp / 4 - 1, one thread per query row (TMEM lane)
+        const uint32_t x = (warp >> 2) - 1;
+        const uint32_t nb = x ? nb1 : nb0;
+        const uint32_t tile_x = x ? u.tile[1] : u.tile[0];
+        const uint32_t slot_x = x ? u.slot[1] : u.slot[0];
+        if (nb > 0) {
+            const uint32_t quarter = warp & 3;
+            const uint32_t r = quarter * 32 + lane;
+            const uint32_t qi = tile_x * 128u + r;
+            const bool valid = qi < p.m;
+            const uint32_t limit = valid ? p.rows[qi] : 0u;
+            const uint32_t lane_base = (quarter * 32u) << 16;
+            const uint32_t s_col = tmem + lane_base + x * 256, o_col = s_col + 128;
+            float m_used = -INFINITY, l = 0.0f;
+            for (uint32_t j = 0; j < nb; ++j) {
+                const uint32_t k0 = (u.b0 + j) * 128u;
+                tc::mbar_wait(&s_full[x], j & 1);
+                const bool dbg_me = p.dbg && blockIdx.x == 0 && x == 0 && r == 0;
+                if (dbg_me) p.dbg[j * 8 + 5] = globaltimer_ns();
                 tc::tc_fence_after();
-                const uint32_t oa = tmem + lane_base + 256 + hsel * 64;
+                // the row's 128 scores, one TMEM round trip (the softmax warpgroups hold 224
+                // registers each after setmaxnreg); keys past the row's position (or an invalid
+                // row) contribute nothing
+                uint32_t v[4][32];
+                tc::tmem_ld32(s_col, v[0]);
+                tc::tmem_ld32(s_col + 32, v[1]);
+                tc::tmem_ld32(s_col + 64, v[2]);
+                tc::tmem_ld32(s_col + 96, v[3]);
+                tc::tmem_ld_wait();
+                const bool masked = __any_sync(0xffffffffu, !valid || k0 + 127 > limit);
+                if (masked) {
+#pragma unroll
+                    for (uint32_t e = 0; e < 128; ++e)
+                        if (!valid || k0 + e > limit) v[e >> 5][e & 31] = __float_as_uint(-INFINITY);
+                }
+                float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+                for (uint32_t e = 0; e < 32; ++e) {
+                    mx0 = fmaxf(mx0, __uint_as_float(v[0][e]));
+                    mx1 = fmaxf(mx1, __uint_as_float(v[1][e]));
+                    mx2 = fmaxf(mx2, __uint_as_float(v[2][e]));
+                    mx3 = fmaxf(mx3, __uint_as_float(v[3][e]));
+                }
+                const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.scale_log2;
+                if (dbg_me) p.dbg[j * 8 + 7] = globaltimer_ns();
+                float alpha = 1.0f;
+                const bool grow = mx > m_used + kRescaleThreshold || (m_used == -INFINITY && mx > -INFINITY);
+                if (grow) {
+                    alpha = m_used == -INFINITY ? 0.0f : tc::ex2_approx(m_used - mx);
+                    m_used = mx;
+                    l *= alpha;
+                }
+                if (j > 0 && __any_sync(0xffffffffu, grow && alpha != 1.0f)) {
+                    // every earlier PV of this tile must have landed before O is rescaled
+                    tc::mbar_wait(&o_done[x], (j - 1) & 1);
+                    tc::tc_fence_after();
+#pragma unroll
+                    for (uint32_t c = 0; c < 128; c += 32) {
+                        uint32_t o[32];
+                        tc::tmem_ld32(o_col + c, o);
+                        tc::tmem_ld_wait();
+#pragma unroll
+                        for (uint32_t e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                        tc::tmem_st32(o_col + c, o);
+                    }
+                    tc::tmem_st_wait();
+                }
+                const float neg_m = m_used == -INFINITY ? 0.0f : -m_used;
+                f2 lsum = mk2(0.f, 0.f);
+                const f2 sc2 = mk2(p.scale_log2, p.scale_log2), nm2 = mk2(neg_m, neg_m);
 #pragma unroll
                 for (uint32_t c = 0; c < 4; ++c) {
-                    uint32_t o[16];
-                    tc::tmem_ld16(oa + c * 16, o);
-                    tc::tmem_ld_wait();
+                    // exp2(s * scale - m) in packed pairs: three of every four pairs on MUFU,
+                    // one on the FMA pipe (balances the MUFU and issue budgets); masked keys
+                    // give exactly 0. P_X(j) (bf16 pairs) goes to TMEM columns [16c, 16c+16)
+                    // of S_X (whose scores are all in registers by now).
+                    uint32_t pk[16];
 #pragma unroll
-                    for (uint32_t e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                    tc::tmem_st16(oa + c * 16, o);
+                    for (uint32_t e = 0; e < 32; e += 2) {
+                        const f2 xs = fma2(mk2(__uint_as_float(v[c][e]), __uint_as_float(v[c][e + 1])), sc2, nm2);
+                        f2 ex;
+                        if ((e & 6) == 6) ex = exp2_poly2(xs);
+                        else ex = mk2(tc::ex2_approx(lo(xs)), tc::ex2_approx(hi(xs)));
+                        lsum = add2(lsum, ex);
+                        pk[e >> 1] = pack_bf16(lo(ex), hi(ex));
+                    }
+                    tc::tmem_st16(s_col + c * 16, pk);
                 }
+                const float l0 = lo(lsum), l1 = hi(lsum);
+                l += l0 + l1;
                 tc::tmem_st_wait();
+                tc::tc_fence_before();
+                if (dbg_me) p.dbg[j * 8 + 6] = globaltimer_ns();
+                tc::mbar_arrive(&p_full[x]);
             }
-            const float neg_m = m_used == -INFINITY ? 0.0f : -m_used;
-            const bool row_dead = m_used == -INFINITY;
-            float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
-            uint32_t pk[32];
+            // ---- epilogue: O / l, or the unnormalised partial + (m, l) for the combine
+            tc::mbar_wait(&o_done[x], (nb - 1) & 1);
+            tc::tc_fence_after();
+            const bool direct = slot_x == kNoTile;
+            const float inv = l > 0.0f ? 1.0f / l : 0.0f;
 #pragma unroll
-            for (uint32_t e = 0; e < 64; e += 2) {
-                float x0 = tc::ex2_approx(fmaf(__uint_as_float(v[e]), p.scale_log2, neg_m));
-                float x1 = tc::ex2_approx(fmaf(__uint_as_float(v[e + 1]), p.scale_log2, neg_m));
-                if (masked) {
-                    x0 = (j0 + e <= limit && !row_dead) ? x0 : 0.0f;
-                    x1 = (j0 + e + 1 <= limit && !row_dead) ? x1 : 0.0f;
+            for (uint32_t c = 0; c < 128; c += 32) {
+                uint32_t o[32];
+                tc::tmem_ld32(o_col + c, o);
+                tc::tmem_ld_wait();
+                if (!valid) continue;
+                if (direct) {
+                    uint4* dst = reinterpret_cast<uint4*>(p.out + (size_t)qi * p.h + u.head * 128u + c);
+#pragma unroll
+                    for (uint32_t q = 0; q < 4; ++q) {
+                        uint4 w;
+                        w.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+                        w.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+                        w.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+                        w.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+                        dst[q] = w;
+                    }
+                } else {
+                    float4* dst = reinterpret_cast<float4*>(p.part_o + ((size_t)slot_x * 128 + r) * 128 + c);
+#pragma unroll
+                    for (uint32_t e = 0; e < 8; ++e)
+                        dst[e] = make_float4(__uint_as_float(o[4 * e]), __uint_as_float(o[4 * e + 1]),
+                                             __uint_as_float(o[4 * e + 2]), __uint_as_float(o[4 * e + 3]));
                 }
-                if (e & 2) { l2 += x0; l3 += x1; } else { l0 += x0; l1 += x1; }
-                pk[e >> 1] = pack_bf16(x0, x1);
             }
-            l += (l0 + l1) + (l2 + l3);
-            // P_b -> TMEM columns [s*128 + hsel*32, +32) of my lanes (S_b already consumed)
-            tc::tmem_st32(tmem + lane_base + s * 128 + hsel * 32, pk);
-            tc::tmem_st_wait();
-            tc::tc_fence_before();
-            tc::mbar_arrive(&p_full[s]);
+            if (valid && !direct) p.part_ml[(size_t)slot_x * 128 + r] = make_float2(m_used, l);
         }
-        // ---- epilogue: O / l over both halves' partial row sums
-        tc::tmem_st1(xchg + 4 + hsel, __float_as_uint(l));
-        tc::tmem_st_wait();
-        tc::mbar_wait(&o_full[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
-        tc::tc_fence_before();
-        tc::named_bar_sync(bar_id, 64);
-        tc::tc_fence_after();
-        l += __uint_as_float(tc::tmem_ld1(xchg + 4 + (hsel ^ 1)));
-        tc::tmem_ld_wait();
-        const uint32_t oa = tmem + lane_base + 256 + hsel * 64;
-        const bool direct = u.slot == 0xffffffffu;
-        const float inv = l > 0.0f ? 1.0f / l : 0.0f;
-#pragma unroll
-        for (uint32_t c = 0; c < 4; ++c) {
-            uint32_t o[16];
-            tc::tmem_ld16(oa + c * 16, o);
-            tc::tmem_ld_wait();
-            if (!valid) continue;
-            const uint32_t d0 = hsel * 64 + c * 16;
-            if (direct) {
-                __nv_bfloat16* dst = p.out + (size_t)qi * p.h + u.head * 128u + d0;
-                uint4 a, b2;
-                a.x = pack_bf16(__uint_as_float(o[0]) * inv, __uint_as_float(o[1]) * inv);
-                a.y = pack_bf16(__uint_as_float(o[2]) * inv, __uint_as_float(o[3]) * inv);
-                a.z = pack_bf16(__uint_as_float(o[4]) * inv, __uint_as_float(o[5]) * inv);
-                a.w = pack_bf16(__uint_as_float(o[6]) * inv, __uint_as_float(o[7]) * inv);
-                b2.x = pack_bf16(__uint_as_float(o[8]) * inv, __uint_as_float(o[9]) * inv);
-                b2.y = pack_bf16(__uint_as_float(o[10]) * inv, __uint_as_float(o[11]) * inv);
-                b2.z = pack_bf16(__uint_as_float(o[12]) * inv, __uint_as_float(o[13]) * inv);
-                b2.w = pack_bf16(__uint_as_float(o[14]) * inv, __uint_as_float(o[15]) * inv);
-                reinterpret_cast<uint4*>(dst)[0] = a;
-                reinterpret_cast<uint4*>(dst)[1] = b2;
-            } else {
-                float4* dst = reinterpret_cast<float4*>(p.part_o + ((size_t)u.slot * 128 + r) * 128 + d0);
-#pragma unroll
-                for (uint32_t e = 0; e < 4; ++e)
-                    dst[e] = make_float4(__uint_as_float(o[4 * e]), __uint_as_float(o[4 * e + 1]),
-                                         __uint_as_float(o[4 * e + 2]), __uint_as_float(o[4 * e + 3]));
-            }
-        }
-        if (valid && !direct && hsel == 0) p.part_ml[(size_t)u.slot * 128 + r] = make_float2(m_used, l);
     }
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
-    if (warp == 1) tc::tmem_dealloc(tmem, 512);
+    if (warp == 0) tc::tmem_dealloc(tmem, 512);
 }
 
 // Merge split partials of one (tile, head): O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s.
@@ -363,7 +439,9 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnCombine* __
 
 }  // namespace
 
-// Host: split every (query tile, head) key range into units of at most `chunk` blocks.
+// Host: split every (query tile, head) key range into chunks of at most `chunk` blocks,
+// then pair the chunks of two query tiles that start at the same key block of the same
+// head into one item (they share the K/V stream; each stops at its own end block).
 AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads) {
     AttnPlan plan;
     const uint32_t tiles = ceil_div(m, 128);
@@ -374,38 +452,68 @@ AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads) {
         nblk[t] = rows[last] / 128 + 1;
         total += (uint64_t)nblk[t] * n_heads;
     }
-    // ~3 waves of units; never split below 2 blocks per unit
+    // ~1.5 waves of items (an item carries up to two tiles); never split below 2 blocks
     uint32_t chunk = (uint32_t)std::max<uint64_t>(2, (total + 3 * kNumSMs - 1) / (3 * kNumSMs));
     uint32_t longest = 0;
     for (uint32_t t = 0; t < tiles; ++t) longest = std::max(longest, nblk[t]);
     chunk = std::max(chunk, ceil_div(longest, 16));  // the combine merges at most 16 splits
+    std::vector<uint32_t> slot0(tiles * n_heads, kNoTile);
     uint32_t slot = 0;
     for (uint32_t t = 0; t < tiles; ++t) {
         const uint32_t splits = ceil_div(nblk[t], chunk);
+        if (splits < 2) continue;
         for (uint32_t hd = 0; hd < n_heads; ++hd) {
-            if (splits > 1) plan.combine.push_back(AttnCombine{t, hd, slot, splits});
-            for (uint32_t sp = 0; sp < splits; ++sp) {
-                AttnUnit u;
-                u.tile = t;
-                u.head = hd;
-                u.b0 = sp * chunk;
-                u.b1 = std::min(nblk[t], (sp + 1) * chunk);
-                u.slot = splits > 1 ? slot + sp : 0xffffffffu;
-                plan.units.push_back(u);
-            }
-            if (splits > 1) slot += splits;
+            plan.combine.push_back(AttnCombine{t, hd, slot, splits});
+            slot0[t * n_heads + hd] = slot;
+            slot += splits;
         }
     }
     plan.slots = slot;
-    // Launch order = (head, key range, query tile): the query tiles that read the same K/V
-    // blocks of a head run side by side, so each block comes from HBM once and the other
-    // tiles hit it in L2 (a layer's K/V, 2*n*h*2 B = 154 MB at n=9418, exceeds the L2).
+    for (uint32_t hd = 0; hd < n_heads; ++hd) {
+        const uint32_t max_splits = ceil_div(longest, chunk);
+        for (uint32_t sp = 0; sp < max_splits; ++sp) {
+            AttnUnit cur{};
+            bool open = false;
+            for (uint32_t t = 0; t < tiles; ++t) {
+                if (sp * chunk >= nblk[t]) continue;
+                const uint32_t b1 = std::min(nblk[t], (sp + 1) * chunk);
+                const uint32_t s0 = slot0[t * n_heads + hd];
+                const uint32_t sl = s0 == kNoTile ? kNoTile : s0 + sp;
+                if (!open) {
+                    cur = AttnUnit{hd, sp * chunk, {t, kNoTile}, {b1, 0}, {sl, kNoTile}};
+                    open = true;
+                } else {
+                    cur.tile[1] = t;
+                    cur.b1[1] = b1;
+                    cur.slot[1] = sl;
+                    plan.units.push_back(cur);
+                    open = false;
+                }
+            }
+            if (open) plan.units.push_back(cur);
+        }
+    }
+    // longest items first (they set the critical path); items of one head stay together
     std::stable_sort(plan.units.begin(), plan.units.end(), [](const AttnUnit& a, const AttnUnit& b) {
-        if (a.head != b.head) return a.head < b.head;
-        if (a.b0 != b.b0) return a.b0 < b.b0;
-        return a.tile < b.tile;
+        const uint32_t la = std::max(a.b1[0], a.tile[1] == kNoTile ? 0u : a.b1[1]) - a.b0;
+        const uint32_t lb = std::max(b.b1[0], b.tile[1] == kNoTile ? 0u : b.b1[1]) - b.b0;
+        return la > lb;
     });
     return plan;
+}
+
+// MPIC_ATTN_TS=1 (diagnostics): CTA 0 records per-block event times; printed by
+// mpic_test_attention.
+unsigned long long* attn_debug_buffer() {
+    static unsigned long long* buf = [] {
+        unsigned long long* b = nullptr;
+        if (getenv("MPIC_ATTN_TS")) {
+            cudaMalloc(&b, 8 * 4096 * sizeof(unsigned long long));
+            cudaMemset(b, 0, 8 * 4096 * sizeof(unsigned long long));
+        }
+        return b;
+    }();
+    return buf;
 }
 
 void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const __nv_bfloat16* vcache,
@@ -426,7 +534,8 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     p.out = out;
     p.part_o = part_o;
     p.part_ml = part_ml;
-    const size_t smem = (1 + 2 * kKvStages) * kTile + 1024 + (1 + 4 * kKvStages + 6) * 8 + 16;
+    p.dbg = attn_debug_buffer();
+    const size_t smem = (2 + kKStages + kVStages) * kTile + 1024 + (1 + 2 * kKStages + 2 * kVStages + 6) * 8 + 16;
     static bool attr = false;
     if (!attr) {
         MPIC_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
