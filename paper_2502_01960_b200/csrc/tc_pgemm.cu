@@ -472,6 +472,10 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
         const char* e = getenv("MPIC_PG_SPLIT");  // diagnostics: force the in-cluster K split
         return e ? (uint32_t)atoi(e) : 0u;
     }();
+    static const bool split_pieces = [] {
+        const char* e = getenv("MPIC_PG_PIECES");  // diagnostics: 1 = two accumulator chains per group
+        return e && atoi(e) != 0;
+    }();
     static const uint32_t kps_env = [] {
         const char* e = getenv("MPIC_PG_KPS");  // diagnostics: k-blocks per pipeline stage
         return e ? (uint32_t)atoi(e) : 0u;
@@ -502,6 +506,13 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
             a.P0 = round16(ceil_div(M, a.ngroups));
             a.P1 = 0;
             if (a.P0 > 256 || (gm > 1 && a.P0 < 64)) continue;
+            // two interleaved accumulator chains (off by default: each cta_group::2 MMA costs at
+            // least ~83 cycles, so halving N loses more than the interleave gains)
+            if (split_pieces && a.P0 >= 64) {
+                const uint32_t g = a.P0;
+                a.P0 = round16((g + 1) / 2);
+                a.P1 = g - a.P0;
+            }
         }
         a.G = a.P0 + a.P1;
         a.nbuf = 2 * a.G <= 512 ? 2 : 1;
@@ -525,7 +536,12 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
         a.ep = ep_in;
         const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 5) * 8 + 16;
         const uint32_t nchunks = (a.G + 31) / 32;
-        const double t_kb = std::max(2.0 * a.G, 256.0 + a.G);
+        // MMA cycles per k-block (4 k16 steps): a cta_group::2 instruction costs
+        // max(N/2, ~83) cycles, and a lone accumulator chain issues ~1.5x slower than two
+        // interleaved ones (tools/mma_pair_probe); operand fill ~256 + G cycles.
+        const double mma = 4.0 * (std::max(a.P0 / 2.0, 83.0) + (a.P1 ? std::max(a.P1 / 2.0, 83.0) : 0.0)) *
+                           (a.P1 ? 1.0 : 1.5);
+        const double t_kb = std::max(mma, 256.0 + a.G);
         for (uint32_t S : {1u, 2u, 3u, 4u}) {
             if (force_s && S != force_s && S != 1) continue;
             if (S > 1 && a.kblocks / S < 2) continue;
