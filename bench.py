@@ -327,9 +327,16 @@ def run_ours(args, world, rank, local):
             if isinstance(v, dict) and "achieved" in v]
     dom = max(cand)[1]
     d = per_phase[dom]
+    traffic = None
+    try:  # DRAM bytes per launch of this kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        pass
     roofline = {"bound": d["bound"], "achieved": d["achieved"],
                 "peak": hbm if d["bound"] == "hbm" else tf_sust, "unit": d["unit"],
-                "frac": d["frac"], "traffic": None, "kernel": dom,
+                "frac": d["frac"], "traffic": traffic, "kernel": dom,
+                "traffic_source": "profiles/traffic.json (ncu --set full, one launch)",
                 "peak_source": peak_src + (" HBM copy" if d["bound"] == "hbm"
                                            else " bf16 sustained"),
                 "per_launch_algorithmic": (asm_bytes if dom == "assemble" else
