@@ -213,6 +213,29 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
  * full PCIe rate): the loader streams layer l of every chunk to HBM on a side stream while
  * layer l-1 is being recomputed; each landed layer is assembled (and cast to the model
  * dtype) right before it is used. */
+/* ---- head-parallel request (one long request over P GPUs) ---------------
+ * Rank r owns heads [head0, head0 + n_local_heads): its model holds those heads' Wq/Wk/Wv
+ * rows and Wo columns (bit-identical slices of build_model's weights) and the full FFN; its
+ * request cache is [L][n][n_local_heads][D]. Per layer l the caller runs
+ *   mpic_hp_layer_attn(l) -> partial[m_pad][h] (fp32: this rank's heads' share of attn.Wo^T)
+ *   reduce-scatter(sum) of partial over the P ranks, rank r receiving rows [r*mr, (r+1)*mr)
+ *   mpic_hp_layer_ffn(l, reduced, r*mr, mr) -> x/xb rows updated (residual + FFN)
+ *   all-gather of the bf16 rows of xb (in place, mpic_workspace_device_ptr(ws, 1))
+ * with m_pad = mr * P >= m. The rank holding row m-1 calls mpic_hp_logits(m-1). Partial
+ * rows >= m must be zero. bf16 models with head_dim 128 only. */
+int mpic_model_create_heads(const mpic_model_config* cfg, int device, mpic_dtype dtype, uint32_t head0,
+                            uint32_t n_local_heads, mpic_model_t* out);
+int mpic_hp_prepare(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt, const mpic_policy* policy,
+                    const mpic_kv_t* chunks, mpic_reposition reposition, const uint32_t* position_bases,
+                    mpic_kv_t linked, uint32_t* selected, uint32_t* m_out, void* stream);
+int mpic_hp_layer_attn(mpic_model_t model, mpic_workspace_t ws, uint32_t layer, mpic_kv_t linked, float* d_partial,
+                       void* stream);
+int mpic_hp_layer_ffn(mpic_model_t model, mpic_workspace_t ws, uint32_t layer, const float* d_reduced, uint32_t row0,
+                      uint32_t rows, void* stream);
+int mpic_hp_logits(mpic_model_t model, mpic_workspace_t ws, uint32_t row, float* logits, void* stream);
+/* Device pointer of a workspace buffer: 0 = x (fp32 [m_pad][h]), 1 = xb (bf16 [m_pad][h]). */
+int mpic_workspace_device_ptr(mpic_workspace_t ws, int which, void** out);
+
 /* CUDA-graph replay of mpic_request_prefill (default on): a request with the same launch
  * signature as the previous one on this workspace (model, linked cache, n, m, chunk count,
  * plan sizes) is captured once and replayed after that, with its inputs re-staged. */

@@ -95,6 +95,12 @@ SIGNATURES = {
                                          _vp, _int, _vp, _vp, _vp, _P(_u32), _vp]),
     "mpic_kv_download_rows": (_int, [_vp, _vp, _u32, _vp, _vp, _vp]),
     "mpic_workspace_set_graphs": (_int, [_vp, _int]),
+    "mpic_model_create_heads": (_int, [_P(ModelConfig), _int, _int, _u32, _u32, _P(_vp)]),
+    "mpic_hp_prepare": (_int, [_vp, _vp, _P(PromptDesc), _P(PolicyDesc), _vp, _int, _vp, _vp, _vp, _P(_u32), _vp]),
+    "mpic_hp_layer_attn": (_int, [_vp, _vp, _u32, _vp, _vp, _vp]),
+    "mpic_hp_layer_ffn": (_int, [_vp, _vp, _u32, _vp, _u32, _u32, _vp]),
+    "mpic_hp_logits": (_int, [_vp, _vp, _u32, _vp, _vp]),
+    "mpic_workspace_device_ptr": (_int, [_vp, _int, _P(_vp)]),
     "mpic_clock_probe": (_int, [_vp, _u32, _vp]),
     "mpic_test_gemm": (_int, [_vp, _vp, _u32, _u32, _u32, _int, _vp, _vp]),
     "mpic_test_gemm_epi": (_int, [_vp, _vp, _u32, _u32, _u32, _int, _vp, _vp, _vp, _vp]),

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmChunk* __restric
             continue;
         }
         const AsmChunk ch = s_chunks[c];
-        const size_t soff = ((size_t)l * ch.src_tokens + ch.src_row0 + (r - ch.dst_row0)) * h;
+        const size_t soff = ((size_t)l * ch.src_tokens + ch.src_row0 + (r - ch.dst_row0)) * ch.src_ld + ch.src_col0;
         const TS* ks = static_cast<const TS*>(ch.src_k) + soff;
         const TS* vs = static_cast<const TS*>(ch.src_v) + soff;
         const float2* tab = s_tab + (size_t)ch.table * half_d;
@@ -210,6 +210,58 @@ void launch_synth(uint64_t seed, uint64_t tag, uint32_t layer, size_t count, flo
     const uint64_t h1 = mix64_host(mix64_host(seed + phi) ^ (stream + phi));
     if (dt == MPIC_F32) synth_kernel<float><<<kNumSMs * 8, 256, 0, s>>>(h1, count, scale, (float*)dst);
     else synth_kernel<__nv_bfloat16><<<kNumSMs * 8, 256, 0, s>>>(h1, count, scale, (__nv_bfloat16*)dst);
+    MPIC_LAUNCHED();
+}
+
+template <typename T>
+__global__ void synth_2d_kernel(uint64_t h1, uint32_t rows, uint32_t cols_total, uint32_t row0, uint32_t col0,
+                                uint32_t ncols, float scale, T* __restrict__ dst) {
+    const size_t count = (size_t)rows * ncols;
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < count; k += (size_t)gridDim.x * blockDim.x) {
+        const size_t r = k / ncols, j = k % ncols;
+        const size_t i = (row0 + r) * (size_t)cols_total + col0 + j;
+        const uint64_t hv = mix64(h1 ^ (i + 0x9e3779b97f4a7c15ull));
+        const uint32_t bits = (uint32_t)(hv >> 40);
+        const float u = __fsub_rn(__fmul_rn((float)bits, 2.0f / 16777216.0f), 1.0f);
+        dst[k] = from_f32<T>(__fmul_rn(u, scale));
+    }
+}
+
+void launch_synth_2d(uint64_t seed, uint64_t tag, uint32_t layer, uint32_t rows, uint32_t cols_total,
+                     uint32_t row0, uint32_t col0, uint32_t ncols, float scale, void* dst, mpic_dtype dt,
+                     cudaStream_t s) {
+    const uint64_t phi = 0x9e3779b97f4a7c15ull;
+    const uint64_t stream = (tag << 32) | layer;
+    const uint64_t h1 = mix64_host(mix64_host(seed + phi) ^ (stream + phi));
+    if (dt == MPIC_F32)
+        synth_2d_kernel<float><<<kNumSMs * 8, 256, 0, s>>>(h1, rows, cols_total, row0, col0, ncols, scale, (float*)dst);
+    else
+        synth_2d_kernel<__nv_bfloat16><<<kNumSMs * 8, 256, 0, s>>>(h1, rows, cols_total, row0, col0, ncols, scale,
+                                                                   (__nv_bfloat16*)dst);
+    MPIC_LAUNCHED();
+}
+
+__global__ void resid_add_kernel(float* __restrict__ x, const float* __restrict__ add, __nv_bfloat16* __restrict__ xb,
+                                 size_t n4) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+        float4 a = reinterpret_cast<float4*>(x)[i];
+        const float4 b = reinterpret_cast<const float4*>(add)[i];
+        a.x += b.x;
+        a.y += b.y;
+        a.z += b.z;
+        a.w += b.w;
+        reinterpret_cast<float4*>(x)[i] = a;
+        __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        reinterpret_cast<uint2*>(xb)[i] = pk;
+    }
+}
+
+void launch_resid_add(float* x, const float* add, __nv_bfloat16* xb, size_t n, cudaStream_t s) {
+    MPIC_REQUIRE(n % 4 == 0, MPIC_ERR_VALIDATION, "resid_add needs n % 4 == 0");
+    resid_add_kernel<<<kNumSMs * 4, 256, 0, s>>>(x, add, xb, n / 4);
     MPIC_LAUNCHED();
 }
 

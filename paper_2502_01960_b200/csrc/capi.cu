@@ -80,6 +80,9 @@ struct mpic_model_s {
     uint32_t rope_cap = 0;
     std::vector<float2*> retired;  // old tables kept alive (other streams may read them)
     std::mutex mu;
+    // head-parallel slice (mpic_model_create_heads): attention weights of heads
+    // [head0, head0 + n_local_heads) only; 0 local heads = the whole model
+    uint32_t head0 = 0, n_local_heads = 0;
 };
 
 struct mpic_kv_s {
@@ -151,6 +154,7 @@ struct mpic_workspace_s {
     GraphSig last_sig{}, graph_sig{};
     cudaGraphExec_t graph = nullptr;
     uint32_t graph_kernels = 0;
+    uint32_t hp_m = 0, hp_n = 0;  // head-parallel request in flight (mpic_hp_prepare)
 };
 
 #define API_BEGIN \
@@ -544,9 +548,12 @@ struct AsmPlan {
     uint32_t n_tables = 0;
 };
 
+// src_ld / src_col0: source row width and first column (head-parallel slices); 0 / 0 =
+// the destination's own width (T_dst_h = H_dst * D).
 AsmPlan plan_assembly(const void* const* src_k, const void* const* src_v, const uint32_t* src_T,
                       const mpic_chunk_ref* chunks, uint32_t n, uint32_t T_dst, uint32_t D,
-                      mpic_reposition rep, float rope_base) {
+                      mpic_reposition rep, float rope_base, uint32_t T_dst_h = 0, uint32_t src_ld = 0,
+                      uint32_t src_col0 = 0) {
     MPIC_REQUIRE(D % 2 == 0, MPIC_ERR_CONFIG, "head_dim must be even on the B200 path");
     AsmPlan p;
     p.chunks.resize(n);
@@ -562,6 +569,9 @@ AsmPlan plan_assembly(const void* const* src_k, const void* const* src_v, const 
         a.src_k = src_k ? src_k[i] : nullptr;
         a.src_v = src_v ? src_v[i] : nullptr;
         a.src_tokens = src_T[i];
+        MPIC_REQUIRE(src_ld || T_dst_h, MPIC_ERR_VALIDATION, "assembly needs the destination row width");
+        a.src_ld = src_ld ? src_ld : T_dst_h;
+        a.src_col0 = src_col0;
         a.src_row0 = c.src_row0;
         a.dst_row0 = c.dst_row0;
         a.rows = c.rows;
@@ -605,7 +615,7 @@ void do_assemble(cudaStream_t s, const void* const* src_k, const void* const* sr
                  const uint32_t* src_T, mpic_dtype src_t, const mpic_chunk_ref* chunks,
                  uint32_t n, mpic_kv_t dst, mpic_reposition rep, int zero_gaps, float rope_base) {
     MPIC_REQUIRE(dst, MPIC_ERR_VALIDATION, "null destination cache");
-    const AsmPlan p = plan_assembly(src_k, src_v, src_T, chunks, n, dst->T, dst->D, rep, rope_base);
+    const AsmPlan p = plan_assembly(src_k, src_v, src_T, chunks, n, dst->T, dst->D, rep, rope_base, dst->H * dst->D);
     const AsmChunk* dc;
     const float2* dt;
     void* buf = upload_plan(p, s, &dc, &dt);
@@ -1260,7 +1270,7 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
     }
     const mpic_dtype src_t = n_img ? chunks[0]->dtype : model->dtype;
     const AsmPlan ap = plan_assembly(ks.data(), vs.data(), ts.data(), r.refs.data(), n_img, linked->T, linked->D,
-                                     reposition, model->cfg.rope_base);
+                                     reposition, model->cfg.rope_base, linked->H * linked->D);
     ensure_rope(model, r.n, s);
     if (use_tc_attention(model)) prepare_attn_plan(ws, r.sel.data(), r.m, r.n - 1, model->cfg.n_heads);
     std::memcpy(ws->h_ids, r.ids_sel.data(), r.m * sizeof(int32_t));
@@ -1350,6 +1360,239 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
     API_END
 }
 
+// ---- head-parallel request ---------------------------------------------
+// Rank r of P owns heads [r*H/P, (r+1)*H/P): its model holds those heads' Wq/Wk/Wv rows
+// and the matching Wo columns (bit-identical slices of the synthetic weights) plus the full
+// FFN; its request cache holds only its heads. Per layer: mpic_hp_layer_attn (QKV, attention,
+// Wo partial sums of all h outputs) -> reduce-scatter of the partials across ranks (caller,
+// NCCL) -> mpic_hp_layer_ffn on this rank's rows -> all-gather of the bf16 rows (caller).
+int mpic_model_create_heads(const mpic_model_config* cfg, int device, mpic_dtype dtype, uint32_t head0,
+                            uint32_t n_local_heads, mpic_model_t* out) {
+    mpic_model_t m = nullptr;
+    API_BEGIN
+    validate_cfg(cfg);
+    validate_device_cfg(cfg);
+    MPIC_REQUIRE(n_local_heads > 0 && head0 + n_local_heads <= cfg->n_heads, MPIC_ERR_VALIDATION,
+                 "head slice outside the model");
+    set_device(device);
+    m = new mpic_model_s();
+    m->cfg = *cfg;
+    m->device = device;
+    m->dtype = dtype;
+    m->head0 = head0;
+    m->n_local_heads = n_local_heads;
+    const size_t h = cfg->hidden_dim, V = cfg->vocab_size, L = cfg->n_layers, D = cfg->head_dim;
+    const size_t hs = n_local_heads * D, e = esz(dtype);
+    m->emb = dmalloc<float>(V * h);
+    MPIC_CUDA(cudaMalloc(&m->lm_head, V * h * e));
+    for (size_t l = 0; l < L; ++l) {
+        void* p;
+        MPIC_CUDA(cudaMalloc(&p, 3 * hs * h * e));
+        m->wqkv.push_back(p);
+        MPIC_CUDA(cudaMalloc(&p, h * hs * e));
+        m->wo.push_back(p);
+        MPIC_CUDA(cudaMalloc(&p, 4 * h * h * e));
+        m->w1.push_back(p);
+        MPIC_CUDA(cudaMalloc(&p, 4 * h * h * e));
+        m->w2.push_back(p);
+    }
+    std::vector<double> inv(D / 2);
+    for (uint32_t i = 0; i + 1 < D; i += 2)  // model.cpp:51-53
+        inv[i / 2] = std::pow(static_cast<double>(cfg->rope_base), -static_cast<double>(i) / D);
+    m->inv_freq = dmalloc<double>(D / 2);
+    MPIC_CUDA(cudaMemcpy(m->inv_freq, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice));
+    const float scale = 1.0f / std::sqrt(static_cast<float>(h));  // model.cpp:106
+    cudaStream_t s = 0;
+    const uint32_t r0 = head0 * (uint32_t)D;
+    launch_synth(cfg->seed, 100, 0, V * h, 1.0f, m->emb, MPIC_F32, s);
+    launch_synth(cfg->seed, 101, 0, V * h, scale, m->lm_head, dtype, s);
+    for (uint32_t l = 0; l < cfg->n_layers; ++l) {
+        for (uint32_t part = 0; part < 3; ++part)  // rows [r0, r0+hs) of Wq, Wk, Wv
+            launch_synth_2d(cfg->seed, 1 + part, l, (uint32_t)hs, (uint32_t)h, r0, 0, (uint32_t)h, scale,
+                            (char*)m->wqkv[l] + part * hs * h * e, dtype, s);
+        launch_synth_2d(cfg->seed, 4, l, (uint32_t)h, (uint32_t)h, 0, r0, (uint32_t)hs, scale, m->wo[l], dtype, s);
+        launch_synth(cfg->seed, 5, l, 4 * h * h, scale, m->w1[l], dtype, s);
+        launch_synth(cfg->seed, 6, l, 4 * h * h, scale, m->w2[l], dtype, s);
+    }
+    ensure_rope(m, 1, s);
+    MPIC_CUDA(cudaDeviceSynchronize());
+    *out = m;
+    m = nullptr;
+    API_END
+}
+
+int mpic_hp_prepare(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt, const mpic_policy* policy,
+                    const mpic_kv_t* chunks, mpic_reposition reposition, const uint32_t* position_bases,
+                    mpic_kv_t linked, uint32_t* selected, uint32_t* m_out, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(model->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    MPIC_REQUIRE(ws && ws->model == model, MPIC_ERR_VALIDATION, "workspace belongs to another model");
+    MPIC_REQUIRE(model->n_local_heads && model->dtype == MPIC_BF16, MPIC_ERR_VALIDATION,
+                 "head-parallel needs a bf16 head-slice model (mpic_model_create_heads)");
+    const uint32_t D = model->cfg.head_dim, hs = model->n_local_heads * D, h = model->cfg.hidden_dim;
+    const RequestPlan r = plan_request(model, prompt, policy, position_bases);
+    MPIC_REQUIRE(linked && linked->L == model->cfg.n_layers && linked->T == r.n && linked->H == model->n_local_heads &&
+                     linked->D == D && linked->dtype == model->dtype,
+                 MPIC_ERR_VALIDATION, "request cache must be [L][n][local heads][D] of the model dtype");
+    MPIC_REQUIRE(r.m <= ws->max_rows, MPIC_ERR_VALIDATION, "more rows than the workspace holds");
+    check_ids(model, r.ids_sel.data(), r.m);
+    const uint32_t n_img = (uint32_t)r.refs.size();
+    std::vector<const void*> ks(n_img), vs(n_img);
+    std::vector<uint32_t> ts(n_img);
+    for (uint32_t i = 0; i < n_img; ++i) {
+        const mpic_kv_t c = chunks[i];
+        MPIC_REQUIRE(c, MPIC_ERR_LINK, "no fetched entry for image segment");
+        MPIC_REQUIRE(c->T == r.refs[i].rows, MPIC_ERR_LINK, "token_count mismatch for image segment");
+        MPIC_REQUIRE(c->L == linked->L && c->H == model->cfg.n_heads && c->D == D, MPIC_ERR_LINK,
+                     "entry tensor shape does not match model");
+        MPIC_REQUIRE(c->dtype == chunks[0]->dtype, MPIC_ERR_VALIDATION, "mixed chunk dtypes");
+        ks[i] = c->k;
+        vs[i] = c->v;
+        ts[i] = c->T;
+    }
+    // this rank's head columns of every chunk -> its request cache
+    const AsmPlan ap = plan_assembly(ks.data(), vs.data(), ts.data(), r.refs.data(), n_img, linked->T, D, reposition,
+                                     model->cfg.rope_base, hs, h, model->head0 * D);
+    const AsmChunk* dc;
+    const float2* dt;
+    void* buf = upload_plan(ap, s, &dc, &dt);
+    {
+        ProfScope ps(s, MPIC_PHASE_ASSEMBLE);
+        launch_assemble(dc, n_img, dt, ap.n_tables, n_img ? chunks[0]->dtype : model->dtype, linked->k, linked->v,
+                        linked->dtype, linked->L, linked->T, linked->H, D, 1, s);
+    }
+    MPIC_CUDA(cudaFreeAsync(buf, s));
+    ensure_rope(model, r.n, s);
+    std::memcpy(ws->h_ids, r.ids_sel.data(), r.m * sizeof(int32_t));
+    std::memcpy(ws->h_rows, r.sel.data(), r.m * sizeof(uint32_t));
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_ids, ws->h_ids, r.m * 4, cudaMemcpyHostToDevice, s));
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_rows, ws->h_rows, r.m * 4, cudaMemcpyHostToDevice, s));
+    MPIC_CUDA(cudaMemsetAsync(ws->x, 0, (size_t)ws->m_pad * h * sizeof(float), s));
+    MPIC_CUDA(cudaMemsetAsync(ws->xb, 0, (size_t)ws->m_pad * h * 2, s));
+    {
+        ProfScope ps(s, MPIC_PHASE_EMBED);
+        launch_embed(model->emb, ws->d_ids, r.m, h, ws->x, ws->xb, s);
+    }
+    launch_rope_gather(model->rope, ws->d_rows, r.m, D / 2, ws->rope_tok, s);
+    if (use_tc_attention(model)) {
+        prepare_attn_plan(ws, r.sel.data(), r.m, r.n - 1, model->n_local_heads);
+        enqueue_attn_plan(ws, s);
+    }
+    ws->hp_m = r.m;
+    ws->hp_n = r.n;
+    if (selected) std::memcpy(selected, r.sel.data(), r.m * sizeof(uint32_t));
+    if (m_out) *m_out = r.m;
+    API_END
+}
+
+int mpic_hp_layer_attn(mpic_model_t md, mpic_workspace_t ws, uint32_t l, mpic_kv_t kv, float* d_partial,
+                       void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(md->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    MPIC_REQUIRE(md->n_local_heads && ws->hp_m && l < md->cfg.n_layers, MPIC_ERR_STATE,
+                 "mpic_hp_prepare must run first");
+    const uint32_t m = ws->hp_m, h = md->cfg.hidden_dim, D = md->cfg.head_dim, Hl = md->n_local_heads,
+                   hs = Hl * D;
+    const size_t plane = (size_t)kv->T * hs * 2;
+    void* kl = (char*)kv->k + l * plane;
+    void* vl = (char*)kv->v + l * plane;
+    EpiParams qkv;
+    qkv.mode = EPI_QKV;
+    qkv.q = ws->q;
+    qkv.kv_k = kl;
+    qkv.kv_v = vl;
+    qkv.kv_rows = ws->d_rows;
+    qkv.rope_pos = ws->d_rows;
+    qkv.rope = md->rope;
+    qkv.rope_tok = ws->rope_tok;
+    qkv.hidden = hs;
+    qkv.head_dim = D;
+    {
+        ProfScope ps(s, MPIC_PHASE_QKV);
+        run_gemm(md, ws->xb, md->wqkv[l], m, 3 * hs, h, qkv, s);
+    }
+    {
+        ProfScope ps(s, MPIC_PHASE_ATTN);
+        MPIC_REQUIRE(use_tc_attention(md), MPIC_ERR_VALIDATION, "head-parallel attention needs head_dim 128");
+        launch_attn_tc(static_cast<const __nv_bfloat16*>(ws->q), static_cast<const __nv_bfloat16*>(kl),
+                       static_cast<const __nv_bfloat16*>(vl), kv->T, ws->d_rows, m, Hl, ws->d_units, ws->n_units,
+                       ws->d_comb, ws->n_comb, ws->part_o, ws->part_ml, static_cast<__nv_bfloat16*>(ws->attn), s);
+    }
+    EpiParams st;
+    st.mode = EPI_STORE_F32;
+    st.out = d_partial;
+    st.ldo = h;
+    {
+        ProfScope ps(s, MPIC_PHASE_WO);
+        run_gemm(md, ws->attn, md->wo[l], m, h, hs, st, s);
+    }
+    API_END
+}
+
+int mpic_hp_layer_ffn(mpic_model_t md, mpic_workspace_t ws, uint32_t l, const float* d_reduced, uint32_t row0,
+                      uint32_t rows, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(md->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    MPIC_REQUIRE(md->n_local_heads && ws->hp_m && l < md->cfg.n_layers, MPIC_ERR_STATE,
+                 "mpic_hp_prepare must run first");
+    MPIC_REQUIRE(row0 + rows <= ws->m_pad, MPIC_ERR_VALIDATION, "row range outside the workspace");
+    if (rows == 0) return MPIC_OK;
+    const uint32_t h = md->cfg.hidden_dim;
+    float* x = ws->x + (size_t)row0 * h;
+    __nv_bfloat16* xb = ws->xb + (size_t)row0 * h;
+    launch_resid_add(x, d_reduced, xb, (size_t)rows * h, s);  // x += sum of the ranks' Wo partials
+    EpiParams gl;
+    gl.mode = EPI_GELU;
+    gl.out = ws->ffn;
+    gl.ldo = 4 * h;
+    {
+        ProfScope ps(s, MPIC_PHASE_W1);
+        run_gemm(md, xb, md->w1[l], rows, 4 * h, h, gl, s);
+    }
+    EpiParams res;
+    res.mode = EPI_RESID;
+    res.x = x;
+    res.ldx = h;
+    res.xb = xb;
+    res.partial = ws->partial;
+    res.partial_cap = ws->partial_cap;
+    {
+        ProfScope ps(s, MPIC_PHASE_W2);
+        run_gemm(md, ws->ffn, md->w2[l], rows, h, 4 * h, res, s);
+    }
+    API_END
+}
+
+int mpic_hp_logits(mpic_model_t md, mpic_workspace_t ws, uint32_t row, float* logits, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(md->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    MPIC_REQUIRE(row < ws->m_pad, MPIC_ERR_VALIDATION, "row outside the workspace");
+    const uint32_t h = md->cfg.hidden_dim;
+    {
+        ProfScope ps(s, MPIC_PHASE_LM_HEAD);
+        launch_lm_head(ws->x + (size_t)row * h, md->lm_head, md->dtype, md->cfg.vocab_size, h, ws->d_logits, s);
+    }
+    MPIC_CUDA(cudaMemcpyAsync(ws->h_logits, ws->d_logits, md->cfg.vocab_size * 4, cudaMemcpyDeviceToHost, s));
+    MPIC_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(logits, ws->h_logits, md->cfg.vocab_size * sizeof(float));
+    API_END
+}
+
+int mpic_workspace_device_ptr(mpic_workspace_t ws, int which, void** out) {
+    API_BEGIN
+    MPIC_REQUIRE(ws && out, MPIC_ERR_VALIDATION, "null argument");
+    switch (which) {
+        case 0: *out = ws->x; break;    // residual stream fp32 [m_pad][h]
+        case 1: *out = ws->xb; break;   // its bf16 copy [m_pad][h]
+        default: throw Error(MPIC_ERR_VALIDATION, "unknown workspace buffer");
+    }
+    API_END
+}
+
 int mpic_workspace_set_graphs(mpic_workspace_t ws, int on) {
     API_BEGIN
     MPIC_REQUIRE(ws, MPIC_ERR_VALIDATION, "null workspace");
@@ -1405,7 +1648,7 @@ int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpi
             vs[i] = base + img_rows * h + off[i];
         }
         const AsmPlan p = plan_assembly(ks.data(), vs.data(), ts.data(), r.refs.data(), n_img,
-                                        linked->T, linked->D, reposition, model->cfg.rope_base);
+                                        linked->T, linked->D, reposition, model->cfg.rope_base, linked->H * linked->D);
         n_tab = p.n_tables;
         bufs[sl] = upload_plan(p, s, &dc[sl], &dt[sl]);
     }

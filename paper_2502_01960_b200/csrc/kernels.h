@@ -52,6 +52,8 @@ struct AsmChunk {
     uint32_t rows;
     uint32_t table;  // index of this chunk's (cos,sin) table in the rerotate tables
     uint32_t rotate; // 1 when this chunk's K rows are rotated
+    uint32_t src_ld;   // elements per source row (the chunk's H*D); the destination row is H_dst*D
+    uint32_t src_col0; // first source column copied (head-parallel: head0 * D)
 };
 
 void launch_embed(const float* emb, const int32_t* ids, uint32_t m, uint32_t h, float* x,
@@ -80,6 +82,13 @@ void launch_x_to_bf16(const float* x, __nv_bfloat16* xb, uint32_t m, uint32_t h,
 // Weight synthesis (model.cpp:28-36): dst[i] = counter_uniform(seed, (tag<<32)|layer, i)*scale
 void launch_synth(uint64_t seed, uint64_t tag, uint32_t layer, size_t count, float scale,
                   void* dst, mpic_dtype dt, cudaStream_t s);
+// Sub-matrix of the same synthetic weight: dst[r][j] = w[(row0 + r) * cols_total + col0 + j]
+// for r < rows, j < ncols (head-parallel slices, bit-identical to the full matrix).
+void launch_synth_2d(uint64_t seed, uint64_t tag, uint32_t layer, uint32_t rows, uint32_t cols_total,
+                     uint32_t row0, uint32_t col0, uint32_t ncols, float scale, void* dst, mpic_dtype dt,
+                     cudaStream_t s);
+// x[i] += add[i], xb[i] = bf16(x[i]) over n floats (head-parallel reduce-scatter result).
+void launch_resid_add(float* x, const float* add, __nv_bfloat16* xb, size_t n, cudaStream_t s);
 
 // Chunk gather + optional K rerotation + dtype cast + gap zero-fill (linker.cpp:260-314).
 void launch_assemble(const AsmChunk* d_chunks, uint32_t n_chunks, const float2* d_tables,
