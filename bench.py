@@ -39,6 +39,7 @@ CONFIGS = {
     "B": (32, 32, 128, 32000, [576], 32),
     "C": (32, 32, 128, 32000, [2304] * 4, 32),
     "D": (32, 32, 128, 32000, [2304] * 8, 32),
+    "E16": (32, 32, 128, 32000, [2304] * 16, 32),
 }
 WORKLOAD_NAMES = {
     "A": "A: tiny decoder L2 H8 D64 V4096, 2x576-token images + text, MPIC-k k=32",
@@ -46,6 +47,7 @@ WORKLOAD_NAMES = {
     "C": "C: LLaVA-1.6-7B shape L32 H32 D128 V32000, 4x2304-token images interleaved with "
          "text (32+7i prefix tokens, 32-token tail), MPIC-k k=32, AsStored",
     "D": "D: MRAG 8x2304-token retrieved images, LLaVA-1.6 shape, MPIC-k k=32",
+    "E16": "E: one long request, 16x2304-token images, LLaVA-1.6 shape, MPIC-k k=32",
 }
 
 
@@ -198,7 +200,7 @@ def run_ours(args, world, rank, local):
     ws = mp.Workspace(model, m, n)
 
     # chunk KV: pinned host fp32 (Host tier / .mpic payload) and a bf16 HBM copy (Device tier)
-    host_k, host_v, dev_chunks = [], [], []
+    host_k, host_v, host_kf, host_vf, dev_chunks = [], [], [], [], []
     g = np.random.default_rng(1234 + rank)
     for t in images:
         rk = g.random((t, h), dtype=np.float32) - 0.5  # U(-0.5, 0.5), one draw per chunk
@@ -206,21 +208,27 @@ def run_ours(args, world, rank, local):
         kv = mp.KV(L, t, H, D, mp.BF16, dev)
         kv.upload(np.broadcast_to(rk, (L, t, h)), np.broadcast_to(rv, (L, t, h)))
         dev_chunks.append(kv)
-        if not args.no_e2e:  # the Host tier copy the e2e leg streams from (pinned fp32)
-            hk, hv = mp.HostBuffer((L, t, h)), mp.HostBuffer((L, t, h))
-            hk.array[:] = rk
-            hv.array[:] = rv
+        if not args.no_e2e:  # the Host tier copies the e2e legs stream from (pinned)
+            hk, hv = mp.HostBuffer((L, t, h), np.uint16), mp.HostBuffer((L, t, h), np.uint16)
+            hk.array[:] = mp.to_bf16_bits(rk)  # model-dtype Host tier (bf16)
+            hv.array[:] = mp.to_bf16_bits(rv)
             host_k.append(hk)
             host_v.append(hv)
+            if args.e2e_fp32:  # .mpic v1 payload (fp32), reported beside it
+                fk, fv = mp.HostBuffer((L, t, h)), mp.HostBuffer((L, t, h))
+                fk.array[:] = rk
+                fv.array[:] = rv
+                host_kf.append(fk)
+                host_vf.append(fv)
     linked = mp.KV(L, n, H, D, mp.BF16, dev)
 
     def step_device():
         logits, _ = mp.request_prefill(model, ws, prompt, dev_chunks, linked, k=k, stream=stream)
         return mp.last_launch_count()
 
-    def step_host():
-        logits, _ = mp.request_prefill_host(model, ws, prompt, [x.array for x in host_k],
-                                            [x.array for x in host_v], linked, k=k,
+    def step_host(ks=None, vs=None):
+        logits, _ = mp.request_prefill_host(model, ws, prompt, [x.array for x in ks or host_k],
+                                            [x.array for x in vs or host_v], linked, k=k,
                                             stream=stream)
         return mp.last_launch_count()
 
@@ -264,32 +272,35 @@ def run_ours(args, world, rank, local):
     value = world * n * args.steps / (total_ms / 1e3)
 
     # ---- end-to-end through the host-buffer C ABI call (e2e) ----
-    e2e = None
-    if not args.no_e2e:
+    def time_host_leg(ks, vs, label):
         for _ in range(max(1, min(args.warmup, 2))):
-            step_host()
+            step_host(ks, vs)
         torch.cuda.synchronize()
         barrier(world)
-        e_steps = args.steps
         t0 = time.perf_counter()
-        ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(e_steps + 1)]
-        e2e_steps = []
+        ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         with torch.cuda.stream(stream):
             ev2[0].record(stream)
-            for i in range(e_steps):
-                launches_h = step_host()
+            for i in range(args.steps):
+                step_host(ks, vs)
                 ev2[i + 1].record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-        for i in range(e_steps):
-            e2e_steps.append(ev2[i].elapsed_time(ev2[i + 1]))
+        e2e_steps = [ev2[i].elapsed_time(ev2[i + 1]) for i in range(args.steps)]
         e_ms = allreduce_max(ev2[0].elapsed_time(ev2[-1]), world)
-        h2d = sum(x.array.nbytes for x in host_k + host_v) + 2 * 4 * m
-        e2e = {"value": world * n * e_steps / (e_ms / 1e3), "unit": "prompt tokens/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * V),
-               "ttft_p50_ms": float(statistics.median(e2e_steps)),
-               "wall_s": wall, "path": "mpic_request_prefill_host (pinned fp32 chunks -> "
-                                       "per-layer H2D on a side stream, overlapped)"}
+        h2d = sum(x.array.nbytes for x in ks + vs) + 2 * 4 * m
+        return {"value": world * n * args.steps / (e_ms / 1e3), "unit": "prompt tokens/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * V),
+                "ttft_p50_ms": float(statistics.median(e2e_steps)), "wall_s": wall,
+                "path": f"mpic_request_prefill_host ({label} chunks in pinned host memory -> "
+                        "per-layer H2D on a side stream overlapped with the layer loop; ids "
+                        "H2D, logits D2H)"}
+
+    e2e = e2e_fp32 = None
+    if not args.no_e2e:
+        e2e = time_host_leg(host_k, host_v, "bf16 Host-tier")
+        if args.e2e_fp32:
+            e2e_fp32 = time_host_leg(host_kf, host_vf, "fp32 .mpic-v1")
 
     # ---- roofline of the dominant phase ----
     hbm, tf_burst, tf_sust, peak_src = load_peaks()
@@ -346,8 +357,61 @@ def run_ours(args, world, rank, local):
         max(sum(gemm_fl.values()) / (tf_sust * 1e12), sum(gemm_b.values()) / (hbm * 1e9)) +
         attn_fl / (tf_sust * 1e12))) * 1e3
     return dict(value=value, ms_per_step=ms_per_step, per_step=per_step, host_ms=host_ms, e2e=e2e,
+                e2e_fp32=e2e_fp32,
                 launches=launches, roofline=roofline, phases=per_phase, clocks=clk.summary(),
                 n=n, m=m, floor_ms=floor_ms, world=world)
+
+
+def run_head_parallel(args, world, rank, local):
+    """One long request split by attention head over the ranks: per layer a
+    reduce-scatter of the Wo partials and an all-gather of the FFN rows over NCCL."""
+    import torch
+
+    import paper_2502_01960_b200 as mp
+    from paper_2502_01960_b200 import headpar
+
+    L, H, D, V, images, k = CONFIGS[args.config]
+    h = H * D
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream()
+    cfg = mp.config(L, H, D, vocab_size=V, image_token_count=images[0], seed=1)
+    segs = build_prompt(args.config, V, seed=42)  # the same request on every rank
+    prompt = mp.Prompt.from_segments(segs)
+    n = prompt.n
+    m_est = len(mp.select_tokens(prompt, mp.POLICY_MPIC_K, k))
+    eng = headpar.HeadParallelRank(cfg, rank, world, device=local, max_rows=m_est + world,
+                                   max_ctx=n)
+    g = np.random.default_rng(1234)
+    chunks = []
+    for t in images:
+        rk = g.random((t, h), dtype=np.float32) - 0.5
+        rv = g.random((t, h), dtype=np.float32) - 0.5
+        kv = mp.KV(L, t, H, D, mp.BF16, local)
+        kv.upload(np.broadcast_to(rk, (L, t, h)), np.broadcast_to(rv, (L, t, h)))
+        chunks.append(kv)
+    linked = eng.linked_cache(n)
+    comm = headpar.TorchComm() if world > 1 else headpar.SoloComm()
+    sh = stream.cuda_stream
+
+    def step():
+        eng.prepare(prompt, chunks, linked, mp.POLICY_MPIC_K, k, sh)
+        headpar.prefill_layers(eng, comm, L)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev[0].record(stream)
+    for i in range(args.steps):
+        step()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total = allreduce_max(ev[0].elapsed_time(ev[-1]), world)
+    return dict(value=n * args.steps / (total / 1e3), ms_per_step=total / args.steps,
+                per_step=per_step, n=n, m=eng.m, world=world)
 
 
 def cpu_reference(cfg_name, steps, warmup, threads=None, layers_sample=2, seed=42):
@@ -393,11 +457,19 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="request", choices=["request", "head-parallel"],
+                    help="request: every rank serves its own requests (request sharding); "
+                         "head-parallel: one long request split by attention head over the ranks")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-fp32", action="store_true", default=True,
+                    help="also time the e2e leg from fp32 (.mpic v1) host chunks")
+    ap.add_argument("--no-e2e-fp32", dest="e2e_fp32", action="store_false")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.config is None:
+        args.config = "E16" if args.mode == "head-parallel" else "C"
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -430,6 +502,22 @@ def main():
         return
 
     world, rank, local = dist_setup(args.gpus)
+    if args.mode == "head-parallel":
+        r = run_head_parallel(args, world, rank, local)
+        if rank == 0:
+            print(json.dumps({
+                "metric": "MPIC-k prefill tokens/s (p50 TTFT alongside)", "value": r["value"],
+                "unit": "prompt tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+                "ttft_p50_ms": float(statistics.median(r["per_step"])), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (seeded ids and hashes, U(-0.5,0.5) chunk KV, weights synthesised from seed 1)",
+                "config": dict(cfg_json, n_tokens=r["n"], recompute_rows=r["m"],
+                               parallelism=f"head-parallel x{world} (NCCL reduce-scatter + all-gather per layer)")}))
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
     r = run_ours(args, world, rank, local)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -449,7 +537,8 @@ def main():
                 "dtype": "bf16", "data": "synthetic (seeded ids and hashes, U(-0.5,0.5) chunk "
                                          "KV, weights synthesised from seed 1)",
                 "config": dict(cfg_json, n_tokens=r["n"], recompute_rows=r["m"]),
-                "e2e": r["e2e"], "gpu_launches": r["launches"], "roofline": r["roofline"],
+                "e2e": r["e2e"], "e2e_fp32_host": r["e2e_fp32"], "gpu_launches": r["launches"],
+                "roofline": r["roofline"],
                 "request_roofline_frac": round(r["floor_ms"] / r["ms_per_step"], 4),
                 "phases": r["phases"], "cpu_baseline": cpu, "clocks": r["clocks"],
                 "step_ms": [round(x, 3) for x in r["per_step"]],

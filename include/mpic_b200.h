@@ -246,6 +246,12 @@ int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpi
                               const float* const* chunk_v, const uint32_t* position_bases,
                               mpic_reposition reposition, mpic_kv_t linked, float* logits,
                               uint32_t* selected, uint32_t* m_out, void* stream);
+/* The same with the Host-tier chunks in `chunk_dtype` (MPIC_BF16: the model dtype, half the
+ * PCIe bytes of the fp32 .mpic v1 payload). */
+int mpic_request_prefill_host2(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
+                               const mpic_policy* policy, const void* const* chunk_k, const void* const* chunk_v,
+                               mpic_dtype chunk_dtype, const uint32_t* position_bases, mpic_reposition reposition,
+                               mpic_kv_t linked, float* logits, uint32_t* selected, uint32_t* m_out, void* stream);
 
 /* Host-pointer fp32 GEMM on the device: c[M][N] = a[M][K] . b[N][K]^T (SIMT FFMA). Backs the
  * reference's gemm_nt/gemm_nn shims (proj/include/mpic/matmul.h:11-21). Synchronous. */

@@ -21,7 +21,7 @@ __all__ = ["ModelConfig", "Model", "KV", "Workspace", "Prompt", "MpicError", "Ex
            "F32", "BF16", "AS_STORED", "REROTATE", "POLICY_MPIC_K", "POLICY_TEXT_ONLY",
            "POLICY_ALL", "POLICY_PREFIX_ONLY", "config", "fingerprint", "image_token_ids",
            "select_tokens", "flatten_ids", "assemble", "selective_prefill", "prefill_extend",
-           "request_prefill", "request_prefill_host", "last_launch_count", "HostBuffer"]
+           "request_prefill", "request_prefill_host", "last_launch_count", "HostBuffer", "to_bf16_bits"]
 
 F32, BF16 = 0, 1
 AS_STORED, REROTATE = 0, 1
@@ -279,9 +279,12 @@ def request_prefill_host(model: Model, ws: Workspace, prompt: Prompt, chunk_k, c
                          linked: KV, policy: int = POLICY_MPIC_K, k: int = 32,
                          global_budget: bool = False, reposition: int = AS_STORED,
                          position_bases=None, stream=None, logits_out=None):
-    """Same request with chunk KV in host memory (numpy fp32 [L][len][h], ideally pinned
-    HostBuffer arrays): the loader streams them layer by layer to HBM."""
+    """Same request with chunk KV in host memory ([L][len][h] arrays, ideally pinned
+    HostBuffers): the loader streams them layer by layer to HBM. fp32 arrays are the .mpic
+    v1 payload; bf16 chunks (numpy uint16 bit patterns, HostBuffer(..., np.uint16)) are the
+    model-dtype Host tier with half the PCIe bytes."""
     n_img = len(chunk_k)
+    dt = BF16 if n_img and chunk_k[0].dtype == np.uint16 else F32
     kp = (C.c_void_p * max(n_img, 1))(*[a.ctypes.data for a in chunk_k])
     vp = (C.c_void_p * max(n_img, 1))(*[a.ctypes.data for a in chunk_v])
     pb = np.ascontiguousarray(position_bases if position_bases is not None else np.zeros(n_img),
@@ -290,11 +293,17 @@ def request_prefill_host(model: Model, ws: Workspace, prompt: Prompt, chunk_k, c
     sel = np.zeros(prompt.n, np.uint32)
     m = C.c_uint32()
     pol = PolicyDesc(policy, k, int(global_budget))
-    check(lib().mpic_request_prefill_host(model.handle, ws.handle, C.byref(prompt.desc()),
-                                          C.byref(pol), kp, vp, pb.ctypes.data, reposition,
-                                          linked.handle, logits.ctypes.data, sel.ctypes.data,
-                                          C.byref(m), _stream_ptr(stream)))
+    check(lib().mpic_request_prefill_host2(model.handle, ws.handle, C.byref(prompt.desc()),
+                                           C.byref(pol), kp, vp, dt, pb.ctypes.data, reposition,
+                                           linked.handle, logits.ctypes.data, sel.ctypes.data,
+                                           C.byref(m), _stream_ptr(stream)))
     return logits, sel[:m.value].copy()
+
+
+def to_bf16_bits(a: np.ndarray) -> np.ndarray:
+    """fp32 -> bf16 (round to nearest even) as uint16 bit patterns."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
 
 
 PHASES = ["assemble", "embed", "qkv", "attn", "wo", "w1", "w2", "cast", "lm_head"]

@@ -1604,26 +1604,26 @@ int mpic_workspace_set_graphs(mpic_workspace_t ws, int on) {
     API_END
 }
 
-int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
-                              const mpic_policy* policy, const float* const* chunk_k,
-                              const float* const* chunk_v, const uint32_t* position_bases,
-                              mpic_reposition reposition, mpic_kv_t linked, float* logits,
-                              uint32_t* selected, uint32_t* m_out, void* stream) {
+int mpic_request_prefill_host2(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
+                               const mpic_policy* policy, const void* const* chunk_k, const void* const* chunk_v,
+                               mpic_dtype chunk_dtype, const uint32_t* position_bases, mpic_reposition reposition,
+                               mpic_kv_t linked, float* logits, uint32_t* selected, uint32_t* m_out, void* stream) {
     API_BEGIN
+    const size_t es = esz(chunk_dtype);
     MPIC_CUDA(cudaSetDevice(model->device));
     cudaStream_t s = (cudaStream_t)stream;
     const RequestPlan r = plan_request(model, prompt, policy, position_bases);
     check_linked(model, linked, r.n);
     const uint32_t n_img = (uint32_t)r.refs.size();
     const size_t h = model->cfg.hidden_dim;
-    // Staging slot = one layer of every chunk, fp32, K then V.
+    // Staging slot = one layer of every chunk in the Host tier's dtype, K then V.
     std::vector<size_t> off(n_img);
     size_t img_rows = 0;
     for (uint32_t i = 0; i < n_img; ++i) {
         off[i] = img_rows * h;
         img_rows += r.refs[i].rows;
     }
-    const size_t slot_bytes = std::max<size_t>(1, img_rows) * h * 4 * 2;
+    const size_t slot_bytes = std::max<size_t>(1, img_rows) * h * es * 2;
     if (ws->stage_cap < slot_bytes) {
         MPIC_CUDA(cudaStreamSynchronize(ws->copy_stream));
         for (int i = 0; i < 2; ++i) {
@@ -1642,10 +1642,10 @@ int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpi
     uint32_t n_tab = 0;
     for (int sl = 0; sl < 2; ++sl) {
         std::vector<const void*> ks(n_img), vs(n_img);
-        float* base = static_cast<float*>(ws->stage[sl]);
+        char* base = static_cast<char*>(ws->stage[sl]);
         for (uint32_t i = 0; i < n_img; ++i) {
-            ks[i] = base + off[i];
-            vs[i] = base + img_rows * h + off[i];
+            ks[i] = base + off[i] * es;
+            vs[i] = base + (img_rows * h + off[i]) * es;
         }
         const AsmPlan p = plan_assembly(ks.data(), vs.data(), ts.data(), r.refs.data(), n_img,
                                         linked->T, linked->D, reposition, model->cfg.rope_base, linked->H * linked->D);
@@ -1661,14 +1661,15 @@ int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpi
     MPIC_CUDA(cudaEventRecord(ws->ev_free[1], s));
     auto issue_copy = [&](uint32_t l) {
         const int sl = l & 1;
-        float* base = static_cast<float*>(ws->stage[sl]);
+        char* base = static_cast<char*>(ws->stage[sl]);
         MPIC_CUDA(cudaStreamWaitEvent(cs, ws->ev_free[sl], 0));
         for (uint32_t i = 0; i < n_img; ++i) {
             const size_t cnt = (size_t)r.refs[i].rows * h;
-            MPIC_CUDA(cudaMemcpyAsync(base + off[i], chunk_k[i] + (size_t)l * cnt, cnt * 4,
+            MPIC_CUDA(cudaMemcpyAsync(base + off[i] * es, static_cast<const char*>(chunk_k[i]) + (size_t)l * cnt * es,
+                                      cnt * es, cudaMemcpyHostToDevice, cs));
+            MPIC_CUDA(cudaMemcpyAsync(base + (img_rows * h + off[i]) * es,
+                                      static_cast<const char*>(chunk_v[i]) + (size_t)l * cnt * es, cnt * es,
                                       cudaMemcpyHostToDevice, cs));
-            MPIC_CUDA(cudaMemcpyAsync(base + img_rows * h + off[i], chunk_v[i] + (size_t)l * cnt,
-                                      cnt * 4, cudaMemcpyHostToDevice, cs));
         }
         MPIC_CUDA(cudaEventRecord(ws->ev_ready[sl], cs));
     };
@@ -1679,7 +1680,7 @@ int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpi
         const int sl = l & 1;
         MPIC_CUDA(cudaStreamWaitEvent(s, ws->ev_ready[sl], 0));
         ProfScope ps(s, MPIC_PHASE_ASSEMBLE);
-        launch_assemble(dc[sl], n_img, dt[sl], n_tab, MPIC_F32, (char*)linked->k + l * plane,
+        launch_assemble(dc[sl], n_img, dt[sl], n_tab, chunk_dtype, (char*)linked->k + l * plane,
                         (char*)linked->v + l * plane, linked->dtype, 1, linked->T, linked->H,
                         linked->D, 1, s);
         MPIC_CUDA(cudaEventRecord(ws->ev_free[sl], s));
@@ -1687,6 +1688,16 @@ int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpi
     run_request(model, ws, r, linked, logits, selected, m_out, s, before_layer);
     for (int sl = 0; sl < 2; ++sl) MPIC_CUDA(cudaFreeAsync(bufs[sl], s));
     API_END
+}
+
+int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
+                              const mpic_policy* policy, const float* const* chunk_k,
+                              const float* const* chunk_v, const uint32_t* position_bases,
+                              mpic_reposition reposition, mpic_kv_t linked, float* logits,
+                              uint32_t* selected, uint32_t* m_out, void* stream) {
+    return mpic_request_prefill_host2(model, ws, prompt, policy, reinterpret_cast<const void* const*>(chunk_k),
+                                      reinterpret_cast<const void* const*>(chunk_v), MPIC_F32, position_bases,
+                                      reposition, linked, logits, selected, m_out, stream);
 }
 
 int mpic_test_gemm(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uint32_t K,

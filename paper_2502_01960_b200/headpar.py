@@ -67,6 +67,17 @@ class TorchComm:
                 full[r * mr:(r + 1) * mr].copy_(parts[r])
 
 
+class SoloComm:
+    """world_size 1: the collectives are identities."""
+    rank, world = 0, 1
+
+    def reduce_scatter(self, partial, out):
+        out.copy_(partial[:out.shape[0]])
+
+    def all_gather_rows(self, full, mr):
+        pass
+
+
 class _DevArray:
     """__cuda_array_interface__ view of a raw device pointer (torch.as_tensor aliases it)."""
 

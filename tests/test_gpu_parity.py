@@ -300,3 +300,34 @@ def test_reference_suites_on_b200_library(suite):
     import subprocess
     r = subprocess.run([os.path.join(CONF_DIR, suite)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+
+
+def test_request_prefill_host_bf16_tier(g):
+    """The model-dtype Host tier: bf16 chunk bits in pinned memory streamed by the loader give
+    exactly the logits and cache of the same chunks resident in HBM (both are RNE(fp32))."""
+    L, H, D = 2, 8, 128
+    cfg = mp.config(L, H, D, vocab_size=4096, image_token_count=192, seed=9)
+    m = mp.Model(cfg, mp.BF16)
+    rng = np.random.default_rng(3)
+    segs = [("text", rng.integers(0, 4095, 21).tolist()), ("image", rng.bytes(32), 192),
+            ("text", rng.integers(0, 4095, 30).tolist()), ("image", rng.bytes(32), 192),
+            ("text", rng.integers(0, 4095, 9).tolist())]
+    p = mp.Prompt.from_segments(segs)
+    chunks = [(rng.random((L, 192, H * D), dtype=np.float32) - 0.5,
+               rng.random((L, 192, H * D), dtype=np.float32) - 0.5) for _ in range(2)]
+    ws = mp.Workspace(m, 128, p.n)
+    dev = [mp.KV.from_host(k, v, H, D, mp.BF16) for k, v in chunks]
+    linked_d = mp.KV(L, p.n, H, D, mp.BF16)
+    ref_logits, ref_sel = mp.request_prefill(m, ws, p, dev, linked_d, k=32)
+    pins = []
+    for k, v in chunks:
+        hk, hv = mp.HostBuffer(k.shape, np.uint16), mp.HostBuffer(v.shape, np.uint16)
+        hk.array[...] = mp.to_bf16_bits(k)
+        hv.array[...] = mp.to_bf16_bits(v)
+        pins += [hk, hv]
+    linked_h = mp.KV(L, p.n, H, D, mp.BF16)
+    logits, sel = mp.request_prefill_host(m, ws, p, [x.array for x in pins[0::2]],
+                                          [x.array for x in pins[1::2]], linked_h, k=32)
+    assert np.array_equal(sel, ref_sel)
+    assert np.array_equal(logits, ref_logits)
+    assert all(np.array_equal(a, b) for a, b in zip(linked_h.download(), linked_d.download()))
