@@ -10,6 +10,8 @@
 // shared memory; the rotation itself is the reference's unfused float expression, so
 // the result is bit-identical. AsStored is a pure copy: bit-exact. Rows no chunk covers
 // are zero-filled (the reference's zero-initialised Dummy slots, tensor.h:20-23).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -71,7 +73,8 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmChunk* __restric
                                                        const float2* __restrict__ tables,
                                                        uint32_t n_tables, TD* __restrict__ dk,
                                                        TD* __restrict__ dv, uint32_t L, uint32_t T,
-                                                       uint32_t H, uint32_t D, int zero_gaps) {
+                                                       uint32_t H, uint32_t D, int zero_gaps,
+                                                       uint32_t src_l0) {
     extern __shared__ float2 s_tab[];
     __shared__ AsmChunk s_chunks[kMaxAsmChunks];
     const uint32_t half_d = D >> 1, h = H * D, nvec = h / VEC;
@@ -102,7 +105,8 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmChunk* __restric
             continue;
         }
         const AsmChunk ch = s_chunks[c];
-        const size_t soff = ((size_t)l * ch.src_tokens + ch.src_row0 + (r - ch.dst_row0)) * ch.src_ld + ch.src_col0;
+        const size_t soff = ((size_t)(src_l0 + l) * ch.src_tokens + ch.src_row0 + (r - ch.dst_row0)) * ch.src_ld +
+                            ch.src_col0;
         const TS* ks = static_cast<const TS*>(ch.src_k) + soff;
         const TS* vs = static_cast<const TS*>(ch.src_v) + soff;
         const float2* tab = s_tab + (size_t)ch.table * half_d;
@@ -140,19 +144,23 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmChunk* __restric
 template <typename TS, typename TD>
 static void launch_asm_typed(const AsmChunk* d_chunks, uint32_t n_chunks, const float2* d_tables,
                              uint32_t n_tables, TD* dk, TD* dv, uint32_t L, uint32_t T, uint32_t H,
-                             uint32_t D, int zero_gaps, cudaStream_t s) {
+                             uint32_t D, int zero_gaps, uint32_t src_l0, cudaStream_t s) {
     const uint32_t h = H * D;
     const uint64_t units = (uint64_t)L * T;
     const size_t smem = (size_t)n_tables * (D / 2) * sizeof(float2);
-    const uint32_t grid = (uint32_t)std::min<uint64_t>(units, (uint64_t)kNumSMs * 8);
+    static const uint32_t per_sm = [] {
+        const char* e = getenv("MPIC_ASM_CTAS_PER_SM");  // diagnostics
+        return e ? (uint32_t)atoi(e) : 8u;
+    }();
+    const uint32_t grid = (uint32_t)std::min<uint64_t>(units, (uint64_t)kNumSMs * per_sm);
     if (h % 8 == 0) {
         auto k = assemble_kernel<TS, TD, 8>;
         if (smem > 48 * 1024) MPIC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k<<<grid, 256, smem, s>>>(d_chunks, n_chunks, d_tables, n_tables, dk, dv, L, T, H, D, zero_gaps);
+        k<<<grid, 256, smem, s>>>(d_chunks, n_chunks, d_tables, n_tables, dk, dv, L, T, H, D, zero_gaps, src_l0);
     } else {
         auto k = assemble_kernel<TS, TD, 2>;
         if (smem > 48 * 1024) MPIC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k<<<grid, 256, smem, s>>>(d_chunks, n_chunks, d_tables, n_tables, dk, dv, L, T, H, D, zero_gaps);
+        k<<<grid, 256, smem, s>>>(d_chunks, n_chunks, d_tables, n_tables, dk, dv, L, T, H, D, zero_gaps, src_l0);
     }
     MPIC_LAUNCHED();
 }
@@ -160,17 +168,17 @@ static void launch_asm_typed(const AsmChunk* d_chunks, uint32_t n_chunks, const 
 void launch_assemble(const AsmChunk* d_chunks, uint32_t n_chunks, const float2* d_tables,
                      uint32_t n_tables, mpic_dtype src_t, void* dst_k, void* dst_v,
                      mpic_dtype dst_t, uint32_t L, uint32_t T_dst, uint32_t H, uint32_t D,
-                     int zero_gaps, cudaStream_t s) {
+                     int zero_gaps, cudaStream_t s, uint32_t src_l0) {
     MPIC_REQUIRE(n_chunks <= kMaxAsmChunks, MPIC_ERR_VALIDATION, "too many chunks in one assembly");
     using bf = __nv_bfloat16;
     if (src_t == MPIC_F32 && dst_t == MPIC_F32)
-        launch_asm_typed<float, float>(d_chunks, n_chunks, d_tables, n_tables, (float*)dst_k, (float*)dst_v, L, T_dst, H, D, zero_gaps, s);
+        launch_asm_typed<float, float>(d_chunks, n_chunks, d_tables, n_tables, (float*)dst_k, (float*)dst_v, L, T_dst, H, D, zero_gaps, src_l0, s);
     else if (src_t == MPIC_F32 && dst_t == MPIC_BF16)
-        launch_asm_typed<float, bf>(d_chunks, n_chunks, d_tables, n_tables, (bf*)dst_k, (bf*)dst_v, L, T_dst, H, D, zero_gaps, s);
+        launch_asm_typed<float, bf>(d_chunks, n_chunks, d_tables, n_tables, (bf*)dst_k, (bf*)dst_v, L, T_dst, H, D, zero_gaps, src_l0, s);
     else if (src_t == MPIC_BF16 && dst_t == MPIC_BF16)
-        launch_asm_typed<bf, bf>(d_chunks, n_chunks, d_tables, n_tables, (bf*)dst_k, (bf*)dst_v, L, T_dst, H, D, zero_gaps, s);
+        launch_asm_typed<bf, bf>(d_chunks, n_chunks, d_tables, n_tables, (bf*)dst_k, (bf*)dst_v, L, T_dst, H, D, zero_gaps, src_l0, s);
     else
-        launch_asm_typed<bf, float>(d_chunks, n_chunks, d_tables, n_tables, (float*)dst_k, (float*)dst_v, L, T_dst, H, D, zero_gaps, s);
+        launch_asm_typed<bf, float>(d_chunks, n_chunks, d_tables, n_tables, (float*)dst_k, (float*)dst_v, L, T_dst, H, D, zero_gaps, src_l0, s);
 }
 
 // ---- weight synthesis (proj/include/mpic/rng.h:10-30, proj/src/model.cpp:28-36) -------

@@ -155,6 +155,10 @@ struct mpic_workspace_s {
     cudaGraphExec_t graph = nullptr;
     uint32_t graph_kernels = 0;
     uint32_t hp_m = 0, hp_n = 0;  // head-parallel request in flight (mpic_hp_prepare)
+    // per-layer assembly overlapped with the layer loop (mpic_request_prefill)
+    cudaStream_t asm_stream = nullptr;
+    cudaEvent_t ev_asm_in = nullptr;
+    std::vector<cudaEvent_t> ev_asm;
 };
 
 #define API_BEGIN \
@@ -396,6 +400,18 @@ void enqueue_attn_plan(mpic_workspace_t ws, cudaStream_t s) {
     if (cs != cudaStreamCaptureStatusNone) return;  // graph requests end in a stream sync
     if (!ws->ev_plan) MPIC_CUDA(cudaEventCreateWithFlags(&ws->ev_plan, cudaEventDisableTiming));
     MPIC_CUDA(cudaEventRecord(ws->ev_plan, s));
+}
+
+void ensure_asm_stream(mpic_workspace_t ws, uint32_t layers) {
+    if (!ws->asm_stream) {
+        MPIC_CUDA(cudaStreamCreateWithFlags(&ws->asm_stream, cudaStreamNonBlocking));
+        MPIC_CUDA(cudaEventCreateWithFlags(&ws->ev_asm_in, cudaEventDisableTiming));
+    }
+    while (ws->ev_asm.size() < layers) {
+        cudaEvent_t e;
+        MPIC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ws->ev_asm.push_back(e);
+    }
 }
 
 // selective_core / extend_rows on the device (linker.cpp:35-135, model.cpp:211-330).
@@ -1124,6 +1140,9 @@ int mpic_workspace_destroy(mpic_workspace_t ws) {
         cudaFree(ws->d_asm);
         if (ws->ev_plan) cudaEventDestroy(ws->ev_plan);
         if (ws->graph) cudaGraphExecDestroy(ws->graph);
+        for (cudaEvent_t e : ws->ev_asm) cudaEventDestroy(e);
+        if (ws->ev_asm_in) cudaEventDestroy(ws->ev_asm_in);
+        if (ws->asm_stream) cudaStreamDestroy(ws->asm_stream);
         delete ws;
     }
     API_END
@@ -1292,17 +1311,40 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
         std::memcpy((char*)ws->h_asm + bytes_c, ap.tables.data(), ap.tables.size() * sizeof(float2));
 
     // ---- device work: one stream-ordered sequence, optionally recorded as a CUDA graph ----
+    static const bool asm_overlap = [] {
+        const char* e = getenv("MPIC_ASM_OVERLAP");  // diagnostics: 0 = assemble all layers up front
+        return !e || atoi(e) != 0;
+    }();
     auto enqueue = [&] {
         MPIC_CUDA(cudaMemcpyAsync(ws->d_ids, ws->h_ids, r.m * 4, cudaMemcpyHostToDevice, s));
         MPIC_CUDA(cudaMemcpyAsync(ws->d_rows, ws->h_rows, r.m * 4, cudaMemcpyHostToDevice, s));
         MPIC_CUDA(cudaMemcpyAsync(ws->d_asm, ws->h_asm, bytes_c + bytes_t, cudaMemcpyHostToDevice, s));
-        {
+        const AsmChunk* dch = static_cast<const AsmChunk*>(ws->d_asm);
+        const float2* dtab = reinterpret_cast<const float2*>((char*)ws->d_asm + bytes_c);
+        std::function<void(uint32_t)> wait_layer;
+        if (asm_overlap) {
+            // Layer l of the assembly runs on a side stream and only layer l's QKV waits for it:
+            // the HBM-bound copy of layers l+1.. overlaps the tensor-bound GEMMs of layer l.
+            ensure_asm_stream(ws, model->cfg.n_layers);
+            const size_t plane = (size_t)linked->T * linked->H * linked->D * esz(linked->dtype);
+            MPIC_CUDA(cudaEventRecord(ws->ev_asm_in, s));
+            MPIC_CUDA(cudaStreamWaitEvent(ws->asm_stream, ws->ev_asm_in, 0));
+            for (uint32_t l = 0; l < linked->L; ++l) {
+                {
+                    ProfScope ps(ws->asm_stream, MPIC_PHASE_ASSEMBLE);
+                    launch_assemble(dch, n_img, dtab, ap.n_tables, src_t, (char*)linked->k + l * plane,
+                                    (char*)linked->v + l * plane, linked->dtype, 1, linked->T, linked->H, linked->D, 1,
+                                    ws->asm_stream, l);
+                }
+                MPIC_CUDA(cudaEventRecord(ws->ev_asm[l], ws->asm_stream));
+            }
+            wait_layer = [&](uint32_t l) { MPIC_CUDA(cudaStreamWaitEvent(s, ws->ev_asm[l], 0)); };
+        } else {
             ProfScope ps(s, MPIC_PHASE_ASSEMBLE);
-            launch_assemble(static_cast<const AsmChunk*>(ws->d_asm), n_img,
-                            reinterpret_cast<const float2*>((char*)ws->d_asm + bytes_c), ap.n_tables, src_t,
-                            linked->k, linked->v, linked->dtype, linked->L, linked->T, linked->H, linked->D, 1, s);
+            launch_assemble(dch, n_img, dtab, ap.n_tables, src_t, linked->k, linked->v, linked->dtype, linked->L,
+                            linked->T, linked->H, linked->D, 1, s);
         }
-        forward_rows(model, ws, ws->d_ids, ws->d_rows, ws->d_rows, r.m, r.n - 1, linked, ws->d_logits, s, {},
+        forward_rows(model, ws, ws->d_ids, ws->d_rows, ws->d_rows, r.m, r.n - 1, linked, ws->d_logits, s, wait_layer,
                      r.sel.data(), nullptr, /*plan_ready=*/true);
         MPIC_CUDA(cudaMemcpyAsync(ws->h_logits, ws->d_logits, model->cfg.vocab_size * 4, cudaMemcpyDeviceToHost, s));
     };

@@ -94,7 +94,7 @@ void launch_resid_add(float* x, const float* add, __nv_bfloat16* xb, size_t n, c
 void launch_assemble(const AsmChunk* d_chunks, uint32_t n_chunks, const float2* d_tables,
                      uint32_t n_tables, mpic_dtype src_t, void* dst_k, void* dst_v,
                      mpic_dtype dst_t, uint32_t L, uint32_t T_dst, uint32_t H, uint32_t D,
-                     int zero_gaps, cudaStream_t s);
+                     int zero_gaps, cudaStream_t s, uint32_t src_l0 = 0);
 
 // Attention work plan (tc_attn.cu): an item is up to two query tiles of one head that
 // stream the same key blocks [b0, max(b1)) — tile[1] == kNoTile when the item has one.
