@@ -17,6 +17,13 @@ thread_local std::string g_last_error;
 thread_local uint32_t g_launches = 0;
 }  // namespace
 void note_launch(uint32_t n) { g_launches += n; }
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("MPIC_PDL");
+        return !e || atoi(e) != 0;
+    }();
+    return on;
+}
 
 // ---- per-phase device timing (CUDA events on the launching stream) ------------------
 // Enabled by mpic_profile_enable(1); each phase of a forward/assembly records a start and

@@ -79,4 +79,7 @@ __device__ __forceinline__ float gelu_ref(float x) {
 
 inline uint32_t ceil_div(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
 
+// Programmatic dependent launch of the layer-loop kernels (MPIC_PDL=0 disables it).
+bool pdl_enabled();
+
 } // namespace mpicb

@@ -122,12 +122,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     uint64_t* o_done = p_full + 2;               // [2 tiles]
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_done + 2);
 
-    const AttnUnit u = p.units[blockIdx.x];
+    tc::pdl_trigger();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool has_b = u.tile[1] != kNoTile;
-    const uint32_t nb0 = u.b1[0] - u.b0, nb1 = has_b ? u.b1[1] - u.b0 : 0;
-    const uint32_t nbmax = max(nb0, nb1);
-    const int hcol = (int)(u.head * 128u);
 
     if (warp == 0 && lane == 0) {
         tc::tma_prefetch_desc(&tmQ);
@@ -153,7 +149,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
+    tc::pdl_wait();  // q and the layer's K/V come from the previous kernel
     const uint32_t tmem = *tmem_holder;
+    const AttnUnit u = p.units[blockIdx.x];
+    const bool has_b = u.tile[1] != kNoTile;
+    const uint32_t nb0 = u.b1[0] - u.b0, nb1 = has_b ? u.b1[1] - u.b0 : 0;
+    const uint32_t nbmax = max(nb0, nb1);
+    const int hcol = (int)(u.head * 128u);
     // TMEM columns: tile X uses S_X [256X, 256X+128) and O_X [256X+128, 256X+256).
     // P_X(j) (bf16, two keys per column) overwrites the first 64 columns of S_X in place.
     constexpr uint32_t idesc_s = tc::idesc_bf16(128, 128, false);
@@ -400,6 +402,8 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnCombine* __
                                                            uint32_t m, uint32_t h,
                                                            __nv_bfloat16* __restrict__ out) {
     constexpr uint32_t kMaxSplits = 16;
+    tc::pdl_trigger();
+    tc::pdl_wait();
     const AttnCombine j = jobs[blockIdx.x];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t r = blockIdx.y * 8 + warp;
@@ -541,10 +545,24 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
         MPIC_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    attn_tc_kernel<<<n_units, kAttnThreads, smem, s>>>(tmQ, tmK, tmV, p);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n_units);
+    cfg.blockDim = dim3(kAttnThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MPIC_CUDA(cudaLaunchKernelEx(&cfg, attn_tc_kernel, tmQ, tmK, tmV, p));
     MPIC_LAUNCHED();
     if (n_combine) {
-        attn_combine_kernel<<<dim3(n_combine, 16), 256, 0, s>>>(d_combine, part_o, part_ml, m, h, out);
+        cfg.gridDim = dim3(n_combine, 16);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = 0;
+        MPIC_CUDA(cudaLaunchKernelEx(&cfg, attn_combine_kernel, d_combine, (const float*)part_o,
+                                     (const float2*)part_ml, m, h, out));
         MPIC_LAUNCHED();
     }
 }

@@ -317,6 +317,12 @@ __device__ __forceinline__ void fence_async_shared() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Programmatic dependent launch: let the next kernel of the stream start launching (its
+// prologue overlaps this kernel's tail), and wait for the previous kernel's completion and
+// memory before touching anything it produced.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Warpgroup register re-allocation (all 4 warps of a warpgroup must execute it).
 template <uint32_t N>
 __device__ __forceinline__ void reg_alloc() {

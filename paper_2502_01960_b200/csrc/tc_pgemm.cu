@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(kPgThreads, 1)
     uint64_t* epi_bar = acc_empty + 2;      // epilogue side-input staging (bulk copies)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(epi_bar + 1);
 
+    tc::pdl_trigger();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t crank = tc::cluster_ctarank();
     const uint32_t rank = crank & 1;          // CTA within the pair
@@ -238,10 +239,19 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         tc::mbar_init(epi_bar, 1);
         tc::fence_barrier_init();
     }
+    if (warp == 0 && lane == 0 && cl < a.tiles) {
+        // weights do not depend on the previous kernel: start pulling this CTA's first
+        // k-blocks into L2 before waiting for it
+        const uint32_t fb = cl / a.ngroups, w_row = fb * 256 + (crank & 1) * 128;
+        for (uint32_t kb = kb0; kb < min(kb1, kb0 + 2 * a.stages * a.kps); ++kb)
+            tc::tma_prefetch_2d(&tmW, a.w_blocked ? 0 : (int)(kb * 64),
+                                a.w_blocked ? (int)(((2 * fb + (crank & 1)) * a.kblocks + kb) * 128) : (int)w_row);
+    }
     if (warp == 1) tc::tmem_alloc_pair(tmem_holder, a.tmem_cols);
     tc::tc_fence_before();
     tc::cluster_sync();
     tc::tc_fence_after();
+    tc::pdl_wait();  // the previous kernel's outputs (this GEMM's X, its output buffers) are ready
     const uint32_t tmem = *tmem_holder;
 
     if (warp == 0) {
@@ -581,13 +591,15 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
     cfg.blockDim = dim3(kPgThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2 * a.S;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     MPIC_CUDA(cudaLaunchKernelEx(&cfg, tc_pgemm_kernel, tmW, tmX0, tmX1, a));
     MPIC_LAUNCHED();
 }
