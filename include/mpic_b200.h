@@ -213,6 +213,16 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
  * full PCIe rate): the loader streams layer l of every chunk to HBM on a side stream while
  * layer l-1 is being recomputed; each landed layer is assembled (and cast to the model
  * dtype) right before it is used. */
+/* The same request with each image's chunk read from a .mpic file (v1 fp32 or v2 bf16
+ * payload; paths[i] for the i-th image segment): a reader thread preads layer l of every
+ * chunk into a pinned ring slot while the GPU computes layer l-1, the copy stream moves the
+ * slot to HBM in one transfer, and the file CRCs (combined from per-segment CRCs) are
+ * verified at the end: MPIC_ERR_INTEGRITY means the result is void and the chunk must be
+ * recomputed (prepare's fallback). position_base comes from each file's header. */
+int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
+                               const mpic_policy* policy, const char* const* paths, mpic_reposition reposition,
+                               mpic_kv_t linked, float* logits, uint32_t* selected, uint32_t* m_out, void* stream);
+
 /* ---- head-parallel request (one long request over P GPUs) ---------------
  * Rank r owns heads [head0, head0 + n_local_heads): its model holds those heads' Wq/Wk/Wv
  * rows and Wo columns (bit-identical slices of build_model's weights) and the full FFN; its

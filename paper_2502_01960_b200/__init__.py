@@ -10,6 +10,7 @@ is missing the call raises ``ExtensionMissing`` (there is no CPU fallback).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -21,7 +22,7 @@ __all__ = ["ModelConfig", "Model", "KV", "Workspace", "Prompt", "MpicError", "Ex
            "F32", "BF16", "AS_STORED", "REROTATE", "POLICY_MPIC_K", "POLICY_TEXT_ONLY",
            "POLICY_ALL", "POLICY_PREFIX_ONLY", "config", "fingerprint", "image_token_ids",
            "select_tokens", "flatten_ids", "assemble", "selective_prefill", "prefill_extend",
-           "request_prefill", "request_prefill_host", "last_launch_count", "HostBuffer", "to_bf16_bits"]
+           "request_prefill", "request_prefill_host", "last_launch_count", "HostBuffer", "to_bf16_bits", "request_prefill_files", "write_mpic"]
 
 F32, BF16 = 0, 1
 AS_STORED, REROTATE = 0, 1
@@ -298,6 +299,50 @@ def request_prefill_host(model: Model, ws: Workspace, prompt: Prompt, chunk_k, c
                                            linked.handle, logits.ctypes.data, sel.ctypes.data,
                                            C.byref(m), _stream_ptr(stream)))
     return logits, sel[:m.value].copy()
+
+
+def request_prefill_files(model: Model, ws: Workspace, prompt: Prompt, paths, linked: KV,
+                          policy: int = POLICY_MPIC_K, k: int = 32, global_budget: bool = False,
+                          reposition: int = AS_STORED, stream=None):
+    """Same request with every image chunk read from its .mpic file by the disk loader
+    (mpic_request_prefill_files): disk -> pinned ring -> HBM per layer, CRC-checked."""
+    n_img = len(paths)
+    enc = [os.fsencode(p) for p in paths]
+    arr = (C.c_char_p * max(n_img, 1))(*enc)
+    logits = np.zeros(model.cfg.vocab_size, np.float32)
+    sel = np.zeros(prompt.n, np.uint32)
+    m = C.c_uint32()
+    pol = PolicyDesc(policy, k, int(global_budget))
+    check(lib().mpic_request_prefill_files(model.handle, ws.handle, C.byref(prompt.desc()), C.byref(pol),
+                                           C.cast(arr, C.c_void_p), reposition, linked.handle,
+                                           logits.ctypes.data, sel.ctypes.data, C.byref(m),
+                                           _stream_ptr(stream)))
+    return logits, sel[:m.value].copy()
+
+
+def write_mpic(path, cfg: ModelConfig, content_hash: bytes, k: np.ndarray, v: np.ndarray,
+               position_base: int = 0, ns: str = "", bf16: bool = False):
+    """Write one chunk as a .mpic container (proj/src/cache.cpp:97-125): v1 with an fp32
+    payload, or v2 with a bf16 payload (uint16 bit patterns), CRC32 of all preceding bytes."""
+    import struct
+    import zlib
+    L, T, h = k.shape
+    D = cfg.head_dim
+    fnv = 0xcbf29ce484222325
+    for b in ns.encode():
+        fnv = ((fnv ^ b) * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    header = (b"MPIC" + struct.pack("<IQQ", 2 if bf16 else 1, fingerprint(cfg), fnv) + bytes(content_hash)
+              + struct.pack("<IIIII", position_base, L, T, h // D, D) + bytes([1 if bf16 else 0]) + bytes(7))
+    crc = zlib.crc32(header)
+    with open(path, "wb") as f:
+        f.write(header)
+        for a in (k, v):
+            payload = to_bf16_bits(a) if bf16 else np.ascontiguousarray(a, np.float32)
+            for l in range(L):  # layer by layer keeps the host copy small
+                buf = payload[l].tobytes()
+                crc = zlib.crc32(buf, crc)
+                f.write(buf)
+        f.write(struct.pack("<I", crc & 0xFFFFFFFF))
 
 
 def to_bf16_bits(a: np.ndarray) -> np.ndarray:

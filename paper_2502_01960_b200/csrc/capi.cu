@@ -1,7 +1,15 @@
 // C ABI of the MPIC B200 path (include/mpic_b200.h): handles, the per-layer launch
 // sequence of the selective recompute, and the assembly entry points.
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+#include <zlib.h>
+
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <memory>
+#include <thread>
 #include <mutex>
 #include <functional>
 #include <mutex>
@@ -140,6 +148,10 @@ struct mpic_workspace_s {
     cudaEvent_t ev_free[2] = {nullptr, nullptr};
     void* stage[2] = {nullptr, nullptr};
     size_t stage_cap = 0;
+    // disk loader (mpic_request_prefill_files): pinned ring of layer slots
+    void* pin[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev_pin[3] = {nullptr, nullptr, nullptr};
+    size_t pin_cap = 0;
     // tcgen05 attention plan (per request) and split partials
     AttnUnit* d_units = nullptr;
     AttnCombine* d_comb = nullptr;
@@ -1147,6 +1159,10 @@ int mpic_workspace_destroy(mpic_workspace_t ws) {
         cudaFree(ws->d_asm);
         if (ws->ev_plan) cudaEventDestroy(ws->ev_plan);
         if (ws->graph) cudaGraphExecDestroy(ws->graph);
+        for (int i = 0; i < 3; ++i) {
+            cudaFreeHost(ws->pin[i]);
+            if (ws->ev_pin[i]) cudaEventDestroy(ws->ev_pin[i]);
+        }
         for (cudaEvent_t e : ws->ev_asm) cudaEventDestroy(e);
         if (ws->ev_asm_in) cudaEventDestroy(ws->ev_asm_in);
         if (ws->asm_stream) cudaStreamDestroy(ws->asm_stream);
@@ -1747,6 +1763,254 @@ int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpi
     return mpic_request_prefill_host2(model, ws, prompt, policy, reinterpret_cast<const void* const*>(chunk_k),
                                       reinterpret_cast<const void* const*>(chunk_v), MPIC_F32, position_bases,
                                       reposition, linked, logits, selected, m_out, stream);
+}
+
+// ---- disk loader: .mpic files -> pinned ring -> HBM, overlapped with the layer loop ----
+// The .mpic container (proj/src/cache.cpp:97-188): 84-byte header, K [L][T][h] then V
+// [L][T][h] (v1: fp32, dtype 0; v2: bf16, dtype 1), then the zlib CRC32 of everything
+// before it. A reader thread preads layer l of every chunk (K and V rows) into a pinned
+// slot laid out exactly like the device staging slot, CRCs each segment on the way and
+// hands the slot to the request, whose copy stream moves it to HBM with ONE cudaMemcpyAsync
+// while layer l-1 computes. The per-segment CRCs are combined in file order
+// (crc32_combine) and checked when the request ends: a mismatch is an integrity error and
+// the caller recomputes the chunk (prepare's fallback, proj/src/transfer.cpp:111-115).
+namespace {
+struct MpicFile {
+    int fd = -1;
+    uint32_t version = 0, position_base = 0, L = 0, T = 0, H = 0, D = 0;
+    mpic_dtype dtype = MPIC_F32;
+    uint64_t fingerprint = 0;
+    uint32_t crc_stored = 0, crc_header = 0;
+    std::vector<uint32_t> crc_k, crc_v;  // per layer
+    ~MpicFile() {
+        if (fd >= 0) close(fd);
+    }
+};
+
+void pread_all(int fd, void* dst, size_t n, off_t off) {
+    char* p = static_cast<char*>(dst);
+    while (n) {
+        const ssize_t r = pread(fd, p, std::min<size_t>(n, (size_t)1 << 30), off);
+        MPIC_REQUIRE(r > 0, MPIC_ERR_IO, "short read of a .mpic file");
+        p += r;
+        n -= (size_t)r;
+        off += r;
+    }
+}
+
+uint32_t crc_of(const void* p, size_t n) {
+    uLong c = crc32(0L, Z_NULL, 0);
+    const Bytef* b = static_cast<const Bytef*>(p);
+    while (n) {
+        const uInt c1 = (uInt)std::min<size_t>(n, (size_t)1 << 30);
+        c = crc32(c, b, c1);
+        b += c1;
+        n -= c1;
+    }
+    return (uint32_t)c;
+}
+
+void open_mpic(MpicFile& f, const char* path, const mpic_model_t md, uint32_t want_T) {
+    f.fd = open(path, O_RDONLY);
+    MPIC_REQUIRE(f.fd >= 0, MPIC_ERR_NOT_FOUND, std::string("cannot open ") + path);
+    uint8_t h[84];
+    pread_all(f.fd, h, sizeof(h), 0);
+    auto u32 = [&](size_t o) { uint32_t v; std::memcpy(&v, h + o, 4); return v; };
+    MPIC_REQUIRE(std::memcmp(h, "MPIC", 4) == 0, MPIC_ERR_INTEGRITY, "bad .mpic magic");
+    f.version = u32(4);
+    MPIC_REQUIRE(f.version == 1 || f.version == 2, MPIC_ERR_INTEGRITY, "unsupported .mpic version");
+    std::memcpy(&f.fingerprint, h + 8, 8);
+    f.position_base = u32(56);
+    f.L = u32(60);
+    f.T = u32(64);
+    f.H = u32(68);
+    f.D = u32(72);
+    const uint8_t dt = h[76];
+    MPIC_REQUIRE((f.version == 1 && dt == 0) || (f.version == 2 && (dt == 0 || dt == 1)), MPIC_ERR_INTEGRITY,
+                 "unsupported .mpic payload dtype");
+    f.dtype = dt == 1 ? MPIC_BF16 : MPIC_F32;
+    const mpic_model_config& c = md->cfg;
+    MPIC_REQUIRE(f.fingerprint == fingerprint_of(&c), MPIC_ERR_LINK, "chunk was computed by a different model");
+    MPIC_REQUIRE(f.L == c.n_layers && f.H == c.n_heads && f.D == c.head_dim, MPIC_ERR_LINK,
+                 "entry tensor shape does not match model");
+    MPIC_REQUIRE(f.T == want_T, MPIC_ERR_LINK, "token_count mismatch for image segment");
+    struct stat st;
+    MPIC_REQUIRE(fstat(f.fd, &st) == 0, MPIC_ERR_IO, "cannot stat a .mpic file");
+    const size_t want = 84 + 2 * (size_t)f.L * f.T * f.H * f.D * esz(f.dtype) + 4;
+    MPIC_REQUIRE((size_t)st.st_size == want, MPIC_ERR_INTEGRITY, ".mpic file size does not match its header");
+    uint8_t tail[4];
+    pread_all(f.fd, tail, 4, (off_t)(want - 4));
+    std::memcpy(&f.crc_stored, tail, 4);
+    f.crc_header = crc_of(h, sizeof(h));
+    f.crc_k.assign(f.L, 0);
+    f.crc_v.assign(f.L, 0);
+}
+}  // namespace
+
+int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
+                               const mpic_policy* policy, const char* const* paths, mpic_reposition reposition,
+                               mpic_kv_t linked, float* logits, uint32_t* selected, uint32_t* m_out, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(model->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const RequestPlan r0 = plan_request(model, prompt, policy, nullptr);
+    check_linked(model, linked, r0.n);
+    const uint32_t n_img = (uint32_t)r0.refs.size();
+    std::vector<std::unique_ptr<MpicFile>> files(n_img);
+    std::vector<uint32_t> bases(n_img);
+    for (uint32_t i = 0; i < n_img; ++i) {
+        files[i] = std::make_unique<MpicFile>();
+        open_mpic(*files[i], paths[i], model, r0.refs[i].rows);
+        MPIC_REQUIRE(files[i]->dtype == files[0]->dtype, MPIC_ERR_VALIDATION, "mixed chunk dtypes");
+        bases[i] = files[i]->position_base;
+    }
+    const RequestPlan r = plan_request(model, prompt, policy, bases.data());
+    const mpic_dtype ct = n_img ? files[0]->dtype : MPIC_F32;
+    const size_t es = esz(ct), h = model->cfg.hidden_dim;
+    const uint32_t L = model->cfg.n_layers;
+    std::vector<size_t> off(n_img);
+    size_t img_rows = 0;
+    for (uint32_t i = 0; i < n_img; ++i) {
+        off[i] = img_rows * h;
+        img_rows += r.refs[i].rows;
+    }
+    const size_t slot_bytes = std::max<size_t>(1, img_rows) * h * es * 2;
+    // device staging ring (as mpic_request_prefill_host2) + pinned host ring of kSlots layers
+    constexpr int kSlots = 3;
+    if (ws->stage_cap < slot_bytes) {
+        MPIC_CUDA(cudaDeviceSynchronize());
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(ws->stage[i]);
+            ws->stage[i] = nullptr;
+            MPIC_CUDA(cudaMalloc(&ws->stage[i], slot_bytes));
+        }
+        ws->stage_cap = slot_bytes;
+    }
+    if (ws->pin_cap < slot_bytes) {
+        for (int i = 0; i < kSlots; ++i) {
+            cudaFreeHost(ws->pin[i]);
+            ws->pin[i] = nullptr;
+            MPIC_CUDA(cudaMallocHost(&ws->pin[i], slot_bytes));
+            if (!ws->ev_pin[i]) MPIC_CUDA(cudaEventCreateWithFlags(&ws->ev_pin[i], cudaEventDisableTiming));
+        }
+        ws->pin_cap = slot_bytes;
+    }
+    std::vector<uint32_t> ts(n_img);
+    for (uint32_t i = 0; i < n_img; ++i) ts[i] = r.refs[i].rows;
+    const AsmChunk* dc[2];
+    const float2* dt[2];
+    void* bufs[2];
+    uint32_t n_tab = 0;
+    for (int sl = 0; sl < 2; ++sl) {
+        std::vector<const void*> ks(n_img), vs(n_img);
+        char* base = static_cast<char*>(ws->stage[sl]);
+        for (uint32_t i = 0; i < n_img; ++i) {
+            ks[i] = base + off[i] * es;
+            vs[i] = base + (img_rows * h + off[i]) * es;
+        }
+        const AsmPlan p = plan_assembly(ks.data(), vs.data(), ts.data(), r.refs.data(), n_img, linked->T, linked->D,
+                                        reposition, model->cfg.rope_base, linked->H * linked->D);
+        n_tab = p.n_tables;
+        bufs[sl] = upload_plan(p, s, &dc[sl], &dt[sl]);
+    }
+    // reader thread: layer l -> pinned slot l % kSlots, with per-segment CRCs
+    std::mutex mu;
+    std::condition_variable cv;
+    int filled = -1;           // highest layer whose pinned slot is ready
+    int released = kSlots - 1; // layers < released + 1 - kSlots ... (slot reuse handshake below)
+    std::vector<bool> copied(L, false);
+    std::string reader_error;
+    std::thread reader([&] {
+        try {
+            for (uint32_t l = 0; l < L; ++l) {
+                const int sl = (int)(l % kSlots);
+                if (l >= (uint32_t)kSlots) {  // wait for the H2D that last used this slot
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return copied[l - kSlots] || !reader_error.empty(); });
+                    lk.unlock();
+                    MPIC_CUDA(cudaEventSynchronize(ws->ev_pin[sl]));
+                }
+                char* dst = static_cast<char*>(ws->pin[sl]);
+                for (uint32_t i = 0; i < n_img; ++i) {
+                    MpicFile& f = *files[i];
+                    const size_t seg = (size_t)f.T * h * es;
+                    char* kd = dst + off[i] * es;
+                    char* vd = dst + (img_rows * h + off[i]) * es;
+                    pread_all(f.fd, kd, seg, (off_t)(84 + (size_t)l * seg));
+                    pread_all(f.fd, vd, seg, (off_t)(84 + ((size_t)L + l) * seg));
+                    f.crc_k[l] = crc_of(kd, seg);
+                    f.crc_v[l] = crc_of(vd, seg);
+                }
+                {
+                    std::lock_guard<std::mutex> lk(mu);
+                    filled = (int)l;
+                }
+                cv.notify_all();
+            }
+        } catch (const std::exception& e) {
+            std::lock_guard<std::mutex> lk(mu);
+            reader_error = e.what();
+            cv.notify_all();
+        }
+    });
+    (void)released;
+    const size_t e = esz(linked->dtype);
+    const size_t plane = (size_t)linked->T * h * e;
+    cudaStream_t cs = ws->copy_stream;
+    MPIC_CUDA(cudaEventRecord(ws->ev_free[0], s));
+    MPIC_CUDA(cudaEventRecord(ws->ev_free[1], s));
+    auto issue_copy = [&](uint32_t l) {
+        {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return filled >= (int)l || !reader_error.empty(); });
+            if (!reader_error.empty()) throw Error(MPIC_ERR_IO, "disk loader: " + reader_error);
+        }
+        const int sl = l & 1, ps = (int)(l % kSlots);
+        MPIC_CUDA(cudaStreamWaitEvent(cs, ws->ev_free[sl], 0));
+        MPIC_CUDA(cudaMemcpyAsync(ws->stage[sl], ws->pin[ps], slot_bytes, cudaMemcpyHostToDevice, cs));
+        MPIC_CUDA(cudaEventRecord(ws->ev_pin[ps], cs));
+        MPIC_CUDA(cudaEventRecord(ws->ev_ready[sl], cs));
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            copied[l] = true;
+        }
+        cv.notify_all();
+    };
+    auto before_layer = [&](uint32_t l) {
+        if (l + 1 < L) issue_copy(l + 1);
+        const int sl = l & 1;
+        MPIC_CUDA(cudaStreamWaitEvent(s, ws->ev_ready[sl], 0));
+        ProfScope ps(s, MPIC_PHASE_ASSEMBLE);
+        launch_assemble(dc[sl], n_img, dt[sl], n_tab, ct, (char*)linked->k + l * plane, (char*)linked->v + l * plane,
+                        linked->dtype, 1, linked->T, linked->H, linked->D, 1, s);
+        MPIC_CUDA(cudaEventRecord(ws->ev_free[sl], s));
+    };
+    try {
+        issue_copy(0);
+        run_request(model, ws, r, linked, logits, selected, m_out, s, before_layer);
+    } catch (...) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (reader_error.empty()) reader_error = "request aborted";
+            for (uint32_t l = 0; l < L; ++l) copied[l] = true;
+        }
+        cv.notify_all();
+        reader.join();
+        throw;
+    }
+    reader.join();
+    for (int sl = 0; sl < 2; ++sl) MPIC_CUDA(cudaFreeAsync(bufs[sl], s));
+    MPIC_REQUIRE(reader_error.empty(), MPIC_ERR_IO, "disk loader: " + reader_error);
+    for (uint32_t i = 0; i < n_img; ++i) {  // CRC of the whole file, in file order
+        MpicFile& f = *files[i];
+        const size_t seg = (size_t)f.T * h * es;
+        uLong c = f.crc_header;
+        for (uint32_t l = 0; l < L; ++l) c = crc32_combine(c, f.crc_k[l], (z_off_t)seg);
+        for (uint32_t l = 0; l < L; ++l) c = crc32_combine(c, f.crc_v[l], (z_off_t)seg);
+        MPIC_REQUIRE((uint32_t)c == f.crc_stored, MPIC_ERR_INTEGRITY,
+                     std::string("crc mismatch in ") + paths[i] + ": the chunk must be recomputed");
+    }
+    API_END
 }
 
 int mpic_test_gemm(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uint32_t K,

@@ -331,3 +331,49 @@ def test_request_prefill_host_bf16_tier(g):
     assert np.array_equal(sel, ref_sel)
     assert np.array_equal(logits, ref_logits)
     assert all(np.array_equal(a, b) for a, b in zip(linked_h.download(), linked_d.download()))
+
+
+@pytest.mark.parametrize("bf16_payload", [False, True])
+def test_request_prefill_from_mpic_files(tmp_path, bf16_payload):
+    """The disk loader: .mpic v1 (fp32) / v2 (bf16) files -> pinned ring -> HBM per layer give
+    exactly the logits and cache of the same chunks resident in HBM; a flipped payload byte is
+    an integrity error (the chunk must be recomputed) and a foreign model a link error."""
+    L, H, D = 2, 8, 128
+    cfg = mp.config(L, H, D, vocab_size=4096, image_token_count=160, seed=4)
+    m = mp.Model(cfg, mp.BF16)
+    rng = np.random.default_rng(8)
+    segs = [("text", rng.integers(0, 4095, 12).tolist()), ("image", rng.bytes(32), 160),
+            ("text", rng.integers(0, 4095, 33).tolist()), ("image", rng.bytes(32), 160),
+            ("text", rng.integers(0, 4095, 5).tolist())]
+    p = mp.Prompt.from_segments(segs)
+    chunks = [(rng.random((L, 160, H * D), dtype=np.float32) - 0.5,
+               rng.random((L, 160, H * D), dtype=np.float32) - 0.5) for _ in range(2)]
+    paths = []
+    for i, (k, v) in enumerate(chunks):
+        path = str(tmp_path / f"c{i}.mpic")
+        mp.write_mpic(path, cfg, segs[1 + 2 * i][1], k, v, bf16=bf16_payload)
+        paths.append(path)
+    ws = mp.Workspace(m, 128, p.n)
+    linked_d = mp.KV(L, p.n, H, D, mp.BF16)
+    ref_logits, ref_sel = mp.request_prefill(m, ws, p, [mp.KV.from_host(k, v, H, D, mp.BF16) for k, v in chunks],
+                                             linked_d, k=32)
+    linked_f = mp.KV(L, p.n, H, D, mp.BF16)
+    logits, sel = mp.request_prefill_files(m, ws, p, paths, linked_f, k=32)
+    assert np.array_equal(sel, ref_sel)
+    assert np.array_equal(logits, ref_logits)
+    assert all(np.array_equal(a, b) for a, b in zip(linked_f.download(), linked_d.download()))
+    # corruption inside the payload -> integrity error after the request
+    with open(paths[1], "r+b") as f:
+        f.seek(84 + 1000)
+        b = f.read(1)
+        f.seek(84 + 1000)
+        f.write(bytes([b[0] ^ 0x10]))
+    with pytest.raises(mp.MpicError) as e:
+        mp.request_prefill_files(m, ws, p, paths, linked_f, k=32)
+    assert e.value.kind == "integrity_error"
+    # a chunk computed by another model
+    other = mp.config(L, H, D, vocab_size=4096, image_token_count=160, seed=5)
+    mp.write_mpic(paths[1], other, segs[3][1], *chunks[1], bf16=bf16_payload)
+    with pytest.raises(mp.MpicError) as e:
+        mp.request_prefill_files(m, ws, p, paths, linked_f, k=32)
+    assert e.value.kind == "link_error"
