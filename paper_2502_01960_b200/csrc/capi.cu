@@ -1913,37 +1913,42 @@ int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mp
         n_tab = p.n_tables;
         bufs[sl] = upload_plan(p, s, &dc[sl], &dt[sl]);
     }
-    // reader thread: layer l -> pinned slot l % kSlots, with per-segment CRCs
+    // reader threads: layer l -> pinned slot l % kSlots, with per-segment CRCs. The 2*n_img
+    // segments of a layer (K and V rows of every chunk) are spread over a few threads, so
+    // pread (page cache or NVMe) and CRC run in parallel.
     std::mutex mu;
     std::condition_variable cv;
-    int filled = -1;           // highest layer whose pinned slot is ready
-    int released = kSlots - 1; // layers < released + 1 - kSlots ... (slot reuse handshake below)
+    int filled = -1;  // highest layer whose pinned slot is complete
     std::vector<bool> copied(L, false);
+    std::vector<uint32_t> done(L, 0);
     std::string reader_error;
-    std::thread reader([&] {
+    const uint32_t n_seg = 2 * n_img;
+    const uint32_t n_threads = std::max<uint32_t>(1, std::min<uint32_t>(
+        n_seg, std::max<uint32_t>(1, std::thread::hardware_concurrency() / 2)));
+    auto read_worker = [&](uint32_t w) {
         try {
             for (uint32_t l = 0; l < L; ++l) {
                 const int sl = (int)(l % kSlots);
                 if (l >= (uint32_t)kSlots) {  // wait for the H2D that last used this slot
                     std::unique_lock<std::mutex> lk(mu);
                     cv.wait(lk, [&] { return copied[l - kSlots] || !reader_error.empty(); });
+                    if (!reader_error.empty()) return;
                     lk.unlock();
                     MPIC_CUDA(cudaEventSynchronize(ws->ev_pin[sl]));
                 }
                 char* dst = static_cast<char*>(ws->pin[sl]);
-                for (uint32_t i = 0; i < n_img; ++i) {
+                for (uint32_t sg = w; sg < n_seg; sg += n_threads) {
+                    const uint32_t i = sg >> 1;
+                    const bool is_v = sg & 1;
                     MpicFile& f = *files[i];
                     const size_t seg = (size_t)f.T * h * es;
-                    char* kd = dst + off[i] * es;
-                    char* vd = dst + (img_rows * h + off[i]) * es;
-                    pread_all(f.fd, kd, seg, (off_t)(84 + (size_t)l * seg));
-                    pread_all(f.fd, vd, seg, (off_t)(84 + ((size_t)L + l) * seg));
-                    f.crc_k[l] = crc_of(kd, seg);
-                    f.crc_v[l] = crc_of(vd, seg);
+                    char* d = dst + ((is_v ? img_rows * h : 0) + off[i]) * es;
+                    pread_all(f.fd, d, seg, (off_t)(84 + ((is_v ? (size_t)L : 0) + l) * seg));
+                    (is_v ? f.crc_v : f.crc_k)[l] = crc_of(d, seg);
                 }
                 {
                     std::lock_guard<std::mutex> lk(mu);
-                    filled = (int)l;
+                    if (++done[l] == n_threads) filled = (int)l;
                 }
                 cv.notify_all();
             }
@@ -1952,8 +1957,12 @@ int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mp
             reader_error = e.what();
             cv.notify_all();
         }
-    });
-    (void)released;
+    };
+    std::vector<std::thread> readers;
+    for (uint32_t w = 0; w < n_threads; ++w) readers.emplace_back(read_worker, w);
+    auto join_readers = [&] {
+        for (std::thread& t : readers) t.join();
+    };
     const size_t e = esz(linked->dtype);
     const size_t plane = (size_t)linked->T * h * e;
     cudaStream_t cs = ws->copy_stream;
@@ -1995,10 +2004,10 @@ int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mp
             for (uint32_t l = 0; l < L; ++l) copied[l] = true;
         }
         cv.notify_all();
-        reader.join();
+        join_readers();
         throw;
     }
-    reader.join();
+    join_readers();
     for (int sl = 0; sl < 2; ++sl) MPIC_CUDA(cudaFreeAsync(bufs[sl], s));
     MPIC_REQUIRE(reader_error.empty(), MPIC_ERR_IO, "disk loader: " + reader_error);
     for (uint32_t i = 0; i < n_img; ++i) {  // CRC of the whole file, in file order
