@@ -11,7 +11,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libmpic_b200.so")
+LIB_PATH = os.environ.get("MPIC_B200_LIB") or os.path.join(LIB_DIR, "libmpic_b200.so")  # env: diagnostics builds
 
 
 class ExtensionMissing(RuntimeError):
@@ -106,6 +106,7 @@ SIGNATURES = {
     "mpic_hp_logits": (_int, [_vp, _vp, _u32, _vp, _vp]),
     "mpic_workspace_device_ptr": (_int, [_vp, _int, _P(_vp)]),
     "mpic_clock_probe": (_int, [_vp, _u32, _vp]),
+    "mpic_pgemm_timestamps": (_int, [_vp]),
     "mpic_test_gemm": (_int, [_vp, _vp, _u32, _u32, _u32, _int, _vp, _vp]),
     "mpic_test_gemm_epi": (_int, [_vp, _vp, _u32, _u32, _u32, _int, _vp, _vp, _vp, _vp]),
     "mpic_profile_enable": (_int, [_int]),

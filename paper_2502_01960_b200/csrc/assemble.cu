@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmChunk* __restric
                                                        uint32_t n_tables, TD* __restrict__ dk,
                                                        TD* __restrict__ dv, uint32_t L, uint32_t T,
                                                        uint32_t H, uint32_t D, int zero_gaps,
-                                                       uint32_t src_l0) {
+                                                       uint32_t src_l0, const uint8_t* __restrict__ skip_blk) {
     extern __shared__ float2 s_tab[];
     __shared__ AsmChunk s_chunks[kMaxAsmChunks];
     const uint32_t half_d = D >> 1, h = H * D, nvec = h / VEC;
@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmChunk* __restric
     const uint64_t units = (uint64_t)L * T;
     for (uint64_t u = blockIdx.x; u < units; u += gridDim.x) {
         const uint32_t l = (uint32_t)(u / T), r = (uint32_t)(u % T);
+        if (skip_blk && skip_blk[r >> 7]) continue;  // linked inside attention (AttnLink)
         TD* kd = dk + u * h;
         TD* vd = dv + u * h;
         int c = -1;
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmChunk* __restric
 template <typename TS, typename TD>
 static void launch_asm_typed(const AsmChunk* d_chunks, uint32_t n_chunks, const float2* d_tables,
                              uint32_t n_tables, TD* dk, TD* dv, uint32_t L, uint32_t T, uint32_t H,
-                             uint32_t D, int zero_gaps, uint32_t src_l0, cudaStream_t s) {
+                             uint32_t D, int zero_gaps, uint32_t src_l0, const uint8_t* skip_blk, cudaStream_t s) {
     const uint32_t h = H * D;
     const uint64_t units = (uint64_t)L * T;
     const size_t smem = (size_t)n_tables * (D / 2) * sizeof(float2);
@@ -156,11 +157,11 @@ static void launch_asm_typed(const AsmChunk* d_chunks, uint32_t n_chunks, const 
     if (h % 8 == 0) {
         auto k = assemble_kernel<TS, TD, 8>;
         if (smem > 48 * 1024) MPIC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k<<<grid, 256, smem, s>>>(d_chunks, n_chunks, d_tables, n_tables, dk, dv, L, T, H, D, zero_gaps, src_l0);
+        k<<<grid, 256, smem, s>>>(d_chunks, n_chunks, d_tables, n_tables, dk, dv, L, T, H, D, zero_gaps, src_l0, skip_blk);
     } else {
         auto k = assemble_kernel<TS, TD, 2>;
         if (smem > 48 * 1024) MPIC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k<<<grid, 256, smem, s>>>(d_chunks, n_chunks, d_tables, n_tables, dk, dv, L, T, H, D, zero_gaps, src_l0);
+        k<<<grid, 256, smem, s>>>(d_chunks, n_chunks, d_tables, n_tables, dk, dv, L, T, H, D, zero_gaps, src_l0, skip_blk);
     }
     MPIC_LAUNCHED();
 }
@@ -168,17 +169,19 @@ static void launch_asm_typed(const AsmChunk* d_chunks, uint32_t n_chunks, const 
 void launch_assemble(const AsmChunk* d_chunks, uint32_t n_chunks, const float2* d_tables,
                      uint32_t n_tables, mpic_dtype src_t, void* dst_k, void* dst_v,
                      mpic_dtype dst_t, uint32_t L, uint32_t T_dst, uint32_t H, uint32_t D,
-                     int zero_gaps, cudaStream_t s, uint32_t src_l0) {
+                     int zero_gaps, cudaStream_t s, uint32_t src_l0, const uint8_t* skip_blk) {
     MPIC_REQUIRE(n_chunks <= kMaxAsmChunks, MPIC_ERR_VALIDATION, "too many chunks in one assembly");
+    static const bool skip = getenv("MPIC_ASM_SKIP") != nullptr;  // diagnostics: timing without the copy
+    if (skip) return;
     using bf = __nv_bfloat16;
     if (src_t == MPIC_F32 && dst_t == MPIC_F32)
-        launch_asm_typed<float, float>(d_chunks, n_chunks, d_tables, n_tables, (float*)dst_k, (float*)dst_v, L, T_dst, H, D, zero_gaps, src_l0, s);
+        launch_asm_typed<float, float>(d_chunks, n_chunks, d_tables, n_tables, (float*)dst_k, (float*)dst_v, L, T_dst, H, D, zero_gaps, src_l0, skip_blk, s);
     else if (src_t == MPIC_F32 && dst_t == MPIC_BF16)
-        launch_asm_typed<float, bf>(d_chunks, n_chunks, d_tables, n_tables, (bf*)dst_k, (bf*)dst_v, L, T_dst, H, D, zero_gaps, src_l0, s);
+        launch_asm_typed<float, bf>(d_chunks, n_chunks, d_tables, n_tables, (bf*)dst_k, (bf*)dst_v, L, T_dst, H, D, zero_gaps, src_l0, skip_blk, s);
     else if (src_t == MPIC_BF16 && dst_t == MPIC_BF16)
-        launch_asm_typed<bf, bf>(d_chunks, n_chunks, d_tables, n_tables, (bf*)dst_k, (bf*)dst_v, L, T_dst, H, D, zero_gaps, src_l0, s);
+        launch_asm_typed<bf, bf>(d_chunks, n_chunks, d_tables, n_tables, (bf*)dst_k, (bf*)dst_v, L, T_dst, H, D, zero_gaps, src_l0, skip_blk, s);
     else
-        launch_asm_typed<bf, float>(d_chunks, n_chunks, d_tables, n_tables, (float*)dst_k, (float*)dst_v, L, T_dst, H, D, zero_gaps, src_l0, s);
+        launch_asm_typed<bf, float>(d_chunks, n_chunks, d_tables, n_tables, (float*)dst_k, (float*)dst_v, L, T_dst, H, D, zero_gaps, src_l0, skip_blk, s);
 }
 
 // ---- weight synthesis (proj/include/mpic/rng.h:10-30, proj/src/model.cpp:28-36) -------

@@ -33,6 +33,20 @@ bool pdl_enabled() {
     return on;
 }
 
+// Scheduling priority of the request's hot kernels (GEMMs, attention): above the default
+// priority of the side-stream assembly, so assembly CTAs only fill SMs the hot path leaves
+// idle. MPIC_PRIO=0 (diagnostics) launches everything at the default priority.
+int hot_priority() {
+    static const int prio = [] {
+        const char* e = getenv("MPIC_PRIO");
+        if (e && atoi(e) == 0) return 0;
+        int least = 0, greatest = 0;
+        if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return 0;
+        return greatest;
+    }();
+    return prio;
+}
+
 // ---- per-phase device timing (CUDA events on the launching stream) ------------------
 // Enabled by mpic_profile_enable(1); each phase of a forward/assembly records a start and
 // stop event around its launches; mpic_profile_collect() synchronizes and sums them.
@@ -116,10 +130,11 @@ struct GraphSig {
     const void* linked = nullptr;
     uint32_t n = 0, m = 0, n_img = 0, n_tables = 0, n_units = 0, n_comb = 0;
     int reposition = 0, src_dtype = 0;
+    bool link = false;
     bool operator==(const GraphSig& o) const {
         return model == o.model && linked == o.linked && n == o.n && m == o.m && n_img == o.n_img &&
                n_tables == o.n_tables && n_units == o.n_units && n_comb == o.n_comb &&
-               reposition == o.reposition && src_dtype == o.src_dtype;
+               reposition == o.reposition && src_dtype == o.src_dtype && link == o.link;
     }
 };
 
@@ -366,6 +381,55 @@ bool use_tc_attention(mpic_model_t md) {
     return md->dtype == MPIC_BF16 && md->cfg.head_dim == 128;
 }
 
+bool attn_link_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("MPIC_ATTN_LINK");  // diagnostics: 0 = assemble every block up front
+        return !e || atoi(e) != 0;
+    }();
+    return on;
+}
+
+// Blocks of 128 cache rows that attention can read straight from a cached chunk (AttnLink):
+// inside one chunk's destination range and holding no recomputed row. Returns false when no
+// block qualifies. blk / skip are per block (kernels.h AttnLink; skip = not assembled).
+bool plan_attn_link(const std::vector<mpic_chunk_ref>& refs, const uint32_t* sel, uint32_t m, uint32_t n,
+                    std::vector<uint32_t>& blk, std::vector<uint16_t>& wtile, std::vector<uint8_t>& skip) {
+    const uint32_t nblk = (n + 127) / 128;
+    blk.assign(nblk, kLinkedBlock);
+    // writer tile: the lowest query tile whose key range reaches the block (the attention
+    // plan's per-tile range is [0, rows[last row of the tile] / 128])
+    wtile.assign(nblk, 0);
+    {
+        uint32_t t = 0;
+        for (uint32_t b = 0; b < nblk; ++b) {
+            while (t + 1 < (m + 127) / 128 && sel[std::min(m, (t + 1) * 128) - 1] / 128 < b) ++t;
+            wtile[b] = (uint16_t)t;
+        }
+    }
+    skip.assign(nblk, 0);
+    std::vector<uint8_t> rec(n, 0);
+    for (uint32_t i = 0; i < m; ++i)
+        if (sel[i] < n) rec[sel[i]] = 1;
+    bool any = false;
+    for (uint32_t b = 0; b * 128 + 128 <= n; ++b) {
+        const uint32_t a0 = b * 128;
+        for (uint32_t c = 0; c < refs.size(); ++c) {
+            const mpic_chunk_ref& ref = refs[c];
+            if (a0 < ref.dst_row0 || a0 + 128 > ref.dst_row0 + ref.rows) continue;
+            bool recomputed = false;
+            for (uint32_t k = a0; k < a0 + 128 && !recomputed; ++k) recomputed = rec[k] != 0;
+            const uint32_t src = ref.src_row0 + (a0 - ref.dst_row0);
+            if (!recomputed && src < (1u << 24)) {
+                blk[b] = (c << 24) | src;
+                skip[b] = 1;
+                any = true;
+            }
+            break;
+        }
+    }
+    return any;
+}
+
 // Build the attention work plan from host rows (or, without them, a conservative plan in
 // which every query may see keys up to max_pos), grow the workspace buffers it needs and
 // stage it in pinned memory. Host-only: nothing is enqueued, so it may run before a
@@ -438,7 +502,8 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
                   const uint32_t* d_rows, const uint32_t* d_pos, uint32_t m, uint32_t max_pos,
                   mpic_kv_t kv, float* d_logits, cudaStream_t s,
                   const std::function<void(uint32_t)>& before_layer = {},
-                  const uint32_t* h_rows = nullptr, float* d_capture = nullptr, bool plan_ready = false) {
+                  const uint32_t* h_rows = nullptr, float* d_capture = nullptr, bool plan_ready = false,
+                  const AttnLink* d_link = nullptr) {
     const mpic_model_config& c = md->cfg;
     const uint32_t h = c.hidden_dim, H = c.n_heads, D = c.head_dim;
     MPIC_REQUIRE(m > 0, MPIC_ERR_VALIDATION, "no tokens to prefill");
@@ -489,7 +554,7 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
                 launch_attn_tc(static_cast<const __nv_bfloat16*>(ws->q), static_cast<const __nv_bfloat16*>(kl),
                                static_cast<const __nv_bfloat16*>(vl), kv->T, d_rows, m, H, ws->d_units,
                                ws->n_units, ws->d_comb, ws->n_comb, ws->part_o, ws->part_ml,
-                               static_cast<__nv_bfloat16*>(ws->attn), s);
+                               static_cast<__nv_bfloat16*>(ws->attn), s, d_link, l);
             else
                 launch_attn_simt(ws->q, kl, vl, md->dtype, d_rows, m, H, D, ws->attn, s);
         }
@@ -1317,21 +1382,45 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
     if (use_tc_attention(model)) prepare_attn_plan(ws, r.sel.data(), r.m, r.n - 1, model->cfg.n_heads);
     std::memcpy(ws->h_ids, r.ids_sel.data(), r.m * sizeof(int32_t));
     std::memcpy(ws->h_rows, r.sel.data(), r.m * sizeof(uint32_t));
+    // linking inside attention: chunk blocks skip the assembly and are stored by attention
+    std::vector<uint32_t> link_blk;
+    std::vector<uint16_t> link_wtile;
+    std::vector<uint8_t> link_skip;
+    const bool link = attn_link_enabled() && use_tc_attention(model) && linked->dtype == MPIC_BF16 &&
+                      src_t == MPIC_BF16 && n_img > 0 && n_img <= kMaxLinkChunks && ap.n_tables == 0 &&
+                      plan_attn_link(r.refs, r.sel.data(), r.m, r.n, link_blk, link_wtile, link_skip);
     const size_t bytes_c = std::max<size_t>(1, ap.chunks.size()) * sizeof(AsmChunk);
     const size_t bytes_t = std::max<size_t>(1, ap.tables.size()) * sizeof(float2);
-    if (ws->asm_cap < bytes_c + bytes_t) {
+    const size_t off_l = (bytes_c + bytes_t + 63) & ~size_t(63);
+    const size_t bytes_l = link ? sizeof(AttnLink) + link_blk.size() * 6 : 0;
+    const size_t off_s = off_l + ((bytes_l + 63) & ~size_t(63));
+    const size_t bytes_all = off_s + link_skip.size();
+    if (ws->asm_cap < bytes_all) {
         MPIC_CUDA(cudaDeviceSynchronize());
         cudaFreeHost(ws->h_asm);
         cudaFree(ws->d_asm);
         ws->h_asm = ws->d_asm = nullptr;
         ws->asm_cap = 0;
-        MPIC_CUDA(cudaMallocHost(&ws->h_asm, bytes_c + bytes_t));
-        MPIC_CUDA(cudaMalloc(&ws->d_asm, bytes_c + bytes_t));
-        ws->asm_cap = bytes_c + bytes_t;
+        MPIC_CUDA(cudaMallocHost(&ws->h_asm, bytes_all));
+        MPIC_CUDA(cudaMalloc(&ws->d_asm, bytes_all));
+        ws->asm_cap = bytes_all;
     }
     if (!ap.chunks.empty()) std::memcpy(ws->h_asm, ap.chunks.data(), ap.chunks.size() * sizeof(AsmChunk));
     if (!ap.tables.empty())
         std::memcpy((char*)ws->h_asm + bytes_c, ap.tables.data(), ap.tables.size() * sizeof(float2));
+    const AttnLink* d_link = nullptr;
+    const uint8_t* d_skip = nullptr;
+    if (link) {
+        AttnLink* hl = reinterpret_cast<AttnLink*>((char*)ws->h_asm + off_l);
+        std::memset(hl, 0, sizeof(AttnLink));
+        make_link_maps(hl, ks.data(), vs.data(), ts.data(), n_img, linked->L, linked->H * linked->D);
+        hl->nblk = (uint32_t)link_blk.size();
+        std::memcpy(hl + 1, link_blk.data(), link_blk.size() * 4);
+        std::memcpy(reinterpret_cast<uint32_t*>(hl + 1) + link_blk.size(), link_wtile.data(), link_wtile.size() * 2);
+        std::memcpy((char*)ws->h_asm + off_s, link_skip.data(), link_skip.size());
+        d_link = reinterpret_cast<const AttnLink*>((char*)ws->d_asm + off_l);
+        d_skip = reinterpret_cast<const uint8_t*>((char*)ws->d_asm + off_s);
+    }
 
     // ---- device work: one stream-ordered sequence, optionally recorded as a CUDA graph ----
     static const bool asm_overlap = [] {
@@ -1341,7 +1430,7 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
     auto enqueue = [&] {
         MPIC_CUDA(cudaMemcpyAsync(ws->d_ids, ws->h_ids, r.m * 4, cudaMemcpyHostToDevice, s));
         MPIC_CUDA(cudaMemcpyAsync(ws->d_rows, ws->h_rows, r.m * 4, cudaMemcpyHostToDevice, s));
-        MPIC_CUDA(cudaMemcpyAsync(ws->d_asm, ws->h_asm, bytes_c + bytes_t, cudaMemcpyHostToDevice, s));
+        MPIC_CUDA(cudaMemcpyAsync(ws->d_asm, ws->h_asm, bytes_all, cudaMemcpyHostToDevice, s));
         const AsmChunk* dch = static_cast<const AsmChunk*>(ws->d_asm);
         const float2* dtab = reinterpret_cast<const float2*>((char*)ws->d_asm + bytes_c);
         std::function<void(uint32_t)> wait_layer;
@@ -1357,7 +1446,7 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
                     ProfScope ps(ws->asm_stream, MPIC_PHASE_ASSEMBLE);
                     launch_assemble(dch, n_img, dtab, ap.n_tables, src_t, (char*)linked->k + l * plane,
                                     (char*)linked->v + l * plane, linked->dtype, 1, linked->T, linked->H, linked->D, 1,
-                                    ws->asm_stream, l);
+                                    ws->asm_stream, l, d_skip);
                 }
                 MPIC_CUDA(cudaEventRecord(ws->ev_asm[l], ws->asm_stream));
             }
@@ -1365,10 +1454,10 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
         } else {
             ProfScope ps(s, MPIC_PHASE_ASSEMBLE);
             launch_assemble(dch, n_img, dtab, ap.n_tables, src_t, linked->k, linked->v, linked->dtype, linked->L,
-                            linked->T, linked->H, linked->D, 1, s);
+                            linked->T, linked->H, linked->D, 1, s, 0, d_skip);
         }
         forward_rows(model, ws, ws->d_ids, ws->d_rows, ws->d_rows, r.m, r.n - 1, linked, ws->d_logits, s, wait_layer,
-                     r.sel.data(), nullptr, /*plan_ready=*/true);
+                     r.sel.data(), nullptr, /*plan_ready=*/true, d_link);
         MPIC_CUDA(cudaMemcpyAsync(ws->h_logits, ws->d_logits, model->cfg.vocab_size * 4, cudaMemcpyDeviceToHost, s));
     };
     GraphSig sig;
@@ -1382,6 +1471,7 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
     sig.n_comb = ws->n_comb;
     sig.reposition = reposition;
     sig.src_dtype = src_t;
+    sig.link = link;
     bool prof;
     {
         std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -2066,6 +2156,12 @@ int mpic_test_gemm_epi(const void* d_a, const void* d_w, uint32_t M, uint32_t N,
     }
     launch_gemm_tc(static_cast<const __nv_bfloat16*>(d_a), K, static_cast<const __nv_bfloat16*>(d_w), M, N, K, ep,
                    (cudaStream_t)stream);
+    API_END
+}
+
+int mpic_pgemm_timestamps(unsigned long long* out9) {
+    API_BEGIN
+    pgemm_timestamps(out9);
     API_END
 }
 

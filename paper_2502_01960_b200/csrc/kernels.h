@@ -40,9 +40,12 @@ struct EpiParams {
     // EPI_STORE / EPI_GELU
     void* out = nullptr;
     uint32_t ldo = 0;
+    uint32_t dbg = 0;  // pair GEMM diagnostics (MPIC_PG_DBG bits 16/32: skip x loads / stores)
 };
 
 // One chunk placement for the assembly kernel (device-side descriptor).
+int hot_priority();  // launch priority of the hot kernels (capi.cu)
+
 struct AsmChunk {
     const void* src_k;
     const void* src_v;
@@ -94,7 +97,8 @@ void launch_resid_add(float* x, const float* add, __nv_bfloat16* xb, size_t n, c
 void launch_assemble(const AsmChunk* d_chunks, uint32_t n_chunks, const float2* d_tables,
                      uint32_t n_tables, mpic_dtype src_t, void* dst_k, void* dst_v,
                      mpic_dtype dst_t, uint32_t L, uint32_t T_dst, uint32_t H, uint32_t D,
-                     int zero_gaps, cudaStream_t s, uint32_t src_l0 = 0);
+                     int zero_gaps, cudaStream_t s, uint32_t src_l0 = 0,
+                     const uint8_t* skip_blk = nullptr);
 
 // Attention work plan (tc_attn.cu): an item is up to two query tiles of one head that
 // stream the same key blocks [b0, max(b1)) — tile[1] == kNoTile when the item has one.
@@ -115,11 +119,33 @@ struct AttnPlan {
 };
 unsigned long long* attn_debug_buffer();
 AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads);
+// Linking inside attention (device-resident bf16 chunks, no re-rotation): 128-key blocks
+// that lie inside one cached chunk and hold no recomputed row are read by the attention
+// kernel straight from the chunk's [L][T_c][h] planes, and the CTA that owns the block for
+// the lowest query tile that reaches it stores it into the request cache (TMA store of the tile it already
+// holds in shared memory). Every other block is assembled beforehand as usual. Lives in
+// device memory, 64-B aligned; the per-block table follows the header.
+constexpr uint32_t kMaxLinkChunks = 8;
+constexpr uint32_t kLinkedBlock = 0xffffffffu;  // block read from the request cache
+struct alignas(64) TmapBytes {
+    unsigned char b[128];  // a CUtensorMap
+};
+struct alignas(64) AttnLink {
+    TmapBytes maps[2 * kMaxLinkChunks];  // per chunk: K, V over [L * T_c rows][h]
+    uint32_t tokens[kMaxLinkChunks];     // T_c
+    uint32_t nblk;
+    uint32_t pad[7];
+    // uint32_t blk[nblk]: (chunk << 24) | first chunk row of the block, or kLinkedBlock
+    // uint16_t wtile[nblk]: the query tile whose item stores block b (lowest tile reaching b)
+};
+void make_link_maps(AttnLink* host, const void* const* k, const void* const* v, const uint32_t* T, uint32_t n,
+                    uint32_t L, uint32_t h);
+
 void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const __nv_bfloat16* vcache,
                     uint32_t n_ctx, const uint32_t* d_rows, uint32_t m, uint32_t H,
                     const AttnUnit* d_units, uint32_t n_units, const AttnCombine* d_combine,
                     uint32_t n_combine, float* part_o, float2* part_ml, __nv_bfloat16* out,
-                    cudaStream_t s);
+                    cudaStream_t s, const AttnLink* link = nullptr, uint32_t layer = 0);
 
 // tcgen05 / TMA kernels (tc_gemm.cu, tc_attn.cu)
 struct TcGemmPlan;
@@ -132,6 +158,10 @@ void launch_gemm_tc(const __nv_bfloat16* A, uint32_t lda, const __nv_bfloat16* W
 bool pgemm_supported(uint32_t M, uint32_t N, uint32_t K);
 void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint32_t N, uint32_t K,
                   const EpiParams& ep, cudaStream_t s, bool w_blocked = false);
+// MPIC_PG_TS diagnostics of the last pair GEMM's CTA 0: 5 x %globaltimer ns (entry, after
+// prologue, MMAs issued, epilogue done, exit), then clock64 cycles: producer waiting on
+// empty slots / producer total / MMA issuer waiting on full slots / MMA issuer total.
+void pgemm_timestamps(unsigned long long* out9);
 // Row-major [N][K] bf16 <-> the blocked weight layout (N % 128 == 0, K % 64 == 0).
 void launch_block_weights(const __nv_bfloat16* src, __nv_bfloat16* dst, uint32_t N, uint32_t K, bool to_blocked,
                           cudaStream_t s);

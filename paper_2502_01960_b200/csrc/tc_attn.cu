@@ -15,7 +15,8 @@
 //              owns TMEM (512 cols: S_A | O_A | S_B | O_B). MMAs: S_X(j) = Q_X . K_j^T (SS, K-major) and O_X += P_X(j) . V_j (P from
 //              TMEM, V MN-major), ordered PV_A(j) S_A(j+1) PV_B(j) S_B(j+1), so one tile's
 //              MMAs run while the other tile's softmax works
-//   warps 1-3  idle (warpgroup 0 hands its registers to the softmax warpgroups: setmaxnreg)
+//   warps 1-3  linker when chunk blocks are linked inside attention (kernels.h AttnLink),
+//              otherwise idle (warpgroup 0 hands its registers to the softmax warpgroups)
 //   warps 4-7  softmax of tile A, warps 8-11 of tile B, 224 registers per thread: ONE THREAD PER QUERY ROW holding
 //              its 128 scores (no cross-warp reduction), scale, per-row causal mask, online
 //              max with lazy O rescaling (only when the max grows by more than 2^8), exp2
@@ -23,6 +24,7 @@
 //              bf16) and half on MUFU, row sums; P written back over S in TMEM as bf16.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -54,7 +56,27 @@ struct AttnParams {
     float* part_o;          // [slots][128][128]
     float2* part_ml;        // [slots][128] (m_used, l)
     unsigned long long* dbg;  // diagnostics: per-block event times of CTA 0, or null
+    const AttnLink* link;     // linking inside attention (kernels.h), or null
+    uint32_t layer;
+    uint32_t link_nostore;    // diagnostics (MPIC_ATTN_LINK=2): read chunks, skip the stores
+    __nv_bfloat16* cache_k;   // the layer's request cache planes (linker stores)
+    __nv_bfloat16* cache_v;
 };
+
+// Source of key block `blk` (absolute): the chunk map and row, or the request cache.
+__device__ __forceinline__ const CUtensorMap* link_src(const AttnParams& p, const CUtensorMap* cache_map,
+                                                       uint32_t blk, uint32_t K, int& row) {
+    if (p.link) {
+        const uint32_t code = reinterpret_cast<const uint32_t*>(p.link + 1)[blk];
+        if (code != kLinkedBlock) {
+            const uint32_t c = code >> 24;
+            row = (int)(p.layer * p.link->tokens[c] + (code & 0xffffffu));
+            return reinterpret_cast<const CUtensorMap*>(&p.link->maps[2 * c + K]);
+        }
+    }
+    row = (int)(blk * 128u);
+    return cache_map;
+}
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
@@ -130,13 +152,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tc::tma_prefetch_desc(&tmK);
         tc::tma_prefetch_desc(&tmV);
         tc::mbar_init(q_full, 1);
+        // with linking, a K/V stage is free once its MMAs are done AND the linker has
+        // finished storing it (or passed it)
+        const uint32_t empties = p.link ? 2u : 1u;
         for (uint32_t i = 0; i < kKStages; ++i) {
             tc::mbar_init(&k_full[i], 1);
-            tc::mbar_init(&k_empty[i], 1);
+            tc::mbar_init(&k_empty[i], empties);
         }
         for (uint32_t i = 0; i < kVStages; ++i) {
             tc::mbar_init(&v_full[i], 1);
-            tc::mbar_init(&v_empty[i], 1);
+            tc::mbar_init(&v_empty[i], empties);
         }
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&s_full[i], 1);
@@ -178,22 +203,26 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 tc::tma_load_2d(sQ + x * kTile, &tmQ, q_full, hcol, q0);
                 tc::tma_load_2d(sQ + x * kTile + kHalf, &tmQ, q_full, hcol + 64, q0);
             }
+            if (p.link)
+                for (uint32_t c = 0; c < 2 * kMaxLinkChunks; ++c) tc::tensormap_acquire(&p.link->maps[c]);
             for (uint32_t j = 0; j < nbmax; ++j) {
                 const uint32_t st = j % kKStages, ph = (j / kKStages) & 1;
-                const int j0 = (int)((u.b0 + j) * 128u);
+                int j0;
+                const CUtensorMap* src = link_src(p, &tmK, u.b0 + j, 0, j0);
                 tc::mbar_wait(&k_empty[st], ph ^ 1);
                 tc::mbar_arrive_expect_tx(&k_full[st], kTile);
-                tc::tma_load_2d(sK + st * kTile, &tmK, &k_full[st], hcol, j0);
-                tc::tma_load_2d(sK + st * kTile + kHalf, &tmK, &k_full[st], hcol + 64, j0);
+                tc::tma_load_2d(sK + st * kTile, src, &k_full[st], hcol, j0);
+                tc::tma_load_2d(sK + st * kTile + kHalf, src, &k_full[st], hcol + 64, j0);
             }
         } else if (lane == 16) {
             for (uint32_t j = 0; j < nbmax; ++j) {
                 const uint32_t st = j % kVStages, ph = (j / kVStages) & 1;
-                const int j0 = (int)((u.b0 + j) * 128u);
+                int j0;
+                const CUtensorMap* src = link_src(p, &tmV, u.b0 + j, 1, j0);
                 tc::mbar_wait(&v_empty[st], ph ^ 1);
                 tc::mbar_arrive_expect_tx(&v_full[st], kTile);
-                tc::tma_load_2d(sV + st * kTile, &tmV, &v_full[st], hcol, j0);
-                tc::tma_load_2d(sV + st * kTile + kHalf, &tmV, &v_full[st], hcol + 64, j0);
+                tc::tma_load_2d(sV + st * kTile, src, &v_full[st], hcol, j0);
+                tc::tma_load_2d(sV + st * kTile + kHalf, src, &v_full[st], hcol + 64, j0);
             }
         }
         else if (lane == 8) {
@@ -257,6 +286,40 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             }
         }
         __syncwarp();
+    } else if (warp < 4) {
+        if (p.link) {
+            // ---- linker (warps 1-3): copies the chunk-sourced K/V blocks this item is the
+            // writer of from the stage buffers into the request cache with 16-B stores on the
+            // LSU path (the TMA unit stays with the K/V loads), then releases the stage.
+            // Writer of block b = the item streaming b for the lowest query tile reaching b.
+            const uint32_t t = threadIdx.x - 32;  // 0 .. 95
+            const uint32_t* blk = reinterpret_cast<const uint32_t*>(p.link + 1);
+            const uint16_t* wtile = reinterpret_cast<const uint16_t*>(blk + p.link->nblk);
+            auto copy_tile = [&](const uint8_t* tile, __nv_bfloat16* cache, uint32_t j0) {
+                // [2 halves][128 rows][128 B] SW128: logical 16-B chunk c of row r sits at chunk c ^ (r & 7)
+                for (uint32_t i = t; i < 2 * 128 * 8; i += 96) {
+                    const uint32_t half = i >> 10, r = (i >> 3) & 127, c = i & 7;
+                    const uint4 v = *reinterpret_cast<const uint4*>(tile + half * kHalf + r * 128 + ((c ^ (r & 7)) << 4));
+                    __stcs(reinterpret_cast<uint4*>(cache + (size_t)(j0 + r) * p.h + hcol + half * 64 + c * 8), v);
+                }
+            };
+            for (uint32_t j = 0; j < nbmax; ++j) {
+                const uint32_t b = u.b0 + j, wt = wtile[b];
+                const bool mine = (u.tile[0] == wt && j < nb0) || (has_b && u.tile[1] == wt && j < nb1);
+                const bool store = mine && blk[b] != kLinkedBlock && !p.link_nostore;
+                const uint32_t sk = j % kKStages, sv = j % kVStages;
+                // every linker thread observes each phase before the stage is released (the
+                // barrier also keeps a lagging thread from waiting on a parity that has come round)
+                tc::mbar_wait(&k_full[sk], (j / kKStages) & 1);
+                if (store) copy_tile(sK + sk * kTile, p.cache_k, b * 128u);
+                tc::named_bar_sync(1, 96);
+                if (t == 0) tc::mbar_arrive(&k_empty[sk]);
+                tc::mbar_wait(&v_full[sv], (j / kVStages) & 1);
+                if (store) copy_tile(sV + sv * kTile, p.cache_v, b * 128u);
+                tc::named_bar_sync(1, 96);
+                if (t == 0) tc::mbar_arrive(&v_empty[sv]);
+            }
+        }
     } else if (warp >= 4) {
         // ---- softmax: tile x = warp / 4 - 1, one thread per query row (TMEM lane)
         const uint32_t x = (warp >> 2) - 1;
@@ -524,7 +587,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
                     uint32_t n_ctx, const uint32_t* d_rows, uint32_t m, uint32_t H,
                     const AttnUnit* d_units, uint32_t n_units, const AttnCombine* d_combine,
                     uint32_t n_combine, float* part_o, float2* part_ml, __nv_bfloat16* out,
-                    cudaStream_t s) {
+                    cudaStream_t s, const AttnLink* link, uint32_t layer) {
     const uint32_t h = H * 128;
     const CUtensorMap tmQ = make_tmap_bf16(q, h, m, 64, 128);
     const CUtensorMap tmK = make_tmap_bf16(kcache, h, n_ctx, 64, 128);
@@ -539,22 +602,33 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     p.part_o = part_o;
     p.part_ml = part_ml;
     p.dbg = attn_debug_buffer();
+    p.link = link;
+    p.cache_k = const_cast<__nv_bfloat16*>(kcache);
+    p.cache_v = const_cast<__nv_bfloat16*>(vcache);
+    p.layer = layer;
+    static const bool nostore = [] {
+        const char* e = getenv("MPIC_ATTN_LINK");
+        return e && atoi(e) == 2;
+    }();
+    p.link_nostore = nostore ? 1u : 0u;
     const size_t smem = (2 + kKStages + kVStages) * kTile + 1024 + (1 + 2 * kKStages + 2 * kVStages + 6) * 8 + 16;
     static bool attr = false;
     if (!attr) {
         MPIC_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    at[1].id = cudaLaunchAttributePriority;
+    at[1].val.priority = hot_priority();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(n_units);
     cfg.blockDim = dim3(kAttnThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     MPIC_CUDA(cudaLaunchKernelEx(&cfg, attn_tc_kernel, tmQ, tmK, tmV, p));
     MPIC_LAUNCHED();
     if (n_combine) {
@@ -564,6 +638,20 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
         MPIC_CUDA(cudaLaunchKernelEx(&cfg, attn_combine_kernel, d_combine, (const float*)part_o,
                                      (const float2*)part_ml, m, h, out));
         MPIC_LAUNCHED();
+    }
+}
+
+void make_link_maps(AttnLink* host, const void* const* k, const void* const* v, const uint32_t* T, uint32_t n,
+                    uint32_t L, uint32_t h) {
+    MPIC_REQUIRE(n <= kMaxLinkChunks, MPIC_ERR_VALIDATION, "too many chunks to link inside attention");
+    static_assert(sizeof(TmapBytes) == sizeof(CUtensorMap), "tensor map size");
+    for (uint32_t c = 0; c < kMaxLinkChunks; ++c) {
+        const uint32_t i = c < n ? c : 0;  // unused slots repeat chunk 0 (never addressed)
+        const CUtensorMap mk = make_tmap_bf16(k[i], h, (uint64_t)L * T[i], 64, 128);
+        const CUtensorMap mv = make_tmap_bf16(v[i], h, (uint64_t)L * T[i], 64, 128);
+        std::memcpy(&host->maps[2 * c], &mk, sizeof(mk));
+        std::memcpy(&host->maps[2 * c + 1], &mv, sizeof(mv));
+        host->tokens[c] = T[i];
     }
 }
 

@@ -52,6 +52,8 @@ namespace {
 constexpr uint32_t kPgThreads = 320;  // producer, MMA, 8 epilogue warps
 constexpr uint32_t kPgWBytes = 128 * 64 * 2;  // one CTA's weight rows per k-block (16 KB)
 constexpr uint32_t kChunkBytes = 32 * 128 * 4;  // one 32-token x 128-feature fp32 chunk
+constexpr uint32_t kNoStage = 0xffffffffu;
+constexpr uint32_t kStageSlice = 4096;  // one epilogue warp's staging slice
 
 struct PgArgs {
     uint32_t M, N, K;
@@ -73,9 +75,20 @@ struct PgArgs {
     uint32_t dbg;        // diagnostics: 1 skip epilogue, 2 skip X loads, 4 skip W loads, 8 skip MMA
     uint32_t stage_rope; // QKV: stage rope/kv_rows of the (single) group in the idle stage buffers
     uint32_t rows_off;   // byte offset of the staged kv_rows
+    unsigned long long* ts;  // diagnostics (MPIC_PG_TS): CTA 0 entry / after prologue / MMAs
+                             // issued / epilogue done / exit, %globaltimer ns
     uint32_t w_blocked;  // W stored as [N/128][K/64][128][64] tiles
+    uint32_t pfd;        // L2 prefetch distance of the weight stream in k-blocks (0: off)
+    uint32_t stg_off;    // staged epilogue stores: byte offset of the 8 x 4 KB warp slices in the
+                         // (then idle) stage ring, or kNoStage
     EpiParams ep;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // GELU (tanh form, proj/src/model.cpp:85-87) with the hardware tanh: the result is rounded
 // to bf16, whose 2^-8 step is coarser than tanh.approx's error (bf16 mode only; the fp32
@@ -93,11 +106,149 @@ __device__ __forceinline__ float gelu_fast(float x) {
 // mode (and for full chunks) so the per-element loops are branch-free.
 // s_rows / s_rope: this group's kv_rows and (cos, sin) rows staged in shared memory
 // (indexed from the group's first token tg), or null to read them from global memory.
+// Staged stores (stg != null: this warp's 4 KB slice of the idle stage ring): the 32 tokens x
+// 32 features of a chunk are transposed through shared memory so that each lane stores 16 B
+// and one instruction covers 8 (bf16) or 4 (fp32) whole 64/128-B token-row segments instead
+// of one — the direct form issues 32 narrow scattered stores per chunk, which bounds the
+// epilogue tail.
+__device__ __forceinline__ void stage_put_bf16(__nv_bfloat16* stg, uint32_t j, uint32_t lane, __nv_bfloat16 v) {
+    stg[j * 32 + lane] = v;
+}
+// row-wise read-back: lane -> token 8i + lane/4, features (lane%4)*8 .. +8
+__device__ __forceinline__ uint4 stage_get_bf16(const __nv_bfloat16* stg, uint32_t i, uint32_t lane) {
+    return *reinterpret_cast<const uint4*>(stg + (i * 8 + (lane >> 2)) * 32 + (lane & 3) * 8);
+}
+
+// Transpose a warp's 32 tokens x 32 features accumulator chunk (lane = feature) into its
+// staging slice as [token][32 features] fp32.
+__device__ __forceinline__ void stage_put_f32(float* sf, uint32_t lane, const uint32_t (&r)[32]) {
+#pragma unroll
+    for (uint32_t j = 0; j < 32; ++j) sf[j * 32 + lane] = __uint_as_float(r[j]);
+    __syncwarp();
+}
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+// Residual add of a transposed chunk (lane -> token 4i + lane/8, features 4*(lane%8) ..+4 of
+// the warp's 32): x += v, xb = bf16(x). One instruction covers 4 whole 128-B x rows.
+// `part(i)` returns the fp32 sum for read-back step i.
+template <class Part>
+__device__ __forceinline__ void resid_rows(const EpiParams& ep, uint32_t n, uint32_t tb, uint32_t f0, uint32_t lane,
+                                           Part part) {
+    const uint32_t c = f0 + (lane & 7) * 4;
+    // all x loads are issued before the first store (the compiler cannot hoist them past
+    // stores to the same array)
+    float4 v[8], xo[8];
+#pragma unroll
+    for (uint32_t i = 0; i < 8; ++i) {
+        const uint32_t t = i * 4 + (lane >> 3);
+        xo[i] = t < n && !(ep.dbg & 16) ? __ldcg(reinterpret_cast<const float4*>(ep.x + (size_t)(tb + t) * ep.ldx + c))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (uint32_t i = 0; i < 8; ++i) v[i] = part(i);
+#pragma unroll
+    for (uint32_t i = 0; i < 8; ++i) {
+        const uint32_t t = i * 4 + (lane >> 3);
+        if (t < n && !(ep.dbg & 32)) {
+            const float4 nv = f4add(xo[i], v[i]);
+            *reinterpret_cast<float4*>(ep.x + (size_t)(tb + t) * ep.ldx + c) = nv;
+            if (ep.xb) {
+                __nv_bfloat162 lo = __floats2bfloat162_rn(nv.x, nv.y), hi = __floats2bfloat162_rn(nv.z, nv.w);
+                uint2 pk;
+                pk.x = *reinterpret_cast<uint32_t*>(&lo);
+                pk.y = *reinterpret_cast<uint32_t*>(&hi);
+                *reinterpret_cast<uint2*>(ep.xb + (size_t)(tb + t) * ep.ldx + c) = pk;
+            }
+        }
+    }
+}
+
 template <int MODE>
 __device__ __forceinline__ void pg_epi(const EpiParams& ep, uint32_t M, uint32_t tb, uint32_t f, uint32_t lane,
                                        const uint32_t (&r)[32], const uint32_t* s_rows, const float2* s_rope,
-                                       uint32_t tg) {
+                                       uint32_t tg, uint8_t* stg = nullptr) {
     const uint32_t n = min(32u, M - tb);  // valid tokens in this chunk
+    if (stg) {
+        __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(stg);
+        const uint32_t f0 = f - lane;  // the warp's first feature
+        if constexpr (MODE == EPI_RESID) {
+            float* sf = reinterpret_cast<float*>(stg);
+            stage_put_f32(sf, lane, r);
+            resid_rows(ep, n, tb, f0, lane, [&](uint32_t i) {
+                return *reinterpret_cast<const float4*>(sf + (i * 4 + (lane >> 3)) * 32 + (lane & 7) * 4);
+            });
+        } else if constexpr (MODE == EPI_STORE_F32) {
+            float* sf = reinterpret_cast<float*>(stg);
+#pragma unroll
+            for (uint32_t j = 0; j < 32; ++j) sf[j * 32 + lane] = __uint_as_float(r[j]);
+            __syncwarp();
+            float* o = static_cast<float*>(ep.out) + f0 + (lane & 7) * 4;
+#pragma unroll
+            for (uint32_t i = 0; i < 8; ++i) {
+                const uint32_t t = i * 4 + (lane >> 3);
+                const float4 v = *reinterpret_cast<const float4*>(sf + t * 32 + (lane & 7) * 4);
+                if (t < n) *reinterpret_cast<float4*>(o + (size_t)(tb + t) * ep.ldo) = v;
+            }
+        } else if constexpr (MODE == EPI_QKV) {
+            const uint32_t h = ep.hidden, part = f0 / h, d0 = f0 - part * h;
+            const uint32_t hd2 = ep.head_dim >> 1, pr = ((f - part * h) % ep.head_dim) >> 1;
+            const bool odd = lane & 1;
+#pragma unroll
+            for (uint32_t j0 = 0; j0 < 32; j0 += 16) {
+                float2 cs[16];
+                if (part < 2) {
+#pragma unroll
+                    for (uint32_t j = 0; j < 16; ++j) {
+                        const uint32_t t = min(tb + j0 + j, M - 1);
+                        cs[j] = s_rope ? s_rope[(t - tg) * hd2 + pr]
+                                       : ep.rope_tok ? __ldg(ep.rope_tok + (size_t)t * hd2 + pr)
+                                                     : __ldg(ep.rope + (size_t)__ldg(ep.rope_pos + t) * hd2 + pr);
+                    }
+                }
+#pragma unroll
+                for (uint32_t j = 0; j < 16; ++j) {
+                    float val = __uint_as_float(r[j0 + j]);
+                    if (part < 2) {  // warp-uniform
+                        const float vp = __shfl_xor_sync(0xffffffffu, val, 1);
+                        float x0 = odd ? vp : val, x1 = odd ? val : vp;
+                        rope_pair(x0, x1, cs[j].x, cs[j].y);
+                        val = odd ? x1 : x0;
+                    }
+                    stage_put_bf16(sb, j0 + j, lane, __float2bfloat16_rn(val));
+                }
+            }
+            __syncwarp();
+            __nv_bfloat16* base = static_cast<__nv_bfloat16*>(part == 0 ? ep.q : part == 1 ? ep.kv_k : ep.kv_v) + d0 +
+                                  (lane & 3) * 8;
+#pragma unroll
+            for (uint32_t i = 0; i < 4; ++i) {
+                const uint32_t t = i * 8 + (lane >> 2);
+                const uint4 v = stage_get_bf16(sb, i, lane);
+                if (t < n) {
+                    const uint32_t tt = tb + t;
+                    const uint32_t row = part == 0 ? tt : s_rows ? s_rows[tt - tg] : __ldg(ep.kv_rows + tt);
+                    *reinterpret_cast<uint4*>(base + (size_t)row * h) = v;
+                }
+            }
+        } else {  // EPI_STORE / EPI_GELU
+#pragma unroll
+            for (uint32_t j = 0; j < 32; ++j) {
+                const float v = __uint_as_float(r[j]);
+                stage_put_bf16(sb, j, lane, __float2bfloat16_rn(MODE == EPI_GELU ? gelu_fast(v) : v));
+            }
+            __syncwarp();
+            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + f0 + (lane & 3) * 8;
+#pragma unroll
+            for (uint32_t i = 0; i < 4; ++i) {
+                const uint32_t t = i * 8 + (lane >> 2);
+                const uint4 v = stage_get_bf16(sb, i, lane);
+                if (t < n) *reinterpret_cast<uint4*>(o + (size_t)(tb + t) * ep.ldo) = v;
+            }
+        }
+        __syncwarp();  // the slice is rewritten by the next chunk
+        return;
+    }
     if constexpr (MODE == EPI_QKV) {
         // linker.cpp:64-78 — q/k rotated at their position (interleaved pairs live on
         // adjacent lanes), k/v scattered to the cache row kv_rows[t]
@@ -190,19 +341,9 @@ __device__ __forceinline__ void pg_epi(const EpiParams& ep, uint32_t M, uint32_t
     }
 }
 
-__device__ __forceinline__ void pg_epilogue(const EpiParams& ep, uint32_t M, uint32_t tb, uint32_t f,
-                                            uint32_t lane, const uint32_t (&r)[32],
-                                            const uint32_t* s_rows = nullptr, const float2* s_rope = nullptr,
-                                            uint32_t tg = 0) {
-    switch (ep.mode) {
-        case EPI_QKV: pg_epi<EPI_QKV>(ep, M, tb, f, lane, r, s_rows, s_rope, tg); break;
-        case EPI_RESID: pg_epi<EPI_RESID>(ep, M, tb, f, lane, r, s_rows, s_rope, tg); break;
-        case EPI_GELU: pg_epi<EPI_GELU>(ep, M, tb, f, lane, r, s_rows, s_rope, tg); break;
-        case EPI_STORE_F32: pg_epi<EPI_STORE_F32>(ep, M, tb, f, lane, r, s_rows, s_rope, tg); break;
-        default: pg_epi<EPI_STORE>(ep, M, tb, f, lane, r, s_rows, s_rope, tg);
-    }
-}
-
+// One instantiation per epilogue mode: the kernel's epilogue runs once, at the end, from a
+// cold instruction cache, so each instantiation carries only its own (unrolled) epilogue.
+template <int MODE>
 __global__ void __launch_bounds__(kPgThreads, 1)
     tc_pgemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX0,
                     const __grid_constant__ CUtensorMap tmX1, const PgArgs a) {
@@ -218,6 +359,8 @@ __global__ void __launch_bounds__(kPgThreads, 1)
     tc::pdl_trigger();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t crank = tc::cluster_ctarank();
+    unsigned long long* ts = a.ts && blockIdx.x == 0 ? a.ts : nullptr;  // diagnostics
+    if (ts && threadIdx.x == 0) ts[0] = gtimer();
     const uint32_t rank = crank & 1;          // CTA within the pair
     const uint32_t split = crank >> 1;        // pair within the cluster = K split
     const uint32_t cl = blockIdx.x / (2 * a.S);
@@ -252,6 +395,7 @@ __global__ void __launch_bounds__(kPgThreads, 1)
     tc::cluster_sync();
     tc::tc_fence_after();
     tc::pdl_wait();  // the previous kernel's outputs (this GEMM's X, its output buffers) are ready
+    if (ts && threadIdx.x == 0) ts[1] = gtimer();
     const uint32_t tmem = *tmem_holder;
 
     if (warp == 0) {
@@ -261,6 +405,8 @@ __global__ void __launch_bounds__(kPgThreads, 1)
             const uint32_t xbytes = (a.dbg & 2) ? 0u : a.sub_bytes - kPgWBytes;
             const uint32_t wbytes = (a.dbg & 4) ? 0u : kPgWBytes;
             const int xr0 = (int)(rank * (a.P0 / 2)), xr1 = (int)(a.P0 + rank * (a.P1 / 2));
+            long long pw = 0;
+            const long long p0 = clock64();
             const uint32_t leader_full = tc::mapa_shared(tc::smem_u32(full), crank & ~1u);
             uint32_t s = 0, ph = 0;
             for (uint32_t tile = cl; tile < a.tiles; tile += a.clusters) {
@@ -268,7 +414,9 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                 const int t0 = (int)(g * a.G), w_row = (int)(fb * 256 + rank * 128);
                 for (uint32_t kb = kb0; kb < kb1; kb += a.kps) {
                     const uint32_t nsub = min(a.kps, kb1 - kb);
+                    const long long w0 = ts ? clock64() : 0;
                     tc::mbar_wait(&empty[s], ph ^ 1);
+                    if (ts) pw += clock64() - w0;
                     if (rank == 0) tc::mbar_arrive_expect_tx(&full[s], 2 * nsub * (xbytes + wbytes));
                     const uint32_t bar = leader_full + s * 8;
                     for (uint32_t j = 0; j < nsub; ++j) {
@@ -281,11 +429,29 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                             else
                                 tc::tma_load_2d_cg2(st, &tmW, bar, k, w_row, pol_w);
                         }
+                        if (a.pfd) {
+                            // keep the weight stream pfd k-blocks ahead of the smem ring in L2
+                            // (DRAM latency hidden without spending shared memory on it);
+                            // crosses into this cluster's next tile
+                            uint32_t kp = kb + j + a.pfd, fp = fb;
+                            if (kp >= kb1 && tile + a.clusters < a.tiles) {
+                                kp = kb0 + (kp - kb1);
+                                fp = (tile + a.clusters) / a.ngroups;
+                            }
+                            if (kp < kb1 && (fp != fb || kp > kb + j))
+                                tc::tma_prefetch_2d(&tmW, a.w_blocked ? 0 : (int)(kp * 64),
+                                                    a.w_blocked ? (int)(((2 * fp + rank) * a.kblocks + kp) * 128)
+                                                                : (int)(fp * 256 + rank * 128));
+                        }
                         if (xbytes) tc::tma_load_2d_cg2(st + kPgWBytes, &tmX0, bar, k, t0 + xr0, pol_x);
                         if (xbytes && a.P1) tc::tma_load_2d_cg2(st + kPgWBytes + a.xoff1, &tmX1, bar, k, t0 + xr1, pol_x);
                     }
                     if (++s == a.stages) { s = 0; ph ^= 1; }
                 }
+            }
+            if (ts) {
+                ts[5] = pw;
+                ts[6] = clock64() - p0;
             }
         }
         __syncwarp();
@@ -294,6 +460,8 @@ __global__ void __launch_bounds__(kPgThreads, 1)
             const uint32_t idesc0 = tc::idesc_bf16(256, a.P0);
             const uint32_t idesc1 = tc::idesc_bf16(256, a.P1 ? a.P1 : 16);
             uint32_t item = 0, s = 0, ph = 0;
+            long long mw = 0;
+            const long long m0 = clock64();
             for (uint32_t tile = cl; tile < a.tiles; tile += a.clusters, ++item) {
                 const uint32_t b = a.nbuf == 2 ? (item & 1) : 0u;
                 const uint32_t use = a.nbuf == 2 ? (item >> 1) : item;
@@ -302,7 +470,9 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                 const uint32_t d = tmem + b * a.G;
                 for (uint32_t kb = kb0; kb < kb1; kb += a.kps) {
                     const uint32_t nsub = min(a.kps, kb1 - kb);
+                    const long long w0 = ts ? clock64() : 0;
                     tc::mbar_wait(&full[s], ph);
+                    if (ts) mw += clock64() - w0;
                     tc::tc_fence_after();
                     for (uint32_t j = 0; j < nsub && !(a.dbg & 8); ++j) {
                         const uint32_t w_base = tc::smem_u32(smem + s * a.stage_bytes + j * a.sub_bytes);
@@ -321,6 +491,11 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                     if (++s == a.stages) { s = 0; ph ^= 1; }
                 }
                 tc::mma_commit_pair_mcast(&acc_full[b], pair_mask);
+                if (ts) ts[2] = gtimer();
+            }
+            if (ts) {
+                ts[7] = mw;
+                ts[8] = clock64() - m0;
             }
         }
         __syncwarp();
@@ -340,8 +515,10 @@ __global__ void __launch_bounds__(kPgThreads, 1)
             const uint32_t tend = min(a.M, tg + a.G);  // tokens of this group: [tg, tend)
             const uint32_t b = a.nbuf == 2 ? (item & 1) : 0u;
             const uint32_t use = a.nbuf == 2 ? (item >> 1) : item;
+            if (ts && row == 0 && half == 0) ts[11] = gtimer();
             tc::mbar_wait(&acc_full[b], use & 1);
             tc::tc_fence_after();
+            if (ts && row == 0 && half == 0) ts[12] = gtimer();
             const uint32_t dcol = tmem + lane_off + b * a.G;
             if (a.S == 1) {
                 // QKV with one tile per pair: every MMA has retired, so the idle stage buffers
@@ -361,22 +538,41 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                     s_rope = reinterpret_cast<const float2*>(smem);
                     s_rows = reinterpret_cast<const uint32_t*>(smem + a.rows_off);
                 }
+                long long c_ld = 0, c_epi = 0;
                 if (!(a.dbg & 1))
                     for (uint32_t c = half * 32; c < a.G && tg + c < tend; c += 64) {
                         uint32_t r[32];
+                        const long long q0 = ts ? clock64() : 0;
                         tc::tmem_ld32(dcol + c, r);
                         tc::tmem_ld_wait();
-                        pg_epilogue(a.ep, tend, tg + c, f, lane, r, s_rows, s_rope, tg);
+                        const long long q1 = ts ? clock64() : 0;
+                        pg_epi<MODE>(a.ep, tend, tg + c, f, lane, r, s_rows, s_rope, tg,
+                                     a.stg_off == kNoStage ? nullptr : smem + a.stg_off + (warp - 2) * kStageSlice);
+                        if (ts) {
+                            c_ld += q1 - q0;
+                            c_epi += clock64() - q1;
+                        }
                     }
+                if (ts && row == 0 && half == 0) {
+                    ts[9] = c_ld;
+                    ts[10] = c_epi;
+                }
             } else {
                 // in-cluster split-K (one tile per cluster): chunk j (32 tokens) belongs to split
                 // j % S. Every MMA of every pair has completed once all CTAs pass this barrier,
                 // so the stage buffers are free to receive [src split][j / S][32 cols][128 rows].
                 tc::cluster_arrive();
                 tc::cluster_wait();
+                const bool tsw = ts && row == 0 && half == 0;
+                if (tsw) ts[13] = gtimer();
                 const uint32_t nchunks = (a.G + 31) / 32;
                 const uint32_t per = (nchunks + a.S - 1) / a.S;
-                const uint32_t recv = tc::smem_u32(smem) + split * per * kChunkBytes + row * 4;
+                // receive slot [src split][j / S] = [32 tokens][128 features] fp32. Nobody sends
+                // to this CTA's own split slots: they hold the warps' 4 KB transpose slices.
+                float* stg = per * kChunkBytes >= 8 * kStageSlice
+                                 ? reinterpret_cast<float*>(smem + split * per * kChunkBytes + (warp - 2) * kStageSlice)
+                                 : nullptr;
+                const uint32_t recv = tc::smem_u32(smem) + split * per * kChunkBytes;
                 for (uint32_t j = half; j < nchunks; j += 2) {
                     const uint32_t owner = j % a.S;
                     if (owner == split) continue;
@@ -384,16 +580,58 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                     tc::tmem_ld32(dcol + j * 32, r);
                     tc::tmem_ld_wait();
                     const uint32_t dst = tc::mapa_shared(recv + (j / a.S) * kChunkBytes, 2 * owner + rank);
+                    if (stg) {  // 16-B remote stores, 4 token rows per instruction
+                        stage_put_f32(stg, lane, r);
 #pragma unroll
-                    for (uint32_t i = 0; i < 32; ++i) tc::st_cluster_f32(dst + i * 512, r[i]);
+                        for (uint32_t i = 0; i < 8; ++i) {
+                            const uint32_t t = i * 4 + (lane >> 3), c = q * 32 + (lane & 7) * 4;
+                            tc::st_cluster_v4(dst + t * 512 + c * 4,
+                                              *reinterpret_cast<const float4*>(stg + t * 32 + (lane & 7) * 4));
+                        }
+                        __syncwarp();
+                    } else {
+#pragma unroll
+                        for (uint32_t i = 0; i < 32; ++i) tc::st_cluster_f32(dst + i * 512 + row * 4, r[i]);
+                    }
                 }
+                if (tsw) ts[14] = gtimer();
                 tc::cluster_arrive();  // release: the pushed chunks are visible after the wait
                 tc::cluster_wait();
+                if (tsw) ts[15] = gtimer();
+                long long o_tm = 0, o_st = 0, o_rs = 0;
                 for (uint32_t j = split + half * a.S; j < nchunks; j += 2 * a.S) {
                     if (a.dbg & 1) break;
                     uint32_t r[32];
+                    const long long z0 = ts ? clock64() : 0;
                     tc::tmem_ld32(dcol + j * 32, r);
                     tc::tmem_ld_wait();
+                    const long long z1 = ts ? clock64() : 0;
+                    o_tm += z1 - z0;
+                    if (MODE == EPI_RESID && stg) {
+                        // sum in split order (deterministic) in the transposed layout, then the
+                        // residual update with 16-B accesses
+                        stage_put_f32(stg, lane, r);
+                        const long long z2 = ts ? clock64() : 0;
+                        o_st += z2 - z1;
+                        const uint32_t tb = tg + j * 32;
+                        const uint32_t n = tb < tend ? min(32u, tend - tb) : 0u;
+                        const uint32_t own = tc::smem_u32(stg) + (lane >> 3) * 128 + (lane & 7) * 16;
+                        const uint32_t oth = tc::smem_u32(smem) + (j / a.S) * kChunkBytes + (lane >> 3) * 512 +
+                                             (q * 32 + (lane & 7) * 4) * 4;
+                        resid_rows(a.ep, n, tb, f - lane, lane, [&](uint32_t i) {
+                            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                            for (uint32_t s2 = 0; s2 < 4; ++s2) {
+                                if (s2 >= a.S) break;
+                                const uint32_t addr = s2 == split ? own + i * 512 : oth + s2 * per * kChunkBytes + i * 2048;
+                                v = f4add(v, tc::ld_shared_v4(addr));
+                            }
+                            return v;
+                        });
+                        __syncwarp();
+                        if (ts) o_rs += clock64() - z2;
+                        continue;
+                    }
                     float v[32];
 #pragma unroll
                     for (uint32_t i = 0; i < 32; ++i) v[i] = 0.0f;
@@ -410,14 +648,20 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                     if (tg + j * 32 < tend) {
 #pragma unroll
                         for (uint32_t i = 0; i < 32; ++i) r[i] = __float_as_uint(v[i]);
-                        pg_epilogue(a.ep, tend, tg + j * 32, f, lane, r);
+                        pg_epi<MODE>(a.ep, tend, tg + j * 32, f, lane, r, nullptr, nullptr, 0);
                     }
+                }
+                if (tsw) {
+                    ts[9] = o_tm;
+                    ts[10] = o_st;
+                    ts[12] = o_rs;
                 }
             }
             // release the accumulator to the pair's MMA issuer (one arrive per warp)
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive_remote(acc_empty_leader + b * 8);
+            if (ts && row == 0 && half == 0) ts[3] = gtimer();
         }
     }
     if (a.S > 1 && warp < 2) {  // the producer / MMA warps take part in the reduction barriers
@@ -430,9 +674,21 @@ __global__ void __launch_bounds__(kPgThreads, 1)
     tc::cluster_sync();
     tc::tc_fence_after();
     if (warp == 1) tc::tmem_dealloc_pair(tmem, a.tmem_cols);
+    if (ts && threadIdx.x == 0) ts[4] = gtimer();
 }
 
 uint32_t round16(uint32_t x) { return (x + 15) / 16 * 16; }
+
+using PgKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, PgArgs);
+PgKernel pg_kernel(int mode) {
+    switch (mode) {
+        case EPI_QKV: return tc_pgemm_kernel<EPI_QKV>;
+        case EPI_RESID: return tc_pgemm_kernel<EPI_RESID>;
+        case EPI_GELU: return tc_pgemm_kernel<EPI_GELU>;
+        case EPI_STORE_F32: return tc_pgemm_kernel<EPI_STORE_F32>;
+        default: return tc_pgemm_kernel<EPI_STORE>;
+    }
+}
 
 // Largest number of co-resident clusters of `size` CTAs at this kernel's footprint.
 uint32_t max_clusters(uint32_t size, size_t smem) {
@@ -453,7 +709,7 @@ uint32_t max_clusters(uint32_t size, size_t smem) {
         cfg.attrs = at;
         cfg.numAttrs = 1;
         int n = 0;
-        MPIC_CUDA(cudaOccupancyMaxActiveClusters(&n, tc_pgemm_kernel, &cfg));
+        MPIC_CUDA(cudaOccupancyMaxActiveClusters(&n, pg_kernel(EPI_STORE), &cfg));
         v = (uint32_t)std::max(1, n);
     }
     return v;
@@ -463,6 +719,15 @@ uint32_t max_clusters(uint32_t size, size_t smem) {
 
 bool pgemm_supported(uint32_t M, uint32_t N, uint32_t K) {
     return M > 0 && N % 256 == 0 && K % 64 == 0 && K >= 64;
+}
+
+static unsigned long long* g_ts_buf = nullptr;
+void pgemm_timestamps(unsigned long long* out9) {
+    if (!g_ts_buf) {
+        for (int i = 0; i < 16; ++i) out9[i] = 0;
+        return;
+    }
+    MPIC_CUDA(cudaMemcpy(out9, g_ts_buf, 16 * 8, cudaMemcpyDeviceToHost));
 }
 
 void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint32_t N, uint32_t K,
@@ -492,8 +757,10 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
     }();
     static std::once_flag once;
     std::call_once(once, [] {
-        MPIC_CUDA(cudaFuncSetAttribute(tc_pgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        MPIC_CUDA(cudaFuncSetAttribute(tc_pgemm_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        for (int m : {EPI_STORE, EPI_QKV, EPI_RESID, EPI_GELU, EPI_STORE_F32}) {
+            MPIC_CUDA(cudaFuncSetAttribute(pg_kernel(m), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            MPIC_CUDA(cudaFuncSetAttribute(pg_kernel(m), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        }
     });
     PgArgs best_a{};
     double best = 1e30;
@@ -544,6 +811,7 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
         if (a.stages < 2) continue;
         a.w_evict_first = a.ngroups == 1;
         a.ep = ep_in;
+    a.ep.dbg = dbg;
         const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 5) * 8 + 16;
         const uint32_t nchunks = (a.G + 31) / 32;
         // MMA cycles per k-block (4 k16 steps): a cta_group::2 instruction costs
@@ -570,7 +838,22 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
     }
     MPIC_REQUIRE(best < 1e29, MPIC_ERR_VALIDATION, "pair gemm: no feasible tiling");
     PgArgs a = best_a;
+    static unsigned long long* ts_buf = [] {
+        unsigned long long* b = nullptr;
+        if (getenv("MPIC_PG_TS")) {
+            cudaMalloc(&b, 128);
+            cudaMemset(b, 0, 128);
+        }
+        return b;
+    }();
+    a.ts = ts_buf;
+    g_ts_buf = ts_buf;
     a.w_blocked = w_blocked ? 1u : 0u;
+    static const int pfd_env = [] {
+        const char* e = getenv("MPIC_PG_PFD");  // diagnostics: weight L2 prefetch distance (k-blocks)
+        return e ? atoi(e) : -1;
+    }();
+    a.pfd = pfd_env >= 0 ? (uint32_t)pfd_env : 2 * a.stages * a.kps;
 
     const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 5) * 8 + 16;
     static const bool verbose = getenv("MPIC_PG_VERBOSE") != nullptr;
@@ -582,6 +865,16 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
         a.rows_off = (rope_bytes + 1023) & ~1023u;
         a.stage_rope = a.rows_off + a.G * 4 + 16 <= a.stages * a.stage_bytes;
     }
+    static const bool staged_env = [] {
+        const char* e = getenv("MPIC_PG_STAGED");  // diagnostics: 0 = direct (narrow) epilogue stores
+        return !e || atoi(e) != 0;
+    }();
+    a.stg_off = kNoStage;
+    if (staged_env && a.S == 1 && a.clusters >= a.tiles) {
+        // one tile per cluster: the stage ring is idle once the accumulator is complete
+        const uint32_t off = a.stage_rope ? (a.rows_off + a.G * 4 + 16 + 1023) & ~1023u : 0u;
+        if (off + 8 * kStageSlice <= a.stages * a.stage_bytes) a.stg_off = off;
+    }
     const CUtensorMap tmW = w_blocked ? make_tmap_bf16(W, 64, (uint64_t)N * a.kblocks, 64, 128)
                                       : make_tmap_bf16(W, K, N, 64, 128);
     const CUtensorMap tmX0 = make_tmap_bf16(A, K, M, 64, a.P0 / 2);
@@ -591,16 +884,18 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
     cfg.blockDim = dim3(kPgThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[3];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2 * a.S;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    at[2].id = cudaLaunchAttributePriority;
+    at[2].val.priority = hot_priority();
     cfg.attrs = at;
-    cfg.numAttrs = 2;
-    MPIC_CUDA(cudaLaunchKernelEx(&cfg, tc_pgemm_kernel, tmW, tmX0, tmX1, a));
+    cfg.numAttrs = 3;
+    MPIC_CUDA(cudaLaunchKernelEx(&cfg, pg_kernel(a.ep.mode), tmW, tmX0, tmX1, a));
     MPIC_LAUNCHED();
 }
 

@@ -302,20 +302,24 @@ def test_reference_suites_on_b200_library(suite):
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
 
 
-def test_request_prefill_host_bf16_tier(g):
+@pytest.mark.parametrize("img,text0", [(192, 21), (448, 21), (448, 150), (700, 300)])
+def test_request_prefill_host_bf16_tier(g, img, text0):
     """The model-dtype Host tier: bf16 chunk bits in pinned memory streamed by the loader give
-    exactly the logits and cache of the same chunks resident in HBM (both are RNE(fp32))."""
+    exactly the logits and cache of the same chunks resident in HBM (both are RNE(fp32)).
+    With images longer than 2 x 128 rows the HBM-resident request links inside attention
+    (chunk blocks read in place and stored by their writer item, 1-3 query tiles) while the
+    Host tier assembles every row: the caches must still be bit-identical."""
     L, H, D = 2, 8, 128
-    cfg = mp.config(L, H, D, vocab_size=4096, image_token_count=192, seed=9)
+    cfg = mp.config(L, H, D, vocab_size=4096, image_token_count=img, seed=9)
     m = mp.Model(cfg, mp.BF16)
     rng = np.random.default_rng(3)
-    segs = [("text", rng.integers(0, 4095, 21).tolist()), ("image", rng.bytes(32), 192),
-            ("text", rng.integers(0, 4095, 30).tolist()), ("image", rng.bytes(32), 192),
+    segs = [("text", rng.integers(0, 4095, text0).tolist()), ("image", rng.bytes(32), img),
+            ("text", rng.integers(0, 4095, 30).tolist()), ("image", rng.bytes(32), img),
             ("text", rng.integers(0, 4095, 9).tolist())]
     p = mp.Prompt.from_segments(segs)
-    chunks = [(rng.random((L, 192, H * D), dtype=np.float32) - 0.5,
-               rng.random((L, 192, H * D), dtype=np.float32) - 0.5) for _ in range(2)]
-    ws = mp.Workspace(m, 128, p.n)
+    chunks = [(rng.random((L, img, H * D), dtype=np.float32) - 0.5,
+               rng.random((L, img, H * D), dtype=np.float32) - 0.5) for _ in range(2)]
+    ws = mp.Workspace(m, 512, p.n)
     dev = [mp.KV.from_host(k, v, H, D, mp.BF16) for k, v in chunks]
     linked_d = mp.KV(L, p.n, H, D, mp.BF16)
     ref_logits, ref_sel = mp.request_prefill(m, ws, p, dev, linked_d, k=32)

@@ -31,7 +31,7 @@ __global__ void __cluster_dims__(2, 1, 1) probe(unsigned long long* out, int n0,
         const uint32_t id0 = tc::idesc_bf16(256, n0), id1 = tc::idesc_bf16(256, n1 ? n1 : 16);
         const unsigned long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
-            if (mode & 2) { tc::mbar_wait(&bar, 1); tc::tc_fence_after(); }  // a completed phase: returns at once
+            if (mode & 2) { tc::mbar_wait(&bar, 1); if (!(mode & 4)) tc::tc_fence_after(); }  // a completed phase: returns at once
             for (int k = 0; k < 4; ++k) {
                 tc::mma_bf16_pair(tmem, tc::desc_k_sw128(a + k * 32), tc::desc_k_sw128(b + k * 32), id0, 1);
                 if (n1) tc::mma_bf16_pair(tmem + n0, tc::desc_k_sw128(a + k * 32), tc::desc_k_sw128(b + n0 * 64 + k * 32), id1, 1);
@@ -55,8 +55,8 @@ int main() {
     unsigned long long* d;
     cudaMalloc(&d, pairs * 8);
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    int shapes[][2] = {{176, 160}, {176, 0}, {256, 0}, {96, 0}};
-    for (int mode = 0; mode < 4; ++mode)
+    int shapes[][2] = {{176, 160}, {128, 128}, {96, 0}};
+    for (int mode : {1, 2, 3, 6, 7})
     for (auto& sh : shapes) {
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -71,7 +71,7 @@ int main() {
         double cyc = 0; for (int i = 0; i < pairs; ++i) cyc += h[i]; cyc /= pairs;
         const int N = sh[0] + sh[1];
         const double flops = 2.0 * 256 * N * 16 * 4 * iters * pairs;
-        printf("mode %d (1 commit/kblock, 2 wait/kblock) N=%3d+%3d: %.1f cyc per k-block (ideal %d), %.0f TFLOP/s chip, err=%s\n",
+        printf("mode %d (1 commit/kblock, 2 wait/kblock, 4 no fence) N=%3d+%3d: %.1f cyc per k-block (ideal %d), %.0f TFLOP/s chip, err=%s\n",
                mode, sh[0], sh[1], cyc / iters, 2 * N, flops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
     }
 }
