@@ -249,12 +249,19 @@ Workspace::Workspace(const DeviceModel& m, uint32_t rows, uint32_t ctx) : rows_(
 }
 
 namespace {
+// Identity of a host model's weights for the device-model cache: every tensor's buffer
+// address and size plus a strided sample of its values (O(1) per call: hashing every weight
+// cost ~1 ms per request even for a toy model and scales with the model size).
 uint64_t weight_hash(const Model& m) {
     uint64_t acc = 0x9e3779b97f4a7c15ull ^ m.config.fingerprint();
+    auto mix = [&](uint64_t v) { acc = (acc ^ v) * 0x100000001b3ull; };
     auto feed = [&](const std::vector<float>& w) {
         const auto* p = reinterpret_cast<const uint32_t*>(w.data());
-        for (size_t i = 0; i < w.size(); ++i) acc = (acc ^ p[i]) * 0x100000001b3ull;
-        acc ^= w.size();
+        mix(reinterpret_cast<uintptr_t>(p));
+        mix(w.size());
+        const size_t n = w.size(), step = std::max<size_t>(1, n / 61);
+        for (size_t i = 0; i < n; i += step) mix(p[i]);
+        if (n) mix(p[n - 1]);
     };
     feed(m.embedding);
     feed(m.lm_head);

@@ -2229,20 +2229,19 @@ int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const
                    static_cast<__nv_bfloat16*>(d_out), s);
     MPIC_CUDA(cudaFreeAsync(buf, s));
     if (unsigned long long* dbg = attn_debug_buffer()) {  // MPIC_ATTN_TS diagnostics
-        std::vector<unsigned long long> h(8 * 64);
+        std::vector<unsigned long long> h(16 * 64);
         MPIC_CUDA(cudaStreamSynchronize(s));
         MPIC_CUDA(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
         MPIC_CUDA(cudaMemset(dbg, 0, h.size() * 8));
         const AttnUnit& u0 = plan.units[0];
         fprintf(stderr, "attn CTA0 item: head %u b0 %u tiles %u/%u b1 %u/%u\n", u0.head, u0.b0, u0.tile[0], u0.tile[1],
                 u0.b1[0], u0.b1[1]);
-        const unsigned long long t0 = h[0];
-        for (int j = 0; j < 64 && h[j * 8]; ++j)
-            fprintf(stderr, "j=%2d start %7.2f v_full %7.2f pA %7.2f pB %7.2f k_next %7.2f | A got S %7.2f max %7.2f A put P %7.2f us\n",
-                    j, (h[j * 8] - t0) / 1e3, (h[j * 8 + 1] - t0) / 1e3, h[j * 8 + 2] ? (h[j * 8 + 2] - t0) / 1e3 : -1.0,
-                    h[j * 8 + 3] ? (h[j * 8 + 3] - t0) / 1e3 : -1.0, h[j * 8 + 4] ? (h[j * 8 + 4] - t0) / 1e3 : -1.0,
-                    ((long long)h[j * 8 + 5] - (long long)t0) / 1e3, ((long long)h[j * 8 + 7] - (long long)t0) / 1e3,
-                    ((long long)h[j * 8 + 6] - (long long)t0) / 1e3);
+        const long long t0 = (long long)h[0];
+        auto at = [&](int j, int k) { return h[j * 16 + k] ? ((long long)h[j * 16 + k] - t0) / 1e3 : -1.0; };
+        for (int j = 0; j < 64 && h[j * 16]; ++j)
+            fprintf(stderr, "j=%2d MMA: start %6.2f v_full %6.2f pA %6.2f pB %6.2f k_next %6.2f | softmax A: S %6.2f "
+                            "loaded %6.2f max %6.2f exps %6.2f P %6.2f us\n",
+                    j, at(j, 0), at(j, 1), at(j, 2), at(j, 3), at(j, 4), at(j, 5), at(j, 8), at(j, 7), at(j, 9), at(j, 6));
     }
     API_END
 }

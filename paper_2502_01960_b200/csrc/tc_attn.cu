@@ -248,15 +248,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             for (uint32_t j = 0; j < nbmax; ++j) {
                 const uint32_t st = j % kVStages, ph = (j / kVStages) & 1;
                 const bool nxt = j + 1 < nbmax;
-                if (p.dbg && blockIdx.x == 0) p.dbg[j * 8 + 0] = globaltimer_ns();
+                if (p.dbg && blockIdx.x == 0) p.dbg[j * 16 + 0] = globaltimer_ns();
                 tc::mbar_wait(&v_full[st], ph);
-                if (p.dbg && blockIdx.x == 0) p.dbg[j * 8 + 1] = globaltimer_ns();
+                if (p.dbg && blockIdx.x == 0) p.dbg[j * 16 + 1] = globaltimer_ns();
                 bool k_ready = false;
 #pragma unroll
                 for (uint32_t x = 0; x < 2; ++x) {
                     if (j >= nbx[x]) continue;
                     tc::mbar_wait(&p_full[x], j & 1);
-                    if (p.dbg && blockIdx.x == 0) p.dbg[j * 8 + 2 + x] = globaltimer_ns();
+                    if (p.dbg && blockIdx.x == 0) p.dbg[j * 16 + 2 + x] = globaltimer_ns();
                     tc::tc_fence_after();
                     const uint32_t va = tc::smem_u32(sV + st * kTile);
 #pragma unroll
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     if (j + 1 < nbx[x]) {
                         if (!k_ready) {
                             tc::mbar_wait(&k_full[(j + 1) % kKStages], ((j + 1) / kKStages) & 1);
-                            if (p.dbg && blockIdx.x == 0) p.dbg[j * 8 + 4] = globaltimer_ns();
+                            if (p.dbg && blockIdx.x == 0) p.dbg[j * 16 + 4] = globaltimer_ns();
                             tc::tc_fence_after();
                             k_ready = true;
                         }
@@ -339,33 +339,62 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 const uint32_t k0 = (u.b0 + j) * 128u;
                 tc::mbar_wait(&s_full[x], j & 1);
                 const bool dbg_me = p.dbg && blockIdx.x == 0 && x == 0 && r == 0;
-                if (dbg_me) p.dbg[j * 8 + 5] = globaltimer_ns();
+                if (dbg_me) p.dbg[j * 16 + 5] = globaltimer_ns();
                 tc::tc_fence_after();
-                // the row's 128 scores, one TMEM round trip (the softmax warpgroups hold 224
-                // registers each after setmaxnreg); keys past the row's position (or an invalid
-                // row) contribute nothing
+                // keys [0, nv) of the block are visible to this row (causal limit = the row's
+                // position; an invalid row sees none). Selected rows are scattered over the
+                // prompt, so a warp often sees few or none of a block's keys: chunks of 32 keys
+                // no lane of the warp sees are neither loaded nor exponentiated (P = 0), and a
+                // warp that sees nothing just writes P = 0.
+                const uint32_t nv = !valid || limit < k0 ? 0u : min(limit - k0 + 1u, 128u);
+                const uint32_t nv_max = __reduce_max_sync(0xffffffffu, nv);
+                const uint32_t nv_min = __reduce_min_sync(0xffffffffu, nv);
+                if (nv_max == 0) {
+                    uint32_t z[16];
+#pragma unroll
+                    for (uint32_t e = 0; e < 16; ++e) z[e] = 0u;
+#pragma unroll
+                    for (uint32_t c = 0; c < 4; ++c) tc::tmem_st16(s_col + c * 16, z);
+                    tc::tmem_st_wait();
+                    tc::tc_fence_before();
+                    tc::mbar_arrive(&p_full[x]);
+                    continue;
+                }
+                const uint32_t nch = (nv_max + 31) >> 5;  // warp-uniform
+                // the row's scores, one TMEM round trip (the softmax warpgroups hold 224
+                // registers each after setmaxnreg)
                 uint32_t v[4][32];
                 tc::tmem_ld32(s_col, v[0]);
-                tc::tmem_ld32(s_col + 32, v[1]);
-                tc::tmem_ld32(s_col + 64, v[2]);
-                tc::tmem_ld32(s_col + 96, v[3]);
+                if (nch > 1) tc::tmem_ld32(s_col + 32, v[1]);
+                if (nch > 2) tc::tmem_ld32(s_col + 64, v[2]);
+                if (nch > 3) tc::tmem_ld32(s_col + 96, v[3]);
                 tc::tmem_ld_wait();
-                const bool masked = __any_sync(0xffffffffu, !valid || k0 + 127 > limit);
-                if (masked) {
+                if (dbg_me) p.dbg[j * 16 + 8] = globaltimer_ns();
 #pragma unroll
-                    for (uint32_t e = 0; e < 128; ++e)
-                        if (!valid || k0 + e > limit) v[e >> 5][e & 31] = __float_as_uint(-INFINITY);
+                for (uint32_t c = 0; c < 4; ++c) {
+                    if (c < nch && nv_min < 32 * (c + 1)) {  // a lane's limit falls in this chunk
+#pragma unroll
+                        for (uint32_t e = 0; e < 32; ++e)
+                            if (32 * c + e >= nv) v[c][e] = __float_as_uint(-INFINITY);
+                    }
                 }
                 float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-                for (uint32_t e = 0; e < 32; ++e) {
-                    mx0 = fmaxf(mx0, __uint_as_float(v[0][e]));
-                    mx1 = fmaxf(mx1, __uint_as_float(v[1][e]));
-                    mx2 = fmaxf(mx2, __uint_as_float(v[2][e]));
-                    mx3 = fmaxf(mx3, __uint_as_float(v[3][e]));
+                for (uint32_t e = 0; e < 32; ++e) mx0 = fmaxf(mx0, __uint_as_float(v[0][e]));
+                if (nch > 1) {
+#pragma unroll
+                    for (uint32_t e = 0; e < 32; ++e) mx1 = fmaxf(mx1, __uint_as_float(v[1][e]));
+                }
+                if (nch > 2) {
+#pragma unroll
+                    for (uint32_t e = 0; e < 32; ++e) mx2 = fmaxf(mx2, __uint_as_float(v[2][e]));
+                }
+                if (nch > 3) {
+#pragma unroll
+                    for (uint32_t e = 0; e < 32; ++e) mx3 = fmaxf(mx3, __uint_as_float(v[3][e]));
                 }
                 const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.scale_log2;
-                if (dbg_me) p.dbg[j * 8 + 7] = globaltimer_ns();
+                if (dbg_me) p.dbg[j * 16 + 7] = globaltimer_ns();
                 float alpha = 1.0f;
                 const bool grow = mx > m_used + kRescaleThreshold || (m_used == -INFINITY && mx > -INFINITY);
                 if (grow) {
@@ -398,22 +427,28 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     // give exactly 0. P_X(j) (bf16 pairs) goes to TMEM columns [16c, 16c+16)
                     // of S_X (whose scores are all in registers by now).
                     uint32_t pk[16];
+                    if (c < nch) {
 #pragma unroll
-                    for (uint32_t e = 0; e < 32; e += 2) {
-                        const f2 xs = fma2(mk2(__uint_as_float(v[c][e]), __uint_as_float(v[c][e + 1])), sc2, nm2);
-                        f2 ex;
-                        if ((e & 6) == 6) ex = exp2_poly2(xs);
-                        else ex = mk2(tc::ex2_approx(lo(xs)), tc::ex2_approx(hi(xs)));
-                        lsum = add2(lsum, ex);
-                        pk[e >> 1] = pack_bf16(lo(ex), hi(ex));
+                        for (uint32_t e = 0; e < 32; e += 2) {
+                            const f2 xs = fma2(mk2(__uint_as_float(v[c][e]), __uint_as_float(v[c][e + 1])), sc2, nm2);
+                            f2 ex;
+                            if ((e & 6) == 6) ex = exp2_poly2(xs);
+                            else ex = mk2(tc::ex2_approx(lo(xs)), tc::ex2_approx(hi(xs)));
+                            lsum = add2(lsum, ex);
+                            pk[e >> 1] = pack_bf16(lo(ex), hi(ex));
+                        }
+                    } else {
+#pragma unroll
+                        for (uint32_t e = 0; e < 16; ++e) pk[e] = 0u;
                     }
                     tc::tmem_st16(s_col + c * 16, pk);
                 }
+                if (dbg_me) p.dbg[j * 16 + 9] = globaltimer_ns();
                 const float l0 = lo(lsum), l1 = hi(lsum);
                 l += l0 + l1;
                 tc::tmem_st_wait();
                 tc::tc_fence_before();
-                if (dbg_me) p.dbg[j * 8 + 6] = globaltimer_ns();
+                if (dbg_me) p.dbg[j * 16 + 6] = globaltimer_ns();
                 tc::mbar_arrive(&p_full[x]);
             }
             // ---- epilogue: O / l, or the unnormalised partial + (m, l) for the combine
@@ -575,8 +610,8 @@ unsigned long long* attn_debug_buffer() {
     static unsigned long long* buf = [] {
         unsigned long long* b = nullptr;
         if (getenv("MPIC_ATTN_TS")) {
-            cudaMalloc(&b, 8 * 4096 * sizeof(unsigned long long));
-            cudaMemset(b, 0, 8 * 4096 * sizeof(unsigned long long));
+            cudaMalloc(&b, 16 * 4096 * sizeof(unsigned long long));
+            cudaMemset(b, 0, 16 * 4096 * sizeof(unsigned long long));
         }
         return b;
     }();
