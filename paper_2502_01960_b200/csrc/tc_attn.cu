@@ -109,21 +109,32 @@ __device__ __forceinline__ f2 add2(f2 a, f2 b) {
     return d;
 }
 
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+    f2 d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+    return d;
+}
+
 // 2^x for two x <= 0 on the FMA/ALU pipes only (no F2I/FRND, which share the MUFU pipe):
-// round x with the 1.5*2^23 magic constant, degree-3 fit of 2^f on [-1/2, 1/2] (max rel.
-// error 1.7e-4, below the bf16 rounding P gets next), exponent added in the integer domain.
+// round x with the 1.5*2^23 magic constant (t's low mantissa bits are then round(x)), a
+// degree-3 fit of 2^f on [-1/2, 1/2] (max rel. error 1.7e-4, below the bf16 rounding P gets
+// next), and the exponent added in the integer domain: bits(p) + (bits(t) << 23), since the
+// magic constant's own bits vanish under the shift. ~10 instructions per pair.
 __device__ __forceinline__ f2 exp2_poly2(f2 x) {
     x = mk2(fmaxf(lo(x), -126.0f), fmaxf(hi(x), -126.0f));
-    const f2 magic = mk2(12582912.0f, 12582912.0f), nmagic = mk2(-12582912.0f, -12582912.0f);
+    const f2 magic = mk2(12582912.0f, 12582912.0f);
     const f2 t = add2(x, magic);
-    const f2 j = add2(t, nmagic);
-    const f2 f = add2(x, mk2(-lo(j), -hi(j)));
+    const f2 f = sub2(x, sub2(t, magic));
     f2 p = fma2(mk2(0.05302752f, 0.05302752f), f, mk2(0.24221394f, 0.24221394f));
     p = fma2(p, f, mk2(0.69357257f, 0.69357257f));
     p = fma2(p, f, mk2(1.0f, 1.0f));
-    const int e0 = (__float_as_int(lo(t)) - 0x4B400000) << 23, e1 = (__float_as_int(hi(t)) - 0x4B400000) << 23;
-    return mk2(__int_as_float(__float_as_int(lo(p)) + e0), __int_as_float(__float_as_int(hi(p)) + e1));
+    const uint32_t e0 = __float_as_uint(lo(t)) << 23, e1 = __float_as_uint(hi(t)) << 23;
+    return mk2(__uint_as_float(__float_as_uint(lo(p)) + e0), __uint_as_float(__float_as_uint(hi(p)) + e1));
 }
+
+#ifndef MPIC_POLY_MASK
+#define MPIC_POLY_MASK 0x88u  // exp pairs (of 8) on the FMA pipe: 2 of 8 = 25%
+#endif
 
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -432,7 +443,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                         for (uint32_t e = 0; e < 32; e += 2) {
                             const f2 xs = fma2(mk2(__uint_as_float(v[c][e]), __uint_as_float(v[c][e + 1])), sc2, nm2);
                             f2 ex;
-                            if ((e & 6) == 6) ex = exp2_poly2(xs);
+                            if ((MPIC_POLY_MASK >> ((e >> 1) & 7)) & 1u) ex = exp2_poly2(xs);
                             else ex = mk2(tc::ex2_approx(lo(xs)), tc::ex2_approx(hi(xs)));
                             lsum = add2(lsum, ex);
                             pk[e >> 1] = pack_bf16(lo(ex), hi(ex));

@@ -824,6 +824,10 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
             if (force_s && S != force_s && S != 1) continue;
             if (S > 1 && a.kblocks / S < 2) continue;
             const uint32_t C = max_clusters(2 * S, smem);
+            static const bool vplan = getenv("MPIC_PG_VERBOSE") != nullptr;
+            if (vplan)
+                fprintf(stderr, "  plan G=%u S=%u: max clusters %u, tiles %u, recv %zu of %u B\n", a.G, S, C, a.tiles,
+                        (size_t)S * ceil_div(nchunks, S) * kChunkBytes, a.stages * a.stage_bytes);
             if (S > 1 && (a.tiles > C || (size_t)S * ceil_div(nchunks, S) * kChunkBytes > (size_t)a.stages * a.stage_bytes))
                 continue;
             const double cost = (double)ceil_div(a.tiles, std::min(C, a.tiles)) * ceil_div(a.kblocks, S) * t_kb +
