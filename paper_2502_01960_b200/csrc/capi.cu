@@ -402,7 +402,7 @@ bool plan_attn_link(const std::vector<mpic_chunk_ref>& refs, const uint32_t* sel
     {
         uint32_t t = 0;
         for (uint32_t b = 0; b < nblk; ++b) {
-            while (t + 1 < (m + 127) / 128 && sel[std::min(m, (t + 1) * 128) - 1] / 128 < b) ++t;
+            while (t + 1 < (m + 127) / 128 && sel[attn_tile_last_row(t, m)] / 128 < b) ++t;
             wtile[b] = (uint16_t)t;
         }
     }

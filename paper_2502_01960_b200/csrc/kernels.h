@@ -119,6 +119,12 @@ struct AttnPlan {
 };
 unsigned long long* attn_debug_buffer();
 AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads);
+// Query tiles are right-aligned: tile t holds selected rows [128t - shift, 128(t+1) - shift)
+// with shift = 128 * ceil(m / 128) - m, so only the FIRST tile is partial. Rows are sorted by
+// position, so every tile then ends at an earlier (or the same) row than with left-aligned
+// tiles and needs at most as many key blocks (config C: 149 -> 130 tile-blocks per head).
+inline uint32_t attn_tile_shift(uint32_t m) { return (m + 127) / 128 * 128 - m; }
+inline uint32_t attn_tile_last_row(uint32_t t, uint32_t m) { return (t + 1) * 128 - attn_tile_shift(m) - 1; }
 // Linking inside attention (device-resident bf16 chunks, no re-rotation): 128-key blocks
 // that lie inside one cached chunk and hold no recomputed row are read by the attention
 // kernel straight from the chunk's [L][T_c][h] planes, and the CTA that owns the block for

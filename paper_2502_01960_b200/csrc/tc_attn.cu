@@ -50,6 +50,7 @@ struct AttnParams {
     const AttnUnit* units;
     const uint32_t* rows;
     uint32_t m;
+    uint32_t shift;         // attn_tile_shift(m): tile t starts at selected row 128t - shift
     uint32_t h;
     float scale_log2;       // inv_sqrt_d * log2(e)
     __nv_bfloat16* out;     // [m][h]
@@ -210,7 +211,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #pragma unroll
             for (uint32_t x = 0; x < 2; ++x) {
                 if (x == 1 && !has_b) break;
-                const int q0 = (int)((x ? u.tile[1] : u.tile[0]) * 128u);
+                // tile 0 may start at a negative row: TMA zero-fills the rows outside [0, m)
+                const int q0 = (int)((x ? u.tile[1] : u.tile[0]) * 128u) - (int)p.shift;
                 tc::tma_load_2d(sQ + x * kTile, &tmQ, q_full, hcol, q0);
                 tc::tma_load_2d(sQ + x * kTile + kHalf, &tmQ, q_full, hcol + 64, q0);
             }
@@ -340,8 +342,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         if (nb > 0) {
             const uint32_t quarter = warp & 3;
             const uint32_t r = quarter * 32 + lane;
-            const uint32_t qi = tile_x * 128u + r;
-            const bool valid = qi < p.m;
+            const uint32_t qi = tile_x * 128u + r - p.shift;  // wraps (invalid) for r < shift in tile 0
+            const bool valid = tile_x * 128u + r >= p.shift && qi < p.m;
             const uint32_t limit = valid ? p.rows[qi] : 0u;
             const uint32_t lane_base = (quarter * 32u) << 16;
             const uint32_t s_col = tmem + lane_base + x * 256, o_col = s_col + 128;
@@ -508,7 +510,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnCombine* __restrict__ jobs,
                                                            const float* __restrict__ part_o,
                                                            const float2* __restrict__ part_ml,
-                                                           uint32_t m, uint32_t h,
+                                                           uint32_t m, uint32_t shift, uint32_t h,
                                                            __nv_bfloat16* __restrict__ out) {
     constexpr uint32_t kMaxSplits = 16;
     tc::pdl_trigger();
@@ -516,7 +518,8 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnCombine* __
     const AttnCombine j = jobs[blockIdx.x];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t r = blockIdx.y * 8 + warp;
-    const uint32_t qi = j.tile * 128u + r;
+    if (j.tile * 128u + r < shift) return;
+    const uint32_t qi = j.tile * 128u + r - shift;
     if (qi >= m) return;
     const uint32_t n = min(j.n, kMaxSplits);
     float2 ml[kMaxSplits];
@@ -561,8 +564,7 @@ AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads) {
     std::vector<uint32_t> nblk(tiles);
     uint64_t total = 0;
     for (uint32_t t = 0; t < tiles; ++t) {
-        const uint32_t last = std::min(m, (t + 1) * 128) - 1;
-        nblk[t] = rows[last] / 128 + 1;
+        nblk[t] = rows[attn_tile_last_row(t, m)] / 128 + 1;
         total += (uint64_t)nblk[t] * n_heads;
     }
     // ~1.5 waves of items (an item carries up to two tiles); never split below 2 blocks
@@ -642,6 +644,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     p.units = d_units;
     p.rows = d_rows;
     p.m = m;
+    p.shift = attn_tile_shift(m);
     p.h = h;
     p.scale_log2 = (1.0f / sqrtf(128.0f)) * 1.4426950408889634f;
     p.out = out;
@@ -682,7 +685,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
         cfg.blockDim = dim3(256);
         cfg.dynamicSmemBytes = 0;
         MPIC_CUDA(cudaLaunchKernelEx(&cfg, attn_combine_kernel, d_combine, (const float*)part_o,
-                                     (const float2*)part_ml, m, h, out));
+                                     (const float2*)part_ml, m, p.shift, h, out));
         MPIC_LAUNCHED();
     }
 }
