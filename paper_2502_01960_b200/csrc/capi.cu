@@ -2144,7 +2144,31 @@ int mpic_test_gemm_epi(const void* d_a, const void* d_w, uint32_t M, uint32_t N,
     API_BEGIN
     MPIC_REQUIRE(tc_gemm_supported(M, N, K), MPIC_ERR_VALIDATION, "shape not supported by the tcgen05 gemm");
     EpiParams ep;
-    if (mode == 0) {
+    if (mode == 3) {  // EPI_QKV with head_dim 128 (timing): q -> d_out, K/V scattered to rows 0..M-1 of
+                      // scratch planes, zero (cos, sin) rows. The scratch is made on the first (uncaptured) call.
+        const uint32_t h = N / 3;
+        const size_t plane = (size_t)M * h * 2, rope = (size_t)M * 64 * sizeof(float2), rows = (size_t)M * 4;
+        static char* b = nullptr;
+        static size_t cap = 0;
+        if (cap < 2 * plane + rope + rows) {
+            cudaFree(b);
+            MPIC_CUDA(cudaMalloc(&b, 2 * plane + rope + rows));
+            cap = 2 * plane + rope + rows;
+            MPIC_CUDA(cudaMemset(b + 2 * plane, 0, rope));
+            std::vector<uint32_t> ident(M);
+            for (uint32_t i = 0; i < M; ++i) ident[i] = i;
+            MPIC_CUDA(cudaMemcpy(b + 2 * plane + rope, ident.data(), rows, cudaMemcpyHostToDevice));
+        }
+        ep.mode = EPI_QKV;
+        ep.q = d_out;
+        ep.kv_k = b;
+        ep.kv_v = b + plane;
+        ep.rope_tok = reinterpret_cast<const float2*>(b + 2 * plane);
+        ep.kv_rows = reinterpret_cast<const uint32_t*>(b + 2 * plane + rope);
+        ep.rope_pos = ep.kv_rows;
+        ep.hidden = h;
+        ep.head_dim = 128;
+    } else if (mode == 0) {
         ep.mode = EPI_RESID;
         ep.x = d_x;
         ep.xb = static_cast<__nv_bfloat16*>(d_xb);

@@ -191,44 +191,47 @@ __device__ __forceinline__ void pg_epi(const EpiParams& ep, uint32_t M, uint32_t
                 if (t < n) *reinterpret_cast<float4*>(o + (size_t)(tb + t) * ep.ldo) = v;
             }
         } else if constexpr (MODE == EPI_QKV) {
+            // linker.cpp:64-78 — the chunk goes through the slice as fp32 [token][32 features];
+            // each lane then owns 4 consecutive features (two interleaved RoPE pairs) of one
+            // token per step: its (cos, sin) pairs are one 16-B load, the rotation needs no
+            // shuffles, and the bf16 result is one 8-B store into q or the K/V cache row.
             const uint32_t h = ep.hidden, part = f0 / h, d0 = f0 - part * h;
-            const uint32_t hd2 = ep.head_dim >> 1, pr = ((f - part * h) % ep.head_dim) >> 1;
-            const bool odd = lane & 1;
+            const uint32_t hd2 = ep.head_dim >> 1, c4 = (lane & 7) * 4;
+            const uint32_t pr0 = ((d0 + c4) % ep.head_dim) >> 1;  // even (head_dim % 4 == 0)
+            // every load of the chunk (cache rows and (cos, sin) staged in shared memory — the
+            // staged QKV path is only used with both staged — and the transposed values) is
+            // issued before its first global store, branch-free, with explicit shared accesses
+            const uint32_t sf = tc::smem_u32(stg);
+            const uint32_t srows = tc::smem_u32(s_rows) - tg * 4u;
+            const uint32_t srope = tc::smem_u32(s_rope) + (pr0 - tg * hd2) * 8u;
+            const bool rot = part < 2 && !(ep.dbg & 64);  // warp-uniform
+            uint32_t rows[8];
+            float4 cs[8];
 #pragma unroll
-            for (uint32_t j0 = 0; j0 < 32; j0 += 16) {
-                float2 cs[16];
-                if (part < 2) {
-#pragma unroll
-                    for (uint32_t j = 0; j < 16; ++j) {
-                        const uint32_t t = min(tb + j0 + j, M - 1);
-                        cs[j] = s_rope ? s_rope[(t - tg) * hd2 + pr]
-                                       : ep.rope_tok ? __ldg(ep.rope_tok + (size_t)t * hd2 + pr)
-                                                     : __ldg(ep.rope + (size_t)__ldg(ep.rope_pos + t) * hd2 + pr);
-                    }
-                }
-#pragma unroll
-                for (uint32_t j = 0; j < 16; ++j) {
-                    float val = __uint_as_float(r[j0 + j]);
-                    if (part < 2) {  // warp-uniform
-                        const float vp = __shfl_xor_sync(0xffffffffu, val, 1);
-                        float x0 = odd ? vp : val, x1 = odd ? val : vp;
-                        rope_pair(x0, x1, cs[j].x, cs[j].y);
-                        val = odd ? x1 : x0;
-                    }
-                    stage_put_bf16(sb, j0 + j, lane, __float2bfloat16_rn(val));
-                }
+            for (uint32_t i = 0; i < 8; ++i) {
+                const uint32_t t = min(tb + i * 4 + (lane >> 3), M - 1);
+                rows[i] = part == 0 ? t : tc::ld_shared_u32(srows + t * 4u);
+                if (rot) cs[i] = tc::ld_shared_v4(srope + t * hd2 * 8u);
             }
-            __syncwarp();
-            __nv_bfloat16* base = static_cast<__nv_bfloat16*>(part == 0 ? ep.q : part == 1 ? ep.kv_k : ep.kv_v) + d0 +
-                                  (lane & 3) * 8;
 #pragma unroll
-            for (uint32_t i = 0; i < 4; ++i) {
-                const uint32_t t = i * 8 + (lane >> 2);
-                const uint4 v = stage_get_bf16(sb, i, lane);
-                if (t < n) {
-                    const uint32_t tt = tb + t;
-                    const uint32_t row = part == 0 ? tt : s_rows ? s_rows[tt - tg] : __ldg(ep.kv_rows + tt);
-                    *reinterpret_cast<uint4*>(base + (size_t)row * h) = v;
+            for (uint32_t j = 0; j < 32; ++j) tc::st_shared_f32(sf + (j * 32 + lane) * 4, __uint_as_float(r[j]));
+            __syncwarp();
+            float4 v[8];
+#pragma unroll
+            for (uint32_t i = 0; i < 8; ++i) v[i] = tc::ld_shared_v4(sf + ((i * 4 + (lane >> 3)) * 32 + c4) * 4);
+            __nv_bfloat16* base = static_cast<__nv_bfloat16*>(part == 0 ? ep.q : part == 1 ? ep.kv_k : ep.kv_v) + d0 + c4;
+#pragma unroll
+            for (uint32_t i = 0; i < 8; ++i) {
+                if (rot) {
+                    rope_pair(v[i].x, v[i].y, cs[i].x, cs[i].y);
+                    rope_pair(v[i].z, v[i].w, cs[i].z, cs[i].w);
+                }
+                if (i * 4 + (lane >> 3) < n && !(ep.dbg & 32)) {
+                    const __nv_bfloat162 lo = __floats2bfloat162_rn(v[i].x, v[i].y), hi = __floats2bfloat162_rn(v[i].z, v[i].w);
+                    uint2 pk;
+                    pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+                    pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+                    *reinterpret_cast<uint2*>(base + (size_t)rows[i] * h) = pk;
                 }
             }
         } else {  // EPI_STORE / EPI_GELU
@@ -239,11 +242,13 @@ __device__ __forceinline__ void pg_epi(const EpiParams& ep, uint32_t M, uint32_t
             }
             __syncwarp();
             __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + f0 + (lane & 3) * 8;
+            uint4 v[4];  // all read back before the first store (see EPI_QKV)
+#pragma unroll
+            for (uint32_t i = 0; i < 4; ++i) v[i] = stage_get_bf16(sb, i, lane);
 #pragma unroll
             for (uint32_t i = 0; i < 4; ++i) {
                 const uint32_t t = i * 8 + (lane >> 2);
-                const uint4 v = stage_get_bf16(sb, i, lane);
-                if (t < n) *reinterpret_cast<uint4*>(o + (size_t)(tb + t) * ep.ldo) = v;
+                if (t < n) *reinterpret_cast<uint4*>(o + (size_t)(tb + t) * ep.ldo) = v[i];
             }
         }
         __syncwarp();  // the slice is rewritten by the next chunk
@@ -529,9 +534,17 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                 if (a.stage_rope && !(a.dbg & 1)) {
                     const uint32_t nt = tend - tg, hd2 = a.ep.head_dim >> 1;
                     const uint32_t rope_bytes = nt * hd2 * 8, rows_bytes = (nt * 4 + 15) & ~15u;
+                    // both CTAs of the pair need the same rows: each loads half of the (cos, sin)
+                    // rows and multicasts it to the pair (halves the L2 reads of a table every
+                    // CTA of the grid wants at once); V-only pairs need no rotation
+                    const bool rot = fb * 256 < 2 * a.ep.hidden;
+                    const uint32_t half_tok = nt / 2, mine = rank ? nt - half_tok : half_tok;
                     if (warp == 2 && lane == 0) {
-                        tc::mbar_arrive_expect_tx(epi_bar, rope_bytes + rows_bytes);
-                        tc::bulk_load(smem, a.ep.rope_tok + (size_t)tg * hd2, rope_bytes, epi_bar);
+                        tc::mbar_arrive_expect_tx(epi_bar, (rot ? rope_bytes : 0u) + rows_bytes);
+                        if (rot && mine)
+                            tc::bulk_load_mcast(smem + (size_t)rank * half_tok * hd2 * 8,
+                                                a.ep.rope_tok + (size_t)(tg + rank * half_tok) * hd2, mine * hd2 * 8,
+                                                epi_bar, (uint16_t)(0x3u << (crank & ~1u)));
                         tc::bulk_load(smem + a.rows_off, a.ep.kv_rows + tg, rows_bytes, epi_bar);
                     }
                     tc::mbar_wait(epi_bar, 0);
@@ -864,17 +877,21 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
     if (verbose)
         fprintf(stderr, "pgemm M=%u N=%u K=%u: groups=%u P0=%u P1=%u S=%u clusters=%u stages=%u x %u kb nbuf=%u\n", M,
                 N, K, a.ngroups, a.P0, a.P1, a.S, a.clusters, a.stages, a.kps, a.nbuf);
-    if (ep_in.mode == EPI_QKV && ep_in.rope_tok && a.S == 1 && a.clusters >= a.tiles && a.ngroups == 1) {
+    if (ep_in.mode == EPI_QKV && ep_in.rope_tok && ep_in.head_dim % 4 == 0 && a.S == 1 && a.clusters >= a.tiles &&
+        a.ngroups == 1) {
         const uint32_t rope_bytes = a.G * (ep_in.head_dim / 2) * 8;
         a.rows_off = (rope_bytes + 1023) & ~1023u;
-        a.stage_rope = a.rows_off + a.G * 4 + 16 <= a.stages * a.stage_bytes;
+        static const bool no_stage = getenv("MPIC_PG_NOROPESTAGE") != nullptr;  // diagnostics
+        a.stage_rope = !no_stage && a.rows_off + a.G * 4 + 16 <= a.stages * a.stage_bytes;
     }
     static const bool staged_env = [] {
         const char* e = getenv("MPIC_PG_STAGED");  // diagnostics: 0 = direct (narrow) epilogue stores
         return !e || atoi(e) != 0;
     }();
     a.stg_off = kNoStage;
-    if (staged_env && a.S == 1 && a.clusters >= a.tiles) {
+    // the staged QKV epilogue reads (cos, sin) as 16-B pairs of pairs from rope_tok
+    const bool qkv_ok = ep_in.mode != EPI_QKV || a.stage_rope;
+    if (staged_env && qkv_ok && a.S == 1 && a.clusters >= a.tiles) {
         // one tile per cluster: the stage ring is idle once the accumulator is complete
         const uint32_t off = a.stage_rope ? (a.rows_off + a.G * 4 + 16 + 1023) & ~1023u : 0u;
         if (off + 8 * kStageSlice <= a.stages * a.stage_bytes) a.stg_off = off;

@@ -11,7 +11,7 @@ from paper_2502_01960_b200 import _lib
 
 L = _lib.lib()
 M = int(os.environ.get("M", "330"))
-for name, N, K, mode in [("qkv", 12288, 4096, 2), ("wo", 4096, 4096, 0), ("w1", 16384, 4096, 1),
+for name, N, K, mode in [("qkv", 12288, 4096, 2), ("qkv-rope", 12288, 4096, 3), ("wo", 4096, 4096, 0), ("w1", 16384, 4096, 1),
                          ("w2", 4096, 16384, 0)]:
     a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     ws = [torch.randn(N, K, device="cuda").to(torch.bfloat16) for _ in range(4)]
