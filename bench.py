@@ -118,15 +118,28 @@ def run_serving(args, world, rank, local):
     del host
     ns = [p.n for p in prompts]
     ms = [len(mp.select_tokens(p, mp.POLICY_MPIC_K, k)) for p in prompts]
-    ws = mp.Workspace(model, max(ms) if ms else 1, max(ns) if ns else 1)
-    linked = {n: mp.KV(L, n, H, D, mp.BF16, local) for n in sorted(set(ns))}
+    B = max(1, args.batch)
+    batches = [list(range(j, min(j + B, len(mine)))) for j in range(0, len(mine), B)]
+    if B > 1:  # batched varlen requests (mpic_request_prefill_batch): one cache holds a batch
+        ws = mp.Workspace(model, max(sum(ms[j] for j in b) for b in batches),
+                          max(sum(ns[j] for j in b) for b in batches))
+        big = mp.KV(L, max(sum(ns[j] for j in b) for b in batches), H, D, mp.BF16, local)
+    else:
+        ws = mp.Workspace(model, max(ms) if ms else 1, max(ns) if ns else 1)
+        linked = {n: mp.KV(L, n, H, D, mp.BF16, local) for n in sorted(set(ns))}
 
     def step(ttft=None):
-        for i, p in zip(mine, prompts):
+        for b in batches:
             t0 = time.perf_counter()
-            mp.request_prefill(model, ws, p, [pool[c] for c in reqs[i][1]], linked[p.n], k=k, stream=stream)
-            if ttft is not None:
-                ttft.append((time.perf_counter() - t0) * 1e3)
+            if B > 1:
+                mp.request_prefill_batch(model, ws, [prompts[j] for j in b],
+                                         [[pool[c] for c in reqs[mine[j]][1]] for j in b], big, k=k, stream=stream)
+            else:
+                (j,) = b
+                mp.request_prefill(model, ws, prompts[j], [pool[c] for c in reqs[mine[j]][1]], linked[prompts[j].n],
+                                   k=k, stream=stream)
+            if ttft is not None:  # every request of a batch gets its logits when the batch ends
+                ttft.extend([(time.perf_counter() - t0) * 1e3] * len(b))
 
     for _ in range(args.warmup):
         step()
@@ -667,6 +680,8 @@ def main():
                     help="also time the request with every chunk read from its .mpic file")
     ap.add_argument("--disk-dir", default=None, help="where the .mpic files are written")
     ap.add_argument("--k", type=int, default=None, help="MPIC-k budget (default: the config's)")
+    ap.add_argument("--batch", type=int, default=64,
+                    help="config E: requests per batched varlen pass (1 = one request at a time)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.config is None:
@@ -735,6 +750,7 @@ def main():
                         "synthesised from seed 1)",
                 "config": dict(cfg_json, requests=E_REQUESTS, pool_chunks=E_POOL, n_tokens_total=r["n"],
                                recompute_rows_total=r["m"], requests_rank0=r["mine"],
+                               batch=max(1, args.batch),
                                parallelism=f"request-sharded x{world} (LPT by predicted cost, no collective)",
                                l2="inputs larger than L2: 12.9 GB bf16 weights stream through HBM per request"),
                 "recompute_rows_per_s": r["rows_per_s"],

@@ -223,6 +223,17 @@ int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mp
                                const mpic_policy* policy, const char* const* paths, mpic_reposition reposition,
                                mpic_kv_t linked, float* logits, uint32_t* selected, uint32_t* m_out, void* stream);
 
+/* Batched varlen MPIC-k: nreq independent requests (device-resident chunks,
+ * request-major in `chunks`) in ONE selective pass on the bf16 head_dim-128 path. Request
+ * r's cache occupies rows [off_r, off_r + n_r) of `linked` (off_r = sum of the earlier
+ * prompts' lengths; linked->T >= sum n_r); its rows attend only to its own rows. logits:
+ * [nreq][vocab] host floats; m_out[r] = rows recomputed for request r. Synchronous.
+ * Replaces nreq calls of the reference's assemble_linked_cache + selective_prefill
+ * (proj/include/mpic/linker.h:107-129), which has no batched form. */
+int mpic_request_prefill_batch(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompts, uint32_t nreq,
+                               const mpic_policy* policy, const mpic_kv_t* chunks, mpic_reposition reposition,
+                               mpic_kv_t linked, float* logits, uint32_t* m_out, void* stream);
+
 /* ---- head-parallel request (one long request over P GPUs) ---------------
  * Rank r owns heads [head0, head0 + n_local_heads): its model holds those heads' Wq/Wk/Wv
  * rows and Wo columns (bit-identical slices of build_model's weights) and the full FFN; its

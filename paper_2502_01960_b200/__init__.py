@@ -276,6 +276,24 @@ def request_prefill(model: Model, ws: Workspace, prompt: Prompt, chunks, linked:
     return logits, sel[:m.value].copy()
 
 
+def request_prefill_batch(model: Model, ws: Workspace, prompts, chunks, linked: KV,
+                          policy: int = POLICY_MPIC_K, k: int = 32, global_budget: bool = False,
+                          reposition: int = AS_STORED, stream=None):
+    """Batched varlen form of request_prefill (mpic_request_prefill_batch): `chunks[r]` lists
+    request r's image chunks. Request r's cache is rows [off_r, off_r + n_r) of `linked`
+    (off_r = sum of the earlier prompts' n). Returns (logits [nreq][vocab], rows per request)."""
+    descs = (PromptDesc * len(prompts))(*[p.desc() for p in prompts])
+    flat = [c.handle for cs in chunks for c in cs]
+    arr = (C.c_void_p * max(len(flat), 1))(*flat)
+    logits = np.zeros((len(prompts), model.cfg.vocab_size), np.float32)
+    m = np.zeros(len(prompts), np.uint32)
+    pol = PolicyDesc(policy, k, int(global_budget))
+    check(lib().mpic_request_prefill_batch(model.handle, ws.handle, descs, len(prompts), C.byref(pol), arr,
+                                           reposition, linked.handle, logits.ctypes.data, m.ctypes.data,
+                                           _stream_ptr(stream)))
+    return logits, m
+
+
 def request_prefill_host(model: Model, ws: Workspace, prompt: Prompt, chunk_k, chunk_v,
                          linked: KV, policy: int = POLICY_MPIC_K, k: int = 32,
                          global_budget: bool = False, reposition: int = AS_STORED,

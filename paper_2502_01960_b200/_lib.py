@@ -95,6 +95,8 @@ SIGNATURES = {
                                          _vp, _int, _vp, _vp, _vp, _P(_u32), _vp]),
     "mpic_kv_download_rows": (_int, [_vp, _vp, _u32, _vp, _vp, _vp]),
     "mpic_workspace_set_graphs": (_int, [_vp, _int]),
+    "mpic_request_prefill_batch": (_int, [_vp, _vp, _P(PromptDesc), _u32, _P(PolicyDesc), _vp, _int, _vp, _vp,
+                                          _vp, _vp]),
     "mpic_request_prefill_files": (_int, [_vp, _vp, _P(PromptDesc), _P(PolicyDesc), _vp, _int, _vp, _vp, _vp,
                                           _P(_u32), _vp]),
     "mpic_request_prefill_host2": (_int, [_vp, _vp, _P(PromptDesc), _P(PolicyDesc), _vp, _vp, _int, _vp,

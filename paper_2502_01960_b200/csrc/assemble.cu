@@ -17,7 +17,7 @@
 
 namespace mpicb {
 
-constexpr int kMaxAsmChunks = 64;
+constexpr int kMaxAsmChunks = 256;  // chunks are sorted by destination row (plan_assembly)
 
 template <typename T, int N>
 struct alignas(sizeof(T) * N >= 16 ? 16 : sizeof(T) * N) Vec {
@@ -88,11 +88,15 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmChunk* __restric
         if (skip_blk && skip_blk[r >> 7]) continue;  // linked inside attention (AttnLink)
         TD* kd = dk + u * h;
         TD* vd = dv + u * h;
-        int c = -1;
-        for (uint32_t i = 0; i < n_chunks; ++i) {
-            const uint32_t d0 = s_chunks[i].dst_row0;
-            if (r >= d0 && r < d0 + s_chunks[i].rows) { c = (int)i; break; }
+        // the last chunk starting at or before r (chunks ascend by destination row and do
+        // not overlap), if r falls inside it
+        uint32_t lo = 0, hi = n_chunks;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (s_chunks[mid].dst_row0 <= r) lo = mid + 1;
+            else hi = mid;
         }
+        const int c = lo > 0 && r < s_chunks[lo - 1].dst_row0 + s_chunks[lo - 1].rows ? (int)lo - 1 : -1;
         if (c < 0) {
             if (zero_gaps) {
                 float z[VEC];
@@ -156,11 +160,13 @@ static void launch_asm_typed(const AsmChunk* d_chunks, uint32_t n_chunks, const 
     const uint32_t grid = (uint32_t)std::min<uint64_t>(units, (uint64_t)kNumSMs * per_sm);
     if (h % 8 == 0) {
         auto k = assemble_kernel<TS, TD, 8>;
-        if (smem > 48 * 1024) MPIC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (smem + sizeof(AsmChunk) * kMaxAsmChunks > 48 * 1024)
+            MPIC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k<<<grid, 256, smem, s>>>(d_chunks, n_chunks, d_tables, n_tables, dk, dv, L, T, H, D, zero_gaps, src_l0, skip_blk);
     } else {
         auto k = assemble_kernel<TS, TD, 2>;
-        if (smem > 48 * 1024) MPIC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (smem + sizeof(AsmChunk) * kMaxAsmChunks > 48 * 1024)
+            MPIC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k<<<grid, 256, smem, s>>>(d_chunks, n_chunks, d_tables, n_tables, dk, dv, L, T, H, D, zero_gaps, src_l0, skip_blk);
     }
     MPIC_LAUNCHED();

@@ -144,6 +144,7 @@ struct mpic_workspace_s {
     int32_t* d_ids = nullptr;
     uint32_t* d_rows = nullptr;
     uint32_t* d_pos = nullptr;
+    uint32_t* d_start = nullptr;        // batched requests: first cache row of each row's request
     float* x = nullptr;                 // residual stream fp32 [m_pad][h]
     float2* rope_tok = nullptr;         // (cos, sin) of each row's position [m_pad][D/2]
     __nv_bfloat16* xb = nullptr;        // bf16 copy of x (GEMM A operand, bf16 mode)
@@ -156,6 +157,7 @@ struct mpic_workspace_s {
     int32_t* h_ids = nullptr;           // pinned staging
     uint32_t* h_rows = nullptr;
     uint32_t* h_pos = nullptr;
+    uint32_t* h_start = nullptr;
     float* h_logits = nullptr;
     // loader lane (mpic_request_prefill_host): side stream, 2-slot HBM staging ring
     cudaStream_t copy_stream = nullptr;
@@ -434,13 +436,14 @@ bool plan_attn_link(const std::vector<mpic_chunk_ref>& refs, const uint32_t* sel
 // which every query may see keys up to max_pos), grow the workspace buffers it needs and
 // stage it in pinned memory. Host-only: nothing is enqueued, so it may run before a
 // stream capture. enqueue_attn_plan() then copies it to the device on the stream.
-void prepare_attn_plan(mpic_workspace_t ws, const uint32_t* h_rows, uint32_t m, uint32_t max_pos, uint32_t H) {
+void prepare_attn_plan(mpic_workspace_t ws, const uint32_t* h_rows, uint32_t m, uint32_t max_pos, uint32_t H,
+                       const uint32_t* h_starts = nullptr) {
     std::vector<uint32_t> conservative;
     if (!h_rows) {
         conservative.assign(m, max_pos);
         h_rows = conservative.data();
     }
-    const AttnPlan plan = plan_attention(h_rows, m, H);
+    const AttnPlan plan = plan_attention(h_rows, m, H, h_starts);
     auto grow = [&](auto*& ptr, size_t& cap, size_t need, size_t elt) {
         if (cap >= need) return;
         MPIC_CUDA(cudaDeviceSynchronize());
@@ -503,7 +506,8 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
                   mpic_kv_t kv, float* d_logits, cudaStream_t s,
                   const std::function<void(uint32_t)>& before_layer = {},
                   const uint32_t* h_rows = nullptr, float* d_capture = nullptr, bool plan_ready = false,
-                  const AttnLink* d_link = nullptr) {
+                  const AttnLink* d_link = nullptr, const uint32_t* d_starts = nullptr,
+                  const std::vector<uint32_t>* logit_rows = nullptr) {
     const mpic_model_config& c = md->cfg;
     const uint32_t h = c.hidden_dim, H = c.n_heads, D = c.head_dim;
     MPIC_REQUIRE(m > 0, MPIC_ERR_VALIDATION, "no tokens to prefill");
@@ -554,7 +558,7 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
                 launch_attn_tc(static_cast<const __nv_bfloat16*>(ws->q), static_cast<const __nv_bfloat16*>(kl),
                                static_cast<const __nv_bfloat16*>(vl), kv->T, d_rows, m, H, ws->d_units,
                                ws->n_units, ws->d_comb, ws->n_comb, ws->part_o, ws->part_ml,
-                               static_cast<__nv_bfloat16*>(ws->attn), s, d_link, l);
+                               static_cast<__nv_bfloat16*>(ws->attn), s, d_link, l, d_starts);
             else
                 launch_attn_simt(ws->q, kl, vl, md->dtype, d_rows, m, H, D, ws->attn, s);
         }
@@ -588,7 +592,12 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
     }
     {
         ProfScope ps(s, MPIC_PHASE_LM_HEAD);
-        launch_lm_head(ws->x + (size_t)(m - 1) * h, md->lm_head, md->dtype, c.vocab_size, h, d_logits, s);
+        if (logit_rows)  // batched requests: each request's last row, logits [request][V]
+            for (size_t i = 0; i < logit_rows->size(); ++i)
+                launch_lm_head(ws->x + (size_t)(*logit_rows)[i] * h, md->lm_head, md->dtype, c.vocab_size, h,
+                               d_logits + i * c.vocab_size, s);
+        else
+            launch_lm_head(ws->x + (size_t)(m - 1) * h, md->lm_head, md->dtype, c.vocab_size, h, d_logits, s);
     }
     (void)e;
 }
@@ -691,6 +700,9 @@ AsmPlan plan_assembly(const void* const* src_k, const void* const* src_v, const 
         }
         p.chunks[i] = a;
     }
+    // the assembly kernel binary-searches the chunk of each destination row
+    std::sort(p.chunks.begin(), p.chunks.end(),
+              [](const AsmChunk& a, const AsmChunk& b) { return a.dst_row0 < b.dst_row0; });
     return p;
 }
 
@@ -1170,6 +1182,7 @@ int mpic_workspace_create(mpic_model_t md, uint32_t max_rows, uint32_t max_ctx, 
     ws->d_ids = dmalloc<int32_t>(mp);
     ws->d_rows = dmalloc<uint32_t>(mp);
     ws->d_pos = dmalloc<uint32_t>(mp);
+    ws->d_start = dmalloc<uint32_t>(mp);
     ws->x = dmalloc<float>(mp * h);
     ws->rope_tok = dmalloc<float2>(mp * (md->cfg.head_dim / 2));
     ws->xb = dmalloc<__nv_bfloat16>(mp * h);
@@ -1188,6 +1201,7 @@ int mpic_workspace_create(mpic_model_t md, uint32_t max_rows, uint32_t max_ctx, 
     MPIC_CUDA(cudaMallocHost(&ws->h_ids, mp * 4));
     MPIC_CUDA(cudaMallocHost(&ws->h_rows, mp * 4));
     MPIC_CUDA(cudaMallocHost(&ws->h_pos, mp * 4));
+    MPIC_CUDA(cudaMallocHost(&ws->h_start, mp * 4));
     MPIC_CUDA(cudaMallocHost(&ws->h_logits, md->cfg.vocab_size * 4));
     MPIC_CUDA(cudaStreamCreateWithFlags(&ws->copy_stream, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
@@ -1203,11 +1217,11 @@ int mpic_workspace_destroy(mpic_workspace_t ws) {
     API_BEGIN
     if (ws) {
         cudaSetDevice(ws->model->device);
-        cudaFree(ws->d_ids); cudaFree(ws->d_rows); cudaFree(ws->d_pos);
+        cudaFree(ws->d_ids); cudaFree(ws->d_rows); cudaFree(ws->d_pos); cudaFree(ws->d_start);
         cudaFree(ws->x); cudaFree(ws->rope_tok); cudaFree(ws->xb); cudaFree(ws->q); cudaFree(ws->attn); cudaFree(ws->ffn);
         cudaFree(ws->d_logits);
         cudaFree(ws->partial);
-        cudaFreeHost(ws->h_ids); cudaFreeHost(ws->h_rows); cudaFreeHost(ws->h_pos);
+        cudaFreeHost(ws->h_ids); cudaFreeHost(ws->h_rows); cudaFreeHost(ws->h_pos); cudaFreeHost(ws->h_start);
         cudaFreeHost(ws->h_logits);
         for (int i = 0; i < 2; ++i) {
             cudaFree(ws->stage[i]);
@@ -1512,6 +1526,117 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
     std::memcpy(logits, ws->h_logits, model->cfg.vocab_size * sizeof(float));
     if (selected) std::memcpy(selected, r.sel.data(), r.m * sizeof(uint32_t));
     if (m_out) *m_out = r.m;
+    API_END
+}
+
+// ---- batched varlen requests (SURVEY §8b "a batched varlen variant") -------------------
+// nreq independent requests in ONE selective pass: request r's cache occupies rows
+// [off_r, off_r + n_r) of `linked` (off_r = sum of the earlier n), its selected rows are
+// scattered there at their own positions (RoPE at the position, KV row = off_r + position),
+// and attention masks every key outside [off_r, off_r + position]. The projections then see
+// sum(m_r) rows at once instead of streaming every weight once per request.
+int mpic_request_prefill_batch(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompts, uint32_t nreq,
+                               const mpic_policy* policy, const mpic_kv_t* chunks, mpic_reposition reposition,
+                               mpic_kv_t linked, float* logits, uint32_t* m_out, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(model->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    MPIC_REQUIRE(ws && ws->model == model, MPIC_ERR_VALIDATION, "workspace belongs to another model");
+    MPIC_REQUIRE(nreq > 0 && prompts && logits, MPIC_ERR_VALIDATION, "empty request batch");
+    MPIC_REQUIRE(use_tc_attention(model), MPIC_ERR_VALIDATION,
+                 "batched requests run on the bf16 head_dim-128 tensor-core path");
+    const mpic_model_config& c = model->cfg;
+    std::vector<RequestPlan> plans;
+    plans.reserve(nreq);
+    uint32_t n_tot = 0, m_tot = 0;
+    for (uint32_t r = 0; r < nreq; ++r) {
+        plans.push_back(plan_request(model, &prompts[r], policy, nullptr));
+        n_tot += plans.back().n;
+        m_tot += plans.back().m;
+    }
+    MPIC_REQUIRE(linked && linked->L == c.n_layers && linked->H == c.n_heads && linked->D == c.head_dim &&
+                     linked->dtype == model->dtype,
+                 MPIC_ERR_VALIDATION, "linked cache shape does not match model");
+    MPIC_REQUIRE(linked->T >= n_tot, MPIC_ERR_CONTRACT, "linked cache shorter than the batch's prompts");
+    MPIC_REQUIRE(m_tot <= ws->max_rows, MPIC_ERR_VALIDATION, "more rows than the workspace holds");
+    std::vector<uint32_t> rows(m_tot), pos(m_tot), starts(m_tot), last(nreq);
+    std::vector<int32_t> ids(m_tot);
+    std::vector<mpic_chunk_ref> refs;
+    std::vector<const void*> ks, vs;
+    std::vector<uint32_t> ts;
+    uint32_t off = 0, at = 0, ci = 0, max_pos = 0;
+    for (uint32_t r = 0; r < nreq; ++r) {
+        const RequestPlan& p = plans[r];
+        check_ids(model, p.ids_sel.data(), p.m);
+        for (uint32_t i = 0; i < p.m; ++i) {
+            rows[at + i] = off + p.sel[i];
+            pos[at + i] = p.sel[i];
+            starts[at + i] = off;
+            ids[at + i] = p.ids_sel[i];
+            max_pos = std::max(max_pos, p.sel[i]);
+        }
+        for (mpic_chunk_ref ref : p.refs) {
+            const mpic_kv_t ch = chunks[ci++];
+            MPIC_REQUIRE(ch, MPIC_ERR_LINK, "no fetched entry for image segment");
+            MPIC_REQUIRE(ch->T == ref.rows, MPIC_ERR_LINK, "token_count mismatch for image segment");
+            MPIC_REQUIRE(ch->L == linked->L && ch->H == linked->H && ch->D == linked->D, MPIC_ERR_LINK,
+                         "entry tensor shape does not match model");
+            MPIC_REQUIRE(ch->dtype == chunks[0]->dtype, MPIC_ERR_VALIDATION, "mixed chunk dtypes");
+            ref.dst_row0 += off;
+            ref.position_base += off;  // Rerotate's delta (dst - base) stays request-relative
+            refs.push_back(ref);
+            ks.push_back(ch->k);
+            vs.push_back(ch->v);
+            ts.push_back(ch->T);
+        }
+        last[r] = at + p.m - 1;
+        if (m_out) m_out[r] = p.m;
+        at += p.m;
+        off += p.n;
+    }
+    const uint32_t n_img = (uint32_t)refs.size();
+    const mpic_dtype src_t = n_img ? chunks[0]->dtype : model->dtype;
+    const AsmPlan ap = plan_assembly(ks.data(), vs.data(), ts.data(), refs.data(), n_img, linked->T, linked->D,
+                                     reposition, c.rope_base, linked->H * linked->D);
+    ensure_rope(model, max_pos + 1, s);
+    prepare_attn_plan(ws, rows.data(), m_tot, n_tot - 1, c.n_heads, starts.data());
+    const size_t bytes_c = std::max<size_t>(1, ap.chunks.size()) * sizeof(AsmChunk);
+    const size_t bytes_t = std::max<size_t>(1, ap.tables.size()) * sizeof(float2);
+    if (ws->asm_cap < bytes_c + bytes_t) {
+        MPIC_CUDA(cudaDeviceSynchronize());
+        cudaFreeHost(ws->h_asm);
+        cudaFree(ws->d_asm);
+        ws->h_asm = ws->d_asm = nullptr;
+        ws->asm_cap = 0;
+        MPIC_CUDA(cudaMallocHost(&ws->h_asm, bytes_c + bytes_t));
+        MPIC_CUDA(cudaMalloc(&ws->d_asm, bytes_c + bytes_t));
+        ws->asm_cap = bytes_c + bytes_t;
+    }
+    if (!ap.chunks.empty()) std::memcpy(ws->h_asm, ap.chunks.data(), ap.chunks.size() * sizeof(AsmChunk));
+    if (!ap.tables.empty())
+        std::memcpy((char*)ws->h_asm + bytes_c, ap.tables.data(), ap.tables.size() * sizeof(float2));
+    std::memcpy(ws->h_ids, ids.data(), m_tot * 4);
+    std::memcpy(ws->h_rows, rows.data(), m_tot * 4);
+    std::memcpy(ws->h_pos, pos.data(), m_tot * 4);
+    std::memcpy(ws->h_start, starts.data(), m_tot * 4);
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_ids, ws->h_ids, m_tot * 4, cudaMemcpyHostToDevice, s));
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_rows, ws->h_rows, m_tot * 4, cudaMemcpyHostToDevice, s));
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_pos, ws->h_pos, m_tot * 4, cudaMemcpyHostToDevice, s));
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_start, ws->h_start, m_tot * 4, cudaMemcpyHostToDevice, s));
+    MPIC_CUDA(cudaMemcpyAsync(ws->d_asm, ws->h_asm, bytes_c + bytes_t, cudaMemcpyHostToDevice, s));
+    {
+        ProfScope ps(s, MPIC_PHASE_ASSEMBLE);
+        launch_assemble(static_cast<const AsmChunk*>(ws->d_asm), n_img,
+                        reinterpret_cast<const float2*>((char*)ws->d_asm + bytes_c), ap.n_tables, src_t, linked->k,
+                        linked->v, linked->dtype, linked->L, linked->T, linked->H, linked->D, 1, s);
+    }
+    float* d_lg = nullptr;
+    MPIC_CUDA(cudaMallocAsync((void**)&d_lg, (size_t)nreq * c.vocab_size * 4, s));
+    forward_rows(model, ws, ws->d_ids, ws->d_rows, ws->d_pos, m_tot, max_pos, linked, d_lg, s, {}, rows.data(),
+                 nullptr, /*plan_ready=*/true, nullptr, ws->d_start, &last);
+    MPIC_CUDA(cudaMemcpyAsync(logits, d_lg, (size_t)nreq * c.vocab_size * 4, cudaMemcpyDeviceToHost, s));
+    MPIC_CUDA(cudaFreeAsync(d_lg, s));
+    MPIC_CUDA(cudaStreamSynchronize(s));
     API_END
 }
 

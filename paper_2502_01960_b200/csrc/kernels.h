@@ -118,7 +118,8 @@ struct AttnPlan {
     uint32_t slots = 0;
 };
 unsigned long long* attn_debug_buffer();
-AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads);
+// starts (optional, batched requests): per selected row, the first cache row of its request.
+AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads, const uint32_t* starts = nullptr);
 // Query tiles are right-aligned: tile t holds selected rows [128t - shift, 128(t+1) - shift)
 // with shift = 128 * ceil(m / 128) - m, so only the FIRST tile is partial. Rows are sorted by
 // position, so every tile then ends at an earlier (or the same) row than with left-aligned
@@ -151,7 +152,8 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
                     uint32_t n_ctx, const uint32_t* d_rows, uint32_t m, uint32_t H,
                     const AttnUnit* d_units, uint32_t n_units, const AttnCombine* d_combine,
                     uint32_t n_combine, float* part_o, float2* part_ml, __nv_bfloat16* out,
-                    cudaStream_t s, const AttnLink* link = nullptr, uint32_t layer = 0);
+                    cudaStream_t s, const AttnLink* link = nullptr, uint32_t layer = 0,
+                    const uint32_t* d_starts = nullptr);
 
 // tcgen05 / TMA kernels (tc_gemm.cu, tc_attn.cu)
 struct TcGemmPlan;

@@ -49,6 +49,7 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 struct AttnParams {
     const AttnUnit* units;
     const uint32_t* rows;
+    const uint32_t* starts;  // batched requests: first key row each query row may see (null: 0)
     uint32_t m;
     uint32_t shift;         // attn_tile_shift(m): tile t starts at selected row 128t - shift
     uint32_t h;
@@ -345,6 +346,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             const uint32_t qi = tile_x * 128u + r - p.shift;  // wraps (invalid) for r < shift in tile 0
             const bool valid = tile_x * 128u + r >= p.shift && qi < p.m;
             const uint32_t limit = valid ? p.rows[qi] : 0u;
+            const uint32_t first = valid && p.starts ? p.starts[qi] : 0u;  // its request's first cache row
             const uint32_t lane_base = (quarter * 32u) << 16;
             const uint32_t s_col = tmem + lane_base + x * 256, o_col = s_col + 128;
             float m_used = -INFINITY, l = 0.0f;
@@ -359,7 +361,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 // prompt, so a warp often sees few or none of a block's keys: chunks of 32 keys
                 // no lane of the warp sees are neither loaded nor exponentiated (P = 0), and a
                 // warp that sees nothing just writes P = 0.
-                const uint32_t nv = !valid || limit < k0 ? 0u : min(limit - k0 + 1u, 128u);
+                // keys [ns, nv) of the block belong to the row's request (batched requests:
+                // rows of other requests' caches below `first` are masked too)
+                const uint32_t ns = first > k0 ? min(first - k0, 128u) : 0u;
+                uint32_t nv = !valid || limit < k0 ? 0u : min(limit - k0 + 1u, 128u);
+                if (ns >= nv) nv = 0u;
                 const uint32_t nv_max = __reduce_max_sync(0xffffffffu, nv);
                 const uint32_t nv_min = __reduce_min_sync(0xffffffffu, nv);
                 if (nv_max == 0) {
@@ -390,6 +396,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                         for (uint32_t e = 0; e < 32; ++e)
                             if (32 * c + e >= nv) v[c][e] = __float_as_uint(-INFINITY);
                     }
+                }
+                if (p.starts && __any_sync(0xffffffffu, ns > 0u)) {  // batched: below the request's start
+#pragma unroll
+                    for (uint32_t c = 0; c < 4; ++c)
+                        if (c < nch) {
+#pragma unroll
+                            for (uint32_t e = 0; e < 32; ++e)
+                                if (32 * c + e < ns) v[c][e] = __float_as_uint(-INFINITY);
+                        }
                 }
                 float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
@@ -558,24 +573,36 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnCombine* __
 // Host: split every (query tile, head) key range into chunks of at most `chunk` blocks,
 // then pair the chunks of two query tiles that start at the same key block of the same
 // head into one item (they share the K/V stream; each stops at its own end block).
-AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads) {
+AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads, const uint32_t* starts) {
     AttnPlan plan;
     const uint32_t tiles = ceil_div(m, 128);
-    std::vector<uint32_t> nblk(tiles);
+    // tile t reads key blocks [sblk[t], nblk[t]): from its first row's request start (rows and
+    // starts ascend) through its last row's position
+    std::vector<uint32_t> nblk(tiles), sblk(tiles, 0);
     uint64_t total = 0;
     for (uint32_t t = 0; t < tiles; ++t) {
         nblk[t] = rows[attn_tile_last_row(t, m)] / 128 + 1;
-        total += (uint64_t)nblk[t] * n_heads;
+        if (starts) {
+            const uint32_t first = t == 0 ? 0u : attn_tile_last_row(t - 1, m) + 1;
+            sblk[t] = std::min(starts[first] / 128, nblk[t] - 1);
+        }
+        total += (uint64_t)(nblk[t] - sblk[t]) * n_heads;
     }
     // ~1.5 waves of items (an item carries up to two tiles); never split below 2 blocks
     uint32_t chunk = (uint32_t)std::max<uint64_t>(2, (total + 3 * kNumSMs - 1) / (3 * kNumSMs));
-    uint32_t longest = 0;
-    for (uint32_t t = 0; t < tiles; ++t) longest = std::max(longest, nblk[t]);
-    chunk = std::max(chunk, ceil_div(longest, 16));  // the combine merges at most 16 splits
+    uint32_t longest = 0, last = 0;
+    for (uint32_t t = 0; t < tiles; ++t) {
+        longest = std::max(longest, nblk[t] - sblk[t]);
+        last = std::max(last, nblk[t]);
+    }
+    chunk = std::max(chunk, ceil_div(longest + 1, 15));  // a tile meets at most 16 grid cells (combine limit)
+    // splits: tile t's range cut by the global grid [sp*chunk, (sp+1)*chunk)
+    auto cell0 = [&](uint32_t t) { return sblk[t] / chunk; };
+    auto cells = [&](uint32_t t) { return ceil_div(nblk[t], chunk) - cell0(t); };
     std::vector<uint32_t> slot0(tiles * n_heads, kNoTile);
     uint32_t slot = 0;
     for (uint32_t t = 0; t < tiles; ++t) {
-        const uint32_t splits = ceil_div(nblk[t], chunk);
+        const uint32_t splits = cells(t);
         if (splits < 2) continue;
         for (uint32_t hd = 0; hd < n_heads; ++hd) {
             plan.combine.push_back(AttnCombine{t, hd, slot, splits});
@@ -584,26 +611,27 @@ AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads) {
         }
     }
     plan.slots = slot;
+    const uint32_t max_cells = ceil_div(last, chunk);
     for (uint32_t hd = 0; hd < n_heads; ++hd) {
-        const uint32_t max_splits = ceil_div(longest, chunk);
-        for (uint32_t sp = 0; sp < max_splits; ++sp) {
+        for (uint32_t sp = 0; sp < max_cells; ++sp) {
             AttnUnit cur{};
             bool open = false;
             for (uint32_t t = 0; t < tiles; ++t) {
-                if (sp * chunk >= nblk[t]) continue;
-                const uint32_t b1 = std::min(nblk[t], (sp + 1) * chunk);
+                const uint32_t lo = std::max(sblk[t], sp * chunk), hi = std::min(nblk[t], (sp + 1) * chunk);
+                if (lo >= hi) continue;
                 const uint32_t s0 = slot0[t * n_heads + hd];
-                const uint32_t sl = s0 == kNoTile ? kNoTile : s0 + sp;
-                if (!open) {
-                    cur = AttnUnit{hd, sp * chunk, {t, kNoTile}, {b1, 0}, {sl, kNoTile}};
-                    open = true;
-                } else {
+                const uint32_t sl = s0 == kNoTile ? kNoTile : s0 + (sp - cell0(t));
+                if (open && cur.b0 == lo) {  // pair with the open item: same first key block
                     cur.tile[1] = t;
-                    cur.b1[1] = b1;
+                    cur.b1[1] = hi;
                     cur.slot[1] = sl;
                     plan.units.push_back(cur);
                     open = false;
+                    continue;
                 }
+                if (open) plan.units.push_back(cur);
+                cur = AttnUnit{hd, lo, {t, kNoTile}, {hi, 0}, {sl, kNoTile}};
+                open = true;
             }
             if (open) plan.units.push_back(cur);
         }
@@ -635,7 +663,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
                     uint32_t n_ctx, const uint32_t* d_rows, uint32_t m, uint32_t H,
                     const AttnUnit* d_units, uint32_t n_units, const AttnCombine* d_combine,
                     uint32_t n_combine, float* part_o, float2* part_ml, __nv_bfloat16* out,
-                    cudaStream_t s, const AttnLink* link, uint32_t layer) {
+                    cudaStream_t s, const AttnLink* link, uint32_t layer, const uint32_t* d_starts) {
     const uint32_t h = H * 128;
     const CUtensorMap tmQ = make_tmap_bf16(q, h, m, 64, 128);
     const CUtensorMap tmK = make_tmap_bf16(kcache, h, n_ctx, 64, 128);
@@ -643,6 +671,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     AttnParams p;
     p.units = d_units;
     p.rows = d_rows;
+    p.starts = d_starts;
     p.m = m;
     p.shift = attn_tile_shift(m);
     p.h = h;
