@@ -520,13 +520,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
 // Merge split partials of one (tile, head): O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s.
 // One warp per query row (blockIdx.y picks 8 rows of the job), lanes along the head
-// dimension: coalesced 512-B partial reads, 256-B bf16 output rows; all loads of a row
-// are issued before they are consumed.
-__global__ void __launch_bounds__(256) attn_combine_kernel(const AttnCombine* __restrict__ jobs,
-                                                           const float* __restrict__ part_o,
-                                                           const float2* __restrict__ part_ml,
-                                                           uint32_t m, uint32_t shift, uint32_t h,
-                                                           __nv_bfloat16* __restrict__ out) {
+// dimension: coalesced 512-B partial reads, 256-B bf16 output rows. Few registers per thread
+// (the (m, l) pass first, then the partials four splits at a time) so that several CTAs share
+// an SM: the kernel is a short burst of latency-bound warps, and occupancy is what hides it.
+__global__ void __launch_bounds__(256, 6) attn_combine_kernel(const AttnCombine* __restrict__ jobs,
+                                                              const float* __restrict__ part_o,
+                                                              const float2* __restrict__ part_ml,
+                                                              uint32_t m, uint32_t shift, uint32_t h,
+                                                              __nv_bfloat16* __restrict__ out) {
     constexpr uint32_t kMaxSplits = 16;
     tc::pdl_trigger();
     tc::pdl_wait();
@@ -537,30 +538,33 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnCombine* __
     const uint32_t qi = j.tile * 128u + r - shift;
     if (qi >= m) return;
     const uint32_t n = min(j.n, kMaxSplits);
-    float2 ml[kMaxSplits];
-    float4 ov[kMaxSplits];
-#pragma unroll
-    for (uint32_t s = 0; s < kMaxSplits; ++s)
-        if (s < n) {
-            ml[s] = __ldcg(part_ml + (size_t)(j.slot0 + s) * 128 + r);
-            ov[s] = __ldcs(reinterpret_cast<const float4*>(part_o + ((size_t)(j.slot0 + s) * 128 + r) * 128) + lane);
-        }
+    const float2* ml = part_ml + (size_t)j.slot0 * 128 + r;
+    const float4* po = reinterpret_cast<const float4*>(part_o + ((size_t)j.slot0 * 128 + r) * 128) + lane;
     float M = -INFINITY;
-#pragma unroll
-    for (uint32_t s = 0; s < kMaxSplits; ++s)
-        if (s < n) M = fmaxf(M, ml[s].x);
+#pragma unroll 4
+    for (uint32_t s = 0; s < n; ++s) M = fmaxf(M, __ldcg(ml + (size_t)s * 128).x);
     float L = 0.0f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t s0 = 0; s0 < n; s0 += 4) {
+        float4 ov[4];
+        float2 w[4];
 #pragma unroll
-    for (uint32_t s = 0; s < kMaxSplits; ++s)
-        if (s < n) {
-            const float w = ml[s].x == -INFINITY ? 0.0f : exp2f(ml[s].x - M);
-            L += w * ml[s].y;
-            acc.x += w * ov[s].x;
-            acc.y += w * ov[s].y;
-            acc.z += w * ov[s].z;
-            acc.w += w * ov[s].w;
-        }
+        for (uint32_t i = 0; i < 4; ++i)
+            if (s0 + i < n) {
+                w[i] = __ldcg(ml + (size_t)(s0 + i) * 128);
+                ov[i] = __ldcs(po + (size_t)(s0 + i) * 128 * 32);
+            }
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i)
+            if (s0 + i < n) {
+                const float wt = w[i].x == -INFINITY ? 0.0f : exp2f(w[i].x - M);
+                L += wt * w[i].y;
+                acc.x += wt * ov[i].x;
+                acc.y += wt * ov[i].y;
+                acc.z += wt * ov[i].z;
+                acc.w += wt * ov[i].w;
+            }
+    }
     const float inv = L > 0.0f ? 1.0f / L : 0.0f;
     uint2 pk;
     pk.x = pack_bf16(acc.x * inv, acc.y * inv);
