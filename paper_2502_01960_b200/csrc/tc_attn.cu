@@ -593,7 +593,11 @@ AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads, cons
         total += (uint64_t)(nblk[t] - sblk[t]) * n_heads;
     }
     // ~1.5 waves of items (an item carries up to two tiles); never split below 2 blocks
-    uint32_t chunk = (uint32_t)std::max<uint64_t>(2, (total + 3 * kNumSMs - 1) / (3 * kNumSMs));
+    static const uint32_t per_sm = [] {
+        const char* e = getenv("MPIC_ATTN_CHUNKS_PER_SM");  // diagnostics: tile-chunks per SM
+        return e ? (uint32_t)std::max(1, atoi(e)) : 3u;
+    }();
+    uint32_t chunk = (uint32_t)std::max<uint64_t>(2, (total + per_sm * kNumSMs - 1) / (per_sm * kNumSMs));
     uint32_t longest = 0, last = 0;
     for (uint32_t t = 0; t < tiles; ++t) {
         longest = std::max(longest, nblk[t] - sblk[t]);
@@ -641,7 +645,17 @@ AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads, cons
         }
     }
     // longest items first (they set the critical path); items of one head stay together
-    std::stable_sort(plan.units.begin(), plan.units.end(), [](const AttnUnit& a, const AttnUnit& b) {
+    // Longest-processing-time first by estimated cost: a block costs ~1.5x for a pair of
+    // tiles (ping-pong hides part of one tile's softmax behind the other's MMAs) than for
+    // one tile; per-item setup ~2 blocks.
+    static const bool by_cost = getenv("MPIC_ATTN_SORT_LEN") == nullptr;  // diagnostics: 1 = by length
+    auto cost = [](const AttnUnit& a) {
+        const uint32_t len = std::max(a.b1[0], a.tile[1] == kNoTile ? 0u : a.b1[1]) - a.b0;
+        const uint32_t both = a.tile[1] == kNoTile ? 0u : std::min(a.b1[0], a.b1[1]) - a.b0;
+        return 2 * (len - both) + 3 * both + 4;  // half-block units
+    };
+    std::stable_sort(plan.units.begin(), plan.units.end(), [&](const AttnUnit& a, const AttnUnit& b) {
+        if (by_cost) return cost(a) > cost(b);
         const uint32_t la = std::max(a.b1[0], a.tile[1] == kNoTile ? 0u : a.b1[1]) - a.b0;
         const uint32_t lb = std::max(b.b1[0], b.tile[1] == kNoTile ? 0u : b.b1[1]) - b.b0;
         return la > lb;
