@@ -1448,12 +1448,14 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
         const AsmChunk* dch = static_cast<const AsmChunk*>(ws->d_asm);
         const float2* dtab = reinterpret_cast<const float2*>((char*)ws->d_asm + bytes_c);
         std::function<void(uint32_t)> wait_layer;
-        // per-layer overlap pays only when the copy is long enough to hide behind the GEMMs
-        // (config C: 4.8 GB); small requests assemble in one launch up front (config B)
+        // per-layer overlap pays only when the copy is long enough to hide behind the GEMMs:
+        // a large request whose chunks are NOT linked inside attention. With linking the
+        // assembly is only the partial blocks (config C: 0.23 ms in one launch up front, the
+        // same request time as overlapped); small requests assemble up front too (config B)
         uint64_t asm_bytes = 0;
         for (uint32_t i = 0; i < n_img; ++i)
             asm_bytes += (uint64_t)r.refs[i].rows * linked->L * linked->H * linked->D * esz(linked->dtype) * 2;
-        if (asm_overlap && asm_bytes >= (2ull << 30)) {
+        if (asm_overlap && !link && asm_bytes >= (2ull << 30)) {
             // Layer l of the assembly runs on a side stream and only layer l's QKV waits for it:
             // the HBM-bound copy of layers l+1.. overlaps the tensor-bound GEMMs of layer l.
             ensure_asm_stream(ws, model->cfg.n_layers);
