@@ -87,3 +87,33 @@ def test_batch_of_one_equals_single_request():
     batch, mrows = mp.request_prefill_batch(m, ws, [p], [chunks], l2, k=32)
     assert mrows[0] == len(sel)
     assert rel_err(batch[0], single) < 1e-3
+
+
+@pytest.mark.parametrize("reposition", [mp.AS_STORED, mp.REROTATE])
+def test_batch_matches_single_requests(reposition):
+    """Each request of a batch against the same request run alone on the GPU (Rerotate too:
+    a chunk's rotation delta stays relative to its own request)."""
+    L, H, D, V = 2, 2, 128, 1024
+    cfg = mp.config(L, H, D, vocab_size=V, image_token_count=64, seed=9)
+    rng = np.random.default_rng(9)
+    reqs = _requests(rng, L, H, D, V, [[("t", 12), ("i", 180), ("t", 5), ("i", 90), ("t", 7)],
+                                       [("t", 40)], [("t", 3), ("i", 257), ("t", 30)]])
+    m = mp.Model(cfg, mp.BF16)
+    prompts = [mp.Prompt.from_segments(segs) for segs, _, _ in reqs]
+    ns = [p.n for p in prompts]
+    ws = mp.Workspace(m, sum(ns), sum(ns))
+    chunks = [[mp.KV.from_host(a, b, H, D, mp.BF16) for a, b in zip(ck, cv)] for _, ck, cv in reqs]
+    big = mp.KV(L, sum(ns), H, D, mp.BF16)
+    logits, mrows = mp.request_prefill_batch(m, ws, prompts, chunks, big, k=16, reposition=reposition)
+    kb, vb = big.download()
+    off = 0
+    for r, p in enumerate(prompts):
+        one = mp.KV(L, p.n, H, D, mp.BF16)
+        lg, sel = mp.request_prefill(m, ws, p, chunks[r], one, k=16, reposition=reposition)
+        k1, v1 = one.download()
+        assert mrows[r] == len(sel)
+        # same kernels, different GEMM tilings (sum(m) rows vs m): bf16 rounding flips only
+        assert rel_err(logits[r], lg) < 1e-2, (r, rel_err(logits[r], lg))
+        assert rel_err(kb[:, off:off + p.n], k1) < 1e-2
+        assert rel_err(vb[:, off:off + p.n], v1) < 1e-2
+        off += p.n
