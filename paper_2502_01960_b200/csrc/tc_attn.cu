@@ -155,8 +155,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     uint64_t* s_full = v_empty + kVStages;       // [2 tiles]
     uint64_t* p_full = s_full + 2;               // [2 tiles]
     uint64_t* o_done = p_full + 2;               // [2 tiles]
-    uint64_t* p_half = o_done + 2;               // [2 tiles] P_X(j) keys 0-63 written
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(p_half + 2);
+    uint64_t* p_part = o_done + 2;               // [2 tiles][3] P_X(j) keys [0, 32(q+1)) written
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(p_part + 6);
 
     tc::pdl_trigger();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&s_full[i], 1);
             tc::mbar_init(&p_full[i], 128);
-            tc::mbar_init(&p_half[i], 128);
+            for (int q = 0; q < 3; ++q) tc::mbar_init(&p_part[3 * i + q], 128);
             tc::mbar_init(&o_done[i], 1);
         }
         tc::fence_barrier_init();
@@ -272,15 +272,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 for (uint32_t x = 0; x < 2; ++x) {
                     if (j >= nbx[x]) continue;
                     const uint32_t va = tc::smem_u32(sV + st * kTile);
-                    // PV_X(j) in two halves: keys 0-63 as soon as the softmax has written that
-                    // half of P (it then works on keys 64-127 while these MMAs run)
+                    // PV_X(j) in quarters: keys [32q, 32q+32) as soon as the softmax has written
+                    // that part of P (it works on the next keys while these MMAs run)
 #pragma unroll
-                    for (uint32_t hf = 0; hf < 2; ++hf) {
-                        tc::mbar_wait(hf ? &p_full[x] : &p_half[x], j & 1);
-                        if (hf && p.dbg && blockIdx.x == 0) p.dbg[j * 16 + 2 + x] = globaltimer_ns();
+                    for (uint32_t hf = 0; hf < 4; ++hf) {
+                        tc::mbar_wait(hf == 3 ? &p_full[x] : &p_part[3 * x + hf], j & 1);
+                        if (hf == 3 && p.dbg && blockIdx.x == 0) p.dbg[j * 16 + 2 + x] = globaltimer_ns();
                         tc::tc_fence_after();
 #pragma unroll
-                        for (uint32_t kk = 4 * hf; kk < 4 * hf + 4; ++kk)  // A = P_X(j) from TMEM: 16 keys = 8 packed columns
+                        for (uint32_t kk = 2 * hf; kk < 2 * hf + 2; ++kk)  // A = P_X(j) from TMEM: 16 keys = 8 packed columns
                             tc::mma_bf16_ts(tmem + x * 256 + 128, tmem + x * 256 + kk * 8,
                                             tc::desc_mn_sw128(va + kk * 2048, kHalf), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
                     }
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     for (uint32_t c = 0; c < 4; ++c) tc::tmem_st16(s_col + c * 16, z);
                     tc::tmem_st_wait();
                     tc::tc_fence_before();
-                    tc::mbar_arrive(&p_half[x]);
+                    for (int q = 0; q < 3; ++q) tc::mbar_arrive(&p_part[3 * x + q]);
                     tc::mbar_arrive(&p_full[x]);
                     continue;
                 }
@@ -478,10 +478,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                         for (uint32_t e = 0; e < 16; ++e) pk[e] = 0u;
                     }
                     tc::tmem_st16(s_col + c * 16, pk);
-                    if (c == 1) {  // keys 0-63 of P_X(j) are in TMEM: the first half of PV can go
+                    if (c < 3) {  // keys [0, 32(c+1)) of P_X(j) are in TMEM: that part of PV can go
                         tc::tmem_st_wait();
                         tc::tc_fence_before();
-                        tc::mbar_arrive(&p_half[x]);
+                        tc::mbar_arrive(&p_part[3 * x + c]);
                     }
                 }
                 if (dbg_me) p.dbg[j * 16 + 9] = globaltimer_ns();
@@ -720,7 +720,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
         return e && atoi(e) == 2;
     }();
     p.link_nostore = nostore ? 1u : 0u;
-    const size_t smem = (2 + kKStages + kVStages) * kTile + 1024 + (1 + 2 * kKStages + 2 * kVStages + 8) * 8 + 16;
+    const size_t smem = (2 + kKStages + kVStages) * kTile + 1024 + (1 + 2 * kKStages + 2 * kVStages + 12) * 8 + 16;
     static bool attr = false;
     if (!attr) {
         MPIC_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
