@@ -2144,9 +2144,18 @@ int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mp
     std::vector<bool> copied(L, false);
     std::vector<uint32_t> done(L, 0);
     std::string reader_error;
+    // work items: every segment cut into `pieces` parts so that all but two host cores read
+    // and checksum in parallel (the piece CRCs are combined in file order at the end)
     const uint32_t n_seg = 2 * n_img;
-    const uint32_t n_threads = std::max<uint32_t>(1, std::min<uint32_t>(
-        n_seg, std::max<uint32_t>(1, std::thread::hardware_concurrency() / 2)));
+    const uint32_t hw = std::max<uint32_t>(1, std::thread::hardware_concurrency());
+    const uint32_t want = std::max<uint32_t>(1, hw > 4 ? hw - 2 : hw);
+    const uint32_t pieces = std::max<uint32_t>(1, std::min<uint32_t>(8, ceil_div(want, n_seg)));
+    const uint32_t n_items = n_seg * pieces;
+    const uint32_t n_threads = std::max<uint32_t>(1, std::min<uint32_t>(n_items, want));
+    for (uint32_t i = 0; i < n_img; ++i) {
+        files[i]->crc_k.assign((size_t)L * pieces, 0);
+        files[i]->crc_v.assign((size_t)L * pieces, 0);
+    }
     auto read_worker = [&](uint32_t w) {
         try {
             for (uint32_t l = 0; l < L; ++l) {
@@ -2159,14 +2168,16 @@ int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mp
                     MPIC_CUDA(cudaEventSynchronize(ws->ev_pin[sl]));
                 }
                 char* dst = static_cast<char*>(ws->pin[sl]);
-                for (uint32_t sg = w; sg < n_seg; sg += n_threads) {
+                for (uint32_t it = w; it < n_items; it += n_threads) {
+                    const uint32_t sg = it / pieces, pc = it % pieces;
                     const uint32_t i = sg >> 1;
                     const bool is_v = sg & 1;
                     MpicFile& f = *files[i];
                     const size_t seg = (size_t)f.T * h * es;
-                    char* d = dst + ((is_v ? img_rows * h : 0) + off[i]) * es;
-                    pread_all(f.fd, d, seg, (off_t)(84 + ((is_v ? (size_t)L : 0) + l) * seg));
-                    (is_v ? f.crc_v : f.crc_k)[l] = crc_of(d, seg);
+                    const size_t p0 = seg * pc / pieces, p1 = seg * (pc + 1) / pieces;
+                    char* d = dst + ((is_v ? img_rows * h : 0) + off[i]) * es + p0;
+                    pread_all(f.fd, d, p1 - p0, (off_t)(84 + ((is_v ? (size_t)L : 0) + l) * seg + p0));
+                    (is_v ? f.crc_v : f.crc_k)[(size_t)l * pieces + pc] = crc_of(d, p1 - p0);
                 }
                 {
                     std::lock_guard<std::mutex> lk(mu);
@@ -2236,8 +2247,12 @@ int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mp
         MpicFile& f = *files[i];
         const size_t seg = (size_t)f.T * h * es;
         uLong c = f.crc_header;
-        for (uint32_t l = 0; l < L; ++l) c = crc32_combine(c, f.crc_k[l], (z_off_t)seg);
-        for (uint32_t l = 0; l < L; ++l) c = crc32_combine(c, f.crc_v[l], (z_off_t)seg);
+        for (int is_v = 0; is_v < 2; ++is_v)
+            for (uint32_t l = 0; l < L; ++l)
+                for (uint32_t pc = 0; pc < pieces; ++pc) {
+                    const size_t p0 = seg * pc / pieces, p1 = seg * (pc + 1) / pieces;
+                    c = crc32_combine(c, (is_v ? f.crc_v : f.crc_k)[(size_t)l * pieces + pc], (z_off_t)(p1 - p0));
+                }
         MPIC_REQUIRE((uint32_t)c == f.crc_stored, MPIC_ERR_INTEGRITY,
                      std::string("crc mismatch in ") + paths[i] + ": the chunk must be recomputed");
     }
