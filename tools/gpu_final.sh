@@ -20,6 +20,7 @@ timeout 300 python bench.py --config A --no-cpu-baseline > $OUT/bench_A.log 2>&1
 timeout 900 python bench.py --config E --steps 3 > $OUT/bench_E.log 2>&1
 timeout 600 python bench.py --mode head-parallel --steps 5 > $OUT/bench_E16_hp.log 2>&1
 timeout 600 python bench.py --config C --disk --no-e2e-fp32 --no-cpu-baseline --steps 5 > $OUT/bench_C_disk.log 2>&1
+timeout 900 python bench.py --config D --disk --no-e2e --no-cpu-baseline --steps 3 > $OUT/bench_D_disk.log 2>&1
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $OUT/bench_ref.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
   --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
