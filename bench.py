@@ -449,7 +449,10 @@ def run_ours(args, world, rank, local):
         wall = time.perf_counter() - t0
         e2e_steps = [ev2[i].elapsed_time(ev2[i + 1]) for i in range(args.steps)]
         e_ms = allreduce_max(ev2[0].elapsed_time(ev2[-1]), world)
-        h2d = sum(x.array.nbytes for x in ks + vs) + 2 * 4 * m
+        # the loader skips each chunk's leading recomputed rows (its first k under MPIC-k)
+        lead = sum(min(k, sg[2]) for sg in segs if sg[0] == "image")
+        skipped = 2 * lead * L * h * ks[0].array.itemsize if ks else 0
+        h2d = sum(x.array.nbytes for x in ks + vs) - skipped + 2 * 4 * m
         return {"value": world * n * args.steps / (e_ms / 1e3), "unit": "prompt tokens/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * V),
                 "ttft_p50_ms": float(statistics.median(e2e_steps)), "wall_s": wall,

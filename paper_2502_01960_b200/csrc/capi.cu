@@ -1942,6 +1942,18 @@ int mpic_request_prefill_host2(mpic_model_t model, mpic_workspace_t ws, const mp
     const size_t e = esz(linked->dtype);
     const size_t plane = (size_t)linked->T * h * e;
     cudaStream_t cs = ws->copy_stream;
+    // The leading rows of a chunk that the request recomputes anyway (MPIC-k: its first k)
+    // are not copied: the assembly moves whatever the staging slot holds there and the
+    // layer's QKV scatter overwrites those cache rows before anything reads them.
+    std::vector<uint32_t> lead(n_img, 0);
+    for (uint32_t i = 0; i < n_img; ++i) {
+        const uint32_t d0 = r.refs[i].dst_row0;
+        auto it = std::lower_bound(r.sel.begin(), r.sel.end(), d0);
+        while (it != r.sel.end() && lead[i] < r.refs[i].rows && *it == d0 + lead[i]) {
+            ++lead[i];
+            ++it;
+        }
+    }
     // The copy lane may not start before the plans (and any earlier user of the ring)
     // are done on the compute stream.
     MPIC_CUDA(cudaEventRecord(ws->ev_free[0], s));
@@ -1951,12 +1963,14 @@ int mpic_request_prefill_host2(mpic_model_t model, mpic_workspace_t ws, const mp
         char* base = static_cast<char*>(ws->stage[sl]);
         MPIC_CUDA(cudaStreamWaitEvent(cs, ws->ev_free[sl], 0));
         for (uint32_t i = 0; i < n_img; ++i) {
-            const size_t cnt = (size_t)r.refs[i].rows * h;
-            MPIC_CUDA(cudaMemcpyAsync(base + off[i] * es, static_cast<const char*>(chunk_k[i]) + (size_t)l * cnt * es,
-                                      cnt * es, cudaMemcpyHostToDevice, cs));
-            MPIC_CUDA(cudaMemcpyAsync(base + (img_rows * h + off[i]) * es,
-                                      static_cast<const char*>(chunk_v[i]) + (size_t)l * cnt * es, cnt * es,
-                                      cudaMemcpyHostToDevice, cs));
+            const size_t cnt = (size_t)r.refs[i].rows * h, skip = (size_t)lead[i] * h;
+            if (skip == cnt) continue;
+            MPIC_CUDA(cudaMemcpyAsync(base + (off[i] + skip) * es,
+                                      static_cast<const char*>(chunk_k[i]) + ((size_t)l * cnt + skip) * es,
+                                      (cnt - skip) * es, cudaMemcpyHostToDevice, cs));
+            MPIC_CUDA(cudaMemcpyAsync(base + (img_rows * h + off[i] + skip) * es,
+                                      static_cast<const char*>(chunk_v[i]) + ((size_t)l * cnt + skip) * es,
+                                      (cnt - skip) * es, cudaMemcpyHostToDevice, cs));
         }
         MPIC_CUDA(cudaEventRecord(ws->ev_ready[sl], cs));
     };
