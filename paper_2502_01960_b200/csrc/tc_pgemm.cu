@@ -54,6 +54,7 @@ constexpr uint32_t kPgWBytes = 128 * 64 * 2;  // one CTA's weight rows per k-blo
 constexpr uint32_t kChunkBytes = 32 * 128 * 4;  // one 32-token x 128-feature fp32 chunk
 constexpr uint32_t kNoStage = 0xffffffffu;
 constexpr uint32_t kStageSlice = 4096;  // one epilogue warp's staging slice
+constexpr uint32_t kEpiBars = 16;       // QKV side-input barriers: one per 32-token chunk of a group
 
 struct PgArgs {
     uint32_t M, N, K;
@@ -358,8 +359,8 @@ __global__ void __launch_bounds__(kPgThreads, 1)
     uint64_t* empty = full + a.stages;
     uint64_t* acc_full = empty + a.stages;  // [2]
     uint64_t* acc_empty = acc_full + 2;     // [2], the even CTA's copy is the one used
-    uint64_t* epi_bar = acc_empty + 2;      // epilogue side-input staging (bulk copies)
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(epi_bar + 1);
+    uint64_t* epi_bar = acc_empty + 2;      // [kEpiBars] epilogue side-input staging, one per 32-token chunk
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(epi_bar + kEpiBars);
 
     tc::pdl_trigger();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(kPgThreads, 1)
             tc::mbar_init(&acc_full[b], 1);
             tc::mbar_init(&acc_empty[b], 16);  // 8 epilogue warps x 2 CTAs
         }
-        tc::mbar_init(epi_bar, 1);
+        for (uint32_t i = 0; i < kEpiBars; ++i) tc::mbar_init(&epi_bar[i], 1);
         tc::fence_barrier_init();
     }
     if (warp == 0 && lane == 0 && cl < a.tiles) {
@@ -537,17 +538,26 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                     // both CTAs of the pair need the same rows: each loads half of the (cos, sin)
                     // rows and multicasts it to the pair (halves the L2 reads of a table every
                     // CTA of the grid wants at once); V-only pairs need no rotation
+                    // Chunk c's rows arrive on epi_bar[c] (the rows table with chunk 0), so the
+                    // epilogue starts on the first chunk while the later ones are in flight; the
+                    // two CTAs alternate chunks and multicast each to the pair.
                     const bool rot = fb * 256 < 2 * a.ep.hidden;
-                    const uint32_t half_tok = nt / 2, mine = rank ? nt - half_tok : half_tok;
+                    const uint32_t nch = (nt + 31) / 32;
+                    (void)rope_bytes;
                     if (warp == 2 && lane == 0) {
-                        tc::mbar_arrive_expect_tx(epi_bar, (rot ? rope_bytes : 0u) + rows_bytes);
-                        if (rot && mine)
-                            tc::bulk_load_mcast(smem + (size_t)rank * half_tok * hd2 * 8,
-                                                a.ep.rope_tok + (size_t)(tg + rank * half_tok) * hd2, mine * hd2 * 8,
-                                                epi_bar, (uint16_t)(0x3u << (crank & ~1u)));
-                        tc::bulk_load(smem + a.rows_off, a.ep.kv_rows + tg, rows_bytes, epi_bar);
+                        for (uint32_t ci = 0; ci < nch; ++ci) {
+                            const uint32_t cnt = min(32u, nt - 32 * ci);
+                            tc::mbar_arrive_expect_tx(&epi_bar[ci], (rot ? cnt * hd2 * 8 : 0u) + (ci ? 0u : rows_bytes));
+                        }
+                        if (rot)
+                            for (uint32_t ci = rank; ci < nch; ci += 2) {
+                                const uint32_t cnt = min(32u, nt - 32 * ci);
+                                tc::bulk_load_mcast(smem + (size_t)ci * 32 * hd2 * 8, a.ep.rope_tok + (size_t)(tg + 32 * ci) * hd2,
+                                                    cnt * hd2 * 8, &epi_bar[ci], (uint16_t)(0x3u << (crank & ~1u)));
+                            }
+                        tc::bulk_load(smem + a.rows_off, a.ep.kv_rows + tg, rows_bytes, &epi_bar[0]);
                     }
-                    tc::mbar_wait(epi_bar, 0);
+                    tc::mbar_wait(&epi_bar[0], 0);
                     s_rope = reinterpret_cast<const float2*>(smem);
                     s_rows = reinterpret_cast<const uint32_t*>(smem + a.rows_off);
                 }
@@ -555,6 +565,7 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                 if (!(a.dbg & 1))
                     for (uint32_t c = half * 32; c < a.G && tg + c < tend; c += 64) {
                         uint32_t r[32];
+                        if (a.stage_rope && c) tc::mbar_wait(&epi_bar[c / 32], 0);  // this chunk's side inputs
                         const long long q0 = ts ? clock64() : 0;
                         tc::tmem_ld32(dcol + c, r);
                         tc::tmem_ld_wait();
@@ -825,7 +836,7 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
         a.w_evict_first = a.ngroups == 1;
         a.ep = ep_in;
     a.ep.dbg = dbg;
-        const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 5) * 8 + 16;
+        const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 4 + kEpiBars) * 8 + 16;
         const uint32_t nchunks = (a.G + 31) / 32;
         // MMA cycles per k-block (4 k16 steps): a cta_group::2 instruction costs
         // max(N/2, ~83) cycles, and a lone accumulator chain issues ~1.5x slower than two
@@ -872,7 +883,7 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
     }();
     a.pfd = pfd_env >= 0 ? (uint32_t)pfd_env : 2 * a.stages * a.kps;
 
-    const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 5) * 8 + 16;
+    const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 4 + kEpiBars) * 8 + 16;
     static const bool verbose = getenv("MPIC_PG_VERBOSE") != nullptr;
     if (verbose)
         fprintf(stderr, "pgemm M=%u N=%u K=%u: groups=%u P0=%u P1=%u S=%u clusters=%u stages=%u x %u kb nbuf=%u\n", M,
