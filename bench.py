@@ -128,9 +128,14 @@ def run_serving(args, world, rank, local):
         ws = mp.Workspace(model, max(ms) if ms else 1, max(ns) if ns else 1)
         linked = {n: mp.KV(L, n, H, D, mp.BF16, local) for n in sorted(set(ns))}
 
-    def step(ttft=None):
+    batch_ms = []
+
+    def step(ttft=None, clk=None):
         for b in batches:
             t0 = time.perf_counter()
+            if ttft is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
             if B > 1:
                 mp.request_prefill_batch(model, ws, [prompts[j] for j in b],
                                          [[pool[c] for c in reqs[mine[j]][1]] for j in b], big, k=k, stream=stream)
@@ -140,6 +145,12 @@ def run_serving(args, world, rank, local):
                                    k=k, stream=stream)
             if ttft is not None:  # every request of a batch gets its logits when the batch ends
                 ttft.extend([(time.perf_counter() - t0) * 1e3] * len(b))
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(stream)
+                if clk is not None:
+                    clk.probe(stream)  # the SM clock right after the batch (device-side)
+                e1.synchronize()
+                batch_ms.append(round(e0.elapsed_time(e1), 2))
 
     for _ in range(args.warmup):
         step()
@@ -147,18 +158,27 @@ def run_serving(args, world, rank, local):
     barrier(world)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ttft = []
-    with torch.cuda.stream(stream):
+    clk = ClockSampler(local, args.steps * len(batches))
+    import gc
+    gc.collect()
+    gc.disable()  # a full Python GC inside the region stalled single steps by 0.3-1.2 s (MPIC_BENCH_GC=1 keeps it)
+    if os.environ.get("MPIC_BENCH_GC") == "1":
+        gc.enable()
+    with clk, torch.cuda.stream(stream):
         ev[0].record(stream)
         for _ in range(args.steps):
-            step(ttft)
+            step(ttft, clk)
         ev[1].record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     ms_total = allreduce_max(ev[0].elapsed_time(ev[1]), world)
     tok_all = sum(mp.Prompt.from_segments(sg).n for sg, _ in reqs)
     rows_all = sum(len(mp.select_tokens(mp.Prompt.from_segments(sg), mp.POLICY_MPIC_K, k)) for sg, _ in reqs)
     return dict(value=tok_all * args.steps / (ms_total / 1e3), ms_per_step=ms_total / args.steps,
                 ttft_p50=float(statistics.median(ttft)) if ttft else None, n=tok_all, m=rows_all,
-                rows_per_s=rows_all * args.steps / (ms_total / 1e3), mine=len(mine), world=world)
+                rows_per_s=rows_all * args.steps / (ms_total / 1e3), mine=len(mine), world=world,
+                batch_ms=batch_ms, clocks=clk.summary(),
+                batch_sm_mhz=[round(x) for x in clk.buf[:clk.i].cpu().tolist()])
 
 
 
@@ -382,6 +402,9 @@ def run_ours(args, world, rank, local):
     launches = 0
     per_step = []
     host_ms = []
+    import gc
+    gc.collect()
+    gc.disable()  # a full collection inside a timed region stalls submission for 100s of ms
     with ClockSampler(dev, args.steps) as clk:
         with torch.cuda.stream(stream):
             ev[0].record(stream)
@@ -392,6 +415,7 @@ def run_ours(args, world, rank, local):
                 ev[i + 1].record(stream)
                 host_ms.append((time.perf_counter() - h0) * 1e3)
         torch.cuda.synchronize()
+    gc.enable()
     barrier(world)
     for i in range(args.steps):
         per_step.append(ev[i].elapsed_time(ev[i + 1]))
@@ -615,16 +639,26 @@ def run_head_parallel(args, world, rank, local):
     torch.cuda.synchronize()
     barrier(world)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    ev[0].record(stream)
-    for i in range(args.steps):
-        step()
-        ev[i + 1].record(stream)
-    torch.cuda.synchronize()
+    clk = ClockSampler(local, args.steps)
+    import gc
+    gc.collect()
+    gc.disable()
+    if os.environ.get("MPIC_BENCH_GC") == "1":
+        gc.enable()
+    with clk:
+        ev[0].record(stream)
+        for i in range(args.steps):
+            step()
+            ev[i + 1].record(stream)
+            clk.probe(stream)
+        torch.cuda.synchronize()
+    gc.enable()
     barrier(world)
     per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     total = allreduce_max(ev[0].elapsed_time(ev[-1]), world)
     return dict(value=n * args.steps / (total / 1e3), ms_per_step=total / args.steps,
-                per_step=per_step, n=n, m=eng.m, world=world)
+                per_step=per_step, n=n, m=eng.m, world=world, clocks=clk.summary(),
+                step_sm_mhz=[round(x) for x in clk.buf[:clk.i].cpu().tolist()])
 
 
 def cpu_reference(cfg_name, steps, warmup, threads=None, layers_sample=2, seed=42):
@@ -774,7 +808,9 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded ids and hashes, U(-0.5,0.5) chunk KV, weights synthesised from seed 1)",
                 "config": dict(cfg_json, n_tokens=r["n"], recompute_rows=r["m"],
-                               parallelism=f"head-parallel x{world} (NCCL reduce-scatter + all-gather per layer)")}))
+                               parallelism=f"head-parallel x{world} (NCCL reduce-scatter + all-gather per layer)"),
+                "step_ms": [round(x, 3) for x in r["per_step"]], "step_sm_mhz": r["step_sm_mhz"],
+                "clocks": r["clocks"]}))
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
@@ -801,7 +837,8 @@ def main():
                                batch=max(1, args.batch),
                                parallelism=f"request-sharded x{world} (LPT by predicted cost, no collective)",
                                l2="inputs larger than L2: 12.9 GB bf16 weights stream through HBM per request"),
-                "recompute_rows_per_s": r["rows_per_s"], "cpu_baseline": cpu,
+                "recompute_rows_per_s": r["rows_per_s"], "cpu_baseline": cpu, "batch_ms": r["batch_ms"],
+                "batch_sm_mhz": r["batch_sm_mhz"], "clocks": r["clocks"],
                 "ttft": "host wall time per request (submission -> logits on the host), p50 over rank 0's requests"}))
         if world > 1:
             import torch.distributed as dist
