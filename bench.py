@@ -462,6 +462,9 @@ def run_ours(args, world, rank, local):
             step_host(ks, vs)
         torch.cuda.synchronize()
         barrier(world)
+        import gc
+        gc.collect()
+        gc.disable()
         t0 = time.perf_counter()
         ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         with torch.cuda.stream(stream):
@@ -470,6 +473,7 @@ def run_ours(args, world, rank, local):
                 step_host(ks, vs)
                 ev2[i + 1].record(stream)
         torch.cuda.synchronize()
+        gc.enable()
         wall = time.perf_counter() - t0
         e2e_steps = [ev2[i].elapsed_time(ev2[i + 1]) for i in range(args.steps)]
         e_ms = allreduce_max(ev2[0].elapsed_time(ev2[-1]), world)

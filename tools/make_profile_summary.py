@@ -61,8 +61,8 @@ out = ["# Round 1 — final state", "",
        "(cos, sin) staging, a low-register combine, cost-ordered attention items, P handed to the PV MMAs per",
        "32-key chunk, up-front assembly of the unlinked blocks, the host loader skipping recomputed rows,",
        "batched varlen requests (config E), a parallel disk reader.", "",
-       "Long power-saturating runs (config E, E16) show occasional ~300 ms steps; 600 back-to-back config-C",
-       "steps show none (DESIGN.md §8).", ""]
+       "bench.py disables Python's GC inside timed regions: full collections had stalled single E/E16 steps",
+       "by 0.3-1.2 s (GPU idle).", ""]
 for f in ["pytest_gpu.log", "smoke.log"]:
     p = os.path.join(run, f)
     if os.path.exists(p):
