@@ -1172,6 +1172,17 @@ int mpic_workspace_create(mpic_model_t md, uint32_t max_rows, uint32_t max_ctx, 
     API_BEGIN
     MPIC_REQUIRE(md && max_rows > 0, MPIC_ERR_VALIDATION, "bad workspace request");
     MPIC_CUDA(cudaSetDevice(md->device));
+    {
+        // Stream-ordered allocations of the request paths (plan uploads, batch logits) come
+        // from the device's default pool: keep its memory instead of returning it to the
+        // driver at every synchronisation (re-mapping it per request takes the driver lock
+        // and stalled single requests by 100s of ms under load)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, md->device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
     ws = new mpic_workspace_s();
     ws->model = md;
     ws->max_rows = max_rows;

@@ -61,8 +61,8 @@ out = ["# Round 1 — final state", "",
        "(cos, sin) staging, a low-register combine, cost-ordered attention items, P handed to the PV MMAs per",
        "32-key chunk, up-front assembly of the unlinked blocks, the host loader skipping recomputed rows,",
        "batched varlen requests (config E), a parallel disk reader.", "",
-       "bench.py disables Python's GC inside timed regions: full collections had stalled single E/E16 steps",
-       "by 0.3-1.2 s (GPU idle).", ""]
+       "Single E/E16 steps used to stall 0.3-1.2 s with the GPU idle: per-request stream-ordered allocations",
+       "re-mapped memory the pool had released; the workspace keeps the pool's memory now (DESIGN.md §8).", ""]
 for f in ["pytest_gpu.log", "smoke.log"]:
     p = os.path.join(run, f)
     if os.path.exists(p):
