@@ -881,7 +881,10 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
         const char* e = getenv("MPIC_PG_PFD");  // diagnostics: weight L2 prefetch distance (k-blocks)
         return e ? atoi(e) : -1;
     }();
-    a.pfd = pfd_env >= 0 ? (uint32_t)pfd_env : 2 * a.stages * a.kps;
+    // The producer's L2 prefetch of weights ahead of the smem ring is off by default: it cost
+    // 2.7% at config C and 10% at config B (m = 96) — the extra requests compete with the
+    // ring's own loads; MPIC_PG_PFD=<k-blocks> turns it back on for diagnostics.
+    a.pfd = pfd_env >= 0 ? (uint32_t)pfd_env : 0u;
 
     const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 4 + kEpiBars) * 8 + 16;
     static const bool verbose = getenv("MPIC_PG_VERBOSE") != nullptr;
