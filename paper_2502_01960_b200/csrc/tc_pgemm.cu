@@ -790,7 +790,9 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
     double best = 1e30;
     // Plan: token groups (1 natural, or the tokens cut into 2-3 groups to create tiles) x
     // in-cluster K split S. Cost model per pair, in cycles: rounds x k-blocks x
-    // max(MMA 2G, operand fill 256 + G) (+ a reduction allowance for S > 1).
+    // max(MMA 2G, operand fill 256 + G), plus for S > 1 the DSMEM reduction and owner
+    // epilogue: ~2000 + 40 per token column pushed ((S-1)/S of the group) — fitted to the
+    // measured Wo/W2 launches at config C (Wo: 2 groups x S=2 beats 1 x S=3 by 2 us).
     const uint32_t ng_nat = M <= 512 ? 1 : ceil_div(M, 256);
     for (uint32_t gm : {1u, 2u, 3u}) {
         PgArgs a{};
@@ -855,7 +857,7 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
             if (S > 1 && (a.tiles > C || (size_t)S * ceil_div(nchunks, S) * kChunkBytes > (size_t)a.stages * a.stage_bytes))
                 continue;
             const double cost = (double)ceil_div(a.tiles, std::min(C, a.tiles)) * ceil_div(a.kblocks, S) * t_kb +
-                                (S > 1 ? 2000.0 : 0.0) + (force_s > 1 && S == 1 ? 1e20 : 0.0);
+                                (S > 1 ? 2000.0 + 40.0 * a.G * (S - 1) / S : 0.0) + (force_s > 1 && S == 1 ? 1e20 : 0.0);
             if (cost < best - 1e-9) {
                 best = cost;
                 best_a = a;
