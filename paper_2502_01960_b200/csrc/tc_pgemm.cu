@@ -80,6 +80,7 @@ struct PgArgs {
                              // issued / epilogue done / exit, %globaltimer ns
     uint32_t w_blocked;  // W stored as [N/128][K/64][128][64] tiles
     uint32_t pfd;        // L2 prefetch distance of the weight stream in k-blocks (0: off)
+    uint32_t prologue_pf;  // prefetch the first k-blocks' weights into L2 before the PDL wait
     uint32_t stg_off;    // staged epilogue stores: byte offset of the 8 x 4 KB warp slices in the
                          // (then idle) stage ring, or kNoStage
     EpiParams ep;
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         for (uint32_t i = 0; i < kEpiBars; ++i) tc::mbar_init(&epi_bar[i], 1);
         tc::fence_barrier_init();
     }
-    if (warp == 0 && lane == 0 && cl < a.tiles) {
+    if (warp == 0 && lane == 0 && cl < a.tiles && a.prologue_pf) {
         // weights do not depend on the previous kernel: start pulling this CTA's first
         // k-blocks into L2 before waiting for it
         const uint32_t fb = cl / a.ngroups, w_row = fb * 256 + (crank & 1) * 128;
@@ -887,6 +888,12 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
     // 2.7% at config C and 10% at config B (m = 96) — the extra requests compete with the
     // ring's own loads; MPIC_PG_PFD=<k-blocks> turns it back on for diagnostics.
     a.pfd = pfd_env >= 0 ? (uint32_t)pfd_env : 0u;
+    static const bool prologue_pf = [] {
+        // off by default, like the ring prefetch: 1% faster at config C without it
+        const char* e = getenv("MPIC_PG_PROLOGUE_PF");  // diagnostics: 1 = prefetch before the PDL wait
+        return e && atoi(e) != 0;
+    }();
+    a.prologue_pf = prologue_pf ? 1u : 0u;
 
     const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 4 + kEpiBars) * 8 + 16;
     static const bool verbose = getenv("MPIC_PG_VERBOSE") != nullptr;
