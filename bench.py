@@ -203,6 +203,40 @@ def build_prompt(cfg_name, V, seed=42):
     return segs
 
 
+def prompt_stats(cfg_name, k=None):
+    """(n prompt tokens, m recomputed rows) of the config's request under MPIC-k
+    (select_tokens, linker.cpp:209-258: every text token + the first k of each image)."""
+    L, H, D, V, images, kk = CONFIGS[cfg_name]
+    k = kk if k is None else k
+    segs = build_prompt(cfg_name, V)
+    n = sum(len(sg[1]) if sg[0] == "text" else sg[2] for sg in segs)
+    m = sum(len(sg[1]) if sg[0] == "text" else min(k, sg[2]) for sg in segs)
+    return n, m
+
+
+def config_json(args):
+    """The `config` object of the JSON line: identical in both arms (--impl ours|reference)."""
+    L, H, D, V, images, k = CONFIGS[args.config]
+    cj = {"workload": WORKLOAD_NAMES[args.config], "layers": L, "heads": H, "head_dim": D,
+          "vocab": V, "image_tokens": images, "k": k,
+          "parallelism": f"request-sharded x{args.gpus} (no collective)",
+          "l2": "inputs larger than L2: 12.9 GB bf16 weights + 4.8 GB chunk KV stream "
+                "through HBM every step"}
+    if args.config == "E":
+        _, reqs = serving_requests(V)
+        cj.update(requests=E_REQUESTS, pool_chunks=E_POOL, batch=max(1, args.batch),
+                  n_tokens_total=sum(sum(len(sg[1]) if sg[0] == "text" else sg[2] for sg in segs)
+                                     for segs, _ in reqs),
+                  parallelism=f"request-sharded x{args.gpus} (LPT by predicted cost, no collective)",
+                  l2="inputs larger than L2: 12.9 GB bf16 weights stream through HBM per request")
+    else:
+        n, m = prompt_stats(args.config, k)
+        cj.update(n_tokens=n, recompute_rows=m)
+    if args.mode == "head-parallel":
+        cj["parallelism"] = f"head-parallel x{args.gpus} (NCCL reduce-scatter + all-gather per layer)"
+    return cj
+
+
 class ClockSampler:
     """Clocks and throttle reasons of the timed region.
 
@@ -741,6 +775,36 @@ def cpu_reference_serving(r, rm, L, ls, H, D, V, k, threads, steps, sample=6):
                        f"assemble_linked_cache + selective_prefill, OpenBLAS {threads} threads"), None
 
 
+def cpu_baseline_legs(cfg_name, thread_counts):
+    """The reference on the host cores, each leg in its own process (so the reference build's
+    .so files never map into the GPU arm). The first count is the headline (None = all
+    cores); the others (1 thread) are reported beside it."""
+    import subprocess
+    out = None
+    for th in thread_counts:
+        one = th == 1
+        cmd = [sys.executable, os.path.abspath(__file__), "--cpu-leg", "--config", cfg_name,
+               "--steps", "1" if (one or cfg_name == "E") else "2", "--warmup", "0" if (one or cfg_name == "E") else "1",
+               "--layers-sample", "1" if one else "2"]
+        if th:
+            cmd += ["--threads", str(th)]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        try:
+            res = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception:
+            res = {"unavailable": (r.stderr or r.stdout)[-300:]}
+        if "ms" not in res:
+            leg = {"value": None, "unavailable": res.get("unavailable")}
+        else:
+            leg = {"value": res["n"] / (res["ms"] / 1e3), "unit": "prompt tokens/s", "cores": res["threads"],
+                   "kind": "reference", "sample": res["sample"], "ttft_ms": res["ms"]}
+        if out is None:
+            out = leg
+        else:
+            out[f"threads_{th}"] = leg
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -762,22 +826,41 @@ def main():
     ap.add_argument("--k", type=int, default=None, help="MPIC-k budget (default: the config's)")
     ap.add_argument("--batch", type=int, default=64,
                     help="config E: requests per batched varlen pass (1 = one request at a time)")
+    ap.add_argument("--no-serving", action="store_true",
+                    help="skip the config-E serving key of the default (config C) line")
+    ap.add_argument("--cpu-leg", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--threads", type=int, default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--layers-sample", type=int, default=2, help=argparse.SUPPRESS)
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
     if args.config is None:
         args.config = "E16" if args.mode == "head-parallel" else "C"
     if args.k is not None:
         c = CONFIGS[args.config]
         CONFIGS[args.config] = c[:5] + (args.k,)
 
+    if args.cpu_leg:  # child process of the cpu_baseline leg (keeps oracle/_ref out of the GPU arm)
+        res, why = cpu_reference(args.config, args.steps, args.warmup, threads=args.threads,
+                                 layers_sample=args.layers_sample)
+        print(json.dumps(res if res is not None else {"unavailable": why}))
+        return
+    args.warmup = max(args.warmup, 3)
+
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one rank per GPU: relaunch this command under torch.distributed.run
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch with torchrun "
+                         f"--nproc-per-node {args.gpus} (or without torchrun: bench.py spawns the ranks)")
     L, H, D, V, images, k = CONFIGS[args.config]
-    cfg_json = {"workload": WORKLOAD_NAMES[args.config], "layers": L, "heads": H, "head_dim": D,
-                "vocab": V, "image_tokens": images, "k": k,
-                "parallelism": f"request-sharded x{args.gpus} (no collective)",
-                "l2": "inputs larger than L2: 12.9 GB bf16 weights + 4.8 GB chunk KV stream "
-                      "through HBM every step"}
+    cfg_json = config_json(args)
 
     if args.impl == "reference":
         if rank != 0:
@@ -790,8 +873,8 @@ def main():
         line = {"metric": "MPIC-k prefill tokens/s (p50 TTFT alongside)", "impl": "reference",
                 "value": val, "unit": "prompt tokens/s", "n_gpus": 0, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": res["ms"], "ttft_p50_ms": res["ms"],
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f32", "data": "synthetic (seeded ids, U(-0.5,0.5) chunk KV)",
+                "higher_is_better": True, "scaling": "strong" if args.config == "E" else "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded ids, U(-0.5,0.5) chunk KV)",
                 "config": cfg_json,
                 "cpu_baseline": {"value": val, "unit": "prompt tokens/s", "cores": res["threads"],
                                  "kind": "reference", "sample": res["sample"]},
@@ -811,8 +894,7 @@ def main():
                 "ttft_p50_ms": float(statistics.median(r["per_step"])), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded ids and hashes, U(-0.5,0.5) chunk KV, weights synthesised from seed 1)",
-                "config": dict(cfg_json, n_tokens=r["n"], recompute_rows=r["m"],
-                               parallelism=f"head-parallel x{world} (NCCL reduce-scatter + all-gather per layer)"),
+                "config": cfg_json,
                 "step_ms": [round(x, 3) for x in r["per_step"]], "step_sm_mhz": r["step_sm_mhz"],
                 "clocks": r["clocks"]}))
         if world > 1:
@@ -823,10 +905,7 @@ def main():
         r = run_serving(args, world, rank, local)
         cpu = None
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            res, why = cpu_reference("E", steps=1, warmup=0)
-            cpu = ({"value": res["n"] / (res["ms"] / 1e3), "unit": "prompt tokens/s", "cores": res["threads"],
-                    "kind": "reference", "sample": res["sample"], "ms_per_256": res["ms"]} if res
-                   else {"value": None, "unavailable": why})
+            cpu = cpu_baseline_legs("E", [None])
         if rank == 0:
             print(json.dumps({
                 "metric": "MPIC-k prefill tokens/s (p50 TTFT alongside)", "value": r["value"],
@@ -836,11 +915,7 @@ def main():
                 "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded requests and hashes, U(-0.5,0.5) pooled chunk KV, weights "
                         "synthesised from seed 1)",
-                "config": dict(cfg_json, requests=E_REQUESTS, pool_chunks=E_POOL, n_tokens_total=r["n"],
-                               recompute_rows_total=r["m"], requests_rank0=r["mine"],
-                               batch=max(1, args.batch),
-                               parallelism=f"request-sharded x{world} (LPT by predicted cost, no collective)",
-                               l2="inputs larger than L2: 12.9 GB bf16 weights stream through HBM per request"),
+                "config": cfg_json, "recompute_rows_total": r["m"], "requests_rank0": r["mine"],
                 "recompute_rows_per_s": r["rows_per_s"], "cpu_baseline": cpu, "batch_ms": r["batch_ms"],
                 "batch_sm_mhz": r["batch_sm_mhz"], "clocks": r["clocks"],
                 "ttft": "host wall time per request (submission -> logits on the host), p50 over rank 0's requests"}))
@@ -849,15 +924,23 @@ def main():
             dist.destroy_process_group()
         return
     r = run_ours(args, world, rank, local)
+    assert (r["n"], r["m"]) == (cfg_json["n_tokens"], cfg_json["recompute_rows"])
+    serving = None
+    if args.config == "C" and not args.no_serving:
+        # config E (256 requests sharded over the ranks: the 1/2/4/8 strong-scaling workload)
+        # as an extra key of the default line
+        import copy
+        ea = copy.copy(args)
+        ea.steps, ea.warmup = 2, 3
+        e = run_serving(ea, world, rank, local)
+        serving = {"workload": WORKLOAD_NAMES["E"], "value": e["value"], "unit": "prompt tokens/s",
+                   "ms_per_256_requests": e["ms_per_step"], "steps": ea.steps, "warmup": ea.warmup,
+                   "n_gpus": world, "scaling": "strong", "batch": max(1, args.batch),
+                   "recompute_rows_per_s": e["rows_per_s"], "ttft_p50_ms": e["ttft_p50"],
+                   "batch_ms_rank0": e["batch_ms"], "clocks": e["clocks"]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        res, why = cpu_reference(args.config, steps=2, warmup=1)
-        if res is not None:
-            cpu = {"value": res["n"] / (res["ms"] / 1e3), "unit": "prompt tokens/s",
-                   "cores": res["threads"], "kind": "reference", "sample": res["sample"],
-                   "ttft_ms": res["ms"]}
-        else:
-            cpu = {"value": None, "unavailable": why}
+        cpu = cpu_baseline_legs(args.config, [None, 1])
     if rank == 0:
         line = {"metric": "MPIC-k prefill tokens/s (p50 TTFT alongside)", "value": r["value"],
                 "unit": "prompt tokens/s", "n_gpus": world, "steps": args.steps,
@@ -866,12 +949,12 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "bf16", "data": "synthetic (seeded ids and hashes, U(-0.5,0.5) chunk "
                                          "KV, weights synthesised from seed 1)",
-                "config": dict(cfg_json, n_tokens=r["n"], recompute_rows=r["m"]),
+                "config": cfg_json,
                 "e2e": r["e2e"], "e2e_fp32_host": r["e2e_fp32"], "e2e_disk": r["e2e_disk"],
                 "gpu_launches": r["launches"],
                 "roofline": r["roofline"],
                 "request_roofline_frac": round(r["floor_ms"] / r["ms_per_step"], 4),
-                "phases": r["phases"], "cpu_baseline": cpu, "clocks": r["clocks"],
+                "phases": r["phases"], "cpu_baseline": cpu, "serving_E": serving, "clocks": r["clocks"],
                 "step_ms": [round(x, 3) for x in r["per_step"]],
                 "host_ms": [round(x, 3) for x in r["host_ms"]]}
         print(json.dumps(line))

@@ -295,6 +295,14 @@ int mpic_test_gemm(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uin
 int mpic_test_gemm_epi(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uint32_t K, int mode,
                        float* d_x, void* d_xb, void* d_out, void* stream);
 
+/* Test hook: the QKV projection exactly as a layer runs it (K3: the GEMM of the bf16 rows
+ * d_a [M][K] with Wqkv d_w [3h][K], fused RoPE of q and k with the per-row (cos, sin)
+ * table d_rope_tok [M][D/2] and the scatter of k, v to rows d_rows[i] of the bf16 cache
+ * planes d_kv_k / d_kv_v [*][h]); q (rotated, bf16 [M][h]) -> d_q. Async on `stream`. */
+int mpic_test_qkv(const void* d_a, const void* d_w, uint32_t M, uint32_t h, uint32_t K, uint32_t head_dim,
+                  const uint32_t* d_rows, const void* d_rope_tok, void* d_q, void* d_kv_k, void* d_kv_v,
+                  void* stream);
+
 /* ---- per-phase device timing ------------------------------------------------------ */
 typedef enum {
     MPIC_PHASE_ASSEMBLE = 0, /* K2 chunk gather (+ rerotate, cast) */

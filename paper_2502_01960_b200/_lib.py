@@ -111,6 +111,7 @@ SIGNATURES = {
     "mpic_pgemm_timestamps": (_int, [_vp]),
     "mpic_test_gemm": (_int, [_vp, _vp, _u32, _u32, _u32, _int, _vp, _vp]),
     "mpic_test_gemm_epi": (_int, [_vp, _vp, _u32, _u32, _u32, _int, _vp, _vp, _vp, _vp]),
+    "mpic_test_qkv": (_int, [_vp, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mpic_profile_enable": (_int, [_int]),
     "mpic_profile_collect": (_int, [_vp, _vp]),
     "mpic_test_attention": (_int, [_vp, _vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp]),

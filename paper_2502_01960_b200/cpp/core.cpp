@@ -249,19 +249,46 @@ Workspace::Workspace(const DeviceModel& m, uint32_t rows, uint32_t ctx) : rows_(
 }
 
 namespace {
-// Identity of a host model's weights for the device-model cache: every tensor's buffer
-// address and size plus a strided sample of its values (O(1) per call: hashing every weight
-// cost ~1 ms per request even for a toy model and scales with the model size).
+// Identity of a host model's weights for the device-model cache. Models up to
+// kFullHashWords weight words (every conformance and test model) hash EVERY word, so any
+// in-place edit between calls re-uploads. Larger models (LLaVA width: 6.7 G words, where a
+// full pass would cost seconds per call) hash each buffer's address and size plus a strided
+// sample of its words; callers that edit such a model in place must build a new Model (the
+// reference treats Model as immutable after build_model, model.h:22-30).
+constexpr size_t kFullHashWords = size_t(64) << 20;  // 256 MB of fp32 weights
+
+size_t weight_words(const Model& m) {
+    size_t n = m.embedding.size() + m.lm_head.size();
+    for (const LayerWeights& l : m.layers)
+        n += l.wq.size() + l.wk.size() + l.wv.size() + l.wo.size() + l.w1.size() + l.w2.size();
+    return n;
+}
+
 uint64_t weight_hash(const Model& m) {
+    const bool full = weight_words(m) <= kFullHashWords;
     uint64_t acc = 0x9e3779b97f4a7c15ull ^ m.config.fingerprint();
     auto mix = [&](uint64_t v) { acc = (acc ^ v) * 0x100000001b3ull; };
     auto feed = [&](const std::vector<float>& w) {
         const auto* p = reinterpret_cast<const uint32_t*>(w.data());
+        const size_t n = w.size();
         mix(reinterpret_cast<uintptr_t>(p));
-        mix(w.size());
-        const size_t n = w.size(), step = std::max<size_t>(1, n / 61);
-        for (size_t i = 0; i < n; i += step) mix(p[i]);
-        if (n) mix(p[n - 1]);
+        mix(n);
+        if (full) {
+            // four independent multiply-xor lanes over 64-bit words (~10 GB/s)
+            uint64_t a[4] = {1, 2, 3, 4};
+            const auto* q = reinterpret_cast<const uint64_t*>(p);
+            const size_t n64 = n / 2;
+            size_t i = 0;
+            for (; i + 4 <= n64; i += 4)
+                for (int j = 0; j < 4; ++j) a[j] = (a[j] ^ q[i + j]) * 0x9fb21c651e98df25ull;
+            for (; i < n64; ++i) a[0] = (a[0] ^ q[i]) * 0x9fb21c651e98df25ull;
+            if (n & 1) a[1] = (a[1] ^ p[n - 1]) * 0x9fb21c651e98df25ull;
+            for (int j = 0; j < 4; ++j) mix(a[j] ^ (a[j] >> 29));
+        } else {
+            const size_t step = std::max<size_t>(1, n / 61);
+            for (size_t i = 0; i < n; i += step) mix(p[i]);
+            if (n) mix(p[n - 1]);
+        }
     };
     feed(m.embedding);
     feed(m.lm_head);

@@ -52,8 +52,10 @@ private:
 
 // Device copy of a host Model, cached across calls. The value-semantic API lets callers
 // edit weights between calls (proj/tests/test_model.cpp zero_weights), so the cache key is
-// the model's address, its config fingerprint and a 64-bit hash of every weight word,
-// recomputed on each lookup; a mismatch re-uploads.
+// the model's address, its config fingerprint and a 64-bit weight hash recomputed on each
+// lookup; a mismatch re-uploads. The hash covers every weight word for models up to 64 Mi
+// words (256 MB fp32: every test/conformance model); above that it samples each tensor
+// (core.cpp weight_hash), so very large models must not be edited in place between calls.
 std::shared_ptr<DeviceModel> device_model_for(const Model& m);
 
 class Workspace {

@@ -125,16 +125,23 @@ struct mpic_kv_s {
 
 // Everything that fixes the launch sequence of a device-resident request: same signature
 // => same kernels, grids and tensor maps; only the staged inputs differ.
+// The graph holds raw device/pinned pointers: the linked cache's K/V planes (not the handle,
+// whose address a later allocation may reuse), the model's RoPE table, and the workspace
+// buffers, whose reallocations bump `ws_gen`.
 struct GraphSig {
     const void* model = nullptr;
-    const void* linked = nullptr;
+    const void* linked_k = nullptr;
+    const void* linked_v = nullptr;
+    const void* rope = nullptr;
+    uint64_t ws_gen = 0;
     uint32_t n = 0, m = 0, n_img = 0, n_tables = 0, n_units = 0, n_comb = 0;
     int reposition = 0, src_dtype = 0;
     bool link = false;
     bool operator==(const GraphSig& o) const {
-        return model == o.model && linked == o.linked && n == o.n && m == o.m && n_img == o.n_img &&
-               n_tables == o.n_tables && n_units == o.n_units && n_comb == o.n_comb &&
-               reposition == o.reposition && src_dtype == o.src_dtype && link == o.link;
+        return model == o.model && linked_k == o.linked_k && linked_v == o.linked_v && rope == o.rope &&
+               ws_gen == o.ws_gen && n == o.n && m == o.m && n_img == o.n_img && n_tables == o.n_tables &&
+               n_units == o.n_units && n_comb == o.n_comb && reposition == o.reposition &&
+               src_dtype == o.src_dtype && link == o.link;
     }
 };
 
@@ -187,6 +194,7 @@ struct mpic_workspace_s {
     // CUDA-graph replay of a device-resident request (mpic_request_prefill): the request
     // whose shape matches the previous one is captured once, later ones replay it
     bool graphs = true;
+    uint64_t gen = 0;  // bumped whenever a buffer a recorded graph may reference is reallocated
     GraphSig last_sig{}, graph_sig{};
     cudaGraphExec_t graph = nullptr;
     uint32_t graph_kernels = 0;
@@ -446,6 +454,7 @@ void prepare_attn_plan(mpic_workspace_t ws, const uint32_t* h_rows, uint32_t m, 
     const AttnPlan plan = plan_attention(h_rows, m, H, h_starts);
     auto grow = [&](auto*& ptr, size_t& cap, size_t need, size_t elt) {
         if (cap >= need) return;
+        ++ws->gen;
         MPIC_CUDA(cudaDeviceSynchronize());
         cudaFree(ptr);
         ptr = nullptr;
@@ -455,6 +464,7 @@ void prepare_attn_plan(mpic_workspace_t ws, const uint32_t* h_rows, uint32_t m, 
     grow(ws->d_units, ws->units_cap, plan.units.size(), sizeof(AttnUnit));
     grow(ws->d_comb, ws->comb_cap, plan.combine.size(), sizeof(AttnCombine));
     if (ws->slots_cap < plan.slots) {
+        ++ws->gen;
         MPIC_CUDA(cudaDeviceSynchronize());
         cudaFree(ws->part_o);
         cudaFree(ws->part_ml);
@@ -467,6 +477,7 @@ void prepare_attn_plan(mpic_workspace_t ws, const uint32_t* h_rows, uint32_t m, 
     // the previous request's copy out of the pinned staging must have landed
     if (ws->ev_plan) MPIC_CUDA(cudaEventSynchronize(ws->ev_plan));
     if (ws->h_plan_cap < bu + bc) {
+        ++ws->gen;
         cudaFreeHost(ws->h_plan);
         MPIC_CUDA(cudaMallocHost(&ws->h_plan, bu + bc));
         ws->h_plan_cap = bu + bc;
@@ -1421,6 +1432,7 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
     const size_t off_s = off_l + ((bytes_l + 63) & ~size_t(63));
     const size_t bytes_all = off_s + link_skip.size();
     if (ws->asm_cap < bytes_all) {
+        ++ws->gen;
         MPIC_CUDA(cudaDeviceSynchronize());
         cudaFreeHost(ws->h_asm);
         cudaFree(ws->d_asm);
@@ -1494,7 +1506,10 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
     };
     GraphSig sig;
     sig.model = model;
-    sig.linked = linked;
+    sig.linked_k = linked->k;
+    sig.linked_v = linked->v;
+    sig.rope = model->rope;
+    sig.ws_gen = ws->gen;
     sig.n = r.n;
     sig.m = r.m;
     sig.n_img = n_img;
@@ -1509,7 +1524,9 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
         std::lock_guard<std::mutex> lk(g_prof_mu);
         prof = g_prof_on;
     }
-    const bool use_graph = ws->graphs && !prof;
+    // the legacy default stream cannot be captured (the library is not built with
+    // per-thread default streams): such requests always run eagerly
+    const bool use_graph = ws->graphs && !prof && s != nullptr && s != cudaStreamLegacy;
     if (use_graph && ws->graph && ws->graph_sig == sig) {
         MPIC_CUDA(cudaGraphLaunch(ws->graph, s));
         note_launch(ws->graph_kernels);
@@ -1621,6 +1638,7 @@ int mpic_request_prefill_batch(mpic_model_t model, mpic_workspace_t ws, const mp
     const size_t bytes_c = std::max<size_t>(1, ap.chunks.size()) * sizeof(AsmChunk);
     const size_t bytes_t = std::max<size_t>(1, ap.tables.size()) * sizeof(float2);
     if (ws->asm_cap < bytes_c + bytes_t) {
+        ++ws->gen;
         MPIC_CUDA(cudaDeviceSynchronize());
         cudaFreeHost(ws->h_asm);
         cudaFree(ws->d_asm);
@@ -2352,6 +2370,26 @@ int mpic_test_gemm_epi(const void* d_a, const void* d_w, uint32_t M, uint32_t N,
     }
     launch_gemm_tc(static_cast<const __nv_bfloat16*>(d_a), K, static_cast<const __nv_bfloat16*>(d_w), M, N, K, ep,
                    (cudaStream_t)stream);
+    API_END
+}
+
+int mpic_test_qkv(const void* d_a, const void* d_w, uint32_t M, uint32_t h, uint32_t K, uint32_t head_dim,
+                  const uint32_t* d_rows, const void* d_rope_tok, void* d_q, void* d_kv_k, void* d_kv_v,
+                  void* stream) {
+    API_BEGIN
+    MPIC_REQUIRE(tc_gemm_supported(M, 3 * h, K), MPIC_ERR_VALIDATION, "shape not supported by the tcgen05 gemm");
+    EpiParams ep;
+    ep.mode = EPI_QKV;
+    ep.q = d_q;
+    ep.kv_k = d_kv_k;
+    ep.kv_v = d_kv_v;
+    ep.kv_rows = d_rows;
+    ep.rope_pos = d_rows;
+    ep.rope_tok = static_cast<const float2*>(d_rope_tok);
+    ep.hidden = h;
+    ep.head_dim = head_dim;
+    launch_gemm_tc(static_cast<const __nv_bfloat16*>(d_a), K, static_cast<const __nv_bfloat16*>(d_w), M, 3 * h, K,
+                   ep, (cudaStream_t)stream);
     API_END
 }
 

@@ -179,6 +179,11 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const TA* __restrict__ A
             Ws[c][r] = (gn < N && gk < K) ? to_f32<TW>(W[(size_t)gn * K + gk]) : 0.0f;
         }
         __syncthreads();
+        // two-level summation: each 16-wide k slice is accumulated on its own and then added
+        // to the running sum, so the rounding error grows with 16 + K/16 terms instead of K
+        // (the fp32 mode stays at least as close to exact as the reference's OpenBLAS sgemm
+        // at K = 4h = 16384 and 32 layers; tests/test_gpu_llava.py)
+        float part[4][4] = {};
 #pragma unroll
         for (int kk = 0; kk < SB_K; ++kk) {
             float a[4], b[4];
@@ -190,8 +195,12 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const TA* __restrict__ A
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                for (int j = 0; j < 4; ++j) part[i][j] = fmaf(a[i], b[j], part[i][j]);
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] += part[i][j];
         __syncthreads();
     }
 #pragma unroll

@@ -110,3 +110,60 @@ def test_attention_vs_torch(n, m, H):
     ref = attention_ref(q, k, v, rows, H)
     err = (out.float() - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-2, err
+
+
+def rope_table(pos, D, base=10000.0):
+    """(cos, sin) per row and pair as the reference computes them: theta = pos * base^(-i/D)
+    in double, then float (proj/src/model.cpp:46-62)."""
+    i = torch.arange(0, D - 1, 2, dtype=torch.float64)
+    theta = torch.as_tensor(pos, dtype=torch.float64)[:, None] * torch.pow(torch.tensor(base, dtype=torch.float64), -i / D)
+    return torch.stack([torch.cos(theta).float(), torch.sin(theta).float()], dim=-1).contiguous()
+
+
+def rope_ref(x, cs, H, D):
+    """model.cpp:46-62 in fp32 on [M][h] rows."""
+    xv = x.view(x.shape[0], H, D // 2, 2)
+    c, s = cs[:, None, :, 0], cs[:, None, :, 1]
+    x0, x1 = xv[..., 0], xv[..., 1]
+    return torch.stack([x0 * c - x1 * s, x0 * s + x1 * c], dim=-1).reshape(x.shape)
+
+
+@pytest.mark.parametrize("cfg_name", ["C", "A", "B"])
+def test_qkv_rope_scatter_vs_torch(cfg_name):
+    """K3 exactly as a layer runs it at the bench configs' tiling (config C: M = 330 rows =
+    one 176 + 160 token group, 48 tiles of 256 features): Wqkv GEMM + RoPE of q and k at each
+    row's position + scatter of k, v into the cache planes at the selected rows
+    (linker.cpp:59-78). Against torch fp32 on the same bf16 operands and (cos, sin) table;
+    cache rows that are not selected must be untouched."""
+    import bench
+    L, H, D, V, images, k = bench.CONFIGS[cfg_name]
+    h = H * D
+    p = mp.Prompt.from_segments(bench.build_prompt(cfg_name, V))
+    sel = mp.select_tokens(p, mp.POLICY_MPIC_K, k)
+    M, n = len(sel), p.n
+    g = torch.Generator(device="cuda").manual_seed(M + n)
+    a = (torch.rand(M, h, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    w = ((torch.rand(3 * h, h, device="cuda", generator=g) - 0.5) / 32).to(torch.bfloat16)
+    rows = torch.as_tensor(sel.astype(np.int64), device="cuda").to(torch.int32)
+    cs = rope_table(sel.astype(np.float64), D).cuda()
+    kk = (torch.rand(n, h, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    vv = (torch.rand(n, h, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    k0, v0 = kk.clone(), vv.clone()
+    q = torch.zeros(M, h, dtype=torch.bfloat16, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.lib().mpic_test_qkv(a.data_ptr(), w.data_ptr(), M, h, h, D, rows.data_ptr(), cs.data_ptr(),
+                                        q.data_ptr(), kk.data_ptr(), vv.data_ptr(), s))
+    torch.cuda.synchronize()
+    y = a.float() @ w.float().t()
+    q_ref = rope_ref(y[:, :h].contiguous(), cs, H, D)
+    k_ref = rope_ref(y[:, h:2 * h].contiguous(), cs, H, D)
+    v_ref = y[:, 2 * h:]
+    ri = rows.long()
+    for got, ref in ((q.float(), q_ref), (kk[ri].float(), k_ref), (vv[ri].float(), v_ref)):
+        # fp32 epilogue then one bf16 rounding: within one bf16 ulp of the fp32 reference
+        # (plus the fp32 accumulation-order envelope)
+        tol = ref.abs() * 2.0 ** -7 + 1e-5 * ref.abs().max()
+        assert ((got - ref).abs() <= tol).all(), (got - ref).abs().max()
+    other = torch.ones(n, dtype=torch.bool, device="cuda")
+    other[ri] = False
+    assert torch.equal(kk[other], k0[other]) and torch.equal(vv[other], v0[other])

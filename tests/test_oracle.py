@@ -131,3 +131,32 @@ def test_reference_suites_pass_on_reference(suite):
     r = subprocess.run([os.path.join(oracle.REF_DIR, "tests", suite)], capture_output=True,
                        text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("policy,k", [(0, 4), (2, 0)])
+def test_fp64_restatement_matches_reference(policy, k):
+    """oracle/fp64.py (selective pass in float64, reference_model.h arithmetic) agrees with
+    the reference's fp32 selective_prefill to fp32 rounding on a mixed prompt."""
+    from oracle.fp64 import selective_prefill_f64
+    r = oracle.RefLib()
+    cfg = Config(3, 4, 16, 64, 211, 12, 10000.0, 5)
+    rm = r.model(cfg)
+    rng = np.random.default_rng(policy + 3)
+    segs = [("text", rng.integers(0, 210, 7).tolist()), ("image", rng.bytes(32), 12),
+            ("text", rng.integers(0, 210, 5).tolist()), ("image", rng.bytes(32), 12),
+            ("text", rng.integers(0, 210, 4).tolist())]
+    p = oracle.make_prompt(segs)
+    for seg in segs:
+        if seg[0] == "image":
+            kk, vv, _ = rm.prefill(rm.image_ids(seg[1], 12), 0)
+            p.chunk_k.append(kk)
+            p.chunk_v.append(vv)
+            p.chunk_base.append(0)
+    sel = rm.select(p, policy, k)
+    res = rm.link_and_prefill(p, sel=sel)
+    flat = rm.flatten(p)
+    lg, kf, vf = selective_prefill_f64(rm.weight, 3, 4, 16, 10000.0, flat[sel], sel, res["asm_k"], res["asm_v"])
+    den = np.abs(lg).max()
+    assert np.abs(lg - res["logits"]).max() / den < 1e-5
+    assert np.abs(kf - res["k"][:, sel]).max() < 1e-5 and np.abs(vf - res["v"][:, sel]).max() < 1e-5
