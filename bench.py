@@ -524,7 +524,7 @@ def run_ours(args, world, rank, local):
 
     e2e = e2e_fp32 = e2e_disk = None
     if args.disk:
-        # MRAG-style: every chunk read from its .mpic v2 (bf16) file by the disk loader
+        # MRAG-style: every chunk read from its .mpic v3 (bf16, per-layer CRCs) file by the disk loader
         # (reader thread -> pinned ring -> HBM per layer, CRC checked); the files are written
         # first, so the reads are served by the page cache (warm), as after a recent fetch.
         import shutil
@@ -554,7 +554,7 @@ def run_ours(args, world, rank, local):
             wall = allreduce_max(time.perf_counter() - t0, world)
             e2e_disk = {"value": world * n * args.steps / wall, "unit": "prompt tokens/s",
                         "ttft_p50_ms": float(statistics.median(ttft)), "file_bytes_per_step": int(fbytes),
-                        "path": "mpic_request_prefill_files (.mpic v2 bf16 files, page cache warm -> "
+                        "path": "mpic_request_prefill_files (.mpic v3 bf16 files with per-layer CRCs, page cache warm -> "
                                 "reader thread -> pinned ring -> HBM per layer, CRC32 verified)",
                         "timing": "host wall clock per request (the loader is host I/O)"}
         finally:
@@ -665,12 +665,20 @@ def run_head_parallel(args, world, rank, local):
         kv.upload(np.broadcast_to(rk, (L, t, h)), np.broadcast_to(rv, (L, t, h)))
         chunks.append(kv)
     linked = eng.linked_cache(n)
-    comm = headpar.TorchComm() if world > 1 else headpar.SoloComm()
     sh = stream.cuda_stream
+    if args.hp_driver == "library":
+        # the production path: mpic_hp_request (layer loop + NCCL collectives in C++, the loop
+        # replayed as one CUDA graph) on a library-created communicator
+        comm = headpar.NcclComm(rank, world, local)
 
-    def step():
-        eng.prepare(prompt, chunks, linked, mp.POLICY_MPIC_K, k, sh)
-        headpar.prefill_layers(eng, comm, L)
+        def step():
+            eng.request(prompt, chunks, linked, k=k, stream=sh, comm=comm)
+    else:
+        comm = headpar.TorchComm() if world > 1 else headpar.SoloComm()
+
+        def step():
+            eng.prepare(prompt, chunks, linked, mp.POLICY_MPIC_K, k, sh)
+            headpar.prefill_layers(eng, comm, L)
 
     for _ in range(args.warmup):
         step()
@@ -815,6 +823,9 @@ def main():
     ap.add_argument("--mode", default="request", choices=["request", "head-parallel"],
                     help="request: every rank serves its own requests (request sharding); "
                          "head-parallel: one long request split by attention head over the ranks")
+    ap.add_argument("--hp-driver", default="library", choices=["library", "python"],
+                    help="head-parallel: mpic_hp_request with NCCL inside the library, or the "
+                         "Python layer loop over torch.distributed")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-fp32", action="store_true", default=True,

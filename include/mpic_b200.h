@@ -213,12 +213,26 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
  * full PCIe rate): the loader streams layer l of every chunk to HBM on a side stream while
  * layer l-1 is being recomputed; each landed layer is assembled (and cast to the model
  * dtype) right before it is used. */
-/* The same request with each image's chunk read from a .mpic file (v1 fp32 or v2 bf16
- * payload; paths[i] for the i-th image segment): a reader thread preads layer l of every
- * chunk into a pinned ring slot while the GPU computes layer l-1, the copy stream moves the
- * slot to HBM in one transfer, and the file CRCs (combined from per-segment CRCs) are
- * verified at the end: MPIC_ERR_INTEGRITY means the result is void and the chunk must be
- * recomputed (prepare's fallback). position_base comes from each file's header. */
+/* The same request with each image's chunk read from a .mpic file (paths[i] for the i-th
+ * image segment; v1 fp32, v2 bf16, v3 = v2/v1 plus per-layer CRCs): reader threads pread
+ * layer l of every chunk into a pinned ring slot while the GPU computes layer l-1, and the
+ * copy stream moves the slot to HBM. position_base comes from each file's header.
+ * Fault semantics of prepare (proj/src/transfer.cpp:83-145, cache.cpp:171-176): a NULL path
+ * or a file that does not exist is a miss (MPIC_CHUNK_COMPUTED); a file with a bad header,
+ * another model's fingerprint, the wrong shape or token count, a content hash other than
+ * the prompt's image hash, a short read or a CRC mismatch is a fallback
+ * (MPIC_CHUNK_FALLBACK). Either way the chunk is computed on the device (compute_entry,
+ * transfer.cpp:41-58) on a side stream concurrently with the loads, and the request uses
+ * it layer by layer. v3 layers are CRC-checked before their H2D; a v1/v2 file CRC is known
+ * only after the last layer, and a mismatch re-runs the request with the chunk computed:
+ * the outputs never come from a corrupt chunk. chunk_status (may be NULL) receives one
+ * mpic_chunk_status per image segment. */
+typedef enum { MPIC_CHUNK_LOADED = 0, MPIC_CHUNK_COMPUTED = 1, MPIC_CHUNK_FALLBACK = 2 } mpic_chunk_status;
+int mpic_request_prefill_files2(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
+                                const mpic_policy* policy, const char* const* paths, mpic_reposition reposition,
+                                mpic_kv_t linked, float* logits, uint32_t* selected, uint32_t* m_out,
+                                uint32_t* chunk_status, void* stream);
+/* mpic_request_prefill_files2 without the per-chunk report. */
 int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
                                const mpic_policy* policy, const char* const* paths, mpic_reposition reposition,
                                mpic_kv_t linked, float* logits, uint32_t* selected, uint32_t* m_out, void* stream);
@@ -254,6 +268,27 @@ int mpic_hp_layer_attn(mpic_model_t model, mpic_workspace_t ws, uint32_t layer, 
 int mpic_hp_layer_ffn(mpic_model_t model, mpic_workspace_t ws, uint32_t layer, const float* d_reduced, uint32_t row0,
                       uint32_t rows, void* stream);
 int mpic_hp_logits(mpic_model_t model, mpic_workspace_t ws, uint32_t row, float* logits, void* stream);
+/* The whole head-parallel request on one rank, collectives inside the library: per layer
+ * mpic_hp_layer_attn -> ncclReduceScatter(sum) of the Wo partials -> mpic_hp_layer_ffn on
+ * this rank's rows -> in-place ncclAllGather of the bf16 rows; the owner of row m-1
+ * computes the logits and broadcasts them, so every rank returns them. `nccl_comm` is an
+ * ncclComm_t of P ranks whose rank r holds heads [r*H/P, (r+1)*H/P) (its model from
+ * mpic_model_create_heads), or NULL for P = 1. The workspace needs max_rows >= m + P. With
+ * graphs on (mpic_workspace_set_graphs) a request with the same shape as the previous one
+ * records the layer loop — kernels and collectives — as one CUDA graph, replayed after
+ * that. Replaces the per-head loop (linker.cpp:80-113) and the Wo reduction
+ * (linker.cpp:115-118) of selective_prefill for one request split over P GPUs. */
+int mpic_hp_request(mpic_model_t model, mpic_workspace_t ws, void* nccl_comm, const mpic_prompt* prompt,
+                    const mpic_policy* policy, const mpic_kv_t* chunks, mpic_reposition reposition,
+                    const uint32_t* position_bases, mpic_kv_t linked, float* logits, uint32_t* selected,
+                    uint32_t* m_out, void* stream);
+/* NCCL communicator plumbing for mpic_hp_request (libnccl.so.2 is loaded at run time):
+ * rank 0 creates the id, the caller distributes its MPIC_NCCL_ID_BYTES bytes (any
+ * out-of-band channel), every rank creates its communicator on its device. */
+#define MPIC_NCCL_ID_BYTES 128
+int mpic_nccl_unique_id(uint8_t* out);
+int mpic_nccl_comm_create(const uint8_t* id, int nranks, int rank, int device, void** out);
+int mpic_nccl_comm_destroy(void* comm);
 /* Device pointer of a workspace buffer: 0 = x (fp32 [m_pad][h]), 1 = xb (bf16 [m_pad][h]). */
 int mpic_workspace_device_ptr(mpic_workspace_t ws, int which, void** out);
 
@@ -268,7 +303,10 @@ int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpi
                               mpic_reposition reposition, mpic_kv_t linked, float* logits,
                               uint32_t* selected, uint32_t* m_out, void* stream);
 /* The same with the Host-tier chunks in `chunk_dtype` (MPIC_BF16: the model dtype, half the
- * PCIe bytes of the fp32 .mpic v1 payload). */
+ * PCIe bytes of the fp32 .mpic v1 payload). A NULL chunk_k[i] / chunk_v[i] is a miss: the
+ * chunk is computed on the device (prefill of the image's token ids at position base 0,
+ * transfer.cpp:41-58) on a side stream while the other chunks stream in, and its
+ * position_bases entry is ignored (0). */
 int mpic_request_prefill_host2(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
                                const mpic_policy* policy, const void* const* chunk_k, const void* const* chunk_v,
                                mpic_dtype chunk_dtype, const uint32_t* position_bases, mpic_reposition reposition,

@@ -22,7 +22,8 @@ __all__ = ["ModelConfig", "Model", "KV", "Workspace", "Prompt", "MpicError", "Ex
            "F32", "BF16", "AS_STORED", "REROTATE", "POLICY_MPIC_K", "POLICY_TEXT_ONLY",
            "POLICY_ALL", "POLICY_PREFIX_ONLY", "config", "fingerprint", "image_token_ids",
            "select_tokens", "flatten_ids", "assemble", "selective_prefill", "prefill_extend",
-           "request_prefill", "request_prefill_host", "last_launch_count", "HostBuffer", "to_bf16_bits", "request_prefill_files", "write_mpic"]
+           "request_prefill", "request_prefill_host", "last_launch_count", "HostBuffer", "to_bf16_bits", "request_prefill_files", "write_mpic",
+           "CHUNK_LOADED", "CHUNK_COMPUTED", "CHUNK_FALLBACK"]
 
 F32, BF16 = 0, 1
 AS_STORED, REROTATE = 0, 1
@@ -301,11 +302,14 @@ def request_prefill_host(model: Model, ws: Workspace, prompt: Prompt, chunk_k, c
     """Same request with chunk KV in host memory ([L][len][h] arrays, ideally pinned
     HostBuffers): the loader streams them layer by layer to HBM. fp32 arrays are the .mpic
     v1 payload; bf16 chunks (numpy uint16 bit patterns, HostBuffer(..., np.uint16)) are the
-    model-dtype Host tier with half the PCIe bytes."""
+    model-dtype Host tier with half the PCIe bytes. A None chunk is a miss: the library
+    computes it on the device (the image's standalone prefill at position base 0) while the
+    other chunks stream in (prepare's compute lane, transfer.cpp:119-127)."""
     n_img = len(chunk_k)
-    dt = BF16 if n_img and chunk_k[0].dtype == np.uint16 else F32
-    kp = (C.c_void_p * max(n_img, 1))(*[a.ctypes.data for a in chunk_k])
-    vp = (C.c_void_p * max(n_img, 1))(*[a.ctypes.data for a in chunk_v])
+    present = [a for a in chunk_k if a is not None]
+    dt = BF16 if present and present[0].dtype == np.uint16 else (model.dtype if not present else F32)
+    kp = (C.c_void_p * max(n_img, 1))(*[None if a is None else a.ctypes.data for a in chunk_k])
+    vp = (C.c_void_p * max(n_img, 1))(*[None if a is None else a.ctypes.data for a in chunk_v])
     pb = np.ascontiguousarray(position_bases if position_bases is not None else np.zeros(n_img),
                               np.uint32)
     logits = logits_out if logits_out is not None else np.zeros(model.cfg.vocab_size, np.float32)
@@ -321,27 +325,40 @@ def request_prefill_host(model: Model, ws: Workspace, prompt: Prompt, chunk_k, c
 
 def request_prefill_files(model: Model, ws: Workspace, prompt: Prompt, paths, linked: KV,
                           policy: int = POLICY_MPIC_K, k: int = 32, global_budget: bool = False,
-                          reposition: int = AS_STORED, stream=None):
+                          reposition: int = AS_STORED, stream=None, with_status: bool = False):
     """Same request with every image chunk read from its .mpic file by the disk loader
-    (mpic_request_prefill_files): disk -> pinned ring -> HBM per layer, CRC-checked."""
+    (mpic_request_prefill_files2): disk -> pinned ring -> HBM per layer, CRC-checked. A path
+    of None or a missing file is a miss, an unusable file (bad header, other model, wrong
+    content hash, CRC mismatch) a fallback: both are computed on the device instead
+    (prepare's semantics, transfer.cpp:83-145). with_status=True also returns the per-chunk
+    outcome (CHUNK_LOADED / CHUNK_COMPUTED / CHUNK_FALLBACK)."""
     n_img = len(paths)
-    enc = [os.fsencode(p) for p in paths]
+    enc = [None if p is None else os.fsencode(p) for p in paths]
     arr = (C.c_char_p * max(n_img, 1))(*enc)
     logits = np.zeros(model.cfg.vocab_size, np.float32)
     sel = np.zeros(prompt.n, np.uint32)
+    status = np.zeros(max(n_img, 1), np.uint32)
     m = C.c_uint32()
     pol = PolicyDesc(policy, k, int(global_budget))
-    check(lib().mpic_request_prefill_files(model.handle, ws.handle, C.byref(prompt.desc()), C.byref(pol),
-                                           C.cast(arr, C.c_void_p), reposition, linked.handle,
-                                           logits.ctypes.data, sel.ctypes.data, C.byref(m),
-                                           _stream_ptr(stream)))
+    check(lib().mpic_request_prefill_files2(model.handle, ws.handle, C.byref(prompt.desc()), C.byref(pol),
+                                            C.cast(arr, C.c_void_p), reposition, linked.handle,
+                                            logits.ctypes.data, sel.ctypes.data, C.byref(m),
+                                            status.ctypes.data, _stream_ptr(stream)))
+    if with_status:
+        return logits, sel[:m.value].copy(), status[:n_img].copy()
     return logits, sel[:m.value].copy()
 
 
+CHUNK_LOADED, CHUNK_COMPUTED, CHUNK_FALLBACK = 0, 1, 2
+
+
 def write_mpic(path, cfg: ModelConfig, content_hash: bytes, k: np.ndarray, v: np.ndarray,
-               position_base: int = 0, ns: str = "", bf16: bool = False):
-    """Write one chunk as a .mpic container (proj/src/cache.cpp:97-125): v1 with an fp32
-    payload, or v2 with a bf16 payload (uint16 bit patterns), CRC32 of all preceding bytes."""
+               position_base: int = 0, ns: str = "", bf16: bool = False, layer_crcs: bool = True):
+    """Write one chunk as a .mpic container (proj/src/cache.cpp:97-125): an fp32 or a bf16
+    payload (uint16 bit patterns), then — layer_crcs=True, version 3 — a table of per-layer
+    CRC32s (crc_k[L], crc_v[L]; the disk loader verifies each layer before its H2D), then the
+    CRC32 of all preceding bytes. layer_crcs=False writes v1 (fp32, the reference's own
+    format) or v2 (bf16)."""
     import struct
     import zlib
     L, T, h = k.shape
@@ -349,17 +366,23 @@ def write_mpic(path, cfg: ModelConfig, content_hash: bytes, k: np.ndarray, v: np
     fnv = 0xcbf29ce484222325
     for b in ns.encode():
         fnv = ((fnv ^ b) * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
-    header = (b"MPIC" + struct.pack("<IQQ", 2 if bf16 else 1, fingerprint(cfg), fnv) + bytes(content_hash)
+    version = 3 if layer_crcs else (2 if bf16 else 1)
+    header = (b"MPIC" + struct.pack("<IQQ", version, fingerprint(cfg), fnv) + bytes(content_hash)
               + struct.pack("<IIIII", position_base, L, T, h // D, D) + bytes([1 if bf16 else 0]) + bytes(7))
     crc = zlib.crc32(header)
+    table = []
     with open(path, "wb") as f:
         f.write(header)
         for a in (k, v):
-            payload = to_bf16_bits(a) if bf16 else np.ascontiguousarray(a, np.float32)
             for l in range(L):  # layer by layer keeps the host copy small
-                buf = payload[l].tobytes()
+                buf = (to_bf16_bits(a[l]) if bf16 else np.ascontiguousarray(a[l], np.float32)).tobytes()
                 crc = zlib.crc32(buf, crc)
+                table.append(zlib.crc32(buf))
                 f.write(buf)
+        if layer_crcs:
+            tb = struct.pack(f"<{len(table)}I", *table)
+            crc = zlib.crc32(tb, crc)
+            f.write(tb)
         f.write(struct.pack("<I", crc & 0xFFFFFFFF))
 
 

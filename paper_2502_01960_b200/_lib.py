@@ -99,6 +99,8 @@ SIGNATURES = {
                                           _vp, _vp]),
     "mpic_request_prefill_files": (_int, [_vp, _vp, _P(PromptDesc), _P(PolicyDesc), _vp, _int, _vp, _vp, _vp,
                                           _P(_u32), _vp]),
+    "mpic_request_prefill_files2": (_int, [_vp, _vp, _P(PromptDesc), _P(PolicyDesc), _vp, _int, _vp, _vp, _vp,
+                                           _P(_u32), _vp, _vp]),
     "mpic_request_prefill_host2": (_int, [_vp, _vp, _P(PromptDesc), _P(PolicyDesc), _vp, _vp, _int, _vp,
                                           _int, _vp, _vp, _vp, _P(_u32), _vp]),
     "mpic_model_create_heads": (_int, [_P(ModelConfig), _int, _int, _u32, _u32, _P(_vp)]),
@@ -107,6 +109,11 @@ SIGNATURES = {
     "mpic_hp_layer_ffn": (_int, [_vp, _vp, _u32, _vp, _u32, _u32, _vp]),
     "mpic_hp_logits": (_int, [_vp, _vp, _u32, _vp, _vp]),
     "mpic_workspace_device_ptr": (_int, [_vp, _int, _P(_vp)]),
+    "mpic_hp_request": (_int, [_vp, _vp, _vp, _P(PromptDesc), _P(PolicyDesc), _vp, _int, _vp, _vp, _vp, _vp,
+                               _P(_u32), _vp]),
+    "mpic_nccl_unique_id": (_int, [_vp]),
+    "mpic_nccl_comm_create": (_int, [_vp, _int, _int, _int, _P(_vp)]),
+    "mpic_nccl_comm_destroy": (_int, [_vp]),
     "mpic_clock_probe": (_int, [_vp, _u32, _vp]),
     "mpic_pgemm_timestamps": (_int, [_vp]),
     "mpic_test_gemm": (_int, [_vp, _vp, _u32, _u32, _u32, _int, _vp, _vp]),

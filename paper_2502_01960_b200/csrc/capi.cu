@@ -4,7 +4,10 @@
 #include <sys/stat.h>
 #include <unistd.h>
 #include <zlib.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
+#include <cerrno>
 #include <cmath>
 #include <condition_variable>
 #include <cstring>
@@ -14,6 +17,7 @@
 #include <functional>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -203,6 +207,18 @@ struct mpic_workspace_s {
     cudaStream_t asm_stream = nullptr;
     cudaEvent_t ev_asm_in = nullptr;
     std::vector<cudaEvent_t> ev_asm;
+    // compute lane of the loader paths (prepare's compute lane, transfer.cpp:119-127): chunks
+    // that are missing or fail to load are prefilled on their own stream and workspace
+    mpic_workspace_s* aux = nullptr;
+    cudaStream_t miss_stream = nullptr;
+    // head-parallel request inside the library (mpic_hp_request): Wo partials [m_pad][h] and
+    // this rank's reduced rows [mr][h] (fp32), and the captured layer loop
+    float* hp_partial = nullptr;
+    float* hp_reduced = nullptr;
+    size_t hp_partial_cap = 0, hp_reduced_cap = 0;
+    cudaGraphExec_t hp_graph = nullptr;
+    uint64_t hp_graph_key = 0, hp_last_key = 0;
+    uint32_t hp_graph_kernels = 0;
 };
 
 #define API_BEGIN \
@@ -923,6 +939,122 @@ void check_linked(mpic_model_t md, mpic_kv_t linked, uint32_t n) {
                  MPIC_ERR_VALIDATION, "linked cache shape does not match model");
 }
 
+// The compute lane of the loader paths (prepare, proj/src/transfer.cpp:119-140): an image
+// chunk that is not in the tier (miss) or fails to load (fallback) is computed on the device
+// as the reference's compute_entry does (transfer.cpp:41-58: prefill_extend of the image's
+// token ids at position base 0), on its own stream and workspace, CONCURRENTLY with the
+// request: the chunk prefill records an event after each layer, and layer l of the chunk is
+// copied into the request's staging slot (cast to the slot dtype) once that event fires — so
+// the request's layer l waits only for the chunk's layer l, not for the whole prefill.
+struct MissLane {
+    struct Job {
+        uint32_t chunk = 0;
+        mpic_kv_s kv;
+        std::vector<cudaEvent_t> ev;  // ev[l]: layer l of the chunk is in kv
+        std::vector<int32_t> ids;
+        std::vector<uint32_t> rows;
+        int32_t* d_ids = nullptr;
+        uint32_t* d_rows = nullptr;
+    };
+    mpic_model_t md;
+    mpic_workspace_t ws;
+    std::vector<std::unique_ptr<Job>> jobs;
+
+    MissLane(mpic_model_t m, mpic_workspace_t w) : md(m), ws(w) {}
+    ~MissLane() {
+        if (jobs.empty()) return;
+        cudaStreamSynchronize(ws->miss_stream);
+        cudaStreamSynchronize(ws->copy_stream);  // its layer copies read the chunk buffers
+        for (auto& j : jobs) {
+            cudaFree(j->kv.k);
+            cudaFree(j->kv.v);
+            cudaFree(j->d_ids);
+            cudaFree(j->d_rows);
+            for (cudaEvent_t e : j->ev) cudaEventDestroy(e);
+        }
+    }
+    Job* find(uint32_t chunk) const {
+        for (auto& j : jobs)
+            if (j->chunk == chunk) return j.get();
+        return nullptr;
+    }
+    // Start computing chunk `chunk` (image hash, T tokens). `after`: stream whose work so far
+    // must precede the lane (the request's plan uploads; nothing of the chunk depends on it,
+    // but the aux workspace must not race an earlier user).
+    Job* start(uint32_t chunk, const uint8_t* hash32, uint32_t T) {
+        if (Job* j = find(chunk)) return j;
+        const mpic_model_config& c = md->cfg;
+        if (!ws->miss_stream) MPIC_CUDA(cudaStreamCreateWithFlags(&ws->miss_stream, cudaStreamNonBlocking));
+        if (!ws->aux || ws->aux->max_rows < T) {
+            if (ws->aux) {
+                MPIC_CUDA(cudaStreamSynchronize(ws->miss_stream));
+                mpic_workspace_destroy(ws->aux);
+                ws->aux = nullptr;
+            }
+            const uint32_t launches = g_launches;  // the nested API call resets the counter
+            const int rc = mpic_workspace_create(md, T, T, &ws->aux);
+            g_launches = launches;
+            if (rc != MPIC_OK) throw Error(rc, std::string("compute lane workspace: ") + g_last_error);
+        }
+        auto job = std::make_unique<Job>();
+        Job& j = *job;
+        j.chunk = chunk;
+        j.kv.L = c.n_layers;
+        j.kv.T = T;
+        j.kv.H = c.n_heads;
+        j.kv.D = c.head_dim;
+        j.kv.dtype = md->dtype;
+        j.kv.device = md->device;
+        const size_t bytes = j.kv.elems() * esz(md->dtype);
+        MPIC_CUDA(cudaMalloc(&j.kv.k, bytes));
+        MPIC_CUDA(cudaMalloc(&j.kv.v, bytes));
+        MPIC_CUDA(cudaMalloc(&j.d_ids, T * sizeof(int32_t)));
+        MPIC_CUDA(cudaMalloc(&j.d_rows, T * sizeof(uint32_t)));
+        j.ids.resize(T);
+        image_ids(&c, hash32, T, j.ids.data());  // model.cpp:148-156
+        j.rows.resize(T);
+        for (uint32_t i = 0; i < T; ++i) j.rows[i] = i;  // rows == positions: base 0
+        j.ev.resize(c.n_layers);
+        for (cudaEvent_t& e : j.ev) MPIC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        cudaStream_t st = ws->miss_stream;
+        MPIC_CUDA(cudaMemcpyAsync(j.d_ids, j.ids.data(), T * 4, cudaMemcpyHostToDevice, st));
+        MPIC_CUDA(cudaMemcpyAsync(j.d_rows, j.rows.data(), T * 4, cudaMemcpyHostToDevice, st));
+        jobs.push_back(std::move(job));
+        forward_rows(md, ws->aux, j.d_ids, j.d_rows, j.d_rows, T, T - 1, &j.kv, ws->aux->d_logits, st,
+                     [&](uint32_t l) {
+                         if (l) MPIC_CUDA(cudaEventRecord(j.ev[l - 1], st));
+                     },
+                     j.rows.data());
+        MPIC_CUDA(cudaEventRecord(j.ev[c.n_layers - 1], st));
+        return &j;
+    }
+    // Layer l of a computed chunk -> dst_k / dst_v (rows [0, T) x h, dtype dt) on stream cs.
+    void copy_layer(const Job& j, uint32_t l, void* dst_k, void* dst_v, mpic_dtype dt, cudaStream_t cs) const {
+        const size_t cnt = (size_t)j.kv.T * j.kv.H * j.kv.D, es = esz(j.kv.dtype);
+        MPIC_CUDA(cudaStreamWaitEvent(cs, j.ev[l], 0));
+        const char* sk = static_cast<const char*>(j.kv.k) + l * cnt * es;
+        const char* sv = static_cast<const char*>(j.kv.v) + l * cnt * es;
+        if (dt == j.kv.dtype) {
+            MPIC_CUDA(cudaMemcpyAsync(dst_k, sk, cnt * es, cudaMemcpyDeviceToDevice, cs));
+            MPIC_CUDA(cudaMemcpyAsync(dst_v, sv, cnt * es, cudaMemcpyDeviceToDevice, cs));
+        } else if (dt == MPIC_F32) {
+            launch_bf16_to_f32(reinterpret_cast<const __nv_bfloat16*>(sk), static_cast<float*>(dst_k), cnt, cs);
+            launch_bf16_to_f32(reinterpret_cast<const __nv_bfloat16*>(sv), static_cast<float*>(dst_v), cnt, cs);
+        } else {
+            launch_f32_to_bf16(reinterpret_cast<const float*>(sk), static_cast<__nv_bfloat16*>(dst_k), cnt, cs);
+            launch_f32_to_bf16(reinterpret_cast<const float*>(sv), static_cast<__nv_bfloat16*>(dst_v), cnt, cs);
+        }
+    }
+};
+
+// Image hashes of a prompt, one per image segment (in segment order).
+std::vector<const uint8_t*> image_hashes(const mpic_prompt* p) {
+    std::vector<const uint8_t*> out;
+    for (uint32_t s = 0, hi = 0; s < p->n_segments; ++s)
+        if (p->kinds[s] == 1) out.push_back(p->hashes + 32 * hi++);
+    return out;
+}
+
 }  // namespace
 
 extern "C" uint64_t mpic_config_fingerprint(const mpic_model_config* c);
@@ -1267,6 +1399,14 @@ int mpic_workspace_destroy(mpic_workspace_t ws) {
         for (cudaEvent_t e : ws->ev_asm) cudaEventDestroy(e);
         if (ws->ev_asm_in) cudaEventDestroy(ws->ev_asm_in);
         if (ws->asm_stream) cudaStreamDestroy(ws->asm_stream);
+        if (ws->miss_stream) {
+            cudaStreamSynchronize(ws->miss_stream);
+            cudaStreamDestroy(ws->miss_stream);
+        }
+        if (ws->aux) mpic_workspace_destroy(ws->aux);
+        cudaFree(ws->hp_partial);
+        cudaFree(ws->hp_reduced);
+        if (ws->hp_graph) cudaGraphExecDestroy(ws->hp_graph);
         delete ws;
     }
     API_END
@@ -1802,11 +1942,11 @@ int mpic_hp_prepare(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* 
     API_END
 }
 
-int mpic_hp_layer_attn(mpic_model_t md, mpic_workspace_t ws, uint32_t l, mpic_kv_t kv, float* d_partial,
-                       void* stream) {
-    API_BEGIN
-    MPIC_CUDA(cudaSetDevice(md->device));
-    cudaStream_t s = (cudaStream_t)stream;
+}  // extern "C"
+
+namespace {
+// One layer of a head-parallel rank (see mpic_hp_layer_attn / mpic_hp_layer_ffn).
+void hp_attn(mpic_model_t md, mpic_workspace_t ws, uint32_t l, mpic_kv_t kv, float* d_partial, cudaStream_t s) {
     MPIC_REQUIRE(md->n_local_heads && ws->hp_m && l < md->cfg.n_layers, MPIC_ERR_STATE,
                  "mpic_hp_prepare must run first");
     const uint32_t m = ws->hp_m, h = md->cfg.hidden_dim, D = md->cfg.head_dim, Hl = md->n_local_heads,
@@ -1844,18 +1984,14 @@ int mpic_hp_layer_attn(mpic_model_t md, mpic_workspace_t ws, uint32_t l, mpic_kv
         ProfScope ps(s, MPIC_PHASE_WO);
         run_gemm(md, ws->attn, md->wo[l], m, h, hs, st, s);
     }
-    API_END
 }
 
-int mpic_hp_layer_ffn(mpic_model_t md, mpic_workspace_t ws, uint32_t l, const float* d_reduced, uint32_t row0,
-                      uint32_t rows, void* stream) {
-    API_BEGIN
-    MPIC_CUDA(cudaSetDevice(md->device));
-    cudaStream_t s = (cudaStream_t)stream;
+void hp_ffn(mpic_model_t md, mpic_workspace_t ws, uint32_t l, const float* d_reduced, uint32_t row0, uint32_t rows,
+            cudaStream_t s) {
     MPIC_REQUIRE(md->n_local_heads && ws->hp_m && l < md->cfg.n_layers, MPIC_ERR_STATE,
                  "mpic_hp_prepare must run first");
     MPIC_REQUIRE(row0 + rows <= ws->m_pad, MPIC_ERR_VALIDATION, "row range outside the workspace");
-    if (rows == 0) return MPIC_OK;
+    if (rows == 0) return;
     const uint32_t h = md->cfg.hidden_dim;
     float* x = ws->x + (size_t)row0 * h;
     __nv_bfloat16* xb = ws->xb + (size_t)row0 * h;
@@ -1879,6 +2015,24 @@ int mpic_hp_layer_ffn(mpic_model_t md, mpic_workspace_t ws, uint32_t l, const fl
         ProfScope ps(s, MPIC_PHASE_W2);
         run_gemm(md, ws->ffn, md->w2[l], rows, h, 4 * h, res, s);
     }
+}
+}  // namespace
+
+extern "C" {
+
+int mpic_hp_layer_attn(mpic_model_t md, mpic_workspace_t ws, uint32_t l, mpic_kv_t kv, float* d_partial,
+                       void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(md->device));
+    hp_attn(md, ws, l, kv, d_partial, (cudaStream_t)stream);
+    API_END
+}
+
+int mpic_hp_layer_ffn(mpic_model_t md, mpic_workspace_t ws, uint32_t l, const float* d_reduced, uint32_t row0,
+                      uint32_t rows, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(md->device));
+    hp_ffn(md, ws, l, d_reduced, row0, rows, (cudaStream_t)stream);
     API_END
 }
 
@@ -1895,6 +2049,203 @@ int mpic_hp_logits(mpic_model_t md, mpic_workspace_t ws, uint32_t row, float* lo
     MPIC_CUDA(cudaMemcpyAsync(ws->h_logits, ws->d_logits, md->cfg.vocab_size * 4, cudaMemcpyDeviceToHost, s));
     MPIC_CUDA(cudaStreamSynchronize(s));
     std::memcpy(logits, ws->h_logits, md->cfg.vocab_size * sizeof(float));
+    API_END
+}
+
+// ---- head-parallel request inside the library, collectives over NCCL -----
+// NCCL is resolved at run time (dlopen of libnccl.so.2: the process's copy when torch has
+// already loaded one, else the system library), so the library itself carries no link-time
+// NCCL dependency and every non-head-parallel entry point works without it.
+}  // extern "C"
+
+namespace {
+struct NcclApi {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*comm_count)(const ncclComm_t, int*) = nullptr;
+    ncclResult_t (*comm_user_rank)(const ncclComm_t, int*) = nullptr;
+    ncclResult_t (*reduce_scatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                   cudaStream_t) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+    std::string why;
+};
+
+const NcclApi& nccl() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            const char* e = dlerror();
+            a.why = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+            return a;
+        }
+        auto sym = [&](auto& fn, const char* name) {
+            fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+            if (!fn && a.why.empty()) a.why = std::string("libnccl.so.2 lacks ") + name;
+        };
+        sym(a.get_unique_id, "ncclGetUniqueId");
+        sym(a.comm_init_rank, "ncclCommInitRank");
+        sym(a.comm_destroy, "ncclCommDestroy");
+        sym(a.comm_count, "ncclCommCount");
+        sym(a.comm_user_rank, "ncclCommUserRank");
+        sym(a.reduce_scatter, "ncclReduceScatter");
+        sym(a.all_gather, "ncclAllGather");
+        sym(a.broadcast, "ncclBroadcast");
+        sym(a.error_string, "ncclGetErrorString");
+        return a;
+    }();
+    MPIC_REQUIRE(api.why.empty(), MPIC_ERR_STATE, api.why);
+    return api;
+}
+
+#define MPIC_NCCL(call)                                                                          \
+    do {                                                                                         \
+        const ncclResult_t r_ = (call);                                                          \
+        if (r_ != ncclSuccess)                                                                   \
+            throw Error(MPIC_ERR_CUDA, std::string("NCCL: ") + #call + ": " + nccl().error_string(r_)); \
+    } while (0)
+
+// Grow a device buffer to `need` floats (contents undefined), bumping the workspace
+// generation so a recorded layer-loop graph is not replayed on freed memory.
+void grow_f32(mpic_workspace_t ws, float*& p, size_t& cap, size_t need) {
+    if (cap >= need) return;
+    MPIC_CUDA(cudaDeviceSynchronize());
+    cudaFree(p);
+    p = nullptr;
+    MPIC_CUDA(cudaMalloc(&p, std::max<size_t>(need, 1) * sizeof(float)));
+    cap = need;
+    ++ws->gen;
+}
+}  // namespace
+
+extern "C" {
+
+int mpic_nccl_unique_id(uint8_t* out) {
+    API_BEGIN
+    MPIC_REQUIRE(out, MPIC_ERR_VALIDATION, "null argument");
+    static_assert(sizeof(ncclUniqueId) == MPIC_NCCL_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId id;
+    MPIC_NCCL(nccl().get_unique_id(&id));
+    std::memcpy(out, &id, sizeof(id));
+    API_END
+}
+
+int mpic_nccl_comm_create(const uint8_t* id, int nranks, int rank, int device, void** out) {
+    API_BEGIN
+    MPIC_REQUIRE(id && out && nranks > 0 && rank >= 0 && rank < nranks, MPIC_ERR_VALIDATION, "bad communicator request");
+    set_device(device);
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclComm_t c = nullptr;
+    MPIC_NCCL(nccl().comm_init_rank(&c, nranks, uid, rank));
+    *out = c;
+    API_END
+}
+
+int mpic_nccl_comm_destroy(void* comm) {
+    API_BEGIN
+    if (comm) MPIC_NCCL(nccl().comm_destroy(static_cast<ncclComm_t>(comm)));
+    API_END
+}
+
+int mpic_hp_request(mpic_model_t md, mpic_workspace_t ws, void* comm, const mpic_prompt* prompt,
+                    const mpic_policy* policy, const mpic_kv_t* chunks, mpic_reposition reposition,
+                    const uint32_t* position_bases, mpic_kv_t linked, float* logits, uint32_t* selected,
+                    uint32_t* m_out, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(md->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    ncclComm_t c = static_cast<ncclComm_t>(comm);
+    int P = 1, rank = 0;
+    if (c) {
+        MPIC_NCCL(nccl().comm_count(c, &P));
+        MPIC_NCCL(nccl().comm_user_rank(c, &rank));
+    }
+    const uint32_t H = md->cfg.n_heads, h = md->cfg.hidden_dim, L = md->cfg.n_layers, V = md->cfg.vocab_size;
+    MPIC_REQUIRE(md->n_local_heads && md->n_local_heads * (uint32_t)P == H &&
+                     md->head0 == (uint32_t)rank * md->n_local_heads,
+                 MPIC_ERR_VALIDATION, "the model must hold heads [rank*H/P, (rank+1)*H/P) of the communicator rank");
+    // step 0: this rank's head slice of the request cache, embeddings, plans
+    uint32_t m = 0;
+    {
+        const uint32_t launches = g_launches;
+        const int rc = mpic_hp_prepare(md, ws, prompt, policy, chunks, reposition, position_bases, linked, selected,
+                                       &m, stream);
+        g_launches += launches;
+        if (rc != MPIC_OK) throw Error(rc, g_last_error);
+    }
+    const uint32_t mr = ceil_div(m, (uint32_t)P), m_pad = mr * (uint32_t)P;
+    MPIC_REQUIRE(m_pad <= ws->m_pad, MPIC_ERR_VALIDATION,
+                 "P * ceil(m / P) rows exceed the workspace: create it with max_rows >= m + P");
+    grow_f32(ws, ws->hp_partial, ws->hp_partial_cap, (size_t)m_pad * h);
+    grow_f32(ws, ws->hp_reduced, ws->hp_reduced_cap, (size_t)mr * h);
+    // partial rows >= m are never written by the Wo GEMM: they must be zero for the reduction
+    if (m_pad > m) MPIC_CUDA(cudaMemsetAsync(ws->hp_partial + (size_t)m * h, 0, (size_t)(m_pad - m) * h * 4, s));
+    const uint32_t owner = (m - 1) / mr;
+    auto layers = [&] {
+        for (uint32_t l = 0; l < L; ++l) {
+            hp_attn(md, ws, l, linked, ws->hp_partial, s);  // QKV + attention of my heads, my share of attn.Wo^T
+            if (c) MPIC_NCCL(nccl().reduce_scatter(ws->hp_partial, ws->hp_reduced, (size_t)mr * h, ncclFloat32, ncclSum, c, s));
+            else MPIC_CUDA(cudaMemcpyAsync(ws->hp_reduced, ws->hp_partial, (size_t)mr * h * 4, cudaMemcpyDeviceToDevice, s));
+            hp_ffn(md, ws, l, ws->hp_reduced, (uint32_t)rank * mr, mr, s);  // residual + FFN on my rows
+            if (c)  // in place: my rows are already at their offset of xb
+                MPIC_NCCL(nccl().all_gather(ws->xb + (size_t)rank * mr * h, ws->xb, (size_t)mr * h, ncclBfloat16, c, s));
+        }
+        if ((uint32_t)rank == owner) {
+            ProfScope ps(s, MPIC_PHASE_LM_HEAD);
+            launch_lm_head(ws->x + (size_t)(m - 1) * h, md->lm_head, md->dtype, V, h, ws->d_logits, s);
+        }
+        if (c && P > 1) MPIC_NCCL(nccl().broadcast(ws->d_logits, ws->d_logits, V, ncclFloat32, (int)owner, c, s));
+        MPIC_CUDA(cudaMemcpyAsync(ws->h_logits, ws->d_logits, V * 4, cudaMemcpyDeviceToHost, s));
+    };
+    // CUDA-graph replay of the layer loop (kernels + collectives): same key = same launches
+    uint64_t key = 0xcbf29ce484222325ull;
+    for (uint64_t v : {(uint64_t)(uintptr_t)md, (uint64_t)(uintptr_t)c, (uint64_t)(uintptr_t)linked->k,
+                       (uint64_t)(uintptr_t)linked->v, (uint64_t)(uintptr_t)md->rope, ws->gen, (uint64_t)m,
+                       (uint64_t)linked->T, (uint64_t)ws->n_units, (uint64_t)ws->n_comb})
+        key = (key ^ v) * 0x100000001b3ull;
+    bool prof;
+    {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        prof = g_prof_on;
+    }
+    const bool use_graph = ws->graphs && !prof && s != nullptr && s != cudaStreamLegacy;
+    if (use_graph && ws->hp_graph && ws->hp_graph_key == key) {
+        MPIC_CUDA(cudaGraphLaunch(ws->hp_graph, s));
+        note_launch(ws->hp_graph_kernels);
+    } else if (use_graph && ws->hp_last_key == key) {
+        if (ws->hp_graph) {
+            cudaGraphExecDestroy(ws->hp_graph);
+            ws->hp_graph = nullptr;
+        }
+        const uint32_t before = g_launches;
+        cudaGraph_t g = nullptr;
+        MPIC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+            layers();
+        } catch (...) {
+            cudaStreamEndCapture(s, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        MPIC_CUDA(cudaStreamEndCapture(s, &g));
+        const cudaError_t ie = cudaGraphInstantiate(&ws->hp_graph, g, 0);
+        cudaGraphDestroy(g);
+        MPIC_CUDA(ie);
+        ws->hp_graph_kernels = g_launches - before;
+        ws->hp_graph_key = key;
+        MPIC_CUDA(cudaGraphLaunch(ws->hp_graph, s));
+    } else {
+        layers();
+    }
+    ws->hp_last_key = key;
+    MPIC_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(logits, ws->h_logits, V * sizeof(float));
+    if (m_out) *m_out = m;
     API_END
 }
 
@@ -1928,9 +2279,17 @@ int mpic_request_prefill_host2(mpic_model_t model, mpic_workspace_t ws, const mp
     const size_t es = esz(chunk_dtype);
     MPIC_CUDA(cudaSetDevice(model->device));
     cudaStream_t s = (cudaStream_t)stream;
-    const RequestPlan r = plan_request(model, prompt, policy, position_bases);
+    const RequestPlan r0 = plan_request(model, prompt, policy, nullptr);
+    const uint32_t n_img = (uint32_t)r0.refs.size();
+    // a NULL chunk is a miss: computed on the device at position base 0 (compute lane)
+    std::vector<uint32_t> bases(n_img, 0);
+    std::vector<bool> miss(n_img, false);
+    for (uint32_t i = 0; i < n_img; ++i) {
+        miss[i] = !chunk_k || !chunk_v || !chunk_k[i] || !chunk_v[i];
+        if (!miss[i] && position_bases) bases[i] = position_bases[i];
+    }
+    const RequestPlan r = plan_request(model, prompt, policy, bases.data());
     check_linked(model, linked, r.n);
-    const uint32_t n_img = (uint32_t)r.refs.size();
     const size_t h = model->cfg.hidden_dim;
     // Staging slot = one layer of every chunk in the Host tier's dtype, K then V.
     std::vector<size_t> off(n_img);
@@ -1971,6 +2330,12 @@ int mpic_request_prefill_host2(mpic_model_t model, mpic_workspace_t ws, const mp
     const size_t e = esz(linked->dtype);
     const size_t plane = (size_t)linked->T * h * e;
     cudaStream_t cs = ws->copy_stream;
+    MissLane lane(model, ws);
+    {
+        const std::vector<const uint8_t*> hashes = image_hashes(prompt);
+        for (uint32_t i = 0; i < n_img; ++i)
+            if (miss[i]) lane.start(i, hashes[i], r.refs[i].rows);
+    }
     // The leading rows of a chunk that the request recomputes anyway (MPIC-k: its first k)
     // are not copied: the assembly moves whatever the staging slot holds there and the
     // layer's QKV scatter overwrites those cache rows before anything reads them.
@@ -1992,6 +2357,11 @@ int mpic_request_prefill_host2(mpic_model_t model, mpic_workspace_t ws, const mp
         char* base = static_cast<char*>(ws->stage[sl]);
         MPIC_CUDA(cudaStreamWaitEvent(cs, ws->ev_free[sl], 0));
         for (uint32_t i = 0; i < n_img; ++i) {
+            if (miss[i]) {
+                lane.copy_layer(*lane.find(i), l, base + off[i] * es, base + (img_rows * h + off[i]) * es, chunk_dtype,
+                                cs);
+                continue;
+            }
             const size_t cnt = (size_t)r.refs[i].rows * h, skip = (size_t)lead[i] * h;
             if (skip == cnt) continue;
             MPIC_CUDA(cudaMemcpyAsync(base + (off[i] + skip) * es,
@@ -2033,12 +2403,24 @@ int mpic_request_prefill_host(mpic_model_t model, mpic_workspace_t ws, const mpi
 // ---- disk loader: .mpic files -> pinned ring -> HBM, overlapped with the layer loop ----
 // The .mpic container (proj/src/cache.cpp:97-188): 84-byte header, K [L][T][h] then V
 // [L][T][h] (v1: fp32, dtype 0; v2: bf16, dtype 1), then the zlib CRC32 of everything
-// before it. A reader thread preads layer l of every chunk (K and V rows) into a pinned
-// slot laid out exactly like the device staging slot, CRCs each segment on the way and
-// hands the slot to the request, whose copy stream moves it to HBM with ONE cudaMemcpyAsync
-// while layer l-1 computes. The per-segment CRCs are combined in file order
-// (crc32_combine) and checked when the request ends: a mismatch is an integrity error and
-// the caller recomputes the chunk (prepare's fallback, proj/src/transfer.cpp:111-115).
+// before it. v3 (this library's writer, mpic.write_mpic) adds a table of per-layer CRCs
+// (crc_k[L], crc_v[L], each over that layer's segment alone) between the payload and the
+// file CRC, so that every layer is verified BEFORE it is copied to the device.
+//
+// Reader threads pread layer l of every loaded chunk into a pinned slot laid out like the
+// device staging slot and CRC each piece on the way; the copy stream moves the slot to HBM
+// while layer l-1 computes. Fault semantics follow prepare (proj/src/transfer.cpp:83-145):
+//   * a chunk whose file does not exist (or whose path is NULL) is a miss: computed;
+//   * a file that cannot be used — wrong magic/version/size, another model's fingerprint,
+//     wrong shape or token count, a content hash other than the prompt's image hash
+//     (CacheStore::fetch, cache.cpp:171-176), a short read, a CRC mismatch — is a
+//     fallback: computed instead;
+// and computed chunks come from the compute lane (MissLane) concurrently with the loads.
+// v3 layer CRCs are checked before the layer's H2D is issued: a mismatch aborts the pass
+// and the request is re-run with that chunk computed. v1/v2 files carry only the file CRC,
+// known once every layer has been read: a mismatch there also re-runs the request with the
+// chunk computed, so the caller never receives logits or a linked cache built from a
+// corrupt chunk.
 namespace {
 struct MpicFile {
     int fd = -1;
@@ -2046,7 +2428,8 @@ struct MpicFile {
     mpic_dtype dtype = MPIC_F32;
     uint64_t fingerprint = 0;
     uint32_t crc_stored = 0, crc_header = 0;
-    std::vector<uint32_t> crc_k, crc_v;  // per layer
+    std::vector<uint32_t> table;      // v3: crc_k[L] then crc_v[L]
+    std::vector<uint32_t> crc_piece;  // [2][L][pieces] CRCs of the pieces as read
     ~MpicFile() {
         if (fd >= 0) close(fd);
     }
@@ -2075,15 +2458,21 @@ uint32_t crc_of(const void* p, size_t n) {
     return (uint32_t)c;
 }
 
-void open_mpic(MpicFile& f, const char* path, const mpic_model_t md, uint32_t want_T) {
+// Header checks of CacheStore::fetch / read_entry (cache.cpp:127-176, 261-304). Throws
+// NOT_FOUND when the file does not exist, another class when it exists but is unusable.
+void open_mpic(MpicFile& f, const char* path, const mpic_model_t md, uint32_t want_T, const uint8_t* want_hash) {
     f.fd = open(path, O_RDONLY);
-    MPIC_REQUIRE(f.fd >= 0, MPIC_ERR_NOT_FOUND, std::string("cannot open ") + path);
+    MPIC_REQUIRE(f.fd >= 0 || errno != ENOENT, MPIC_ERR_NOT_FOUND, std::string("no such chunk file: ") + path);
+    MPIC_REQUIRE(f.fd >= 0, MPIC_ERR_IO, std::string("cannot open ") + path);
+    struct stat st;
+    MPIC_REQUIRE(fstat(f.fd, &st) == 0, MPIC_ERR_IO, "cannot stat a .mpic file");
+    MPIC_REQUIRE(st.st_size >= 88, MPIC_ERR_FORMAT, ".mpic file too short");
     uint8_t h[84];
     pread_all(f.fd, h, sizeof(h), 0);
     auto u32 = [&](size_t o) { uint32_t v; std::memcpy(&v, h + o, 4); return v; };
-    MPIC_REQUIRE(std::memcmp(h, "MPIC", 4) == 0, MPIC_ERR_INTEGRITY, "bad .mpic magic");
+    MPIC_REQUIRE(std::memcmp(h, "MPIC", 4) == 0, MPIC_ERR_FORMAT, "bad .mpic magic");
     f.version = u32(4);
-    MPIC_REQUIRE(f.version == 1 || f.version == 2, MPIC_ERR_INTEGRITY, "unsupported .mpic version");
+    MPIC_REQUIRE(f.version >= 1 && f.version <= 3, MPIC_ERR_FORMAT, "unsupported .mpic version");
     std::memcpy(&f.fingerprint, h + 8, 8);
     f.position_base = u32(56);
     f.L = u32(60);
@@ -2091,56 +2480,68 @@ void open_mpic(MpicFile& f, const char* path, const mpic_model_t md, uint32_t wa
     f.H = u32(68);
     f.D = u32(72);
     const uint8_t dt = h[76];
-    MPIC_REQUIRE((f.version == 1 && dt == 0) || (f.version == 2 && (dt == 0 || dt == 1)), MPIC_ERR_INTEGRITY,
+    MPIC_REQUIRE((f.version == 1 && dt == 0) || (f.version >= 2 && (dt == 0 || dt == 1)), MPIC_ERR_FORMAT,
                  "unsupported .mpic payload dtype");
     f.dtype = dt == 1 ? MPIC_BF16 : MPIC_F32;
     const mpic_model_config& c = md->cfg;
     MPIC_REQUIRE(f.fingerprint == fingerprint_of(&c), MPIC_ERR_LINK, "chunk was computed by a different model");
+    MPIC_REQUIRE(std::memcmp(h + 24, want_hash, 32) == 0, MPIC_ERR_INTEGRITY, "content hash mismatch on load");
     MPIC_REQUIRE(f.L == c.n_layers && f.H == c.n_heads && f.D == c.head_dim, MPIC_ERR_LINK,
                  "entry tensor shape does not match model");
     MPIC_REQUIRE(f.T == want_T, MPIC_ERR_LINK, "token_count mismatch for image segment");
-    struct stat st;
-    MPIC_REQUIRE(fstat(f.fd, &st) == 0, MPIC_ERR_IO, "cannot stat a .mpic file");
-    const size_t want = 84 + 2 * (size_t)f.L * f.T * f.H * f.D * esz(f.dtype) + 4;
-    MPIC_REQUIRE((size_t)st.st_size == want, MPIC_ERR_INTEGRITY, ".mpic file size does not match its header");
+    const size_t payload = 2 * (size_t)f.L * f.T * f.H * f.D * esz(f.dtype);
+    const size_t table = f.version == 3 ? 2 * (size_t)f.L * 4 : 0;
+    const size_t want = 84 + payload + table + 4;
+    MPIC_REQUIRE((size_t)st.st_size == want, MPIC_ERR_FORMAT, ".mpic file size does not match its header");
+    if (table) {
+        f.table.resize(2 * f.L);
+        pread_all(f.fd, f.table.data(), table, (off_t)(84 + payload));
+    }
     uint8_t tail[4];
     pread_all(f.fd, tail, 4, (off_t)(want - 4));
     std::memcpy(&f.crc_stored, tail, 4);
     f.crc_header = crc_of(h, sizeof(h));
-    f.crc_k.assign(f.L, 0);
-    f.crc_v.assign(f.L, 0);
 }
-}  // namespace
 
-int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
-                               const mpic_policy* policy, const char* const* paths, mpic_reposition reposition,
-                               mpic_kv_t linked, float* logits, uint32_t* selected, uint32_t* m_out, void* stream) {
-    API_BEGIN
-    MPIC_CUDA(cudaSetDevice(model->device));
-    cudaStream_t s = (cudaStream_t)stream;
+// Thrown from the layer loop when a loaded chunk turns out to be unusable mid-request.
+struct RerunWithCompute {
+    uint32_t chunk;
+};
+
+// One pass of a files request with a fixed set of chunks to compute. Returns the chunk
+// whose file failed verification (the caller re-runs with it computed), or -1 on success.
+int files_pass(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt, const mpic_policy* policy,
+               const char* const* paths, mpic_reposition reposition, mpic_kv_t linked, float* logits,
+               uint32_t* selected, uint32_t* m_out, cudaStream_t s, std::vector<uint32_t>& status,
+               std::vector<std::unique_ptr<MpicFile>>& files) {
     const RequestPlan r0 = plan_request(model, prompt, policy, nullptr);
-    check_linked(model, linked, r0.n);
     const uint32_t n_img = (uint32_t)r0.refs.size();
-    std::vector<std::unique_ptr<MpicFile>> files(n_img);
-    std::vector<uint32_t> bases(n_img);
-    for (uint32_t i = 0; i < n_img; ++i) {
-        files[i] = std::make_unique<MpicFile>();
-        open_mpic(*files[i], paths[i], model, r0.refs[i].rows);
-        MPIC_REQUIRE(files[i]->dtype == files[0]->dtype, MPIC_ERR_VALIDATION, "mixed chunk dtypes");
-        bases[i] = files[i]->position_base;
-    }
+    const std::vector<const uint8_t*> hashes = image_hashes(prompt);
+    std::vector<uint32_t> bases(n_img, 0);
+    for (uint32_t i = 0; i < n_img; ++i)
+        if (status[i] == MPIC_CHUNK_LOADED) bases[i] = files[i]->position_base;
     const RequestPlan r = plan_request(model, prompt, policy, bases.data());
-    const mpic_dtype ct = n_img ? files[0]->dtype : MPIC_F32;
+    mpic_dtype ct = model->dtype;  // slot dtype: the files' payload dtype, else the model's
+    bool any_loaded = false;
+    for (uint32_t i = 0; i < n_img; ++i)
+        if (status[i] == MPIC_CHUNK_LOADED) {
+            if (!any_loaded) ct = files[i]->dtype;
+            MPIC_REQUIRE(files[i]->dtype == ct, MPIC_ERR_VALIDATION, "mixed chunk dtypes");
+            any_loaded = true;
+        }
     const size_t es = esz(ct), h = model->cfg.hidden_dim;
     const uint32_t L = model->cfg.n_layers;
+    // slot layout: loaded chunks first (one contiguous H2D per K / V region), then computed
     std::vector<size_t> off(n_img);
-    size_t img_rows = 0;
-    for (uint32_t i = 0; i < n_img; ++i) {
-        off[i] = img_rows * h;
-        img_rows += r.refs[i].rows;
-    }
+    size_t img_rows = 0, loaded_rows = 0;
+    for (int pass = 0; pass < 2; ++pass)
+        for (uint32_t i = 0; i < n_img; ++i)
+            if ((status[i] == MPIC_CHUNK_LOADED) == (pass == 0)) {
+                off[i] = img_rows * h;
+                img_rows += r.refs[i].rows;
+                if (pass == 0) loaded_rows = img_rows;
+            }
     const size_t slot_bytes = std::max<size_t>(1, img_rows) * h * es * 2;
-    // device staging ring (as mpic_request_prefill_host2) + pinned host ring of kSlots layers
     constexpr int kSlots = 3;
     if (ws->stage_cap < slot_bytes) {
         MPIC_CUDA(cudaDeviceSynchronize());
@@ -2164,7 +2565,7 @@ int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mp
     for (uint32_t i = 0; i < n_img; ++i) ts[i] = r.refs[i].rows;
     const AsmChunk* dc[2];
     const float2* dt[2];
-    void* bufs[2];
+    void* bufs[2] = {nullptr, nullptr};
     uint32_t n_tab = 0;
     for (int sl = 0; sl < 2; ++sl) {
         std::vector<const void*> ks(n_img), vs(n_img);
@@ -2178,28 +2579,42 @@ int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mp
         n_tab = p.n_tables;
         bufs[sl] = upload_plan(p, s, &dc[sl], &dt[sl]);
     }
-    // reader threads: layer l -> pinned slot l % kSlots, with per-segment CRCs. The 2*n_img
-    // segments of a layer (K and V rows of every chunk) are spread over a few threads, so
-    // pread (page cache or NVMe) and CRC run in parallel.
+    // compute lane: every chunk not loaded from its file, started before the first load
+    MissLane lane(model, ws);
+    for (uint32_t i = 0; i < n_img; ++i)
+        if (status[i] != MPIC_CHUNK_LOADED) lane.start(i, hashes[i], r.refs[i].rows);
+
+    // reader threads: layer l -> pinned slot l % kSlots, per-piece CRCs; the thread that
+    // completes a layer checks the v3 per-layer CRCs of every chunk before the layer is
+    // handed to the copy stream
+    std::vector<uint32_t> loaded;
+    for (uint32_t i = 0; i < n_img; ++i)
+        if (status[i] == MPIC_CHUNK_LOADED) loaded.push_back(i);
     std::mutex mu;
     std::condition_variable cv;
-    int filled = -1;  // highest layer whose pinned slot is complete
+    int filled = -1;  // highest layer whose pinned slot is complete and verified
     std::vector<bool> copied(L, false);
     std::vector<uint32_t> done(L, 0);
     std::string reader_error;
-    // work items: every segment cut into `pieces` parts so that all but two host cores read
-    // and checksum in parallel (the piece CRCs are combined in file order at the end)
-    const uint32_t n_seg = 2 * n_img;
+    int bad_chunk = -1;  // a loaded chunk that failed verification (or its read)
+    const uint32_t n_seg = 2 * (uint32_t)loaded.size();
     const uint32_t hw = std::max<uint32_t>(1, std::thread::hardware_concurrency());
     const uint32_t want = std::max<uint32_t>(1, hw > 4 ? hw - 2 : hw);
-    const uint32_t pieces = std::max<uint32_t>(1, std::min<uint32_t>(8, ceil_div(want, n_seg)));
+    const uint32_t pieces = n_seg ? std::max<uint32_t>(1, std::min<uint32_t>(8, ceil_div(want, n_seg))) : 1;
     const uint32_t n_items = n_seg * pieces;
-    const uint32_t n_threads = std::max<uint32_t>(1, std::min<uint32_t>(n_items, want));
-    for (uint32_t i = 0; i < n_img; ++i) {
-        files[i]->crc_k.assign((size_t)L * pieces, 0);
-        files[i]->crc_v.assign((size_t)L * pieces, 0);
-    }
+    const uint32_t n_threads = n_items ? std::max<uint32_t>(1, std::min<uint32_t>(n_items, want)) : 0;
+    for (uint32_t i : loaded) files[i]->crc_piece.assign(2 * (size_t)L * pieces, 0);
+    auto seg_crc = [&](const MpicFile& f, uint32_t is_v, uint32_t l) {
+        const size_t seg = (size_t)f.T * h * es;
+        uLong c = f.crc_piece[((size_t)is_v * L + l) * pieces];
+        for (uint32_t pc = 1; pc < pieces; ++pc) {
+            const size_t p0 = seg * pc / pieces, p1 = seg * (pc + 1) / pieces;
+            c = crc32_combine(c, f.crc_piece[((size_t)is_v * L + l) * pieces + pc], (z_off_t)(p1 - p0));
+        }
+        return (uint32_t)c;
+    };
     auto read_worker = [&](uint32_t w) {
+        uint32_t cur = 0;
         try {
             for (uint32_t l = 0; l < L; ++l) {
                 const int sl = (int)(l % kSlots);
@@ -2213,21 +2628,35 @@ int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mp
                 char* dst = static_cast<char*>(ws->pin[sl]);
                 for (uint32_t it = w; it < n_items; it += n_threads) {
                     const uint32_t sg = it / pieces, pc = it % pieces;
-                    const uint32_t i = sg >> 1;
-                    const bool is_v = sg & 1;
+                    const uint32_t i = loaded[sg >> 1];
+                    cur = i;
+                    const uint32_t is_v = sg & 1;
                     MpicFile& f = *files[i];
                     const size_t seg = (size_t)f.T * h * es;
                     const size_t p0 = seg * pc / pieces, p1 = seg * (pc + 1) / pieces;
                     char* d = dst + ((is_v ? img_rows * h : 0) + off[i]) * es + p0;
                     pread_all(f.fd, d, p1 - p0, (off_t)(84 + ((is_v ? (size_t)L : 0) + l) * seg + p0));
-                    (is_v ? f.crc_v : f.crc_k)[(size_t)l * pieces + pc] = crc_of(d, p1 - p0);
+                    f.crc_piece[((size_t)is_v * L + l) * pieces + pc] = crc_of(d, p1 - p0);
                 }
                 {
                     std::lock_guard<std::mutex> lk(mu);
-                    if (++done[l] == n_threads) filled = (int)l;
+                    if (++done[l] == n_threads) {
+                        for (uint32_t i : loaded) {  // v3: verify the layer before it is used
+                            const MpicFile& f = *files[i];
+                            if (f.version == 3 && bad_chunk < 0 &&
+                                (seg_crc(f, 0, l) != f.table[l] || seg_crc(f, 1, l) != f.table[L + l]))
+                                bad_chunk = (int)i;
+                        }
+                        filled = (int)l;
+                    }
                 }
                 cv.notify_all();
             }
+        } catch (const Error&) {  // a short read: the chunk falls back to the compute lane
+            std::lock_guard<std::mutex> lk(mu);
+            if (bad_chunk < 0) bad_chunk = (int)cur;
+            reader_error = "read failure";
+            cv.notify_all();
         } catch (const std::exception& e) {
             std::lock_guard<std::mutex> lk(mu);
             reader_error = e.what();
@@ -2236,8 +2665,15 @@ int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mp
     };
     std::vector<std::thread> readers;
     for (uint32_t w = 0; w < n_threads; ++w) readers.emplace_back(read_worker, w);
-    auto join_readers = [&] {
+    auto stop_readers = [&] {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (reader_error.empty()) reader_error = "request aborted";
+            for (uint32_t l = 0; l < L; ++l) copied[l] = true;
+        }
+        cv.notify_all();
         for (std::thread& t : readers) t.join();
+        readers.clear();
     };
     const size_t e = esz(linked->dtype);
     const size_t plane = (size_t)linked->T * h * e;
@@ -2245,17 +2681,26 @@ int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mp
     MPIC_CUDA(cudaEventRecord(ws->ev_free[0], s));
     MPIC_CUDA(cudaEventRecord(ws->ev_free[1], s));
     auto issue_copy = [&](uint32_t l) {
-        {
+        if (n_threads) {
             std::unique_lock<std::mutex> lk(mu);
-            cv.wait(lk, [&] { return filled >= (int)l || !reader_error.empty(); });
+            cv.wait(lk, [&] { return filled >= (int)l || bad_chunk >= 0 || !reader_error.empty(); });
+            if (bad_chunk >= 0) throw RerunWithCompute{(uint32_t)bad_chunk};
             if (!reader_error.empty()) throw Error(MPIC_ERR_IO, "disk loader: " + reader_error);
         }
         const int sl = l & 1, ps = (int)(l % kSlots);
+        char* stage = static_cast<char*>(ws->stage[sl]);
         MPIC_CUDA(cudaStreamWaitEvent(cs, ws->ev_free[sl], 0));
-        MPIC_CUDA(cudaMemcpyAsync(ws->stage[sl], ws->pin[ps], slot_bytes, cudaMemcpyHostToDevice, cs));
+        if (loaded_rows) {
+            const char* pin = static_cast<const char*>(ws->pin[ps]);
+            const size_t lb = loaded_rows * h * es, vo = img_rows * h * es;
+            MPIC_CUDA(cudaMemcpyAsync(stage, pin, lb, cudaMemcpyHostToDevice, cs));
+            MPIC_CUDA(cudaMemcpyAsync(stage + vo, pin + vo, lb, cudaMemcpyHostToDevice, cs));
+        }
         MPIC_CUDA(cudaEventRecord(ws->ev_pin[ps], cs));
+        for (const auto& j : lane.jobs)
+            lane.copy_layer(*j, l, stage + off[j->chunk] * es, stage + (img_rows * h + off[j->chunk]) * es, ct, cs);
         MPIC_CUDA(cudaEventRecord(ws->ev_ready[sl], cs));
-        {
+        if (n_threads) {
             std::lock_guard<std::mutex> lk(mu);
             copied[l] = true;
         }
@@ -2270,36 +2715,83 @@ int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mp
                         linked->dtype, 1, linked->T, linked->H, linked->D, 1, s);
         MPIC_CUDA(cudaEventRecord(ws->ev_free[sl], s));
     };
+    auto drain = [&] {  // nothing of this pass may still touch the rings when it returns
+        cudaStreamSynchronize(s);
+        cudaStreamSynchronize(cs);
+        for (int sl = 0; sl < 2; ++sl) cudaFreeAsync(bufs[sl], s);
+    };
     try {
         issue_copy(0);
         run_request(model, ws, r, linked, logits, selected, m_out, s, before_layer);
+    } catch (const RerunWithCompute& rr) {
+        stop_readers();
+        drain();
+        return (int)rr.chunk;
     } catch (...) {
-        {
-            std::lock_guard<std::mutex> lk(mu);
-            if (reader_error.empty()) reader_error = "request aborted";
-            for (uint32_t l = 0; l < L; ++l) copied[l] = true;
-        }
-        cv.notify_all();
-        join_readers();
+        stop_readers();
+        drain();
         throw;
     }
-    join_readers();
+    for (std::thread& t : readers) t.join();
     for (int sl = 0; sl < 2; ++sl) MPIC_CUDA(cudaFreeAsync(bufs[sl], s));
+    if (bad_chunk >= 0) return bad_chunk;
     MPIC_REQUIRE(reader_error.empty(), MPIC_ERR_IO, "disk loader: " + reader_error);
-    for (uint32_t i = 0; i < n_img; ++i) {  // CRC of the whole file, in file order
+    for (uint32_t i : loaded) {  // CRC of the whole file, in file order (v1/v2: the only check)
         MpicFile& f = *files[i];
         const size_t seg = (size_t)f.T * h * es;
         uLong c = f.crc_header;
-        for (int is_v = 0; is_v < 2; ++is_v)
-            for (uint32_t l = 0; l < L; ++l)
-                for (uint32_t pc = 0; pc < pieces; ++pc) {
-                    const size_t p0 = seg * pc / pieces, p1 = seg * (pc + 1) / pieces;
-                    c = crc32_combine(c, (is_v ? f.crc_v : f.crc_k)[(size_t)l * pieces + pc], (z_off_t)(p1 - p0));
-                }
-        MPIC_REQUIRE((uint32_t)c == f.crc_stored, MPIC_ERR_INTEGRITY,
-                     std::string("crc mismatch in ") + paths[i] + ": the chunk must be recomputed");
+        for (uint32_t is_v = 0; is_v < 2; ++is_v)
+            for (uint32_t l = 0; l < L; ++l) c = crc32_combine(c, seg_crc(f, is_v, l), (z_off_t)seg);
+        if (f.version == 3) c = crc32(c, reinterpret_cast<const Bytef*>(f.table.data()), (uInt)(f.table.size() * 4));
+        if ((uint32_t)c != f.crc_stored) return (int)i;
     }
+    return -1;
+}
+}  // namespace
+
+int mpic_request_prefill_files2(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
+                                const mpic_policy* policy, const char* const* paths, mpic_reposition reposition,
+                                mpic_kv_t linked, float* logits, uint32_t* selected, uint32_t* m_out,
+                                uint32_t* chunk_status, void* stream) {
+    API_BEGIN
+    MPIC_CUDA(cudaSetDevice(model->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const RequestPlan r0 = plan_request(model, prompt, policy, nullptr);
+    check_linked(model, linked, r0.n);
+    const uint32_t n_img = (uint32_t)r0.refs.size();
+    const std::vector<const uint8_t*> hashes = image_hashes(prompt);
+    std::vector<std::unique_ptr<MpicFile>> files(n_img);
+    std::vector<uint32_t> status(n_img, MPIC_CHUNK_LOADED);
+    for (uint32_t i = 0; i < n_img; ++i) {  // the store lookup (split_request, transfer.cpp:65-79)
+        if (!paths || !paths[i]) {
+            status[i] = MPIC_CHUNK_COMPUTED;
+            continue;
+        }
+        files[i] = std::make_unique<MpicFile>();
+        try {
+            open_mpic(*files[i], paths[i], model, r0.refs[i].rows, hashes[i]);
+        } catch (const Error& e) {
+            status[i] = e.code == MPIC_ERR_NOT_FOUND ? MPIC_CHUNK_COMPUTED : MPIC_CHUNK_FALLBACK;
+            files[i].reset();
+        }
+    }
+    for (uint32_t attempt = 0;; ++attempt) {
+        const int bad = files_pass(model, ws, prompt, policy, paths, reposition, linked, logits, selected, m_out, s,
+                                   status, files);
+        if (bad < 0) break;
+        MPIC_REQUIRE(attempt < n_img, MPIC_ERR_STATE, "disk loader: re-run did not converge");
+        status[bad] = MPIC_CHUNK_FALLBACK;
+        files[bad].reset();
+    }
+    if (chunk_status) std::memcpy(chunk_status, status.data(), n_img * sizeof(uint32_t));
     API_END
+}
+
+int mpic_request_prefill_files(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* prompt,
+                               const mpic_policy* policy, const char* const* paths, mpic_reposition reposition,
+                               mpic_kv_t linked, float* logits, uint32_t* selected, uint32_t* m_out, void* stream) {
+    return mpic_request_prefill_files2(model, ws, prompt, policy, paths, reposition, linked, logits, selected, m_out,
+                                       nullptr, stream);
 }
 
 int mpic_test_gemm(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uint32_t K,

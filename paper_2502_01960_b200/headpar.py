@@ -14,10 +14,16 @@ Rank r of P owns heads [r*H/P, (r+1)*H/P). Per layer:
 Steps 2+4 move the bytes of one all-reduce per layer (the north star's "one NCCL all-reduce
 per layer") without replicating the FFN. The rank holding row m-1 computes the logits.
 
-`HeadParallelRank` drives the native library (mpic_hp_* in include/mpic_b200.h) and
-`prefill_layers` the per-layer loop; the collectives come from `TorchComm`
-(torch.distributed: NCCL between GPUs, gloo on CPU). `prefill_local` runs P virtual ranks on
-one GPU in lockstep with the same data movement (the single-device parity test).
+Two drivers:
+  * `HeadParallelRank.request(..., comm=NcclComm)` — the production path: the whole request
+    runs inside the library (mpic_hp_request): the layer loop, the NCCL reduce-scatter /
+    all-gather and the logits broadcast are issued by C++ on the caller's stream, and the
+    loop is captured as one CUDA graph for same-shape requests. NcclComm is a communicator
+    the library creates (mpic_nccl_comm_create) from an id rank 0 distributes.
+  * `prefill_layers(engine, comm)` — the same decomposition step by step from Python with
+    the collectives of `TorchComm` (torch.distributed: NCCL between GPUs, gloo on CPU or
+    between processes sharing a GPU); `prefill_local` runs P virtual ranks on one GPU in
+    lockstep. These exercise the row split / padding / owner logic on any backend.
 """
 from __future__ import annotations
 
@@ -60,11 +66,14 @@ class TorchComm:
         mine = full[self.rank * mr:(self.rank + 1) * mr].clone()
         if self.nccl:
             self.dist.all_gather_into_tensor(full, mine, group=self.group)
-        else:
-            parts = [full[r * mr:(r + 1) * mr].clone() for r in range(self.world)]
-            self.dist.all_gather(parts, mine, group=self.group)
+        else:  # gloo has no 16-bit integer type: move bf16 bit patterns as int32 pairs
+            import torch
+            wide = mine.element_size() == 2 and mine.shape[-1] % 2 == 0
+            mine_w = mine.view(torch.int32) if wide else mine
+            parts = [torch.empty_like(mine_w) for _ in range(self.world)]
+            self.dist.all_gather(parts, mine_w, group=self.group)
             for r in range(self.world):
-                full[r * mr:(r + 1) * mr].copy_(parts[r])
+                full[r * mr:(r + 1) * mr].copy_(parts[r].view(mine.dtype) if wide else parts[r])
 
 
 class SoloComm:
@@ -76,6 +85,40 @@ class SoloComm:
 
     def all_gather_rows(self, full, mr):
         pass
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (mpic_nccl_unique_id), as bytes."""
+    buf = (C.c_uint8 * 128)()
+    check(lib().mpic_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class NcclComm:
+    """An NCCL communicator created by the library (mpic_nccl_comm_create) for
+    mpic_hp_request. Rank 0's id reaches the other ranks through torch.distributed
+    (broadcast_object_list on `group`, any backend) unless `uid` is given."""
+
+    def __init__(self, rank: int, world: int, device: int = 0, uid: bytes | None = None, group=None):
+        if uid is None:
+            if world == 1:
+                uid = nccl_unique_id()
+            else:
+                import torch.distributed as dist
+                box = [nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(box, src=0, group=group)
+                uid = box[0]
+        self.rank, self.world = rank, world
+        h = C.c_void_p()
+        check(lib().mpic_nccl_comm_create((C.c_uint8 * 128).from_buffer_copy(uid), world, rank, device, C.byref(h)))
+        self.handle = h.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().mpic_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
 
 
 class _DevArray:
@@ -112,6 +155,7 @@ class HeadParallelRank:
         self.model = _M()
         self.model.handle, self.model.cfg, self.model.dtype = h.value, cfg, BF16
         self.ws = Workspace(self.model, max_rows, max_ctx)
+        self.ws_rows = -(-max_rows // 128) * 128  # the workspace's padded row capacity
 
     def close(self):
         if getattr(self, "ws", None):
@@ -144,6 +188,9 @@ class HeadParallelRank:
         self.m = m.value
         self.linked = linked
         self.mr, self.m_pad = row_split(self.m, self.world)
+        if self.m_pad > self.ws_rows:  # the all-gather writes m_pad rows of the workspace's xb
+            raise ValueError(f"{self.world} x ceil(m/{self.world}) = {self.m_pad} rows exceed the workspace "
+                             f"({self.ws_rows}): create the rank with max_rows >= m + world")
         h = self.cfg.hidden_dim
         self.partial = torch.zeros(self.m_pad, h, dtype=torch.float32, device=f"cuda:{self.device}")
         self.reduced = torch.zeros(self.mr, h, dtype=torch.float32, device=f"cuda:{self.device}")
@@ -151,6 +198,24 @@ class HeadParallelRank:
         check(lib().mpic_workspace_device_ptr(self.ws.handle, 1, C.byref(p)))
         self.xb_all = device_tensor(p.value, (self.m_pad, h), torch.int16)  # bf16 bits
         return sel[:self.m].copy()
+
+    def request(self, prompt, chunks, linked, k: int = 32, stream=None, comm: NcclComm | None = None,
+                policy: int = 0, reposition: int = 0, position_bases=None):
+        """The whole head-parallel request in the library (mpic_hp_request): every rank gets
+        the logits. comm=None runs P = 1 (this rank must own every head)."""
+        n_img = len(chunks)
+        arr = (C.c_void_p * max(n_img, 1))(*[c.handle for c in chunks])
+        pb = np.ascontiguousarray(position_bases if position_bases is not None else np.zeros(n_img),
+                                  np.uint32)
+        sel = np.zeros(prompt.n, np.uint32)
+        logits = np.zeros(self.cfg.vocab_size, np.float32)
+        m = C.c_uint32()
+        pol = PolicyDesc(policy, k, 0)
+        check(lib().mpic_hp_request(self.model.handle, self.ws.handle, comm.handle if comm else None,
+                                    C.byref(prompt.desc()), C.byref(pol), arr, reposition, pb.ctypes.data,
+                                    linked.handle, logits.ctypes.data, sel.ctypes.data, C.byref(m), stream))
+        self.m = m.value
+        return logits, sel[:self.m].copy()
 
     def attn(self, layer):
         check(lib().mpic_hp_layer_attn(self.model.handle, self.ws.handle, layer, self.linked.handle,

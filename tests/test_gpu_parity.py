@@ -364,14 +364,10 @@ def test_request_prefill_host_bf16_tier(g, img, text0):
     assert all(np.array_equal(a, b) for a, b in zip(linked_h.download(), linked_d.download()))
 
 
-@pytest.mark.parametrize("bf16_payload", [False, True])
-def test_request_prefill_from_mpic_files(tmp_path, bf16_payload):
-    """The disk loader: .mpic v1 (fp32) / v2 (bf16) files -> pinned ring -> HBM per layer give
-    exactly the logits and cache of the same chunks resident in HBM; a flipped payload byte is
-    an integrity error (the chunk must be recomputed) and a foreign model a link error."""
+def _files_case(dtype=None):
     L, H, D = 2, 8, 128
     cfg = mp.config(L, H, D, vocab_size=4096, image_token_count=160, seed=4)
-    m = mp.Model(cfg, mp.BF16)
+    m = mp.Model(cfg, mp.BF16 if dtype is None else dtype)
     rng = np.random.default_rng(8)
     segs = [("text", rng.integers(0, 4095, 12).tolist()), ("image", rng.bytes(32), 160),
             ("text", rng.integers(0, 4095, 33).tolist()), ("image", rng.bytes(32), 160),
@@ -379,32 +375,135 @@ def test_request_prefill_from_mpic_files(tmp_path, bf16_payload):
     p = mp.Prompt.from_segments(segs)
     chunks = [(rng.random((L, 160, H * D), dtype=np.float32) - 0.5,
                rng.random((L, 160, H * D), dtype=np.float32) - 0.5) for _ in range(2)]
+    return cfg, m, segs, p, chunks
+
+
+def _computed_chunk(m, cfg, hash32, T):
+    """compute_entry (transfer.cpp:41-58) through the standalone miss path: prefill_extend of
+    the image's token ids at base 0 — the chunk the loader's compute lane must produce."""
+    L, H, D = cfg.n_layers, cfg.n_heads, cfg.head_dim
+    kv = mp.KV(L, T, H, D, m.dtype)
+    ws = mp.Workspace(m, T, T)
+    mp.prefill_extend(m, ws, mp.image_token_ids(cfg, hash32, T), 0, 0, kv)
+    return kv
+
+
+@pytest.mark.parametrize("version", ["v1", "v2", "v3-f32", "v3-bf16"])
+def test_request_prefill_from_mpic_files(tmp_path, version):
+    """The disk loader: .mpic files -> pinned ring -> HBM per layer give exactly the logits and
+    cache of the same chunks resident in HBM; every failure mode of the reference's prepare
+    (transfer.cpp:83-145; CacheStore::fetch checks, cache.cpp:171-176) turns into the chunk
+    being computed on the device instead, with the SAME outputs as a request given that
+    computed chunk: a flipped payload byte (v3: caught by the layer CRC before the H2D; v1/v2:
+    by the file CRC, then the request re-runs), a chunk of another model, a wrong content
+    hash, a truncated file, a missing file and a None path."""
+    bf16 = version in ("v2", "v3-bf16")
+    layer_crcs = version.startswith("v3")
+    cfg, m, segs, p, chunks = _files_case()
+    L, H, D = cfg.n_layers, cfg.n_heads, cfg.head_dim
     paths = []
     for i, (k, v) in enumerate(chunks):
         path = str(tmp_path / f"c{i}.mpic")
-        mp.write_mpic(path, cfg, segs[1 + 2 * i][1], k, v, bf16=bf16_payload)
+        mp.write_mpic(path, cfg, segs[1 + 2 * i][1], k, v, bf16=bf16, layer_crcs=layer_crcs)
         paths.append(path)
+    with open(paths[0], "rb") as f:
+        assert int.from_bytes(f.read(8)[4:], "little") == {"v1": 1, "v2": 2}.get(version, 3)
     ws = mp.Workspace(m, 128, p.n)
+    dev = [mp.KV.from_host(k, v, H, D, mp.BF16) for k, v in chunks]
     linked_d = mp.KV(L, p.n, H, D, mp.BF16)
-    ref_logits, ref_sel = mp.request_prefill(m, ws, p, [mp.KV.from_host(k, v, H, D, mp.BF16) for k, v in chunks],
-                                             linked_d, k=32)
+    ref_logits, ref_sel = mp.request_prefill(m, ws, p, dev, linked_d, k=32)
+    ref_cache = linked_d.download()
     linked_f = mp.KV(L, p.n, H, D, mp.BF16)
-    logits, sel = mp.request_prefill_files(m, ws, p, paths, linked_f, k=32)
+    logits, sel, st = mp.request_prefill_files(m, ws, p, paths, linked_f, k=32, with_status=True)
+    assert list(st) == [mp.CHUNK_LOADED] * 2
     assert np.array_equal(sel, ref_sel)
     assert np.array_equal(logits, ref_logits)
-    assert all(np.array_equal(a, b) for a, b in zip(linked_f.download(), linked_d.download()))
-    # corruption inside the payload -> integrity error after the request
+    assert all(np.array_equal(a, b) for a, b in zip(linked_f.download(), ref_cache))
+
+    # the expected outputs when chunk 1 (resp. both) is computed instead of loaded
+    comp = [_computed_chunk(m, cfg, segs[1 + 2 * i][1], 160) for i in range(2)]
+    want1 = mp.request_prefill(m, ws, p, [dev[0], comp[1]], linked_d, k=32)[0], linked_d.download()
+    want_all = mp.request_prefill(m, ws, p, comp, linked_d, k=32)[0], linked_d.download()
+
+    def expect(paths_, status, want):
+        lf = mp.KV(L, p.n, H, D, mp.BF16)
+        lg, sl, st = mp.request_prefill_files(m, ws, p, paths_, lf, k=32, with_status=True)
+        assert list(st) == status, (st, status)
+        assert np.array_equal(sl, ref_sel)
+        assert np.array_equal(lg, want[0]), float(np.abs(lg - want[0]).max())
+        assert all(np.array_equal(a, b) for a, b in zip(lf.download(), want[1]))
+
+    good1 = open(paths[1], "rb").read()
+    # corruption inside the LAST layer's V payload (v1/v2: found after the whole pass)
+    with open(paths[1], "r+b") as f:
+        seg = 160 * H * D * (2 if bf16 else 4)
+        pos = 84 + (2 * L - 1) * seg + 100
+        f.seek(pos)
+        b = f.read(1)
+        f.seek(pos)
+        f.write(bytes([b[0] ^ 0x10]))
+    expect(paths, [mp.CHUNK_LOADED, mp.CHUNK_FALLBACK], want1)
+    # corruption in layer 0 of K
+    open(paths[1], "wb").write(good1)
     with open(paths[1], "r+b") as f:
         f.seek(84 + 1000)
         b = f.read(1)
         f.seek(84 + 1000)
-        f.write(bytes([b[0] ^ 0x10]))
-    with pytest.raises(mp.MpicError) as e:
-        mp.request_prefill_files(m, ws, p, paths, linked_f, k=32)
-    assert e.value.kind == "integrity_error"
+        f.write(bytes([b[0] ^ 0x01]))
+    expect(paths, [mp.CHUNK_LOADED, mp.CHUNK_FALLBACK], want1)
     # a chunk computed by another model
     other = mp.config(L, H, D, vocab_size=4096, image_token_count=160, seed=5)
-    mp.write_mpic(paths[1], other, segs[3][1], *chunks[1], bf16=bf16_payload)
-    with pytest.raises(mp.MpicError) as e:
-        mp.request_prefill_files(m, ws, p, paths, linked_f, k=32)
-    assert e.value.kind == "link_error"
+    mp.write_mpic(paths[1], other, segs[3][1], *chunks[1], bf16=bf16, layer_crcs=layer_crcs)
+    expect(paths, [mp.CHUNK_LOADED, mp.CHUNK_FALLBACK], want1)
+    # a file holding another image (content hash mismatch on load)
+    mp.write_mpic(paths[1], cfg, segs[1][1], *chunks[1], bf16=bf16, layer_crcs=layer_crcs)
+    expect(paths, [mp.CHUNK_LOADED, mp.CHUNK_FALLBACK], want1)
+    # truncated
+    open(paths[1], "wb").write(good1[:len(good1) // 2])
+    expect(paths, [mp.CHUNK_LOADED, mp.CHUNK_FALLBACK], want1)
+    # missing file / no path: a miss (computed lane, not a fallback)
+    os.remove(paths[1])
+    expect(paths, [mp.CHUNK_LOADED, mp.CHUNK_COMPUTED], want1)
+    expect([paths[0], None], [mp.CHUNK_LOADED, mp.CHUNK_COMPUTED], want1)
+    expect([None, None], [mp.CHUNK_COMPUTED, mp.CHUNK_COMPUTED], want_all)
+    # restored: loads again
+    open(paths[1], "wb").write(good1)
+    expect(paths, [mp.CHUNK_LOADED, mp.CHUNK_LOADED], (ref_logits, ref_cache))
+
+
+def test_request_prefill_host_miss_lane():
+    """mpic_request_prefill_host2 with a NULL chunk: the chunk is computed on the device
+    concurrently with the other chunk's loads and the request equals the one given the
+    standalone computed chunk (bf16 Host tier and fp32 payload)."""
+    cfg, m, segs, p, chunks = _files_case()
+    L, H, D = cfg.n_layers, cfg.n_heads, cfg.head_dim
+    ws = mp.Workspace(m, 128, p.n)
+    comp = _computed_chunk(m, cfg, segs[3][1], 160)
+    linked_d = mp.KV(L, p.n, H, D, mp.BF16)
+    want = mp.request_prefill(m, ws, p, [mp.KV.from_host(*chunks[0], H, D, mp.BF16), comp], linked_d, k=32)[0]
+    want_cache = linked_d.download()
+    for bits in (True, False):
+        ck = [mp.to_bf16_bits(chunks[0][0]) if bits else chunks[0][0], None]
+        cv = [mp.to_bf16_bits(chunks[0][1]) if bits else chunks[0][1], None]
+        lh = mp.KV(L, p.n, H, D, mp.BF16)
+        got, _ = mp.request_prefill_host(m, ws, p, ck, cv, lh, k=32)
+        assert np.array_equal(got, want)
+        assert all(np.array_equal(a, b) for a, b in zip(lh.download(), want_cache))
+
+
+def test_request_prefill_files_fp32_model(tmp_path):
+    """fp32 mode (the reference's precision): a v1 file loads bit-exactly like the HBM chunk,
+    and a missing chunk computed by the lane matches the standalone miss path."""
+    cfg, m, segs, p, chunks = _files_case(mp.F32)
+    L, H, D = cfg.n_layers, cfg.n_heads, cfg.head_dim
+    path = str(tmp_path / "c0.mpic")
+    mp.write_mpic(path, cfg, segs[1][1], *chunks[0], layer_crcs=False)
+    ws = mp.Workspace(m, 128, p.n)
+    comp = _computed_chunk(m, cfg, segs[3][1], 160)
+    ld = mp.KV(L, p.n, H, D, mp.F32)
+    want = mp.request_prefill(m, ws, p, [mp.KV.from_host(*chunks[0], H, D, mp.F32), comp], ld, k=32)[0]
+    lf = mp.KV(L, p.n, H, D, mp.F32)
+    got, _, st = mp.request_prefill_files(m, ws, p, [path, None], lf, k=32, with_status=True)
+    assert list(st) == [mp.CHUNK_LOADED, mp.CHUNK_COMPUTED]
+    assert np.array_equal(got, want)
+    assert all(np.array_equal(a, b) for a, b in zip(lf.download(), ld.download()))

@@ -82,3 +82,39 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(mp.MpicError) as e:
         mp.Model(tiny())
     assert e.value.kind == "no_device"
+
+
+def test_nccl_unique_id_without_gpu():
+    """The head-parallel plumbing resolves NCCL at run time (dlopen): an id can be created on
+    a host without a GPU, and it is MPIC_NCCL_ID_BYTES long and fresh each call."""
+    from paper_2502_01960_b200 import headpar
+    a, b = headpar.nccl_unique_id(), headpar.nccl_unique_id()
+    assert len(a) == 128 and a != b
+
+
+def test_write_mpic_v3_layer_crcs(tmp_path):
+    """.mpic v3 (this library's writer): header, K then V payload, the per-layer CRC table
+    (crc_k[L], crc_v[L]), then the CRC32 of everything before it; v1 keeps the reference's
+    layout (no table)."""
+    import struct
+    import zlib
+    cfg = mp.config(3, 2, 8, vocab_size=101, image_token_count=5, seed=7)
+    rng = np.random.default_rng(1)
+    k = rng.random((3, 5, 16), dtype=np.float32)
+    v = rng.random((3, 5, 16), dtype=np.float32)
+    for bf16, crcs in ((False, True), (True, True), (False, False)):
+        path = tmp_path / f"c{int(bf16)}{int(crcs)}.mpic"
+        mp.write_mpic(str(path), cfg, bytes(range(32)), k, v, bf16=bf16, layer_crcs=crcs)
+        b = path.read_bytes()
+        ver = struct.unpack_from("<I", b, 4)[0]
+        assert ver == (3 if crcs else (2 if bf16 else 1))
+        assert b[24:56] == bytes(range(32))
+        assert struct.unpack_from("<I", b, len(b) - 4)[0] == zlib.crc32(b[:-4])
+        seg = 5 * 16 * (2 if bf16 else 4)
+        if crcs:
+            table = struct.unpack_from("<6I", b, len(b) - 4 - 24)
+            for i in range(6):
+                assert table[i] == zlib.crc32(b[84 + i * seg:84 + (i + 1) * seg])
+            assert len(b) == 84 + 6 * seg + 24 + 4
+        else:
+            assert len(b) == 84 + 6 * seg + 4
