@@ -2955,10 +2955,21 @@ int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const
                    static_cast<__nv_bfloat16*>(d_out), s);
     MPIC_CUDA(cudaFreeAsync(buf, s));
     if (unsigned long long* dbg = attn_debug_buffer()) {  // MPIC_ATTN_TS diagnostics
-        std::vector<unsigned long long> h(16 * 64);
+        std::vector<unsigned long long> h(16 * 4096);
         MPIC_CUDA(cudaStreamSynchronize(s));
         MPIC_CUDA(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
         MPIC_CUDA(cudaMemset(dbg, 0, h.size() * 8));
+        {  // per-CTA spans (start, end, smid): one line per CTA, relative to the earliest start
+            const size_t base = 16 * 64, ncta = std::min<size_t>(plan.units.size(), (h.size() - base) / 4);
+            unsigned long long t_min = ~0ull;
+            for (size_t c = 0; c < ncta; ++c) t_min = std::min(t_min, h[base + 4 * c]);
+            for (size_t c = 0; c < ncta; ++c) {
+                const AttnUnit& u = plan.units[c];
+                fprintf(stderr, "cta %4zu sm %3llu start %8.2f end %8.2f us  head %u b0 %u tiles %u/%u b1 %u/%u\n", c,
+                        h[base + 4 * c + 2], (h[base + 4 * c] - t_min) / 1e3, (h[base + 4 * c + 1] - t_min) / 1e3,
+                        u.head, u.b0, u.tile[0], u.tile[1] == kNoTile ? 999u : u.tile[1], u.b1[0], u.b1[1]);
+            }
+        }
         const AttnUnit& u0 = plan.units[0];
         fprintf(stderr, "attn CTA0 item: head %u b0 %u tiles %u/%u b1 %u/%u\n", u0.head, u0.b0, u0.tile[0], u0.tile[1],
                 u0.b1[0], u0.b1[1]);

@@ -9,13 +9,13 @@
 // cover the 148 SMs; attn_combine_kernel merges split partials. One CTA per item, the two
 // query tiles in ping-pong (FlashAttention-4 style), sharing every K/V block they load:
 //
-//   warp 0     control warp, one role per lane (independent thread scheduling): lane 0 TMA
-//              loads Q_A, Q_B once and K_j into a 2-stage ring, lane 16 V_j into a 3-stage
-//              ring ([128 keys x 128] blocks), lane 8 issues every tcgen05.mma; the warp also
-//              owns TMEM (512 cols: S_A | O_A | S_B | O_B). MMAs: S_X(j) = Q_X . K_j^T (SS, K-major) and O_X += P_X(j) . V_j (P from
-//              TMEM, V MN-major), ordered PV_A(j) S_A(j+1) PV_B(j) S_B(j+1), so one tile's
-//              MMAs run while the other tile's softmax works
-//   warps 1-3  linker when chunk blocks are linked inside attention (kernels.h AttnLink),
+//   warp 0     lane 0 TMA-loads Q_A, Q_B once and K_j into a 2-stage ring; the warp owns
+//              TMEM (512 cols: S_A | O_A | S_B | O_B)
+//   warp 1     lane 0 TMA-loads V_j into a 3-stage ring ([128 keys x 128] blocks)
+//   warp 2     lane 0 issues every tcgen05.mma: S_X(j) = Q_X . K_j^T (SS, K-major) and
+//              O_X += P_X(j) . V_j (P from TMEM, V MN-major), ordered PV_A(j) S_A(j+1) PV_B(j)
+//              S_B(j+1), so one tile's MMAs run while the other tile's softmax works
+//   warp 3     linker when chunk blocks are linked inside attention (kernels.h AttnLink),
 //              otherwise idle (warpgroup 0 hands its registers to the softmax warpgroups)
 //   warps 4-7  softmax of tile A, warps 8-11 of tile B, 224 registers per thread: ONE THREAD PER QUERY ROW holding
 //              its 128 scores (no cross-warp reduction), scale, per-row causal mask, online
@@ -39,12 +39,13 @@ CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t outer, uint
 namespace {
 
 constexpr uint32_t kAttnThreads = 384;  // 3 warpgroups: control, softmax tile A, softmax tile B
-constexpr uint32_t kCtrlRegs = 56, kSoftmaxRegs = 224;  // setmaxnreg split of the 64K registers
+constexpr uint32_t kCtrlRegs = 72, kSoftmaxRegs = 216;  // setmaxnreg split of the 168 x 384 launch registers
 constexpr uint32_t kTile = 32 * 1024;   // one [128 x 128] bf16 tile as 2 swizzled 64-col halves
 constexpr uint32_t kHalf = 16 * 1024;
 constexpr uint32_t kKStages = 2;
 constexpr uint32_t kVStages = 3;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr uint32_t kDbgCtaBase = 16 * 64, kDbgCtas = (16 * 4096 - kDbgCtaBase) / 4;  // MPIC_ATTN_TS layout
 
 struct AttnParams {
     const AttnUnit* units;
@@ -61,8 +62,6 @@ struct AttnParams {
     const AttnLink* link;     // linking inside attention (kernels.h), or null
     uint32_t layer;
     uint32_t link_nostore;    // diagnostics (MPIC_ATTN_LINK=2): read chunks, skip the stores
-    __nv_bfloat16* cache_k;   // the layer's request cache planes (linker stores)
-    __nv_bfloat16* cache_v;
 };
 
 // Source of key block `blk` (absolute): the chunk map and row, or the request cache.
@@ -192,6 +191,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tc::pdl_wait();  // q and the layer's K/V come from the previous kernel
     const uint32_t tmem = *tmem_holder;
     const AttnUnit u = p.units[blockIdx.x];
+    if (p.dbg && threadIdx.x == 0 && blockIdx.x < kDbgCtas) {  // diagnostics: per-CTA span and SM
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.dbg[kDbgCtaBase + 4 * blockIdx.x] = globaltimer_ns();
+        p.dbg[kDbgCtaBase + 4 * blockIdx.x + 2] = smid;
+    }
     const bool has_b = u.tile[1] != kNoTile;
     const uint32_t nb0 = u.b1[0] - u.b0, nb1 = has_b ? u.b1[1] - u.b0 : 0;
     const uint32_t nbmax = max(nb0, nb1);
@@ -201,14 +206,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     constexpr uint32_t idesc_s = tc::idesc_bf16(128, 128, false);
     constexpr uint32_t idesc_o = tc::idesc_bf16(128, 128, true);
 
-    if (warp < 4) {
-        tc::reg_dealloc<kCtrlRegs>();
-    } else {
-        tc::reg_alloc<kSoftmaxRegs>();
-    }
+    // Each role owns a whole warp: roles sharing a warp diverge, and a lane sleeping in an
+    // mbarrier try_wait holds back the other paths of its warp (the MMA issuer then stalled
+    // ~1.5 us per key block behind its producers).
+    // setmaxnreg inside the role branches: ptxas sizes each branch by the limit that
+    // dominates it (set before a join, the softmax got the control warps' limit and spilled)
+    if (warp < 4) tc::reg_dealloc<kCtrlRegs>();
     if (warp == 0) {
-        // lane 0: Q tiles then the K ring; lane 16: the V ring (independent producers, so a
-        // late PV never holds back the next K block)
+        // lane 0: Q tiles then the K ring
         if (lane == 0) {
             tc::mbar_arrive_expect_tx(q_full, (has_b ? 2 : 1) * kTile);
 #pragma unroll
@@ -230,7 +235,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 tc::tma_load_2d(sK + st * kTile, src, &k_full[st], hcol, j0);
                 tc::tma_load_2d(sK + st * kTile + kHalf, src, &k_full[st], hcol + 64, j0);
             }
-        } else if (lane == 16) {
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // lane 0: the V ring (an independent producer, so a late PV never holds back the
+        // next K block)
+        if (lane == 0) {
+            if (p.link)
+                for (uint32_t c = 0; c < 2 * kMaxLinkChunks; ++c) tc::tensormap_acquire(&p.link->maps[c]);
             for (uint32_t j = 0; j < nbmax; ++j) {
                 const uint32_t st = j % kVStages, ph = (j / kVStages) & 1;
                 int j0;
@@ -241,7 +253,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 tc::tma_load_2d(sV + st * kTile + kHalf, src, &v_full[st], hcol + 64, j0);
             }
         }
-        else if (lane == 8) {
+        __syncwarp();
+    } else if (warp == 2) {
+        // lane 0: the single MMA-issuing thread
+        if (lane == 0) {
             const uint32_t nbx[2] = {nb0, nb1};
             auto issue_s = [&](uint32_t x, uint32_t j) {
                 const uint32_t qa = tc::smem_u32(sQ + x * kTile);
@@ -307,41 +322,42 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             }
         }
         __syncwarp();
-    } else if (warp < 4) {
-        if (p.link) {
-            // ---- linker (warps 1-3): copies the chunk-sourced K/V blocks this item is the
-            // writer of from the stage buffers into the request cache with 16-B stores on the
-            // LSU path (the TMA unit stays with the K/V loads), then releases the stage.
+    } else if (warp == 3) {
+        if (p.link && lane == 0) {
+            // ---- linker (warp 3, one thread): TMA-stores the chunk-sourced K/V blocks this
+            // item is the writer of from the stage buffers into the request cache (the cache
+            // tensor maps have the stage's 128-B swizzle, so a block is two bulk stores and no
+            // thread touches the data), then releases the stage once the stores have read it.
             // Writer of block b = the item streaming b for the lowest query tile reaching b.
-            const uint32_t t = threadIdx.x - 32;  // 0 .. 95
             const uint32_t* blk = reinterpret_cast<const uint32_t*>(p.link + 1);
             const uint16_t* wtile = reinterpret_cast<const uint16_t*>(blk + p.link->nblk);
-            auto copy_tile = [&](const uint8_t* tile, __nv_bfloat16* cache, uint32_t j0) {
-                // [2 halves][128 rows][128 B] SW128: logical 16-B chunk c of row r sits at chunk c ^ (r & 7)
-                for (uint32_t i = t; i < 2 * 128 * 8; i += 96) {
-                    const uint32_t half = i >> 10, r = (i >> 3) & 127, c = i & 7;
-                    const uint4 v = *reinterpret_cast<const uint4*>(tile + half * kHalf + r * 128 + ((c ^ (r & 7)) << 4));
-                    __stcs(reinterpret_cast<uint4*>(cache + (size_t)(j0 + r) * p.h + hcol + half * 64 + c * 8), v);
-                }
-            };
             for (uint32_t j = 0; j < nbmax; ++j) {
                 const uint32_t b = u.b0 + j, wt = wtile[b];
                 const bool mine = (u.tile[0] == wt && j < nb0) || (has_b && u.tile[1] == wt && j < nb1);
                 const bool store = mine && blk[b] != kLinkedBlock && !p.link_nostore;
                 const uint32_t sk = j % kKStages, sv = j % kVStages;
-                // every linker thread observes each phase before the stage is released (the
-                // barrier also keeps a lagging thread from waiting on a parity that has come round)
                 tc::mbar_wait(&k_full[sk], (j / kKStages) & 1);
-                if (store) copy_tile(sK + sk * kTile, p.cache_k, b * 128u);
-                tc::named_bar_sync(1, 96);
-                if (t == 0) tc::mbar_arrive(&k_empty[sk]);
+                if (store) {
+                    tc::tma_store_2d(&tmK, sK + sk * kTile, hcol, (int)(b * 128u));
+                    tc::tma_store_2d(&tmK, sK + sk * kTile + kHalf, hcol + 64, (int)(b * 128u));
+                    tc::bulk_commit_group();
+                    tc::bulk_wait_group_read<0>();
+                }
+                tc::mbar_arrive(&k_empty[sk]);
                 tc::mbar_wait(&v_full[sv], (j / kVStages) & 1);
-                if (store) copy_tile(sV + sv * kTile, p.cache_v, b * 128u);
-                tc::named_bar_sync(1, 96);
-                if (t == 0) tc::mbar_arrive(&v_empty[sv]);
+                if (store) {
+                    tc::tma_store_2d(&tmV, sV + sv * kTile, hcol, (int)(b * 128u));
+                    tc::tma_store_2d(&tmV, sV + sv * kTile + kHalf, hcol + 64, (int)(b * 128u));
+                    tc::bulk_commit_group();
+                    tc::bulk_wait_group_read<0>();
+                }
+                tc::mbar_arrive(&v_empty[sv]);
             }
+            tc::bulk_wait_group<0>();  // the stores are complete before the CTA exits
         }
-    } else if (warp >= 4) {
+        __syncwarp();
+    } else {
+        tc::reg_alloc<kSoftmaxRegs>();
         // ---- softmax: tile x = warp / 4 - 1, one thread per query row (TMEM lane)
         const uint32_t x = (warp >> 2) - 1;
         const uint32_t nb = x ? nb1 : nb0;
@@ -529,6 +545,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     __syncthreads();
     tc::tc_fence_after();
     if (warp == 0) tc::tmem_dealloc(tmem, 512);
+    if (p.dbg && threadIdx.x == 0 && blockIdx.x < kDbgCtas) p.dbg[kDbgCtaBase + 4 * blockIdx.x + 1] = globaltimer_ns();
 }
 
 // Merge split partials of one (tile, head): O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s.
@@ -712,8 +729,6 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     p.part_ml = part_ml;
     p.dbg = attn_debug_buffer();
     p.link = link;
-    p.cache_k = const_cast<__nv_bfloat16*>(kcache);
-    p.cache_v = const_cast<__nv_bfloat16*>(vcache);
     p.layer = layer;
     static const bool nostore = [] {
         const char* e = getenv("MPIC_ATTN_LINK");
