@@ -2959,15 +2959,17 @@ int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const
         MPIC_CUDA(cudaStreamSynchronize(s));
         MPIC_CUDA(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
         MPIC_CUDA(cudaMemset(dbg, 0, h.size() * 8));
-        {  // per-CTA spans (start, end, smid): one line per CTA, relative to the earliest start
-            const size_t base = 16 * 64, ncta = std::min<size_t>(plan.units.size(), (h.size() - base) / 4);
+        {  // per-CTA spans (start, end, smid, first MMA, last burst, epilogue start/end), relative to the earliest start
+            const size_t base = 16 * 64, ncta = std::min<size_t>(plan.units.size(), (h.size() - base) / 8);
             unsigned long long t_min = ~0ull;
-            for (size_t c = 0; c < ncta; ++c) t_min = std::min(t_min, h[base + 4 * c]);
+            for (size_t c = 0; c < ncta; ++c) t_min = std::min(t_min, h[base + 8 * c]);
+            auto rel = [&](size_t c, int k) { return h[base + 8 * c + k] ? (h[base + 8 * c + k] - t_min) / 1e3 : -1.0; };
             for (size_t c = 0; c < ncta; ++c) {
                 const AttnUnit& u = plan.units[c];
-                fprintf(stderr, "cta %4zu sm %3llu start %8.2f end %8.2f us  head %u b0 %u tiles %u/%u b1 %u/%u\n", c,
-                        h[base + 4 * c + 2], (h[base + 4 * c] - t_min) / 1e3, (h[base + 4 * c + 1] - t_min) / 1e3,
-                        u.head, u.b0, u.tile[0], u.tile[1] == kNoTile ? 999u : u.tile[1], u.b1[0], u.b1[1]);
+                fprintf(stderr, "cta %4zu sm %3llu start %8.2f end %8.2f us  head %u b0 %u tiles %u/%u b1 %u/%u | mma0 %8.2f "
+                                "lastmma %8.2f epi %8.2f epi_end %8.2f\n", c,
+                        h[base + 8 * c + 2], rel(c, 0), rel(c, 1), u.head, u.b0, u.tile[0], u.tile[1] == kNoTile ? 999u : u.tile[1],
+                        u.b1[0], u.b1[1], rel(c, 3), rel(c, 4), rel(c, 5), rel(c, 6));
             }
         }
         const AttnUnit& u0 = plan.units[0];
@@ -2975,10 +2977,15 @@ int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const
                 u0.b1[0], u0.b1[1]);
         const long long t0 = (long long)h[0];
         auto at = [&](int j, int k) { return h[j * 16 + k] ? ((long long)h[j * 16 + k] - t0) / 1e3 : -1.0; };
+        for (int j = 1; j < 64 && h[j * 16]; ++j)
+            if (h[j * 16 + 14] && h[(j - 1) * 16 + 14])
+                fprintf(stderr, "step %d: SM clock %.0f MHz\n", j,
+                        1e3 * (double)(h[j * 16 + 14] - h[(j - 1) * 16 + 14]) / (double)(h[j * 16] - h[(j - 1) * 16]));
         for (int j = 0; j < 64 && h[j * 16]; ++j)
-            fprintf(stderr, "j=%2d MMA: start %6.2f v_full %6.2f pA %6.2f pB %6.2f k_next %6.2f | softmax A: S %6.2f "
-                            "loaded %6.2f max %6.2f exps %6.2f P %6.2f us\n",
-                    j, at(j, 0), at(j, 1), at(j, 2), at(j, 3), at(j, 4), at(j, 5), at(j, 8), at(j, 7), at(j, 9), at(j, 6));
+            fprintf(stderr, "j=%2d MMA: start %6.2f pA %6.2f vA %6.2f pB %6.2f vB %6.2f deps %6.2f issued %6.2f | softmax A: S %6.2f "
+                            "loaded %6.2f max %6.2f exps %6.2f P %6.2f | softmax B: S %6.2f P %6.2f us\n",
+                    j, at(j, 0), at(j, 3), at(j, 12), at(j, 4), at(j, 13), at(j, 1), at(j, 2), at(j, 5), at(j, 8), at(j, 7),
+                    at(j, 9), at(j, 6), at(j, 10), at(j, 11));
     }
     API_END
 }

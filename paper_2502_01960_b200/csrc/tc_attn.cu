@@ -4,24 +4,33 @@
 // [0, rows[i]] of the just-scattered layer cache (proj/src/linker.cpp:80-113): the
 // per-row causal limit is the row's POSITION, not its index in the tile.
 //
-// Work item = one head x a range of 128-key blocks x up to TWO 128-query tiles that need
+// Work item = one head x a range of 128-key blocks x one or two 128-query tiles that need
 // those keys. The host splits long key ranges (flash-decoding style) so ~3 waves of items
-// cover the 148 SMs; attn_combine_kernel merges split partials. One CTA per item, the two
-// query tiles in ping-pong (FlashAttention-4 style), sharing every K/V block they load:
+// cover the 148 SMs; attn_combine_kernel merges split partials. One CTA per item with two
+// LANES (FlashAttention-4 style ping-pong), each with its own softmax warpgroup, O
+// accumulator and TWO S buffers, walking 64-key steps:
+//   pair mode  (two query tiles) lane X = tile X over both key halves of every block; the
+//              lanes share every K/V block the CTA loads
+//   split mode (one query tile) both lanes take the tile, lane X the key half X of every
+//              block (they share the block too); lane 1's (m, l, O) is merged into lane 0's
+//              at the end
+// S_X(s + 1) is computed while the softmax of step s runs (double-buffered S), so a softmax
+// warpgroup never waits for the PV -> S round trip of its own lane.
 //
-//   warp 0     lane 0 TMA-loads Q_A, Q_B once and K_j into a 2-stage ring; the warp owns
-//              TMEM (512 cols: S_A | O_A | S_B | O_B)
+//   warp 0     lane 0 TMA-loads the Q tile(s) once and K_j into a 2-stage ring; the warp
+//              owns TMEM (512 cols: S_A[2] (64 each) | O_A | S_B[2] | O_B)
 //   warp 1     lane 0 TMA-loads V_j into a 3-stage ring ([128 keys x 128] blocks)
-//   warp 2     lane 0 issues every tcgen05.mma: S_X(j) = Q_X . K_j^T (SS, K-major) and
-//              O_X += P_X(j) . V_j (P from TMEM, V MN-major), ordered PV_A(j) S_A(j+1) PV_B(j)
-//              S_B(j+1), so one tile's MMAs run while the other tile's softmax works
-//   warp 3     linker when chunk blocks are linked inside attention (kernels.h AttnLink),
-//              otherwise idle (warpgroup 0 hands its registers to the softmax warpgroups)
-//   warps 4-7  softmax of tile A, warps 8-11 of tile B, 224 registers per thread: ONE THREAD PER QUERY ROW holding
-//              its 128 scores (no cross-warp reduction), scale, per-row causal mask, online
-//              max with lazy O rescaling (only when the max grows by more than 2^8), exp2
-//              with half of the exponentials on the FMA pipe (degree-3 polynomial, exact to
-//              bf16) and half on MUFU, row sums; P written back over S in TMEM as bf16.
+//   warp 2     lane 0 issues every tcgen05.mma: S_X(s) = Q_X . K_half^T (SS, K-major, N = 64)
+//              and O_X += P_X(s) . V_half (P from TMEM, V MN-major); per step, lane by lane,
+//              PV_X(s) then S_X(s + 2) into the buffer P_X(s) occupied
+//   warp 3     linker when chunk blocks are linked inside attention (kernels.h AttnLink):
+//              TMA bulk stores of the loaded K/V blocks into the request cache
+//   warps 4-7  softmax of lane 0, warps 8-11 of lane 1, 216 registers per thread: ONE
+//              THREAD PER QUERY ROW holding its 64 scores (no cross-warp reduction), scale,
+//              per-row causal mask, online max with lazy O rescaling (only when the max
+//              grows by more than 2^8), exp2 with a quarter of the exponentials on the FMA
+//              pipe (degree-3 polynomial, exact to bf16) and the rest on MUFU, row sums; P
+//              written back over S in TMEM as bf16.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -45,7 +54,7 @@ constexpr uint32_t kHalf = 16 * 1024;
 constexpr uint32_t kKStages = 2;
 constexpr uint32_t kVStages = 3;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-constexpr uint32_t kDbgCtaBase = 16 * 64, kDbgCtas = (16 * 4096 - kDbgCtaBase) / 4;  // MPIC_ATTN_TS layout
+constexpr uint32_t kDbgCtaBase = 16 * 64, kDbgCtas = (16 * 4096 - kDbgCtaBase) / 8;  // MPIC_ATTN_TS layout
 
 struct AttnParams {
     const AttnUnit* units;
@@ -84,6 +93,25 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+
+#ifdef MPIC_ATTN_WATCHDOG  // diagnostics build: a wait that spins ~1 s reports where it hangs and traps
+__device__ __noinline__ void wd_wait(uint64_t* bar, uint32_t parity, int tag, uint32_t a) {
+    const long long t0 = clock64();
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.b32 %0, 1, 0, P1;\n}"
+                     : "=r"(ok) : "r"(tc::smem_u32(bar)), "r"(parity) : "memory");
+        if (!ok && clock64() - t0 > 2000000000ll) {
+            printf("attn watchdog: cta %d warp %d lane %d tag %d arg %u parity %u\n", blockIdx.x, threadIdx.x / 32,
+                   threadIdx.x % 32, tag, a, parity);
+            asm volatile("trap;");
+        }
+    }
+}
+#define WD_WAIT(bar, par, tag, a) wd_wait(bar, par, tag, a)
+#else
+#define WD_WAIT(bar, par, tag, a) tc::mbar_wait(bar, par)
+#endif
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
@@ -151,11 +179,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     uint64_t* k_empty = k_full + kKStages;
     uint64_t* v_full = k_empty + kKStages;       // [kVStages]
     uint64_t* v_empty = v_full + kVStages;
-    uint64_t* s_full = v_empty + kVStages;       // [2 tiles]
-    uint64_t* p_full = s_full + 2;               // [2 tiles]
-    uint64_t* o_done = p_full + 2;               // [2 tiles]
-    uint64_t* p_part = o_done + 2;               // [2 tiles][3] P_X(j) keys [0, 32(q+1)) written
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(p_part + 6);
+    uint64_t* s_full = v_empty + kVStages;       // [2 lanes][2 buffers]
+    uint64_t* p_full = s_full + 4;               // [2 lanes][2 buffers]
+    uint64_t* o_done = p_full + 4;               // [2 lanes] one phase per PV
+    uint64_t* o_fin = o_done + 2;                // [2 lanes] the lane's last PV
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_fin + 2);
+    float2* ml_x = reinterpret_cast<float2*>(tmem_holder + 4);  // [128] split mode: lane 1's (m, l)
 
     tc::pdl_trigger();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -165,9 +194,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tc::tma_prefetch_desc(&tmK);
         tc::tma_prefetch_desc(&tmV);
         tc::mbar_init(q_full, 1);
-        // with linking, a K/V stage is free once its MMAs are done AND the linker has
-        // finished storing it (or passed it)
-        const uint32_t empties = p.link ? 2u : 1u;
+        // a K/V stage is free once both MMA warps' reads of it are done and, with linking,
+        // the linker has finished storing it (or passed it)
+        const uint32_t empties = p.link ? 3u : 2u;  // both MMA warps (+ the linker)
         for (uint32_t i = 0; i < kKStages; ++i) {
             tc::mbar_init(&k_full[i], 1);
             tc::mbar_init(&k_empty[i], empties);
@@ -176,11 +205,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             tc::mbar_init(&v_full[i], 1);
             tc::mbar_init(&v_empty[i], empties);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 4; ++i) {
             tc::mbar_init(&s_full[i], 1);
             tc::mbar_init(&p_full[i], 128);
-            for (int q = 0; q < 3; ++q) tc::mbar_init(&p_part[3 * i + q], 128);
+        }
+        for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&o_done[i], 1);
+            tc::mbar_init(&o_fin[i], 1);
         }
         tc::fence_barrier_init();
     }
@@ -194,133 +225,146 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (p.dbg && threadIdx.x == 0 && blockIdx.x < kDbgCtas) {  // diagnostics: per-CTA span and SM
         uint32_t smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        p.dbg[kDbgCtaBase + 4 * blockIdx.x] = globaltimer_ns();
-        p.dbg[kDbgCtaBase + 4 * blockIdx.x + 2] = smid;
+        p.dbg[kDbgCtaBase + 8 * blockIdx.x] = globaltimer_ns();
+        p.dbg[kDbgCtaBase + 8 * blockIdx.x + 2] = smid;
     }
-    const bool has_b = u.tile[1] != kNoTile;
-    const uint32_t nb0 = u.b1[0] - u.b0, nb1 = has_b ? u.b1[1] - u.b0 : 0;
-    const uint32_t nbmax = max(nb0, nb1);
+    // Two lanes (X = 0, 1), each with its own softmax warpgroup, O accumulator and two S
+    // buffers, walk 64-key steps. Pair mode (two query tiles): lane X = tile X over every
+    // half-block of its range, step s = half s & 1 of block s >> 1. Split mode (one tile):
+    // both lanes take the tile, lane X the key half X of every block, step s = block s;
+    // their (m, l, O) are merged at the end.
+    const bool split = u.tile[1] == kNoTile;
+    const uint32_t nb0 = u.b1[0] - u.b0, nb1 = split ? nb0 : u.b1[1] - u.b0;
+    const uint32_t nblk = max(nb0, nb1);
+    const uint32_t nst[2] = {split ? nb0 : 2 * nb0, split ? nb0 : 2 * nb1};
     const int hcol = (int)(u.head * 128u);
-    // TMEM columns: tile X uses S_X [256X, 256X+128) and O_X [256X+128, 256X+256).
-    // P_X(j) (bf16, two keys per column) overwrites the first 64 columns of S_X in place.
-    constexpr uint32_t idesc_s = tc::idesc_bf16(128, 128, false);
+    // TMEM columns: lane X uses S_X[b] = [256X + 64b, +64) and O_X = [256X + 128, +128).
+    // P_X (bf16, two keys per column) overwrites the first 32 columns of its S buffer.
+    constexpr uint32_t idesc_s = tc::idesc_bf16(128, 64, false);
     constexpr uint32_t idesc_o = tc::idesc_bf16(128, 128, true);
 
     // Each role owns a whole warp: roles sharing a warp diverge, and a lane sleeping in an
-    // mbarrier try_wait holds back the other paths of its warp (the MMA issuer then stalled
-    // ~1.5 us per key block behind its producers).
+    // mbarrier try_wait holds back the other paths of its warp.
     // setmaxnreg inside the role branches: ptxas sizes each branch by the limit that
     // dominates it (set before a join, the softmax got the control warps' limit and spilled)
     if (warp < 4) tc::reg_dealloc<kCtrlRegs>();
     if (warp == 0) {
-        // lane 0: Q tiles then the K ring
+        // lane 0: the Q tile(s), then K_j and V_j of every block in order (K into a 2-stage,
+        // V into a 3-stage ring: V_j's slot frees long before K_{j+2} is needed)
         if (lane == 0) {
-            tc::mbar_arrive_expect_tx(q_full, (has_b ? 2 : 1) * kTile);
+            tc::mbar_arrive_expect_tx(q_full, (split ? 1 : 2) * kTile);
 #pragma unroll
             for (uint32_t x = 0; x < 2; ++x) {
-                if (x == 1 && !has_b) break;
+                if (x == 1 && split) break;
                 // tile 0 may start at a negative row: TMA zero-fills the rows outside [0, m)
-                const int q0 = (int)((x ? u.tile[1] : u.tile[0]) * 128u) - (int)p.shift;
+                const int q0 = (int)(u.tile[x] * 128u) - (int)p.shift;
                 tc::tma_load_2d(sQ + x * kTile, &tmQ, q_full, hcol, q0);
                 tc::tma_load_2d(sQ + x * kTile + kHalf, &tmQ, q_full, hcol + 64, q0);
             }
             if (p.link)
                 for (uint32_t c = 0; c < 2 * kMaxLinkChunks; ++c) tc::tensormap_acquire(&p.link->maps[c]);
-            for (uint32_t j = 0; j < nbmax; ++j) {
-                const uint32_t st = j % kKStages, ph = (j / kKStages) & 1;
+            for (uint32_t j = 0; j < nblk; ++j) {
                 int j0;
-                const CUtensorMap* src = link_src(p, &tmK, u.b0 + j, 0, j0);
-                tc::mbar_wait(&k_empty[st], ph ^ 1);
-                tc::mbar_arrive_expect_tx(&k_full[st], kTile);
-                tc::tma_load_2d(sK + st * kTile, src, &k_full[st], hcol, j0);
-                tc::tma_load_2d(sK + st * kTile + kHalf, src, &k_full[st], hcol + 64, j0);
+                const uint32_t sk = j % kKStages, sv = j % kVStages;
+                const CUtensorMap* srck = link_src(p, &tmK, u.b0 + j, 0, j0);
+                WD_WAIT(&k_empty[sk], ((j / kKStages) & 1) ^ 1, 1, j);
+                tc::mbar_arrive_expect_tx(&k_full[sk], kTile);
+                tc::tma_load_2d(sK + sk * kTile, srck, &k_full[sk], hcol, j0);
+                tc::tma_load_2d(sK + sk * kTile + kHalf, srck, &k_full[sk], hcol + 64, j0);
+                const CUtensorMap* srcv = link_src(p, &tmV, u.b0 + j, 1, j0);
+                WD_WAIT(&v_empty[sv], ((j / kVStages) & 1) ^ 1, 2, j);
+                tc::mbar_arrive_expect_tx(&v_full[sv], kTile);
+                tc::tma_load_2d(sV + sv * kTile, srcv, &v_full[sv], hcol, j0);
+                tc::tma_load_2d(sV + sv * kTile + kHalf, srcv, &v_full[sv], hcol + 64, j0);
             }
         }
         __syncwarp();
-    } else if (warp == 1) {
-        // lane 0: the V ring (an independent producer, so a late PV never holds back the
-        // next K block)
-        if (lane == 0) {
-            if (p.link)
-                for (uint32_t c = 0; c < 2 * kMaxLinkChunks; ++c) tc::tensormap_acquire(&p.link->maps[c]);
-            for (uint32_t j = 0; j < nbmax; ++j) {
-                const uint32_t st = j % kVStages, ph = (j / kVStages) & 1;
-                int j0;
-                const CUtensorMap* src = link_src(p, &tmV, u.b0 + j, 1, j0);
-                tc::mbar_wait(&v_empty[st], ph ^ 1);
-                tc::mbar_arrive_expect_tx(&v_full[st], kTile);
-                tc::tma_load_2d(sV + st * kTile, src, &v_full[st], hcol, j0);
-                tc::tma_load_2d(sV + st * kTile + kHalf, src, &v_full[st], hcol + 64, j0);
-            }
-        }
-        __syncwarp();
-    } else if (warp == 2) {
-        // lane 0: the single MMA-issuing thread
-        if (lane == 0) {
-            const uint32_t nbx[2] = {nb0, nb1};
-            auto issue_s = [&](uint32_t x, uint32_t j) {
-                const uint32_t qa = tc::smem_u32(sQ + x * kTile);
-                const uint32_t ka = tc::smem_u32(sK + (j % kKStages) * kTile);
+    } else if (warp <= 2) {
+        // MMA warps: warp 1 issues lane 0's MMAs, warp 2 lane 1's, so one lane's waits
+        // never stall the other lane's MMAs (the tensor pipe queues only ~4 MMAs, and a
+        // single issuer's per-step bookkeeping left it idle ~40% of the time). All 32 lanes
+        // run the control flow (warp-uniform: descriptors in uniform registers); lane 0
+        // polls the barriers (then __syncwarp), one elected lane issues. Per step s: PV_x(s)
+        // once P_x(s) is written, then S_x(s + 2) into the buffer P_x(s) occupied (in-order
+        // after the PV that reads it), so the softmax finds S_x(s + 1) computed while it
+        // works on step s. A K/V stage needs one release (commit) from each MMA warp.
+        const uint32_t x = warp - 1;
+        const uint32_t ns = nst[x];
+        const bool stamp = lane == 0 && p.dbg && blockIdx.x == 0 && x == 0;
+        auto blk_of = [&](uint32_t s) { return split ? s : s >> 1; };
+        auto half_of = [&](uint32_t s) { return split ? x : s & 1u; };
+        uint32_t k_avail = 0, v_avail = 0, k_rel = 0, v_rel = 0;
+        auto need_k = [&](uint32_t j) {
+            for (; k_avail <= j; ++k_avail)
+                if (lane == 0) WD_WAIT(&k_full[k_avail % kKStages], (k_avail / kKStages) & 1, 3, k_avail);
+        };
+        auto need_v = [&](uint32_t j) {
+            for (; v_avail <= j; ++v_avail)
+                if (lane == 0) WD_WAIT(&v_full[v_avail % kVStages], (v_avail / kVStages) & 1, 4, v_avail);
+        };
+        const uint32_t qa = tc::smem_u32(sQ + (split ? 0u : x) * kTile);
+        auto issue_s = [&](uint32_t s) {
+            const uint32_t j = blk_of(s);
+            const uint32_t ka = tc::smem_u32(sK + (j % kKStages) * kTile) + half_of(s) * 8192u;  // keys [64h, +64)
+            if (tc::elect_one_sync()) {
 #pragma unroll
                 for (uint32_t kk = 0; kk < 8; ++kk) {
                     const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-                    tc::mma_bf16(tmem + x * 256, tc::desc_k_sw128(qa + off), tc::desc_k_sw128(ka + off), idesc_s,
-                                 kk > 0 ? 1u : 0u);
+                    tc::mma_bf16(tmem + x * 256 + (s & 1) * 64, tc::desc_k_sw128(qa + off), tc::desc_k_sw128(ka + off),
+                                 idesc_s, kk > 0 ? 1u : 0u);
                 }
-                tc::mma_commit(&s_full[x]);
-            };
-            tc::mbar_wait(q_full, 0);
-            tc::mbar_wait(&k_full[0], 0);
-            tc::tc_fence_after();
-#pragma unroll
-            for (uint32_t x = 0; x < 2; ++x)
-                if (nbx[x] > 0) issue_s(x, 0);
-            tc::mma_commit(&k_empty[0]);
-            for (uint32_t j = 0; j < nbmax; ++j) {
-                const uint32_t st = j % kVStages, ph = (j / kVStages) & 1;
-                const bool nxt = j + 1 < nbmax;
-                if (p.dbg && blockIdx.x == 0) p.dbg[j * 16 + 0] = globaltimer_ns();
-                tc::mbar_wait(&v_full[st], ph);
-                if (p.dbg && blockIdx.x == 0) p.dbg[j * 16 + 1] = globaltimer_ns();
-                bool k_ready = false;
-#pragma unroll
-                for (uint32_t x = 0; x < 2; ++x) {
-                    if (j >= nbx[x]) continue;
-                    const uint32_t va = tc::smem_u32(sV + st * kTile);
-                    // PV_X(j) in quarters: keys [32q, 32q+32) as soon as the softmax has written
-                    // that part of P (it works on the next keys while these MMAs run)
-#pragma unroll
-                    for (uint32_t hf = 0; hf < 4; ++hf) {
-                        tc::mbar_wait(hf == 3 ? &p_full[x] : &p_part[3 * x + hf], j & 1);
-                        if (hf == 3 && p.dbg && blockIdx.x == 0) p.dbg[j * 16 + 2 + x] = globaltimer_ns();
-                        tc::tc_fence_after();
-#pragma unroll
-                        for (uint32_t kk = 2 * hf; kk < 2 * hf + 2; ++kk)  // A = P_X(j) from TMEM: 16 keys = 8 packed columns
-                            tc::mma_bf16_ts(tmem + x * 256 + 128, tmem + x * 256 + kk * 8,
-                                            tc::desc_mn_sw128(va + kk * 2048, kHalf), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-                    }
-                    tc::mma_commit(&o_done[x]);
-                    // in-order after PV_X(j), which reads P_X(j) from S_X's columns
-                    if (j + 1 < nbx[x]) {
-                        if (!k_ready) {
-                            tc::mbar_wait(&k_full[(j + 1) % kKStages], ((j + 1) / kKStages) & 1);
-                            if (p.dbg && blockIdx.x == 0) p.dbg[j * 16 + 4] = globaltimer_ns();
-                            tc::tc_fence_after();
-                            k_ready = true;
-                        }
-                        issue_s(x, j + 1);
-                    }
-                }
-                tc::mma_commit(&v_empty[st]);
-                if (nxt) {
-                    if (!k_ready) {  // no tile needs K_{j+1} any more: just release it
-                        tc::mbar_wait(&k_full[(j + 1) % kKStages], ((j + 1) / kKStages) & 1);
-                        tc::tc_fence_after();
-                    }
-                    tc::mma_commit(&k_empty[(j + 1) % kKStages]);
-                }
+                tc::mma_commit(&s_full[2 * x + (s & 1)]);
             }
+        };
+        auto issue_pv = [&](uint32_t s) {
+            const uint32_t j = blk_of(s);
+            const uint32_t va = tc::smem_u32(sV + (j % kVStages) * kTile) + half_of(s) * 8192u;
+            if (tc::elect_one_sync()) {
+#pragma unroll
+                for (uint32_t kk = 0; kk < 4; ++kk)  // A = P_x(s) from TMEM: 16 keys = 8 packed columns
+                    tc::mma_bf16_ts(tmem + x * 256 + 128, tmem + x * 256 + (s & 1) * 64 + kk * 8,
+                                    tc::desc_mn_sw128(va + kk * 2048, kHalf), idesc_o, (s > 0 || kk > 0) ? 1u : 0u);
+                tc::mma_commit(&o_done[x]);
+                if (s + 1 == ns) tc::mma_commit(&o_fin[x]);
+            }
+        };
+        // release every block below the lowest block a later MMA of this lane still reads
+        auto release = [&](uint32_t next_s, uint32_t next_pv) {
+            const uint32_t lk = next_s < ns ? blk_of(next_s) : nblk;
+            const uint32_t lv = next_pv < ns ? blk_of(next_pv) : nblk;
+            if (tc::elect_one_sync()) {
+                for (uint32_t j = k_rel; j < lk; ++j) tc::mma_commit(&k_empty[j % kKStages]);
+                for (uint32_t j = v_rel; j < lv; ++j) tc::mma_commit(&v_empty[j % kVStages]);
+            }
+            k_rel = max(k_rel, lk);
+            v_rel = max(v_rel, lv);
+        };
+        if (lane == 0) WD_WAIT(q_full, 0, 5, 0);
+        need_k(blk_of(min(2u, ns) - 1));
+        __syncwarp();
+        tc::tc_fence_after();
+        issue_s(0);
+        if (ns > 1) issue_s(1);
+        release(2, 0);
+        const bool cta_stamp = lane == 0 && x == 0 && p.dbg && blockIdx.x < kDbgCtas;
+        if (cta_stamp) p.dbg[kDbgCtaBase + 8 * blockIdx.x + 3] = globaltimer_ns();
+        for (uint32_t s = 0; s < ns; ++s) {
+            if (stamp && s < 64) {
+                p.dbg[s * 16 + 0] = globaltimer_ns();
+                p.dbg[s * 16 + 14] = clock64();
+            }
+            if (lane == 0) WD_WAIT(&p_full[2 * x + (s & 1)], (s >> 1) & 1, 6, s);
+            need_v(blk_of(s));
+            if (s + 2 < ns) need_k(blk_of(s + 2));
+            __syncwarp();
+            tc::tc_fence_after();
+            if (stamp && s < 64) p.dbg[s * 16 + 1] = globaltimer_ns();
+            issue_pv(s);
+            if (s + 2 < ns) issue_s(s + 2);
+            release(s + 3, s + 1);
+            if (stamp && s < 64) p.dbg[s * 16 + 2] = globaltimer_ns();
         }
+        if (cta_stamp) p.dbg[kDbgCtaBase + 8 * blockIdx.x + 4] = globaltimer_ns();
         __syncwarp();
     } else if (warp == 3) {
         if (p.link && lane == 0) {
@@ -331,12 +375,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             // Writer of block b = the item streaming b for the lowest query tile reaching b.
             const uint32_t* blk = reinterpret_cast<const uint32_t*>(p.link + 1);
             const uint16_t* wtile = reinterpret_cast<const uint16_t*>(blk + p.link->nblk);
-            for (uint32_t j = 0; j < nbmax; ++j) {
+            for (uint32_t j = 0; j < nblk; ++j) {
                 const uint32_t b = u.b0 + j, wt = wtile[b];
-                const bool mine = (u.tile[0] == wt && j < nb0) || (has_b && u.tile[1] == wt && j < nb1);
+                const bool mine = (u.tile[0] == wt && j < nb0) || (!split && u.tile[1] == wt && j < nb1);
                 const bool store = mine && blk[b] != kLinkedBlock && !p.link_nostore;
                 const uint32_t sk = j % kKStages, sv = j % kVStages;
-                tc::mbar_wait(&k_full[sk], (j / kKStages) & 1);
+                WD_WAIT(&k_full[sk], (j / kKStages) & 1, 7, 0);
                 if (store) {
                     tc::tma_store_2d(&tmK, sK + sk * kTile, hcol, (int)(b * 128u));
                     tc::tma_store_2d(&tmK, sK + sk * kTile + kHalf, hcol + 64, (int)(b * 128u));
@@ -344,7 +388,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     tc::bulk_wait_group_read<0>();
                 }
                 tc::mbar_arrive(&k_empty[sk]);
-                tc::mbar_wait(&v_full[sv], (j / kVStages) & 1);
+                WD_WAIT(&v_full[sv], (j / kVStages) & 1, 8, 0);
                 if (store) {
                     tc::tma_store_2d(&tmV, sV + sv * kTile, hcol, (int)(b * 128u));
                     tc::tma_store_2d(&tmV, sV + sv * kTile + kHalf, hcol + 64, (int)(b * 128u));
@@ -358,166 +402,187 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         __syncwarp();
     } else {
         tc::reg_alloc<kSoftmaxRegs>();
-        // ---- softmax: tile x = warp / 4 - 1, one thread per query row (TMEM lane)
+        // ---- softmax: lane x = warp / 4 - 1, one thread per query row (TMEM lane)
         const uint32_t x = (warp >> 2) - 1;
-        const uint32_t nb = x ? nb1 : nb0;
-        const uint32_t tile_x = x ? u.tile[1] : u.tile[0];
-        const uint32_t slot_x = x ? u.slot[1] : u.slot[0];
-        if (nb > 0) {
-            const uint32_t quarter = warp & 3;
-            const uint32_t r = quarter * 32 + lane;
-            const uint32_t qi = tile_x * 128u + r - p.shift;  // wraps (invalid) for r < shift in tile 0
-            const bool valid = tile_x * 128u + r >= p.shift && qi < p.m;
-            const uint32_t limit = valid ? p.rows[qi] : 0u;
-            const uint32_t first = valid && p.starts ? p.starts[qi] : 0u;  // its request's first cache row
-            const uint32_t lane_base = (quarter * 32u) << 16;
-            const uint32_t s_col = tmem + lane_base + x * 256, o_col = s_col + 128;
-            float m_used = -INFINITY, l = 0.0f;
-            for (uint32_t j = 0; j < nb; ++j) {
-                const uint32_t k0 = (u.b0 + j) * 128u;
-                tc::mbar_wait(&s_full[x], j & 1);
-                const bool dbg_me = p.dbg && blockIdx.x == 0 && x == 0 && r == 0;
-                if (dbg_me) p.dbg[j * 16 + 5] = globaltimer_ns();
-                tc::tc_fence_after();
-                // keys [0, nv) of the block are visible to this row (causal limit = the row's
-                // position; an invalid row sees none). Selected rows are scattered over the
-                // prompt, so a warp often sees few or none of a block's keys: chunks of 32 keys
-                // no lane of the warp sees are neither loaded nor exponentiated (P = 0), and a
-                // warp that sees nothing just writes P = 0.
-                // keys [ns, nv) of the block belong to the row's request (batched requests:
-                // rows of other requests' caches below `first` are masked too)
-                const uint32_t ns = first > k0 ? min(first - k0, 128u) : 0u;
-                uint32_t nv = !valid || limit < k0 ? 0u : min(limit - k0 + 1u, 128u);
-                if (ns >= nv) nv = 0u;
-                const uint32_t nv_max = __reduce_max_sync(0xffffffffu, nv);
-                const uint32_t nv_min = __reduce_min_sync(0xffffffffu, nv);
-                if (nv_max == 0) {
-                    uint32_t z[16];
+        const uint32_t ns_x = nst[x];
+        const uint32_t tile_x = split ? u.tile[0] : u.tile[x];
+        const uint32_t slot_x = split ? u.slot[0] : u.slot[x];
+        const uint32_t quarter = warp & 3;
+        const uint32_t r = quarter * 32 + lane;
+        const uint32_t qi = tile_x * 128u + r - p.shift;  // wraps (invalid) for r < shift in tile 0
+        const bool valid = tile_x * 128u + r >= p.shift && qi < p.m;
+        const uint32_t limit = valid ? p.rows[qi] : 0u;
+        const uint32_t first = valid && p.starts ? p.starts[qi] : 0u;  // its request's first cache row
+        const uint32_t lane_base = (quarter * 32u) << 16;
+        const uint32_t o_col = tmem + lane_base + x * 256 + 128;
+        float m_used = -INFINITY, l = 0.0f;
+        for (uint32_t s = 0; s < ns_x; ++s) {
+            const uint32_t k0 = (u.b0 + (split ? s : s >> 1)) * 128u + 64u * (split ? x : s & 1u);
+            const uint32_t s_col = tmem + lane_base + x * 256 + (s & 1) * 64;
+            if (lane == 0) WD_WAIT(&s_full[2 * x + (s & 1)], (s >> 1) & 1, 9, s);  // one poller per warp
+            __syncwarp();
+            const bool dbg_me = p.dbg && blockIdx.x == 0 && x == 0 && r == 0 && s < 64;
+            if (dbg_me) p.dbg[s * 16 + 5] = globaltimer_ns();
+            if (p.dbg && blockIdx.x == 0 && x == 1 && r == 0 && s < 64) p.dbg[s * 16 + 10] = globaltimer_ns();
+            tc::tc_fence_after();
+            // keys [ns, nv) of the 64-key step are visible to this row: the causal limit is
+            // the row's position (an invalid row sees none), and batched requests also mask
+            // the rows of other requests' caches below `first`. Selected rows are scattered
+            // over the prompt, so a warp often sees few or none of a step's keys: 32-key
+            // chunks no lane of the warp sees are neither loaded nor exponentiated (P = 0),
+            // and a warp that sees nothing just writes P = 0.
+            const uint32_t ns = first > k0 ? min(first - k0, 64u) : 0u;
+            uint32_t nv = !valid || limit < k0 ? 0u : min(limit - k0 + 1u, 64u);
+            if (ns >= nv) nv = 0u;
+            const uint32_t nv_max = __reduce_max_sync(0xffffffffu, nv);
+            const uint32_t nv_min = __reduce_min_sync(0xffffffffu, nv);
+            if (nv_max == 0) {
+                uint32_t z[16];
 #pragma unroll
-                    for (uint32_t e = 0; e < 16; ++e) z[e] = 0u;
-#pragma unroll
-                    for (uint32_t c = 0; c < 4; ++c) tc::tmem_st16(s_col + c * 16, z);
-                    tc::tmem_st_wait();
-                    tc::tc_fence_before();
-                    for (int q = 0; q < 3; ++q) tc::mbar_arrive(&p_part[3 * x + q]);
-                    tc::mbar_arrive(&p_full[x]);
-                    continue;
-                }
-                const uint32_t nch = (nv_max + 31) >> 5;  // warp-uniform
-                // the row's scores, one TMEM round trip (the softmax warpgroups hold 224
-                // registers each after setmaxnreg)
-                uint32_t v[4][32];
-                tc::tmem_ld32(s_col, v[0]);
-                if (nch > 1) tc::tmem_ld32(s_col + 32, v[1]);
-                if (nch > 2) tc::tmem_ld32(s_col + 64, v[2]);
-                if (nch > 3) tc::tmem_ld32(s_col + 96, v[3]);
-                tc::tmem_ld_wait();
-                if (dbg_me) p.dbg[j * 16 + 8] = globaltimer_ns();
-#pragma unroll
-                for (uint32_t c = 0; c < 4; ++c) {
-                    if (c < nch && nv_min < 32 * (c + 1)) {  // a lane's limit falls in this chunk
-#pragma unroll
-                        for (uint32_t e = 0; e < 32; ++e)
-                            if (32 * c + e >= nv) v[c][e] = __float_as_uint(-INFINITY);
-                    }
-                }
-                if (p.starts && __any_sync(0xffffffffu, ns > 0u)) {  // batched: below the request's start
-#pragma unroll
-                    for (uint32_t c = 0; c < 4; ++c)
-                        if (c < nch) {
-#pragma unroll
-                            for (uint32_t e = 0; e < 32; ++e)
-                                if (32 * c + e < ns) v[c][e] = __float_as_uint(-INFINITY);
-                        }
-                }
-                float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-#pragma unroll
-                for (uint32_t e = 0; e < 32; ++e) mx0 = fmaxf(mx0, __uint_as_float(v[0][e]));
-                if (nch > 1) {
-#pragma unroll
-                    for (uint32_t e = 0; e < 32; ++e) mx1 = fmaxf(mx1, __uint_as_float(v[1][e]));
-                }
-                if (nch > 2) {
-#pragma unroll
-                    for (uint32_t e = 0; e < 32; ++e) mx2 = fmaxf(mx2, __uint_as_float(v[2][e]));
-                }
-                if (nch > 3) {
-#pragma unroll
-                    for (uint32_t e = 0; e < 32; ++e) mx3 = fmaxf(mx3, __uint_as_float(v[3][e]));
-                }
-                const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.scale_log2;
-                if (dbg_me) p.dbg[j * 16 + 7] = globaltimer_ns();
-                float alpha = 1.0f;
-                const bool grow = mx > m_used + kRescaleThreshold || (m_used == -INFINITY && mx > -INFINITY);
-                if (grow) {
-                    alpha = m_used == -INFINITY ? 0.0f : tc::ex2_approx(m_used - mx);
-                    m_used = mx;
-                    l *= alpha;
-                }
-                if (j > 0 && __any_sync(0xffffffffu, grow && alpha != 1.0f)) {
-                    // every earlier PV of this tile must have landed before O is rescaled
-                    tc::mbar_wait(&o_done[x], (j - 1) & 1);
-                    tc::tc_fence_after();
-#pragma unroll
-                    for (uint32_t c = 0; c < 128; c += 32) {
-                        uint32_t o[32];
-                        tc::tmem_ld32(o_col + c, o);
-                        tc::tmem_ld_wait();
-#pragma unroll
-                        for (uint32_t e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                        tc::tmem_st32(o_col + c, o);
-                    }
-                    tc::tmem_st_wait();
-                }
-                const float neg_m = m_used == -INFINITY ? 0.0f : -m_used;
-                f2 lsum = mk2(0.f, 0.f);
-                const f2 sc2 = mk2(p.scale_log2, p.scale_log2), nm2 = mk2(neg_m, neg_m);
-#pragma unroll
-                for (uint32_t c = 0; c < 4; ++c) {
-                    // exp2(s * scale - m) in packed pairs: three of every four pairs on MUFU,
-                    // one on the FMA pipe (balances the MUFU and issue budgets); masked keys
-                    // give exactly 0. P_X(j) (bf16 pairs) goes to TMEM columns [16c, 16c+16)
-                    // of S_X (whose scores are all in registers by now).
-                    uint32_t pk[16];
-                    if (c < nch) {
-#pragma unroll
-                        for (uint32_t e = 0; e < 32; e += 2) {
-                            const f2 xs = fma2(mk2(__uint_as_float(v[c][e]), __uint_as_float(v[c][e + 1])), sc2, nm2);
-                            f2 ex;
-                            if ((MPIC_POLY_MASK >> ((e >> 1) & 7)) & 1u) ex = exp2_poly2(xs);
-                            else ex = mk2(tc::ex2_approx(lo(xs)), tc::ex2_approx(hi(xs)));
-                            lsum = add2(lsum, ex);
-                            pk[e >> 1] = pack_bf16(lo(ex), hi(ex));
-                        }
-                    } else {
-#pragma unroll
-                        for (uint32_t e = 0; e < 16; ++e) pk[e] = 0u;
-                    }
-                    tc::tmem_st16(s_col + c * 16, pk);
-                    if (c < 3) {  // keys [0, 32(c+1)) of P_X(j) are in TMEM: that part of PV can go
-                        tc::tmem_st_wait();
-                        tc::tc_fence_before();
-                        tc::mbar_arrive(&p_part[3 * x + c]);
-                    }
-                }
-                if (dbg_me) p.dbg[j * 16 + 9] = globaltimer_ns();
-                const float l0 = lo(lsum), l1 = hi(lsum);
-                l += l0 + l1;
+                for (uint32_t e = 0; e < 16; ++e) z[e] = 0u;
+                tc::tmem_st16(s_col, z);
+                tc::tmem_st16(s_col + 16, z);
                 tc::tmem_st_wait();
                 tc::tc_fence_before();
-                if (dbg_me) p.dbg[j * 16 + 6] = globaltimer_ns();
-                tc::mbar_arrive(&p_full[x]);
+                tc::mbar_arrive(&p_full[2 * x + (s & 1)]);
+                continue;
             }
-            // ---- epilogue: O / l, or the unnormalised partial + (m, l) for the combine
-            tc::mbar_wait(&o_done[x], (nb - 1) & 1);
-            tc::tc_fence_after();
+            const uint32_t nch = (nv_max + 31) >> 5;  // warp-uniform: 1 or 2
+            uint32_t v[2][32];
+            tc::tmem_ld32(s_col, v[0]);
+            if (nch > 1) tc::tmem_ld32(s_col + 32, v[1]);
+            tc::tmem_ld_wait();
+            if (dbg_me) p.dbg[s * 16 + 8] = globaltimer_ns();
+#pragma unroll
+            for (uint32_t c = 0; c < 2; ++c) {
+                if (c < nch && nv_min < 32 * (c + 1)) {  // a lane's limit falls in this chunk
+#pragma unroll
+                    for (uint32_t e = 0; e < 32; ++e)
+                        if (32 * c + e >= nv) v[c][e] = __float_as_uint(-INFINITY);
+                }
+            }
+            if (p.starts && __any_sync(0xffffffffu, ns > 0u)) {  // batched: below the request's start
+#pragma unroll
+                for (uint32_t c = 0; c < 2; ++c)
+                    if (c < nch) {
+#pragma unroll
+                        for (uint32_t e = 0; e < 32; ++e)
+                            if (32 * c + e < ns) v[c][e] = __float_as_uint(-INFINITY);
+                    }
+            }
+            float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+            for (uint32_t e = 0; e < 32; e += 2) {
+                mx0 = fmaxf(mx0, __uint_as_float(v[0][e]));
+                mx1 = fmaxf(mx1, __uint_as_float(v[0][e + 1]));
+            }
+            if (nch > 1) {
+#pragma unroll
+                for (uint32_t e = 0; e < 32; e += 2) {
+                    mx2 = fmaxf(mx2, __uint_as_float(v[1][e]));
+                    mx3 = fmaxf(mx3, __uint_as_float(v[1][e + 1]));
+                }
+            }
+            const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.scale_log2;
+            if (dbg_me) p.dbg[s * 16 + 7] = globaltimer_ns();
+            float alpha = 1.0f;
+            const bool grow = mx > m_used + kRescaleThreshold || (m_used == -INFINITY && mx > -INFINITY);
+            if (grow) {
+                alpha = m_used == -INFINITY ? 0.0f : tc::ex2_approx(m_used - mx);
+                m_used = mx;
+                l *= alpha;
+            }
+            if (s > 0 && __any_sync(0xffffffffu, grow && alpha != 1.0f)) {
+                // every earlier PV of this lane must have landed before O is rescaled (S_X(s)
+                // completing implies PV_X(s - 2) did, so only phase s - 1 can be pending)
+                if (lane == 0) WD_WAIT(&o_done[x], (s - 1) & 1, 10, 0);
+                __syncwarp();
+                tc::tc_fence_after();
+#pragma unroll
+                for (uint32_t c = 0; c < 128; c += 32) {
+                    uint32_t o[32];
+                    tc::tmem_ld32(o_col + c, o);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (uint32_t e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                    tc::tmem_st32(o_col + c, o);
+                }
+                tc::tmem_st_wait();
+            }
+            const float neg_m = m_used == -INFINITY ? 0.0f : -m_used;
+            f2 lsum = mk2(0.f, 0.f);
+            const f2 sc2 = mk2(p.scale_log2, p.scale_log2), nm2 = mk2(neg_m, neg_m);
+#pragma unroll
+            for (uint32_t c = 0; c < 2; ++c) {
+                // exp2(s * scale - m) in packed pairs, a quarter of them on the FMA pipe
+                // (balances the MUFU and issue budgets); masked keys give exactly 0. P (bf16
+                // pairs) goes to TMEM columns [16c, 16c + 16) of the step's S buffer (whose
+                // scores are all in registers by now).
+                uint32_t pk[16];
+                if (c < nch) {
+#pragma unroll
+                    for (uint32_t e = 0; e < 32; e += 2) {
+                        const f2 xs = fma2(mk2(__uint_as_float(v[c][e]), __uint_as_float(v[c][e + 1])), sc2, nm2);
+                        f2 ex;
+                        if ((MPIC_POLY_MASK >> ((e >> 1) & 7)) & 1u) ex = exp2_poly2(xs);
+                        else ex = mk2(tc::ex2_approx(lo(xs)), tc::ex2_approx(hi(xs)));
+                        lsum = add2(lsum, ex);
+                        pk[e >> 1] = pack_bf16(lo(ex), hi(ex));
+                    }
+                } else {
+#pragma unroll
+                    for (uint32_t e = 0; e < 16; ++e) pk[e] = 0u;
+                }
+                tc::tmem_st16(s_col + c * 16, pk);
+            }
+            if (dbg_me) p.dbg[s * 16 + 9] = globaltimer_ns();
+            l += lo(lsum) + hi(lsum);
+            tc::tmem_st_wait();
+            tc::tc_fence_before();
+            if (dbg_me) p.dbg[s * 16 + 6] = globaltimer_ns();
+            if (p.dbg && blockIdx.x == 0 && x == 1 && r == 0 && s < 64) p.dbg[s * 16 + 11] = globaltimer_ns();
+            tc::mbar_arrive(&p_full[2 * x + (s & 1)]);
+        }
+        // ---- epilogue: O / l, or the unnormalised partial + (m, l) for the combine. Split
+        // mode: lane 1 hands its (m, l) over through shared memory and lane 0 merges both
+        // accumulators (same TMEM lanes) into the tile's result.
+        // a barrier of its own for the last PV: with S double-buffered, o_done can be one
+        // phase behind or already past the last PV here, and its parity cannot tell which
+        if (lane == 0) WD_WAIT(&o_fin[x], 0, 12, 0);
+        __syncwarp();
+        tc::tc_fence_after();
+        const bool cta_stamp = x == 0 && r == 0 && p.dbg && blockIdx.x < kDbgCtas;
+        if (cta_stamp) p.dbg[kDbgCtaBase + 8 * blockIdx.x + 5] = globaltimer_ns();
+        float wa = 1.0f, wb = 0.0f;
+        if (split) {
+            if (x == 1) ml_x[r] = make_float2(m_used, l);
+            tc::named_bar_sync(1, 256);
+            if (x == 1) goto softmax_done;
+            const float2 mb = ml_x[r];
+            const float M = fmaxf(m_used, mb.x);
+            wa = m_used == -INFINITY ? 0.0f : tc::ex2_approx(m_used - M);
+            wb = mb.x == -INFINITY ? 0.0f : tc::ex2_approx(mb.x - M);
+            l = wa * l + wb * mb.y;
+            m_used = M;
+        }
+        {
             const bool direct = slot_x == kNoTile;
             const float inv = l > 0.0f ? 1.0f / l : 0.0f;
-#pragma unroll
+            const uint32_t o_col_b = tmem + lane_base + 256 + 128;  // lane 1's O (split mode)
+#pragma unroll 1
             for (uint32_t c = 0; c < 128; c += 32) {
                 uint32_t o[32];
                 tc::tmem_ld32(o_col + c, o);
-                tc::tmem_ld_wait();
+                if (split) {
+                    uint32_t ob[32];
+                    tc::tmem_ld32(o_col_b + c, ob);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (uint32_t e = 0; e < 32; ++e)
+                        o[e] = __float_as_uint(wa * __uint_as_float(o[e]) + wb * __uint_as_float(ob[e]));
+                } else {
+                    tc::tmem_ld_wait();
+                }
                 if (!valid) continue;
                 if (direct) {
                     uint4* dst = reinterpret_cast<uint4*>(p.out + (size_t)qi * p.h + u.head * 128u + c);
@@ -531,28 +596,33 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                         dst[q] = w;
                     }
                 } else {
-                    float4* dst = reinterpret_cast<float4*>(p.part_o + ((size_t)slot_x * 128 + r) * 128 + c);
+                    // partial layout [slot][32 float4 columns][128 rows]: a warp's 32 rows of one
+                    // float4 column are 512 contiguous bytes (one coalesced store per column)
+                    float4* dst = reinterpret_cast<float4*>(p.part_o) + ((size_t)slot_x * 32 + c / 4) * 128 + r;
 #pragma unroll
                     for (uint32_t e = 0; e < 8; ++e)
-                        dst[e] = make_float4(__uint_as_float(o[4 * e]), __uint_as_float(o[4 * e + 1]),
-                                             __uint_as_float(o[4 * e + 2]), __uint_as_float(o[4 * e + 3]));
+                        __stcg(dst + (size_t)e * 128, make_float4(__uint_as_float(o[4 * e]), __uint_as_float(o[4 * e + 1]),
+                                                                  __uint_as_float(o[4 * e + 2]), __uint_as_float(o[4 * e + 3])));
                 }
             }
             if (valid && !direct) p.part_ml[(size_t)slot_x * 128 + r] = make_float2(m_used, l);
         }
+        if (cta_stamp) p.dbg[kDbgCtaBase + 8 * blockIdx.x + 6] = globaltimer_ns();
+    softmax_done:;
     }
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
     if (warp == 0) tc::tmem_dealloc(tmem, 512);
-    if (p.dbg && threadIdx.x == 0 && blockIdx.x < kDbgCtas) p.dbg[kDbgCtaBase + 4 * blockIdx.x + 1] = globaltimer_ns();
+    if (p.dbg && threadIdx.x == 0 && blockIdx.x < kDbgCtas) p.dbg[kDbgCtaBase + 8 * blockIdx.x + 1] = globaltimer_ns();
 }
 
 // Merge split partials of one (tile, head): O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s.
-// One warp per query row (blockIdx.y picks 8 rows of the job), lanes along the head
-// dimension: coalesced 512-B partial reads, 256-B bf16 output rows. Few registers per thread
-// (the (m, l) pass first, then the partials four splits at a time) so that several CTAs share
-// an SM: the kernel is a short burst of latency-bound warps, and occupancy is what hides it.
+// A thread per (row, float4 column) of the job (blockIdx.y picks 256 of its 128 x 32): lanes
+// run along the rows, so every partial read is a coalesced 512-B line per warp ([slot][32
+// float4 columns][128 rows], as the attention kernel writes them). Few registers per
+// thread (the (m, l) pass first, then the partials four splits at a time) so that several
+// CTAs share an SM: the kernel is a short burst of latency-bound warps.
 __global__ void __launch_bounds__(256, 6) attn_combine_kernel(const AttnCombine* __restrict__ jobs,
                                                               const float* __restrict__ part_o,
                                                               const float2* __restrict__ part_ml,
@@ -562,14 +632,14 @@ __global__ void __launch_bounds__(256, 6) attn_combine_kernel(const AttnCombine*
     tc::pdl_trigger();
     tc::pdl_wait();
     const AttnCombine j = jobs[blockIdx.x];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t r = blockIdx.y * 8 + warp;
+    const uint32_t t = blockIdx.y * 256 + threadIdx.x;
+    const uint32_t r = t & 127, col4 = t >> 7;
     if (j.tile * 128u + r < shift) return;
     const uint32_t qi = j.tile * 128u + r - shift;
     if (qi >= m) return;
     const uint32_t n = min(j.n, kMaxSplits);
     const float2* ml = part_ml + (size_t)j.slot0 * 128 + r;
-    const float4* po = reinterpret_cast<const float4*>(part_o + ((size_t)j.slot0 * 128 + r) * 128) + lane;
+    const float4* po = reinterpret_cast<const float4*>(part_o) + ((size_t)j.slot0 * 32 + col4) * 128 + r;
     float M = -INFINITY;
 #pragma unroll 4
     for (uint32_t s = 0; s < n; ++s) M = fmaxf(M, __ldcg(ml + (size_t)s * 128).x);
@@ -582,7 +652,7 @@ __global__ void __launch_bounds__(256, 6) attn_combine_kernel(const AttnCombine*
         for (uint32_t i = 0; i < 4; ++i)
             if (s0 + i < n) {
                 w[i] = __ldcg(ml + (size_t)(s0 + i) * 128);
-                ov[i] = __ldcs(po + (size_t)(s0 + i) * 128 * 32);
+                ov[i] = __ldcs(po + (size_t)(s0 + i) * 32 * 128);
             }
 #pragma unroll
         for (uint32_t i = 0; i < 4; ++i)
@@ -599,7 +669,7 @@ __global__ void __launch_bounds__(256, 6) attn_combine_kernel(const AttnCombine*
     uint2 pk;
     pk.x = pack_bf16(acc.x * inv, acc.y * inv);
     pk.y = pack_bf16(acc.z * inv, acc.w * inv);
-    reinterpret_cast<uint2*>(out + (size_t)qi * h + j.head * 128u)[lane] = pk;
+    *reinterpret_cast<uint2*>(out + (size_t)qi * h + j.head * 128u + col4 * 4) = pk;
 }
 
 }  // namespace
@@ -674,15 +744,16 @@ AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads, cons
             if (open) plan.units.push_back(cur);
         }
     }
-    // longest items first (they set the critical path); items of one head stay together
-    // Longest-processing-time first by estimated cost: a block costs ~1.5x for a pair of
-    // tiles (ping-pong hides part of one tile's softmax behind the other's MMAs) than for
-    // one tile; per-item setup ~2 blocks.
+    // Longest-processing-time first by estimated cost (half-block units, from the kernel's
+    // measured per-CTA spans): a pair item's 128-key block ~2 (two tiles' MMAs), a block one
+    // tile of a pair streams alone ~1.5 (its lane's softmax chain), a split item's block ~1
+    // (both lanes on one tile); per-item setup ~3 blocks.
     static const bool by_cost = getenv("MPIC_ATTN_SORT_LEN") == nullptr;  // diagnostics: 1 = by length
     auto cost = [](const AttnUnit& a) {
-        const uint32_t len = std::max(a.b1[0], a.tile[1] == kNoTile ? 0u : a.b1[1]) - a.b0;
-        const uint32_t both = a.tile[1] == kNoTile ? 0u : std::min(a.b1[0], a.b1[1]) - a.b0;
-        return 2 * (len - both) + 3 * both + 4;  // half-block units
+        if (a.tile[1] == kNoTile) return 2 * (a.b1[0] - a.b0) + 6;
+        const uint32_t len = std::max(a.b1[0], a.b1[1]) - a.b0;
+        const uint32_t both = std::min(a.b1[0], a.b1[1]) - a.b0;
+        return 4 * both + 3 * (len - both) + 6;
     };
     std::stable_sort(plan.units.begin(), plan.units.end(), [&](const AttnUnit& a, const AttnUnit& b) {
         if (by_cost) return cost(a) > cost(b);
@@ -735,7 +806,8 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
         return e && atoi(e) == 2;
     }();
     p.link_nostore = nostore ? 1u : 0u;
-    const size_t smem = (2 + kKStages + kVStages) * kTile + 1024 + (1 + 2 * kKStages + 2 * kVStages + 12) * 8 + 16;
+    const size_t smem = (2 + kKStages + kVStages) * kTile + 1024 + (1 + 2 * kKStages + 2 * kVStages + 12) * 8 + 16 +
+                        128 * sizeof(float2);
     static bool attr = false;
     if (!attr) {
         MPIC_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

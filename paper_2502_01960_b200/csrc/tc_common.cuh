@@ -377,6 +377,16 @@ __device__ __forceinline__ void fence_async_shared() {
 // prologue overlaps this kernel's tail), and wait for the previous kernel's completion and
 // memory before touching anything it produced.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// One lane of a converged warp (elect.sync): the issuing lane of a warp-uniform MMA loop.
+__device__ __forceinline__ bool elect_one_sync() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.b32 %0, 1, 0, P;\n}"
+        : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Warpgroup register re-allocation (all 4 warps of a warpgroup must execute it).

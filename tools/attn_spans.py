@@ -23,6 +23,18 @@ def summarise(path):
         n0 = int(b10) - int(b0); n1 = int(b11) - int(b0) if int(t1) != 999 else 0
         rows.append((float(s), float(e), max(n0, n1) - min(n0, n1) if n1 else n0, min(n0, n1) if n1 else 0))
     span = max(r[1] for r in rows)
+    ph = []
+    for l in g:
+        m = re.search(r"start\s+([\d.]+) end\s+([\d.]+).*mma0\s+(-?[\d.]+) lastmma\s+(-?[\d.]+) epi\s+(-?[\d.]+) epi_end\s+(-?[\d.]+)", l)
+        if m:
+            s0, e0, a, b, c, d = map(float, m.groups())
+            if min(a, b, c, d) >= 0:
+                ph.append((a - s0, b - a, c - b, d - c, e0 - d))
+    phase_txt = ""
+    if ph:
+        pm = np.median(np.array(ph), axis=0)
+        phase_txt = (f"; per CTA median: start->mma0 {pm[0]:.2f}, mma loop {pm[1]:.2f}, lastmma->epi {pm[2]:.2f}, "
+                     f"epilogue {pm[3]:.2f}, epi->end {pm[4]:.2f} us")
     A = np.array([[1, r[2], r[3]] for r in rows], float)
     y = np.array([r[1] - r[0] for r in rows])
     coef = np.linalg.lstsq(A, y, rcond=None)[0]
@@ -34,7 +46,7 @@ def summarise(path):
             ph.append((v[1] - v[0], v[2] - v[1], v[3] - v[2], v[4] - v[0]))
     phs = np.median(np.array(ph), axis=0) if ph else [float("nan")] * 4
     return (f"{path}: span {span:6.1f} us, sum/148 {y.sum()/148:6.1f}; fit setup {coef[0]:.2f} single-blk {coef[1]:.2f} "
-            f"pair-blk {coef[2]:.2f} us; CTA0 softmax ld {phs[0]:.2f} max {phs[1]:.2f} exp {phs[2]:.2f} total {phs[3]:.2f} us")
+            f"pair-blk {coef[2]:.2f} us{phase_txt}; CTA0 softmax ld {phs[0]:.2f} max {phs[1]:.2f} exp {phs[2]:.2f} total {phs[3]:.2f} us")
 
 for p in sys.argv[1:]:
     print(summarise(p))
