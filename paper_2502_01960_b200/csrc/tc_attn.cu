@@ -328,16 +328,40 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 if (s + 1 == ns) tc::mma_commit(&o_fin[x]);
             }
         };
-        // release every block below the lowest block a later MMA of this lane still reads
+        // release every block below the lowest block a later MMA of this lane still reads.
+        // A block this lane never reads (pair mode, the other tile's longer range) is released
+        // only once it has landed: an early arrival would count towards the stage's previous
+        // phase and free it under the other lane's MMAs.
         auto release = [&](uint32_t next_s, uint32_t next_pv) {
             const uint32_t lk = next_s < ns ? blk_of(next_s) : nblk;
             const uint32_t lv = next_pv < ns ? blk_of(next_pv) : nblk;
+            const uint32_t used = min(blk_of(ns - 1) + 1, nblk);  // blocks this lane reads: [0, used)
+            // blocks this lane read: released as soon as no later MMA of the lane reads them
             if (tc::elect_one_sync()) {
-                for (uint32_t j = k_rel; j < lk; ++j) tc::mma_commit(&k_empty[j % kKStages]);
-                for (uint32_t j = v_rel; j < lv; ++j) tc::mma_commit(&v_empty[j % kVStages]);
+                for (uint32_t j = k_rel; j < min(lk, used); ++j) tc::mma_commit(&k_empty[j % kKStages]);
+                for (uint32_t j = v_rel; j < min(lv, used); ++j) tc::mma_commit(&v_empty[j % kVStages]);
             }
-            k_rel = max(k_rel, lk);
-            v_rel = max(v_rel, lv);
+            k_rel = max(k_rel, min(lk, used));
+            v_rel = max(v_rel, min(lv, used));
+            // blocks it never reads (pair mode, the other tile's longer range): released after
+            // the lane's last MMA, in the producer's load order (K_j, V_j, K_j+1, ...), each
+            // once it has landed (never while this lane still has PVs to issue: the other lane
+            // could be waiting for a V stage only this lane's release frees)
+            if (next_pv < ns) return;
+            while (k_rel < lk || v_rel < lv) {
+                const bool do_k = k_rel < lk && (v_rel >= lv || k_rel <= v_rel);
+                if (do_k) {
+                    need_k(k_rel);
+                    __syncwarp();
+                    if (tc::elect_one_sync()) tc::mma_commit(&k_empty[k_rel % kKStages]);
+                    ++k_rel;
+                } else {
+                    need_v(v_rel);
+                    __syncwarp();
+                    if (tc::elect_one_sync()) tc::mma_commit(&v_empty[v_rel % kVStages]);
+                    ++v_rel;
+                }
+            }
         };
         if (lane == 0) WD_WAIT(q_full, 0, 5, 0);
         need_k(blk_of(min(2u, ns) - 1));
