@@ -463,7 +463,11 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         }
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {
+        // MMA issue (even CTA of the pair). The whole warp runs the loop (warp-uniform, so
+        // the descriptors live in uniform registers); lane 0 polls the barriers, one elected
+        // lane issues each k-block's MMAs back to back. (A lone issuing thread wrapped every
+        // tcgen05.mma in an elect/broadcast loop: ~15 instructions of issue overhead per MMA.)
+        if (rank == 0) {
             const uint32_t idesc0 = tc::idesc_bf16(256, a.P0);
             const uint32_t idesc1 = tc::idesc_bf16(256, a.P1 ? a.P1 : 16);
             uint32_t item = 0, s = 0, ph = 0;
@@ -472,35 +476,39 @@ __global__ void __launch_bounds__(kPgThreads, 1)
             for (uint32_t tile = cl; tile < a.tiles; tile += a.clusters, ++item) {
                 const uint32_t b = a.nbuf == 2 ? (item & 1) : 0u;
                 const uint32_t use = a.nbuf == 2 ? (item >> 1) : item;
-                tc::mbar_wait_cluster(&acc_empty[b], (use & 1) ^ 1);
+                if (lane == 0) tc::mbar_wait_cluster(&acc_empty[b], (use & 1) ^ 1);
+                __syncwarp();
                 tc::tc_fence_after();
                 const uint32_t d = tmem + b * a.G;
                 for (uint32_t kb = kb0; kb < kb1; kb += a.kps) {
                     const uint32_t nsub = min(a.kps, kb1 - kb);
                     const long long w0 = ts ? clock64() : 0;
-                    tc::mbar_wait(&full[s], ph);
+                    if (lane == 0) tc::mbar_wait(&full[s], ph);
+                    __syncwarp();
                     if (ts) mw += clock64() - w0;
                     tc::tc_fence_after();
-                    for (uint32_t j = 0; j < nsub && !(a.dbg & 8); ++j) {
-                        const uint32_t w_base = tc::smem_u32(smem + s * a.stage_bytes + j * a.sub_bytes);
-                        const uint32_t x_base = w_base + kPgWBytes;
+                    if (tc::elect_one_sync()) {
+                        for (uint32_t j = 0; j < nsub && !(a.dbg & 8); ++j) {
+                            const uint32_t w_base = tc::smem_u32(smem + s * a.stage_bytes + j * a.sub_bytes);
+                            const uint32_t x_base = w_base + kPgWBytes;
 #pragma unroll
-                        for (uint32_t kk = 0; kk < 4; ++kk) {
-                            const uint64_t adesc = tc::desc_k_sw128(w_base + kk * 32);
-                            const uint32_t acc = (kb + j > kb0 || kk > 0) ? 1u : 0u;
-                            tc::mma_bf16_pair(d, adesc, tc::desc_k_sw128(x_base + kk * 32), idesc0, acc);
-                            if (a.P1)
-                                tc::mma_bf16_pair(d + a.P0, adesc, tc::desc_k_sw128(x_base + a.xoff1 + kk * 32),
-                                                  idesc1, acc);
+                            for (uint32_t kk = 0; kk < 4; ++kk) {
+                                const uint64_t adesc = tc::desc_k_sw128(w_base + kk * 32);
+                                const uint32_t acc = (kb + j > kb0 || kk > 0) ? 1u : 0u;
+                                tc::mma_bf16_pair(d, adesc, tc::desc_k_sw128(x_base + kk * 32), idesc0, acc);
+                                if (a.P1)
+                                    tc::mma_bf16_pair(d + a.P0, adesc, tc::desc_k_sw128(x_base + a.xoff1 + kk * 32),
+                                                      idesc1, acc);
+                            }
                         }
+                        tc::mma_commit_pair_mcast(&empty[s], pair_mask);
                     }
-                    tc::mma_commit_pair_mcast(&empty[s], pair_mask);
                     if (++s == a.stages) { s = 0; ph ^= 1; }
                 }
-                tc::mma_commit_pair_mcast(&acc_full[b], pair_mask);
-                if (ts) ts[2] = gtimer();
+                if (tc::elect_one_sync()) tc::mma_commit_pair_mcast(&acc_full[b], pair_mask);
+                if (ts && lane == 0) ts[2] = gtimer();
             }
-            if (ts) {
+            if (ts && lane == 0) {
                 ts[7] = mw;
                 ts[8] = clock64() - m0;
             }
