@@ -559,10 +559,47 @@ def run_ours(args, world, rank, local):
                         "timing": "host wall clock per request (the loader is host I/O)"}
         finally:
             shutil.rmtree(ddir, ignore_errors=True)
+    sweep = None
+    if args.disk and args.k_sweep:
+        sweep = disk_k_sweep(args, mp, torch, model, cfg, prompt, segs, dev_chunks, stream, L, H, D, h, n, world,
+                             rank, [int(x) for x in args.k_sweep.split(",")])
     if not args.no_e2e:
         e2e = time_host_leg(host_k, host_v, "bf16 Host-tier")
         if args.e2e_fp32:
             e2e_fp32 = time_host_leg(host_kf, host_vf, "fp32 .mpic-v1")
+
+    # ---- fp32 mode: the same request at the reference's own precision (fp32 weights, KV and
+    # arithmetic: SIMT FFMA GEMMs with two-level summation + fp32 online-softmax attention;
+    # parity 1e-4 vs the reference in tests/test_gpu_llava.py), device-resident chunks ----
+    fp32_mode = None
+    if args.fp32_mode and rank == 0:
+        model32 = mp.Model(cfg, mp.F32, device=dev)
+        ws32 = mp.Workspace(model32, m, n)
+        g32 = np.random.default_rng(1234 + rank)
+        chunks32 = []
+        for t in images:
+            rk = g32.random((t, h), dtype=np.float32) - 0.5
+            rv = g32.random((t, h), dtype=np.float32) - 0.5
+            kv = mp.KV(L, t, H, D, mp.F32, dev)
+            kv.upload(np.broadcast_to(rk, (L, t, h)), np.broadcast_to(rv, (L, t, h)))
+            chunks32.append(kv)
+        linked32 = mp.KV(L, n, H, D, mp.F32, dev)
+        mp.request_prefill(model32, ws32, prompt, chunks32, linked32, k=k, stream=stream)
+        torch.cuda.synchronize()
+        e32 = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        with torch.cuda.stream(stream):
+            e32[0].record(stream)
+            for i in range(2):
+                mp.request_prefill(model32, ws32, prompt, chunks32, linked32, k=k, stream=stream)
+                e32[i + 1].record(stream)
+        torch.cuda.synchronize()
+        ms32 = [e32[i].elapsed_time(e32[i + 1]) for i in range(2)]
+        fp32_mode = {"value": n / (statistics.mean(ms32) / 1e3), "unit": "prompt tokens/s",
+                     "ms_per_step": round(statistics.mean(ms32), 3), "steps": 2, "dtype": "f32",
+                     "path": "mpic_request_prefill, fp32 model: SIMT FFMA GEMMs (two-level summation) + fp32 "
+                             "online-softmax attention, fp32 chunks HBM-resident (the reference's precision; "
+                             "parity <= 1e-4 in tests/test_gpu_llava.py)"}
+        del model32, ws32, chunks32, linked32
 
     # ---- roofline of the dominant phase ----
     hbm, tf_burst, tf_sust, peak_src = load_peaks()
@@ -632,9 +669,82 @@ def run_ours(args, world, rank, local):
         max(sum(gemm_fl.values()) / (tf_sust * 1e12), sum(gemm_b.values()) / (hbm * 1e9)) +
         attn_fl / (tf_sust * 1e12))) * 1e3
     return dict(value=value, ms_per_step=ms_per_step, per_step=per_step, host_ms=host_ms, e2e=e2e,
-                e2e_fp32=e2e_fp32, e2e_disk=e2e_disk,
+                e2e_fp32=e2e_fp32, e2e_disk=e2e_disk, fp32_mode=fp32_mode, k_sweep=sweep,
                 launches=launches, roofline=roofline, phases=per_phase, clocks=clk.summary(),
                 n=n, m=m, floor_ms=floor_ms, world=world)
+
+
+def disk_k_sweep(args, mp, torch, model, cfg, prompt, segs, dev_chunks, stream, L, H, D, h, n, world, rank, ks):
+    """MRAG sweep (SURVEY config D): for each MPIC-k budget (k >= the image length = full
+    recompute), the request with its chunks read from .mpic v3 files — warm (page cache, the
+    files were just written) and cold (posix_fadvise DONTNEED on every file before each
+    request, so the reads come from the device) — beside the device-resident time of the
+    same request. Host wall clock per request (the loader is host I/O)."""
+    import shutil
+    import tempfile
+    ddir = tempfile.mkdtemp(prefix="mpic_sweep_", dir=args.disk_dir)
+    out = {"k": [], "recompute_rows": [], "device_ms": [], "warm_ttft_ms": [], "cold_ttft_ms": [],
+           "what": "per k: device-resident request (CUDA events), then from .mpic v3 bf16 files warm and cold "
+                   "(host wall clock, median of the timed requests)"}
+    try:
+        paths = []
+        gd = np.random.default_rng(1234 + rank)
+        for i, seg in enumerate([sg for sg in segs if sg[0] == "image"]):
+            t = seg[2]
+            rk = gd.random((t, h), dtype=np.float32) - 0.5
+            rv = gd.random((t, h), dtype=np.float32) - 0.5
+            path = os.path.join(ddir, f"chunk{i}.mpic")
+            mp.write_mpic(path, cfg, seg[1], np.broadcast_to(rk, (L, t, h)), np.broadcast_to(rv, (L, t, h)), bf16=True)
+            paths.append(path)
+        out["file_bytes_per_request"] = int(sum(os.path.getsize(x) for x in paths))
+
+        def drop_cache():
+            for pth in paths:
+                fd = os.open(pth, os.O_RDONLY)
+                try:
+                    os.fsync(fd)
+                    os.posix_fadvise(fd, 0, 0, os.POSIX_FADV_DONTNEED)
+                finally:
+                    os.close(fd)
+
+        reps = max(2, min(args.steps, 3))
+        for kk in ks:
+            sel = mp.select_tokens(prompt, mp.POLICY_MPIC_K, kk)
+            m = len(sel)
+            ws = mp.Workspace(model, m, n)
+            linked = mp.KV(L, n, H, D, mp.BF16, torch.cuda.current_device())
+            mp.request_prefill(model, ws, prompt, dev_chunks, linked, k=kk, stream=stream)
+            torch.cuda.synchronize()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+            with torch.cuda.stream(stream):
+                ev[0].record(stream)
+                for i in range(reps):
+                    mp.request_prefill(model, ws, prompt, dev_chunks, linked, k=kk, stream=stream)
+                    ev[i + 1].record(stream)
+            torch.cuda.synchronize()
+            dev_ms = statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(reps))
+            mp.request_prefill_files(model, ws, prompt, paths, linked, k=kk, stream=stream)  # page cache warm
+            torch.cuda.synchronize()
+            warm, cold = [], []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                mp.request_prefill_files(model, ws, prompt, paths, linked, k=kk, stream=stream)
+                warm.append((time.perf_counter() - t0) * 1e3)
+            for _ in range(reps):
+                drop_cache()
+                t0 = time.perf_counter()
+                mp.request_prefill_files(model, ws, prompt, paths, linked, k=kk, stream=stream)
+                cold.append((time.perf_counter() - t0) * 1e3)
+            out["k"].append(kk)
+            out["recompute_rows"].append(m)
+            out["device_ms"].append(round(dev_ms, 3))
+            out["warm_ttft_ms"].append(round(statistics.median(warm), 2))
+            out["cold_ttft_ms"].append(round(statistics.median(cold), 2))
+            del ws, linked
+            torch.cuda.empty_cache()
+    finally:
+        shutil.rmtree(ddir, ignore_errors=True)
+    return out
 
 
 def run_head_parallel(args, world, rank, local):
@@ -834,9 +944,15 @@ def main():
     ap.add_argument("--disk", action="store_true",
                     help="also time the request with every chunk read from its .mpic file")
     ap.add_argument("--disk-dir", default=None, help="where the .mpic files are written")
+    ap.add_argument("--k-sweep", default=None,
+                    help="with --disk: comma-separated MPIC-k budgets timed device-resident, warm and cold "
+                         "(config D: 0,16,32,64,2304)")
     ap.add_argument("--k", type=int, default=None, help="MPIC-k budget (default: the config's)")
     ap.add_argument("--batch", type=int, default=64,
                     help="config E: requests per batched varlen pass (1 = one request at a time)")
+    ap.add_argument("--fp32-mode", action="store_true", default=True,
+                    help="also time the request in fp32 mode (the reference's precision)")
+    ap.add_argument("--no-fp32-mode", dest="fp32_mode", action="store_false")
     ap.add_argument("--no-serving", action="store_true",
                     help="skip the config-E serving key of the default (config C) line")
     ap.add_argument("--cpu-leg", action="store_true", help=argparse.SUPPRESS)
@@ -962,6 +1078,7 @@ def main():
                                          "KV, weights synthesised from seed 1)",
                 "config": cfg_json,
                 "e2e": r["e2e"], "e2e_fp32_host": r["e2e_fp32"], "e2e_disk": r["e2e_disk"],
+                "fp32_mode": r.get("fp32_mode"), "k_sweep": r.get("k_sweep"),
                 "gpu_launches": r["launches"],
                 "roofline": r["roofline"],
                 "request_roofline_frac": round(r["floor_ms"] / r["ms_per_step"], 4),
