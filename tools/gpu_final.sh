@@ -26,10 +26,10 @@ timeout 300 python bench.py --config A --no-cpu-baseline > $OUT/bench_A.log 2>&1
 timeout 900 python bench.py --config E --steps 3 > $OUT/bench_E.log 2>&1
 timeout 600 python bench.py --mode head-parallel --steps 5 > $OUT/bench_E16_hp.log 2>&1
 timeout 600 python bench.py --config C --disk --no-e2e-fp32 --no-cpu-baseline --steps 5 > $OUT/bench_C_disk.log 2>&1
-timeout 900 python bench.py --config D --disk --no-e2e --no-cpu-baseline --steps 3 > $OUT/bench_D_disk.log 2>&1
+timeout 900 python bench.py --config D --disk --no-e2e --no-cpu-baseline --no-fp32-mode --steps 3 --k-sweep 0,16,32,64,2304 > $OUT/bench_D_disk.log 2>&1
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $OUT/bench_ref.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
-  --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
+  --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-serving --no-fp32-mode > $OUT/ncu_bench.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:tc_pgemm|attn_tc|attn_combine|assemble" -s 60 -c 8 \
-  -o $OUT/prof python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_full.log 2>&1
+  -o $OUT/prof python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-serving --no-fp32-mode > $OUT/ncu_full.log 2>&1
 echo done > $OUT/DONE

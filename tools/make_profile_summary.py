@@ -1,6 +1,6 @@
-"""Write profiles/r1_final.md and profiles/traffic.json from a tools/gpu_final.sh run.
+"""Write profiles/r<N>_final.md and profiles/traffic.json from a tools/gpu_final.sh run.
 
-    python tools/make_profile_summary.py gpurun_out/<tag>
+    python tools/make_profile_summary.py gpurun_out/<tag> [round]
 
 Needs ncu on PATH (reads <tag>/prof.ncu-rep) and the bench logs of that run."""
 import json
@@ -11,6 +11,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 run = sys.argv[1]
 tag = os.path.basename(run.rstrip("/"))
+rnd = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+summary = f"r{rnd}_final.md"
 
 
 def line(f):
@@ -46,23 +48,26 @@ for r in rows:
                 name = names[0]
             traffic.setdefault(name, dram)
             seen[key] = i + 1
-traffic["source"] = (f"ncu --set full --clock-control none, one layer of bench.py config C (profiles/r1_final.md, "
+traffic["source"] = (f"ncu --set full --clock-control none, one layer of bench.py config C (profiles/{summary}, "
                      f"gpurun_out/{tag}); dram__bytes_read.sum + dram__bytes_write.sum per launch. attn includes the "
                      f"linked chunk blocks it stores into the request cache (assembly folded into attention).")
 json.dump(traffic, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
 
-out = ["# Round 1 — final state", "",
+INTRO = {
+    1: ["Config C step time: 16.9 ms (first measurement, profiles/r1_baseline.md) -> 10.2 ms (session 2) -> this run."],
+    2: ["Config C step time: 8.86 ms at the start of round 2 (round 1 final: 8.81) -> this run.",
+        "Round 2: attention with 64-key steps and double-buffered S per lane, split mode for single-tile items,",
+        "one MMA-issuing warp per lane with warp-uniform elect.sync issue, TMA bulk-store linking, coalesced",
+        "partials; the pair GEMM's MMA warp made warp-uniform; loader fault semantics of `prepare` on the fast",
+        "paths (v3 per-layer CRCs, compute lane); `mpic_hp_request` with NCCL inside the library; fp32-mode",
+        "and config-D k-sweep bench keys (DESIGN.md)."],
+}
+out = [f"# Round {rnd} — final state", "",
        f"B200, 1 GPU. `tools/gpu_final.sh {tag}` on one fresh box: GPU tests, smoke, the reference's own suites",
        "compiled against our library, bench lines, the reference arm, the ncu launch list of",
        "`bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline` and `ncu --set full` of one layer's kernels.",
-       f"Raw files: gpurun_out/{tag} (scratch). Regenerate: `python tools/make_profile_summary.py gpurun_out/{tag}`.", "",
-       "Config C step time: 16.9 ms (first measurement, profiles/r1_baseline.md) -> 10.2 ms (session 2) -> this run.",
-       "This session: right-aligned attention query tiles, a vectorised QKV RoPE epilogue with pair-multicast",
-       "(cos, sin) staging, a low-register combine, cost-ordered attention items, P handed to the PV MMAs per",
-       "32-key chunk, up-front assembly of the unlinked blocks, the host loader skipping recomputed rows,",
-       "batched varlen requests (config E), a parallel disk reader.", "",
-       "Single E/E16 steps used to stall 0.3-1.2 s with the GPU idle: per-request stream-ordered allocations",
-       "re-mapped memory the pool had released; the workspace keeps the pool's memory now (DESIGN.md §8).", ""]
+       f"Raw files: gpurun_out/{tag} (scratch). Regenerate: `python tools/make_profile_summary.py gpurun_out/{tag} {rnd}`.", ""]
+out += INTRO.get(rnd, []) + [""]
 for f in ["pytest_gpu.log", "smoke.log"]:
     p = os.path.join(run, f)
     if os.path.exists(p):
@@ -75,8 +80,8 @@ for f in sorted(x for x in os.listdir(run) if x.startswith("conf_") and x.endswi
                 "not a parity check; the pytest wrapper warms the GPU and reruns it, and passed)" if fails else ""))
 out.append("")
 for name, f in [("config C (default; headline)", "bench_C.log"),
-                ("config C from .mpic v2 files (--disk)", "bench_C_disk.log"),
-                ("config D: 8 x 2304-token images from .mpic v2 files (--disk)", "bench_D_disk.log"),
+                ("config C from .mpic files (--disk)", "bench_C_disk.log"),
+                ("config D: 8 x 2304-token images from .mpic files (--disk; round 2: --k-sweep)", "bench_D_disk.log"),
                 ("config B", "bench_B.log"), ("config A", "bench_A.log"),
                 ("config E: 256-request serving, batched varlen (--batch 64)", "bench_E.log"),
                 ("config E16: one 16-image request, head-parallel code path at P=1", "bench_E16_hp.log"),
@@ -85,5 +90,5 @@ for name, f in [("config C (default; headline)", "bench_C.log"),
 out += ["## ncu launch list (model synthesis + 7 config-C requests; cold-cache, serialised — compare shares)", "",
         launches, "", "## ncu --set full, one layer of config C", "", full, "",
         "Per-launch DRAM traffic of these kernels is in profiles/traffic.json (bench.py reads the attention entry).", ""]
-open(os.path.join(ROOT, "profiles", "r1_final.md"), "w").write("\n".join(out) + "\n")
-print("wrote profiles/r1_final.md and profiles/traffic.json;", {k: v for k, v in traffic.items() if k != "source"})
+open(os.path.join(ROOT, "profiles", summary), "w").write("\n".join(out) + "\n")
+print(f"wrote profiles/{summary} and profiles/traffic.json;", {k: v for k, v in traffic.items() if k != "source"})
