@@ -1,22 +1,22 @@
-// K3/K5/K6/K7 — projection GEMMs of the selective recompute on the 5th-gen tensor cores.
+// K3/K5/K6/K7 for feature counts that are not a multiple of 256 (the pair GEMM's feature
+// block, tc_pgemm.cu, which takes every N % 256 == 0 shape), plus the shared host helpers
+// (tensor-map cache, tc_gemm_supported, launch_gemm_tc dispatch).
 //
 //   out[t][f] = sum_k X[t][k] * W[f][k]      (y = x . W^T, proj/src/linker.cpp:64-128)
 //
-// Swap-AB mapping for the small-m regime of MPIC (m = text + k*images rows, 96..2000):
-// the UMMA M=128 side is the WEIGHT tile (128 output features), the UMMA N side is the
-// token tile (any multiple of 16 up to 512), so no MMA work is spent on padding rows.
-// One CTA owns 128 features x up to 512 tokens (TMEM: 128 lanes x 512 fp32 columns).
+// Token-major 1-CTA kernels: UMMA M = 128 TOKENS (TMEM lane = token row), N = 64/128/256
+// FEATURES; one wave of (feature tile x token tile) CTAs when that fills the SMs
+// (tc_gemm_tok_kernel), else a persistent stream-K walk over the (tile, k-block) list with
+// deterministic in-order partial fix-up (tc_gemm_sk_kernel). Covered by
+// tests/test_gpu_kernels.py (N = 128, 384, 768, 1024 with K up to 4096).
 //
-//   warp 0     TMA producer: W tile [128 x 64] + X tile [tt x 64] per stage (SWIZZLE_128B)
-//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer (kind::f16, fp32 accum)
+//   warp 0     TMA producer (SWIZZLE_128B boxes)
+//   warp 1     TMEM allocator + tcgen05.mma issuer (kind::f16, fp32 accum)
 //   warps 2-5  epilogue: tcgen05.ld of the accumulator, fused RoPE+scatter into the KV
-//              cache (QKV), GELU (W1), residual add into the fp32 stream (Wo/W2, split-K
-//              via red.global.add) — each thread owns one output feature, lanes of a
-//              warp own 32 consecutive features, so stores are coalesced per token.
-//
-// Full/empty mbarrier ring between TMA and MMA; tcgen05.commit releases smem stages and
-// signals the epilogue. Split-K over blockIdx.z keeps >=120 CTAs busy on 148 SMs when
-// the feature dimension alone is too small (Wo, W2 at h=4096).
+//              cache (QKV), GELU (W1), residual add (Wo/W2); one token row per thread, so
+//              stores are 16-byte vectors and RoPE pairs sit in adjacent registers.
+// (Round 1's swap-AB 1-CTA and 2-CTA variants, superseded by tc_pgemm.cu and reachable only
+// through a diagnostics switch, are retired.)
 #include <cstdlib>
 #include <mutex>
 #include <tuple>
@@ -35,294 +35,10 @@ constexpr uint32_t kWTileBytes = 128 * 64 * 2;  // 16 KB
 constexpr uint32_t kXBoxRows = 128;
 constexpr uint32_t kXBoxBytes = kXBoxRows * 64 * 2;  // 16 KB
 
-struct TcGemmArgs {
-    uint32_t M, N, K;
-    uint32_t tt;            // token columns per CTA (multiple of 16, <= 512)
-    uint32_t xr;            // rows per X TMA box (<= 128, multiple of 8)
-    uint32_t nbox;          // X boxes per stage
-    uint32_t kb_per_split;  // 64-wide K blocks per CTA
-    uint32_t stages;
-    uint32_t tmem_cols;
-    uint32_t dbg;  // diagnostics: 1 skip X loads, 2 skip W loads, 4 skip MMAs
-    EpiParams ep;
-};
-
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<const uint32_t*>(&v);
 }
-
-template <typename TO>
-__device__ __forceinline__ void tc_epilogue(const EpiParams& ep, uint32_t t, uint32_t f, float v) {
-    switch (ep.mode) {
-        case EPI_RESID: {
-            if (ep.split_k > 1) {  // deterministic split-K: partial tile, reduced afterwards
-                ep.partial[((size_t)blockIdx.z * ep.rows_total + t) * ep.ldx + f] = v;
-            } else {
-                float* x = ep.x + (size_t)t * ep.ldx + f;
-                const float nv = *x + v;
-                *x = nv;
-                if (ep.xb) ep.xb[(size_t)t * ep.ldx + f] = __float2bfloat16_rn(nv);
-            }
-            break;
-        }
-        case EPI_GELU:
-            static_cast<TO*>(ep.out)[(size_t)t * ep.ldo + f] = from_f32<TO>(gelu_ref(v));
-            break;
-        case EPI_STORE_F32:
-            static_cast<float*>(ep.out)[(size_t)t * ep.ldo + f] = v;
-            break;
-        default:
-            static_cast<TO*>(ep.out)[(size_t)t * ep.ldo + f] = from_f32<TO>(v);
-    }
-}
-
-// Epilogue over one accumulator tile: thread <-> output feature f (TMEM lane q*32+lane),
-// TMEM columns <-> tokens t0 .. t0+tt-1.
-__device__ __forceinline__ void gemm_epilogue(const EpiParams& ep, uint32_t M, uint32_t t0, uint32_t tt,
-                                              uint32_t f, uint32_t q, uint32_t lane, uint32_t tmem_base) {
-    const bool qkv = ep.mode == EPI_QKV;
-    const uint32_t part = qkv ? f / ep.hidden : 0;  // warp-uniform (hidden % 128 == 0)
-    const uint32_t pair = qkv ? ((f - part * ep.hidden) % ep.head_dim) >> 1 : 0;
-    for (uint32_t c = 0; c < tt; c += 16) {
-        uint32_t r[16];
-        tc::tmem_ld16(tmem_base + ((q * 32u) << 16) + c, r);
-        if (qkv) {
-            // issue every per-token load of this chunk before the first store
-            uint32_t dst_row[16];
-            float2 cs[16];
-#pragma unroll
-            for (uint32_t j = 0; j < 16; ++j) {
-                const uint32_t t = min(t0 + c + j, M - 1);
-                dst_row[j] = part == 0 ? t : __ldg(ep.kv_rows + t);
-                cs[j] = part < 2 ? __ldg(ep.rope + (size_t)__ldg(ep.rope_pos + t) * (ep.head_dim >> 1) + pair)
-                                 : make_float2(1.f, 0.f);
-            }
-            tc::tmem_ld_wait();
-            __nv_bfloat16* base = static_cast<__nv_bfloat16*>(part == 0 ? ep.q : part == 1 ? ep.kv_k : ep.kv_v) +
-                                  (f - part * ep.hidden);
-#pragma unroll
-            for (uint32_t j = 0; j < 16; ++j) {
-                float v = __uint_as_float(r[j]);
-                const float vp = __shfl_xor_sync(0xffffffffu, v, 1);
-                if (part < 2) {
-                    float x0 = (lane & 1) ? vp : v, x1 = (lane & 1) ? v : vp;
-                    rope_pair(x0, x1, cs[j].x, cs[j].y);
-                    v = (lane & 1) ? x1 : x0;
-                }
-                if (t0 + c + j < M) base[(size_t)dst_row[j] * ep.hidden] = __float2bfloat16_rn(v);
-            }
-        } else {
-            tc::tmem_ld_wait();
-#pragma unroll
-            for (uint32_t j = 0; j < 16; ++j) {
-                const uint32_t t = t0 + c + j;
-                if (t < M) tc_epilogue<__nv_bfloat16>(ep, t, f, __uint_as_float(r[j]));
-            }
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kTcThreads, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                   const TcGemmArgs a) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t x_bytes = a.nbox * a.xr * 128;
-    const uint32_t stage_bytes = kWTileBytes + x_bytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
-    uint64_t* empty = full + a.stages;
-    uint64_t* tmem_full = empty + a.stages;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
-
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t n0 = blockIdx.x * 128, t0 = blockIdx.y * a.tt;
-    const uint32_t kb0 = blockIdx.z * a.kb_per_split;
-
-    if (warp == 0 && lane == 0) {
-        tc::tma_prefetch_desc(&tmW);
-        tc::tma_prefetch_desc(&tmX);
-        for (uint32_t s = 0; s < a.stages; ++s) {
-            tc::mbar_init(&full[s], 1);
-            tc::mbar_init(&empty[s], 1);
-        }
-        tc::mbar_init(tmem_full, 1);
-        tc::fence_barrier_init();
-    }
-    if (warp == 1) tc::tmem_alloc(tmem_holder, a.tmem_cols);
-    tc::tc_fence_before();
-    __syncthreads();
-    tc::tc_fence_after();
-    const uint32_t tmem_base = *tmem_holder;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            const uint64_t pol_w = tc::policy_evict_first();  // weights stream through once
-            const uint64_t pol_x = tc::policy_evict_last();   // token tile re-read by every cluster
-            for (uint32_t i = 0; i < a.kb_per_split; ++i) {
-                const uint32_t s = i % a.stages, ph = (i / a.stages) & 1;
-                tc::mbar_wait(&empty[s], ph ^ 1);
-                tc::mbar_arrive_expect_tx(&full[s], ((a.dbg & 2) ? 0 : kWTileBytes) + ((a.dbg & 1) ? 0 : x_bytes));
-                const int k = (int)((kb0 + i) * 64);
-                uint8_t* st = smem + s * stage_bytes;
-                if (!(a.dbg & 2)) tc::tma_load_2d_hint(st, &tmW, &full[s], k, (int)n0, pol_w);
-                if (!(a.dbg & 1))
-                    for (uint32_t b = 0; b < a.nbox; ++b)
-                        tc::tma_load_2d_hint(st + kWTileBytes + b * a.xr * 128, &tmX, &full[s], k,
-                                             (int)(t0 + b * a.xr), pol_x);
-            }
-        }
-        __syncwarp();
-    } else if (warp == 1) {
-        if (lane == 0) {
-            for (uint32_t i = 0; i < a.kb_per_split; ++i) {
-                const uint32_t s = i % a.stages, ph = (i / a.stages) & 1;
-                tc::mbar_wait(&full[s], ph);
-                tc::tc_fence_after();
-                const uint32_t w_base = tc::smem_u32(smem + s * stage_bytes);
-                const uint32_t x_base = w_base + kWTileBytes;
-                if (a.dbg & 4) {
-                    tc::mbar_arrive(&empty[s]);
-                    continue;
-                }
-#pragma unroll
-                for (uint32_t kk = 0; kk < 4; ++kk) {
-                    const uint64_t adesc = tc::desc_k_sw128(w_base + kk * 32);
-                    for (uint32_t c0 = 0; c0 < a.tt; c0 += 256) {
-                        const uint32_t cn = min(256u, a.tt - c0);
-                        const uint64_t bdesc = tc::desc_k_sw128(x_base + c0 * 128 + kk * 32);
-                        tc::mma_bf16(tmem_base + c0, adesc, bdesc, tc::idesc_bf16(128, cn),
-                                     (i > 0 || kk > 0) ? 1u : 0u);
-                    }
-                }
-                tc::mma_commit(&empty[s]);
-            }
-            if (a.dbg & 4) tc::mbar_arrive(tmem_full);
-            else tc::mma_commit(tmem_full);
-        }
-        __syncwarp();
-    } else {
-        // epilogue: warp w may only touch TMEM lanes [32*(w%4), 32*(w%4)+32)
-        const uint32_t q = warp & 3;
-        const uint32_t f = n0 + q * 32 + lane;
-        tc::mbar_wait(tmem_full, 0);
-        tc::tc_fence_after();
-        gemm_epilogue(a.ep, a.M, t0, a.tt, f, q, lane, tmem_base);
-    }
-    tc::tc_fence_before();
-    __syncthreads();
-    tc::tc_fence_after();
-    if (warp == 1) tc::tmem_dealloc(tmem_base, a.tmem_cols);
-}
-
-
-// ---- 2-CTA variant: cta_group::2, UMMA M = 256 features per CTA pair --------------------
-// Each CTA of the pair loads its 128 weight rows and HALF of the token tile; the leader
-// issues tcgen05.mma.cta_group::2 reading both CTAs' shared memory, so every token row is
-// fetched once per 256 features (half the L2->SM traffic of the 1-CTA kernel) and each
-// instruction covers twice the work.
-struct Tc2Args {
-    uint32_t M, N, K;
-    uint32_t tt;           // token columns per pair (multiple of 16, <= 512)
-    uint32_t n_instr;      // token-range instructions per K step (1 or 2)
-    uint32_t in_n[2];      // instruction N (multiple of 16, <= 256)
-    uint32_t in_off[2];    // token offset of each instruction (== its TMEM column)
-    uint32_t x_off[2];     // byte offset of each instruction's half-tile in a stage
-    uint32_t x_bytes;      // token bytes per stage per CTA
-    uint32_t kb_per_split;
-    uint32_t stages;
-    uint32_t tmem_cols;
-    EpiParams ep;
-};
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
-    tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX0,
-                        const __grid_constant__ CUtensorMap tmX1, const Tc2Args a) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t stage_bytes = kWTileBytes + a.x_bytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
-    uint64_t* empty = full + a.stages;
-    uint64_t* tmem_full = empty + a.stages;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
-
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = tc::cluster_ctarank();
-    const uint32_t n0 = blockIdx.x * 128;  // this CTA's 128 features (pair = 256)
-    const uint32_t t0 = blockIdx.y * a.tt;
-    const uint32_t kb0 = blockIdx.z * a.kb_per_split;
-
-    if (warp == 0 && lane == 0) {
-        tc::tma_prefetch_desc(&tmW);
-        tc::tma_prefetch_desc(&tmX0);
-        tc::tma_prefetch_desc(&tmX1);
-        for (uint32_t s = 0; s < a.stages; ++s) {
-            tc::mbar_init(&full[s], 1);
-            tc::mbar_init(&empty[s], 1);
-        }
-        tc::mbar_init(tmem_full, 1);
-        tc::fence_barrier_init();
-    }
-    if (warp == 1) tc::tmem_alloc_pair(tmem_holder, a.tmem_cols);
-    tc::tc_fence_before();
-    tc::cluster_sync();
-    tc::tc_fence_after();
-    const uint32_t tmem_base = *tmem_holder;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            const uint64_t pol_w = tc::policy_evict_first();
-            const uint64_t pol_x = tc::policy_evict_last();
-            for (uint32_t i = 0; i < a.kb_per_split; ++i) {
-                const uint32_t s = i % a.stages, ph = (i / a.stages) & 1;
-                tc::mbar_wait(&empty[s], ph ^ 1);
-                if (rank == 0) tc::mbar_arrive_expect_tx(&full[s], 2 * stage_bytes);
-                const int k = (int)((kb0 + i) * 64);
-                uint8_t* st = smem + s * stage_bytes;
-                tc::tma_load_2d_pair(st, &tmW, &full[s], k, (int)n0, pol_w);
-                tc::tma_load_2d_pair(st + kWTileBytes + a.x_off[0], &tmX0, &full[s], k,
-                                     (int)(t0 + a.in_off[0] + rank * (a.in_n[0] / 2)), pol_x);
-                if (a.n_instr > 1)
-                    tc::tma_load_2d_pair(st + kWTileBytes + a.x_off[1], &tmX1, &full[s], k,
-                                         (int)(t0 + a.in_off[1] + rank * (a.in_n[1] / 2)), pol_x);
-            }
-        }
-        __syncwarp();
-    } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {
-            for (uint32_t i = 0; i < a.kb_per_split; ++i) {
-                const uint32_t s = i % a.stages, ph = (i / a.stages) & 1;
-                tc::mbar_wait(&full[s], ph);
-                tc::tc_fence_after();
-                const uint32_t w_base = tc::smem_u32(smem + s * stage_bytes);
-                const uint32_t x_base = w_base + kWTileBytes;
-#pragma unroll
-                for (uint32_t kk = 0; kk < 4; ++kk) {
-                    const uint64_t adesc = tc::desc_k_sw128(w_base + kk * 32);
-                    for (uint32_t j = 0; j < a.n_instr; ++j) {
-                        const uint64_t bdesc = tc::desc_k_sw128(x_base + a.x_off[j] + kk * 32);
-                        tc::mma_bf16_pair(tmem_base + a.in_off[j], adesc, bdesc, tc::idesc_bf16(256, a.in_n[j]),
-                                          (i > 0 || kk > 0) ? 1u : 0u);
-                    }
-                }
-                tc::mma_commit_pair_mcast(&empty[s], 0x3);
-            }
-            tc::mma_commit_pair_mcast(tmem_full, 0x3);
-        }
-        __syncwarp();
-    } else {
-        const uint32_t q = warp & 3;
-        const uint32_t f = n0 + q * 32 + lane;
-        tc::mbar_wait(tmem_full, 0);
-        tc::tc_fence_after();
-        gemm_epilogue(a.ep, a.M, t0, a.tt, f, q, lane, tmem_base);
-    }
-    tc::tc_fence_before();
-    tc::cluster_sync();
-    tc::tc_fence_after();
-    if (warp == 1) tc::tmem_dealloc_pair(tmem_base, a.tmem_cols);
-}
-
 
 // ---- token-major GEMM (the production path) ---------------------------------------------
 // UMMA M = 128 TOKENS (TMEM lane = token row), N = bn FEATURES (<= 256). Each epilogue
@@ -863,52 +579,6 @@ void launch_tok(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint
 }
 }  // namespace
 
-namespace {
-void launch_pair(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint32_t N, uint32_t K,
-                 uint32_t tt, uint32_t tiles_t, uint32_t split, uint32_t kblocks, const EpiParams& ep_in,
-                 cudaStream_t s) {
-    Tc2Args a{};
-    a.M = M;
-    a.N = N;
-    a.K = K;
-    a.tt = tt;
-    a.n_instr = tt > 256 ? 2 : 1;
-    a.in_n[0] = std::min(tt, 256u);
-    a.in_n[1] = tt > 256 ? tt - 256 : 0;
-    a.in_off[0] = 0;
-    a.in_off[1] = 256;
-    a.x_off[0] = 0;
-    a.x_off[1] = (a.in_n[0] / 2) * 128;
-    a.x_bytes = (a.in_n[0] / 2 + a.in_n[1] / 2) * 128;
-    const uint32_t stage_bytes = kWTileBytes + a.x_bytes;
-    const uint32_t budget = 227 * 1024 - 1024 - 256;
-    a.stages = std::min<uint32_t>(8, budget / stage_bytes);
-    MPIC_REQUIRE(a.stages >= 2, MPIC_ERR_VALIDATION, "tc gemm tile does not fit shared memory");
-    a.tmem_cols = 32;
-    while (a.tmem_cols < tt) a.tmem_cols *= 2;
-    a.kb_per_split = kblocks / split;
-    a.ep = ep_in;
-    a.ep.split_k = split;
-    a.ep.rows_total = M;
-    const CUtensorMap tmW = make_tmap_bf16(W, K, N, 64, 128);
-    const CUtensorMap tmX0 = make_tmap_bf16(A, K, M, 64, a.in_n[0] / 2);
-    const CUtensorMap tmX1 = a.n_instr > 1 ? make_tmap_bf16(A, K, M, 64, a.in_n[1] / 2) : tmX0;
-    const size_t smem = (size_t)a.stages * stage_bytes + 1024 + (2 * a.stages + 1) * 8 + 16;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        MPIC_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    });
-    dim3 grid(N / 128, tiles_t, split);
-    tc_gemm_pair_kernel<<<grid, kTcThreads, smem, s>>>(tmW, tmX0, tmX1, a);
-    MPIC_LAUNCHED();
-    if (split > 1) {
-        const size_t n4 = (size_t)M * N / 4;
-        resid_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(ep_in.partial, split, (size_t)M * N, ep_in.x,
-                                                         ep_in.xb, n4);
-        MPIC_LAUNCHED();
-    }
-}
-}  // namespace
 
 namespace {
 struct SkWorkspace {
@@ -972,88 +642,21 @@ void launch_sk(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint3
 void launch_gemm_tc(const __nv_bfloat16* A, uint32_t lda, const __nv_bfloat16* W, uint32_t M,
                     uint32_t N, uint32_t K, const EpiParams& ep_in, cudaStream_t s, bool w_blocked) {
     MPIC_REQUIRE(tc_gemm_supported(M, N, K) && lda == K, MPIC_ERR_VALIDATION, "unsupported tc gemm shape");
-    static const char* variant = getenv("MPIC_GEMM_VARIANT");  // diagnostics: "tok", "sk", "wswap", "pair"
+    static const char* variant = getenv("MPIC_GEMM_VARIANT");  // diagnostics: "tok", "sk"
     if (w_blocked || (!variant && pgemm_supported(M, N, K))) {
         launch_pgemm(A, W, M, N, K, ep_in, s, w_blocked);
         return;
     }
-    if (!variant || (variant[0] != 'w' && variant[0] != 'p')) {
-        MPIC_REQUIRE(ep_in.mode != EPI_QKV || (ep_in.head_dim % 32 == 0 && ep_in.hidden % 32 == 0),
-                     MPIC_ERR_VALIDATION, "tc gemm QKV epilogue needs head_dim % 32 == 0");
-        const uint32_t bn = N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : 64;
-        const uint32_t tiles = (N / bn) * ceil_div(M, 128);
-        const bool one_wave = tiles <= (uint32_t)kNumSMs && tiles * 8 >= (uint32_t)kNumSMs * 7;
-        if (variant && variant[0] == 't') launch_tok(A, W, M, N, K, ep_in, s);
-        else if (variant && variant[0] == 's') launch_sk(A, W, M, N, K, ep_in, s);
-        else if (one_wave) launch_tok(A, W, M, N, K, ep_in, s);
-        else launch_sk(A, W, M, N, K, ep_in, s);
-        return;
-    }
-    MPIC_REQUIRE(N % 128 == 0, MPIC_ERR_VALIDATION, "swap-AB gemm needs N % 128 == 0");
-    TcGemmArgs a{};
-    a.M = M;
-    a.N = N;
-    a.K = K;
-    a.tt = M <= 512 ? (M + 15) / 16 * 16 : 256;
-    const uint32_t tiles_t = ceil_div(M, a.tt);
-    const uint32_t ntiles = N / 128;
-    const uint32_t kblocks = K / 64;
-    // split-K (residual epilogues only, into a partial buffer) to fill the SMs
-    uint32_t split = 1;
-    if (ep_in.mode == EPI_RESID && ep_in.partial) {
-        double best = 0.0;
-        for (uint32_t sp = 1; sp <= 4; sp *= 2) {
-            if (kblocks % sp || kblocks / sp < 4) break;
-            if ((size_t)sp * M * N > ep_in.partial_cap) break;
-            const uint32_t ctas = ntiles * tiles_t * sp;
-            const double eff = (double)ctas / (kNumSMs * ceil_div(ctas, kNumSMs));
-            const double score = std::min(1.0, (double)ctas / kNumSMs) * eff;
-            if (score > best + 1e-9) {
-                best = score;
-                split = sp;
-            }
-        }
-    }
-    static const uint32_t dbg = [] {
-        const char* e = getenv("MPIC_GEMM_DBG");
-        return e ? (uint32_t)atoi(e) : 0u;
-    }();
-    a.dbg = dbg;
-    if (N % 256 == 0 && variant[0] == 'p' && !dbg) {
-        launch_pair(A, W, M, N, K, a.tt, tiles_t, split, kblocks, ep_in, s);
-        return;
-    }
-    // (Multicast of the token tile across a cluster does not reduce L2 traffic at cluster
-    // sizes <= 4 on this part — B300_MICROARCH.md, TMA-multicast — so the 1-CTA path is
-    // unclustered; the 2-CTA path halves the token traffic instead.)
-    a.xr = a.tt <= 128 ? (a.tt + 7) / 8 * 8 : 128;
-    a.nbox = ceil_div(a.tt, a.xr);
-    const uint32_t stage_bytes = kWTileBytes + a.nbox * a.xr * 128;
-    const uint32_t budget = 227 * 1024 - 1024 - 256;
-    a.stages = std::min<uint32_t>(8, budget / stage_bytes);
-    MPIC_REQUIRE(a.stages >= 2, MPIC_ERR_VALIDATION, "tc gemm tile does not fit shared memory");
-    a.tmem_cols = 32;
-    while (a.tmem_cols < a.tt) a.tmem_cols *= 2;
-    a.kb_per_split = kblocks / split;
-    a.ep = ep_in;
-    a.ep.split_k = split;
-    a.ep.rows_total = M;
-    const CUtensorMap tmW = make_tmap_bf16(W, K, N, 64, 128);
-    // Rows >= M are out of bounds for the map: TMA zero-fills them.
-    const CUtensorMap tmX = make_tmap_bf16(A, K, M, 64, a.xr);
-    const size_t smem = (size_t)a.stages * stage_bytes + 1024 + (2 * a.stages + 1) * 8 + 16;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        MPIC_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    });
-    tc_gemm_kernel<<<dim3(ntiles, tiles_t, split), kTcThreads, smem, s>>>(tmW, tmX, a);
-    MPIC_LAUNCHED();
-    if (split > 1) {
-        const size_t n4 = (size_t)M * N / 4;
-        resid_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(ep_in.partial, split, (size_t)M * N, ep_in.x,
-                                                         ep_in.xb, n4);
-        MPIC_LAUNCHED();
-    }
+    // N % 256 != 0 (the pair GEMM's feature block): the token-major 1-CTA kernels
+    MPIC_REQUIRE(ep_in.mode != EPI_QKV || (ep_in.head_dim % 32 == 0 && ep_in.hidden % 32 == 0),
+                 MPIC_ERR_VALIDATION, "tc gemm QKV epilogue needs head_dim % 32 == 0");
+    const uint32_t bn = N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : 64;
+    const uint32_t tiles = (N / bn) * ceil_div(M, 128);
+    const bool one_wave = tiles <= (uint32_t)kNumSMs && tiles * 8 >= (uint32_t)kNumSMs * 7;
+    if (variant && variant[0] == 't') launch_tok(A, W, M, N, K, ep_in, s);
+    else if (variant && variant[0] == 's') launch_sk(A, W, M, N, K, ep_in, s);
+    else if (one_wave) launch_tok(A, W, M, N, K, ep_in, s);
+    else launch_sk(A, W, M, N, K, ep_in, s);
 }
 
 }  // namespace mpicb
