@@ -2960,7 +2960,7 @@ int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const
         MPIC_CUDA(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
         MPIC_CUDA(cudaMemset(dbg, 0, h.size() * 8));
         {  // per-CTA spans (start, end, smid, first MMA, last burst, epilogue start/end), relative to the earliest start
-            const size_t base = 16 * 64, ncta = std::min<size_t>(plan.units.size(), (h.size() - base) / 8);
+            const size_t base = 16 * 64, ncta = std::min<size_t>(std::min<size_t>(plan.units.size(), kNumSMs), (h.size() - base) / 8);
             unsigned long long t_min = ~0ull;
             for (size_t c = 0; c < ncta; ++c) t_min = std::min(t_min, h[base + 8 * c]);
             auto rel = [&](size_t c, int k) { return h[base + 8 * c + k] ? (h[base + 8 * c + k] - t_min) / 1e3 : -1.0; };

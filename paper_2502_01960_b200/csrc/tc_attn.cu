@@ -58,6 +58,7 @@ constexpr uint32_t kDbgCtaBase = 16 * 64, kDbgCtas = (16 * 4096 - kDbgCtaBase) /
 
 struct AttnParams {
     const AttnUnit* units;
+    uint32_t n_units;
     const uint32_t* rows;
     const uint32_t* starts;  // batched requests: first key row each query row may see (null: 0)
     uint32_t m;
@@ -175,15 +176,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     uint8_t* sV = sK + kKStages * kTile;         // [kVStages]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVStages * kTile);
     uint64_t* q_full = bars;
-    uint64_t* k_full = q_full + 1;               // [kKStages]
+    uint64_t* q_empty = q_full + 1;              // both MMA warps issued their item's last S
+    uint64_t* k_full = q_empty + 1;              // [kKStages]
     uint64_t* k_empty = k_full + kKStages;
     uint64_t* v_full = k_empty + kKStages;       // [kVStages]
     uint64_t* v_empty = v_full + kVStages;
     uint64_t* s_full = v_empty + kVStages;       // [2 lanes][2 buffers]
     uint64_t* p_full = s_full + 4;               // [2 lanes][2 buffers]
     uint64_t* o_done = p_full + 4;               // [2 lanes] one phase per PV
-    uint64_t* o_fin = o_done + 2;                // [2 lanes] the lane's last PV
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_fin + 2);
+    uint64_t* o_fin = o_done + 2;                // [2 lanes] the item's last PV
+    uint64_t* o_free = o_fin + 2;                // [2 lanes] O read out by the epilogue
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_free + 2);
     float2* ml_x = reinterpret_cast<float2*>(tmem_holder + 4);  // [128] split mode: lane 1's (m, l)
 
     tc::pdl_trigger();
@@ -194,6 +197,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tc::tma_prefetch_desc(&tmK);
         tc::tma_prefetch_desc(&tmV);
         tc::mbar_init(q_full, 1);
+        tc::mbar_init(q_empty, 2);
         // a K/V stage is free once both MMA warps' reads of it are done and, with linking,
         // the linker has finished storing it (or passed it)
         const uint32_t empties = p.link ? 3u : 2u;  // both MMA warps (+ the linker)
@@ -212,6 +216,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&o_done[i], 1);
             tc::mbar_init(&o_fin[i], 1);
+            tc::mbar_init(&o_free[i], 128);
         }
         tc::fence_barrier_init();
     }
@@ -221,23 +226,42 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tc::tc_fence_after();
     tc::pdl_wait();  // q and the layer's K/V come from the previous kernel
     const uint32_t tmem = *tmem_holder;
-    const AttnUnit u = p.units[blockIdx.x];
     if (p.dbg && threadIdx.x == 0 && blockIdx.x < kDbgCtas) {  // diagnostics: per-CTA span and SM
         uint32_t smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         p.dbg[kDbgCtaBase + 8 * blockIdx.x] = globaltimer_ns();
         p.dbg[kDbgCtaBase + 8 * blockIdx.x + 2] = smid;
     }
+    // Persistent CTA: items idx(0), idx(1), ... of the cost-sorted list, dealt round-robin in
+    // snake order (round r: CTA c takes r*G + c, or r*G + G-1-c on odd rounds). Every role
+    // walks the same item sequence with running block / step / item counters, so barrier
+    // phases continue across items and the next item's Q/K/V loads and first S MMAs overlap
+    // the current item's tail and epilogue.
+    const uint32_t G = gridDim.x;
+    auto item_at = [&](uint32_t r) { return r * G + ((r & 1) ? G - 1 - blockIdx.x : blockIdx.x); };
     // Two lanes (X = 0, 1), each with its own softmax warpgroup, O accumulator and two S
     // buffers, walk 64-key steps. Pair mode (two query tiles): lane X = tile X over every
     // half-block of its range, step s = half s & 1 of block s >> 1. Split mode (one tile):
     // both lanes take the tile, lane X the key half X of every block, step s = block s;
     // their (m, l, O) are merged at the end.
-    const bool split = u.tile[1] == kNoTile;
-    const uint32_t nb0 = u.b1[0] - u.b0, nb1 = split ? nb0 : u.b1[1] - u.b0;
-    const uint32_t nblk = max(nb0, nb1);
-    const uint32_t nst[2] = {split ? nb0 : 2 * nb0, split ? nb0 : 2 * nb1};
-    const int hcol = (int)(u.head * 128u);
+    struct Item {
+        AttnUnit u;
+        bool split;
+        uint32_t nb0, nb1, nblk, nst[2];
+        int hcol;
+    };
+    auto item = [&](uint32_t idx) {
+        Item it;
+        it.u = p.units[idx];
+        it.split = it.u.tile[1] == kNoTile;
+        it.nb0 = it.u.b1[0] - it.u.b0;
+        it.nb1 = it.split ? it.nb0 : it.u.b1[1] - it.u.b0;
+        it.nblk = max(it.nb0, it.nb1);
+        it.nst[0] = it.split ? it.nb0 : 2 * it.nb0;
+        it.nst[1] = it.split ? it.nb0 : 2 * it.nb1;
+        it.hcol = (int)(it.u.head * 128u);
+        return it;
+    };
     // TMEM columns: lane X uses S_X[b] = [256X + 64b, +64) and O_X = [256X + 128, +128).
     // P_X (bf16, two keys per column) overwrites the first 32 columns of its S buffer.
     constexpr uint32_t idesc_s = tc::idesc_bf16(128, 64, false);
@@ -249,33 +273,39 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // dominates it (set before a join, the softmax got the control warps' limit and spilled)
     if (warp < 4) tc::reg_dealloc<kCtrlRegs>();
     if (warp == 0) {
-        // lane 0: the Q tile(s), then K_j and V_j of every block in order (K into a 2-stage,
-        // V into a 3-stage ring: V_j's slot frees long before K_{j+2} is needed)
+        // lane 0: per item the Q tile(s) (once both MMA warps issued the previous item's
+        // last S), then K_j and V_j of every block in order (K into a 2-stage, V into a
+        // 3-stage ring: V_j's slot frees long before K_{j+2} is needed)
         if (lane == 0) {
-            tc::mbar_arrive_expect_tx(q_full, (split ? 1 : 2) * kTile);
-#pragma unroll
-            for (uint32_t x = 0; x < 2; ++x) {
-                if (x == 1 && split) break;
-                // tile 0 may start at a negative row: TMA zero-fills the rows outside [0, m)
-                const int q0 = (int)(u.tile[x] * 128u) - (int)p.shift;
-                tc::tma_load_2d(sQ + x * kTile, &tmQ, q_full, hcol, q0);
-                tc::tma_load_2d(sQ + x * kTile + kHalf, &tmQ, q_full, hcol + 64, q0);
-            }
             if (p.link)
                 for (uint32_t c = 0; c < 2 * kMaxLinkChunks; ++c) tc::tensormap_acquire(&p.link->maps[c]);
-            for (uint32_t j = 0; j < nblk; ++j) {
-                int j0;
-                const uint32_t sk = j % kKStages, sv = j % kVStages;
-                const CUtensorMap* srck = link_src(p, &tmK, u.b0 + j, 0, j0);
-                WD_WAIT(&k_empty[sk], ((j / kKStages) & 1) ^ 1, 1, j);
-                tc::mbar_arrive_expect_tx(&k_full[sk], kTile);
-                tc::tma_load_2d(sK + sk * kTile, srck, &k_full[sk], hcol, j0);
-                tc::tma_load_2d(sK + sk * kTile + kHalf, srck, &k_full[sk], hcol + 64, j0);
-                const CUtensorMap* srcv = link_src(p, &tmV, u.b0 + j, 1, j0);
-                WD_WAIT(&v_empty[sv], ((j / kVStages) & 1) ^ 1, 2, j);
-                tc::mbar_arrive_expect_tx(&v_full[sv], kTile);
-                tc::tma_load_2d(sV + sv * kTile, srcv, &v_full[sv], hcol, j0);
-                tc::tma_load_2d(sV + sv * kTile + kHalf, srcv, &v_full[sv], hcol + 64, j0);
+            uint32_t gb = 0;  // blocks loaded so far (all items)
+            for (uint32_t ni = 0, idx; (idx = item_at(ni)) < p.n_units; ++ni) {
+                const Item it = item(idx);
+                if (ni > 0) WD_WAIT(q_empty, (ni - 1) & 1, 13, ni);
+                tc::mbar_arrive_expect_tx(q_full, (it.split ? 1 : 2) * kTile);
+#pragma unroll
+                for (uint32_t x = 0; x < 2; ++x) {
+                    if (x == 1 && it.split) break;
+                    // tile 0 may start at a negative row: TMA zero-fills the rows outside [0, m)
+                    const int q0 = (int)(it.u.tile[x] * 128u) - (int)p.shift;
+                    tc::tma_load_2d(sQ + x * kTile, &tmQ, q_full, it.hcol, q0);
+                    tc::tma_load_2d(sQ + x * kTile + kHalf, &tmQ, q_full, it.hcol + 64, q0);
+                }
+                for (uint32_t j = 0; j < it.nblk; ++j, ++gb) {
+                    int j0;
+                    const uint32_t sk = gb % kKStages, sv = gb % kVStages;
+                    const CUtensorMap* srck = link_src(p, &tmK, it.u.b0 + j, 0, j0);
+                    WD_WAIT(&k_empty[sk], ((gb / kKStages) & 1) ^ 1, 1, gb);
+                    tc::mbar_arrive_expect_tx(&k_full[sk], kTile);
+                    tc::tma_load_2d(sK + sk * kTile, srck, &k_full[sk], it.hcol, j0);
+                    tc::tma_load_2d(sK + sk * kTile + kHalf, srck, &k_full[sk], it.hcol + 64, j0);
+                    const CUtensorMap* srcv = link_src(p, &tmV, it.u.b0 + j, 1, j0);
+                    WD_WAIT(&v_empty[sv], ((gb / kVStages) & 1) ^ 1, 2, gb);
+                    tc::mbar_arrive_expect_tx(&v_full[sv], kTile);
+                    tc::tma_load_2d(sV + sv * kTile, srcv, &v_full[sv], it.hcol, j0);
+                    tc::tma_load_2d(sV + sv * kTile + kHalf, srcv, &v_full[sv], it.hcol + 64, j0);
+                }
             }
         }
         __syncwarp();
@@ -289,137 +319,152 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         // after the PV that reads it), so the softmax finds S_x(s + 1) computed while it
         // works on step s. A K/V stage needs one release (commit) from each MMA warp.
         const uint32_t x = warp - 1;
-        const uint32_t ns = nst[x];
-        const bool stamp = lane == 0 && p.dbg && blockIdx.x == 0 && x == 0;
-        auto blk_of = [&](uint32_t s) { return split ? s : s >> 1; };
-        auto half_of = [&](uint32_t s) { return split ? x : s & 1u; };
-        uint32_t k_avail = 0, v_avail = 0, k_rel = 0, v_rel = 0;
-        auto need_k = [&](uint32_t j) {
-            for (; k_avail <= j; ++k_avail)
-                if (lane == 0) WD_WAIT(&k_full[k_avail % kKStages], (k_avail / kKStages) & 1, 3, k_avail);
-        };
-        auto need_v = [&](uint32_t j) {
-            for (; v_avail <= j; ++v_avail)
-                if (lane == 0) WD_WAIT(&v_full[v_avail % kVStages], (v_avail / kVStages) & 1, 4, v_avail);
-        };
-        const uint32_t qa = tc::smem_u32(sQ + (split ? 0u : x) * kTile);
-        auto issue_s = [&](uint32_t s) {
-            const uint32_t j = blk_of(s);
-            const uint32_t ka = tc::smem_u32(sK + (j % kKStages) * kTile) + half_of(s) * 8192u;  // keys [64h, +64)
-            if (tc::elect_one_sync()) {
+        // running counters over the CTA's items: blocks (K/V stage and phase), steps of this
+        // lane (S/P buffer and phase; one PV per step: o_done phase)
+        uint32_t gb0 = 0, sg0 = 0;
+        uint32_t k_avail = 0, v_avail = 0, k_rel = 0, v_rel = 0;  // global block indices
+        for (uint32_t ni = 0, idx; (idx = item_at(ni)) < p.n_units; ++ni) {
+            const Item it = item(idx);
+            const uint32_t ns = it.nst[x], nblk = it.nblk;
+            const bool split = it.split;
+            const bool stamp = lane == 0 && p.dbg && blockIdx.x == 0 && x == 0 && ni == 0;
+            auto blk_of = [&](uint32_t s) { return split ? s : s >> 1; };
+            auto half_of = [&](uint32_t s) { return split ? x : s & 1u; };
+            auto need_k = [&](uint32_t j) {  // local block j has landed
+                for (; k_avail <= gb0 + j; ++k_avail)
+                    if (lane == 0) WD_WAIT(&k_full[k_avail % kKStages], (k_avail / kKStages) & 1, 3, k_avail);
+            };
+            auto need_v = [&](uint32_t j) {
+                for (; v_avail <= gb0 + j; ++v_avail)
+                    if (lane == 0) WD_WAIT(&v_full[v_avail % kVStages], (v_avail / kVStages) & 1, 4, v_avail);
+            };
+            const uint32_t qa = tc::smem_u32(sQ + (split ? 0u : x) * kTile);
+            auto issue_s = [&](uint32_t s) {
+                const uint32_t jg = gb0 + blk_of(s), sg = sg0 + s;
+                const uint32_t ka = tc::smem_u32(sK + (jg % kKStages) * kTile) + half_of(s) * 8192u;  // keys [64h, +64)
+                if (tc::elect_one_sync()) {
 #pragma unroll
-                for (uint32_t kk = 0; kk < 8; ++kk) {
-                    const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-                    tc::mma_bf16(tmem + x * 256 + (s & 1) * 64, tc::desc_k_sw128(qa + off), tc::desc_k_sw128(ka + off),
-                                 idesc_s, kk > 0 ? 1u : 0u);
+                    for (uint32_t kk = 0; kk < 8; ++kk) {
+                        const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+                        tc::mma_bf16(tmem + x * 256 + (sg & 1) * 64, tc::desc_k_sw128(qa + off),
+                                     tc::desc_k_sw128(ka + off), idesc_s, kk > 0 ? 1u : 0u);
+                    }
+                    tc::mma_commit(&s_full[2 * x + (sg & 1)]);
+                    if (s + 1 == ns) tc::mma_commit(q_empty);  // the item's Q is no longer read
                 }
-                tc::mma_commit(&s_full[2 * x + (s & 1)]);
-            }
-        };
-        auto issue_pv = [&](uint32_t s) {
-            const uint32_t j = blk_of(s);
-            const uint32_t va = tc::smem_u32(sV + (j % kVStages) * kTile) + half_of(s) * 8192u;
-            if (tc::elect_one_sync()) {
+            };
+            auto issue_pv = [&](uint32_t s) {
+                const uint32_t jg = gb0 + blk_of(s), sg = sg0 + s;
+                const uint32_t va = tc::smem_u32(sV + (jg % kVStages) * kTile) + half_of(s) * 8192u;
+                if (tc::elect_one_sync()) {
 #pragma unroll
-                for (uint32_t kk = 0; kk < 4; ++kk)  // A = P_x(s) from TMEM: 16 keys = 8 packed columns
-                    tc::mma_bf16_ts(tmem + x * 256 + 128, tmem + x * 256 + (s & 1) * 64 + kk * 8,
-                                    tc::desc_mn_sw128(va + kk * 2048, kHalf), idesc_o, (s > 0 || kk > 0) ? 1u : 0u);
-                tc::mma_commit(&o_done[x]);
-                if (s + 1 == ns) tc::mma_commit(&o_fin[x]);
-            }
-        };
-        // release every block below the lowest block a later MMA of this lane still reads.
-        // A block this lane never reads (pair mode, the other tile's longer range) is released
-        // only once it has landed: an early arrival would count towards the stage's previous
-        // phase and free it under the other lane's MMAs.
-        auto release = [&](uint32_t next_s, uint32_t next_pv) {
-            const uint32_t lk = next_s < ns ? blk_of(next_s) : nblk;
-            const uint32_t lv = next_pv < ns ? blk_of(next_pv) : nblk;
-            const uint32_t used = min(blk_of(ns - 1) + 1, nblk);  // blocks this lane reads: [0, used)
-            // blocks this lane read: released as soon as no later MMA of the lane reads them
-            if (tc::elect_one_sync()) {
-                for (uint32_t j = k_rel; j < min(lk, used); ++j) tc::mma_commit(&k_empty[j % kKStages]);
-                for (uint32_t j = v_rel; j < min(lv, used); ++j) tc::mma_commit(&v_empty[j % kVStages]);
-            }
-            k_rel = max(k_rel, min(lk, used));
-            v_rel = max(v_rel, min(lv, used));
-            // blocks it never reads (pair mode, the other tile's longer range): released after
-            // the lane's last MMA, in the producer's load order (K_j, V_j, K_j+1, ...), each
-            // once it has landed (never while this lane still has PVs to issue: the other lane
-            // could be waiting for a V stage only this lane's release frees)
-            if (next_pv < ns) return;
-            while (k_rel < lk || v_rel < lv) {
-                const bool do_k = k_rel < lk && (v_rel >= lv || k_rel <= v_rel);
-                if (do_k) {
-                    need_k(k_rel);
-                    __syncwarp();
-                    if (tc::elect_one_sync()) tc::mma_commit(&k_empty[k_rel % kKStages]);
-                    ++k_rel;
-                } else {
-                    need_v(v_rel);
-                    __syncwarp();
-                    if (tc::elect_one_sync()) tc::mma_commit(&v_empty[v_rel % kVStages]);
-                    ++v_rel;
+                    for (uint32_t kk = 0; kk < 4; ++kk)  // A = P_x(s) from TMEM: 16 keys = 8 packed columns
+                        tc::mma_bf16_ts(tmem + x * 256 + 128, tmem + x * 256 + (sg & 1) * 64 + kk * 8,
+                                        tc::desc_mn_sw128(va + kk * 2048, kHalf), idesc_o, (s > 0 || kk > 0) ? 1u : 0u);
+                    tc::mma_commit(&o_done[x]);
+                    if (s + 1 == ns) tc::mma_commit(&o_fin[x]);
                 }
-            }
-        };
-        if (lane == 0) WD_WAIT(q_full, 0, 5, 0);
-        need_k(blk_of(min(2u, ns) - 1));
-        __syncwarp();
-        tc::tc_fence_after();
-        issue_s(0);
-        if (ns > 1) issue_s(1);
-        release(2, 0);
-        const bool cta_stamp = lane == 0 && x == 0 && p.dbg && blockIdx.x < kDbgCtas;
-        if (cta_stamp) p.dbg[kDbgCtaBase + 8 * blockIdx.x + 3] = globaltimer_ns();
-        for (uint32_t s = 0; s < ns; ++s) {
-            if (stamp && s < 64) {
-                p.dbg[s * 16 + 0] = globaltimer_ns();
-                p.dbg[s * 16 + 14] = clock64();
-            }
-            if (lane == 0) WD_WAIT(&p_full[2 * x + (s & 1)], (s >> 1) & 1, 6, s);
-            need_v(blk_of(s));
-            if (s + 2 < ns) need_k(blk_of(s + 2));
+            };
+            // release every block below the lowest block a later MMA of this lane still reads.
+            // A block this lane never reads (pair mode, the other tile's longer range) is
+            // released only once it has landed: an early arrival would count towards the
+            // stage's previous phase and free it under the other lane's MMAs.
+            auto release = [&](uint32_t next_s, uint32_t next_pv) {
+                const uint32_t lk = gb0 + (next_s < ns ? blk_of(next_s) : nblk);
+                const uint32_t lv = gb0 + (next_pv < ns ? blk_of(next_pv) : nblk);
+                const uint32_t used = gb0 + min(blk_of(ns - 1) + 1, nblk);  // blocks this lane reads
+                if (tc::elect_one_sync()) {
+                    for (uint32_t j = k_rel; j < min(lk, used); ++j) tc::mma_commit(&k_empty[j % kKStages]);
+                    for (uint32_t j = v_rel; j < min(lv, used); ++j) tc::mma_commit(&v_empty[j % kVStages]);
+                }
+                k_rel = max(k_rel, min(lk, used));
+                v_rel = max(v_rel, min(lv, used));
+                // blocks it never reads: released after the lane's last MMA, in the producer's
+                // load order (K_j, V_j, K_j+1, ...), each once it has landed (never while this
+                // lane still has PVs to issue: the other lane could be waiting for a V stage
+                // only this lane's release frees)
+                if (next_pv < ns) return;
+                while (k_rel < lk || v_rel < lv) {
+                    const bool do_k = k_rel < lk && (v_rel >= lv || k_rel <= v_rel);
+                    if (do_k) {
+                        need_k(k_rel - gb0);
+                        __syncwarp();
+                        if (tc::elect_one_sync()) tc::mma_commit(&k_empty[k_rel % kKStages]);
+                        ++k_rel;
+                    } else {
+                        need_v(v_rel - gb0);
+                        __syncwarp();
+                        if (tc::elect_one_sync()) tc::mma_commit(&v_empty[v_rel % kVStages]);
+                        ++v_rel;
+                    }
+                }
+            };
+            if (lane == 0) WD_WAIT(q_full, ni & 1, 5, ni);
+            need_k(blk_of(min(2u, ns) - 1));
             __syncwarp();
             tc::tc_fence_after();
-            if (stamp && s < 64) p.dbg[s * 16 + 1] = globaltimer_ns();
-            issue_pv(s);
-            if (s + 2 < ns) issue_s(s + 2);
-            release(s + 3, s + 1);
-            if (stamp && s < 64) p.dbg[s * 16 + 2] = globaltimer_ns();
+            issue_s(0);
+            if (ns > 1) issue_s(1);
+            release(2, 0);
+            for (uint32_t s = 0; s < ns; ++s) {
+                if (stamp && s < 64) {
+                    p.dbg[s * 16 + 0] = globaltimer_ns();
+                    p.dbg[s * 16 + 14] = clock64();
+                }
+                const uint32_t sg = sg0 + s;
+                if (lane == 0) {
+                    WD_WAIT(&p_full[2 * x + (sg & 1)], (sg >> 1) & 1, 6, sg);
+                    // the first PV overwrites O: the previous item's epilogue must have read it
+                    if (s == 0 && ni > 0) WD_WAIT(&o_free[x], (ni - 1) & 1, 14, ni);
+                }
+                need_v(blk_of(s));
+                if (s + 2 < ns) need_k(blk_of(s + 2));
+                __syncwarp();
+                tc::tc_fence_after();
+                if (stamp && s < 64) p.dbg[s * 16 + 1] = globaltimer_ns();
+                issue_pv(s);
+                if (s + 2 < ns) issue_s(s + 2);
+                release(s + 3, s + 1);
+                if (stamp && s < 64) p.dbg[s * 16 + 2] = globaltimer_ns();
+            }
+            gb0 += nblk;
+            sg0 += ns;
         }
-        if (cta_stamp) p.dbg[kDbgCtaBase + 8 * blockIdx.x + 4] = globaltimer_ns();
         __syncwarp();
     } else if (warp == 3) {
         if (p.link && lane == 0) {
-            // ---- linker (warp 3, one thread): TMA-stores the chunk-sourced K/V blocks this
-            // item is the writer of from the stage buffers into the request cache (the cache
+            // ---- linker (warp 3, one thread): TMA-stores the chunk-sourced K/V blocks its
+            // items are the writer of from the stage buffers into the request cache (the cache
             // tensor maps have the stage's 128-B swizzle, so a block is two bulk stores and no
             // thread touches the data), then releases the stage once the stores have read it.
             // Writer of block b = the item streaming b for the lowest query tile reaching b.
             const uint32_t* blk = reinterpret_cast<const uint32_t*>(p.link + 1);
             const uint16_t* wtile = reinterpret_cast<const uint16_t*>(blk + p.link->nblk);
-            for (uint32_t j = 0; j < nblk; ++j) {
-                const uint32_t b = u.b0 + j, wt = wtile[b];
-                const bool mine = (u.tile[0] == wt && j < nb0) || (!split && u.tile[1] == wt && j < nb1);
-                const bool store = mine && blk[b] != kLinkedBlock && !p.link_nostore;
-                const uint32_t sk = j % kKStages, sv = j % kVStages;
-                WD_WAIT(&k_full[sk], (j / kKStages) & 1, 7, 0);
-                if (store) {
-                    tc::tma_store_2d(&tmK, sK + sk * kTile, hcol, (int)(b * 128u));
-                    tc::tma_store_2d(&tmK, sK + sk * kTile + kHalf, hcol + 64, (int)(b * 128u));
-                    tc::bulk_commit_group();
-                    tc::bulk_wait_group_read<0>();
+            uint32_t gb = 0;
+            for (uint32_t ni = 0, idx; (idx = item_at(ni)) < p.n_units; ++ni) {
+                const Item it = item(idx);
+                for (uint32_t j = 0; j < it.nblk; ++j, ++gb) {
+                    const uint32_t b = it.u.b0 + j, wt = wtile[b];
+                    const bool mine = (it.u.tile[0] == wt && j < it.nb0) || (!it.split && it.u.tile[1] == wt && j < it.nb1);
+                    const bool store = mine && blk[b] != kLinkedBlock && !p.link_nostore;
+                    const uint32_t sk = gb % kKStages, sv = gb % kVStages;
+                    WD_WAIT(&k_full[sk], (gb / kKStages) & 1, 7, gb);
+                    if (store) {
+                        tc::tma_store_2d(&tmK, sK + sk * kTile, it.hcol, (int)(b * 128u));
+                        tc::tma_store_2d(&tmK, sK + sk * kTile + kHalf, it.hcol + 64, (int)(b * 128u));
+                        tc::bulk_commit_group();
+                        tc::bulk_wait_group_read<0>();
+                    }
+                    tc::mbar_arrive(&k_empty[sk]);
+                    WD_WAIT(&v_full[sv], (gb / kVStages) & 1, 8, gb);
+                    if (store) {
+                        tc::tma_store_2d(&tmV, sV + sv * kTile, it.hcol, (int)(b * 128u));
+                        tc::tma_store_2d(&tmV, sV + sv * kTile + kHalf, it.hcol + 64, (int)(b * 128u));
+                        tc::bulk_commit_group();
+                        tc::bulk_wait_group_read<0>();
+                    }
+                    tc::mbar_arrive(&v_empty[sv]);
                 }
-                tc::mbar_arrive(&k_empty[sk]);
-                WD_WAIT(&v_full[sv], (j / kVStages) & 1, 8, 0);
-                if (store) {
-                    tc::tma_store_2d(&tmV, sV + sv * kTile, hcol, (int)(b * 128u));
-                    tc::tma_store_2d(&tmV, sV + sv * kTile + kHalf, hcol + 64, (int)(b * 128u));
-                    tc::bulk_commit_group();
-                    tc::bulk_wait_group_read<0>();
-                }
-                tc::mbar_arrive(&v_empty[sv]);
             }
             tc::bulk_wait_group<0>();  // the stores are complete before the CTA exits
         }
@@ -428,168 +473,174 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tc::reg_alloc<kSoftmaxRegs>();
         // ---- softmax: lane x = warp / 4 - 1, one thread per query row (TMEM lane)
         const uint32_t x = (warp >> 2) - 1;
-        const uint32_t ns_x = nst[x];
-        const uint32_t tile_x = split ? u.tile[0] : u.tile[x];
-        const uint32_t slot_x = split ? u.slot[0] : u.slot[x];
         const uint32_t quarter = warp & 3;
         const uint32_t r = quarter * 32 + lane;
-        const uint32_t qi = tile_x * 128u + r - p.shift;  // wraps (invalid) for r < shift in tile 0
-        const bool valid = tile_x * 128u + r >= p.shift && qi < p.m;
-        const uint32_t limit = valid ? p.rows[qi] : 0u;
-        const uint32_t first = valid && p.starts ? p.starts[qi] : 0u;  // its request's first cache row
         const uint32_t lane_base = (quarter * 32u) << 16;
         const uint32_t o_col = tmem + lane_base + x * 256 + 128;
-        float m_used = -INFINITY, l = 0.0f;
-        for (uint32_t s = 0; s < ns_x; ++s) {
-            const uint32_t k0 = (u.b0 + (split ? s : s >> 1)) * 128u + 64u * (split ? x : s & 1u);
-            const uint32_t s_col = tmem + lane_base + x * 256 + (s & 1) * 64;
-            if (lane == 0) WD_WAIT(&s_full[2 * x + (s & 1)], (s >> 1) & 1, 9, s);  // one poller per warp
-            __syncwarp();
-            const bool dbg_me = p.dbg && blockIdx.x == 0 && x == 0 && r == 0 && s < 64;
-            if (dbg_me) p.dbg[s * 16 + 5] = globaltimer_ns();
-            if (p.dbg && blockIdx.x == 0 && x == 1 && r == 0 && s < 64) p.dbg[s * 16 + 10] = globaltimer_ns();
-            tc::tc_fence_after();
-            // keys [ns, nv) of the 64-key step are visible to this row: the causal limit is
-            // the row's position (an invalid row sees none), and batched requests also mask
-            // the rows of other requests' caches below `first`. Selected rows are scattered
-            // over the prompt, so a warp often sees few or none of a step's keys: 32-key
-            // chunks no lane of the warp sees are neither loaded nor exponentiated (P = 0),
-            // and a warp that sees nothing just writes P = 0.
-            const uint32_t ns = first > k0 ? min(first - k0, 64u) : 0u;
-            uint32_t nv = !valid || limit < k0 ? 0u : min(limit - k0 + 1u, 64u);
-            if (ns >= nv) nv = 0u;
-            const uint32_t nv_max = __reduce_max_sync(0xffffffffu, nv);
-            const uint32_t nv_min = __reduce_min_sync(0xffffffffu, nv);
-            if (nv_max == 0) {
-                uint32_t z[16];
+        uint32_t sg0 = 0;
+        for (uint32_t ni = 0, idx; (idx = item_at(ni)) < p.n_units; ++ni) {
+            const Item it = item(idx);
+            const bool split = it.split;
+            const uint32_t ns_x = it.nst[x];
+            const uint32_t tile_x = split ? it.u.tile[0] : it.u.tile[x];
+            const uint32_t slot_x = split ? it.u.slot[0] : it.u.slot[x];
+            const uint32_t qi = tile_x * 128u + r - p.shift;  // wraps (invalid) for r < shift in tile 0
+            const bool valid = tile_x * 128u + r >= p.shift && qi < p.m;
+            const uint32_t limit = valid ? p.rows[qi] : 0u;
+            const uint32_t first = valid && p.starts ? p.starts[qi] : 0u;  // its request's first cache row
+            float m_used = -INFINITY, l = 0.0f;
+            for (uint32_t s = 0; s < ns_x; ++s) {
+                const uint32_t sg = sg0 + s;
+                const uint32_t k0 = (it.u.b0 + (split ? s : s >> 1)) * 128u + 64u * (split ? x : s & 1u);
+                const uint32_t s_col = tmem + lane_base + x * 256 + (sg & 1) * 64;
+                if (lane == 0) WD_WAIT(&s_full[2 * x + (sg & 1)], (sg >> 1) & 1, 9, sg);  // one poller per warp
+                __syncwarp();
+                const bool dbg_me = p.dbg && blockIdx.x == 0 && ni == 0 && x == 0 && r == 0 && s < 64;
+                if (dbg_me) p.dbg[s * 16 + 5] = globaltimer_ns();
+                if (p.dbg && blockIdx.x == 0 && ni == 0 && x == 1 && r == 0 && s < 64) p.dbg[s * 16 + 10] = globaltimer_ns();
+                tc::tc_fence_after();
+                // keys [ns, nv) of the 64-key step are visible to this row: the causal limit is
+                // the row's position (an invalid row sees none), and batched requests also mask
+                // the rows of other requests' caches below `first`. Selected rows are scattered
+                // over the prompt, so a warp often sees few or none of a step's keys: 32-key
+                // chunks no lane of the warp sees are neither loaded nor exponentiated (P = 0),
+                // and a warp that sees nothing just writes P = 0.
+                const uint32_t ns = first > k0 ? min(first - k0, 64u) : 0u;
+                uint32_t nv = !valid || limit < k0 ? 0u : min(limit - k0 + 1u, 64u);
+                if (ns >= nv) nv = 0u;
+                const uint32_t nv_max = __reduce_max_sync(0xffffffffu, nv);
+                const uint32_t nv_min = __reduce_min_sync(0xffffffffu, nv);
+                if (nv_max == 0) {
+                    uint32_t z[16];
 #pragma unroll
-                for (uint32_t e = 0; e < 16; ++e) z[e] = 0u;
-                tc::tmem_st16(s_col, z);
-                tc::tmem_st16(s_col + 16, z);
-                tc::tmem_st_wait();
-                tc::tc_fence_before();
-                tc::mbar_arrive(&p_full[2 * x + (s & 1)]);
-                continue;
-            }
-            const uint32_t nch = (nv_max + 31) >> 5;  // warp-uniform: 1 or 2
-            uint32_t v[2][32];
-            tc::tmem_ld32(s_col, v[0]);
-            if (nch > 1) tc::tmem_ld32(s_col + 32, v[1]);
-            tc::tmem_ld_wait();
-            if (dbg_me) p.dbg[s * 16 + 8] = globaltimer_ns();
-#pragma unroll
-            for (uint32_t c = 0; c < 2; ++c) {
-                if (c < nch && nv_min < 32 * (c + 1)) {  // a lane's limit falls in this chunk
-#pragma unroll
-                    for (uint32_t e = 0; e < 32; ++e)
-                        if (32 * c + e >= nv) v[c][e] = __float_as_uint(-INFINITY);
+                    for (uint32_t e = 0; e < 16; ++e) z[e] = 0u;
+                    tc::tmem_st16(s_col, z);
+                    tc::tmem_st16(s_col + 16, z);
+                    tc::tmem_st_wait();
+                    tc::tc_fence_before();
+                    tc::mbar_arrive(&p_full[2 * x + (sg & 1)]);
+                    continue;
                 }
-            }
-            if (p.starts && __any_sync(0xffffffffu, ns > 0u)) {  // batched: below the request's start
+                const uint32_t nch = (nv_max + 31) >> 5;  // warp-uniform: 1 or 2
+                uint32_t v[2][32];
+                tc::tmem_ld32(s_col, v[0]);
+                if (nch > 1) tc::tmem_ld32(s_col + 32, v[1]);
+                tc::tmem_ld_wait();
+                if (dbg_me) p.dbg[s * 16 + 8] = globaltimer_ns();
 #pragma unroll
-                for (uint32_t c = 0; c < 2; ++c)
-                    if (c < nch) {
+                for (uint32_t c = 0; c < 2; ++c) {
+                    if (c < nch && nv_min < 32 * (c + 1)) {  // a lane's limit falls in this chunk
 #pragma unroll
                         for (uint32_t e = 0; e < 32; ++e)
-                            if (32 * c + e < ns) v[c][e] = __float_as_uint(-INFINITY);
+                            if (32 * c + e >= nv) v[c][e] = __float_as_uint(-INFINITY);
                     }
-            }
-            float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+                }
+                if (p.starts && __any_sync(0xffffffffu, ns > 0u)) {  // batched: below the request's start
 #pragma unroll
-            for (uint32_t e = 0; e < 32; e += 2) {
-                mx0 = fmaxf(mx0, __uint_as_float(v[0][e]));
-                mx1 = fmaxf(mx1, __uint_as_float(v[0][e + 1]));
-            }
-            if (nch > 1) {
+                    for (uint32_t c = 0; c < 2; ++c)
+                        if (c < nch) {
+#pragma unroll
+                            for (uint32_t e = 0; e < 32; ++e)
+                                if (32 * c + e < ns) v[c][e] = __float_as_uint(-INFINITY);
+                        }
+                }
+                float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
                 for (uint32_t e = 0; e < 32; e += 2) {
-                    mx2 = fmaxf(mx2, __uint_as_float(v[1][e]));
-                    mx3 = fmaxf(mx3, __uint_as_float(v[1][e + 1]));
+                    mx0 = fmaxf(mx0, __uint_as_float(v[0][e]));
+                    mx1 = fmaxf(mx1, __uint_as_float(v[0][e + 1]));
                 }
-            }
-            const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.scale_log2;
-            if (dbg_me) p.dbg[s * 16 + 7] = globaltimer_ns();
-            float alpha = 1.0f;
-            const bool grow = mx > m_used + kRescaleThreshold || (m_used == -INFINITY && mx > -INFINITY);
-            if (grow) {
-                alpha = m_used == -INFINITY ? 0.0f : tc::ex2_approx(m_used - mx);
-                m_used = mx;
-                l *= alpha;
-            }
-            if (s > 0 && __any_sync(0xffffffffu, grow && alpha != 1.0f)) {
-                // every earlier PV of this lane must have landed before O is rescaled (S_X(s)
-                // completing implies PV_X(s - 2) did, so only phase s - 1 can be pending)
-                if (lane == 0) WD_WAIT(&o_done[x], (s - 1) & 1, 10, 0);
-                __syncwarp();
-                tc::tc_fence_after();
-#pragma unroll
-                for (uint32_t c = 0; c < 128; c += 32) {
-                    uint32_t o[32];
-                    tc::tmem_ld32(o_col + c, o);
-                    tc::tmem_ld_wait();
-#pragma unroll
-                    for (uint32_t e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                    tc::tmem_st32(o_col + c, o);
-                }
-                tc::tmem_st_wait();
-            }
-            const float neg_m = m_used == -INFINITY ? 0.0f : -m_used;
-            f2 lsum = mk2(0.f, 0.f);
-            const f2 sc2 = mk2(p.scale_log2, p.scale_log2), nm2 = mk2(neg_m, neg_m);
-#pragma unroll
-            for (uint32_t c = 0; c < 2; ++c) {
-                // exp2(s * scale - m) in packed pairs, a quarter of them on the FMA pipe
-                // (balances the MUFU and issue budgets); masked keys give exactly 0. P (bf16
-                // pairs) goes to TMEM columns [16c, 16c + 16) of the step's S buffer (whose
-                // scores are all in registers by now).
-                uint32_t pk[16];
-                if (c < nch) {
+                if (nch > 1) {
 #pragma unroll
                     for (uint32_t e = 0; e < 32; e += 2) {
-                        const f2 xs = fma2(mk2(__uint_as_float(v[c][e]), __uint_as_float(v[c][e + 1])), sc2, nm2);
-                        f2 ex;
-                        if ((MPIC_POLY_MASK >> ((e >> 1) & 7)) & 1u) ex = exp2_poly2(xs);
-                        else ex = mk2(tc::ex2_approx(lo(xs)), tc::ex2_approx(hi(xs)));
-                        lsum = add2(lsum, ex);
-                        pk[e >> 1] = pack_bf16(lo(ex), hi(ex));
+                        mx2 = fmaxf(mx2, __uint_as_float(v[1][e]));
+                        mx3 = fmaxf(mx3, __uint_as_float(v[1][e + 1]));
                     }
-                } else {
-#pragma unroll
-                    for (uint32_t e = 0; e < 16; ++e) pk[e] = 0u;
                 }
-                tc::tmem_st16(s_col + c * 16, pk);
+                const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.scale_log2;
+                if (dbg_me) p.dbg[s * 16 + 7] = globaltimer_ns();
+                float alpha = 1.0f;
+                const bool grow = mx > m_used + kRescaleThreshold || (m_used == -INFINITY && mx > -INFINITY);
+                if (grow) {
+                    alpha = m_used == -INFINITY ? 0.0f : tc::ex2_approx(m_used - mx);
+                    m_used = mx;
+                    l *= alpha;
+                }
+                if (s > 0 && __any_sync(0xffffffffu, grow && alpha != 1.0f)) {
+                    // every earlier PV of this item must have landed before O is rescaled (S_X(s)
+                    // completing implies PV_X(s - 2) did, so only PV s - 1's phase can be pending)
+                    if (lane == 0) WD_WAIT(&o_done[x], (sg - 1) & 1, 10, sg);
+                    __syncwarp();
+                    tc::tc_fence_after();
+#pragma unroll
+                    for (uint32_t c = 0; c < 128; c += 32) {
+                        uint32_t o[32];
+                        tc::tmem_ld32(o_col + c, o);
+                        tc::tmem_ld_wait();
+#pragma unroll
+                        for (uint32_t e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                        tc::tmem_st32(o_col + c, o);
+                    }
+                    tc::tmem_st_wait();
+                }
+                const float neg_m = m_used == -INFINITY ? 0.0f : -m_used;
+                f2 lsum = mk2(0.f, 0.f);
+                const f2 sc2 = mk2(p.scale_log2, p.scale_log2), nm2 = mk2(neg_m, neg_m);
+#pragma unroll
+                for (uint32_t c = 0; c < 2; ++c) {
+                    // exp2(s * scale - m) in packed pairs, a quarter of them on the FMA pipe
+                    // (balances the MUFU and issue budgets); masked keys give exactly 0. P (bf16
+                    // pairs) goes to TMEM columns [16c, 16c + 16) of the step's S buffer (whose
+                    // scores are all in registers by now).
+                    uint32_t pk[16];
+                    if (c < nch) {
+#pragma unroll
+                        for (uint32_t e = 0; e < 32; e += 2) {
+                            const f2 xs = fma2(mk2(__uint_as_float(v[c][e]), __uint_as_float(v[c][e + 1])), sc2, nm2);
+                            f2 ex;
+                            if ((MPIC_POLY_MASK >> ((e >> 1) & 7)) & 1u) ex = exp2_poly2(xs);
+                            else ex = mk2(tc::ex2_approx(lo(xs)), tc::ex2_approx(hi(xs)));
+                            lsum = add2(lsum, ex);
+                            pk[e >> 1] = pack_bf16(lo(ex), hi(ex));
+                        }
+                    } else {
+#pragma unroll
+                        for (uint32_t e = 0; e < 16; ++e) pk[e] = 0u;
+                    }
+                    tc::tmem_st16(s_col + c * 16, pk);
+                }
+                if (dbg_me) p.dbg[s * 16 + 9] = globaltimer_ns();
+                l += lo(lsum) + hi(lsum);
+                tc::tmem_st_wait();
+                tc::tc_fence_before();
+                if (dbg_me) p.dbg[s * 16 + 6] = globaltimer_ns();
+                if (p.dbg && blockIdx.x == 0 && ni == 0 && x == 1 && r == 0 && s < 64) p.dbg[s * 16 + 11] = globaltimer_ns();
+                tc::mbar_arrive(&p_full[2 * x + (sg & 1)]);
             }
-            if (dbg_me) p.dbg[s * 16 + 9] = globaltimer_ns();
-            l += lo(lsum) + hi(lsum);
-            tc::tmem_st_wait();
-            tc::tc_fence_before();
-            if (dbg_me) p.dbg[s * 16 + 6] = globaltimer_ns();
-            if (p.dbg && blockIdx.x == 0 && x == 1 && r == 0 && s < 64) p.dbg[s * 16 + 11] = globaltimer_ns();
-            tc::mbar_arrive(&p_full[2 * x + (s & 1)]);
-        }
-        // ---- epilogue: O / l, or the unnormalised partial + (m, l) for the combine. Split
-        // mode: lane 1 hands its (m, l) over through shared memory and lane 0 merges both
-        // accumulators (same TMEM lanes) into the tile's result.
-        // a barrier of its own for the last PV: with S double-buffered, o_done can be one
-        // phase behind or already past the last PV here, and its parity cannot tell which
-        if (lane == 0) WD_WAIT(&o_fin[x], 0, 12, 0);
-        __syncwarp();
-        tc::tc_fence_after();
-        const bool cta_stamp = x == 0 && r == 0 && p.dbg && blockIdx.x < kDbgCtas;
-        if (cta_stamp) p.dbg[kDbgCtaBase + 8 * blockIdx.x + 5] = globaltimer_ns();
-        float wa = 1.0f, wb = 0.0f;
-        if (split) {
-            if (x == 1) ml_x[r] = make_float2(m_used, l);
-            tc::named_bar_sync(1, 256);
-            if (x == 1) goto softmax_done;
-            const float2 mb = ml_x[r];
-            const float M = fmaxf(m_used, mb.x);
-            wa = m_used == -INFINITY ? 0.0f : tc::ex2_approx(m_used - M);
-            wb = mb.x == -INFINITY ? 0.0f : tc::ex2_approx(mb.x - M);
-            l = wa * l + wb * mb.y;
-            m_used = M;
-        }
-        {
+            sg0 += ns_x;
+            // ---- epilogue: O / l, or the unnormalised partial + (m, l) for the combine. Split
+            // mode: lane 1 hands its (m, l) over through shared memory and lane 0 merges both
+            // accumulators (same TMEM lanes) into the tile's result. Whoever reads an O
+            // releases it (o_free) to the next item's first PV.
+            // A barrier of its own for the last PV: with S double-buffered, o_done can be one
+            // phase behind or already past the last PV here, and its parity cannot tell which.
+            if (lane == 0) WD_WAIT(&o_fin[x], ni & 1, 12, ni);
+            __syncwarp();
+            tc::tc_fence_after();
+            const bool cta_stamp = ni == 0 && x == 0 && r == 0 && p.dbg && blockIdx.x < kDbgCtas;
+            if (cta_stamp) p.dbg[kDbgCtaBase + 8 * blockIdx.x + 5] = globaltimer_ns();
+            float wa = 1.0f, wb = 0.0f;
+            if (split) {
+                if (x == 1) ml_x[r] = make_float2(m_used, l);
+                tc::named_bar_sync(1, 256);
+                if (x == 1) continue;  // lane 0 reads (and releases) both accumulators
+                const float2 mb = ml_x[r];
+                const float M = fmaxf(m_used, mb.x);
+                wa = m_used == -INFINITY ? 0.0f : tc::ex2_approx(m_used - M);
+                wb = mb.x == -INFINITY ? 0.0f : tc::ex2_approx(mb.x - M);
+                l = wa * l + wb * mb.y;
+                m_used = M;
+            }
             const bool direct = slot_x == kNoTile;
             const float inv = l > 0.0f ? 1.0f / l : 0.0f;
             const uint32_t o_col_b = tmem + lane_base + 256 + 128;  // lane 1's O (split mode)
@@ -607,9 +658,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 } else {
                     tc::tmem_ld_wait();
                 }
+                if (c + 32 == 128) {  // every O column of this thread is in registers
+                    tc::tc_fence_before();
+                    tc::mbar_arrive(&o_free[x]);
+                    if (split) tc::mbar_arrive(&o_free[1]);
+                }
                 if (!valid) continue;
                 if (direct) {
-                    uint4* dst = reinterpret_cast<uint4*>(p.out + (size_t)qi * p.h + u.head * 128u + c);
+                    uint4* dst = reinterpret_cast<uint4*>(p.out + (size_t)qi * p.h + it.u.head * 128u + c);
 #pragma unroll
                     for (uint32_t q = 0; q < 4; ++q) {
                         uint4 w;
@@ -630,9 +686,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 }
             }
             if (valid && !direct) p.part_ml[(size_t)slot_x * 128 + r] = make_float2(m_used, l);
+            if (cta_stamp) p.dbg[kDbgCtaBase + 8 * blockIdx.x + 6] = globaltimer_ns();
         }
-        if (cta_stamp) p.dbg[kDbgCtaBase + 8 * blockIdx.x + 6] = globaltimer_ns();
-    softmax_done:;
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -813,6 +868,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     const CUtensorMap tmV = make_tmap_bf16(vcache, h, n_ctx, 64, 128);
     AttnParams p;
     p.units = d_units;
+    p.n_units = n_units;
     p.rows = d_rows;
     p.starts = d_starts;
     p.m = m;
@@ -830,7 +886,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
         return e && atoi(e) == 2;
     }();
     p.link_nostore = nostore ? 1u : 0u;
-    const size_t smem = (2 + kKStages + kVStages) * kTile + 1024 + (1 + 2 * kKStages + 2 * kVStages + 12) * 8 + 16 +
+    const size_t smem = (2 + kKStages + kVStages) * kTile + 1024 + (2 + 2 * kKStages + 2 * kVStages + 14) * 8 + 16 +
                         128 * sizeof(float2);
     static bool attr = false;
     if (!attr) {
@@ -843,7 +899,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     at[1].id = cudaLaunchAttributePriority;
     at[1].val.priority = hot_priority();
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(n_units);
+    cfg.gridDim = dim3(std::min<uint32_t>(n_units, kNumSMs));  // persistent: items dealt in snake order
     cfg.blockDim = dim3(kAttnThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;

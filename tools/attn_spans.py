@@ -19,6 +19,8 @@ def summarise(path):
     rows = []
     for l in g:
         m = re.search(r"start\s+([\d.]+) end\s+([\d.]+) us  head \d+ b0 (\d+) tiles \d+/(\d+) b1 (\d+)/(\d+)", l)
+        if not m:
+            continue
         s, e, b0, t1, b10, b11 = m.groups()
         n0 = int(b10) - int(b0); n1 = int(b11) - int(b0) if int(t1) != 999 else 0
         rows.append((float(s), float(e), max(n0, n1) - min(n0, n1) if n1 else n0, min(n0, n1) if n1 else 0))
