@@ -440,6 +440,25 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             // Writer of block b = the item streaming b for the lowest query tile reaching b.
             const uint32_t* blk = reinterpret_cast<const uint32_t*>(p.link + 1);
             const uint16_t* wtile = reinterpret_cast<const uint16_t*>(blk + p.link->nblk);
+            // One store group stays in flight: a stage is released once the NEXT store has
+            // been issued and the one before it has finished reading shared memory.
+            uint64_t* pending = nullptr;
+            auto stored = [&](uint64_t* empty_bar) {
+                tc::bulk_commit_group();
+                tc::bulk_wait_group_read<1>();
+                if (pending) tc::mbar_arrive(pending);
+                pending = empty_bar;
+            };
+            // a block without stores releases at once; the held stage goes first (its release
+            // must not wait for a later store: the producer may need that stage before then)
+            auto passed = [&](uint64_t* empty_bar) {
+                if (pending) {
+                    tc::bulk_wait_group_read<0>();
+                    tc::mbar_arrive(pending);
+                    pending = nullptr;
+                }
+                tc::mbar_arrive(empty_bar);
+            };
             uint32_t gb = 0;
             for (uint32_t ni = 0, idx; (idx = item_at(ni)) < p.n_units; ++ni) {
                 const Item it = item(idx);
@@ -452,20 +471,22 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     if (store) {
                         tc::tma_store_2d(&tmK, sK + sk * kTile, it.hcol, (int)(b * 128u));
                         tc::tma_store_2d(&tmK, sK + sk * kTile + kHalf, it.hcol + 64, (int)(b * 128u));
-                        tc::bulk_commit_group();
-                        tc::bulk_wait_group_read<0>();
+                        stored(&k_empty[sk]);
+                    } else {
+                        passed(&k_empty[sk]);
                     }
-                    tc::mbar_arrive(&k_empty[sk]);
                     WD_WAIT(&v_full[sv], (gb / kVStages) & 1, 8, gb);
                     if (store) {
                         tc::tma_store_2d(&tmV, sV + sv * kTile, it.hcol, (int)(b * 128u));
                         tc::tma_store_2d(&tmV, sV + sv * kTile + kHalf, it.hcol + 64, (int)(b * 128u));
-                        tc::bulk_commit_group();
-                        tc::bulk_wait_group_read<0>();
+                        stored(&v_empty[sv]);
+                    } else {
+                        passed(&v_empty[sv]);
                     }
-                    tc::mbar_arrive(&v_empty[sv]);
                 }
             }
+            tc::bulk_wait_group_read<0>();
+            if (pending) tc::mbar_arrive(pending);
             tc::bulk_wait_group<0>();  // the stores are complete before the CTA exits
         }
         __syncwarp();
