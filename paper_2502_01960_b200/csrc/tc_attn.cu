@@ -529,8 +529,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 const uint32_t ns = first > k0 ? min(first - k0, 64u) : 0u;
                 uint32_t nv = !valid || limit < k0 ? 0u : min(limit - k0 + 1u, 64u);
                 if (ns >= nv) nv = 0u;
-                const uint32_t nv_max = __reduce_max_sync(0xffffffffu, nv);
-                const uint32_t nv_min = __reduce_min_sync(0xffffffffu, nv);
+                // common case (every row of the warp sees the whole step): one vote instead
+                // of two warp reductions
+                const bool all_full = __all_sync(0xffffffffu, nv == 64u && ns == 0u);
+                const uint32_t nv_max = all_full ? 64u : __reduce_max_sync(0xffffffffu, nv);
+                const uint32_t nv_min = all_full ? 64u : __reduce_min_sync(0xffffffffu, nv);
                 if (nv_max == 0) {
                     uint32_t z[16];
 #pragma unroll
@@ -544,8 +547,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 }
                 const uint32_t nch = (nv_max + 31) >> 5;  // warp-uniform: 1 or 2
                 uint32_t v[2][32];
-                tc::tmem_ld32(s_col, v[0]);
-                if (nch > 1) tc::tmem_ld32(s_col + 32, v[1]);
+                if (nch > 1) tc::tmem_ld64(s_col, v[0], v[1]);
+                else tc::tmem_ld32(s_col, v[0]);
                 tc::tmem_ld_wait();
                 if (dbg_me) p.dbg[s * 16 + 8] = globaltimer_ns();
 #pragma unroll

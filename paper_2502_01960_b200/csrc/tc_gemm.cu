@@ -177,21 +177,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {
+        // warp-uniform MMA issue: lane 0 polls, one elected lane issues from uniform registers
+        {
             const uint32_t idesc = tc::idesc_bf16(128, a.bn);
             for (uint32_t kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
                 const uint32_t s = i % a.stages, ph = (i / a.stages) & 1;
-                tc::mbar_wait(&full[s], ph);
+                if (lane == 0) tc::mbar_wait(&full[s], ph);
+                __syncwarp();
                 tc::tc_fence_after();
                 const uint32_t x_base = tc::smem_u32(smem + s * stage_bytes);
                 const uint32_t w_base = x_base + kXBoxBytes;
+                if (tc::elect_one_sync()) {
 #pragma unroll
-                for (uint32_t kk = 0; kk < 4; ++kk)
-                    tc::mma_bf16(tmem_base, tc::desc_k_sw128(x_base + kk * 32), tc::desc_k_sw128(w_base + kk * 32),
-                                 idesc, (i > 0 || kk > 0) ? 1u : 0u);
-                tc::mma_commit(&empty[s]);
+                    for (uint32_t kk = 0; kk < 4; ++kk)
+                        tc::mma_bf16(tmem_base, tc::desc_k_sw128(x_base + kk * 32), tc::desc_k_sw128(w_base + kk * 32),
+                                     idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                    tc::mma_commit(&empty[s]);
+                }
             }
-            tc::mma_commit(tmem_full);
+            if (tc::elect_one_sync()) tc::mma_commit(tmem_full);
         }
         __syncwarp();
     } else {
@@ -299,7 +303,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {
+        // warp-uniform MMA issue: lane 0 polls, one elected lane issues from uniform registers
+        {
             const uint32_t idesc = tc::idesc_bf16(128, a.bn);
             uint32_t i = 0, seg = 0;
             uint64_t u = u_begin;
@@ -307,23 +312,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const uint32_t kb_begin = (uint32_t)(u % a.kblocks);
                 const uint64_t seg_end = u_end < u - kb_begin + a.kblocks ? u_end : u - kb_begin + a.kblocks;
                 const uint32_t buf = seg & 1;
-                tc::mbar_wait(&acc_empty[buf], ((seg >> 1) & 1) ^ 1);
+                if (lane == 0) tc::mbar_wait(&acc_empty[buf], ((seg >> 1) & 1) ^ 1);
+                __syncwarp();
                 tc::tc_fence_after();
                 const uint32_t d = tmem_base + buf * a.bn;
                 for (; u < seg_end; ++u, ++i) {
                     const uint32_t s = i % a.stages, ph = (i / a.stages) & 1;
-                    tc::mbar_wait(&full[s], ph);
+                    if (lane == 0) tc::mbar_wait(&full[s], ph);
+                    __syncwarp();
                     tc::tc_fence_after();
                     const uint32_t x_base = tc::smem_u32(smem + s * stage_bytes);
                     const uint32_t w_base = x_base + kXBoxBytes;
                     const bool first = (u % a.kblocks) == kb_begin;
+                    if (tc::elect_one_sync()) {
 #pragma unroll
-                    for (uint32_t kk = 0; kk < 4; ++kk)
-                        tc::mma_bf16(d, tc::desc_k_sw128(x_base + kk * 32), tc::desc_k_sw128(w_base + kk * 32), idesc,
-                                     (!first || kk > 0) ? 1u : 0u);
-                    tc::mma_commit(&empty[s]);
+                        for (uint32_t kk = 0; kk < 4; ++kk)
+                            tc::mma_bf16(d, tc::desc_k_sw128(x_base + kk * 32), tc::desc_k_sw128(w_base + kk * 32),
+                                         idesc, (!first || kk > 0) ? 1u : 0u);
+                        tc::mma_commit(&empty[s]);
+                    }
                 }
-                tc::mma_commit(&acc_full[buf]);
+                if (tc::elect_one_sync()) tc::mma_commit(&acc_full[buf]);
                 ++seg;
             }
         }

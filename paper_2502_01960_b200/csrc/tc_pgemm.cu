@@ -850,10 +850,15 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
         const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 4 + kEpiBars) * 8 + 16;
         const uint32_t nchunks = (a.G + 31) / 32;
         // MMA cycles per k-block (4 k16 steps): a cta_group::2 instruction costs
-        // max(N/2, ~83) cycles, and a lone accumulator chain issues ~1.5x slower than two
-        // interleaved ones (tools/mma_pair_probe); operand fill ~256 + G cycles.
+        // max(N/2, ~83) cycles; operand fill ~256 + G cycles. (With the single-thread issuer a
+        // lone accumulator chain issued ~1.5x slower than two interleaved ones; the
+        // warp-uniform issuer removed that: W2 at config C now takes 2 groups x S=2.)
+        static const double chain = [] {
+            const char* e = getenv("MPIC_PG_CHAIN");  // diagnostics: lone-chain issue factor
+            return e ? atof(e) : 1.0;  // 1.5 with the old single-thread issuer
+        }();
         const double mma = 4.0 * (std::max(a.P0 / 2.0, 83.0) + (a.P1 ? std::max(a.P1 / 2.0, 83.0) : 0.0)) *
-                           (a.P1 ? 1.0 : 1.5);
+                           (a.P1 ? 1.0 : chain);
         const double t_kb = std::max(mma, 256.0 + a.G);
         for (uint32_t S : {1u, 2u, 3u, 4u}) {
             if (force_s && S != force_s && S != 1) continue;
