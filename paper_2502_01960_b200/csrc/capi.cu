@@ -189,7 +189,7 @@ struct mpic_workspace_s {
     size_t slots_cap = 0;
     void* h_plan = nullptr;  // pinned staging for the plan
     size_t h_plan_cap = 0;
-    uint32_t n_units = 0, n_comb = 0;
+    uint32_t n_units = 0, n_unit_entries = 0, n_comb = 0;
     cudaEvent_t ev_plan = nullptr;
     // assembly descriptors (AsmChunk table + rerotation tables), pinned staging + device copy
     void* h_asm = nullptr;
@@ -500,12 +500,13 @@ void prepare_attn_plan(mpic_workspace_t ws, const uint32_t* h_rows, uint32_t m, 
     }
     std::memcpy(ws->h_plan, plan.units.data(), bu);
     std::memcpy((char*)ws->h_plan + bu, plan.combine.data(), bc);
-    ws->n_units = (uint32_t)plan.units.size();
+    ws->n_units = plan.items;  // work items; the per-CTA offsets follow them (AttnPlan)
+    ws->n_unit_entries = (uint32_t)plan.units.size();
     ws->n_comb = (uint32_t)plan.combine.size();
 }
 
 void enqueue_attn_plan(mpic_workspace_t ws, cudaStream_t s) {
-    const size_t bu = ws->n_units * sizeof(AttnUnit), bc = ws->n_comb * sizeof(AttnCombine);
+    const size_t bu = ws->n_unit_entries * sizeof(AttnUnit), bc = ws->n_comb * sizeof(AttnCombine);
     if (bu) MPIC_CUDA(cudaMemcpyAsync(ws->d_units, ws->h_plan, bu, cudaMemcpyHostToDevice, s));
     if (bc) MPIC_CUDA(cudaMemcpyAsync(ws->d_comb, (char*)ws->h_plan + bu, bc, cudaMemcpyHostToDevice, s));
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -2949,7 +2950,7 @@ int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const
     launch_attn_tc(static_cast<const __nv_bfloat16*>(d_q), static_cast<const __nv_bfloat16*>(d_k),
                    static_cast<const __nv_bfloat16*>(d_v), n_ctx,
                    reinterpret_cast<const uint32_t*>(b + bu + bc + bo + bm), m, n_heads,
-                   reinterpret_cast<const AttnUnit*>(b), (uint32_t)plan.units.size(),
+                   reinterpret_cast<const AttnUnit*>(b), plan.items,
                    reinterpret_cast<const AttnCombine*>(b + bu), (uint32_t)plan.combine.size(),
                    reinterpret_cast<float*>(b + bu + bc), reinterpret_cast<float2*>(b + bu + bc + bo),
                    static_cast<__nv_bfloat16*>(d_out), s);
@@ -2960,12 +2961,13 @@ int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const
         MPIC_CUDA(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
         MPIC_CUDA(cudaMemset(dbg, 0, h.size() * 8));
         {  // per-CTA spans (start, end, smid, first MMA, last burst, epilogue start/end), relative to the earliest start
-            const size_t base = 16 * 64, ncta = std::min<size_t>(std::min<size_t>(plan.units.size(), kNumSMs), (h.size() - base) / 8);
+            const size_t base = 16 * 64, ncta = std::min<size_t>(std::min<size_t>(plan.items, kNumSMs), (h.size() - base) / 8);
+            const uint32_t* offs = attn_cta_offsets(plan.units.data(), plan.items);
             unsigned long long t_min = ~0ull;
             for (size_t c = 0; c < ncta; ++c) t_min = std::min(t_min, h[base + 8 * c]);
             auto rel = [&](size_t c, int k) { return h[base + 8 * c + k] ? (h[base + 8 * c + k] - t_min) / 1e3 : -1.0; };
             for (size_t c = 0; c < ncta; ++c) {
-                const AttnUnit& u = plan.units[c];
+                const AttnUnit& u = plan.units[offs[c]];  // the CTA's first item
                 fprintf(stderr, "cta %4zu sm %3llu start %8.2f end %8.2f us  head %u b0 %u tiles %u/%u b1 %u/%u | mma0 %8.2f "
                                 "lastmma %8.2f epi %8.2f epi_end %8.2f\n", c,
                         h[base + 8 * c + 2], rel(c, 0), rel(c, 1), u.head, u.b0, u.tile[0], u.tile[1] == kNoTile ? 999u : u.tile[1],

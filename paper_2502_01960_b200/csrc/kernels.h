@@ -113,10 +113,21 @@ struct AttnCombine {
     uint32_t tile, head, slot0, n;
 };
 struct AttnPlan {
+    // units[0, items): the work items grouped by persistent CTA (CTA c runs items
+    // [off[c], off[c + 1])), then the offsets themselves packed into the trailing entries
+    // (attn_cta_offsets): one device buffer carries both
     std::vector<AttnUnit> units;
     std::vector<AttnCombine> combine;
     uint32_t slots = 0;
+    uint32_t items = 0;
 };
+// The per-CTA item offsets stored after a plan's `items` work items.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline const uint32_t* attn_cta_offsets(const AttnUnit* units, uint32_t items) {
+    return reinterpret_cast<const uint32_t*>(units + items);
+}
 unsigned long long* attn_debug_buffer();
 // starts (optional, batched requests): per selected row, the first cache row of its request.
 AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads, const uint32_t* starts = nullptr);

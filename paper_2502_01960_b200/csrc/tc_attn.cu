@@ -232,13 +232,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         p.dbg[kDbgCtaBase + 8 * blockIdx.x] = globaltimer_ns();
         p.dbg[kDbgCtaBase + 8 * blockIdx.x + 2] = smid;
     }
-    // Persistent CTA: items idx(0), idx(1), ... of the cost-sorted list, dealt round-robin in
-    // snake order (round r: CTA c takes r*G + c, or r*G + G-1-c on odd rounds). Every role
-    // walks the same item sequence with running block / step / item counters, so barrier
-    // phases continue across items and the next item's Q/K/V loads and first S MMAs overlap
-    // the current item's tail and epilogue.
-    const uint32_t G = gridDim.x;
-    auto item_at = [&](uint32_t r) { return r * G + ((r & 1) ? G - 1 - blockIdx.x : blockIdx.x); };
+    // Persistent CTA: the items the host assigned to this CTA (longest-processing-time over
+    // the estimated costs, plan_attention). Every role walks the same item sequence with
+    // running block / step / item counters, so barrier phases continue across items and the
+    // next item's Q/K/V loads and first S MMAs overlap the current item's tail and epilogue.
+    const uint32_t* cta_off = attn_cta_offsets(p.units, p.n_units);
+    const uint32_t it_begin = cta_off[blockIdx.x], it_end = cta_off[blockIdx.x + 1];
+    auto item_at = [&](uint32_t r) { return it_begin + r < it_end ? it_begin + r : p.n_units; };
     // Two lanes (X = 0, 1), each with its own softmax warpgroup, O accumulator and two S
     // buffers, walk 64-key steps. Pair mode (two query tiles): lane X = tile X over every
     // half-block of its range, step s = half s & 1 of block s >> 1. Split mode (one tile):
@@ -847,16 +847,16 @@ AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads, cons
             if (open) plan.units.push_back(cur);
         }
     }
-    // Longest-processing-time first by estimated cost (half-block units, from the kernel's
-    // measured per-CTA spans): a pair item's 128-key block ~2 (two tiles' MMAs), a block one
-    // tile of a pair streams alone ~1.5 (its lane's softmax chain), a split item's block ~1
-    // (both lanes on one tile); per-item setup ~3 blocks.
+    // Estimated cost in 0.1 us, from the kernel's measured per-block times (MPIC_ATTN_TS
+    // fits): a pair item's 128-key block ~2.7 us (two tiles), a block one tile of a pair
+    // streams alone ~2.0, a split item's block ~1.6 (both lanes on one tile); ~2 us per item
+    // (first loads and epilogue not hidden by the persistent loop).
     static const bool by_cost = getenv("MPIC_ATTN_SORT_LEN") == nullptr;  // diagnostics: 1 = by length
-    auto cost = [](const AttnUnit& a) {
-        if (a.tile[1] == kNoTile) return 2 * (a.b1[0] - a.b0) + 6;
+    auto cost = [](const AttnUnit& a) -> uint32_t {
+        if (a.tile[1] == kNoTile) return 16 * (a.b1[0] - a.b0) + 20;
         const uint32_t len = std::max(a.b1[0], a.b1[1]) - a.b0;
         const uint32_t both = std::min(a.b1[0], a.b1[1]) - a.b0;
-        return 4 * both + 3 * (len - both) + 6;
+        return 27 * both + 20 * (len - both) + 20;
     };
     std::stable_sort(plan.units.begin(), plan.units.end(), [&](const AttnUnit& a, const AttnUnit& b) {
         if (by_cost) return cost(a) > cost(b);
@@ -864,6 +864,34 @@ AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads, cons
         const uint32_t lb = std::max(b.b1[0], b.tile[1] == kNoTile ? 0u : b.b1[1]) - b.b0;
         return la > lb;
     });
+    // Longest-processing-time assignment to the persistent CTAs: each item (largest first)
+    // goes to the least-loaded CTA; the items are then grouped by CTA and the offsets packed
+    // behind them.
+    const uint32_t n = (uint32_t)plan.units.size(), G = std::min<uint32_t>(n, kNumSMs);
+    plan.items = n;
+    if (n) {
+        std::vector<std::vector<AttnUnit>> per(G);
+        std::vector<std::pair<uint64_t, uint32_t>> heap;  // (load, cta), min-heap
+        for (uint32_t c = 0; c < G; ++c) heap.push_back({0, c});
+        auto gt = [](const std::pair<uint64_t, uint32_t>& a, const std::pair<uint64_t, uint32_t>& b) { return a > b; };
+        for (const AttnUnit& u : plan.units) {
+            std::pop_heap(heap.begin(), heap.end(), gt);
+            auto& top = heap.back();
+            per[top.second].push_back(u);
+            top.first += cost(u);
+            std::push_heap(heap.begin(), heap.end(), gt);
+        }
+        std::vector<uint32_t> off(G + 1, 0);
+        plan.units.clear();
+        for (uint32_t c = 0; c < G; ++c) {
+            off[c] = (uint32_t)plan.units.size();
+            plan.units.insert(plan.units.end(), per[c].begin(), per[c].end());
+        }
+        off[G] = n;
+        const size_t entries = (off.size() * sizeof(uint32_t) + sizeof(AttnUnit) - 1) / sizeof(AttnUnit);
+        plan.units.resize(n + entries);
+        std::memcpy(plan.units.data() + n, off.data(), off.size() * sizeof(uint32_t));
+    }
     return plan;
 }
 
@@ -923,7 +951,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     at[1].id = cudaLaunchAttributePriority;
     at[1].val.priority = hot_priority();
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(std::min<uint32_t>(n_units, kNumSMs));  // persistent: items dealt in snake order
+    cfg.gridDim = dim3(std::min<uint32_t>(n_units, kNumSMs));  // persistent: one CTA per SM, items per CTA from the plan
     cfg.blockDim = dim3(kAttnThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
