@@ -37,6 +37,18 @@ bool pdl_enabled() {
     return on;
 }
 
+// MPIC_ATTN_FUSED_COMBINE=1 (diagnostics): the split that completes a (tile, head) merges the
+// partials inside the attention kernel instead of attn_combine_kernel. Measured slower at
+// config C (attention 2.85 -> 4.32 ms per request): a merge is a latency-bound read of up to
+// 16 x 64 KB by one warpgroup, on the critical path of whichever CTA finishes a job last.
+static bool fused_combine() {
+    static const bool on = [] {
+        const char* e = getenv("MPIC_ATTN_FUSED_COMBINE");
+        return e && atoi(e) != 0;
+    }();
+    return on;
+}
+
 // Scheduling priority of the request's hot kernels (GEMMs, attention): above the default
 // priority of the side-stream assembly, so assembly CTAs only fill SMs the hot path leaves
 // idle. MPIC_PRIO=0 (diagnostics) launches everything at the default priority.
@@ -183,7 +195,8 @@ struct mpic_workspace_s {
     // tcgen05 attention plan (per request) and split partials
     AttnUnit* d_units = nullptr;
     AttnCombine* d_comb = nullptr;
-    size_t units_cap = 0, comb_cap = 0;
+    uint32_t* d_comb_cnt = nullptr;  // fused combine: per job, splits finished (self-resetting, zeroed once)
+    size_t units_cap = 0, comb_cap = 0, comb_cnt_cap = 0;
     float* part_o = nullptr;
     float2* part_ml = nullptr;
     size_t slots_cap = 0;
@@ -479,6 +492,14 @@ void prepare_attn_plan(mpic_workspace_t ws, const uint32_t* h_rows, uint32_t m, 
     };
     grow(ws->d_units, ws->units_cap, plan.units.size(), sizeof(AttnUnit));
     grow(ws->d_comb, ws->comb_cap, plan.combine.size(), sizeof(AttnCombine));
+    if (ws->comb_cnt_cap < plan.combine.size()) {  // the kernel leaves every counter at 0
+        ++ws->gen;
+        MPIC_CUDA(cudaDeviceSynchronize());
+        cudaFree(ws->d_comb_cnt);
+        MPIC_CUDA(cudaMalloc(&ws->d_comb_cnt, plan.combine.size() * sizeof(uint32_t)));
+        MPIC_CUDA(cudaMemset(ws->d_comb_cnt, 0, plan.combine.size() * sizeof(uint32_t)));
+        ws->comb_cnt_cap = plan.combine.size();
+    }
     if (ws->slots_cap < plan.slots) {
         ++ws->gen;
         MPIC_CUDA(cudaDeviceSynchronize());
@@ -586,7 +607,8 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
                 launch_attn_tc(static_cast<const __nv_bfloat16*>(ws->q), static_cast<const __nv_bfloat16*>(kl),
                                static_cast<const __nv_bfloat16*>(vl), kv->T, d_rows, m, H, ws->d_units,
                                ws->n_units, ws->d_comb, ws->n_comb, ws->part_o, ws->part_ml,
-                               static_cast<__nv_bfloat16*>(ws->attn), s, d_link, l, d_starts);
+                               static_cast<__nv_bfloat16*>(ws->attn), s, d_link, l, d_starts,
+                               fused_combine() ? ws->d_comb_cnt : nullptr);
             else
                 launch_attn_simt(ws->q, kl, vl, md->dtype, d_rows, m, H, D, ws->attn, s);
         }
@@ -1386,6 +1408,7 @@ int mpic_workspace_destroy(mpic_workspace_t ws) {
         if (ws->copy_stream) cudaStreamDestroy(ws->copy_stream);
         cudaFree(ws->d_units);
         cudaFree(ws->d_comb);
+        cudaFree(ws->d_comb_cnt);
         cudaFree(ws->part_o);
         cudaFree(ws->part_ml);
         cudaFreeHost(ws->h_plan);
@@ -1975,7 +1998,8 @@ void hp_attn(mpic_model_t md, mpic_workspace_t ws, uint32_t l, mpic_kv_t kv, flo
         MPIC_REQUIRE(use_tc_attention(md), MPIC_ERR_VALIDATION, "head-parallel attention needs head_dim 128");
         launch_attn_tc(static_cast<const __nv_bfloat16*>(ws->q), static_cast<const __nv_bfloat16*>(kl),
                        static_cast<const __nv_bfloat16*>(vl), kv->T, ws->d_rows, m, Hl, ws->d_units, ws->n_units,
-                       ws->d_comb, ws->n_comb, ws->part_o, ws->part_ml, static_cast<__nv_bfloat16*>(ws->attn), s);
+                       ws->d_comb, ws->n_comb, ws->part_o, ws->part_ml, static_cast<__nv_bfloat16*>(ws->attn), s,
+                       nullptr, 0, nullptr, fused_combine() ? ws->d_comb_cnt : nullptr);
     }
     EpiParams st;
     st.mode = EPI_STORE_F32;
@@ -2939,9 +2963,12 @@ int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const
     void* buf = nullptr;
     auto al = [](size_t x) { return (x + 255) / 256 * 256; };
     const size_t bu = al(plan.units.size() * sizeof(AttnUnit)), bc = al(plan.combine.size() * sizeof(AttnCombine));
-    const size_t bo = al((size_t)plan.slots * 128 * 128 * 4), bm = al((size_t)plan.slots * 128 * 8), br = (size_t)m * 4;
-    MPIC_CUDA(cudaMallocAsync(&buf, bu + bc + bo + bm + br + 64, s));
+    const size_t bo = al((size_t)plan.slots * 128 * 128 * 4), bm = al((size_t)plan.slots * 128 * 8), br = al((size_t)m * 4);
+    const size_t bn = (size_t)plan.combine.size() * 4;
+    MPIC_CUDA(cudaMallocAsync(&buf, bu + bc + bo + bm + br + bn + 64, s));
     char* b = static_cast<char*>(buf);
+    uint32_t* d_cnt = !fused_combine() || !bn ? nullptr : reinterpret_cast<uint32_t*>(b + bu + bc + bo + bm + br);
+    if (d_cnt) MPIC_CUDA(cudaMemsetAsync(d_cnt, 0, bn, s));
     MPIC_CUDA(cudaMemcpyAsync(b, plan.units.data(), plan.units.size() * sizeof(AttnUnit), cudaMemcpyHostToDevice, s));
     if (!plan.combine.empty())
         MPIC_CUDA(cudaMemcpyAsync(b + bu, plan.combine.data(), plan.combine.size() * sizeof(AttnCombine),
@@ -2953,7 +2980,7 @@ int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const
                    reinterpret_cast<const AttnUnit*>(b), plan.items,
                    reinterpret_cast<const AttnCombine*>(b + bu), (uint32_t)plan.combine.size(),
                    reinterpret_cast<float*>(b + bu + bc), reinterpret_cast<float2*>(b + bu + bc + bo),
-                   static_cast<__nv_bfloat16*>(d_out), s);
+                   static_cast<__nv_bfloat16*>(d_out), s, nullptr, 0, nullptr, d_cnt);
     MPIC_CUDA(cudaFreeAsync(buf, s));
     if (unsigned long long* dbg = attn_debug_buffer()) {  // MPIC_ATTN_TS diagnostics
         std::vector<unsigned long long> h(16 * 4096);

@@ -108,6 +108,7 @@ struct AttnUnit {
     uint32_t tile[2];
     uint32_t b1[2];    // per-tile end block
     uint32_t slot[2];  // kNoTile: write the final output; else partial slot for the combine
+    uint32_t job[2];   // with a partial slot: its combine job (the last split to finish merges it)
 };
 struct AttnCombine {
     uint32_t tile, head, slot0, n;
@@ -164,7 +165,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
                     const AttnUnit* d_units, uint32_t n_units, const AttnCombine* d_combine,
                     uint32_t n_combine, float* part_o, float2* part_ml, __nv_bfloat16* out,
                     cudaStream_t s, const AttnLink* link = nullptr, uint32_t layer = 0,
-                    const uint32_t* d_starts = nullptr);
+                    const uint32_t* d_starts = nullptr, uint32_t* d_counters = nullptr);
 
 // tcgen05 / TMA kernels (tc_gemm.cu, tc_attn.cu)
 struct TcGemmPlan;

@@ -59,6 +59,8 @@ constexpr uint32_t kDbgCtaBase = 16 * 64, kDbgCtas = (16 * 4096 - kDbgCtaBase) /
 struct AttnParams {
     const AttnUnit* units;
     uint32_t n_units;
+    const AttnCombine* combine;  // fused combine (counters != null): the jobs
+    uint32_t* counters;          // per job: splits finished (the last one merges, then resets it)
     const uint32_t* rows;
     const uint32_t* starts;  // batched requests: first key row each query row may see (null: 0)
     uint32_t m;
@@ -188,6 +190,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     uint64_t* o_free = o_fin + 2;                // [2 lanes] O read out by the epilogue
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_free + 2);
     float2* ml_x = reinterpret_cast<float2*>(tmem_holder + 4);  // [128] split mode: lane 1's (m, l)
+    uint32_t* merge_flag = reinterpret_cast<uint32_t*>(ml_x + 128);  // [2] fused combine: this lane merges
 
     tc::pdl_trigger();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -710,6 +713,75 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 }
             }
             if (valid && !direct) p.part_ml[(size_t)slot_x * 128 + r] = make_float2(m_used, l);
+            if (!direct && p.counters) {
+                // fused combine: the split that completes its (tile, head) job merges it —
+                // O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s over the job's partial slots
+                // (L2-coherent loads: the other splits were written by other SMs)
+                const uint32_t job = split ? it.u.job[0] : it.u.job[x];
+                __threadfence();
+                tc::named_bar_sync(2 + x, 128);
+                if (r == 0) {
+                    const AttnCombine jb = p.combine[job];
+                    merge_flag[x] = atomicAdd(&p.counters[job], 1u) + 1u == jb.n ? 1u : 0u;
+                }
+                tc::named_bar_sync(2 + x, 128);
+                if (merge_flag[x]) {
+                    __threadfence();
+                    const AttnCombine jb = p.combine[job];
+                    const uint32_t n = min(jb.n, 16u);
+                    float wt[16];
+                    float M = -INFINITY, L = 0.0f;
+#pragma unroll
+                    for (uint32_t s2 = 0; s2 < 16; ++s2)
+                        if (s2 < n) {
+                            const float2 ml = __ldcg(p.part_ml + (size_t)(jb.slot0 + s2) * 128 + r);
+                            wt[s2] = ml.x;
+                            M = fmaxf(M, ml.x);
+                        }
+#pragma unroll
+                    for (uint32_t s2 = 0; s2 < 16; ++s2)
+                        if (s2 < n) {
+                            const float2 ml = __ldcg(p.part_ml + (size_t)(jb.slot0 + s2) * 128 + r);
+                            wt[s2] = ml.x == -INFINITY ? 0.0f : exp2f(ml.x - M);
+                            L += wt[s2] * ml.y;
+                        }
+                    const float invL = L > 0.0f ? 1.0f / L : 0.0f;
+                    const float4* po = reinterpret_cast<const float4*>(p.part_o) + (size_t)jb.slot0 * 32 * 128 + r;
+#pragma unroll 1
+                    for (uint32_t c8 = 0; c8 < 32; c8 += 8) {  // 8 float4 columns (32 dims) at a time
+                        float4 acc[8];
+#pragma unroll
+                        for (uint32_t e = 0; e < 8; ++e) acc[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (uint32_t s2 = 0; s2 < n; ++s2) {
+                            float w = 0.0f;
+#pragma unroll
+                            for (uint32_t i = 0; i < 16; ++i)
+                                if (i == s2) w = wt[i];
+#pragma unroll
+                            for (uint32_t e = 0; e < 8; ++e) {
+                                const float4 v4 = __ldcg(po + ((size_t)s2 * 32 + c8 + e) * 128);
+                                acc[e].x += w * v4.x;
+                                acc[e].y += w * v4.y;
+                                acc[e].z += w * v4.z;
+                                acc[e].w += w * v4.w;
+                            }
+                        }
+                        if (valid) {
+                            uint4* dst = reinterpret_cast<uint4*>(p.out + (size_t)qi * p.h + it.u.head * 128u + c8 * 4);
+#pragma unroll
+                            for (uint32_t q = 0; q < 4; ++q) {
+                                uint4 w4;
+                                w4.x = pack_bf16(acc[2 * q].x * invL, acc[2 * q].y * invL);
+                                w4.y = pack_bf16(acc[2 * q].z * invL, acc[2 * q].w * invL);
+                                w4.z = pack_bf16(acc[2 * q + 1].x * invL, acc[2 * q + 1].y * invL);
+                                w4.w = pack_bf16(acc[2 * q + 1].z * invL, acc[2 * q + 1].w * invL);
+                                dst[q] = w4;
+                            }
+                        }
+                    }
+                    if (r == 0) p.counters[job] = 0u;  // reset for the next launch
+                }
+            }
             if (cta_stamp) p.dbg[kDbgCtaBase + 8 * blockIdx.x + 6] = globaltimer_ns();
         }
     }
@@ -810,12 +882,13 @@ AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads, cons
     // splits: tile t's range cut by the global grid [sp*chunk, (sp+1)*chunk)
     auto cell0 = [&](uint32_t t) { return sblk[t] / chunk; };
     auto cells = [&](uint32_t t) { return ceil_div(nblk[t], chunk) - cell0(t); };
-    std::vector<uint32_t> slot0(tiles * n_heads, kNoTile);
+    std::vector<uint32_t> slot0(tiles * n_heads, kNoTile), job0(tiles * n_heads, kNoTile);
     uint32_t slot = 0;
     for (uint32_t t = 0; t < tiles; ++t) {
         const uint32_t splits = cells(t);
         if (splits < 2) continue;
         for (uint32_t hd = 0; hd < n_heads; ++hd) {
+            job0[t * n_heads + hd] = (uint32_t)plan.combine.size();
             plan.combine.push_back(AttnCombine{t, hd, slot, splits});
             slot0[t * n_heads + hd] = slot;
             slot += splits;
@@ -830,18 +903,19 @@ AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads, cons
             for (uint32_t t = 0; t < tiles; ++t) {
                 const uint32_t lo = std::max(sblk[t], sp * chunk), hi = std::min(nblk[t], (sp + 1) * chunk);
                 if (lo >= hi) continue;
-                const uint32_t s0 = slot0[t * n_heads + hd];
+                const uint32_t s0 = slot0[t * n_heads + hd], jb = job0[t * n_heads + hd];
                 const uint32_t sl = s0 == kNoTile ? kNoTile : s0 + (sp - cell0(t));
                 if (open && cur.b0 == lo) {  // pair with the open item: same first key block
                     cur.tile[1] = t;
                     cur.b1[1] = hi;
                     cur.slot[1] = sl;
+                    cur.job[1] = jb;
                     plan.units.push_back(cur);
                     open = false;
                     continue;
                 }
                 if (open) plan.units.push_back(cur);
-                cur = AttnUnit{hd, lo, {t, kNoTile}, {hi, 0}, {sl, kNoTile}};
+                cur = AttnUnit{hd, lo, {t, kNoTile}, {hi, 0}, {sl, kNoTile}, {jb, kNoTile}};
                 open = true;
             }
             if (open) plan.units.push_back(cur);
@@ -913,7 +987,8 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
                     uint32_t n_ctx, const uint32_t* d_rows, uint32_t m, uint32_t H,
                     const AttnUnit* d_units, uint32_t n_units, const AttnCombine* d_combine,
                     uint32_t n_combine, float* part_o, float2* part_ml, __nv_bfloat16* out,
-                    cudaStream_t s, const AttnLink* link, uint32_t layer, const uint32_t* d_starts) {
+                    cudaStream_t s, const AttnLink* link, uint32_t layer, const uint32_t* d_starts,
+                    uint32_t* d_counters) {
     const uint32_t h = H * 128;
     const CUtensorMap tmQ = make_tmap_bf16(q, h, m, 64, 128);
     const CUtensorMap tmK = make_tmap_bf16(kcache, h, n_ctx, 64, 128);
@@ -921,6 +996,8 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     AttnParams p;
     p.units = d_units;
     p.n_units = n_units;
+    p.combine = d_combine;
+    p.counters = d_counters;
     p.rows = d_rows;
     p.starts = d_starts;
     p.m = m;
@@ -939,7 +1016,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     }();
     p.link_nostore = nostore ? 1u : 0u;
     const size_t smem = (2 + kKStages + kVStages) * kTile + 1024 + (2 + 2 * kKStages + 2 * kVStages + 14) * 8 + 16 +
-                        128 * sizeof(float2);
+                        128 * sizeof(float2) + 16;
     static bool attr = false;
     if (!attr) {
         MPIC_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -959,7 +1036,7 @@ void launch_attn_tc(const __nv_bfloat16* q, const __nv_bfloat16* kcache, const _
     cfg.numAttrs = 2;
     MPIC_CUDA(cudaLaunchKernelEx(&cfg, attn_tc_kernel, tmQ, tmK, tmV, p));
     MPIC_LAUNCHED();
-    if (n_combine) {
+    if (n_combine && !d_counters) {  // (with counters the attention kernel merges the splits itself)
         cfg.gridDim = dim3(n_combine, 16);
         cfg.blockDim = dim3(256);
         cfg.dynamicSmemBytes = 0;
