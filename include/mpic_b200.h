@@ -363,6 +363,16 @@ int mpic_profile_collect(double* ms, uint32_t* counts);
 /* Test hook: the head_dim-128 tcgen05 selective attention on bf16 device buffers
  * q [m][H*128], k/v [n_ctx][H*128]; query i attends keys [0, rows[i]] (host rows,
  * ascending). out [m][H*128] bf16. Async on `stream`. */
+/* Host-only inspection of the tcgen05 attention work plan (tc_attn.cu plan_attention) for
+ * the recomputed rows' positions `rows` (ascending), m rows, n_heads heads, optional batched
+ * request starts: counts[0] = work items, counts[1] = persistent CTAs, counts[2] = combine
+ * jobs, counts[3] = partial slots. units_out (may be NULL, units_cap entries of 10 uint32:
+ * head, b0, tile[2], b1[2], slot[2], job[2]) receives the items grouped by CTA, offs_out
+ * (ctas + 1 entries) the per-CTA item offsets, jobs_out (4 uint32 each: tile, head, slot0,
+ * n) the combine jobs. No GPU needed. Diagnostics / tests. */
+int mpic_attention_plan(const uint32_t* rows, uint32_t m, uint32_t n_heads, const uint32_t* starts,
+                        uint32_t* counts, uint32_t* units_out, uint32_t units_cap, uint32_t* offs_out,
+                        uint32_t offs_cap, uint32_t* jobs_out, uint32_t jobs_cap);
 int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const uint32_t* rows,
                         uint32_t m, uint32_t n_ctx, uint32_t n_heads, void* d_out, void* stream);
 

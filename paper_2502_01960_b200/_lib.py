@@ -122,6 +122,7 @@ SIGNATURES = {
     "mpic_profile_enable": (_int, [_int]),
     "mpic_profile_collect": (_int, [_vp, _vp]),
     "mpic_test_attention": (_int, [_vp, _vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp]),
+    "mpic_attention_plan": (_int, [_vp, _u32, _u32, _vp, _vp, _vp, _u32, _vp, _u32, _vp, _u32]),
     "mpic_host_gemm_f32": (_int, [_vp, _vp, _u32, _u32, _u32, _vp, _int]),
     "mpic_host_alloc": (_int, [C.c_size_t, _P(_vp)]),
     "mpic_host_free": (_int, [_vp]),

@@ -2955,6 +2955,33 @@ int mpic_profile_collect(double* ms, uint32_t* launches) {
     API_END
 }
 
+int mpic_attention_plan(const uint32_t* rows, uint32_t m, uint32_t n_heads, const uint32_t* starts,
+                        uint32_t* counts, uint32_t* units_out, uint32_t units_cap, uint32_t* offs_out,
+                        uint32_t offs_cap, uint32_t* jobs_out, uint32_t jobs_cap) {
+    API_BEGIN
+    MPIC_REQUIRE(rows && counts && m > 0 && n_heads > 0, MPIC_ERR_VALIDATION, "attention plan: bad arguments");
+    const AttnPlan plan = plan_attention(rows, m, n_heads, starts);
+    const uint32_t ctas = std::min<uint32_t>(plan.items, kNumSMs);
+    counts[0] = plan.items;
+    counts[1] = ctas;
+    counts[2] = (uint32_t)plan.combine.size();
+    counts[3] = plan.slots;
+    static_assert(sizeof(AttnUnit) == 10 * sizeof(uint32_t), "AttnUnit layout");
+    if (units_out) {
+        MPIC_REQUIRE(units_cap >= plan.items, MPIC_ERR_VALIDATION, "attention plan: units_out too small");
+        std::memcpy(units_out, plan.units.data(), (size_t)plan.items * sizeof(AttnUnit));
+    }
+    if (offs_out) {
+        MPIC_REQUIRE(offs_cap >= ctas + 1, MPIC_ERR_VALIDATION, "attention plan: offs_out too small");
+        std::memcpy(offs_out, attn_cta_offsets(plan.units.data(), plan.items), (ctas + 1) * sizeof(uint32_t));
+    }
+    if (jobs_out) {
+        MPIC_REQUIRE(jobs_cap >= plan.combine.size(), MPIC_ERR_VALIDATION, "attention plan: jobs_out too small");
+        std::memcpy(jobs_out, plan.combine.data(), plan.combine.size() * sizeof(AttnCombine));
+    }
+    API_END
+}
+
 int mpic_test_attention(const void* d_q, const void* d_k, const void* d_v, const uint32_t* rows,
                         uint32_t m, uint32_t n_ctx, uint32_t n_heads, void* d_out, void* stream) {
     API_BEGIN
