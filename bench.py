@@ -568,6 +568,40 @@ def run_ours(args, world, rank, local):
         if args.e2e_fp32:
             e2e_fp32 = time_host_leg(host_kf, host_vf, "fp32 .mpic-v1")
 
+    # ---- decode after the prefill (decode_step, proj/src/model.cpp:356-367 = extend_rows of
+    # one row at the end of the cache): bf16 tensor-core path (tcgen05 GEMMs at one token,
+    # tcgen05 attention over the whole cache), synchronous per token (host id in, logits out).
+    # Per token it must stream every weight (12.9 GB at config C) and the cache's K/V: an
+    # HBM-bound step, reported against the measured copy rate.
+    decode = None
+    if args.decode_steps and rank == 0:
+        D_ = args.decode_steps
+        kvd = mp.KV(L, n + D_ + 1, H, D, mp.BF16, dev)
+        wsd = mp.Workspace(model, 16, n + D_ + 1)
+        tok = [int(x) for x in np.random.default_rng(5).integers(0, V - 1, D_ + 1)]
+        mp.prefill_extend(model, wsd, [tok[0]], n, 0, kvd, stream=stream)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_d = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e_d[0].record(stream)
+        for i in range(D_):
+            mp.prefill_extend(model, wsd, [tok[i + 1]], n + 1 + i, 0, kvd, stream=stream)
+        e_d[1].record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / D_ * 1e3
+        dev_ms = e_d[0].elapsed_time(e_d[1]) / D_
+        ctx = n + 1 + D_ / 2
+        wbytes = L * 12 * h * h * 2 + V * h * 2  # bf16 projection weights + lm_head
+        kvbytes = L * ctx * 2 * h * 2            # the cache's K and V (bf16) read by attention
+        hbm, _, _, _ = load_peaks()
+        decode = {"value": 1e3 / wall, "unit": "tokens/s", "ms_per_token": round(wall, 3),
+                  "device_ms_per_token": round(dev_ms, 3), "context_tokens": int(ctx), "steps": D_,
+                  "bytes_per_token": int(wbytes + kvbytes),
+                  "hbm_frac": round((wbytes + kvbytes) / (wall / 1e3) / 1e9 / hbm, 4),
+                  "path": "mpic_prefill_extend of one row at the end of a bf16 cache (decode_step): tcgen05 GEMMs at "
+                          "M = 1 token, tcgen05 attention over the cache; host id in, logits out per token"}
+        del kvd, wsd
+
     # ---- fp32 mode: the same request at the reference's own precision (fp32 weights, KV and
     # arithmetic: SIMT FFMA GEMMs with two-level summation + fp32 online-softmax attention;
     # parity 1e-4 vs the reference in tests/test_gpu_llava.py), device-resident chunks ----
@@ -669,7 +703,7 @@ def run_ours(args, world, rank, local):
         max(sum(gemm_fl.values()) / (tf_sust * 1e12), sum(gemm_b.values()) / (hbm * 1e9)) +
         attn_fl / (tf_sust * 1e12))) * 1e3
     return dict(value=value, ms_per_step=ms_per_step, per_step=per_step, host_ms=host_ms, e2e=e2e,
-                e2e_fp32=e2e_fp32, e2e_disk=e2e_disk, fp32_mode=fp32_mode, k_sweep=sweep,
+                e2e_fp32=e2e_fp32, e2e_disk=e2e_disk, fp32_mode=fp32_mode, k_sweep=sweep, decode=decode,
                 launches=launches, roofline=roofline, phases=per_phase, clocks=clk.summary(),
                 n=n, m=m, floor_ms=floor_ms, world=world)
 
@@ -953,6 +987,8 @@ def main():
     ap.add_argument("--fp32-mode", action="store_true", default=True,
                     help="also time the request in fp32 mode (the reference's precision)")
     ap.add_argument("--no-fp32-mode", dest="fp32_mode", action="store_false")
+    ap.add_argument("--decode-steps", type=int, default=8,
+                    help="decode tokens timed after the prefill (0: skip)")
     ap.add_argument("--no-serving", action="store_true",
                     help="skip the config-E serving key of the default (config C) line")
     ap.add_argument("--cpu-leg", action="store_true", help=argparse.SUPPRESS)
@@ -1078,7 +1114,7 @@ def main():
                                          "KV, weights synthesised from seed 1)",
                 "config": cfg_json,
                 "e2e": r["e2e"], "e2e_fp32_host": r["e2e_fp32"], "e2e_disk": r["e2e_disk"],
-                "fp32_mode": r.get("fp32_mode"), "k_sweep": r.get("k_sweep"),
+                "fp32_mode": r.get("fp32_mode"), "k_sweep": r.get("k_sweep"), "decode": r.get("decode"),
                 "gpu_launches": r["launches"],
                 "roofline": r["roofline"],
                 "request_roofline_frac": round(r["floor_ms"] / r["ms_per_step"], 4),
