@@ -168,6 +168,14 @@ int device() {
     return dev;
 }
 
+mpic_dtype compute_dtype() {
+    static const mpic_dtype dt = [] {
+        const char* e = std::getenv("MPIC_B200_DTYPE");
+        return e && std::string(e) == "bf16" ? MPIC_BF16 : MPIC_F32;
+    }();
+    return dt;
+}
+
 mpic_model_config to_c(const ModelConfig& c) {
     mpic_model_config o{};
     o.n_layers = c.n_layers;
@@ -187,7 +195,7 @@ DeviceModel::DeviceModel(const Model& m) {
     lw.reserve(6 * m.layers.size());
     for (const LayerWeights& l : m.layers)
         for (const std::vector<float>* w : {&l.wq, &l.wk, &l.wv, &l.wo, &l.w1, &l.w2}) lw.push_back(w->data());
-    check(mpic_model_upload(&c, device(), MPIC_F32, m.embedding.data(), m.lm_head.data(), lw.data(), &h_));
+    check(mpic_model_upload(&c, device(), compute_dtype(), m.embedding.data(), m.lm_head.data(), lw.data(), &h_));
 }
 DeviceModel::~DeviceModel() { mpic_model_destroy(h_); }
 
@@ -213,7 +221,7 @@ DeviceKv::DeviceKv(uint32_t layers, uint32_t tokens, uint32_t heads, uint32_t di
             pool.erase(it);
             return;
         }
-    check(mpic_kv_alloc(layers, tokens, heads, dim, MPIC_F32, device(), &h_));
+    check(mpic_kv_alloc(layers, tokens, heads, dim, compute_dtype(), device(), &h_));
 }
 DeviceKv::DeviceKv(const KvTensor& t) : DeviceKv(t.n_layers, t.n_tokens, t.n_heads, t.head_dim) {
     upload(t);

@@ -16,12 +16,17 @@ namespace mpic::b200 {
 // Throws the mpic:: exception class matching an mpic_status (errors.h <-> mpic_b200.h).
 void check(int rc);
 int device();  // MPIC_DEVICE environment variable, default 0
+// Arithmetic of the drop-in API's device copies: fp32 (default: the reference's precision,
+// SIMT kernels, the reference's own tests pass at their 1e-5 bars) or, with
+// MPIC_B200_DTYPE=bf16, bf16 weights and KV — the tcgen05 GEMMs and (head_dim 128) the tcgen05
+// attention, within the bf16 bar (1e-2). Host data stay fp32 either way.
+mpic_dtype compute_dtype();
 
 mpic_model_config to_c(const ModelConfig& c);
 
 class DeviceModel {
 public:
-    explicit DeviceModel(const Model& m);  // uploads the current host weights (fp32)
+    explicit DeviceModel(const Model& m);  // uploads the current host weights (compute_dtype())
     ~DeviceModel();
     DeviceModel(const DeviceModel&) = delete;
     DeviceModel& operator=(const DeviceModel&) = delete;
