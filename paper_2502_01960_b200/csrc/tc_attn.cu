@@ -872,7 +872,11 @@ AttnPlan plan_attention(const uint32_t* rows, uint32_t m, uint32_t n_heads, cons
         const char* e = getenv("MPIC_ATTN_CHUNKS_PER_SM");  // diagnostics: tile-chunks per SM
         return e ? (uint32_t)std::max(1, atoi(e)) : 3u;
     }();
-    uint32_t chunk = (uint32_t)std::max<uint64_t>(2, (total + per_sm * kNumSMs - 1) / (per_sm * kNumSMs));
+    static const uint32_t min_chunk = [] {
+        const char* e = getenv("MPIC_ATTN_MIN_CHUNK");  // diagnostics: shortest split (blocks)
+        return e ? (uint32_t)std::max(1, atoi(e)) : 2u;
+    }();
+    uint32_t chunk = (uint32_t)std::max<uint64_t>(min_chunk, (total + per_sm * kNumSMs - 1) / (per_sm * kNumSMs));
     uint32_t longest = 0, last = 0;
     for (uint32_t t = 0; t < tiles; ++t) {
         longest = std::max(longest, nblk[t] - sblk[t]);
