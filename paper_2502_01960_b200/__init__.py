@@ -74,7 +74,10 @@ class Model:
 
     def close(self):
         if getattr(self, "handle", None):
-            lib().mpic_model_destroy(self.handle)
+            try:
+                lib().mpic_model_destroy(self.handle)
+            except Exception:  # interpreter shutdown: module globals may be gone
+                pass
             self.handle = None
 
     __del__ = close
@@ -125,7 +128,10 @@ class KV:
 
     def close(self):
         if getattr(self, "handle", None):
-            lib().mpic_kv_free(self.handle)
+            try:
+                lib().mpic_kv_free(self.handle)
+            except Exception:  # interpreter shutdown: module globals may be gone
+                pass
             self.handle = None
 
     __del__ = close
@@ -139,7 +145,10 @@ class Workspace:
 
     def close(self):
         if getattr(self, "handle", None):
-            lib().mpic_workspace_destroy(self.handle)
+            try:
+                lib().mpic_workspace_destroy(self.handle)
+            except Exception:  # interpreter shutdown: module globals may be gone
+                pass
             self.handle = None
 
     __del__ = close
