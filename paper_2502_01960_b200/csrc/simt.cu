@@ -310,11 +310,153 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const TQ* __restrict__ q
     }
 }
 
+// fp32 attention, query-tiled (the fp32 mode's hot attention, head_dim 64/128): a CTA takes
+// 16 query rows of one head and streams 64-key blocks of K and V through shared memory once
+// for all 16 rows (the per-row kernel above re-read every key for every row: at config C
+// ~50 GB of L2 traffic per layer). Thread t owns row t / 8 and, per block, the scores of
+// keys t % 8 + 8j (j < 8) and the output dims 32q + 4 (t % 8) + e; online softmax per row
+// over the row's 8 threads (shuffles), causal limit = the row's cache index.
+constexpr uint32_t kTR = 16, kTK = 64;
+template <uint32_t D>
+__global__ void __launch_bounds__(128, 2) attn_simt_tiled_kernel(const float* __restrict__ q,
+                                                                 const float* __restrict__ kk,
+                                                                 const float* __restrict__ vv,
+                                                                 const uint32_t* __restrict__ rows,
+                                                                 uint32_t m, uint32_t h, float inv_sqrt_d,
+                                                                 float* __restrict__ out) {
+    constexpr uint32_t DP = D + 4;           // padded row (16-B aligned, conflict-free float4 reads)
+    constexpr uint32_t ND = D / 32;          // float4 output groups per thread (4 or 2)
+    extern __shared__ float sm_t[];
+    float* Qs = sm_t;                        // [kTR][DP]
+    float* Ks = Qs + kTR * DP;               // [kTK][DP]
+    float* Vs = Ks + kTK * DP;               // [kTK][DP]
+    float* Ps = Vs + kTK * DP;               // [kTR][kTK + 4]
+    __shared__ uint32_t s_maxrow;
+    const uint32_t t = threadIdx.x, r = t >> 3, c = t & 7;
+    const uint32_t i0 = blockIdx.x * kTR, head = blockIdx.y;
+    const size_t hoff = (size_t)head * D;
+    const uint32_t qi = i0 + r;
+    const bool valid = qi < m;
+    const uint32_t limit = valid ? rows[qi] : 0u;  // keys [0, limit] visible
+    if (t == 0) s_maxrow = 0;
+    for (uint32_t x = t; x < kTR * (D / 4); x += 128) {
+        const uint32_t rr = x / (D / 4), d4 = x % (D / 4);
+        const float4 v4 = i0 + rr < m ? __ldg(reinterpret_cast<const float4*>(q + (size_t)(i0 + rr) * h + hoff) + d4)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4*>(Qs + rr * DP + d4 * 4) = v4;
+    }
+    __syncthreads();
+    if (valid && c == 0) atomicMax(&s_maxrow, limit);
+    __syncthreads();
+    const uint32_t nkeys = s_maxrow + 1;
+    float m_run = -INFINITY, l_run = 0.0f;
+    float4 o[ND];
+#pragma unroll
+    for (uint32_t q4 = 0; q4 < ND; ++q4) o[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t k0 = 0; k0 < nkeys; k0 += kTK) {
+        const uint32_t nk = min(kTK, nkeys - k0);
+        for (uint32_t x = t; x < kTK * (D / 4); x += 128) {
+            const uint32_t kr = x / (D / 4), d4 = x % (D / 4);
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+            if (kr < nk) {
+                a = __ldg(reinterpret_cast<const float4*>(kk + (size_t)(k0 + kr) * h + hoff) + d4);
+                b = __ldg(reinterpret_cast<const float4*>(vv + (size_t)(k0 + kr) * h + hoff) + d4);
+            }
+            *reinterpret_cast<float4*>(Ks + kr * DP + d4 * 4) = a;
+            *reinterpret_cast<float4*>(Vs + kr * DP + d4 * 4) = b;
+        }
+        __syncthreads();
+        float sc[8];
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) sc[j] = 0.0f;
+#pragma unroll 4
+        for (uint32_t d4 = 0; d4 < D / 4; ++d4) {
+            const float4 qv = *reinterpret_cast<const float4*>(Qs + r * DP + d4 * 4);
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                const float4 kv = *reinterpret_cast<const float4*>(Ks + (c + 8 * j) * DP + d4 * 4);
+                sc[j] = fmaf(qv.x, kv.x, sc[j]);
+                sc[j] = fmaf(qv.y, kv.y, sc[j]);
+                sc[j] = fmaf(qv.z, kv.z, sc[j]);
+                sc[j] = fmaf(qv.w, kv.w, sc[j]);
+            }
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            const uint32_t kg = k0 + c + 8 * j;
+            sc[j] = valid && kg <= limit ? sc[j] * inv_sqrt_d : -INFINITY;
+            mx = fmaxf(mx, sc[j]);
+        }
+#pragma unroll
+        for (uint32_t off = 1; off < 8; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        const float m_new = fmaxf(m_run, mx);
+        const float alpha = m_new == -INFINITY ? 1.0f : expf(m_run - m_new);
+        float ls = 0.0f;
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            const float pj = sc[j] == -INFINITY ? 0.0f : expf(sc[j] - m_new);
+            Ps[r * (kTK + 4) + c + 8 * j] = pj;
+            ls += pj;
+        }
+#pragma unroll
+        for (uint32_t off = 1; off < 8; off <<= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
+        l_run = l_run * alpha + ls;
+        m_run = m_new;
+#pragma unroll
+        for (uint32_t q4 = 0; q4 < ND; ++q4) {
+            o[q4].x *= alpha;
+            o[q4].y *= alpha;
+            o[q4].z *= alpha;
+            o[q4].w *= alpha;
+        }
+        __syncwarp();  // Ps rows are written and read by the same warp (row r's 8 threads)
+#pragma unroll 4
+        for (uint32_t kr = 0; kr < nk; ++kr) {
+            const float pk = Ps[r * (kTK + 4) + kr];
+#pragma unroll
+            for (uint32_t q4 = 0; q4 < ND; ++q4) {
+                const float4 vv4 = *reinterpret_cast<const float4*>(Vs + kr * DP + 32 * q4 + 4 * c);
+                o[q4].x = fmaf(pk, vv4.x, o[q4].x);
+                o[q4].y = fmaf(pk, vv4.y, o[q4].y);
+                o[q4].z = fmaf(pk, vv4.z, o[q4].z);
+                o[q4].w = fmaf(pk, vv4.w, o[q4].w);
+            }
+        }
+        __syncthreads();  // K/V tiles are reloaded next
+    }
+    if (!valid) return;
+    const float inv = l_run > 0.0f ? 1.0f / l_run : 0.0f;
+#pragma unroll
+    for (uint32_t q4 = 0; q4 < ND; ++q4)
+        *reinterpret_cast<float4*>(out + (size_t)qi * h + hoff + 32 * q4 + 4 * c) =
+            make_float4(o[q4].x * inv, o[q4].y * inv, o[q4].z * inv, o[q4].w * inv);
+}
+
+template <uint32_t D>
+static void launch_tiled(const float* q, const float* k, const float* v, const uint32_t* rows, uint32_t m,
+                         uint32_t H, float* out, cudaStream_t s) {
+    const size_t smem = ((size_t)(kTR + 2 * kTK) * (D + 4) + kTR * (kTK + 4)) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+        MPIC_CUDA(cudaFuncSetAttribute(attn_simt_tiled_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    attn_simt_tiled_kernel<D><<<dim3(ceil_div(m, kTR), H), 128, smem, s>>>(q, k, v, rows, m, H * D,
+                                                                            1.0f / sqrtf((float)D), out);
+}
+
 void launch_attn_simt(const void* q, const void* k, const void* v, mpic_dtype dt,
                       const uint32_t* rows, uint32_t m, uint32_t H, uint32_t D, void* out,
                       cudaStream_t s, float* capture, uint32_t T) {
     const uint32_t h = H * D;
     const float inv_sqrt_d = 1.0f / sqrtf((float)D);
+    if (dt == MPIC_F32 && !capture && (D == 128 || D == 64)) {
+        if (D == 128) launch_tiled<128>((const float*)q, (const float*)k, (const float*)v, rows, m, H, (float*)out, s);
+        else launch_tiled<64>((const float*)q, (const float*)k, (const float*)v, rows, m, H, (float*)out, s);
+        MPIC_LAUNCHED();
+        return;
+    }
     dim3 grid(m, H);
     if (dt == MPIC_F32)
         attn_simt_kernel<float, float, float><<<grid, 128, 0, s>>>(
