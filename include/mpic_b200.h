@@ -324,7 +324,9 @@ int mpic_host_free(void* p);
 /* Test hook: out[M][N] (fp32, device) = A[M][K] . W[N][K]^T for bf16 device operands,
  * through the tcgen05 GEMM (path 1), the tcgen05 GEMM on a blocked copy of W made on the
  * device (path 2), the tcgen05 GEMM with d_w already blocked [N/128][K/64][128][64]
- * (path 3) or the SIMT GEMM (path 0). Async on `stream`. */
+ * (path 3) or the SIMT GEMM (path 0); for fp32 device operands, the fp32 mode's 3xTF32
+ * tcgen05 GEMM (path 4, operands split on the device) or the SIMT FFMA GEMM (path 5).
+ * Async on `stream`. */
 int mpic_test_gemm(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uint32_t K, int path,
                    float* d_out, void* stream);
 /* Test hook: the tcgen05 GEMM with a fused epilogue. mode 0: residual (d_x fp32 [M][N]

@@ -128,6 +128,9 @@ struct mpic_model_s {
     // head-parallel slice (mpic_model_create_heads): attention weights of heads
     // [head0, head0 + n_local_heads) only; 0 local heads = the whole model
     uint32_t head0 = 0, n_local_heads = 0;
+    // fp32 mode on the tensor cores (3xTF32): the tf32 hi / lo split of every projection
+    // weight, keyed by the weight's pointer (weights are immutable after creation)
+    std::unordered_map<const void*, std::pair<float*, float*>> x3w;
 };
 
 struct mpic_kv_s {
@@ -176,6 +179,7 @@ struct mpic_workspace_s {
     void* ffn = nullptr;                // [m_pad][4h] dtype
     float* d_logits = nullptr;          // [V]
     float* partial = nullptr;           // split-K partials [8][m_pad][h]
+    float* x3buf = nullptr;             // fp32 mode, 3xTF32: tf32 hi / lo split of a GEMM's A [2][m_pad][4h]
     size_t partial_cap = 0;
     int32_t* h_ids = nullptr;           // pinned staging
     uint32_t* h_rows = nullptr;
@@ -304,7 +308,40 @@ void free_model(mpic_model_t m) {
     cudaFree(m->inv_freq);
     cudaFree(m->rope);
     for (auto* p : m->retired) cudaFree(p);
+    for (auto& kv : m->x3w) {
+        cudaFree(kv.second.first);
+        cudaFree(kv.second.second);
+    }
     delete m;
+}
+
+// fp32 projections on the tensor cores (3xTF32, tc_pgemm.cu) unless MPIC_F32_GEMM=simt
+// selects the SIMT FFMA GEMM (simt.cu).
+bool f32_tensor_gemm() {
+    static const bool on = [] {
+        const char* e = getenv("MPIC_F32_GEMM");
+        return !(e && std::string(e) == "simt");
+    }();
+    return on;
+}
+
+// Split every projection weight of an fp32 model whose shape the 3xTF32 GEMM takes.
+void prepare_x3(mpic_model_t m, cudaStream_t s) {
+    if (m->dtype != MPIC_F32 || !f32_tensor_gemm() || m->n_local_heads) return;
+    const size_t h = m->cfg.hidden_dim;
+    auto split = [&](const void* w, size_t N, size_t K) {
+        if (!pgemm_x3_supported(1, (uint32_t)N, (uint32_t)K)) return;
+        float* hi = dmalloc<float>(N * K);
+        float* lo = dmalloc<float>(N * K);
+        launch_tf32_split(static_cast<const float*>(w), hi, lo, N * K, s);
+        m->x3w[w] = {hi, lo};
+    };
+    for (size_t l = 0; l < m->cfg.n_layers; ++l) {
+        split(m->wqkv[l], 3 * h, h);
+        split(m->wo[l], h, h);
+        split(m->w1[l], 4 * h, h);
+        split(m->w2[l], h, 4 * h);
+    }
 }
 
 void alloc_model(mpic_model_t m) {
@@ -399,9 +436,11 @@ void download_cast(float* dst, const void* src, mpic_dtype dt, size_t n, cudaStr
     cudaFree(tmp);
 }
 
-// One projection GEMM with its fused epilogue; tcgen05 for bf16, SIMT FFMA for fp32.
+// One projection GEMM with its fused epilogue: tcgen05 for bf16; for fp32, 3xTF32 tcgen05
+// when the weight has its split and the caller passes split scratch for A (x3buf: 2 x M x K
+// floats), else SIMT FFMA.
 void run_gemm(mpic_model_t md, const void* A, const void* W, uint32_t M, uint32_t N, uint32_t K,
-              const EpiParams& ep, cudaStream_t s) {
+              const EpiParams& ep, cudaStream_t s, float* x3buf = nullptr) {
     if (md->dtype == MPIC_BF16) {
         if (tc_gemm_supported(M, N, K) && (ep.mode != EPI_QKV || md->cfg.head_dim % 32 == 0)) {
             launch_gemm_tc(static_cast<const __nv_bfloat16*>(A), K,
@@ -412,6 +451,16 @@ void run_gemm(mpic_model_t md, const void* A, const void* W, uint32_t M, uint32_
         e2.split_k = 1;
         launch_gemm_simt(A, MPIC_BF16, K, W, MPIC_BF16, M, N, K, e2, MPIC_BF16, s);
         return;
+    }
+    if (x3buf && pgemm_x3_supported(M, N, K)) {
+        const auto it = md->x3w.find(W);
+        if (it != md->x3w.end()) {
+            float* a_hi = x3buf;
+            float* a_lo = x3buf + (size_t)M * K;
+            launch_tf32_split(static_cast<const float*>(A), a_hi, a_lo, (size_t)M * K, s);
+            launch_pgemm_x3(a_hi, a_lo, it->second.first, it->second.second, M, N, K, ep, s);
+            return;
+        }
     }
     launch_gemm_simt(A, MPIC_F32, K, W, MPIC_F32, M, N, K, ep, MPIC_F32, s);
 }
@@ -596,7 +645,7 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
         qkv.head_dim = D;
         {
             ProfScope ps(s, MPIC_PHASE_QKV);
-            run_gemm(md, bf ? (const void*)ws->xb : (const void*)ws->x, md->wqkv[l], m, 3 * h, h, qkv, s);
+            run_gemm(md, bf ? (const void*)ws->xb : (const void*)ws->x, md->wqkv[l], m, 3 * h, h, qkv, s, ws->x3buf);
         }
         {
             ProfScope ps(s, MPIC_PHASE_ATTN);
@@ -624,7 +673,7 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
         }
         {
             ProfScope ps(s, MPIC_PHASE_WO);
-            run_gemm(md, ws->attn, md->wo[l], m, h, h, res, s);
+            run_gemm(md, ws->attn, md->wo[l], m, h, h, res, s, ws->x3buf);
         }
 
         EpiParams gl;
@@ -633,11 +682,11 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
         gl.ldo = 4 * h;
         {
             ProfScope ps(s, MPIC_PHASE_W1);
-            run_gemm(md, bf ? (const void*)ws->xb : (const void*)ws->x, md->w1[l], m, 4 * h, h, gl, s);
+            run_gemm(md, bf ? (const void*)ws->xb : (const void*)ws->x, md->w1[l], m, 4 * h, h, gl, s, ws->x3buf);
         }
         {
             ProfScope ps(s, MPIC_PHASE_W2);
-            run_gemm(md, ws->ffn, md->w2[l], m, h, 4 * h, res, s);
+            run_gemm(md, ws->ffn, md->w2[l], m, h, 4 * h, res, s, ws->x3buf);
         }
     }
     {
@@ -1138,6 +1187,7 @@ int mpic_model_create(const mpic_model_config* cfg, int device, mpic_dtype dtype
         launch_synth(cfg->seed, 6, l, 4 * h * h, scale, m->w2[l], dtype, s);
     }
     ensure_rope(m, 1, s);
+    prepare_x3(m, s);
     MPIC_CUDA(cudaDeviceSynchronize());
     *out = m;
     m = nullptr;
@@ -1168,6 +1218,8 @@ int mpic_model_upload(const mpic_model_config* cfg, int device, mpic_dtype dtype
         }
     }
     ensure_rope(m, 1, s);
+    prepare_x3(m, s);
+    MPIC_CUDA(cudaDeviceSynchronize());
     *out = m;
     m = nullptr;
     API_END
@@ -1375,6 +1427,7 @@ int mpic_workspace_create(mpic_model_t md, uint32_t max_rows, uint32_t max_ctx, 
         ws->partial_cap = 8 * mp * h;
         ws->partial = dmalloc<float>(ws->partial_cap);
     }
+    if (!md->x3w.empty()) ws->x3buf = dmalloc<float>(2 * mp * 4 * h);
     MPIC_CUDA(cudaMallocHost(&ws->h_ids, mp * 4));
     MPIC_CUDA(cudaMallocHost(&ws->h_rows, mp * 4));
     MPIC_CUDA(cudaMallocHost(&ws->h_pos, mp * 4));
@@ -1398,6 +1451,7 @@ int mpic_workspace_destroy(mpic_workspace_t ws) {
         cudaFree(ws->x); cudaFree(ws->rope_tok); cudaFree(ws->xb); cudaFree(ws->q); cudaFree(ws->attn); cudaFree(ws->ffn);
         cudaFree(ws->d_logits);
         cudaFree(ws->partial);
+        cudaFree(ws->x3buf);
         cudaFreeHost(ws->h_ids); cudaFreeHost(ws->h_rows); cudaFreeHost(ws->h_pos); cudaFreeHost(ws->h_start);
         cudaFreeHost(ws->h_logits);
         for (int i = 0; i < 2; ++i) {
@@ -2840,6 +2894,19 @@ int mpic_test_gemm(const void* d_a, const void* d_w, uint32_t M, uint32_t N, uin
         launch_block_weights(static_cast<const __nv_bfloat16*>(d_w), wb, N, K, true, s);
         launch_gemm_tc(static_cast<const __nv_bfloat16*>(d_a), K, wb, M, N, K, ep, s, true);
         MPIC_CUDA(cudaFreeAsync(wb, s));
+    } else if (path == 4 || path == 5) {  // fp32 operands: 4 = 3xTF32 pair gemm, 5 = SIMT FFMA
+        if (path == 5) {
+            launch_gemm_simt(d_a, MPIC_F32, K, d_w, MPIC_F32, M, N, K, ep, MPIC_F32, s);
+        } else {
+            MPIC_REQUIRE(pgemm_x3_supported(M, N, K), MPIC_ERR_VALIDATION, "shape not supported by the 3xTF32 gemm");
+            float* buf = nullptr;
+            const size_t na = (size_t)M * K, nw = (size_t)N * K;
+            MPIC_CUDA(cudaMallocAsync((void**)&buf, (2 * na + 2 * nw) * 4, s));
+            launch_tf32_split(static_cast<const float*>(d_a), buf, buf + na, na, s);
+            launch_tf32_split(static_cast<const float*>(d_w), buf + 2 * na, buf + 2 * na + nw, nw, s);
+            launch_pgemm_x3(buf, buf + na, buf + 2 * na, buf + 2 * na + nw, M, N, K, ep, s);
+            MPIC_CUDA(cudaFreeAsync(buf, s));
+        }
     } else {
         launch_gemm_simt(d_a, MPIC_BF16, K, d_w, MPIC_BF16, M, N, K, ep, MPIC_BF16, s);
     }

@@ -178,6 +178,13 @@ void launch_gemm_tc(const __nv_bfloat16* A, uint32_t lda, const __nv_bfloat16* W
 bool pgemm_supported(uint32_t M, uint32_t N, uint32_t K);
 void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint32_t N, uint32_t K,
                   const EpiParams& ep, cudaStream_t s, bool w_blocked = false);
+// fp32 mode on the tensor cores (3xTF32): operands pre-split by launch_tf32_split, fp32
+// epilogue outputs. N % 256 == 0, K % 32 == 0.
+bool pgemm_x3_supported(uint32_t M, uint32_t N, uint32_t K);
+void launch_pgemm_x3(const float* A_hi, const float* A_lo, const float* W_hi, const float* W_lo, uint32_t M,
+                     uint32_t N, uint32_t K, const EpiParams& ep, cudaStream_t s);
+// hi = tf32_rna(x), lo = tf32_rna(x - hi) over n floats (n % 4 == 0, 16-B aligned).
+void launch_tf32_split(const float* x, float* hi, float* lo, size_t n, cudaStream_t s);
 // MPIC_PG_TS diagnostics of the last pair GEMM's CTA 0: 5 x %globaltimer ns (entry, after
 // prologue, MMAs issued, epilogue done, exit), then clock64 cycles: producer waiting on
 // empty slots / producer total / MMA issuer waiting on full slots / MMA issuer total.

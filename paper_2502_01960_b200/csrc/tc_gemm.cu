@@ -496,11 +496,12 @@ struct MapKeyHash {
 
 // 2-D bf16 tensor map, row-major [outer][inner], SWIZZLE_128B box {box_inner, box_outer}.
 // Maps are cached by (pointer, shape, box); buffers are long-lived (weights, workspace).
-CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                           uint32_t box_outer) {
+namespace {
+CUtensorMap make_tmap_2d(const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner, uint32_t box_outer,
+                         bool f32) {
     static std::mutex mu;
     static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-    const MapKey key{ptr, inner, outer, box_inner, box_outer};
+    const MapKey key{ptr, inner | (f32 ? 1ull << 63 : 0ull), outer, box_inner, box_outer};
     {
         std::lock_guard<std::mutex> lk(mu);
         auto it = cache.find(key);
@@ -508,17 +509,28 @@ CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t outer, uint
     }
     CUtensorMap m;
     const cuuint64_t dims[2] = {inner, outer};
-    const cuuint64_t strides[1] = {inner * 2};
+    const cuuint64_t strides[1] = {inner * (f32 ? 4 : 2)};
     const cuuint32_t box[2] = {box_inner, box_outer};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
-                                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    const CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     MPIC_REQUIRE(r == CUDA_SUCCESS, MPIC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     std::lock_guard<std::mutex> lk(mu);
     cache.emplace(key, m);
     return m;
+}
+}  // namespace
+
+CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                           uint32_t box_outer) {
+    return make_tmap_2d(ptr, inner, outer, box_inner, box_outer, false);
+}
+// fp32 [outer][inner] (the 3xTF32 GEMM operands): box_inner = 32 elements = one 128-B row
+CUtensorMap make_tmap_f32(const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                          uint32_t box_outer) {
+    return make_tmap_2d(ptr, inner, outer, box_inner, box_outer, true);
 }
 
 bool tc_gemm_supported(uint32_t M, uint32_t N, uint32_t K) {

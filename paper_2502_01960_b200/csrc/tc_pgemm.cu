@@ -35,6 +35,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include <unordered_map>
 
 #include "common.cuh"
@@ -46,6 +47,8 @@ namespace mpicb {
 
 CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
                            uint32_t box_outer);
+CUtensorMap make_tmap_f32(const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                          uint32_t box_outer);
 
 namespace {
 
@@ -83,6 +86,10 @@ struct PgArgs {
     uint32_t prologue_pf;  // prefetch the first k-blocks' weights into L2 before the PDL wait
     uint32_t stg_off;    // staged epilogue stores: byte offset of the 8 x 4 KB warp slices in the
                          // (then idle) stage ring, or kNoStage
+    uint32_t kel;        // K elements per k-block (one 128-B operand row): 64 bf16, 32 fp32 (3xTF32)
+    uint32_t wsub;       // weight bytes of a k-block: 16 KB, 32 KB with the 3xTF32 hi and lo tiles
+    uint32_t xlo;        // 3xTF32: byte offset of the token rows' lo tile from their hi tile
+    uint32_t segn;       // 3xTF32: stage iterations per accumulation segment (see the kernel)
     EpiParams ep;
 };
 
@@ -134,6 +141,13 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
 // Residual add of a transposed chunk (lane -> token 4i + lane/8, features 4*(lane%8) ..+4 of
 // the warp's 32): x += v, xb = bf16(x). One instruction covers 4 whole 128-B x rows.
 // `part(i)` returns the fp32 sum for read-back step i.
+template <typename T>
+__device__ __forceinline__ T to_out(float v);
+template <>
+__device__ __forceinline__ float to_out<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
 template <class Part>
 __device__ __forceinline__ void resid_rows(const EpiParams& ep, uint32_t n, uint32_t tb, uint32_t f0, uint32_t lane,
                                            Part part) {
@@ -166,12 +180,15 @@ __device__ __forceinline__ void resid_rows(const EpiParams& ep, uint32_t n, uint
     }
 }
 
-template <int MODE>
+// F32 (3xTF32 fp32 mode): fp32 outputs (q, K/V cache rows, FFN activations) and the exact
+// GELU, as the SIMT fp32 GEMM's epilogue (simt.cu epi_pair); direct stores only.
+template <int MODE, bool F32 = false>
 __device__ __forceinline__ void pg_epi(const EpiParams& ep, uint32_t M, uint32_t tb, uint32_t f, uint32_t lane,
                                        const uint32_t (&r)[32], const uint32_t* s_rows, const float2* s_rope,
                                        uint32_t tg, uint8_t* stg = nullptr) {
+    using TO = typename std::conditional<F32, float, __nv_bfloat16>::type;
     const uint32_t n = min(32u, M - tb);  // valid tokens in this chunk
-    if (stg) {
+    if (!F32 && stg) {
         __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(stg);
         const uint32_t f0 = f - lane;  // the warp's first feature
         if constexpr (MODE == EPI_RESID) {
@@ -261,7 +278,7 @@ __device__ __forceinline__ void pg_epi(const EpiParams& ep, uint32_t M, uint32_t
         // adjacent lanes), k/v scattered to the cache row kv_rows[t]
         const uint32_t h = ep.hidden, part = f / h, d = f - part * h;
         const uint32_t hd2 = ep.head_dim >> 1, pr = (d % ep.head_dim) >> 1;
-        __nv_bfloat16* base = static_cast<__nv_bfloat16*>(part == 0 ? ep.q : part == 1 ? ep.kv_k : ep.kv_v) + d;
+        TO* base = static_cast<TO*>(part == 0 ? ep.q : part == 1 ? ep.kv_k : ep.kv_v) + d;
         const bool odd = lane & 1;
         if (part == 2) {  // V: no rotation
 #pragma unroll
@@ -269,7 +286,7 @@ __device__ __forceinline__ void pg_epi(const EpiParams& ep, uint32_t M, uint32_t
                 if (j >= n) continue;
                 const uint32_t t = tb + j;
                 const uint32_t row = s_rows ? s_rows[t - tg] : __ldg(ep.kv_rows + t);
-                base[(size_t)row * h] = __float2bfloat16_rn(__uint_as_float(r[j]));
+                base[(size_t)row * h] = to_out<TO>(__uint_as_float(r[j]));
             }
             return;
         }
@@ -289,14 +306,14 @@ __device__ __forceinline__ void pg_epi(const EpiParams& ep, uint32_t M, uint32_t
                                         : __ldg(ep.rope + (size_t)__ldg(ep.rope_pos + t) * hd2 + pr);
                 }
             }
-            __nv_bfloat16 o[16];
+            TO o[16];
 #pragma unroll
             for (uint32_t j = 0; j < 16; ++j) {
                 const float val = __uint_as_float(r[j0 + j]);
                 const float vp = __shfl_xor_sync(0xffffffffu, val, 1);
                 float x0 = odd ? vp : val, x1 = odd ? val : vp;
                 rope_pair(x0, x1, cs[j].x, cs[j].y);
-                o[j] = __float2bfloat16_rn(odd ? x1 : x0);
+                o[j] = to_out<TO>(odd ? x1 : x0);
             }
             if (j0 + 16 <= n) {
 #pragma unroll
@@ -331,29 +348,37 @@ __device__ __forceinline__ void pg_epi(const EpiParams& ep, uint32_t M, uint32_t
             }
         }
     } else if constexpr (MODE == EPI_GELU) {
-        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + (size_t)tb * ep.ldo + f;
+        TO* o = static_cast<TO*>(ep.out) + (size_t)tb * ep.ldo + f;
 #pragma unroll
         for (uint32_t j = 0; j < 32; ++j)
-            if (j < n) o[(size_t)j * ep.ldo] = __float2bfloat16_rn(gelu_fast(__uint_as_float(r[j])));
+            if (j < n)
+                o[(size_t)j * ep.ldo] = F32 ? to_out<TO>(gelu_ref(__uint_as_float(r[j])))
+                                            : to_out<TO>(gelu_fast(__uint_as_float(r[j])));
     } else if constexpr (MODE == EPI_STORE_F32) {
         float* o = static_cast<float*>(ep.out) + (size_t)tb * ep.ldo + f;
 #pragma unroll
         for (uint32_t j = 0; j < 32; ++j)
             if (j < n) o[(size_t)j * ep.ldo] = __uint_as_float(r[j]);
     } else {
-        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + (size_t)tb * ep.ldo + f;
+        TO* o = static_cast<TO*>(ep.out) + (size_t)tb * ep.ldo + f;
 #pragma unroll
         for (uint32_t j = 0; j < 32; ++j)
-            if (j < n) o[(size_t)j * ep.ldo] = __float2bfloat16_rn(__uint_as_float(r[j]));
+            if (j < n) o[(size_t)j * ep.ldo] = to_out<TO>(__uint_as_float(r[j]));
     }
 }
 
 // One instantiation per epilogue mode: the kernel's epilogue runs once, at the end, from a
 // cold instruction cache, so each instantiation carries only its own (unrolled) epilogue.
-template <int MODE>
+// X3: the fp32 mode's 3xTF32 GEMM. Operands are pre-split into tf32-rounded hi and lo parts
+// (x = hi + lo to ~2^-22, tf32_split_kernel), a k-block is 32 fp32 (one 128-B row, so the
+// smem descriptors are the bf16 ones) and each K = 8 step issues lo*hi + hi*lo + hi*hi
+// into the fp32 TMEM accumulator (lo*lo, ~2^-22 relative, is dropped).
+template <int MODE, bool X3>
 __global__ void __launch_bounds__(kPgThreads, 1)
     tc_pgemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX0,
-                    const __grid_constant__ CUtensorMap tmX1, const PgArgs a) {
+                    const __grid_constant__ CUtensorMap tmX1, const __grid_constant__ CUtensorMap tmWl,
+                    const __grid_constant__ CUtensorMap tmX0l, const __grid_constant__ CUtensorMap tmX1l,
+                    const PgArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * a.stage_bytes);
@@ -378,6 +403,11 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         tc::tma_prefetch_desc(&tmW);
         tc::tma_prefetch_desc(&tmX0);
         tc::tma_prefetch_desc(&tmX1);
+        if (X3) {
+            tc::tma_prefetch_desc(&tmWl);
+            tc::tma_prefetch_desc(&tmX0l);
+            tc::tma_prefetch_desc(&tmX1l);
+        }
         for (uint32_t s = 0; s < a.stages; ++s) {
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&empty[s], 1);
@@ -409,8 +439,8 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         if (lane == 0) {
             const uint64_t pol_w = a.w_evict_first ? tc::policy_evict_first() : tc::policy_evict_last();
             const uint64_t pol_x = tc::policy_evict_last();
-            const uint32_t xbytes = (a.dbg & 2) ? 0u : a.sub_bytes - kPgWBytes;
-            const uint32_t wbytes = (a.dbg & 4) ? 0u : kPgWBytes;
+            const uint32_t xbytes = (a.dbg & 2) ? 0u : a.sub_bytes - a.wsub;
+            const uint32_t wbytes = (a.dbg & 4) ? 0u : a.wsub;
             const int xr0 = (int)(rank * (a.P0 / 2)), xr1 = (int)(a.P0 + rank * (a.P1 / 2));
             long long pw = 0;
             const long long p0 = clock64();
@@ -428,7 +458,8 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                     const uint32_t bar = leader_full + s * 8;
                     for (uint32_t j = 0; j < nsub; ++j) {
                         uint8_t* st = smem + s * a.stage_bytes + j * a.sub_bytes;
-                        const int k = (int)((kb + j) * 64);
+                        const int k = (int)((kb + j) * a.kel);
+                        if (X3 && wbytes) tc::tma_load_2d_cg2(st + kPgWBytes, &tmWl, bar, k, w_row, pol_w);
                         if (wbytes) {
                             if (a.w_blocked)  // one contiguous 16 KB tile per box
                                 tc::tma_load_2d_cg2(st, &tmW, bar, 0, (int)(((2 * fb + rank) * a.kblocks + kb + j) * 128),
@@ -450,8 +481,13 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                                                     a.w_blocked ? (int)(((2 * fp + rank) * a.kblocks + kp) * 128)
                                                                 : (int)(fp * 256 + rank * 128));
                         }
-                        if (xbytes) tc::tma_load_2d_cg2(st + kPgWBytes, &tmX0, bar, k, t0 + xr0, pol_x);
-                        if (xbytes && a.P1) tc::tma_load_2d_cg2(st + kPgWBytes + a.xoff1, &tmX1, bar, k, t0 + xr1, pol_x);
+                        if (xbytes) tc::tma_load_2d_cg2(st + a.wsub, &tmX0, bar, k, t0 + xr0, pol_x);
+                        if (xbytes && a.P1) tc::tma_load_2d_cg2(st + a.wsub + a.xoff1, &tmX1, bar, k, t0 + xr1, pol_x);
+                        if (X3 && xbytes) {
+                            tc::tma_load_2d_cg2(st + a.wsub + a.xlo, &tmX0l, bar, k, t0 + xr0, pol_x);
+                            if (a.P1)
+                                tc::tma_load_2d_cg2(st + a.wsub + a.xlo + a.xoff1, &tmX1l, bar, k, t0 + xr1, pol_x);
+                        }
                     }
                     if (++s == a.stages) { s = 0; ph ^= 1; }
                 }
@@ -468,20 +504,37 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         // lane issues each k-block's MMAs back to back. (A lone issuing thread wrapped every
         // tcgen05.mma in an elect/broadcast loop: ~15 instructions of issue overhead per MMA.)
         if (rank == 0) {
-            const uint32_t idesc0 = tc::idesc_bf16(256, a.P0);
-            const uint32_t idesc1 = tc::idesc_bf16(256, a.P1 ? a.P1 : 16);
-            uint32_t item = 0, s = 0, ph = 0;
+            const uint32_t idesc0 = X3 ? tc::idesc_tf32(256, a.P0) : tc::idesc_bf16(256, a.P0);
+            const uint32_t idesc1 = X3 ? tc::idesc_tf32(256, a.P1 ? a.P1 : 16) : tc::idesc_bf16(256, a.P1 ? a.P1 : 16);
+            uint32_t item = 0, s = 0, ph = 0, seg = 0;
             long long mw = 0;
             const long long m0 = clock64();
             for (uint32_t tile = cl; tile < a.tiles; tile += a.clusters, ++item) {
-                const uint32_t b = a.nbuf == 2 ? (item & 1) : 0u;
+                uint32_t b = a.nbuf == 2 ? (item & 1) : 0u;
                 const uint32_t use = a.nbuf == 2 ? (item >> 1) : item;
-                if (lane == 0) tc::mbar_wait_cluster(&acc_empty[b], (use & 1) ^ 1);
-                __syncwarp();
-                tc::tc_fence_after();
-                const uint32_t d = tmem + b * a.G;
-                for (uint32_t kb = kb0; kb < kb1; kb += a.kps) {
+                if (!X3) {
+                    if (lane == 0) tc::mbar_wait_cluster(&acc_empty[b], (use & 1) ^ 1);
+                    __syncwarp();
+                    tc::tc_fence_after();
+                }
+                uint32_t d = tmem + b * a.G;
+                uint32_t it = 0;
+                for (uint32_t kb = kb0; kb < kb1; kb += a.kps, ++it) {
                     const uint32_t nsub = min(a.kps, kb1 - kb);
+                    // 3xTF32: the tile's k range is accumulated in segments of segn stage
+                    // iterations, alternating between the two TMEM buffers; the epilogue warps
+                    // drain each finished segment into fp32 register sums (round to nearest).
+                    // The tensor core rounds its accumulation toward zero, so one chain over
+                    // all of K (3 x K/8 instructions) biases the result by ~K/16 ulp.
+                    const bool seg_first = X3 && it % a.segn == 0;
+                    const bool seg_last = X3 && ((it + 1) % a.segn == 0 || kb + a.kps >= kb1);
+                    if (seg_first) {
+                        b = seg & 1;
+                        d = tmem + b * a.G;
+                        if (lane == 0) tc::mbar_wait_cluster(&acc_empty[b], ((seg >> 1) & 1) ^ 1);
+                        __syncwarp();
+                        tc::tc_fence_after();
+                    }
                     const long long w0 = ts ? clock64() : 0;
                     if (lane == 0) tc::mbar_wait(&full[s], ph);
                     __syncwarp();
@@ -490,22 +543,37 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                     if (tc::elect_one_sync()) {
                         for (uint32_t j = 0; j < nsub && !(a.dbg & 8); ++j) {
                             const uint32_t w_base = tc::smem_u32(smem + s * a.stage_bytes + j * a.sub_bytes);
-                            const uint32_t x_base = w_base + kPgWBytes;
+                            const uint32_t x_base = w_base + a.wsub;
 #pragma unroll
                             for (uint32_t kk = 0; kk < 4; ++kk) {
                                 const uint64_t adesc = tc::desc_k_sw128(w_base + kk * 32);
-                                const uint32_t acc = (kb + j > kb0 || kk > 0) ? 1u : 0u;
-                                tc::mma_bf16_pair(d, adesc, tc::desc_k_sw128(x_base + kk * 32), idesc0, acc);
-                                if (a.P1)
-                                    tc::mma_bf16_pair(d + a.P0, adesc, tc::desc_k_sw128(x_base + a.xoff1 + kk * 32),
-                                                      idesc1, acc);
+                                const uint32_t acc = (X3 ? (!seg_first || j > 0) : kb + j > kb0) || kk > 0 ? 1u : 0u;
+                                if constexpr (X3) {
+                                    const uint64_t alo = tc::desc_k_sw128(w_base + kPgWBytes + kk * 32);
+#pragma unroll
+                                    for (uint32_t pc = 0; pc < 2; ++pc) {
+                                        if (pc && !a.P1) break;
+                                        const uint32_t xo = pc ? a.xoff1 : 0u, dd = pc ? d + a.P0 : d;
+                                        const uint32_t id = pc ? idesc1 : idesc0;
+                                        tc::mma_tf32_pair(dd, alo, tc::desc_k_sw128(x_base + xo + kk * 32), id, acc);
+                                        tc::mma_tf32_pair(dd, adesc, tc::desc_k_sw128(x_base + a.xlo + xo + kk * 32), id, 1u);
+                                        tc::mma_tf32_pair(dd, adesc, tc::desc_k_sw128(x_base + xo + kk * 32), id, 1u);
+                                    }
+                                } else {
+                                    tc::mma_bf16_pair(d, adesc, tc::desc_k_sw128(x_base + kk * 32), idesc0, acc);
+                                    if (a.P1)
+                                        tc::mma_bf16_pair(d + a.P0, adesc, tc::desc_k_sw128(x_base + a.xoff1 + kk * 32),
+                                                          idesc1, acc);
+                                }
                             }
                         }
                         tc::mma_commit_pair_mcast(&empty[s], pair_mask);
+                        if (seg_last) tc::mma_commit_pair_mcast(&acc_full[b], pair_mask);
                     }
+                    if (seg_last) ++seg;
                     if (++s == a.stages) { s = 0; ph ^= 1; }
                 }
-                if (tc::elect_one_sync()) tc::mma_commit_pair_mcast(&acc_full[b], pair_mask);
+                if (!X3 && tc::elect_one_sync()) tc::mma_commit_pair_mcast(&acc_full[b], pair_mask);
                 if (ts && lane == 0) ts[2] = gtimer();
             }
             if (ts && lane == 0) {
@@ -522,17 +590,83 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         const uint32_t row = q * 32 + lane;
         const uint32_t lane_off = (q * 32u) << 16;
         const uint32_t acc_empty_leader = tc::mapa_shared(tc::smem_u32(&acc_empty[0]), crank & ~1u);
-        uint32_t item = 0;
+        uint32_t item = 0, seg = 0;
         for (uint32_t tile = cl; tile < a.tiles; tile += a.clusters, ++item) {
             const uint32_t fb = tile / a.ngroups, g = tile % a.ngroups;
             const uint32_t f = fb * 256 + rank * 128 + row;
             const uint32_t tg = g * a.G;
             const uint32_t tend = min(a.M, tg + a.G);  // tokens of this group: [tg, tend)
-            const uint32_t b = a.nbuf == 2 ? (item & 1) : 0u;
+            uint32_t b = a.nbuf == 2 ? (item & 1) : 0u;
             const uint32_t use = a.nbuf == 2 ? (item >> 1) : item;
             if (ts && row == 0 && half == 0) ts[11] = gtimer();
-            tc::mbar_wait(&acc_full[b], use & 1);
-            tc::tc_fence_after();
+            if constexpr (X3) {
+                // drain the tile's accumulation segments (see the MMA warp): this warp owns
+                // the 32-column chunks half, half + 2, half + 4 (G <= 192)
+                float sum[3][32];
+#pragma unroll
+                for (uint32_t i = 0; i < 3; ++i)
+#pragma unroll
+                    for (uint32_t j = 0; j < 32; ++j) sum[i][j] = 0.0f;
+                const uint32_t nit = (kb1 - kb0 + a.kps - 1) / a.kps;
+                const uint32_t nseg = (nit + a.segn - 1) / a.segn;
+                for (uint32_t sg = 0; sg < nseg; ++sg, ++seg) {
+                    const uint32_t sb = seg & 1;
+                    const uint32_t col = tmem + lane_off + sb * a.G + half * 32;
+                    tc::mbar_wait(&acc_full[sb], (seg >> 1) & 1);
+                    tc::tc_fence_after();
+                    // (one 32-column load in flight: the register sums leave no room for more; the
+                    // buffer is released as soon as the last load has landed)
+                    uint32_t r[32];
+#pragma unroll
+                    for (uint32_t i = 0; i < 3; ++i) {
+                        if (half * 32 + 64 * i < a.G) {
+                            tc::tmem_ld32(col + 64 * i, r);
+                            tc::tmem_ld_wait();
+                        }
+                        if (i == 2 || half * 32 + 64 * (i + 1) >= a.G) {
+                            tc::tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) tc::mbar_arrive_remote(acc_empty_leader + sb * 8);
+                        }
+                        if (half * 32 + 64 * i < a.G) {
+#pragma unroll
+                            for (uint32_t j = 0; j < 32; ++j) sum[i][j] += __uint_as_float(r[j]);
+                        }
+                        if (half * 32 + 64 * (i + 1) >= a.G) break;
+                    }
+                }
+                if (a.S == 1) {
+#pragma unroll
+                    for (uint32_t i = 0; i < 3; ++i) {
+                        const uint32_t c = half * 32 + 64 * i;
+                        if (c < a.G && tg + c < tend && !(a.dbg & 1)) {
+                            uint32_t r[32];
+#pragma unroll
+                            for (uint32_t j = 0; j < 32; ++j) r[j] = __float_as_uint(sum[i][j]);
+                            pg_epi<MODE, true>(a.ep, tend, tg + c, f, lane, r, nullptr, nullptr, tg);
+                        }
+                    }
+                    if (ts && row == 0 && half == 0) ts[3] = gtimer();
+                    continue;
+                }
+                // split K: the sums go back into TMEM buffer 0 (idle: one tile per cluster, all
+                // of its MMAs done) for the in-cluster reduction below
+                b = 0;
+#pragma unroll
+                for (uint32_t i = 0; i < 3; ++i) {
+                    const uint32_t c = half * 32 + 64 * i;
+                    if (c < a.G) {
+                        uint32_t r[32];
+#pragma unroll
+                        for (uint32_t j = 0; j < 32; ++j) r[j] = __float_as_uint(sum[i][j]);
+                        tc::tmem_st32(tmem + lane_off + c, r);
+                    }
+                }
+                tc::tmem_st_wait();
+            } else {
+                tc::mbar_wait(&acc_full[b], use & 1);
+                tc::tc_fence_after();
+            }
             if (ts && row == 0 && half == 0) ts[12] = gtimer();
             const uint32_t dcol = tmem + lane_off + b * a.G;
             if (a.S == 1) {
@@ -579,8 +713,8 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                         tc::tmem_ld32(dcol + c, r);
                         tc::tmem_ld_wait();
                         const long long q1 = ts ? clock64() : 0;
-                        pg_epi<MODE>(a.ep, tend, tg + c, f, lane, r, s_rows, s_rope, tg,
-                                     a.stg_off == kNoStage ? nullptr : smem + a.stg_off + (warp - 2) * kStageSlice);
+                        pg_epi<MODE, X3>(a.ep, tend, tg + c, f, lane, r, s_rows, s_rope, tg,
+                                         a.stg_off == kNoStage ? nullptr : smem + a.stg_off + (warp - 2) * kStageSlice);
                         if (ts) {
                             c_ld += q1 - q0;
                             c_epi += clock64() - q1;
@@ -681,7 +815,7 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                     if (tg + j * 32 < tend) {
 #pragma unroll
                         for (uint32_t i = 0; i < 32; ++i) r[i] = __float_as_uint(v[i]);
-                        pg_epi<MODE>(a.ep, tend, tg + j * 32, f, lane, r, nullptr, nullptr, 0);
+                        pg_epi<MODE, X3>(a.ep, tend, tg + j * 32, f, lane, r, nullptr, nullptr, 0);
                     }
                 }
                 if (tsw) {
@@ -690,10 +824,11 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                     ts[12] = o_rs;
                 }
             }
-            // release the accumulator to the pair's MMA issuer (one arrive per warp)
+            // release the accumulator to the pair's MMA issuer (one arrive per warp; 3xTF32
+            // released each segment as it was drained)
             tc::tc_fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive_remote(acc_empty_leader + b * 8);
+            if (lane == 0 && !X3) tc::mbar_arrive_remote(acc_empty_leader + b * 8);
             if (ts && row == 0 && half == 0) ts[3] = gtimer();
         }
     }
@@ -712,14 +847,21 @@ __global__ void __launch_bounds__(kPgThreads, 1)
 
 uint32_t round16(uint32_t x) { return (x + 15) / 16 * 16; }
 
-using PgKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, PgArgs);
-PgKernel pg_kernel(int mode) {
+using PgKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, PgArgs);
+PgKernel pg_kernel(int mode, bool x3 = false) {
+    if (x3) switch (mode) {
+            case EPI_QKV: return tc_pgemm_kernel<EPI_QKV, true>;
+            case EPI_RESID: return tc_pgemm_kernel<EPI_RESID, true>;
+            case EPI_GELU: return tc_pgemm_kernel<EPI_GELU, true>;
+            case EPI_STORE_F32: return tc_pgemm_kernel<EPI_STORE_F32, true>;
+            default: return tc_pgemm_kernel<EPI_STORE, true>;
+        }
     switch (mode) {
-        case EPI_QKV: return tc_pgemm_kernel<EPI_QKV>;
-        case EPI_RESID: return tc_pgemm_kernel<EPI_RESID>;
-        case EPI_GELU: return tc_pgemm_kernel<EPI_GELU>;
-        case EPI_STORE_F32: return tc_pgemm_kernel<EPI_STORE_F32>;
-        default: return tc_pgemm_kernel<EPI_STORE>;
+        case EPI_QKV: return tc_pgemm_kernel<EPI_QKV, false>;
+        case EPI_RESID: return tc_pgemm_kernel<EPI_RESID, false>;
+        case EPI_GELU: return tc_pgemm_kernel<EPI_GELU, false>;
+        case EPI_STORE_F32: return tc_pgemm_kernel<EPI_STORE_F32, false>;
+        default: return tc_pgemm_kernel<EPI_STORE, false>;
     }
 }
 
@@ -742,7 +884,7 @@ uint32_t max_clusters(uint32_t size, size_t smem) {
         cfg.attrs = at;
         cfg.numAttrs = 1;
         int n = 0;
-        MPIC_CUDA(cudaOccupancyMaxActiveClusters(&n, pg_kernel(EPI_STORE), &cfg));
+        MPIC_CUDA(cudaOccupancyMaxActiveClusters(&n, pg_kernel(EPI_STORE, false), &cfg));
         v = (uint32_t)std::max(1, n);
     }
     return v;
@@ -752,6 +894,9 @@ uint32_t max_clusters(uint32_t size, size_t smem) {
 
 bool pgemm_supported(uint32_t M, uint32_t N, uint32_t K) {
     return M > 0 && N % 256 == 0 && K % 64 == 0 && K >= 64;
+}
+bool pgemm_x3_supported(uint32_t M, uint32_t N, uint32_t K) {
+    return M > 0 && N % 256 == 0 && K % 32 == 0 && K >= 64;
 }
 
 static unsigned long long* g_ts_buf = nullptr;
@@ -763,9 +908,12 @@ void pgemm_timestamps(unsigned long long* out9) {
     MPIC_CUDA(cudaMemcpy(out9, g_ts_buf, 16 * 8, cudaMemcpyDeviceToHost));
 }
 
-void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint32_t N, uint32_t K,
-                  const EpiParams& ep_in, cudaStream_t s, bool w_blocked) {
-    MPIC_REQUIRE(pgemm_supported(M, N, K), MPIC_ERR_VALIDATION, "unsupported pair gemm shape");
+namespace {
+// A, W: bf16 operands, or (x3) the fp32 hi parts with A_lo / W_lo the lo parts.
+void launch_pgemm_impl(const void* A, const void* A_lo, const void* W, const void* W_lo, uint32_t M, uint32_t N,
+                       uint32_t K, const EpiParams& ep_in, cudaStream_t s, bool w_blocked, bool x3) {
+    MPIC_REQUIRE(x3 ? pgemm_x3_supported(M, N, K) : pgemm_supported(M, N, K), MPIC_ERR_VALIDATION,
+                 "unsupported pair gemm shape");
     MPIC_REQUIRE(ep_in.mode != EPI_QKV || (ep_in.head_dim % 2 == 0 && ep_in.hidden % 32 == 0),
                  MPIC_ERR_VALIDATION, "pair gemm QKV epilogue needs hidden % 32 == 0");
     static const uint32_t group_max = [] {
@@ -790,10 +938,11 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
     }();
     static std::once_flag once;
     std::call_once(once, [] {
-        for (int m : {EPI_STORE, EPI_QKV, EPI_RESID, EPI_GELU, EPI_STORE_F32}) {
-            MPIC_CUDA(cudaFuncSetAttribute(pg_kernel(m), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-            MPIC_CUDA(cudaFuncSetAttribute(pg_kernel(m), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        }
+        for (int m : {EPI_STORE, EPI_QKV, EPI_RESID, EPI_GELU, EPI_STORE_F32})
+            for (bool x : {false, true}) {
+                MPIC_CUDA(cudaFuncSetAttribute(pg_kernel(m, x), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+                MPIC_CUDA(cudaFuncSetAttribute(pg_kernel(m, x), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            }
     });
     PgArgs best_a{};
     double best = 1e30;
@@ -802,7 +951,9 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
     // max(MMA 2G, operand fill 256 + G), plus for S > 1 the DSMEM reduction and owner
     // epilogue: ~2000 + 40 per token column pushed ((S-1)/S of the group) — fitted to the
     // measured Wo/W2 launches at config C (Wo: 2 groups x S=2 beats 1 x S=3 by 2 us).
-    const uint32_t ng_nat = M <= 512 ? 1 : ceil_div(M, 256);
+    // 3xTF32: two TMEM buffers of G columns and the epilogue's register sums cap G at 192
+    const uint32_t gcap = x3 ? 192u : 256u;
+    const uint32_t ng_nat = x3 ? ceil_div(M, gcap) : M <= 512 ? 1 : ceil_div(M, 256);
     for (uint32_t gm : {1u, 2u, 3u}) {
         PgArgs a{};
         a.M = M;
@@ -810,17 +961,17 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
         a.K = K;
         a.dbg = dbg;
         a.ngroups = ng_nat * gm;
-        if (a.ngroups == 1 && M > 256 && M <= group_max) {
+        if (!x3 && a.ngroups == 1 && M > 256 && M <= group_max) {
             a.P0 = round16((M + 1) / 2);
             a.P1 = round16(M - a.P0);
         } else {
             if (a.ngroups == 1 && M > 256) continue;  // MPIC_PG_GROUP=256 diagnostics
             a.P0 = round16(ceil_div(M, a.ngroups));
             a.P1 = 0;
-            if (a.P0 > 256 || (gm > 1 && a.P0 < 64)) continue;
+            if (a.P0 > gcap || (gm > 1 && a.P0 < 64)) continue;
             // two interleaved accumulator chains (off by default: each cta_group::2 MMA costs at
             // least ~83 cycles, so halving N loses more than the interleave gains)
-            if (split_pieces && a.P0 >= 64) {
+            if (split_pieces && !x3 && a.P0 >= 64) {
                 const uint32_t g = a.P0;
                 a.P0 = round16((g + 1) / 2);
                 a.P1 = g - a.P0;
@@ -830,11 +981,15 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
         a.nbuf = 2 * a.G <= 512 ? 2 : 1;
         a.tmem_cols = 32;
         while (a.tmem_cols < a.nbuf * a.G) a.tmem_cols *= 2;
-        a.kblocks = K / 64;
+        a.kel = x3 ? 32 : 64;
+        a.kblocks = K / a.kel;
         a.tiles = (N / 256) * a.ngroups;
-        a.sub_bytes = kPgWBytes + a.G * 64;
+        a.wsub = x3 ? 2 * kPgWBytes : kPgWBytes;
+        a.xlo = x3 ? a.G * 64 : 0u;
+        a.sub_bytes = a.wsub + (x3 ? 2 : 1) * a.G * 64;
         a.kps = kps_env ? kps_env : 2;
         a.stage_bytes = a.kps * a.sub_bytes;
+        a.segn = 1;
         a.xoff1 = a.P0 * 64;
         const uint32_t budget = 227 * 1024 - 1024 - 128;
         a.stages = std::min<uint32_t>(8, budget / a.stage_bytes);
@@ -844,6 +999,13 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
             a.stages = std::min<uint32_t>(8, budget / a.stage_bytes);
         }
         if (a.stages < 2) continue;
+        static const uint32_t seg_kb = [] {
+            const char* e = getenv("MPIC_X3_SEG");  // diagnostics: k-blocks (32 K) per accumulation segment
+            return e ? std::max(1, atoi(e)) : 1;
+        }();
+        // default 1 k-block (12 MMAs per chain): at config C's 32 layers 2 k-blocks left the
+        // logits at 0.97 of the fp64-referenced gate, 1 k-block at 0.27
+        if (x3) a.segn = std::max(1u, seg_kb / a.kps);
         a.w_evict_first = a.ngroups == 1;
         a.ep = ep_in;
     a.ep.dbg = dbg;
@@ -857,9 +1019,10 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
             const char* e = getenv("MPIC_PG_CHAIN");  // diagnostics: lone-chain issue factor
             return e ? atof(e) : 1.0;  // 1.5 with the old single-thread issuer
         }();
+        // (3xTF32: three K = 8 tf32 instructions per 32-B step, twice the operand bytes)
         const double mma = 4.0 * (std::max(a.P0 / 2.0, 83.0) + (a.P1 ? std::max(a.P1 / 2.0, 83.0) : 0.0)) *
-                           (a.P1 ? 1.0 : chain);
-        const double t_kb = std::max(mma, 256.0 + a.G);
+                           (a.P1 ? 1.0 : chain) * (x3 ? 3.0 : 1.0);
+        const double t_kb = std::max(mma, (256.0 + a.G) * (x3 ? 2.0 : 1.0));
         for (uint32_t S : {1u, 2u, 3u, 4u}) {
             if (force_s && S != force_s && S != 1) continue;
             if (S > 1 && a.kblocks / S < 2) continue;
@@ -900,21 +1063,21 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
     // The producer's L2 prefetch of weights ahead of the smem ring is off by default: it cost
     // 2.7% at config C and 10% at config B (m = 96) — the extra requests compete with the
     // ring's own loads; MPIC_PG_PFD=<k-blocks> turns it back on for diagnostics.
-    a.pfd = pfd_env >= 0 ? (uint32_t)pfd_env : 0u;
+    a.pfd = pfd_env >= 0 && !x3 ? (uint32_t)pfd_env : 0u;
     static const bool prologue_pf = [] {
         // off by default, like the ring prefetch: 1% faster at config C without it
         const char* e = getenv("MPIC_PG_PROLOGUE_PF");  // diagnostics: 1 = prefetch before the PDL wait
         return e && atoi(e) != 0;
     }();
-    a.prologue_pf = prologue_pf ? 1u : 0u;
+    a.prologue_pf = prologue_pf && !x3 ? 1u : 0u;
 
     const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 4 + kEpiBars) * 8 + 16;
     static const bool verbose = getenv("MPIC_PG_VERBOSE") != nullptr;
     if (verbose)
         fprintf(stderr, "pgemm M=%u N=%u K=%u: groups=%u P0=%u P1=%u S=%u clusters=%u stages=%u x %u kb nbuf=%u\n", M,
                 N, K, a.ngroups, a.P0, a.P1, a.S, a.clusters, a.stages, a.kps, a.nbuf);
-    if (ep_in.mode == EPI_QKV && ep_in.rope_tok && ep_in.head_dim % 4 == 0 && a.S == 1 && a.clusters >= a.tiles &&
-        a.ngroups == 1) {
+    if (!x3 && ep_in.mode == EPI_QKV && ep_in.rope_tok && ep_in.head_dim % 4 == 0 && a.S == 1 &&
+        a.clusters >= a.tiles && a.ngroups == 1) {
         const uint32_t rope_bytes = a.G * (ep_in.head_dim / 2) * 8;
         a.rows_off = (rope_bytes + 1023) & ~1023u;
         static const bool no_stage = getenv("MPIC_PG_NOROPESTAGE") != nullptr;  // diagnostics
@@ -927,15 +1090,27 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
     a.stg_off = kNoStage;
     // the staged QKV epilogue reads (cos, sin) as 16-B pairs of pairs from rope_tok
     const bool qkv_ok = ep_in.mode != EPI_QKV || a.stage_rope;
-    if (staged_env && qkv_ok && a.S == 1 && a.clusters >= a.tiles) {
+    if (!x3 && staged_env && qkv_ok && a.S == 1 && a.clusters >= a.tiles) {
         // one tile per cluster: the stage ring is idle once the accumulator is complete
         const uint32_t off = a.stage_rope ? (a.rows_off + a.G * 4 + 16 + 1023) & ~1023u : 0u;
         if (off + 8 * kStageSlice <= a.stages * a.stage_bytes) a.stg_off = off;
     }
-    const CUtensorMap tmW = w_blocked ? make_tmap_bf16(W, 64, (uint64_t)N * a.kblocks, 64, 128)
-                                      : make_tmap_bf16(W, K, N, 64, 128);
-    const CUtensorMap tmX0 = make_tmap_bf16(A, K, M, 64, a.P0 / 2);
-    const CUtensorMap tmX1 = a.P1 ? make_tmap_bf16(A, K, M, 64, a.P1 / 2) : tmX0;
+    CUtensorMap tmW, tmX0, tmX1, tmWl, tmX0l, tmX1l;
+    if (x3) {
+        tmW = make_tmap_f32(W, K, N, 32, 128);
+        tmWl = make_tmap_f32(W_lo, K, N, 32, 128);
+        tmX0 = make_tmap_f32(A, K, M, 32, a.P0 / 2);
+        tmX0l = make_tmap_f32(A_lo, K, M, 32, a.P0 / 2);
+        tmX1 = a.P1 ? make_tmap_f32(A, K, M, 32, a.P1 / 2) : tmX0;
+        tmX1l = a.P1 ? make_tmap_f32(A_lo, K, M, 32, a.P1 / 2) : tmX0l;
+    } else {
+        tmW = w_blocked ? make_tmap_bf16(W, 64, (uint64_t)N * a.kblocks, 64, 128) : make_tmap_bf16(W, K, N, 64, 128);
+        tmX0 = make_tmap_bf16(A, K, M, 64, a.P0 / 2);
+        tmX1 = a.P1 ? make_tmap_bf16(A, K, M, 64, a.P1 / 2) : tmX0;
+        tmWl = tmW;
+        tmX0l = tmX0;
+        tmX1l = tmX1;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.clusters * 2 * a.S);
     cfg.blockDim = dim3(kPgThreads);
@@ -952,7 +1127,51 @@ void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, ui
     at[2].val.priority = hot_priority();
     cfg.attrs = at;
     cfg.numAttrs = 3;
-    MPIC_CUDA(cudaLaunchKernelEx(&cfg, pg_kernel(a.ep.mode), tmW, tmX0, tmX1, a));
+    MPIC_CUDA(cudaLaunchKernelEx(&cfg, pg_kernel(a.ep.mode, x3), tmW, tmX0, tmX1, tmWl, tmX0l, tmX1l, a));
+    MPIC_LAUNCHED();
+}
+}  // namespace
+
+void launch_pgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, uint32_t M, uint32_t N, uint32_t K,
+                  const EpiParams& ep, cudaStream_t s, bool w_blocked) {
+    launch_pgemm_impl(A, nullptr, W, nullptr, M, N, K, ep, s, w_blocked, false);
+}
+
+void launch_pgemm_x3(const float* A_hi, const float* A_lo, const float* W_hi, const float* W_lo, uint32_t M,
+                     uint32_t N, uint32_t K, const EpiParams& ep, cudaStream_t s) {
+    MPIC_REQUIRE(ep.mode != EPI_QKV || ep.rope, MPIC_ERR_VALIDATION, "3xTF32 QKV epilogue needs the RoPE table");
+    launch_pgemm_impl(A_hi, A_lo, W_hi, W_lo, M, N, K, ep, s, false, true);
+}
+
+// x = hi + lo with hi = tf32(x), lo = tf32(x - hi) (round to nearest, ties away): both parts
+// carry tf32 bits only, so the tensor core reads them exactly whatever its own rounding.
+__global__ void tf32_split_kernel(const float4* __restrict__ x, float4* __restrict__ hi, float4* __restrict__ lo,
+                                  size_t n4) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+        const float4 v = x[i];
+        float4 h, l;
+        float* pv = (float*)&v;
+        float* ph = (float*)&h;
+        float* pl = (float*)&l;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint32_t a, b;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(a) : "f"(pv[c]));
+            ph[c] = __uint_as_float(a);
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(pv[c] - ph[c]));
+            pl[c] = __uint_as_float(b);
+        }
+        hi[i] = h;
+        lo[i] = l;
+    }
+}
+
+void launch_tf32_split(const float* x, float* hi, float* lo, size_t n, cudaStream_t s) {
+    MPIC_REQUIRE(n % 4 == 0, MPIC_ERR_VALIDATION, "tf32 split needs a multiple of 4 elements");
+    const size_t n4 = n / 4;
+    const uint32_t blocks = (uint32_t)std::min<size_t>(kNumSMs * 8, std::max<size_t>(1, (n4 + 255) / 256));
+    tf32_split_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(hi),
+                                             reinterpret_cast<float4*>(lo), n4);
     MPIC_LAUNCHED();
 }
 

@@ -47,6 +47,27 @@ def test_gemm_vs_torch(M, N, K, path):
     assert err < 1e-5 * max(1.0, K / 4096), err
 
 
+@pytest.mark.parametrize("M,N,K", [(1, 256, 64), (17, 256, 96), (330, 12288, 4096), (330, 4096, 4096),
+                                   (330, 16384, 4096), (330, 4096, 16384), (96, 4096, 4096),
+                                   (600, 512, 256), (1100, 768, 1024)])
+def test_gemm_3xtf32_vs_fp64(M, N, K):
+    """The fp32 mode's tensor-core GEMM (3xTF32: hi/lo tf32 split, three tcgen05 kind::tf32
+    products per step, fp32 TMEM accumulation) is as close to the exact (fp64) product as
+    the SIMT FFMA GEMM it replaces."""
+    g = torch.Generator(device="cuda").manual_seed(M * 5 + N + K)
+    a = torch.rand(M, K, device="cuda", generator=g) - 0.5
+    w = (torch.rand(N, K, device="cuda", generator=g) - 0.5) / K ** 0.5
+    ref = a.double() @ w.double().t()
+    scale = ref.abs().max().item()
+    err_tc = (run_gemm(a, w, 4).double() - ref).abs().max().item() / scale
+    err_simt = (run_gemm(a, w, 5).double() - ref).abs().max().item() / scale
+    print(f"3xTF32 {M}x{N}x{K}: tc {err_tc:.3e} simt {err_simt:.3e}")
+    # measured: 3e-7 .. 7e-7 (SIMT 1e-7 .. 1.3e-6); one accumulation chain over all of K
+    # (no segments) gave 3e-5 .. 6e-5 — the tensor core truncates its fp32 accumulation
+    assert err_tc < 2e-6, (err_tc, err_simt)
+    assert err_tc < 4 * err_simt + 5e-7, (err_tc, err_simt)
+
+
 @pytest.mark.parametrize("M,N,K", [(330, 4096, 4096), (96, 1024, 2048), (600, 512, 256),
                                    (330, 16384, 512)])
 @pytest.mark.parametrize("mode", [0, 1, 2])
