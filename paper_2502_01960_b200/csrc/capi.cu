@@ -658,8 +658,9 @@ void forward_rows(mpic_model_t md, mpic_workspace_t ws, const int32_t* d_ids,
                                ws->n_units, ws->d_comb, ws->n_comb, ws->part_o, ws->part_ml,
                                static_cast<__nv_bfloat16*>(ws->attn), s, d_link, l, d_starts,
                                fused_combine() ? ws->d_comb_cnt : nullptr);
-            else
-                launch_attn_simt(ws->q, kl, vl, md->dtype, d_rows, m, H, D, ws->attn, s);
+            else  // fp32: the 3xTF32 GEMMs' split scratch is idle during attention
+                launch_attn_simt(ws->q, kl, vl, md->dtype, d_rows, m, H, D, ws->attn, s, nullptr, 0, ws->x3buf,
+                                 ws->x3buf ? (size_t)8 * ws->m_pad * h : 0);
         }
 
         EpiParams res;

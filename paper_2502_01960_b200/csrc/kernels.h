@@ -69,9 +69,12 @@ void launch_rope_table(const double* inv_freq, uint32_t half_d, uint32_t p0, uin
 void launch_gemm_simt(const void* A, mpic_dtype a_t, uint32_t lda, const void* W, mpic_dtype w_t,
                       uint32_t M, uint32_t N, uint32_t K, const EpiParams& ep, mpic_dtype o_t,
                       cudaStream_t s);
+// scratch (optional, fp32 head_dim 128): room for key-split partials (split x m x (h + 2H)
+// floats); without it the fp32 attention runs unsplit.
 void launch_attn_simt(const void* q, const void* k, const void* v, mpic_dtype dt,
                       const uint32_t* rows, uint32_t m, uint32_t H, uint32_t D, void* out,
-                      cudaStream_t s, float* capture = nullptr, uint32_t T = 0);
+                      cudaStream_t s, float* capture = nullptr, uint32_t T = 0, float* scratch = nullptr,
+                      size_t scratch_floats = 0);
 void launch_lm_head(const float* x_last, const void* W, mpic_dtype w_t, uint32_t V, uint32_t h,
                     float* logits, cudaStream_t s);
 // out_k/out_v[l][i][:] = k/v[l][rows[i]][:] as fp32 (rows of a [L][T][h] cache).

@@ -3,6 +3,7 @@
 // causal attention (fp32 accumulation, online softmax), lm_head GEMV and dtype casts.
 // The bf16 production path uses these only for the small non-GEMM steps; its GEMMs and
 // attention are the tcgen05 kernels in tc_gemm.cu / tc_attn.cu.
+#include <string>
 #include "common.cuh"
 #include "kernels.h"
 
@@ -311,12 +312,22 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const TQ* __restrict__ q
 }
 
 // fp32 attention, query-tiled (the fp32 mode's hot attention, head_dim 64/128): a CTA takes
-// 16 query rows of one head and streams 64-key blocks of K and V through shared memory once
+// 16 query rows of one head and streams 32-key blocks of K and V through shared memory once
 // for all 16 rows (the per-row kernel above re-read every key for every row: at config C
-// ~50 GB of L2 traffic per layer). Thread t owns row t / 8 and, per block, the scores of
-// keys t % 8 + 8j (j < 8) and the output dims 32q + 4 (t % 8) + e; online softmax per row
-// over the row's 8 threads (shuffles), causal limit = the row's cache index.
-constexpr uint32_t kTR = 16, kTK = 64;
+// ~50 GB of L2 traffic per layer). The blocks are double-buffered with cp.async, so block
+// b + 1 is in flight while block b is computed. Thread t owns row t / 8 and, per block, the
+// scores of keys t % 8 + 8j (j < 4) and the output dims 32q + 4 (t % 8) + e; online softmax
+// per row over the row's 8 threads (shuffles), causal limit = the row's cache index.
+constexpr uint32_t kTR = 16, kTK = 32;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 template <uint32_t D>
 __global__ void __launch_bounds__(128, 2) attn_simt_tiled_kernel(const float* __restrict__ q,
                                                                  const float* __restrict__ kk,
@@ -326,11 +337,12 @@ __global__ void __launch_bounds__(128, 2) attn_simt_tiled_kernel(const float* __
                                                                  float* __restrict__ out) {
     constexpr uint32_t DP = D + 4;           // padded row (16-B aligned, conflict-free float4 reads)
     constexpr uint32_t ND = D / 32;          // float4 output groups per thread (4 or 2)
+    constexpr uint32_t NJ = kTK / 8;         // scores per thread per block
     extern __shared__ float sm_t[];
     float* Qs = sm_t;                        // [kTR][DP]
-    float* Ks = Qs + kTR * DP;               // [kTK][DP]
-    float* Vs = Ks + kTK * DP;               // [kTK][DP]
-    float* Ps = Vs + kTK * DP;               // [kTR][kTK + 4]
+    float* Ks = Qs + kTR * DP;               // [2][kTK][DP]
+    float* Vs = Ks + 2 * kTK * DP;           // [2][kTK][DP]
+    float* Ps = Vs + 2 * kTK * DP;           // [kTR][kTK + 4]
     __shared__ uint32_t s_maxrow;
     const uint32_t t = threadIdx.x, r = t >> 3, c = t & 7;
     const uint32_t i0 = blockIdx.x * kTR, head = blockIdx.y;
@@ -349,32 +361,45 @@ __global__ void __launch_bounds__(128, 2) attn_simt_tiled_kernel(const float* __
     if (valid && c == 0) atomicMax(&s_maxrow, limit);
     __syncthreads();
     const uint32_t nkeys = s_maxrow + 1;
+    const uint32_t nblk = (nkeys + kTK - 1) / kTK;
+    // rows of a block past nkeys are not loaded: their scores are masked (kg > every limit)
+    // and the PV loop stops at nk
+    auto issue = [&](uint32_t blk) {
+        const uint32_t k0 = blk * kTK, nk = min(kTK, nkeys - k0), buf = blk & 1;
+        for (uint32_t x = t; x < kTK * (D / 4); x += 128) {
+            const uint32_t kr = x / (D / 4), d4 = x % (D / 4);
+            if (kr < nk) {
+                cp_async16(Ks + (buf * kTK + kr) * DP + d4 * 4, kk + (size_t)(k0 + kr) * h + hoff + d4 * 4);
+                cp_async16(Vs + (buf * kTK + kr) * DP + d4 * 4, vv + (size_t)(k0 + kr) * h + hoff + d4 * 4);
+            }
+        }
+        cp_async_commit();
+    };
     float m_run = -INFINITY, l_run = 0.0f;
     float4 o[ND];
 #pragma unroll
     for (uint32_t q4 = 0; q4 < ND; ++q4) o[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (uint32_t k0 = 0; k0 < nkeys; k0 += kTK) {
-        const uint32_t nk = min(kTK, nkeys - k0);
-        for (uint32_t x = t; x < kTK * (D / 4); x += 128) {
-            const uint32_t kr = x / (D / 4), d4 = x % (D / 4);
-            float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-            if (kr < nk) {
-                a = __ldg(reinterpret_cast<const float4*>(kk + (size_t)(k0 + kr) * h + hoff) + d4);
-                b = __ldg(reinterpret_cast<const float4*>(vv + (size_t)(k0 + kr) * h + hoff) + d4);
-            }
-            *reinterpret_cast<float4*>(Ks + kr * DP + d4 * 4) = a;
-            *reinterpret_cast<float4*>(Vs + kr * DP + d4 * 4) = b;
+    issue(0);
+    for (uint32_t blk = 0; blk < nblk; ++blk) {
+        const uint32_t k0 = blk * kTK, nk = min(kTK, nkeys - k0);
+        if (blk + 1 < nblk) {
+            issue(blk + 1);  // its buffer was last read in iteration blk - 1 (closing barrier)
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
-        float sc[8];
+        const float* Kb = Ks + (blk & 1) * kTK * DP;
+        const float* Vb = Vs + (blk & 1) * kTK * DP;
+        float sc[NJ];
 #pragma unroll
-        for (uint32_t j = 0; j < 8; ++j) sc[j] = 0.0f;
-#pragma unroll 4
+        for (uint32_t j = 0; j < NJ; ++j) sc[j] = 0.0f;
+#pragma unroll 8
         for (uint32_t d4 = 0; d4 < D / 4; ++d4) {
             const float4 qv = *reinterpret_cast<const float4*>(Qs + r * DP + d4 * 4);
 #pragma unroll
-            for (uint32_t j = 0; j < 8; ++j) {
-                const float4 kv = *reinterpret_cast<const float4*>(Ks + (c + 8 * j) * DP + d4 * 4);
+            for (uint32_t j = 0; j < NJ; ++j) {
+                const float4 kv = *reinterpret_cast<const float4*>(Kb + (c + 8 * j) * DP + d4 * 4);
                 sc[j] = fmaf(qv.x, kv.x, sc[j]);
                 sc[j] = fmaf(qv.y, kv.y, sc[j]);
                 sc[j] = fmaf(qv.z, kv.z, sc[j]);
@@ -383,7 +408,7 @@ __global__ void __launch_bounds__(128, 2) attn_simt_tiled_kernel(const float* __
         }
         float mx = -INFINITY;
 #pragma unroll
-        for (uint32_t j = 0; j < 8; ++j) {
+        for (uint32_t j = 0; j < NJ; ++j) {
             const uint32_t kg = k0 + c + 8 * j;
             sc[j] = valid && kg <= limit ? sc[j] * inv_sqrt_d : -INFINITY;
             mx = fmaxf(mx, sc[j]);
@@ -394,7 +419,7 @@ __global__ void __launch_bounds__(128, 2) attn_simt_tiled_kernel(const float* __
         const float alpha = m_new == -INFINITY ? 1.0f : expf(m_run - m_new);
         float ls = 0.0f;
 #pragma unroll
-        for (uint32_t j = 0; j < 8; ++j) {
+        for (uint32_t j = 0; j < NJ; ++j) {
             const float pj = sc[j] == -INFINITY ? 0.0f : expf(sc[j] - m_new);
             Ps[r * (kTK + 4) + c + 8 * j] = pj;
             ls += pj;
@@ -411,19 +436,33 @@ __global__ void __launch_bounds__(128, 2) attn_simt_tiled_kernel(const float* __
             o[q4].w *= alpha;
         }
         __syncwarp();  // Ps rows are written and read by the same warp (row r's 8 threads)
-#pragma unroll 4
-        for (uint32_t kr = 0; kr < nk; ++kr) {
-            const float pk = Ps[r * (kTK + 4) + kr];
+        if (nk == kTK) {
+#pragma unroll 8
+            for (uint32_t kr = 0; kr < kTK; ++kr) {
+                const float pk = Ps[r * (kTK + 4) + kr];
 #pragma unroll
-            for (uint32_t q4 = 0; q4 < ND; ++q4) {
-                const float4 vv4 = *reinterpret_cast<const float4*>(Vs + kr * DP + 32 * q4 + 4 * c);
-                o[q4].x = fmaf(pk, vv4.x, o[q4].x);
-                o[q4].y = fmaf(pk, vv4.y, o[q4].y);
-                o[q4].z = fmaf(pk, vv4.z, o[q4].z);
-                o[q4].w = fmaf(pk, vv4.w, o[q4].w);
+                for (uint32_t q4 = 0; q4 < ND; ++q4) {
+                    const float4 vv4 = *reinterpret_cast<const float4*>(Vb + kr * DP + 32 * q4 + 4 * c);
+                    o[q4].x = fmaf(pk, vv4.x, o[q4].x);
+                    o[q4].y = fmaf(pk, vv4.y, o[q4].y);
+                    o[q4].z = fmaf(pk, vv4.z, o[q4].z);
+                    o[q4].w = fmaf(pk, vv4.w, o[q4].w);
+                }
+            }
+        } else {
+            for (uint32_t kr = 0; kr < nk; ++kr) {
+                const float pk = Ps[r * (kTK + 4) + kr];
+#pragma unroll
+                for (uint32_t q4 = 0; q4 < ND; ++q4) {
+                    const float4 vv4 = *reinterpret_cast<const float4*>(Vb + kr * DP + 32 * q4 + 4 * c);
+                    o[q4].x = fmaf(pk, vv4.x, o[q4].x);
+                    o[q4].y = fmaf(pk, vv4.y, o[q4].y);
+                    o[q4].z = fmaf(pk, vv4.z, o[q4].z);
+                    o[q4].w = fmaf(pk, vv4.w, o[q4].w);
+                }
             }
         }
-        __syncthreads();  // K/V tiles are reloaded next
+        __syncthreads();  // this buffer is refilled by the next iteration's issue
     }
     if (!valid) return;
     const float inv = l_run > 0.0f ? 1.0f / l_run : 0.0f;
@@ -433,10 +472,246 @@ __global__ void __launch_bounds__(128, 2) attn_simt_tiled_kernel(const float* __
             make_float4(o[q4].x * inv, o[q4].y * inv, o[q4].z * inv, o[q4].w * inv);
 }
 
+// fp32 attention for head_dim 128 with register micro-tiles (the fp32 mode's hot attention).
+// The query-tiled kernel above reads one or two operands per FMA from shared memory, and a
+// warp-wide 16-B shared load costs four wavefronts: it runs at the shared-memory wavefront
+// limit with the FMA pipe ~20% busy. Here a CTA takes 64 query rows of one head (8 warps, warp
+// w = rows 8w .. 8w + 7) and streams 128-key blocks: per 4-dim step a lane loads 8 query
+// float4s (broadcast) and 4 key float4s (keys lane + 32i, conflict-free) for 128 FMAs, then
+// P (warp-private, [key][8 rows]) times V (lane = dims 4 lane .. + 3) at 3 loads per 32 FMAs.
+// K and V are single-buffered but staggered: K(b + 1) loads during softmax + PV of block b,
+// V(b + 1) during S of block b + 1. Online softmax per row over the warp (shuffles); causal
+// limit = the row's cache index; fp32 throughout (the reference's linker.cpp:80-113).
+constexpr uint32_t kMR = 64, kMK = 128, kMDP = 132, kMPP = 12;
+// Grid: one CTA per (query tile, key split, head), heaviest tiles (the last rows: the longest
+// key ranges) first so the hardware's in-order dispatch approximates longest-first. With
+// nsplit > 1 a CTA takes key blocks [s * nblk / nsplit, (s + 1) * nblk / nsplit) of its tile
+// and writes its unnormalised O with the rows' (max, sum) to part_o / part_ml for
+// attn_f32_combine_kernel.
+__global__ void __launch_bounds__(256, 1) attn_f32_mt_kernel(const float* __restrict__ q, const float* __restrict__ kk,
+                                                            const float* __restrict__ vv,
+                                                            const uint32_t* __restrict__ rows, uint32_t m, uint32_t h,
+                                                            float inv_sqrt_d, float* __restrict__ out, uint32_t nsplit,
+                                                            float* __restrict__ part_o, float2* __restrict__ part_ml) {
+    extern __shared__ __align__(16) float sm_m[];
+    float* Qs = sm_m;                 // [kMR][kMDP]
+    float* Ks = Qs + kMR * kMDP;      // [kMK][kMDP]
+    float* Vs = Ks + kMK * kMDP;      // [kMK][kMDP]
+    float* Pw = Vs + kMK * kMDP;      // [8 warps][kMK][kMPP]
+    __shared__ uint32_t s_maxrow;
+    const uint32_t t = threadIdx.x, w = t >> 5, lane = t & 31;
+    const uint32_t H = h / 128, ntiles = (m + kMR - 1) / kMR;
+    const uint32_t head = blockIdx.x % H, split = (blockIdx.x / H) % nsplit;
+    const uint32_t i0 = (ntiles - 1 - blockIdx.x / (H * nsplit)) * kMR;
+    const size_t hoff = (size_t)head * 128;
+    float* Pme = Pw + w * kMK * kMPP;
+    uint32_t lim[8];
+#pragma unroll
+    for (uint32_t a = 0; a < 8; ++a) {
+        const uint32_t qi = i0 + 8 * w + a;
+        lim[a] = qi < m ? rows[qi] : 0xffffffffu;  // 0xffffffff: padding row (every key masked)
+    }
+    if (t == 0) s_maxrow = 0;
+    __syncthreads();
+    if (lane < 8 && i0 + 8 * w + lane < m) atomicMax(&s_maxrow, rows[i0 + 8 * w + lane]);
+    for (uint32_t x = t; x < kMR * 32; x += 256) {
+        const uint32_t rr = x >> 5, d4 = x & 31;
+        if (i0 + rr < m) cp_async16(Qs + rr * kMDP + d4 * 4, q + (size_t)(i0 + rr) * h + hoff + d4 * 4);
+    }
+    __syncthreads();
+    const uint32_t nkeys = s_maxrow + 1;
+    const uint32_t nblk_all = (nkeys + kMK - 1) / kMK;
+    const uint32_t blk0 = split * nblk_all / nsplit, blk1 = (split + 1) * nblk_all / nsplit;
+    auto load = [&](float* dst, const float* src, uint32_t blk) {
+        const uint32_t k0 = blk * kMK, nk = min(kMK, nkeys - k0);
+        for (uint32_t x = t; x < kMK * 32; x += 256) {
+            const uint32_t kr = x >> 5, d4 = x & 31;
+            if (kr < nk) cp_async16(dst + kr * kMDP + d4 * 4, src + (size_t)(k0 + kr) * h + hoff + d4 * 4);
+        }
+        cp_async_commit();
+    };
+    if (blk0 < blk1) {  // (an empty split — fewer blocks than splits — loads nothing)
+        load(Ks, kk, blk0);  // (with the Q rows)
+        load(Vs, vv, blk0);
+    }
+    float m_run[8], l_run[8];
+    float4 o[8];
+#pragma unroll
+    for (uint32_t a = 0; a < 8; ++a) {
+        m_run[a] = -INFINITY;
+        l_run[a] = 0.0f;
+        o[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (uint32_t blk = blk0; blk < blk1; ++blk) {
+        const uint32_t k0 = blk * kMK, nk = min(kMK, nkeys - k0);
+        cp_async_wait<1>();  // K(blk) (and Q); V(blk) may still be in flight
+        __syncthreads();
+        float sc[8][4];
+#pragma unroll
+        for (uint32_t a = 0; a < 8; ++a)
+#pragma unroll
+            for (uint32_t i = 0; i < 4; ++i) sc[a][i] = 0.0f;
+#pragma unroll 2
+        for (uint32_t d4 = 0; d4 < 32; ++d4) {
+            float4 kv[4];
+#pragma unroll
+            for (uint32_t i = 0; i < 4; ++i) kv[i] = *reinterpret_cast<const float4*>(Ks + (lane + 32 * i) * kMDP + d4 * 4);
+#pragma unroll
+            for (uint32_t a = 0; a < 8; ++a) {
+                const float4 qv = *reinterpret_cast<const float4*>(Qs + (8 * w + a) * kMDP + d4 * 4);
+#pragma unroll
+                for (uint32_t i = 0; i < 4; ++i) {
+                    sc[a][i] = fmaf(qv.x, kv[i].x, sc[a][i]);
+                    sc[a][i] = fmaf(qv.y, kv[i].y, sc[a][i]);
+                    sc[a][i] = fmaf(qv.z, kv[i].z, sc[a][i]);
+                    sc[a][i] = fmaf(qv.w, kv[i].w, sc[a][i]);
+                }
+            }
+        }
+        __syncthreads();  // every warp is done with K(blk)
+        if (blk + 1 < blk1) load(Ks, kk, blk + 1);
+        float pv[8][4];
+#pragma unroll
+        for (uint32_t a = 0; a < 8; ++a) {
+            float mx = -INFINITY;
+#pragma unroll
+            for (uint32_t i = 0; i < 4; ++i) {
+                const uint32_t kg = k0 + lane + 32 * i;
+                sc[a][i] = lim[a] != 0xffffffffu && kg <= lim[a] ? sc[a][i] * inv_sqrt_d : -INFINITY;
+                mx = fmaxf(mx, sc[a][i]);
+            }
+#pragma unroll
+            for (uint32_t off = 1; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            const float m_new = fmaxf(m_run[a], mx);
+            const float alpha = m_new == -INFINITY ? 1.0f : expf(m_run[a] - m_new);
+            float ls = 0.0f;
+#pragma unroll
+            for (uint32_t i = 0; i < 4; ++i) {
+                pv[a][i] = sc[a][i] == -INFINITY ? 0.0f : expf(sc[a][i] - m_new);
+                ls += pv[a][i];
+            }
+#pragma unroll
+            for (uint32_t off = 1; off < 32; off <<= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
+            l_run[a] = l_run[a] * alpha + ls;
+            m_run[a] = m_new;
+            o[a].x *= alpha;
+            o[a].y *= alpha;
+            o[a].z *= alpha;
+            o[a].w *= alpha;
+        }
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i) {
+            float* pr = Pme + (lane + 32 * i) * kMPP;
+            *reinterpret_cast<float4*>(pr) = make_float4(pv[0][i], pv[1][i], pv[2][i], pv[3][i]);
+            *reinterpret_cast<float4*>(pr + 4) = make_float4(pv[4][i], pv[5][i], pv[6][i], pv[7][i]);
+        }
+        if (blk + 1 < blk1) cp_async_wait<1>();  // V(blk); K(blk + 1) may still be in flight
+        else cp_async_wait<0>();
+        __syncthreads();  // V(blk) visible to all warps (P is warp-private: also ordered by this)
+        const auto pv_step = [&](uint32_t kr) {
+            const float4 p0 = *reinterpret_cast<const float4*>(Pme + kr * kMPP);
+            const float4 p1 = *reinterpret_cast<const float4*>(Pme + kr * kMPP + 4);
+            const float4 v4 = *reinterpret_cast<const float4*>(Vs + kr * kMDP + lane * 4);
+            const float pa[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+            for (uint32_t a = 0; a < 8; ++a) {
+                o[a].x = fmaf(pa[a], v4.x, o[a].x);
+                o[a].y = fmaf(pa[a], v4.y, o[a].y);
+                o[a].z = fmaf(pa[a], v4.z, o[a].z);
+                o[a].w = fmaf(pa[a], v4.w, o[a].w);
+            }
+        };
+        if (nk == kMK) {
+#pragma unroll 4
+            for (uint32_t kr = 0; kr < kMK; ++kr) pv_step(kr);
+        } else {
+            for (uint32_t kr = 0; kr < nk; ++kr) pv_step(kr);
+        }
+        __syncthreads();  // every warp is done with V(blk)
+        if (blk + 1 < blk1) load(Vs, vv, blk + 1);
+    }
+    cp_async_wait<0>();  // (the Q rows of an empty split)
+    if (nsplit > 1) {
+#pragma unroll
+        for (uint32_t a = 0; a < 8; ++a) {
+            const uint32_t qi = i0 + 8 * w + a;
+            if (qi >= m) continue;
+            *reinterpret_cast<float4*>(part_o + ((size_t)split * m + qi) * h + hoff + lane * 4) = o[a];
+            if (lane == 0) part_ml[((size_t)split * m + qi) * H + head] = make_float2(m_run[a], l_run[a]);
+        }
+        return;
+    }
+#pragma unroll
+    for (uint32_t a = 0; a < 8; ++a) {
+        const uint32_t qi = i0 + 8 * w + a;
+        if (qi >= m) continue;
+        const float inv = l_run[a] > 0.0f ? 1.0f / l_run[a] : 0.0f;
+        *reinterpret_cast<float4*>(out + (size_t)qi * h + hoff + lane * 4) =
+            make_float4(o[a].x * inv, o[a].y * inv, o[a].z * inv, o[a].w * inv);
+    }
+}
+
+// out[row][head dims] = sum_s O_s e^(m_s - M) / sum_s l_s e^(m_s - M), M = max_s m_s (splits
+// with no visible key have m_s = -inf, l_s = 0). One thread per (row, head, 4 dims).
+__global__ void attn_f32_combine_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
+                                        uint32_t nsplit, uint32_t m, uint32_t H, float* __restrict__ out) {
+    const uint32_t h = H * 128;
+    const size_t n4 = (size_t)m * h / 4;
+    for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < n4; x += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t row = (uint32_t)(x / (h / 4)), c4 = (uint32_t)(x % (h / 4)), head = c4 / 32;
+        float mx = -INFINITY;
+        for (uint32_t sp = 0; sp < nsplit; ++sp) mx = fmaxf(mx, part_ml[((size_t)sp * m + row) * H + head].x);
+        float l = 0.0f;
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (uint32_t sp = 0; sp < nsplit; ++sp) {
+            const float2 ml = part_ml[((size_t)sp * m + row) * H + head];
+            if (ml.y == 0.0f) continue;
+            const float wgt = expf(ml.x - mx);
+            const float4 po = reinterpret_cast<const float4*>(part_o + ((size_t)sp * m + row) * h)[c4];
+            l = fmaf(ml.y, wgt, l);
+            o.x = fmaf(po.x, wgt, o.x);
+            o.y = fmaf(po.y, wgt, o.y);
+            o.z = fmaf(po.z, wgt, o.z);
+            o.w = fmaf(po.w, wgt, o.w);
+        }
+        const float inv = l > 0.0f ? 1.0f / l : 0.0f;
+        reinterpret_cast<float4*>(out + (size_t)row * h)[c4] = make_float4(o.x * inv, o.y * inv, o.z * inv, o.w * inv);
+    }
+}
+
+static void launch_attn_f32_mt(const float* q, const float* k, const float* v, const uint32_t* rows, uint32_t m,
+                               uint32_t H, float* out, cudaStream_t s, float* scratch, size_t scratch_floats) {
+    const size_t smem = ((size_t)(kMR + 2 * kMK) * kMDP + 8 * kMK * kMPP) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+        MPIC_CUDA(cudaFuncSetAttribute(attn_f32_mt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const uint32_t h = H * 128, ntiles = ceil_div(m, kMR);
+    // key splits: enough CTAs for ~2 per SM (one is resident at a time; the second evens out
+    // the causal imbalance of the tiles), if the caller's scratch holds the partials
+    static const uint32_t split_env = [] {
+        const char* e = getenv("MPIC_F32_ATTN_SPLIT");  // diagnostics: force the split count
+        return e ? (uint32_t)atoi(e) : 0u;
+    }();
+    uint32_t nsplit = split_env ? split_env : std::max(1u, std::min(4u, ceil_div(2 * kNumSMs, ntiles * H)));
+    const size_t need = [&](uint32_t ns) { return (size_t)ns * m * h + 2 * (size_t)ns * m * H; }(nsplit);
+    if (nsplit > 1 && (!scratch || scratch_floats < need)) nsplit = 1;
+    float* part_o = nsplit > 1 ? scratch : nullptr;
+    float2* part_ml = nsplit > 1 ? reinterpret_cast<float2*>(scratch + (size_t)nsplit * m * h) : nullptr;
+    attn_f32_mt_kernel<<<ntiles * nsplit * H, 256, smem, s>>>(q, k, v, rows, m, h, 1.0f / sqrtf(128.0f), out, nsplit,
+                                                              part_o, part_ml);
+    if (nsplit > 1) {
+        const size_t n4 = (size_t)m * h / 4;
+        attn_f32_combine_kernel<<<(uint32_t)std::min<size_t>(kNumSMs * 8, (n4 + 255) / 256), 256, 0, s>>>(
+            part_o, part_ml, nsplit, m, H, out);
+    }
+}
+
 template <uint32_t D>
 static void launch_tiled(const float* q, const float* k, const float* v, const uint32_t* rows, uint32_t m,
                          uint32_t H, float* out, cudaStream_t s) {
-    const size_t smem = ((size_t)(kTR + 2 * kTK) * (D + 4) + kTR * (kTK + 4)) * sizeof(float);
+    const size_t smem = ((size_t)(kTR + 4 * kTK) * (D + 4) + kTR * (kTK + 4)) * sizeof(float);
     static bool attr = false;
     if (!attr) {
         MPIC_CUDA(cudaFuncSetAttribute(attn_simt_tiled_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -448,11 +723,18 @@ static void launch_tiled(const float* q, const float* k, const float* v, const u
 
 void launch_attn_simt(const void* q, const void* k, const void* v, mpic_dtype dt,
                       const uint32_t* rows, uint32_t m, uint32_t H, uint32_t D, void* out,
-                      cudaStream_t s, float* capture, uint32_t T) {
+                      cudaStream_t s, float* capture, uint32_t T, float* scratch, size_t scratch_floats) {
     const uint32_t h = H * D;
     const float inv_sqrt_d = 1.0f / sqrtf((float)D);
     if (dt == MPIC_F32 && !capture && (D == 128 || D == 64)) {
-        if (D == 128) launch_tiled<128>((const float*)q, (const float*)k, (const float*)v, rows, m, H, (float*)out, s);
+        static const bool mt = [] {
+            const char* e = getenv("MPIC_F32_ATTN");  // diagnostics: "tiled" = the 16-row kernel
+            return !(e && std::string(e) == "tiled");
+        }();
+        if (D == 128 && mt)
+            launch_attn_f32_mt((const float*)q, (const float*)k, (const float*)v, rows, m, H, (float*)out, s, scratch,
+                               scratch_floats);
+        else if (D == 128) launch_tiled<128>((const float*)q, (const float*)k, (const float*)v, rows, m, H, (float*)out, s);
         else launch_tiled<64>((const float*)q, (const float*)k, (const float*)v, rows, m, H, (float*)out, s);
         MPIC_LAUNCHED();
         return;
