@@ -80,6 +80,8 @@ int mpic_model_upload(const mpic_model_config* cfg, int device, mpic_dtype dtype
                       const float* const* layer_w, mpic_model_t* out);
 int mpic_model_destroy(mpic_model_t model);
 int mpic_model_config_get(mpic_model_t model, mpic_model_config* out);
+/* The model's device ordinal. */
+int mpic_model_device(mpic_model_t model);
 mpic_dtype mpic_model_dtype(mpic_model_t model);
 /* Copy one weight matrix back to host fp32 (which: 0 emb, 1 lm_head, 2..7 wq wk wv wo
  * w1 w2). Test hook for the bit-exact synthesis check. */
@@ -311,6 +313,38 @@ int mpic_request_prefill_host2(mpic_model_t model, mpic_workspace_t ws, const mp
                                const mpic_policy* policy, const void* const* chunk_k, const void* const* chunk_v,
                                mpic_dtype chunk_dtype, const uint32_t* position_bases, mpic_reposition reposition,
                                mpic_kv_t linked, float* logits, uint32_t* selected, uint32_t* m_out, void* stream);
+
+/* ---- tiered chunk store on the device (CacheStore, proj/include/mpic/cache.h:70-133) ---
+ * Entries are keyed by (content hash, namespace) for the store's model. Device tier: a KV
+ * tensor in HBM in the model dtype; Host tier: pinned memory; Disk tier: a .mpic v3 file
+ * under dir/<hex(ns)>/<fingerprint>/<hex(hash)>.mpic (cache.cpp:198-201; dir NULL or "" =
+ * no disk tier: Host-tier victims are dropped). device_budget / host_budget are entry
+ * counts; the least recently used entry beyond a budget moves one tier down
+ * (cache.cpp:426-461). The per-layer CRC32s of every entry are computed on the GPU when it
+ * enters the store and checked on the GPU after every Host / Disk -> Device promotion. */
+typedef struct mpic_store_s* mpic_store_t;
+typedef enum { MPIC_TIER_DEVICE = 0, MPIC_TIER_HOST = 1, MPIC_TIER_DISK = 2 } mpic_tier;
+int mpic_store_create(mpic_model_t model, const char* dir, uint32_t device_budget, uint32_t host_budget,
+                      mpic_store_t* out);
+int mpic_store_destroy(mpic_store_t store);
+/* put (cache.cpp:203-225): a copy of kv (cast to the model dtype) enters the Device tier. */
+int mpic_store_put(mpic_store_t store, const uint8_t* hash32, const char* ns, mpic_kv_t kv, uint32_t position_base);
+/* tier_of (cache.cpp:249-254): *tier = mpic_tier, or -1 when absent. */
+int mpic_store_tier(mpic_store_t store, const uint8_t* hash32, const char* ns, int* tier);
+/* demote_to (cache.cpp:363-380, test hook): move an entry down to `tier`. */
+int mpic_store_demote(mpic_store_t store, const uint8_t* hash32, const char* ns, int tier);
+int mpic_store_remove(mpic_store_t store, const uint8_t* hash32, const char* ns);
+/* prepare + selective_prefill (transfer.cpp:83-145 with test_transfer.cpp:153-188): every image
+ * chunk of the prompt is fetched into the Device tier (Host / Disk entries copied to HBM and
+ * CRC-checked on the device); a miss, and an entry that fails its checks, is computed on the
+ * device (compute_entry, transfer.cpp:41-58) and stored; then the device-resident MPIC request
+ * runs (mpic_request_prefill). Budgets are enforced after the request. chunk_status (may be
+ * NULL): one mpic_chunk_status per image segment. */
+int mpic_store_request(mpic_store_t store, mpic_workspace_t ws, const mpic_prompt* prompt, const mpic_policy* policy,
+                       const char* ns, mpic_reposition reposition, mpic_kv_t linked, float* logits,
+                       uint32_t* selected, uint32_t* m_out, uint32_t* chunk_status, void* stream);
+/* zlib-compatible CRC32 of n bytes of device memory (the store's GPU CRC). Synchronous. */
+int mpic_crc32_device(const void* d_ptr, size_t n, uint32_t* crc, void* stream);
 
 /* Host-pointer fp32 GEMM on the device: c[M][N] = a[M][K] . b[N][K]^T (SIMT FFMA). Backs the
  * reference's gemm_nt/gemm_nn shims (proj/include/mpic/matmul.h:11-21). Synchronous. */

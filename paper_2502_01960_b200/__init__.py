@@ -18,7 +18,7 @@ import numpy as np
 from ._lib import (ChunkRef, ExtensionMissing, ModelConfig, MpicError, PolicyDesc, PromptDesc,
                    check, lib)
 
-__all__ = ["ModelConfig", "Model", "KV", "Workspace", "Prompt", "MpicError", "ExtensionMissing",
+__all__ = ["ModelConfig", "Model", "KV", "Workspace", "Prompt", "MpicError", "ExtensionMissing", "Store",
            "F32", "BF16", "AS_STORED", "REROTATE", "POLICY_MPIC_K", "POLICY_TEXT_ONLY",
            "POLICY_ALL", "POLICY_PREFIX_ONLY", "config", "fingerprint", "image_token_ids",
            "select_tokens", "flatten_ids", "assemble", "selective_prefill", "prefill_extend",
@@ -359,6 +359,74 @@ def request_prefill_files(model: Model, ws: Workspace, prompt: Prompt, paths, li
 
 
 CHUNK_LOADED, CHUNK_COMPUTED, CHUNK_FALLBACK = 0, 1, 2
+TIER_DEVICE, TIER_HOST, TIER_DISK = 0, 1, 2
+
+
+class Store:
+    """Tiered chunk store on the device (mpic_store_*, CacheStore of
+    proj/include/mpic/cache.h:70-133): Device tier in HBM, Host tier in pinned memory, Disk
+    tier as .mpic v3 files under `dir` (None: no disk tier), LRU demotion by entry-count
+    budgets (cache.cpp:426-461), per-layer CRC32s computed and checked on the GPU."""
+
+    def __init__(self, model: "Model", dir: str | None = None, device_budget: int = 64, host_budget: int = 256):
+        h = C.c_void_p()
+        check(lib().mpic_store_create(model.handle, dir.encode() if dir else None, device_budget, host_budget,
+                                      C.byref(h)))
+        self.handle, self.model = h.value, model
+
+    @staticmethod
+    def _hash(content_hash: bytes):
+        b = bytes(content_hash)
+        assert len(b) == 32
+        return C.create_string_buffer(b, 32)
+
+    def put(self, content_hash: bytes, kv: "KV", position_base: int = 0, ns: str = ""):
+        check(lib().mpic_store_put(self.handle, self._hash(content_hash), ns.encode(), kv.handle, position_base))
+
+    def tier(self, content_hash: bytes, ns: str = "") -> int:
+        """TIER_DEVICE / TIER_HOST / TIER_DISK, or -1 when absent (tier_of)."""
+        t = C.c_int()
+        check(lib().mpic_store_tier(self.handle, self._hash(content_hash), ns.encode(), C.byref(t)))
+        return t.value
+
+    def demote(self, content_hash: bytes, tier: int, ns: str = ""):
+        check(lib().mpic_store_demote(self.handle, self._hash(content_hash), ns.encode(), tier))
+
+    def remove(self, content_hash: bytes, ns: str = ""):
+        check(lib().mpic_store_remove(self.handle, self._hash(content_hash), ns.encode()))
+
+    def request(self, ws: "Workspace", prompt: "Prompt", linked: "KV", policy: int = POLICY_MPIC_K, k: int = 32,
+                global_budget: bool = False, reposition: int = AS_STORED, ns: str = "", stream=None):
+        """prepare + selective_prefill from the store (mpic_store_request). Returns
+        (logits, selected rows, per-image chunk status)."""
+        n_img = int((prompt.kinds == 1).sum())
+        logits = np.zeros(self.model.cfg.vocab_size, np.float32)
+        sel = np.zeros(prompt.n, np.uint32)
+        status = np.zeros(max(n_img, 1), np.uint32)
+        m = C.c_uint32()
+        pol = PolicyDesc(policy, k, int(global_budget))
+        check(lib().mpic_store_request(self.handle, ws.handle, C.byref(prompt.desc()), C.byref(pol), ns.encode(),
+                                       reposition, linked.handle, logits.ctypes.data, sel.ctypes.data, C.byref(m),
+                                       status.ctypes.data, _stream_ptr(stream)))
+        return logits, sel[:m.value].copy(), status[:n_img].copy()
+
+    def close(self):
+        if getattr(self, "handle", None):
+            try:
+                lib().mpic_store_destroy(self.handle)
+            except Exception:  # interpreter shutdown
+                pass
+            self.handle = None
+
+    def __del__(self):
+        self.close()
+
+
+def crc32_device(ptr: int, n: int, stream=None) -> int:
+    """zlib-compatible CRC32 of n bytes at a device address (the store's GPU CRC kernel)."""
+    c = C.c_uint32()
+    check(lib().mpic_crc32_device(ptr, n, C.byref(c), _stream_ptr(stream)))
+    return c.value
 
 
 def write_mpic(path, cfg: ModelConfig, content_hash: bytes, k: np.ndarray, v: np.ndarray,

@@ -69,6 +69,16 @@ SIGNATURES = {
     "mpic_model_destroy": (_int, [_vp]),
     "mpic_model_config_get": (_int, [_vp, _P(ModelConfig)]),
     "mpic_model_dtype": (_int, [_vp]),
+    "mpic_model_device": (_int, [_vp]),
+    "mpic_store_create": (_int, [_vp, C.c_char_p, _u32, _u32, _P(_vp)]),
+    "mpic_store_destroy": (_int, [_vp]),
+    "mpic_store_put": (_int, [_vp, _vp, C.c_char_p, _vp, _u32]),
+    "mpic_store_tier": (_int, [_vp, _vp, C.c_char_p, _P(_int)]),
+    "mpic_store_demote": (_int, [_vp, _vp, C.c_char_p, _int]),
+    "mpic_store_remove": (_int, [_vp, _vp, C.c_char_p]),
+    "mpic_store_request": (_int, [_vp, _vp, _P(PromptDesc), _P(PolicyDesc), C.c_char_p, _int, _vp, _vp, _vp,
+                                  _P(_u32), _vp, _vp]),
+    "mpic_crc32_device": (_int, [_vp, C.c_size_t, _P(_u32), _vp]),
     "mpic_model_download_weight": (_int, [_vp, _int, _u32, _vp]),
     "mpic_kv_alloc": (_int, [_u32, _u32, _u32, _u32, _int, _int, _P(_vp)]),
     "mpic_kv_free": (_int, [_vp]),

@@ -29,6 +29,7 @@ thread_local std::string g_last_error;
 thread_local uint32_t g_launches = 0;
 }  // namespace
 void note_launch(uint32_t n) { g_launches += n; }
+void set_last_error(const std::string& m) { g_last_error = m; }
 bool pdl_enabled() {
     static const bool on = [] {
         const char* e = getenv("MPIC_PDL");
@@ -1239,6 +1240,7 @@ int mpic_model_config_get(mpic_model_t model, mpic_model_config* out) {
 }
 
 mpic_dtype mpic_model_dtype(mpic_model_t model) { return model->dtype; }
+int mpic_model_device(mpic_model_t model) { return model->device; }
 
 int mpic_model_download_weight(mpic_model_t m, int which, uint32_t layer, float* out) {
     API_BEGIN

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
 #include <vector>
 
 #include "mpic_b200.h"
@@ -58,6 +59,8 @@ struct AsmChunk {
     uint32_t src_ld;   // elements per source row (the chunk's H*D); the destination row is H_dst*D
     uint32_t src_col0; // first source column copied (head-parallel: head0 * D)
 };
+
+void set_last_error(const std::string& m);  // the message mpic_last_error() returns
 
 void launch_embed(const float* emb, const int32_t* ids, uint32_t m, uint32_t h, float* x,
                   __nv_bfloat16* xb, cudaStream_t s);
