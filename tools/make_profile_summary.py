@@ -32,8 +32,9 @@ full = subprocess.run(summ + ["full", os.path.join(run, "prof.ncu-rep")], captur
 # combine, Wo, W1, W2)
 rows = [r for r in full.splitlines() if r.startswith("| `")]
 traffic = {}
-roles = {"tc_pgemm_kernel<1>": ["qkv"], "attn_tc_kernel": ["attn"], "attn_combine_kernel": ["combine"],
-         "tc_pgemm_kernel<2>": ["wo", "w2"], "tc_pgemm_kernel<3>": ["w1"]}
+# (pair GEMM instantiations are <MODE, X3>; the bf16 request runs the X3 = false ones)
+roles = {"tc_pgemm_kernel<1, false>": ["qkv"], "attn_tc_kernel": ["attn"], "attn_combine_kernel": ["combine"],
+         "tc_pgemm_kernel<2, false>": ["wo", "w2"], "tc_pgemm_kernel<3, false>": ["w1"]}
 seen = {}
 for r in rows:
     c = [x.strip() for x in r.split("|")]
@@ -42,7 +43,7 @@ for r in rows:
             i = seen.get(key, 0)
             # the capture starts mid-layer: a residual GEMM with ~h*h*2 B of weights is Wo
             dram = (float(c[5]) + float(c[6])) * 1e6
-            if key == "tc_pgemm_kernel<2>":
+            if key == "tc_pgemm_kernel<2, false>":
                 name = "wo" if dram < 80e6 else "w2"
             else:
                 name = names[0]
