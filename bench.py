@@ -602,6 +602,49 @@ def run_ours(args, world, rank, local):
                           "M = 1 token, tcgen05 attention over the cache; host id in, logits out per token"}
         del kvd, wsd
 
+    # ---- miss path: compute_entry of one image chunk on the device
+    # (prefill_extend of its token ids at position base 0, transfer.cpp:41-58: a full causal
+    # prefill of the chunk's tokens on the tcgen05 kernels), and the request with every chunk
+    # missing (mpic_request_prefill_files with no files: the loader's compute lane prefills all
+    # chunks on a side stream while the request consumes them layer by layer)
+    miss = None
+    if args.miss and rank == 0:
+        T0 = images[0]
+        img_hashes = [sg[1] for sg in segs if sg[0] == "image"]
+        wsm = mp.Workspace(model, T0, T0)
+        kvm = mp.KV(L, T0, H, D, mp.BF16, dev)
+        ids0 = mp.image_token_ids(cfg, img_hashes[0], T0)
+        mp.prefill_extend(model, wsm, ids0, 0, 0, kvm, stream=stream)  # warm-up
+        torch.cuda.synchronize()
+        nrep = 3
+        e_m = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e_m[0].record(stream)
+        for _ in range(nrep):
+            mp.prefill_extend(model, wsm, ids0, 0, 0, kvm, stream=stream)
+        e_m[1].record(stream)
+        torch.cuda.synchronize()
+        chunk_ms = e_m[0].elapsed_time(e_m[1]) / nrep
+        fl = L * (2 * T0 * 12 * h * h + 4 * h * T0 * (T0 + 1) / 2)
+        _, _, tf_s, _ = load_peaks()
+        linked_m = mp.KV(L, n, H, D, mp.BF16, dev)
+        none_paths = [None] * len(img_hashes)
+        mp.request_prefill_files(model, ws, prompt, none_paths, linked_m, k=k, stream=stream)  # warm-up
+        torch.cuda.synchronize()
+        walls = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            mp.request_prefill_files(model, ws, prompt, none_paths, linked_m, k=k, stream=stream)
+            torch.cuda.synchronize()
+            walls.append((time.perf_counter() - t0) * 1e3)
+        miss = {"chunk_prefill_ms": round(chunk_ms, 3), "chunk_tokens": T0,
+                "chunk_tflops": round(fl / (chunk_ms / 1e3) / 1e12, 1),
+                "chunk_tensor_frac": round(fl / (chunk_ms / 1e3) / 1e12 / tf_s, 4),
+                "request_all_miss_ms": round(statistics.median(walls), 3), "chunks": len(img_hashes),
+                "path": "prefill_extend of an image chunk's token ids at base 0 (compute_entry) on the tcgen05 "
+                        "kernels; the all-miss request through mpic_request_prefill_files (compute lane concurrent "
+                        "with the request), host wall time"}
+        del wsm, kvm, linked_m
+
     # ---- fp32 mode: the same request at the reference's own precision (fp32 weights, KV and
     # arithmetic: 3xTF32 tcgen05 GEMMs with segmented accumulation + fp32 online-softmax
     # attention; parity 1e-4 vs the reference in tests/test_gpu_llava.py), device-resident
@@ -707,7 +750,7 @@ def run_ours(args, world, rank, local):
         max(sum(gemm_fl.values()) / (tf_sust * 1e12), sum(gemm_b.values()) / (hbm * 1e9)) +
         attn_fl / (tf_sust * 1e12))) * 1e3
     return dict(value=value, ms_per_step=ms_per_step, per_step=per_step, host_ms=host_ms, e2e=e2e,
-                e2e_fp32=e2e_fp32, e2e_disk=e2e_disk, fp32_mode=fp32_mode, k_sweep=sweep, decode=decode,
+                e2e_fp32=e2e_fp32, e2e_disk=e2e_disk, fp32_mode=fp32_mode, k_sweep=sweep, decode=decode, miss=miss,
                 launches=launches, roofline=roofline, phases=per_phase, clocks=clk.summary(),
                 n=n, m=m, floor_ms=floor_ms, world=world)
 
@@ -991,6 +1034,8 @@ def main():
     ap.add_argument("--fp32-mode", action="store_true", default=True,
                     help="also time the request in fp32 mode (the reference's precision)")
     ap.add_argument("--no-fp32-mode", dest="fp32_mode", action="store_false")
+    ap.add_argument("--no-miss", dest="miss", action="store_false", default=True,
+                    help="skip the miss-path key (chunk prefill + all-miss request)")
     ap.add_argument("--decode-steps", type=int, default=8,
                     help="decode tokens timed after the prefill (0: skip)")
     ap.add_argument("--no-serving", action="store_true",
@@ -1119,6 +1164,7 @@ def main():
                 "config": cfg_json,
                 "e2e": r["e2e"], "e2e_fp32_host": r["e2e_fp32"], "e2e_disk": r["e2e_disk"],
                 "fp32_mode": r.get("fp32_mode"), "k_sweep": r.get("k_sweep"), "decode": r.get("decode"),
+                "miss": r.get("miss"),
                 "gpu_launches": r["launches"],
                 "roofline": r["roofline"],
                 "request_roofline_frac": round(r["floor_ms"] / r["ms_per_step"], 4),

@@ -503,38 +503,92 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         // the descriptors live in uniform registers); lane 0 polls the barriers, one elected
         // lane issues each k-block's MMAs back to back. (A lone issuing thread wrapped every
         // tcgen05.mma in an elect/broadcast loop: ~15 instructions of issue overhead per MMA.)
-        if (rank == 0) {
-            const uint32_t idesc0 = X3 ? tc::idesc_tf32(256, a.P0) : tc::idesc_bf16(256, a.P0);
-            const uint32_t idesc1 = X3 ? tc::idesc_tf32(256, a.P1 ? a.P1 : 16) : tc::idesc_bf16(256, a.P1 ? a.P1 : 16);
-            uint32_t item = 0, s = 0, ph = 0, seg = 0;
+        if (rank == 0 && X3) {
+            // 3xTF32: the tile's k range is accumulated in segments of segn stages, alternating
+            // between the two TMEM buffers; the epilogue warps drain each finished segment into
+            // fp32 register sums (round to nearest). The tensor core truncates its fp32
+            // accumulation toward zero at every instruction, so one chain over all of K biases
+            // the result by ~K/16 ulp. Within a segment the small lo*hi and hi*lo products of
+            // all its stages are issued first, while the accumulator is still small, and the
+            // hi*hi products last: only those truncate a full-size partial sum.
+            const uint32_t idesc0 = tc::idesc_tf32(256, a.P0);
+            const uint32_t idesc1 = tc::idesc_tf32(256, a.P1 ? a.P1 : 16);
+            uint32_t s = 0, ph = 0, seg = 0;
+            const uint32_t nit = (kb1 - kb0 + a.kps - 1) / a.kps;
+            for (uint32_t tile = cl; tile < a.tiles; tile += a.clusters) {
+                for (uint32_t it0 = 0; it0 < nit; it0 += a.segn, ++seg) {
+                    const uint32_t nst = min(a.segn, nit - it0);
+                    const uint32_t b = seg & 1, d = tmem + b * a.G;
+                    if (lane == 0) {
+                        tc::mbar_wait_cluster(&acc_empty[b], ((seg >> 1) & 1) ^ 1);
+                        uint32_t s2 = s, ph2 = ph;
+                        for (uint32_t q = 0; q < nst; ++q) {
+                            tc::mbar_wait(&full[s2], ph2);
+                            if (++s2 == a.stages) { s2 = 0; ph2 ^= 1; }
+                        }
+                    }
+                    __syncwarp();
+                    tc::tc_fence_after();
+                    if (tc::elect_one_sync()) {
+                        bool first = true;
+                        for (uint32_t pass = 0; pass < 2; ++pass) {
+                            uint32_t s2 = s;
+                            for (uint32_t q = 0; q < nst; ++q) {
+                                const uint32_t nsub = min(a.kps, kb1 - (kb0 + (it0 + q) * a.kps));
+                                for (uint32_t j = 0; j < nsub && !(a.dbg & 8); ++j) {
+                                    const uint32_t w_base = tc::smem_u32(smem + s2 * a.stage_bytes + j * a.sub_bytes);
+                                    const uint32_t x_base = w_base + a.wsub;
+#pragma unroll
+                                    for (uint32_t kk = 0; kk < 4; ++kk) {
+                                        const uint64_t ahi = tc::desc_k_sw128(w_base + kk * 32);
+                                        const uint64_t alo = tc::desc_k_sw128(w_base + kPgWBytes + kk * 32);
+#pragma unroll
+                                        for (uint32_t pc = 0; pc < 2; ++pc) {
+                                            if (pc && !a.P1) break;
+                                            const uint32_t xo = pc ? a.xoff1 : 0u, dd = pc ? d + a.P0 : d;
+                                            const uint32_t id = pc ? idesc1 : idesc0;
+                                            const uint64_t xh = tc::desc_k_sw128(x_base + xo + kk * 32);
+                                            if (pass == 0) {
+                                                tc::mma_tf32_pair(dd, alo, xh, id, first ? 0u : 1u);
+                                                tc::mma_tf32_pair(dd, ahi, tc::desc_k_sw128(x_base + a.xlo + xo + kk * 32),
+                                                                  id, 1u);
+                                            } else {
+                                                tc::mma_tf32_pair(dd, ahi, xh, id, 1u);
+                                            }
+                                        }
+                                        first = false;
+                                    }
+                                }
+                                if (++s2 == a.stages) s2 = 0;
+                            }
+                        }
+                        uint32_t s2 = s;
+                        for (uint32_t q = 0; q < nst; ++q) {
+                            tc::mma_commit_pair_mcast(&empty[s2], pair_mask);
+                            if (++s2 == a.stages) s2 = 0;
+                        }
+                        tc::mma_commit_pair_mcast(&acc_full[b], pair_mask);
+                    }
+                    __syncwarp();
+                    for (uint32_t q = 0; q < nst; ++q)
+                        if (++s == a.stages) { s = 0; ph ^= 1; }
+                }
+            }
+        } else if (rank == 0) {
+            const uint32_t idesc0 = tc::idesc_bf16(256, a.P0);
+            const uint32_t idesc1 = tc::idesc_bf16(256, a.P1 ? a.P1 : 16);
+            uint32_t item = 0, s = 0, ph = 0;
             long long mw = 0;
             const long long m0 = clock64();
             for (uint32_t tile = cl; tile < a.tiles; tile += a.clusters, ++item) {
-                uint32_t b = a.nbuf == 2 ? (item & 1) : 0u;
+                const uint32_t b = a.nbuf == 2 ? (item & 1) : 0u;
                 const uint32_t use = a.nbuf == 2 ? (item >> 1) : item;
-                if (!X3) {
-                    if (lane == 0) tc::mbar_wait_cluster(&acc_empty[b], (use & 1) ^ 1);
-                    __syncwarp();
-                    tc::tc_fence_after();
-                }
-                uint32_t d = tmem + b * a.G;
-                uint32_t it = 0;
-                for (uint32_t kb = kb0; kb < kb1; kb += a.kps, ++it) {
+                if (lane == 0) tc::mbar_wait_cluster(&acc_empty[b], (use & 1) ^ 1);
+                __syncwarp();
+                tc::tc_fence_after();
+                const uint32_t d = tmem + b * a.G;
+                for (uint32_t kb = kb0; kb < kb1; kb += a.kps) {
                     const uint32_t nsub = min(a.kps, kb1 - kb);
-                    // 3xTF32: the tile's k range is accumulated in segments of segn stage
-                    // iterations, alternating between the two TMEM buffers; the epilogue warps
-                    // drain each finished segment into fp32 register sums (round to nearest).
-                    // The tensor core rounds its accumulation toward zero, so one chain over
-                    // all of K (3 x K/8 instructions) biases the result by ~K/16 ulp.
-                    const bool seg_first = X3 && it % a.segn == 0;
-                    const bool seg_last = X3 && ((it + 1) % a.segn == 0 || kb + a.kps >= kb1);
-                    if (seg_first) {
-                        b = seg & 1;
-                        d = tmem + b * a.G;
-                        if (lane == 0) tc::mbar_wait_cluster(&acc_empty[b], ((seg >> 1) & 1) ^ 1);
-                        __syncwarp();
-                        tc::tc_fence_after();
-                    }
                     const long long w0 = ts ? clock64() : 0;
                     if (lane == 0) tc::mbar_wait(&full[s], ph);
                     __syncwarp();
@@ -547,33 +601,18 @@ __global__ void __launch_bounds__(kPgThreads, 1)
 #pragma unroll
                             for (uint32_t kk = 0; kk < 4; ++kk) {
                                 const uint64_t adesc = tc::desc_k_sw128(w_base + kk * 32);
-                                const uint32_t acc = (X3 ? (!seg_first || j > 0) : kb + j > kb0) || kk > 0 ? 1u : 0u;
-                                if constexpr (X3) {
-                                    const uint64_t alo = tc::desc_k_sw128(w_base + kPgWBytes + kk * 32);
-#pragma unroll
-                                    for (uint32_t pc = 0; pc < 2; ++pc) {
-                                        if (pc && !a.P1) break;
-                                        const uint32_t xo = pc ? a.xoff1 : 0u, dd = pc ? d + a.P0 : d;
-                                        const uint32_t id = pc ? idesc1 : idesc0;
-                                        tc::mma_tf32_pair(dd, alo, tc::desc_k_sw128(x_base + xo + kk * 32), id, acc);
-                                        tc::mma_tf32_pair(dd, adesc, tc::desc_k_sw128(x_base + a.xlo + xo + kk * 32), id, 1u);
-                                        tc::mma_tf32_pair(dd, adesc, tc::desc_k_sw128(x_base + xo + kk * 32), id, 1u);
-                                    }
-                                } else {
-                                    tc::mma_bf16_pair(d, adesc, tc::desc_k_sw128(x_base + kk * 32), idesc0, acc);
-                                    if (a.P1)
-                                        tc::mma_bf16_pair(d + a.P0, adesc, tc::desc_k_sw128(x_base + a.xoff1 + kk * 32),
-                                                          idesc1, acc);
-                                }
+                                const uint32_t acc = (kb + j > kb0 || kk > 0) ? 1u : 0u;
+                                tc::mma_bf16_pair(d, adesc, tc::desc_k_sw128(x_base + kk * 32), idesc0, acc);
+                                if (a.P1)
+                                    tc::mma_bf16_pair(d + a.P0, adesc, tc::desc_k_sw128(x_base + a.xoff1 + kk * 32),
+                                                      idesc1, acc);
                             }
                         }
                         tc::mma_commit_pair_mcast(&empty[s], pair_mask);
-                        if (seg_last) tc::mma_commit_pair_mcast(&acc_full[b], pair_mask);
                     }
-                    if (seg_last) ++seg;
                     if (++s == a.stages) { s = 0; ph ^= 1; }
                 }
-                if (!X3 && tc::elect_one_sync()) tc::mma_commit_pair_mcast(&acc_full[b], pair_mask);
+                if (tc::elect_one_sync()) tc::mma_commit_pair_mcast(&acc_full[b], pair_mask);
                 if (ts && lane == 0) ts[2] = gtimer();
             }
             if (ts && lane == 0) {
@@ -1005,7 +1044,8 @@ void launch_pgemm_impl(const void* A, const void* A_lo, const void* W, const voi
         }();
         // default 1 k-block (12 MMAs per chain): at config C's 32 layers 2 k-blocks left the
         // logits at 0.97 of the fp64-referenced gate, 1 k-block at 0.27
-        if (x3) a.segn = std::max(1u, seg_kb / a.kps);
+        if (x3) a.segn = std::min(std::max(1u, seg_kb / a.kps), a.stages - 1);  // (a segment's stages are all
+                                                                                // resident before its MMAs)
         a.w_evict_first = a.ngroups == 1;
         a.ep = ep_in;
     a.ep.dbg = dbg;

@@ -33,8 +33,8 @@ full = subprocess.run(summ + ["full", os.path.join(run, "prof.ncu-rep")], captur
 rows = [r for r in full.splitlines() if r.startswith("| `")]
 traffic = {}
 # (pair GEMM instantiations are <MODE, X3>; the bf16 request runs the X3 = false ones)
-roles = {"tc_pgemm_kernel<1, false>": ["qkv"], "attn_tc_kernel": ["attn"], "attn_combine_kernel": ["combine"],
-         "tc_pgemm_kernel<2, false>": ["wo", "w2"], "tc_pgemm_kernel<3, false>": ["w1"]}
+roles = {"tc_pgemm_kernel<1, 0>": ["qkv"], "attn_tc_kernel": ["attn"], "attn_combine_kernel": ["combine"],
+         "tc_pgemm_kernel<2, 0>": ["wo", "w2"], "tc_pgemm_kernel<3, 0>": ["w1"]}
 seen = {}
 for r in rows:
     c = [x.strip() for x in r.split("|")]
@@ -43,7 +43,7 @@ for r in rows:
             i = seen.get(key, 0)
             # the capture starts mid-layer: a residual GEMM with ~h*h*2 B of weights is Wo
             dram = (float(c[5]) + float(c[6])) * 1e6
-            if key == "tc_pgemm_kernel<2, false>":
+            if key == "tc_pgemm_kernel<2, 0>":
                 name = "wo" if dram < 80e6 else "w2"
             else:
                 name = names[0]
@@ -61,7 +61,9 @@ INTRO = {
         "one MMA-issuing warp per lane with warp-uniform elect.sync issue, TMA bulk-store linking, coalesced",
         "partials; the pair GEMM's MMA warp made warp-uniform; loader fault semantics of `prepare` on the fast",
         "paths (v3 per-layer CRCs, compute lane); `mpic_hp_request` with NCCL inside the library; fp32-mode",
-        "and config-D k-sweep bench keys (DESIGN.md)."],
+        "and config-D k-sweep bench keys; fp32 mode on the tensor cores (3xTF32 pair GEMM with segmented",
+        "accumulation) and a register-tiled fp32 attention (fp32 request 455 -> 78 ms); the tiered chunk store",
+        "(`mpic_store_*`, Device tier in HBM, GPU CRC32) (DESIGN.md)."],
 }
 out = [f"# Round {rnd} — final state", "",
        f"B200, 1 GPU. `tools/gpu_final.sh {tag}` on one fresh box: GPU tests, smoke, the reference's own suites",
