@@ -229,6 +229,18 @@ struct mpic_workspace_s {
     // that are missing or fail to load are prefilled on their own stream and workspace
     mpic_workspace_s* aux = nullptr;
     cudaStream_t miss_stream = nullptr;
+    // the compute lane's chunk buffers, kept across requests (allocating and freeing ~1 GB
+    // chunk tensors per request cost more than computing them)
+    struct MissBuf {
+        void* k = nullptr;
+        void* v = nullptr;
+        int32_t* d_ids = nullptr;
+        uint32_t* d_rows = nullptr;
+        size_t bytes = 0;
+        uint32_t rows = 0;
+        std::vector<cudaEvent_t> ev;
+    };
+    std::vector<MissBuf> miss_pool;
     // head-parallel request inside the library (mpic_hp_request): Wo partials [m_pad][h] and
     // this rank's reduced rows [mr][h] (fp32), and the captured layer loop
     float* hp_partial = nullptr;
@@ -1029,6 +1041,8 @@ struct MissLane {
         std::vector<uint32_t> rows;
         int32_t* d_ids = nullptr;
         uint32_t* d_rows = nullptr;
+        size_t cap_bytes = 0;  // capacities of the (pooled) buffers
+        uint32_t cap_rows = 0;
     };
     mpic_model_t md;
     mpic_workspace_t ws;
@@ -1039,12 +1053,16 @@ struct MissLane {
         if (jobs.empty()) return;
         cudaStreamSynchronize(ws->miss_stream);
         cudaStreamSynchronize(ws->copy_stream);  // its layer copies read the chunk buffers
-        for (auto& j : jobs) {
-            cudaFree(j->kv.k);
-            cudaFree(j->kv.v);
-            cudaFree(j->d_ids);
-            cudaFree(j->d_rows);
-            for (cudaEvent_t e : j->ev) cudaEventDestroy(e);
+        for (auto& j : jobs) {  // back to the workspace's pool
+            mpic_workspace_s::MissBuf b;
+            b.k = j->kv.k;
+            b.v = j->kv.v;
+            b.d_ids = j->d_ids;
+            b.d_rows = j->d_rows;
+            b.bytes = j->cap_bytes;
+            b.rows = j->cap_rows;
+            b.ev = std::move(j->ev);
+            ws->miss_pool.push_back(std::move(b));
         }
     }
     Job* find(uint32_t chunk) const {
@@ -1080,16 +1098,39 @@ struct MissLane {
         j.kv.dtype = md->dtype;
         j.kv.device = md->device;
         const size_t bytes = j.kv.elems() * esz(md->dtype);
-        MPIC_CUDA(cudaMalloc(&j.kv.k, bytes));
-        MPIC_CUDA(cudaMalloc(&j.kv.v, bytes));
-        MPIC_CUDA(cudaMalloc(&j.d_ids, T * sizeof(int32_t)));
-        MPIC_CUDA(cudaMalloc(&j.d_rows, T * sizeof(uint32_t)));
+        auto& pool = ws->miss_pool;
+        size_t pick = pool.size();
+        for (size_t i = 0; i < pool.size(); ++i)  // the smallest pooled buffer set that fits
+            if (pool[i].bytes >= bytes && pool[i].rows >= T && pool[i].ev.size() >= c.n_layers &&
+                (pick == pool.size() || pool[i].bytes < pool[pick].bytes))
+                pick = i;
+        if (pick < pool.size()) {
+            mpic_workspace_s::MissBuf& b = pool[pick];
+            j.kv.k = b.k;
+            j.kv.v = b.v;
+            j.d_ids = b.d_ids;
+            j.d_rows = b.d_rows;
+            j.cap_bytes = b.bytes;
+            j.cap_rows = b.rows;
+            j.ev = std::move(b.ev);
+            pool.erase(pool.begin() + (ptrdiff_t)pick);
+        } else {
+            MPIC_CUDA(cudaMalloc(&j.kv.k, bytes));
+            MPIC_CUDA(cudaMalloc(&j.kv.v, bytes));
+            MPIC_CUDA(cudaMalloc(&j.d_ids, T * sizeof(int32_t)));
+            MPIC_CUDA(cudaMalloc(&j.d_rows, T * sizeof(uint32_t)));
+            j.cap_bytes = bytes;
+            j.cap_rows = T;
+        }
         j.ids.resize(T);
         image_ids(&c, hash32, T, j.ids.data());  // model.cpp:148-156
         j.rows.resize(T);
         for (uint32_t i = 0; i < T; ++i) j.rows[i] = i;  // rows == positions: base 0
-        j.ev.resize(c.n_layers);
-        for (cudaEvent_t& e : j.ev) MPIC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        while (j.ev.size() < c.n_layers) {
+            cudaEvent_t e;
+            MPIC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            j.ev.push_back(e);
+        }
         cudaStream_t st = ws->miss_stream;
         MPIC_CUDA(cudaMemcpyAsync(j.d_ids, j.ids.data(), T * 4, cudaMemcpyHostToDevice, st));
         MPIC_CUDA(cudaMemcpyAsync(j.d_rows, j.rows.data(), T * 4, cudaMemcpyHostToDevice, st));
@@ -1485,6 +1526,13 @@ int mpic_workspace_destroy(mpic_workspace_t ws) {
             cudaStreamDestroy(ws->miss_stream);
         }
         if (ws->aux) mpic_workspace_destroy(ws->aux);
+        for (auto& b : ws->miss_pool) {
+            cudaFree(b.k);
+            cudaFree(b.v);
+            cudaFree(b.d_ids);
+            cudaFree(b.d_rows);
+            for (cudaEvent_t e : b.ev) cudaEventDestroy(e);
+        }
         cudaFree(ws->hp_partial);
         cudaFree(ws->hp_reduced);
         if (ws->hp_graph) cudaGraphExecDestroy(ws->hp_graph);

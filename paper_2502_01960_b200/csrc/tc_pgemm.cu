@@ -1040,10 +1040,11 @@ void launch_pgemm_impl(const void* A, const void* A_lo, const void* W, const voi
         if (a.stages < 2) continue;
         static const uint32_t seg_kb = [] {
             const char* e = getenv("MPIC_X3_SEG");  // diagnostics: k-blocks (32 K) per accumulation segment
-            return e ? std::max(1, atoi(e)) : 1;
+            return e ? std::max(1, atoi(e)) : 2;
         }();
-        // default 1 k-block (12 MMAs per chain): at config C's 32 layers 2 k-blocks left the
-        // logits at 0.97 of the fp64-referenced gate, 1 k-block at 0.27
+        // default 2 k-blocks (64 K): with the small products issued first, config C's 32-layer
+        // logits sit at 0.11 of the fp64-referenced gate and the fp32 GEMMs take 30 ms per
+        // request (1 k-block: 40 ms, drain-bound; 4: slower, fewer stages in flight)
         if (x3) a.segn = std::min(std::max(1u, seg_kb / a.kps), a.stages - 1);  // (a segment's stages are all
                                                                                 // resident before its MMAs)
         a.w_evict_first = a.ngroups == 1;
