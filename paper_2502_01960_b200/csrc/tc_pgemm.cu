@@ -993,13 +993,17 @@ void launch_pgemm_impl(const void* A, const void* A_lo, const void* W, const voi
     // 3xTF32: two TMEM buffers of G columns and the epilogue's register sums cap G at 192
     const uint32_t gcap = x3 ? 192u : 256u;
     const uint32_t ng_nat = x3 ? ceil_div(M, gcap) : M <= 512 ? 1 : ceil_div(M, 256);
-    for (uint32_t gm : {1u, 2u, 3u}) {
+    // candidates: 1-3x the natural group count, and (3xTF32) one group more — m = 330 as 3 x 112
+    // tokens fills two rounds of 74 pairs with 144 QKV tiles where 2 x 176 leave the second
+    // round 30% full
+    for (uint32_t gm : {1u, 2u, 3u, 0u}) {
+        if (gm == 0 && !x3) continue;
         PgArgs a{};
         a.M = M;
         a.N = N;
         a.K = K;
         a.dbg = dbg;
-        a.ngroups = ng_nat * gm;
+        a.ngroups = gm ? ng_nat * gm : ng_nat + 1;
         if (!x3 && a.ngroups == 1 && M > 256 && M <= group_max) {
             a.P0 = round16((M + 1) / 2);
             a.P1 = round16(M - a.P0);
@@ -1007,7 +1011,7 @@ void launch_pgemm_impl(const void* A, const void* A_lo, const void* W, const voi
             if (a.ngroups == 1 && M > 256) continue;  // MPIC_PG_GROUP=256 diagnostics
             a.P0 = round16(ceil_div(M, a.ngroups));
             a.P1 = 0;
-            if (a.P0 > gcap || (gm > 1 && a.P0 < 64)) continue;
+            if (a.P0 > gcap || (gm != 1 && a.P0 < 64)) continue;
             // two interleaved accumulator chains (off by default: each cta_group::2 MMA costs at
             // least ~83 cycles, so halving N loses more than the interleave gains)
             if (split_pieces && !x3 && a.P0 >= 64) {
