@@ -86,6 +86,7 @@ struct PgArgs {
     uint32_t prologue_pf;  // prefetch the first k-blocks' weights into L2 before the PDL wait
     uint32_t stg_off;    // staged epilogue stores: byte offset of the 8 x 4 KB warp slices in the
                          // (then idle) stage ring, or kNoStage
+    uint32_t w_early;    // weights of the first ring stages loaded before the PDL wait
     uint32_t kel;        // K elements per k-block (one 128-B operand row): 64 bf16, 32 fp32 (3xTF32)
     uint32_t wsub;       // weight bytes of a k-block: 16 KB, 32 KB with the 3xTF32 hi and lo tiles
     uint32_t xlo;        // 3xTF32: byte offset of the token rows' lo tile from their hi tile
@@ -431,42 +432,59 @@ __global__ void __launch_bounds__(kPgThreads, 1)
     tc::tc_fence_before();
     tc::cluster_sync();
     tc::tc_fence_after();
+    const uint32_t xbytes = (a.dbg & 2) ? 0u : a.sub_bytes - a.wsub;
+    const uint32_t wbytes = (a.dbg & 4) ? 0u : a.wsub;
+    const uint64_t pol_w = a.w_evict_first ? tc::policy_evict_first() : tc::policy_evict_last();
+    const uint32_t leader_full = tc::mapa_shared(tc::smem_u32(full), crank & ~1u);
+    // one k-block of weights (hi, and the lo tile in 3xTF32) of feature block fb into stage st
+    auto load_w = [&](uint8_t* st, uint32_t bar, uint32_t fb, uint32_t kbj) {
+        if (!wbytes) return;
+        const int k = (int)(kbj * a.kel), w_row = (int)(fb * 256 + rank * 128);
+        if (X3) tc::tma_load_2d_cg2(st + kPgWBytes, &tmWl, bar, k, w_row, pol_w);
+        if (a.w_blocked)  // one contiguous 16 KB tile per box
+            tc::tma_load_2d_cg2(st, &tmW, bar, 0, (int)(((2 * fb + rank) * a.kblocks + kbj) * 128), pol_w);
+        else
+            tc::tma_load_2d_cg2(st, &tmW, bar, k, w_row, pol_w);
+    };
+    // Weights do not depend on the previous kernel: the producer fills the weight half of the
+    // first ring stages before waiting for it (their barriers expect the full stage), so after
+    // the wait only the token rows (L2-resident activations) remain on the critical path.
+    uint32_t early = 0;
+    if (warp == 0 && lane == 0 && a.w_early && cl < a.tiles) {
+        const uint32_t fb = cl / a.ngroups;
+        for (uint32_t kb = kb0; kb < kb1 && early < a.stages; kb += a.kps, ++early) {
+            const uint32_t nsub = min(a.kps, kb1 - kb);
+            if (rank == 0) tc::mbar_arrive_expect_tx(&full[early], 2 * nsub * (xbytes + wbytes));
+            for (uint32_t j = 0; j < nsub; ++j)
+                load_w(smem + early * a.stage_bytes + j * a.sub_bytes, leader_full + early * 8, fb, kb + j);
+        }
+    }
     tc::pdl_wait();  // the previous kernel's outputs (this GEMM's X, its output buffers) are ready
     if (ts && threadIdx.x == 0) ts[1] = gtimer();
     const uint32_t tmem = *tmem_holder;
 
     if (warp == 0) {
         if (lane == 0) {
-            const uint64_t pol_w = a.w_evict_first ? tc::policy_evict_first() : tc::policy_evict_last();
             const uint64_t pol_x = tc::policy_evict_last();
-            const uint32_t xbytes = (a.dbg & 2) ? 0u : a.sub_bytes - a.wsub;
-            const uint32_t wbytes = (a.dbg & 4) ? 0u : a.wsub;
             const int xr0 = (int)(rank * (a.P0 / 2)), xr1 = (int)(a.P0 + rank * (a.P1 / 2));
             long long pw = 0;
             const long long p0 = clock64();
-            const uint32_t leader_full = tc::mapa_shared(tc::smem_u32(full), crank & ~1u);
-            uint32_t s = 0, ph = 0;
+            uint32_t s = 0, ph = 0, it = 0;
             for (uint32_t tile = cl; tile < a.tiles; tile += a.clusters) {
                 const uint32_t fb = tile / a.ngroups, g = tile % a.ngroups;
-                const int t0 = (int)(g * a.G), w_row = (int)(fb * 256 + rank * 128);
-                for (uint32_t kb = kb0; kb < kb1; kb += a.kps) {
+                const int t0 = (int)(g * a.G);
+                for (uint32_t kb = kb0; kb < kb1; kb += a.kps, ++it) {
                     const uint32_t nsub = min(a.kps, kb1 - kb);
+                    const bool pre = it < early;  // weights already issued before the PDL wait
                     const long long w0 = ts ? clock64() : 0;
-                    tc::mbar_wait(&empty[s], ph ^ 1);
+                    if (!pre) tc::mbar_wait(&empty[s], ph ^ 1);
                     if (ts) pw += clock64() - w0;
-                    if (rank == 0) tc::mbar_arrive_expect_tx(&full[s], 2 * nsub * (xbytes + wbytes));
+                    if (rank == 0 && !pre) tc::mbar_arrive_expect_tx(&full[s], 2 * nsub * (xbytes + wbytes));
                     const uint32_t bar = leader_full + s * 8;
                     for (uint32_t j = 0; j < nsub; ++j) {
                         uint8_t* st = smem + s * a.stage_bytes + j * a.sub_bytes;
                         const int k = (int)((kb + j) * a.kel);
-                        if (X3 && wbytes) tc::tma_load_2d_cg2(st + kPgWBytes, &tmWl, bar, k, w_row, pol_w);
-                        if (wbytes) {
-                            if (a.w_blocked)  // one contiguous 16 KB tile per box
-                                tc::tma_load_2d_cg2(st, &tmW, bar, 0, (int)(((2 * fb + rank) * a.kblocks + kb + j) * 128),
-                                                    pol_w);
-                            else
-                                tc::tma_load_2d_cg2(st, &tmW, bar, k, w_row, pol_w);
-                        }
+                        if (!pre) load_w(st, bar, fb, kb + j);
                         if (a.pfd) {
                             // keep the weight stream pfd k-blocks ahead of the smem ring in L2
                             // (DRAM latency hidden without spending shared memory on it);
@@ -1115,6 +1133,13 @@ void launch_pgemm_impl(const void* A, const void* A_lo, const void* W, const voi
         return e && atoi(e) != 0;
     }();
     a.prologue_pf = prologue_pf && !x3 ? 1u : 0u;
+    // Off by default, like the L2 prefetch: config B 4.00 -> 4.04 ms and config C unchanged with
+    // it (the early weight stream competes with the previous kernel's tail).
+    static const bool w_early = [] {
+        const char* e = getenv("MPIC_PG_WEARLY");  // diagnostics: 1 = first stages' weights before the PDL wait
+        return e && atoi(e) != 0;
+    }();
+    a.w_early = w_early ? 1u : 0u;
 
     const size_t smem = (size_t)a.stages * a.stage_bytes + 1024 + (2 * a.stages + 4 + kEpiBars) * 8 + 16;
     static const bool verbose = getenv("MPIC_PG_VERBOSE") != nullptr;
