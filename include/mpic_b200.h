@@ -225,7 +225,9 @@ int mpic_request_prefill(mpic_model_t model, mpic_workspace_t ws, const mpic_pro
  * the prompt's image hash, a short read or a CRC mismatch is a fallback
  * (MPIC_CHUNK_FALLBACK). Either way the chunk is computed on the device (compute_entry,
  * transfer.cpp:41-58) on a side stream concurrently with the loads, and the request uses
- * it layer by layer. v3 layers are CRC-checked before their H2D; a v1/v2 file CRC is known
+ * it layer by layer. Every loaded layer is CRC-checked on the GPU right after its H2D (v3:
+ * against the per-layer table; MPIC_FILES_CRC=host checks v3 layers on the reader threads
+ * before the H2D instead); the per-layer and file CRCs are known
  * only after the last layer, and a mismatch re-runs the request with the chunk computed:
  * the outputs never come from a corrupt chunk. chunk_status (may be NULL) receives one
  * mpic_chunk_status per image segment. */
@@ -345,6 +347,10 @@ int mpic_store_request(mpic_store_t store, mpic_workspace_t ws, const mpic_promp
                        uint32_t* selected, uint32_t* m_out, uint32_t* chunk_status, void* stream);
 /* zlib-compatible CRC32 of n bytes of device memory (the store's GPU CRC). Synchronous. */
 int mpic_crc32_device(const void* d_ptr, size_t n, uint32_t* crc, void* stream);
+/* Per-plane CRC32s of n_planes consecutive planes of plane_bytes bytes of device memory, as
+ * the disk loader computes them after each layer's H2D (128 KB pieces, one warp each for
+ * plane_bytes % 4096 == 0, combined on the host). Synchronous. */
+int mpic_crc32_planes_device(const void* d_ptr, size_t plane_bytes, uint32_t n_planes, uint32_t* crcs, void* stream);
 
 /* Host-pointer fp32 GEMM on the device: c[M][N] = a[M][K] . b[N][K]^T (SIMT FFMA). Backs the
  * reference's gemm_nt/gemm_nn shims (proj/include/mpic/matmul.h:11-21). Synchronous. */

@@ -422,6 +422,13 @@ class Store:
         self.close()
 
 
+def crc32_planes_device(ptr: int, plane_bytes: int, n_planes: int, stream=None) -> list:
+    """Per-plane CRC32s of consecutive device planes, computed as the disk loader does."""
+    out = np.zeros(max(n_planes, 1), np.uint32)
+    check(lib().mpic_crc32_planes_device(ptr, plane_bytes, n_planes, out.ctypes.data, _stream_ptr(stream)))
+    return [int(x) for x in out[:n_planes]]
+
+
 def crc32_device(ptr: int, n: int, stream=None) -> int:
     """zlib-compatible CRC32 of n bytes at a device address (the store's GPU CRC kernel)."""
     c = C.c_uint32()
@@ -433,7 +440,7 @@ def write_mpic(path, cfg: ModelConfig, content_hash: bytes, k: np.ndarray, v: np
                position_base: int = 0, ns: str = "", bf16: bool = False, layer_crcs: bool = True):
     """Write one chunk as a .mpic container (proj/src/cache.cpp:97-125): an fp32 or a bf16
     payload (uint16 bit patterns), then — layer_crcs=True, version 3 — a table of per-layer
-    CRC32s (crc_k[L], crc_v[L]; the disk loader verifies each layer before its H2D), then the
+    CRC32s (crc_k[L], crc_v[L]; the disk loader verifies each layer on the GPU), then the
     CRC32 of all preceding bytes. layer_crcs=False writes v1 (fp32, the reference's own
     format) or v2 (bf16)."""
     import struct

@@ -79,6 +79,7 @@ SIGNATURES = {
     "mpic_store_request": (_int, [_vp, _vp, _P(PromptDesc), _P(PolicyDesc), C.c_char_p, _int, _vp, _vp, _vp,
                                   _P(_u32), _vp, _vp]),
     "mpic_crc32_device": (_int, [_vp, C.c_size_t, _P(_u32), _vp]),
+    "mpic_crc32_planes_device": (_int, [_vp, C.c_size_t, _u32, _vp, _vp]),
     "mpic_model_download_weight": (_int, [_vp, _int, _u32, _vp]),
     "mpic_kv_alloc": (_int, [_u32, _u32, _u32, _u32, _int, _int, _P(_vp)]),
     "mpic_kv_free": (_int, [_vp]),

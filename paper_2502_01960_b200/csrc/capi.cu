@@ -2560,6 +2560,7 @@ struct MpicFile {
     uint32_t crc_stored = 0, crc_header = 0;
     std::vector<uint32_t> table;      // v3: crc_k[L] then crc_v[L]
     std::vector<uint32_t> crc_piece;  // [2][L][pieces] CRCs of the pieces as read
+    std::vector<uint32_t> layer_crc;  // [2][L] per-layer CRCs computed on the GPU
     ~MpicFile() {
         if (fd >= 0) close(fd);
     }
@@ -2734,8 +2735,29 @@ int files_pass(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* promp
     const uint32_t n_items = n_seg * pieces;
     const uint32_t n_threads = n_items ? std::max<uint32_t>(1, std::min<uint32_t>(n_items, want)) : 0;
     for (uint32_t i : loaded) files[i]->crc_piece.assign(2 * (size_t)L * pieces, 0);
+    // CRCs on the GPU (default): every loaded layer is checksummed in HBM right after its H2D,
+    // on the copy stream, so the reader threads only move bytes (the host CRC pass cost ~45% of
+    // a page-cache-warm request at config C); the per-layer (v3) and file CRCs are compared
+    // once the request has run, and a mismatch re-runs it with that chunk computed — as for a
+    // v1/v2 file CRC — so the outputs never come from corrupt bytes. MPIC_FILES_CRC=host checks
+    // on the reader threads before each H2D instead.
+    static const bool gpu_crc_env = [] {
+        const char* e = getenv("MPIC_FILES_CRC");
+        return !(e && std::string(e) == "host");
+    }();
+    const bool gpu_crc = gpu_crc_env;
+    constexpr uint32_t kFilePiece = 128 * 1024;
+    std::vector<size_t> pc_off(n_img, 0);  // chunk i's first piece in d_pcrc ([2][L][ppp_i])
+    size_t n_pc = 0;
+    for (uint32_t i : loaded) {
+        pc_off[i] = n_pc;
+        n_pc += 2 * (size_t)L * ceil_div((size_t)files[i]->T * h * es, (size_t)kFilePiece);
+    }
+    uint32_t* d_pcrc = nullptr;
+    if (gpu_crc && n_pc) MPIC_CUDA(cudaMallocAsync((void**)&d_pcrc, n_pc * 4, ws->copy_stream));
     auto seg_crc = [&](const MpicFile& f, uint32_t is_v, uint32_t l) {
         const size_t seg = (size_t)f.T * h * es;
+        if (gpu_crc) return f.layer_crc[is_v * L + l];
         uLong c = f.crc_piece[((size_t)is_v * L + l) * pieces];
         for (uint32_t pc = 1; pc < pieces; ++pc) {
             const size_t p0 = seg * pc / pieces, p1 = seg * (pc + 1) / pieces;
@@ -2766,14 +2788,14 @@ int files_pass(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* promp
                     const size_t p0 = seg * pc / pieces, p1 = seg * (pc + 1) / pieces;
                     char* d = dst + ((is_v ? img_rows * h : 0) + off[i]) * es + p0;
                     pread_all(f.fd, d, p1 - p0, (off_t)(84 + ((is_v ? (size_t)L : 0) + l) * seg + p0));
-                    f.crc_piece[((size_t)is_v * L + l) * pieces + pc] = crc_of(d, p1 - p0);
+                    if (!gpu_crc) f.crc_piece[((size_t)is_v * L + l) * pieces + pc] = crc_of(d, p1 - p0);
                 }
                 {
                     std::lock_guard<std::mutex> lk(mu);
                     if (++done[l] == n_threads) {
                         for (uint32_t i : loaded) {  // v3: verify the layer before it is used
                             const MpicFile& f = *files[i];
-                            if (f.version == 3 && bad_chunk < 0 &&
+                            if (f.version == 3 && bad_chunk < 0 && !gpu_crc &&
                                 (seg_crc(f, 0, l) != f.table[l] || seg_crc(f, 1, l) != f.table[L + l]))
                                 bad_chunk = (int)i;
                         }
@@ -2830,6 +2852,13 @@ int files_pass(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* promp
         for (const auto& j : lane.jobs)
             lane.copy_layer(*j, l, stage + off[j->chunk] * es, stage + (img_rows * h + off[j->chunk]) * es, ct, cs);
         MPIC_CUDA(cudaEventRecord(ws->ev_ready[sl], cs));
+        if (d_pcrc)  // this layer's loaded K / V planes, checksummed in HBM behind the copy
+            for (uint32_t i : loaded) {
+                const size_t seg = (size_t)files[i]->T * h * es, ppp = ceil_div(seg, (size_t)kFilePiece);
+                launch_crc32_pieces(stage + off[i] * es, seg, 1, kFilePiece, d_pcrc + pc_off[i] + l * ppp, cs);
+                launch_crc32_pieces(stage + (img_rows * h + off[i]) * es, seg, 1, kFilePiece,
+                                    d_pcrc + pc_off[i] + (L + l) * ppp, cs);
+            }
         if (n_threads) {
             std::lock_guard<std::mutex> lk(mu);
             copied[l] = true;
@@ -2849,6 +2878,7 @@ int files_pass(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* promp
         cudaStreamSynchronize(s);
         cudaStreamSynchronize(cs);
         for (int sl = 0; sl < 2; ++sl) cudaFreeAsync(bufs[sl], s);
+        if (d_pcrc) cudaFreeAsync(d_pcrc, cs);
     };
     try {
         issue_copy(0);
@@ -2864,6 +2894,25 @@ int files_pass(mpic_model_t model, mpic_workspace_t ws, const mpic_prompt* promp
     }
     for (std::thread& t : readers) t.join();
     for (int sl = 0; sl < 2; ++sl) MPIC_CUDA(cudaFreeAsync(bufs[sl], s));
+    if (d_pcrc) {
+        std::vector<uint32_t> hp(n_pc);
+        MPIC_CUDA(cudaMemcpyAsync(hp.data(), d_pcrc, n_pc * 4, cudaMemcpyDeviceToHost, cs));
+        MPIC_CUDA(cudaFreeAsync(d_pcrc, cs));
+        MPIC_CUDA(cudaStreamSynchronize(cs));
+        for (uint32_t i : loaded) {
+            MpicFile& f = *files[i];
+            const size_t seg = (size_t)f.T * h * es, ppp = ceil_div(seg, (size_t)kFilePiece);
+            f.layer_crc.resize(2 * L);
+            for (uint32_t q = 0; q < 2 * L; ++q)
+                f.layer_crc[q] = combine_crc_pieces(hp.data() + pc_off[i] + q * ppp, seg, kFilePiece);
+            if (f.version == 3 && bad_chunk < 0)
+                for (uint32_t q = 0; q < 2 * L; ++q)
+                    if (f.layer_crc[q] != f.table[q]) {
+                        bad_chunk = (int)i;
+                        break;
+                    }
+        }
+    }
     if (bad_chunk >= 0) return bad_chunk;
     MPIC_REQUIRE(reader_error.empty(), MPIC_ERR_IO, "disk loader: " + reader_error);
     for (uint32_t i : loaded) {  // CRC of the whole file, in file order (v1/v2: the only check)

@@ -191,6 +191,12 @@ void launch_pgemm_x3(const float* A_hi, const float* A_lo, const float* W_hi, co
                      uint32_t N, uint32_t K, const EpiParams& ep, cudaStream_t s);
 // hi = tf32_rna(x), lo = tf32_rna(x - hi) over n floats (n % 4 == 0, 16-B aligned).
 void launch_tf32_split(const float* x, float* hi, float* lo, size_t n, cudaStream_t s);
+// zlib CRC32 of n_planes consecutive planes of plane_bytes bytes at a device address, one
+// value per `piece` bytes of each plane into d_out (async; store.cu), and the host combination
+// of one plane's piece CRCs (h[ceil(plane_bytes / piece)]) into the plane's CRC.
+void launch_crc32_pieces(const void* base, size_t plane_bytes, uint32_t n_planes, uint32_t piece, uint32_t* d_out,
+                         cudaStream_t s);
+uint32_t combine_crc_pieces(const uint32_t* h, size_t plane_bytes, uint32_t piece);
 // MPIC_PG_TS diagnostics of the last pair GEMM's CTA 0: 5 x %globaltimer ns (entry, after
 // prologue, MMAs issued, epilogue done, exit), then clock64 cycles: producer waiting on
 // empty slots / producer total / MMA issuer waiting on full slots / MMA issuer total.

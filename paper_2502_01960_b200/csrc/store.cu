@@ -106,6 +106,106 @@ std::vector<uint32_t> device_plane_crcs(const void* base, size_t plane_bytes, ui
     return out;
 }
 
+}  // namespace
+
+// Warp per piece of 32 x 4 KB (the last piece of a plane may hold fewer): lane i checksums
+// sub-piece i with four 16-B loads in flight, lane 0 folds the 32 sub-CRCs with the
+// "append 4 KB" operator (zlib crc32_combine as a GF(2) matrix, m4k[j] = image of bit j).
+// plane_bytes % 4096 == 0.
+__constant__ uint32_t c_m4k[32];
+__global__ void __launch_bounds__(128) crc32_warp_kernel(const uint8_t* __restrict__ base, size_t plane_bytes,
+                                                         uint32_t n_planes, uint32_t* __restrict__ out) {
+    __shared__ uint32_t tab[8][256];
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
+        uint32_t c = i;
+        for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+        tab[0][i] = c;
+    }
+    __syncthreads();
+    for (uint32_t t = 1; t < 8; ++t) {
+        for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x)
+            tab[t][i] = (tab[t - 1][i] >> 8) ^ tab[0][tab[t - 1][i] & 0xFFu];
+        __syncthreads();
+    }
+    constexpr uint32_t kSub = 4096, kPiece = 32 * kSub;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t ppp = (plane_bytes + kPiece - 1) / kPiece;
+    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    if (w >= ppp * n_planes) return;
+    const uint64_t plane = w / ppp, j = w % ppp;
+    const size_t off = j * (size_t)kPiece;
+    const uint32_t nsub = (uint32_t)(min((size_t)kPiece, plane_bytes - off) / kSub);
+    uint32_t c = 0xFFFFFFFFu;
+    if (lane < nsub) {
+        const uint4* p = reinterpret_cast<const uint4*>(base + plane * plane_bytes + off + (size_t)lane * kSub);
+        auto step8 = [&](uint32_t a, uint32_t b) {
+            a ^= c;
+            c = tab[7][a & 0xFFu] ^ tab[6][(a >> 8) & 0xFFu] ^ tab[5][(a >> 16) & 0xFFu] ^ tab[4][a >> 24] ^
+                tab[3][b & 0xFFu] ^ tab[2][(b >> 8) & 0xFFu] ^ tab[1][(b >> 16) & 0xFFu] ^ tab[0][b >> 24];
+        };
+        for (uint32_t q = 0; q < kSub / 16; q += 4) {
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldg(p + q + u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                step8(v[u].x, v[u].y);
+                step8(v[u].z, v[u].w);
+            }
+        }
+    }
+    c = ~c;
+    uint32_t acc = __shfl_sync(0xffffffffu, c, 0);
+    for (uint32_t i = 1; i < nsub; ++i) {  // lane 0 (all lanes compute it: warp-uniform)
+        uint32_t sh = 0;
+#pragma unroll
+        for (uint32_t b = 0; b < 32; ++b)
+            if (acc >> b & 1u) sh ^= c_m4k[b];
+        acc = sh ^ __shfl_sync(0xffffffffu, c, i);
+    }
+    if (lane == 0) out[w] = acc;
+}
+
+void launch_crc32_pieces(const void* base, size_t plane_bytes, uint32_t n_planes, uint32_t piece, uint32_t* d_out,
+                         cudaStream_t s) {
+    const uint64_t n = (plane_bytes + piece - 1) / piece * n_planes;
+    if (!n) return;
+    if (piece == 32 * 4096 && plane_bytes % 4096 == 0) {
+        static std::mutex mu;
+        static bool init[64] = {};
+        int dev = 0;
+        MPIC_CUDA(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lk(mu);
+        if (!init[dev & 63]) {  // __constant__ memory is per device
+            uint32_t m[32];
+            const uLong op = crc32_combine_gen((z_off_t)4096);
+            for (int b = 0; b < 32; ++b) m[b] = (uint32_t)crc32_combine_op(1uL << b, 0, op);
+            MPIC_CUDA(cudaMemcpyToSymbol(c_m4k, m, sizeof(m)));
+            init[dev & 63] = true;
+        }
+        crc32_warp_kernel<<<(uint32_t)((n * 32 + 127) / 128), 128, 0, s>>>(static_cast<const uint8_t*>(base),
+                                                                            plane_bytes, n_planes, d_out);
+    } else {
+        crc32_pieces_kernel<<<(uint32_t)((n + 127) / 128), 128, 0, s>>>(static_cast<const uint8_t*>(base),
+                                                                           plane_bytes, n_planes, piece, d_out);
+    }
+    MPIC_LAUNCHED();
+}
+
+uint32_t combine_crc_pieces(const uint32_t* h, size_t plane_bytes, uint32_t piece) {
+    const uint64_t ppp = (plane_bytes + piece - 1) / piece;
+    if (!ppp) return (uint32_t)crc32(0L, Z_NULL, 0);
+    static thread_local std::pair<uint32_t, uLong> op{0, 0};
+    if (op.first != piece) op = {piece, crc32_combine_gen((z_off_t)piece)};
+    uLong c = h[0];
+    const size_t tail = plane_bytes - (ppp - 1) * (size_t)piece;
+    for (uint64_t j = 1; j < ppp; ++j)
+        c = j + 1 < ppp ? crc32_combine_op(c, h[j], op.second) : crc32_combine(c, h[j], (z_off_t)tail);
+    return (uint32_t)c;
+}
+
+namespace {
+
 uint64_t fnv1a_bytes(const void* p, size_t n) {
     uint64_t h = 0xcbf29ce484222325ull;
     const uint8_t* b = static_cast<const uint8_t*>(p);
@@ -552,5 +652,26 @@ int mpic_crc32_device(const void* d_ptr, size_t n, uint32_t* crc, void* stream) 
     STORE_BEGIN
     MPIC_REQUIRE(crc && (d_ptr || !n), MPIC_ERR_VALIDATION, "null argument");
     *crc = device_plane_crcs(d_ptr, n, 1, (cudaStream_t)stream)[0];
+    STORE_END
+}
+
+int mpic_crc32_planes_device(const void* d_ptr, size_t plane_bytes, uint32_t n_planes, uint32_t* crcs, void* stream) {
+    STORE_BEGIN
+    MPIC_REQUIRE(crcs && (d_ptr || !plane_bytes || !n_planes), MPIC_ERR_VALIDATION, "null argument");
+    constexpr uint32_t piece = 32 * 4096;  // the files loader's pieces
+    const size_t ppp = (plane_bytes + piece - 1) / piece;
+    if (!ppp || !n_planes) {
+        for (uint32_t i = 0; i < n_planes; ++i) crcs[i] = (uint32_t)crc32(0L, Z_NULL, 0);
+        return MPIC_OK;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t* d = nullptr;
+    MPIC_CUDA(cudaMallocAsync((void**)&d, ppp * n_planes * 4, s));
+    launch_crc32_pieces(d_ptr, plane_bytes, n_planes, piece, d, s);
+    std::vector<uint32_t> h(ppp * n_planes);
+    MPIC_CUDA(cudaMemcpyAsync(h.data(), d, h.size() * 4, cudaMemcpyDeviceToHost, s));
+    MPIC_CUDA(cudaFreeAsync(d, s));
+    MPIC_CUDA(cudaStreamSynchronize(s));
+    for (uint32_t i = 0; i < n_planes; ++i) crcs[i] = combine_crc_pieces(h.data() + i * ppp, plane_bytes, piece);
     STORE_END
 }

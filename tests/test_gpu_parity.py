@@ -394,8 +394,9 @@ def test_request_prefill_from_mpic_files(tmp_path, version):
     cache of the same chunks resident in HBM; every failure mode of the reference's prepare
     (transfer.cpp:83-145; CacheStore::fetch checks, cache.cpp:171-176) turns into the chunk
     being computed on the device instead, with the SAME outputs as a request given that
-    computed chunk: a flipped payload byte (v3: caught by the layer CRC before the H2D; v1/v2:
-    by the file CRC, then the request re-runs), a chunk of another model, a wrong content
+    computed chunk: a flipped payload byte (caught by the GPU CRC of the layer after its H2D — v3
+    against the layer table, v1/v2 through the file CRC — then the request re-runs), a chunk
+    of another model, a wrong content
     hash, a truncated file, a missing file and a None path."""
     bf16 = version in ("v2", "v3-bf16")
     layer_crcs = version.startswith("v3")

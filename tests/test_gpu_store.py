@@ -27,6 +27,19 @@ def test_crc32_device_matches_zlib(n):
     assert mp.crc32_device(buf.data_ptr() + off, n - off) == want
 
 
+@pytest.mark.parametrize("nplanes,plane", [(1, 4096), (3, 32 * 4096), (2, 33 * 4096), (4, 4608 * 4096 // 16)])
+def test_crc32_pieces_warp_kernel(nplanes, plane):
+    """The files loader's GPU CRC: 128 KB pieces of 4 KB-multiple planes, each folded by one warp
+    (GF(2) 'append 4 KB' operator), combined on the host — bit-exact with zlib per plane."""
+    from paper_2502_01960_b200 import _lib
+    g = np.random.default_rng(plane + nplanes)
+    data = g.integers(0, 256, nplanes * plane, dtype=np.uint8)
+    buf = torch.from_numpy(data).cuda()
+    got = [mp.crc32_planes_device(buf.data_ptr(), plane, nplanes)[i] for i in range(nplanes)]
+    want = [zlib.crc32(data[i * plane:(i + 1) * plane].tobytes()) for i in range(nplanes)]
+    assert got == want
+
+
 def _want(m, ws, p, chunks, L, H, D):
     linked = mp.KV(L, p.n, H, D, m.dtype)
     logits, sel = mp.request_prefill(m, ws, p, chunks, linked, k=32)
