@@ -62,8 +62,9 @@ INTRO = {
         "partials; the pair GEMM's MMA warp made warp-uniform; loader fault semantics of `prepare` on the fast",
         "paths (v3 per-layer CRCs, compute lane); `mpic_hp_request` with NCCL inside the library; fp32-mode",
         "and config-D k-sweep bench keys; fp32 mode on the tensor cores (3xTF32 pair GEMM with segmented",
-        "accumulation) and a register-tiled fp32 attention (fp32 request 455 -> 78 ms); the tiered chunk store",
-        "(`mpic_store_*`, Device tier in HBM, GPU CRC32) (DESIGN.md)."],
+        "accumulation) and a register-tiled fp32 attention (fp32 request 455 -> 66 ms); the tiered chunk store",
+        "(`mpic_store_*`, Device tier in HBM, GPU CRC32); the disk loader's CRCs on the GPU (C from files",
+        "239 -> 139 ms); the miss-path bench key (DESIGN.md)."],
 }
 out = [f"# Round {rnd} — final state", "",
        f"B200, 1 GPU. `tools/gpu_final.sh {tag}` on one fresh box: GPU tests, smoke, the reference's own suites",
