@@ -1022,6 +1022,11 @@ void launch_pgemm_impl(const void* A, const void* A_lo, const void* W, const voi
         a.K = K;
         a.dbg = dbg;
         a.ngroups = gm ? ng_nat * gm : ng_nat + 1;
+        static const uint32_t force_ng = [] {
+            const char* e = getenv("MPIC_PG_NGROUPS");  // diagnostics: force the token-group count
+            return e ? (uint32_t)atoi(e) : 0u;
+        }();
+        if (force_ng && a.ngroups != force_ng) continue;
         if (!x3 && a.ngroups == 1 && M > 256 && M <= group_max) {
             a.P0 = round16((M + 1) / 2);
             a.P1 = round16(M - a.P0);
