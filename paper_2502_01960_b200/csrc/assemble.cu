@@ -176,9 +176,18 @@ void launch_assemble(const AsmChunk* d_chunks, uint32_t n_chunks, const float2* 
                      uint32_t n_tables, mpic_dtype src_t, void* dst_k, void* dst_v,
                      mpic_dtype dst_t, uint32_t L, uint32_t T_dst, uint32_t H, uint32_t D,
                      int zero_gaps, cudaStream_t s, uint32_t src_l0, const uint8_t* skip_blk) {
-    MPIC_REQUIRE(n_chunks <= kMaxAsmChunks, MPIC_ERR_VALIDATION, "too many chunks in one assembly");
     static const bool skip = getenv("MPIC_ASM_SKIP") != nullptr;  // diagnostics: timing without the copy
     if (skip) return;
+    if (n_chunks > kMaxAsmChunks) {
+        // more descriptors than one CTA stages (batched requests): one launch per group of
+        // kMaxAsmChunks (each group a contiguous destination range, the descriptors being sorted
+        // by destination row); only the first zero-fills the gaps — rows of later groups are
+        // zeroed there and overwritten by their own launch, in stream order
+        for (uint32_t g0 = 0; g0 < n_chunks; g0 += kMaxAsmChunks)
+            launch_assemble(d_chunks + g0, std::min<uint32_t>(kMaxAsmChunks, n_chunks - g0), d_tables, n_tables, src_t,
+                            dst_k, dst_v, dst_t, L, T_dst, H, D, g0 == 0 ? zero_gaps : 0, s, src_l0, skip_blk);
+        return;
+    }
     using bf = __nv_bfloat16;
     if (src_t == MPIC_F32 && dst_t == MPIC_F32)
         launch_asm_typed<float, float>(d_chunks, n_chunks, d_tables, n_tables, (float*)dst_k, (float*)dst_v, L, T_dst, H, D, zero_gaps, src_l0, skip_blk, s);

@@ -117,3 +117,34 @@ def test_batch_matches_single_requests(reposition):
         assert rel_err(kb[:, off:off + p.n], k1) < 1e-2
         assert rel_err(vb[:, off:off + p.n], v1) < 1e-2
         off += p.n
+
+
+def test_batch_more_chunks_than_one_assembly_launch():
+    """A batch whose requests carry more image chunks (300) than one assembly launch stages
+    (256 descriptors): the assembly runs in descriptor groups, and every request still matches
+    the same request run alone (assembled rows exactly, logits within bf16 rounding)."""
+    L, H, D, V = 1, 2, 128, 512
+    cfg = mp.config(L, H, D, vocab_size=V, image_token_count=16, seed=11)
+    rng = np.random.default_rng(11)
+    layouts = [[("t", 3), ("i", 16), ("t", 2), ("i", 16), ("t", 4)]] * 150
+    reqs = _requests(rng, L, H, D, V, layouts)
+    m = mp.Model(cfg, mp.BF16)
+    prompts = [mp.Prompt.from_segments(segs) for segs, _, _ in reqs]
+    ns = [p.n for p in prompts]
+    ws = mp.Workspace(m, sum(ns), sum(ns))
+    chunks = [[mp.KV.from_host(a, b, H, D, mp.BF16) for a, b in zip(ck, cv)] for _, ck, cv in reqs]
+    assert sum(len(c) for c in chunks) == 300
+    big = mp.KV(L, sum(ns), H, D, mp.BF16)
+    logits, mrows = mp.request_prefill_batch(m, ws, prompts, chunks, big, k=4)
+    kb, _ = big.download()
+    off = 0
+    for r in (0, 77, 127, 128, 149):  # requests on both sides of the 256-descriptor boundary
+        p = prompts[r]
+        one = mp.KV(L, p.n, H, D, mp.BF16)
+        lg, sel = mp.request_prefill(m, ws, p, chunks[r], one, k=4)
+        k1, _ = one.download()
+        o = sum(ns[:r])
+        assert mrows[r] == len(sel)
+        img = np.setdiff1d(np.arange(p.n), sel)
+        assert np.array_equal(kb[:, o + img], k1[:, img])
+        assert rel_err(logits[r], lg) < 1e-2, (r, rel_err(logits[r], lg))
